@@ -1,0 +1,234 @@
+/*
+ * ohx.h -- C ABI of the B200 (sm_100a) heaphull filter layer.
+ *
+ * This is the drop-in boundary under the reference's public C++ API
+ * (/root/reference/proj/include/octohull/{filter,hull}.hpp).  The
+ * reference has no C ABI of its own -- its only FFI is the pybind11
+ * module python/module.cpp -- so each entry point below names the
+ * reference interface it replaces (file:line, paths relative to
+ * /root/reference/proj).  INTEGRATION.md shows the bindings a
+ * maintainer adds (ctypes stub, pybind11 module relink, C++ relink).
+ *
+ * Conventions
+ *   - Every function returns OHX_OK (0) or a negative OHX_E* code and never
+ *     throws or aborts across the ABI; ohx_last_error() returns a
+ *     thread-local message for the last failure on the calling thread.
+ *   - Points are the reference's AoS Point2D layout (geometry.hpp:10-15):
+ *     interleaved IEEE binary64, xy[2j] = x_j, xy[2j+1] = y_j, 16-byte
+ *     aligned.  Coordinates must be finite (the reference enforces this at
+ *     ingestion, geometry.cpp:27-34); the filter does not re-check.
+ *   - Indices are 64-bit global point indices.  Sharded callers pass
+ *     `index_base` = first global index of the shard so that the
+ *     smallest-index tie rule (parallel.hpp:34-43) holds across shards.
+ *   - d_* pointers are device pointers (cudaMalloc / torch), h_* are host.
+ *   - `stream` is a cudaStream_t passed as void*; NULL = the context's own
+ *     stream.  Shard-level calls are synchronous w.r.t. their small host
+ *     outputs (they end with a stream sync) unless stated otherwise.
+ *   - There is no CPU fallback: without a usable sm_100 device every
+ *     compute entry point fails with OHX_E_CUDA / OHX_E_NODEVICE.
+ */
+#ifndef OHX_H
+#define OHX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OHX_ABI_VERSION 1
+
+enum {
+  OHX_OK = 0,
+  OHX_E_INVALID = -1,  /* std::invalid_argument in the reference */
+  OHX_E_CUDA = -2,     /* CUDA runtime error (std::runtime_error) */
+  OHX_E_NODEVICE = -3, /* no sm_100 device visible */
+  OHX_E_NOMEM = -4,    /* device or pinned allocation failed */
+  OHX_E_INTERNAL = -5
+};
+
+/* Distributions of pointgen.hpp:10 (generate, pointgen.cpp:44-88). */
+enum { OHX_NORMAL = 0, OHX_SQUARE = 1, OHX_DISK = 2, OHX_CIRCLE = 3 };
+
+/* Direction slots of an extremes record.  Slots 0..3 are the axis extremes
+ * (AxisExtremes, filter.hpp:15-20), 4..7 the corner extremes
+ * (CornerExtremes, filter.hpp:24-29). */
+enum {
+  OHX_EAST = 0, OHX_NORTH = 1, OHX_WEST = 2, OHX_SOUTH = 3,
+  OHX_NE = 4, OHX_NW = 5, OHX_SW = 6, OHX_SE = 7
+};
+
+/* One shard's single-pass extremes (kernel K1).  Every slot is an argmax of
+ * a maximised key with ties to the smaller global index:
+ *   east x, north y, west -x, south -y,
+ *   ne fl(x+y), nw fl(y-x), sw -fl(x+y), se fl(x-y).
+ * second[k] is the second-largest diagonal key (as a multiset) of slot 4+k;
+ * it feeds the corner certificate (see ohx_extremes_resolve).  x/y are the
+ * coordinates of each slot's winner. */
+typedef struct {
+  double key[8];
+  uint64_t idx[8];
+  double second[4];
+  double x[8];
+  double y[8];
+  uint64_t n; /* points covered by this record */
+} ohx_extremes_rec;
+
+/* Exact Manhattan corner argmins (kernel K1b), corners ne, nw, sw, se as in
+ * find_corner_extremes (filter.cpp:25-45); key = the reference's
+ * manhattan() value (geometry.hpp:35-37). */
+typedef struct {
+  double key[4];
+  uint64_t idx[4];
+  double x[4];
+  double y[4];
+  uint64_t n;
+} ohx_corner_rec;
+
+/* The resolved ExtremeSet (filter.hpp:33-41): ext[8] in slot order
+ * {east, north, west, south, ne, nw, sw, se}, with coordinates. */
+typedef struct {
+  uint64_t ext[8];
+  double x[8];
+  double y[8];
+} ohx_extreme_set;
+
+/* Everything kernel K2 needs, built on the host from an Octagon and an
+ * ExtremeSet (ohx_filter_plan_build).  Edge constants are the reference's
+ * (b.x-a.x), (b.y-a.y) of orientation() (geometry.hpp:27-32). */
+typedef struct {
+  double ax[8], ay[8];   /* octagon edge origin a_i (padded: 0) */
+  double ea[8], ec[8];   /* fl(b.x-a.x), fl(b.y-a.y) (padded: 0 => never < 0) */
+  double qax[4], qay[4]; /* find_queue edges E->N, N->W, W->S, S->E */
+  double qa[4], qc[4];
+  double box[4];         /* certified interior box xlo,xhi,ylo,yhi (empty if xlo>xhi) */
+  uint64_t kept[8];      /* kept indices in override order E,NE,N,NW,W,SW,S,SE */
+  uint8_t kept_label[8]; /* 1,1,2,2,3,3,4,4 */
+  int32_t m;             /* octagon vertices; < 3 = degenerate (filter nothing) */
+  int32_t pad;
+} ohx_filter_plan;
+
+typedef struct ohx_ctx ohx_ctx;
+
+/* ---- runtime ----------------------------------------------------------- */
+int ohx_abi_version(void);
+const char* ohx_last_error(void);
+int ohx_device_count(int* n);
+/* Per-device context: stream, workspaces (grow-only, reused across calls),
+ * pinned staging.  One call at a time per context (ReduceEngine contract,
+ * parallel.hpp:50-52); distinct contexts may run concurrently. */
+int ohx_ctx_create(int device, ohx_ctx** out);
+int ohx_ctx_destroy(ohx_ctx* ctx);
+/* Process-wide lazily created context for `device` (used by the C++ API). */
+int ohx_ctx_default(int device, ohx_ctx** out);
+int ohx_ctx_device(const ohx_ctx* ctx);
+/* Kernels launched by this context since creation (evidence counter). */
+uint64_t ohx_ctx_launches(const ohx_ctx* ctx);
+/* Device duration (CUDA events on the launching stream) of the last launch
+ * of K1, K1b and K2 in this context; -1 for a kernel not yet launched. */
+int ohx_ctx_kernel_ms(ohx_ctx* ctx, double ms[3]);
+
+/* ---- kernel-level (one shard, device-resident points) ------------------ */
+
+/* K1. Replaces the 8 reduction passes of find_axis_extremes
+ * (filter.cpp:8-23) + find_corner_extremes (filter.cpp:25-45) by one
+ * streaming pass.  n >= 1. */
+int ohx_extremes(ohx_ctx* ctx, const double* d_xy, uint64_t n,
+                 uint64_t index_base, ohx_extremes_rec* h_rec, void* stream);
+
+/* Associative, commutative merge of shard records (ties -> smaller global
+ * index); every rank computes the identical result.  Host only. */
+int ohx_extremes_combine(const ohx_extremes_rec* recs, int k,
+                         ohx_extremes_rec* out);
+
+/* Axis extremes + certified corner extremes from a (global) record.
+ * Corner slot k is certified when the reference's Manhattan argmin is
+ * provably the diagonal winner (gap between best and second diagonal key
+ * exceeds the binary64 rounding bound).  Uncertified slots are reported in
+ * *uncertified_mask (bit k = corner 4+k) and must be resolved with
+ * ohx_corners_exact.  Host only. */
+int ohx_extremes_resolve(const ohx_extremes_rec* rec, ohx_extreme_set* out,
+                         uint32_t* uncertified_mask);
+
+/* K1b. Exact corner argmins against the bounding box
+ * bbox = {x_max, y_max, x_min, y_min} (filter.cpp:28-43). */
+int ohx_corners_exact(ohx_ctx* ctx, const double* d_xy, uint64_t n,
+                      uint64_t index_base, const double bbox[4],
+                      ohx_corner_rec* h_rec, void* stream);
+int ohx_corners_combine(const ohx_corner_rec* recs, int k, ohx_corner_rec* out);
+
+/* build_octagon (filter.cpp:54-86) on the 8 candidate coordinates in
+ * candidate order E,NE,N,NW,W,SW,S,SE (filter.hpp:37-40).  Host only. */
+int ohx_build_octagon(const double cand_xy[16], double oct_xy[16], int* m);
+
+/* K2 plan from an octagon (m vertices, CCW) and the extreme set. Host only. */
+int ohx_filter_plan_build(const ohx_extreme_set* ext, const double* oct_xy,
+                          int m, ohx_filter_plan* plan);
+
+/* K2. Replaces classify_points (filter.cpp:104-131) + build_queues
+ * (hull.cpp:124-131): labels every point of the shard and compacts the
+ * survivors, in index order, into four per-quadrant queues held in the
+ * context.  d_labels (nullable) receives the n labels (LabelArray,
+ * filter.hpp:53-54).  h_counts receives the four queue lengths. */
+int ohx_filter(ohx_ctx* ctx, const double* d_xy, uint64_t n,
+               uint64_t index_base, const ohx_filter_plan* plan,
+               uint8_t* d_labels, uint64_t h_counts[4], void* stream);
+
+/* Copy queue q (1..4) of the last ohx_filter to the host: global indices
+ * (nullable) and survivor coordinates (nullable, gathered on the device). */
+int ohx_queue_fetch(ohx_ctx* ctx, int q, uint64_t* h_idx, double* h_xy,
+                    uint64_t cap, void* stream);
+/* Device pointer + element width (4 or 8 bytes, shard-local indices) of
+ * queue q of the last ohx_filter. */
+int ohx_queue_device(ohx_ctx* ctx, int q, const void** d_idx,
+                     int* idx_bytes, uint64_t* count);
+
+/* ---- pipeline-level (host buffers; the reference's bound entry points) --- */
+
+/* heaphull (hull.cpp:196-203; python/module.cpp:62-75): host points in,
+ * CCW hull coordinates out (h_hull capacity `cap` points, *h = size).
+ * timings (nullable) = {filter_ms, hull_ms, total_ms, h2d_ms}. */
+int ohx_heaphull(const double* h_xy, uint64_t n, double* h_hull, uint64_t cap,
+                 uint64_t* h, double* timings);
+/* Same, points already on the device of `ctx`. */
+int ohx_heaphull_device(ohx_ctx* ctx, const double* d_xy, uint64_t n,
+                        double* h_hull, uint64_t cap, uint64_t* h,
+                        double* timings);
+/* classify (python/module.cpp:91-108): find_extremes + build_octagon +
+ * classify_points, labels to the host. */
+int ohx_classify(const double* h_xy, uint64_t n, uint8_t* h_labels);
+/* heaphull_run (hull.cpp:152-194): hull + labels + timings. */
+int ohx_heaphull_run(const double* h_xy, uint64_t n, double* h_hull,
+                     uint64_t cap, uint64_t* h, uint8_t* h_labels,
+                     double* timings);
+/* find_extremes (filter.cpp:47-52) from host points: ext[8] slot order. */
+int ohx_find_extremes(const double* h_xy, uint64_t n, uint64_t ext[8]);
+
+/* monotone_chain_hull (hull.cpp:205-232; python/module.cpp:77-89): the
+ * independent full-set reference hull, host only. */
+int ohx_monotone_chain(const double* h_xy, uint64_t n, double* h_hull,
+                       uint64_t cap, uint64_t* h);
+
+/* generate (pointgen.cpp:44-88), multi-threaded and bit-identical to the
+ * reference's single-threaded stream; threads = 0 -> all cores. */
+int ohx_generate(int dist, uint64_t n, uint64_t seed, double distort_pct,
+                 double* h_xy, int threads);
+
+/* Host hull stage of heaphull_run (hull.cpp:164-183) on given queues:
+ * pts = all points (host), queues as global indices. */
+int ohx_hull_from_queues(const double* h_xy, const uint64_t ext_axis[4],
+                         const uint64_t* const q_idx[4],
+                         const uint64_t q_len[4], double* h_hull,
+                         uint64_t cap, uint64_t* h);
+/* Same, survivor coordinates given directly per queue (index order). */
+int ohx_hull_from_queue_points(const double anchors_xy[8],
+                               const double* const q_xy[4],
+                               const uint64_t q_len[4], double* h_hull,
+                               uint64_t cap, uint64_t* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OHX_H */

@@ -1,0 +1,285 @@
+"""B200-native heaphull filter (arXiv 2209.12310) -- Python front-end.
+
+Drop-in for the reference Python package ``octohull``
+(/root/reference/proj/python/octohull/__init__.py and python/module.cpp):
+the same functions with the same arguments, return types and errors --
+``generate``, ``heaphull``, ``monotone_chain``, ``classify``,
+``filter_rate`` -- backed by the C ABI of ``include/ohx.h`` whose filter
+runs as sm_100a kernels.  ``threads``/``chunk`` are accepted for
+compatibility (the reference's CPU lane geometry); results never depend
+on them, as in the reference.
+
+``Context`` exposes the kernel-level entry points for device-resident
+points (torch CUDA tensors or raw device pointers), which is what the
+benchmarks and the multi-GPU sharded path (``sharded.py``) use.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import (DISTS, SLOTS, CornerRec, ExtremeSet, ExtremesRec, FilterPlan, OhxError,
+                   check, lib)
+
+__all__ = ["classify", "filter_rate", "generate", "heaphull", "monotone_chain",
+           "heaphull_run", "find_extremes", "Context", "OhxError", "device_count"]
+
+_dp = C.POINTER(C.c_double)
+_u64p = C.POINTER(C.c_uint64)
+_u8p = C.POINTER(C.c_uint8)
+
+
+def _points(points) -> np.ndarray:
+    """python/module.cpp:18-28: (n, 2) C-contiguous float64, finite."""
+    a = np.ascontiguousarray(points, dtype=np.float64)
+    if a.ndim != 2 or a.shape[1] != 2:
+        raise ValueError("expected an array of shape (n, 2)")
+    if a.size:
+        bad = ~np.isfinite(a).all(axis=1)
+        if bad.any():
+            raise ValueError(f"non-finite coordinate at point index {int(np.argmax(bad))}")
+    return a
+
+
+def _check_cfg(threads: int, chunk: int) -> None:
+    # ReduceConfig validation, reference parallel.cpp:8-13
+    if chunk < 1:
+        raise ValueError("ReduceConfig.chunk_size must be >= 1")
+    if threads < 1:
+        raise ValueError("ReduceConfig.workers must be >= 1")
+
+
+def generate(dist: str, n: int, seed: int = 0, distort: float = 0.0, threads: int = 0) -> np.ndarray:
+    """Seeded synthetic points: normal | square | disk | circle (bit-identical
+    to the reference generator; multi-threaded)."""
+    if dist not in DISTS:
+        raise ValueError(f"unknown distribution '{dist}' (expected normal|square|disk|circle)")
+    out = np.empty((max(int(n), 0), 2), dtype=np.float64)
+    check(lib.ohx_generate(DISTS[dist], int(n), int(seed), float(distort),
+                           out.ctypes.data_as(_dp), int(threads)))
+    return out
+
+
+def heaphull(points, threads: int = 1, chunk: int = 32) -> np.ndarray:
+    """Octagon-filtered convex hull; returns the CCW vertex cycle (h, 2)."""
+    _check_cfg(threads, chunk)
+    a = _points(points)
+    hull = np.empty((len(a) + 8, 2), dtype=np.float64)
+    h = C.c_uint64(0)
+    check(lib.ohx_heaphull(a.ctypes.data_as(_dp), len(a), hull.ctypes.data_as(_dp),
+                           len(hull), C.byref(h), None))
+    return hull[: h.value].copy()
+
+
+def heaphull_run(points):
+    """heaphull_run (hull.cpp:152-194): (hull, labels, timings dict)."""
+    a = _points(points)
+    hull = np.empty((len(a) + 8, 2), dtype=np.float64)
+    labels = np.empty(len(a), dtype=np.uint8)
+    t = np.zeros(4, dtype=np.float64)
+    h = C.c_uint64(0)
+    check(lib.ohx_heaphull_run(a.ctypes.data_as(_dp), len(a), hull.ctypes.data_as(_dp),
+                               len(hull), C.byref(h), labels.ctypes.data_as(_u8p),
+                               t.ctypes.data_as(_dp)))
+    return hull[: h.value].copy(), labels, dict(filter_ms=t[0], hull_ms=t[1], total_ms=t[2])
+
+
+def monotone_chain(points) -> np.ndarray:
+    """Full-set reference hull (Andrew's monotone chain), host only."""
+    a = _points(points)
+    hull = np.empty((len(a) + 2, 2), dtype=np.float64)
+    h = C.c_uint64(0)
+    check(lib.ohx_monotone_chain(a.ctypes.data_as(_dp), len(a), hull.ctypes.data_as(_dp),
+                                 len(hull), C.byref(h)))
+    return hull[: h.value].copy()
+
+
+def classify(points, threads: int = 1, chunk: int = 32) -> np.ndarray:
+    """Filter labels per point: 0 = discarded, 1..4 = quadrant queue."""
+    _check_cfg(threads, chunk)
+    a = _points(points)
+    labels = np.empty(len(a), dtype=np.uint8)
+    if len(a) == 0:
+        raise ValueError("find_axis_extremes: empty point set")
+    check(lib.ohx_classify(a.ctypes.data_as(_dp), len(a), labels.ctypes.data_as(_u8p)))
+    return labels
+
+
+def find_extremes(points) -> np.ndarray:
+    """ExtremeSet as 8 indices {east, north, west, south, ne, nw, sw, se}."""
+    a = _points(points)
+    ext = np.zeros(8, dtype=np.uint64)
+    check(lib.ohx_find_extremes(a.ctypes.data_as(_dp), len(a), ext.ctypes.data_as(_u64p)))
+    return ext
+
+
+def filter_rate(labels) -> float:
+    """Fraction of points discarded by the filter (label == 0)."""
+    labels = np.asarray(labels)
+    if labels.size == 0:
+        raise ValueError("empty label array")
+    return float((labels == 0).mean())
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    check(lib.ohx_device_count(C.byref(n)))
+    return n.value
+
+
+def _ptr(x) -> int:
+    """Device address of a torch tensor (or an int pointer)."""
+    if isinstance(x, int):
+        return x
+    return int(x.data_ptr())
+
+
+def _stream(s):
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return int(s.cuda_stream)  # torch.cuda.Stream
+
+
+def rec_to_dict(rec: ExtremesRec) -> dict:
+    return {
+        "idx": [int(v) for v in rec.idx], "key": list(rec.key), "x": list(rec.x),
+        "y": list(rec.y), "second": list(rec.second), "n": int(rec.n),
+    }
+
+
+class Context:
+    """A device context (stream + grow-only workspaces) of the C ABI."""
+
+    def __init__(self, device: int = 0, default: bool = False):
+        h = C.c_void_p()
+        check((lib.ohx_ctx_default if default else lib.ohx_ctx_create)(device, C.byref(h)))
+        self.h = h
+        self.device = device
+        self._owned = not default
+
+    def close(self):
+        if self._owned and self.h:
+            lib.ohx_ctx_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(lib.ohx_ctx_launches(self.h))
+
+    def kernel_ms(self) -> dict:
+        """CUDA-event durations of the last K1 / K1b / K2 launches (ms)."""
+        out = (C.c_double * 3)()
+        check(lib.ohx_ctx_kernel_ms(self.h, out))
+        return {"k1": out[0], "k1b": out[1], "k2": out[2]}
+
+    # ---- kernel level --------------------------------------------------
+    def extremes(self, d_xy, n: int, index_base: int = 0, stream=None) -> ExtremesRec:
+        rec = ExtremesRec()
+        check(lib.ohx_extremes(self.h, _ptr(d_xy), n, index_base, C.byref(rec), _stream(stream)))
+        return rec
+
+    def corners_exact(self, d_xy, n: int, bbox, index_base: int = 0, stream=None) -> CornerRec:
+        b = (C.c_double * 4)(*bbox)
+        rec = CornerRec()
+        check(lib.ohx_corners_exact(self.h, _ptr(d_xy), n, index_base, b, C.byref(rec),
+                                    _stream(stream)))
+        return rec
+
+    def filter(self, d_xy, n: int, plan: FilterPlan, index_base: int = 0, d_labels=None,
+               stream=None) -> list:
+        counts = (C.c_uint64 * 4)()
+        check(lib.ohx_filter(self.h, _ptr(d_xy), n, index_base, C.byref(plan),
+                             None if d_labels is None else _ptr(d_labels), counts,
+                             _stream(stream)))
+        return [int(c) for c in counts]
+
+    def queue(self, q: int, count: int, with_idx: bool = True, with_xy: bool = False,
+              stream=None):
+        idx = np.empty(count, dtype=np.uint64) if with_idx else None
+        xy = np.empty((count, 2), dtype=np.float64) if with_xy else None
+        check(lib.ohx_queue_fetch(self.h, q, None if idx is None else idx.ctypes.data_as(_u64p),
+                                  None if xy is None else xy.ctypes.data_as(_dp), count,
+                                  _stream(stream)))
+        return idx, xy
+
+    def heaphull_device(self, d_xy, n: int):
+        """Full pipeline on device-resident points -> (hull, timings)."""
+        hull = np.empty((n + 8, 2), dtype=np.float64)
+        h = C.c_uint64(0)
+        t = np.zeros(4, dtype=np.float64)
+        check(lib.ohx_heaphull_device(self.h, _ptr(d_xy), n, hull.ctypes.data_as(_dp),
+                                      len(hull), C.byref(h), t.ctypes.data_as(_dp)))
+        return hull[: h.value].copy(), dict(filter_ms=t[0], hull_ms=t[1], total_ms=t[2])
+
+
+# ---- host-only helpers of the C ABI (pure functions, no device) ---------
+def combine_extremes(recs) -> ExtremesRec:
+    arr = (ExtremesRec * len(recs))(*recs)
+    out = ExtremesRec()
+    check(lib.ohx_extremes_combine(arr, len(recs), C.byref(out)))
+    return out
+
+
+def combine_corners(recs) -> CornerRec:
+    arr = (CornerRec * len(recs))(*recs)
+    out = CornerRec()
+    check(lib.ohx_corners_combine(arr, len(recs), C.byref(out)))
+    return out
+
+
+def resolve_extremes(rec: ExtremesRec):
+    """-> (ExtremeSet, uncertified corner mask)."""
+    out = ExtremeSet()
+    mask = C.c_uint32(0)
+    check(lib.ohx_extremes_resolve(C.byref(rec), C.byref(out), C.byref(mask)))
+    return out, int(mask.value)
+
+
+def apply_corners(ext: ExtremeSet, crec: CornerRec) -> ExtremeSet:
+    for k in range(4):
+        ext.ext[4 + k] = crec.idx[k]
+        ext.x[4 + k] = crec.x[k]
+        ext.y[4 + k] = crec.y[k]
+    return ext
+
+
+CANDIDATE_SLOTS = (0, 4, 1, 5, 2, 6, 3, 7)  # E, NE, N, NW, W, SW, S, SE
+
+
+def build_octagon_from_set(ext: ExtremeSet) -> np.ndarray:
+    cand = np.array([[ext.x[s], ext.y[s]] for s in CANDIDATE_SLOTS], dtype=np.float64)
+    out = np.zeros((8, 2), dtype=np.float64)
+    m = C.c_int(0)
+    check(lib.ohx_build_octagon(cand.ctypes.data_as(_dp), out.ctypes.data_as(_dp), C.byref(m)))
+    return out[: m.value].copy()
+
+
+def make_plan(ext: ExtremeSet, octagon) -> FilterPlan:
+    o = np.ascontiguousarray(octagon, dtype=np.float64).reshape(-1, 2)
+    plan = FilterPlan()
+    check(lib.ohx_filter_plan_build(C.byref(ext), o.ctypes.data_as(_dp), len(o), C.byref(plan)))
+    return plan
+
+
+def hull_from_queue_points(anchors, queues) -> np.ndarray:
+    """Host hull stage on per-quadrant survivor coordinates (index order)."""
+    a = np.ascontiguousarray(anchors, dtype=np.float64).reshape(4, 2)
+    qs = [np.ascontiguousarray(q, dtype=np.float64).reshape(-1, 2) for q in queues]
+    ptrs = (_dp * 4)(*[q.ctypes.data_as(_dp) for q in qs])
+    lens = (C.c_uint64 * 4)(*[len(q) for q in qs])
+    total = sum(len(q) for q in qs) + 8
+    out = np.empty((total, 2), dtype=np.float64)
+    h = C.c_uint64(0)
+    check(lib.ohx_hull_from_queue_points(a.ctypes.data_as(_dp), ptrs, lens,
+                                         out.ctypes.data_as(_dp), total, C.byref(h)))
+    return out[: h.value].copy()

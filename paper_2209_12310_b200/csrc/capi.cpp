@@ -1,0 +1,718 @@
+// capi.cpp -- the C ABI of include/ohx.h: device contexts and workspaces,
+// kernel orchestration, and the small host-side steps between the kernels
+// (extremes combine + corner certificate, build_octagon, the K2 plan with
+// its certified interior box).
+//
+// Host arithmetic that must match the reference (orientation, manhattan,
+// edge constants) is plain binary64 in a TU built with -ffp-contract=off
+// and no -march, like the reference objects.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+#include "ohx.h"
+#include "pipeline.hpp"
+
+// ====================================================================== ctx
+struct ohx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  std::uint64_t launches = 0;
+
+  // K1 / K1b scratch
+  int partial_cap = 0;
+  ohx::K1Partial* d_partials = nullptr;
+  unsigned* d_ticket = nullptr;
+  ohx_extremes_rec* d_rec = nullptr;
+  ohx_corner_rec* d_crec = nullptr;
+  ohx_extremes_rec* h_rec = nullptr;  // pinned
+  ohx_corner_rec* h_crec = nullptr;   // pinned
+  unsigned long long* d_counts = nullptr;
+  unsigned long long* h_counts = nullptr;  // pinned
+
+  // K2 scratch and queues
+  std::uint64_t* d_status = nullptr;
+  std::uint64_t status_bytes = 0;
+  void* d_queues = nullptr;
+  std::uint64_t queue_bytes = 0;
+
+  // result of the last ohx_filter
+  const double* last_xy = nullptr;
+  std::uint64_t last_n = 0, last_base = 0, last_cap = 0;
+  int last_idx_bytes = 4;
+  std::uint64_t last_counts[4] = {0, 0, 0, 0};
+
+  // staging for host-API calls
+  double* d_pts = nullptr;
+  std::uint64_t pts_bytes = 0;
+  std::uint8_t* d_labels = nullptr;
+  std::uint64_t labels_bytes = 0;
+  double* d_gather = nullptr;
+  std::uint64_t gather_bytes = 0;
+
+  // CUDA events bracketing the last launch of each kernel (K1, K1b, K2)
+  cudaEvent_t ev[3][2] = {};
+  bool timed[3] = {false, false, false};
+};
+
+namespace ohx {
+namespace {
+
+void dev_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what) {
+  if (*have >= need && *p) return;
+  if (*p) check_cuda(cudaFree(*p), "cudaFree");
+  *p = nullptr;
+  *have = 0;
+  cudaError_t e = cudaMalloc(p, need);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(OHX_E_NOMEM, std::string("cudaMalloc(") + what + ", " +
+                                 std::to_string(need) + " bytes) failed: " +
+                                 cudaGetErrorString(e));
+  }
+  *have = need;
+}
+
+cudaStream_t pick(ohx_ctx* c, void* s) {
+  return s ? static_cast<cudaStream_t>(s) : c->stream;
+}
+
+void bind(ohx_ctx* c) { check_cuda(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+void ensure_partials(ohx_ctx* c, int grid) {
+  if (grid <= c->partial_cap) return;
+  if (c->d_partials) check_cuda(cudaFree(c->d_partials), "cudaFree");
+  c->d_partials = nullptr;
+  check_cuda(cudaMalloc(&c->d_partials, sizeof(K1Partial) * grid), "cudaMalloc(partials)");
+  c->partial_cap = grid;
+}
+
+// Corner certificate (SURVEY §7 hard part 1).  For corner slot k with
+// signs (sx, sy) every point of the bounding box satisfies
+//   manhattan(p, corner) = C - s_p,  C = sx*cx + sy*cy,  s_p = sx*x + sy*y
+// exactly in the reals; K1 maximised t_p = fl(s_p).  With u = 2^-53 and
+// t2 the second-largest t, every p other than the winner has
+//   s_p <= t2 + u/(1-u)|t2|   and   fl-manhattan(p) >= (C - s_p)(1-u)^2,
+// so the winner is the unique reference argmin whenever its exact
+// reference key is below (C - t2 - u'|t2|)(1 - 2u).  Evaluated in long
+// double with an extra 2^-60 relative slack.
+bool certify_corner(const ohx_extremes_rec& r, int k) {
+  static const int sx[4] = {1, -1, -1, 1};
+  static const int sy[4] = {1, 1, -1, -1};
+  const double cx = sx[k] > 0 ? r.x[OHX_EAST] : r.x[OHX_WEST];
+  const double cy = sy[k] > 0 ? r.y[OHX_NORTH] : r.y[OHX_SOUTH];
+  const double t2 = r.second[k];
+  if (std::isinf(t2) && t2 < 0) return true;  // a single point: nothing to beat
+  const double m1 = std::abs(r.x[4 + k] - cx) + std::abs(r.y[4 + k] - cy);
+  const long double u = 0x1p-53L;
+  const long double C = static_cast<long double>(sx[k]) * cx +
+                        static_cast<long double>(sy[k]) * cy;
+  const long double g = C - static_cast<long double>(t2) -
+                        (u / (1.0L - u)) * std::fabs(static_cast<long double>(t2));
+  const long double scale = std::fabs(static_cast<long double>(cx)) +
+                            std::fabs(static_cast<long double>(cy)) +
+                            std::fabs(static_cast<long double>(t2));
+  const long double bound = g * (1.0L - 2.0000001L * u) - 0x1p-60L * scale;
+  return static_cast<long double>(m1) < bound;
+}
+
+// ------------------------------------------------ certified interior box --
+// Each edge i (origin a, constants A = fl(b.x-a.x), C = fl(b.y-a.y)) has
+// computed det = fl(fl(A*fl(p.y-a.y)) - fl(C*fl(p.x-a.x))) whose sign is that
+// of P1 - P2 with |P1 - A(p.y-a.y)| <= g2|A||p.y-a.y| (g2 = 2u+u^2), same for
+// P2.  det(p) >= E(p) - g2(|A||p.y-a.y| + |C||p.x-a.x|) with the exact affine
+// E(p) = A(p.y-a.y) - C(p.x-a.x).  That lower bound is concave in p, so its
+// minimum over a box sits at a corner: the box is certified when every
+// corner c of it has E(c) > 8u(|A||c.y-a.y| + |C||c.x-a.x|) (8u > g2 leaves
+// room for the long double evaluation), and then every point of the box has
+// det > 0 on every edge.
+struct EdgeL {
+  long double ax, ay, A, C;
+};
+
+bool box_ok(const std::vector<EdgeL>& edges, long double x0, long double x1,
+            long double y0, long double y1) {
+  if (!(x0 <= x1) || !(y0 <= y1)) return false;
+  const long double u8 = 8.0L * 0x1p-53L;
+  const long double xs[2] = {x0, x1}, ys[2] = {y0, y1};
+  for (const EdgeL& e : edges) {
+    for (long double cx : xs)
+      for (long double cy : ys) {
+        const long double dy = cy - e.ay, dx = cx - e.ax;
+        const long double E = e.A * dy - e.C * dx;
+        const long double margin =
+            u8 * (std::fabs(e.A) * std::fabs(dy) + std::fabs(e.C) * std::fabs(dx)) + 0x1p-1000L;
+        if (!(E > margin)) return false;
+      }
+  }
+  return true;
+}
+
+void fit_box(const double* oct, int m, const double* ea, const double* ec,
+             double box[4]) {
+  box[0] = 1.0;
+  box[1] = 0.0;
+  box[2] = 1.0;
+  box[3] = 0.0;  // empty
+  if (m < 3) return;
+  std::vector<EdgeL> edges;
+  long double vx0 = oct[0], vx1 = oct[0], vy0 = oct[1], vy1 = oct[1];
+  long double cx = 0, cy = 0;
+  for (int i = 0; i < m; ++i) {
+    edges.push_back({oct[2 * i], oct[2 * i + 1], ea[i], ec[i]});
+    vx0 = std::min<long double>(vx0, oct[2 * i]);
+    vx1 = std::max<long double>(vx1, oct[2 * i]);
+    vy0 = std::min<long double>(vy0, oct[2 * i + 1]);
+    vy1 = std::max<long double>(vy1, oct[2 * i + 1]);
+    cx += oct[2 * i];
+    cy += oct[2 * i + 1];
+  }
+  cx /= m;
+  cy /= m;
+  const long double hx = (vx1 - vx0) / 2, hy = (vy1 - vy0) / 2;
+  // 1) the largest centred box with the octagon's aspect ratio
+  long double lo = 0, hi = 1;
+  if (!box_ok(edges, cx - 1e-9L * hx, cx + 1e-9L * hx, cy - 1e-9L * hy, cy + 1e-9L * hy))
+    return;  // sliver octagon: no certified box, every point takes the full test
+  for (int it = 0; it < 60; ++it) {
+    const long double s = (lo + hi) / 2;
+    if (box_ok(edges, cx - s * hx, cx + s * hx, cy - s * hy, cy + s * hy)) lo = s;
+    else hi = s;
+  }
+  long double b[4] = {cx - lo * hx, cx + lo * hx, cy - lo * hy, cy + lo * hy};
+  // 2) grow the sides together: each round moves every side half way to the
+  //    furthest position it could reach alone, so no side pins a corner
+  //    early (a greedy one-side-at-a-time push gets stuck on near-flat
+  //    octagon edges); the last round takes the full step
+  const long double lim[4] = {vx0, vx1, vy0, vy1};
+  for (int round = 0; round < 24; ++round) {
+    const long double step = round == 23 ? 1.0L : 0.5L;
+    for (int side = 0; side < 4; ++side) {
+      long double good = b[side], bad = lim[side];
+      for (int it = 0; it < 48; ++it) {
+        const long double mid = (good + bad) / 2;
+        long double t[4] = {b[0], b[1], b[2], b[3]};
+        t[side] = mid;
+        if (box_ok(edges, t[0], t[1], t[2], t[3])) good = mid;
+        else bad = mid;
+      }
+      b[side] += step * (good - b[side]);
+    }
+  }
+  // round inwards to doubles, then re-verify the exact double box
+  double d[4] = {static_cast<double>(b[0]), static_cast<double>(b[1]),
+                 static_cast<double>(b[2]), static_cast<double>(b[3])};
+  if (static_cast<long double>(d[0]) < b[0]) d[0] = std::nextafter(d[0], INFINITY);
+  if (static_cast<long double>(d[1]) > b[1]) d[1] = std::nextafter(d[1], -INFINITY);
+  if (static_cast<long double>(d[2]) < b[2]) d[2] = std::nextafter(d[2], INFINITY);
+  if (static_cast<long double>(d[3]) > b[3]) d[3] = std::nextafter(d[3], -INFINITY);
+  if (box_ok(edges, d[0], d[1], d[2], d[3])) std::memcpy(box, d, sizeof(d));
+}
+
+}  // namespace
+
+namespace {
+thread_local std::string g_last_error;
+}
+void set_last_error(const char* msg) { g_last_error = msg; }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    const int code = (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+                         ? OHX_E_NODEVICE
+                         : (e == cudaErrorMemoryAllocation ? OHX_E_NOMEM : OHX_E_CUDA);
+    throw Error(code, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+// =================================================== internal pipeline API
+cudaStream_t ctx_stream(ohx_ctx* c) { return c->stream; }
+std::mutex& ctx_mutex(ohx_ctx* c) { return c->mu; }
+void ctx_bind(ohx_ctx* c) { bind(c); }
+
+const double* stage_points(ohx_ctx* c, const double* h_xy, std::uint64_t n,
+                           cudaStream_t s) {
+  const std::uint64_t bytes = n * 16;
+  dev_grow(reinterpret_cast<void**>(&c->d_pts), &c->pts_bytes, bytes, "points");
+  check_cuda(cudaMemcpyAsync(c->d_pts, h_xy, bytes, cudaMemcpyHostToDevice, s),
+             "cudaMemcpyAsync(points H2D)");
+  return c->d_pts;
+}
+
+std::uint8_t* stage_labels(ohx_ctx* c, std::uint64_t n) {
+  dev_grow(reinterpret_cast<void**>(&c->d_labels), &c->labels_bytes, n, "labels");
+  return c->d_labels;
+}
+
+void extremes(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+              ohx_extremes_rec* out, cudaStream_t s) {
+  if (n == 0) throw std::invalid_argument("find_axis_extremes: empty point set");
+  const int grid = k1_grid(c->device, n);
+  ensure_partials(c, grid);
+  check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
+  launch_k1(d_xy, n, base, c->d_partials, grid, c->d_ticket, c->d_rec, s);
+  check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
+  c->timed[0] = true;
+  ++c->launches;
+  check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
+                             cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec)");
+  check_cuda(cudaStreamSynchronize(s), "k1_extremes");
+  *out = *c->h_rec;
+}
+
+void corners_exact(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                   std::uint64_t base, const double bbox[4], ohx_corner_rec* out,
+                   cudaStream_t s) {
+  if (n == 0) throw std::invalid_argument("find_corner_extremes: empty point set");
+  const int grid = k1_grid(c->device, n);
+  ensure_partials(c, grid);
+  check_cuda(cudaEventRecord(c->ev[1][0], s), "cudaEventRecord");
+  launch_k1b(d_xy, n, base, bbox, c->d_partials, grid, c->d_ticket, c->d_crec, s);
+  check_cuda(cudaEventRecord(c->ev[1][1], s), "cudaEventRecord");
+  c->timed[1] = true;
+  ++c->launches;
+  check_cuda(cudaMemcpyAsync(c->h_crec, c->d_crec, sizeof(ohx_corner_rec),
+                             cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(crec)");
+  check_cuda(cudaStreamSynchronize(s), "k1b_corners");
+  *out = *c->h_crec;
+}
+
+void combine_extremes(const ohx_extremes_rec* recs, int k, ohx_extremes_rec* out) {
+  if (k < 1) throw std::invalid_argument("ohx_extremes_combine: no records");
+  ohx_extremes_rec r = recs[0];
+  for (int j = 1; j < k; ++j) {
+    const ohx_extremes_rec& b = recs[j];
+    for (int a = 0; a < 8; ++a) {
+      if (a >= 4) {
+        const double lo = std::min(r.key[a], b.key[a]);
+        r.second[a - 4] = std::max(std::max(r.second[a - 4], b.second[a - 4]), lo);
+      }
+      if (b.key[a] > r.key[a] || (b.key[a] == r.key[a] && b.idx[a] < r.idx[a])) {
+        r.key[a] = b.key[a];
+        r.idx[a] = b.idx[a];
+        r.x[a] = b.x[a];
+        r.y[a] = b.y[a];
+      }
+    }
+    r.n += b.n;
+  }
+  *out = r;
+}
+
+void combine_corners(const ohx_corner_rec* recs, int k, ohx_corner_rec* out) {
+  if (k < 1) throw std::invalid_argument("ohx_corners_combine: no records");
+  ohx_corner_rec r = recs[0];
+  for (int j = 1; j < k; ++j) {
+    const ohx_corner_rec& b = recs[j];
+    for (int a = 0; a < 4; ++a) {
+      if (b.key[a] < r.key[a] || (b.key[a] == r.key[a] && b.idx[a] < r.idx[a])) {
+        r.key[a] = b.key[a];
+        r.idx[a] = b.idx[a];
+        r.x[a] = b.x[a];
+        r.y[a] = b.y[a];
+      }
+    }
+    r.n += b.n;
+  }
+  *out = r;
+}
+
+std::uint32_t resolve_extremes(const ohx_extremes_rec& r, ohx_extreme_set* out) {
+  std::uint32_t mask = 0;
+  for (int a = 0; a < 8; ++a) {
+    out->ext[a] = r.idx[a];
+    out->x[a] = r.x[a];
+    out->y[a] = r.y[a];
+  }
+  for (int k = 0; k < 4; ++k)
+    if (!certify_corner(r, k)) mask |= 1u << k;
+  return mask;
+}
+
+void apply_corners(const ohx_corner_rec& c, ohx_extreme_set* ext) {
+  for (int k = 0; k < 4; ++k) {
+    ext->ext[4 + k] = c.idx[k];
+    ext->x[4 + k] = c.x[k];
+    ext->y[4 + k] = c.y[k];
+  }
+}
+
+int build_octagon(const double cand[16], double oct[16]) {
+  // reference filter.cpp:54-86: cyclic de-duplication, then repeatedly erase
+  // the first vertex that does not turn strictly left
+  std::vector<P2> cyc;
+  for (int k = 0; k < 8; ++k) {
+    const P2 p{cand[2 * k], cand[2 * k + 1]};
+    if (cyc.empty() || cyc.back().x != p.x || cyc.back().y != p.y) cyc.push_back(p);
+  }
+  while (cyc.size() > 1 && cyc.front().x == cyc.back().x && cyc.front().y == cyc.back().y)
+    cyc.pop_back();
+  for (bool again = true; again && cyc.size() > 2;) {
+    again = false;
+    const std::size_t m = cyc.size();
+    for (std::size_t i = 0; i < m; ++i) {
+      const P2& a = cyc[(i + m - 1) % m];
+      const P2& c = cyc[(i + 1) % m];
+      if (orient(a, cyc[i], c) <= 0) {
+        cyc.erase(cyc.begin() + static_cast<std::ptrdiff_t>(i));
+        again = true;
+        break;
+      }
+    }
+  }
+  for (std::size_t i = 0; i < cyc.size(); ++i) {
+    oct[2 * i] = cyc[i].x;
+    oct[2 * i + 1] = cyc[i].y;
+  }
+  return static_cast<int>(cyc.size());
+}
+
+void make_plan(const ohx_extreme_set& e, const double* oct, int m,
+               ohx_filter_plan* p) {
+  std::memset(p, 0, sizeof(*p));
+  if (m < 0 || m > 8) throw std::invalid_argument("octagon must have 0..8 vertices");
+  p->m = m;
+  if (m >= 3) {
+    for (int i = 0; i < m; ++i) {
+      const int j = (i + 1 == m) ? 0 : i + 1;
+      p->ax[i] = oct[2 * i];
+      p->ay[i] = oct[2 * i + 1];
+      p->ea[i] = oct[2 * j] - oct[2 * i];          // (b.x - a.x)
+      p->ec[i] = oct[2 * j + 1] - oct[2 * i + 1];  // (b.y - a.y)
+    }
+  }
+  // find_queue edges E->N, N->W, W->S, S->E (filter.cpp:94-97)
+  const int from[4] = {OHX_EAST, OHX_NORTH, OHX_WEST, OHX_SOUTH};
+  const int to[4] = {OHX_NORTH, OHX_WEST, OHX_SOUTH, OHX_EAST};
+  for (int q = 0; q < 4; ++q) {
+    p->qax[q] = e.x[from[q]];
+    p->qay[q] = e.y[from[q]];
+    p->qa[q] = e.x[to[q]] - e.x[from[q]];
+    p->qc[q] = e.y[to[q]] - e.y[from[q]];
+  }
+  // kept overrides in the reference's first-match order (filter.cpp:108-117)
+  const int slot[8] = {OHX_EAST, OHX_NE, OHX_NORTH, OHX_NW,
+                       OHX_WEST, OHX_SW, OHX_SOUTH, OHX_SE};
+  for (int k = 0; k < 8; ++k) {
+    p->kept[k] = e.ext[slot[k]];
+    p->kept_label[k] = static_cast<std::uint8_t>(1 + k / 2);
+  }
+  fit_box(oct, m, p->ea, p->ec, p->box);
+}
+
+void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+            const ohx_filter_plan& plan, std::uint8_t* d_labels,
+            std::uint64_t counts[4], cudaStream_t s) {
+  if (n == 0) throw std::invalid_argument("classify_points: empty point set");
+  KPlan kp;
+  std::memcpy(kp.ax, plan.ax, sizeof(kp.ax));
+  std::memcpy(kp.ay, plan.ay, sizeof(kp.ay));
+  std::memcpy(kp.ea, plan.ea, sizeof(kp.ea));
+  std::memcpy(kp.ec, plan.ec, sizeof(kp.ec));
+  std::memcpy(kp.qax, plan.qax, sizeof(kp.qax));
+  std::memcpy(kp.qay, plan.qay, sizeof(kp.qay));
+  std::memcpy(kp.qa, plan.qa, sizeof(kp.qa));
+  std::memcpy(kp.qc, plan.qc, sizeof(kp.qc));
+  std::memcpy(kp.box, plan.box, sizeof(kp.box));
+  for (int k = 0; k < 8; ++k) {
+    const std::uint64_t g = plan.kept[k];
+    kp.kept[k] = (g >= base && g - base < n) ? g - base : ~0ull;
+    kp.kept_label[k] = plan.kept_label[k];
+  }
+  kp.m = plan.m;
+
+  const std::uint64_t ntiles = (n + kK2Tile - 1) / kK2Tile;
+  dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes,
+           k2_status_bytes(ntiles), "look-back status");
+  const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
+  // queue capacity: a quarter of the shard plus slack; grown and re-run on
+  // overflow (counts are exact even when stores are dropped)
+  std::uint64_t cap = std::min<std::uint64_t>(n, std::max<std::uint64_t>(4096, n / 4 + n / 16));
+  if (c->queue_bytes / (4ull * idx_bytes) > cap)
+    cap = std::min<std::uint64_t>(n, c->queue_bytes / (4ull * idx_bytes));
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    dev_grow(&c->d_queues, &c->queue_bytes, 4ull * idx_bytes * cap, "queues");
+    check_cuda(cudaEventRecord(c->ev[2][0], s), "cudaEventRecord");
+    launch_k2(d_xy, n, kp, c->d_status, ntiles, c->d_queues, idx_bytes, cap,
+              d_labels, c->d_counts, s);
+    check_cuda(cudaEventRecord(c->ev[2][1], s), "cudaEventRecord");
+    c->timed[2] = true;
+    ++c->launches;
+    check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
+    check_cuda(cudaStreamSynchronize(s), "k2_filter");
+    std::uint64_t mx = 0;
+    for (int q = 0; q < 4; ++q) {
+      counts[q] = c->h_counts[q];
+      mx = std::max<std::uint64_t>(mx, counts[q]);
+    }
+    if (mx <= cap) break;
+    if (attempt == 1) throw Error(OHX_E_INTERNAL, "k2_filter: queue overflow after regrow");
+    cap = std::min<std::uint64_t>(n, mx + mx / 8 + 1024);
+  }
+  c->last_xy = d_xy;
+  c->last_n = n;
+  c->last_base = base;
+  c->last_cap = cap;
+  c->last_idx_bytes = idx_bytes;
+  for (int q = 0; q < 4; ++q) c->last_counts[q] = counts[q];
+}
+
+void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
+                 std::uint64_t cap, cudaStream_t s) {
+  if (q < 1 || q > 4) throw std::invalid_argument("queue must be 1..4");
+  if (c->last_n == 0) throw std::invalid_argument("no filter result in this context");
+  const std::uint64_t cnt = c->last_counts[q - 1];
+  if (cnt > cap) throw std::invalid_argument("queue larger than the output capacity");
+  if (cnt == 0) return;
+  const auto* qbase = static_cast<const char*>(c->d_queues) +
+                      std::uint64_t(q - 1) * c->last_cap * c->last_idx_bytes;
+  if (h_xy) {
+    dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, cnt * 16, "gather");
+    launch_gather(c->last_xy, qbase, c->last_idx_bytes, cnt, c->d_gather, s);
+    ++c->launches;
+    check_cuda(cudaMemcpyAsync(h_xy, c->d_gather, cnt * 16, cudaMemcpyDeviceToHost, s),
+               "cudaMemcpyAsync(queue xy)");
+  }
+  if (h_idx) {
+    if (c->last_idx_bytes == 8) {
+      check_cuda(cudaMemcpyAsync(h_idx, qbase, cnt * 8, cudaMemcpyDeviceToHost, s),
+                 "cudaMemcpyAsync(queue idx)");
+      check_cuda(cudaStreamSynchronize(s), "queue fetch");
+    } else {
+      std::vector<std::uint32_t> tmp(cnt);
+      check_cuda(cudaMemcpyAsync(tmp.data(), qbase, cnt * 4, cudaMemcpyDeviceToHost, s),
+                 "cudaMemcpyAsync(queue idx)");
+      check_cuda(cudaStreamSynchronize(s), "queue fetch");
+      for (std::uint64_t k = 0; k < cnt; ++k) h_idx[k] = c->last_base + tmp[k];
+    }
+    if (c->last_idx_bytes == 8 && c->last_base)
+      for (std::uint64_t k = 0; k < cnt; ++k) h_idx[k] += c->last_base;
+  }
+  check_cuda(cudaStreamSynchronize(s), "queue fetch");
+}
+
+FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                        std::uint8_t* d_labels, cudaStream_t s) {
+  FilterOut f{};
+  ohx_extremes_rec rec;
+  extremes(c, d_xy, n, 0, &rec, s);
+  const std::uint32_t mask = resolve_extremes(rec, &f.ext);
+  f.corner_pass = mask != 0;
+  if (mask) {
+    const double bbox[4] = {rec.x[OHX_EAST], rec.y[OHX_NORTH], rec.x[OHX_WEST],
+                            rec.y[OHX_SOUTH]};
+    ohx_corner_rec cr;
+    corners_exact(c, d_xy, n, 0, bbox, &cr, s);
+    apply_corners(cr, &f.ext);
+  }
+  const int slot[8] = {OHX_EAST, OHX_NE, OHX_NORTH, OHX_NW,
+                       OHX_WEST, OHX_SW, OHX_SOUTH, OHX_SE};
+  double cand[16];
+  for (int k = 0; k < 8; ++k) {
+    cand[2 * k] = f.ext.x[slot[k]];
+    cand[2 * k + 1] = f.ext.y[slot[k]];
+  }
+  f.m = build_octagon(cand, f.oct);
+  make_plan(f.ext, f.oct, f.m, &f.plan);
+  filter(c, d_xy, n, 0, f.plan, d_labels, f.counts, s);
+  return f;
+}
+
+ohx_ctx* create_ctx(int device) {
+  int ndev = 0;
+  check_cuda(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev)
+    throw Error(OHX_E_NODEVICE, "device " + std::to_string(device) + " not visible (" +
+                                    std::to_string(ndev) + " devices)");
+  cudaDeviceProp prop;
+  check_cuda(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10)
+    throw Error(OHX_E_NODEVICE, std::string("device ") + prop.name +
+                                    " is not sm_100 (this library is built for sm_100a only)");
+  auto c = std::make_unique<ohx_ctx>();
+  c->device = device;
+  bind(c.get());
+  check_cuda(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  check_cuda(cudaMalloc(&c->d_ticket, 256), "cudaMalloc(ticket)");
+  check_cuda(cudaMemset(c->d_ticket, 0, 256), "cudaMemset(ticket)");
+  check_cuda(cudaMalloc(&c->d_rec, sizeof(ohx_extremes_rec)), "cudaMalloc(rec)");
+  check_cuda(cudaMalloc(&c->d_crec, sizeof(ohx_corner_rec)), "cudaMalloc(crec)");
+  check_cuda(cudaMalloc(&c->d_counts, 64), "cudaMalloc(counts)");
+  check_cuda(cudaMallocHost(&c->h_rec, sizeof(ohx_extremes_rec)), "cudaMallocHost");
+  check_cuda(cudaMallocHost(&c->h_crec, sizeof(ohx_corner_rec)), "cudaMallocHost");
+  check_cuda(cudaMallocHost(&c->h_counts, 64), "cudaMallocHost");
+  for (auto& pair : c->ev)
+    for (auto& e : pair) check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+  return c.release();
+}
+
+void destroy_ctx(ohx_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (void* p : {static_cast<void*>(c->d_partials), static_cast<void*>(c->d_ticket),
+                  static_cast<void*>(c->d_rec), static_cast<void*>(c->d_crec),
+                  static_cast<void*>(c->d_counts), static_cast<void*>(c->d_status),
+                  c->d_queues, static_cast<void*>(c->d_pts),
+                  static_cast<void*>(c->d_labels), static_cast<void*>(c->d_gather)})
+    if (p) cudaFree(p);
+  for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_crec),
+                  static_cast<void*>(c->h_counts)})
+    if (p) cudaFreeHost(p);
+  for (auto& pair : c->ev)
+    for (auto& e : pair)
+      if (e) cudaEventDestroy(e);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+ohx_ctx* default_ctx(int device) {
+  static std::mutex mu;
+  static std::vector<ohx_ctx*> ctxs;  // intentionally leaked at exit
+  std::lock_guard<std::mutex> g(mu);
+  if (device < 0) {
+    const char* env = std::getenv("OHX_DEVICE");
+    device = env ? std::atoi(env) : 0;
+  }
+  if (static_cast<int>(ctxs.size()) <= device) ctxs.resize(device + 1, nullptr);
+  if (!ctxs[device]) ctxs[device] = create_ctx(device);
+  return ctxs[device];
+}
+
+}  // namespace ohx
+
+// =================================================================== C ABI
+using namespace ohx;
+
+extern "C" {
+
+int ohx_abi_version(void) { return OHX_ABI_VERSION; }
+
+const char* ohx_last_error(void) { return g_last_error.c_str(); }
+
+int ohx_device_count(int* n) {
+  return guard([&] {
+    int k = 0;
+    check_cuda(cudaGetDeviceCount(&k), "cudaGetDeviceCount");
+    *n = k;
+  });
+}
+
+int ohx_ctx_create(int device, ohx_ctx** out) {
+  return guard([&] { *out = create_ctx(device); });
+}
+
+int ohx_ctx_destroy(ohx_ctx* ctx) {
+  return guard([&] { destroy_ctx(ctx); });
+}
+
+int ohx_ctx_default(int device, ohx_ctx** out) {
+  return guard([&] { *out = default_ctx(device); });
+}
+
+int ohx_ctx_device(const ohx_ctx* ctx) { return ctx ? ctx->device : -1; }
+
+uint64_t ohx_ctx_launches(const ohx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ohx_ctx_kernel_ms(ohx_ctx* ctx, double ms[3]) {
+  return guard([&] {
+    std::lock_guard<std::mutex> g(ctx->mu);
+    bind(ctx);
+    for (int k = 0; k < 3; ++k) {
+      ms[k] = -1.0;
+      if (!ctx->timed[k]) continue;
+      float v = 0.f;
+      check_cuda(cudaEventSynchronize(ctx->ev[k][1]), "cudaEventSynchronize");
+      check_cuda(cudaEventElapsedTime(&v, ctx->ev[k][0], ctx->ev[k][1]), "cudaEventElapsedTime");
+      ms[k] = v;
+    }
+  });
+}
+
+int ohx_extremes(ohx_ctx* ctx, const double* d_xy, uint64_t n, uint64_t index_base,
+                 ohx_extremes_rec* h_rec, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> g(ctx->mu);
+    bind(ctx);
+    extremes(ctx, d_xy, n, index_base, h_rec, pick(ctx, stream));
+  });
+}
+
+int ohx_extremes_combine(const ohx_extremes_rec* recs, int k, ohx_extremes_rec* out) {
+  return guard([&] { combine_extremes(recs, k, out); });
+}
+
+int ohx_extremes_resolve(const ohx_extremes_rec* rec, ohx_extreme_set* out,
+                         uint32_t* uncertified_mask) {
+  return guard([&] {
+    const std::uint32_t m = resolve_extremes(*rec, out);
+    if (uncertified_mask) *uncertified_mask = m;
+  });
+}
+
+int ohx_corners_exact(ohx_ctx* ctx, const double* d_xy, uint64_t n,
+                      uint64_t index_base, const double bbox[4],
+                      ohx_corner_rec* h_rec, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> g(ctx->mu);
+    bind(ctx);
+    corners_exact(ctx, d_xy, n, index_base, bbox, h_rec, pick(ctx, stream));
+  });
+}
+
+int ohx_corners_combine(const ohx_corner_rec* recs, int k, ohx_corner_rec* out) {
+  return guard([&] { combine_corners(recs, k, out); });
+}
+
+int ohx_build_octagon(const double cand_xy[16], double oct_xy[16], int* m) {
+  return guard([&] { *m = build_octagon(cand_xy, oct_xy); });
+}
+
+int ohx_filter_plan_build(const ohx_extreme_set* ext, const double* oct_xy, int m,
+                          ohx_filter_plan* plan) {
+  return guard([&] { make_plan(*ext, oct_xy, m, plan); });
+}
+
+int ohx_filter(ohx_ctx* ctx, const double* d_xy, uint64_t n, uint64_t index_base,
+               const ohx_filter_plan* plan, uint8_t* d_labels, uint64_t h_counts[4],
+               void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> g(ctx->mu);
+    bind(ctx);
+    filter(ctx, d_xy, n, index_base, *plan, d_labels, h_counts, pick(ctx, stream));
+  });
+}
+
+int ohx_queue_fetch(ohx_ctx* ctx, int q, uint64_t* h_idx, double* h_xy, uint64_t cap,
+                    void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> g(ctx->mu);
+    bind(ctx);
+    queue_fetch(ctx, q, h_idx, h_xy, cap, pick(ctx, stream));
+  });
+}
+
+int ohx_queue_device(ohx_ctx* ctx, int q, const void** d_idx, int* idx_bytes,
+                     uint64_t* count) {
+  return guard([&] {
+    if (q < 1 || q > 4) throw std::invalid_argument("queue must be 1..4");
+    *d_idx = static_cast<const char*>(ctx->d_queues) +
+             std::uint64_t(q - 1) * ctx->last_cap * ctx->last_idx_bytes;
+    *idx_bytes = ctx->last_idx_bytes;
+    *count = ctx->last_counts[q - 1];
+  });
+}
+
+}  // extern "C"

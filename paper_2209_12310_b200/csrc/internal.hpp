@@ -1,0 +1,112 @@
+// internal.hpp -- declarations shared by the CUDA kernels (kernels.cu), the
+// C ABI (capi.cpp), the host hull (hull.cpp) and the C++ API
+// (octohull_api.cpp).  Not installed; the public surfaces are
+// include/ohx.h and include/octohull/*.hpp.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ohx.h"
+
+namespace ohx {
+
+// ---- kernel-side plan (K2): the C-ABI plan with shard-local kept indices
+struct KPlan {
+  double ax[8], ay[8], ea[8], ec[8];
+  double qax[4], qay[4], qa[4], qc[4];
+  double box[4];
+  std::uint64_t kept[8];  // shard-local, ~0 when not in this shard
+  std::uint32_t kept_label[8];
+  std::int32_t m;
+};
+
+// per-block K1 partial (device scratch)
+struct K1Partial {
+  double key[8];
+  std::uint64_t idx[8];
+  double second[4];
+};
+
+// geometry of the K2 tiles (kernels.cu)
+constexpr int kK2Block = 256;
+constexpr int kK2Items = 8;
+constexpr std::uint64_t kK2Tile = std::uint64_t(kK2Block) * kK2Items;
+
+// Launchers (kernels.cu).  All asynchronous on `stream`.
+int k1_grid(int device, std::uint64_t n);
+void launch_k1(const double* d_xy, std::uint64_t n, std::uint64_t base,
+               K1Partial* partials, int grid, unsigned* ticket,
+               ohx_extremes_rec* d_out, cudaStream_t stream);
+void launch_k1b(const double* d_xy, std::uint64_t n, std::uint64_t base,
+                const double bbox[4], K1Partial* partials, int grid,
+                unsigned* ticket, ohx_corner_rec* d_out, cudaStream_t stream);
+// K2 scratch: 4*ntiles look-back status words followed by the tile counter.
+inline std::uint64_t k2_status_bytes(std::uint64_t ntiles) {
+  return ntiles * 4 * sizeof(std::uint64_t) + 64;
+}
+// K2 (re-arms its scratch with one memset on `stream` first).  d_queues
+// holds 4 queues of `cap` shard-local indices of idx_bytes each.
+void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan,
+               std::uint64_t* d_status, std::uint64_t ntiles, void* d_queues,
+               int idx_bytes, std::uint64_t cap, std::uint8_t* d_labels,
+               unsigned long long* d_counts, cudaStream_t stream);
+void launch_gather(const double* d_xy, const void* d_idx, int idx_bytes,
+                   std::uint64_t count, double* d_out, cudaStream_t stream);
+
+// ---- host helpers (capi.cpp)
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+void check_cuda(cudaError_t e, const char* what);
+// thread-local message returned by ohx_last_error()
+void set_last_error(const char* msg);
+
+// Runs f() and maps exceptions to the C ABI's status codes; nothing ever
+// propagates across the extern "C" boundary.
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return OHX_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    set_last_error(e.what());
+    return OHX_E_INVALID;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return OHX_E_NOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return OHX_E_INTERNAL;
+  } catch (...) {
+    set_last_error("unknown exception");
+    return OHX_E_INTERNAL;
+  }
+}
+
+// ---- host hull (hull.cpp), semantics of hull.cpp:18-150 of the reference
+struct P2 {
+  double x, y;
+};
+std::vector<P2> quadrant_chain(std::vector<P2> pts, int quadrant);
+std::vector<P2> finalize_cycle(std::vector<P2> cycle);
+std::vector<P2> hull_from_queue_points(const P2 anchors[4],
+                                       const P2* const q_pts[4],
+                                       const std::uint64_t q_len[4]);
+std::vector<P2> monotone_chain(const P2* pts, std::uint64_t n);
+int orient(const P2& a, const P2& b, const P2& c);
+
+// ---- host generator (pointgen.cpp)
+void generate_points(int dist, std::uint64_t n, std::uint64_t seed,
+                     double distort_pct, double* xy, int threads);
+
+}  // namespace ohx

@@ -1,0 +1,594 @@
+// kernels.cu -- the sm_100a kernels of the heaphull filter.
+//
+//   K1  k1_extremes    one streaming pass: 4 axis argmax/argmin + 4 diagonal
+//                      argmax with second-best keys (corner certificate).
+//                      Replaces the 8 passes of find_axis_extremes and
+//                      find_corner_extremes (reference filter.cpp:8-45).
+//   K1b k1b_corners    exact Manhattan corner argmins (filter.cpp:25-45),
+//                      run only when the certificate fails.
+//   K2  k2_filter      octagon classify (filter.cpp:104-131, geometry.cpp:8-25,
+//                      filter.cpp:88-102) fused with the ordered per-quadrant
+//                      compaction of build_queues (hull.cpp:124-131):
+//                      warp ballot/popc, block scan, decoupled look-back.
+//   gather_xy          survivor coordinates for a queue (index order).
+//
+// All arithmetic on point data reproduces the reference's binary64
+// operations exactly: explicit __dadd_rn/__dsub_rn/__dmul_rn (no FMA
+// contraction; the TU is also built with -fmad=false).
+//
+// HBM is the roofline: every kernel streams AoS double2 points with 16-byte
+// non-allocating loads, several loads in flight per thread, grids sized from
+// the SM count and the occupancy of the kernel.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "internal.hpp"
+
+namespace ohx {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ std::uint64_t ld_relaxed(const std::uint64_t* p) {
+  std::uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_relaxed(std::uint64_t* p, std::uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ===================================================================== K1 ==
+// Every slot is an argmax of a maximised key; ties keep the smaller index
+// (combine_max / combine_min, reference parallel.hpp:34-43; argmin of a key
+// is argmax of its exact negation).  Within a thread indices only grow, so
+// a strict '>' keeps the earliest index.
+
+template <int NK, int NS>
+struct ArgState {
+  double k[NK];
+  std::uint64_t i[NK];
+  double s[NS > 0 ? NS : 1];
+
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int a = 0; a < NK; ++a) {
+      k[a] = __longlong_as_double(0xfff0000000000000ll);  // -inf
+      i[a] = ~0ull;
+    }
+#pragma unroll
+    for (int a = 0; a < (NS > 0 ? NS : 1); ++a) s[a] = __longlong_as_double(0xfff0000000000000ll);
+  }
+};
+
+// in-thread update: strict improvement only
+__device__ __forceinline__ void upd(double& bk, std::uint64_t& bi, double key,
+                                    std::uint64_t j) {
+  const bool take = key > bk;
+  bk = take ? key : bk;
+  bi = take ? j : bi;
+}
+
+// in-thread update tracking the second-largest key of the multiset
+__device__ __forceinline__ void upd2(double& bk, std::uint64_t& bi, double& s2,
+                                     double key, std::uint64_t j) {
+  const bool take = key > bk;
+  const double lo = take ? bk : key;  // the value that does not become best
+  s2 = lo > s2 ? lo : s2;
+  bk = take ? key : bk;
+  bi = take ? j : bi;
+}
+
+// cross-thread merge of (ak,ai) with (bk,bi): argmax, ties -> smaller index
+__device__ __forceinline__ void merge(double& ak, std::uint64_t& ai, double bk,
+                                      std::uint64_t bi) {
+  const bool take = bk > ak || (bk == ak && bi < ai);
+  ak = take ? bk : ak;
+  ai = take ? bi : ai;
+}
+
+__device__ __forceinline__ void merge2(double& ak, std::uint64_t& ai, double& as,
+                                       double bk, std::uint64_t bi, double bs) {
+  // second of the union = max(both seconds, the smaller of the two bests)
+  const double lo = ak < bk ? ak : bk;
+  double s = as > bs ? as : bs;
+  s = lo > s ? lo : s;
+  as = s;
+  merge(ak, ai, bk, bi);
+}
+
+template <int NK, int NS>
+__device__ __forceinline__ void warp_reduce(ArgState<NK, NS>& st) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int a = 0; a < NK; ++a) {
+      const double ok = __shfl_xor_sync(kFull, st.k[a], off);
+      const std::uint64_t oi = __shfl_xor_sync(kFull, st.i[a], off);
+      if (a >= NK - NS) {
+        const double os = __shfl_xor_sync(kFull, st.s[a - (NK - NS)], off);
+        merge2(st.k[a], st.i[a], st.s[a - (NK - NS)], ok, oi, os);
+      } else {
+        merge(st.k[a], st.i[a], ok, oi);
+      }
+    }
+  }
+}
+
+// Block-wide reduction; the result is valid in warp 0.
+template <int NK, int NS, int BLOCK>
+__device__ __forceinline__ void block_reduce(ArgState<NK, NS>& st) {
+  constexpr int W = BLOCK / 32;
+  __shared__ double sk[W][NK];
+  __shared__ std::uint64_t si[W][NK];
+  __shared__ double ss[W][NS > 0 ? NS : 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  warp_reduce(st);
+  __syncthreads();  // smem may be reused by a previous call
+  if (lane == 0) {
+#pragma unroll
+    for (int a = 0; a < NK; ++a) {
+      sk[warp][a] = st.k[a];
+      si[warp][a] = st.i[a];
+    }
+#pragma unroll
+    for (int a = 0; a < NS; ++a) ss[warp][a] = st.s[a];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    st.init();
+    if (lane < W) {
+#pragma unroll
+      for (int a = 0; a < NK; ++a) {
+        st.k[a] = sk[lane][a];
+        st.i[a] = si[lane][a];
+      }
+#pragma unroll
+      for (int a = 0; a < NS; ++a) st.s[a] = ss[lane][a];
+    }
+    warp_reduce(st);
+  }
+}
+
+// Final grid combine: the last block to finish (atomic ticket) merges all
+// per-block partials.  Returns true in the block that holds the result
+// (valid in warp 0).
+template <int NK, int NS, int BLOCK>
+__device__ __forceinline__ bool grid_combine(ArgState<NK, NS>& st,
+                                             K1Partial* partials,
+                                             unsigned* ticket) {
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    K1Partial& p = partials[blockIdx.x];
+#pragma unroll
+    for (int a = 0; a < NK; ++a) {
+      p.key[a] = st.k[a];
+      p.idx[a] = st.i[a];
+    }
+#pragma unroll
+    for (int a = 0; a < NS; ++a) p.second[a] = st.s[a];
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  st.init();
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += BLOCK) {
+    const K1Partial* p = partials + b;
+#pragma unroll
+    for (int a = 0; a < NK; ++a) {
+      const double k = __ldcg(&p->key[a]);
+      const std::uint64_t i = __ldcg(reinterpret_cast<const unsigned long long*>(&p->idx[a]));
+      if (a >= NK - NS) {
+        merge2(st.k[a], st.i[a], st.s[a - (NK - NS)], k, i,
+               __ldcg(&p->second[a - (NK - NS)]));
+      } else {
+        merge(st.k[a], st.i[a], k, i);
+      }
+    }
+  }
+  block_reduce<NK, NS, BLOCK>(st);
+  if (threadIdx.x == 0) *ticket = 0u;  // re-arm for the next launch
+  return true;
+}
+
+constexpr int kK1Block = 256;
+constexpr int kK1Unroll = 4;
+
+// Slots (ohx.h): 0 east x, 1 north y, 2 west -x, 3 south -y,
+//                4 ne fl(x+y), 5 nw fl(y-x), 6 sw -fl(x+y), 7 se fl(x-y);
+// slots 4..7 also keep their second-best key.
+struct K1Visit {
+  __device__ __forceinline__ static void visit(ArgState<8, 4>& st, double2 p,
+                                               std::uint64_t j) {
+    const double t = __dadd_rn(p.x, p.y);
+    const double d = __dsub_rn(p.x, p.y);
+    upd(st.k[0], st.i[0], p.x, j);
+    upd(st.k[1], st.i[1], p.y, j);
+    upd(st.k[2], st.i[2], -p.x, j);
+    upd(st.k[3], st.i[3], -p.y, j);
+    upd2(st.k[4], st.i[4], st.s[0], t, j);
+    upd2(st.k[5], st.i[5], st.s[1], -d, j);
+    upd2(st.k[6], st.i[6], st.s[2], -t, j);
+    upd2(st.k[7], st.i[7], st.s[3], d, j);
+  }
+};
+
+__global__ void __launch_bounds__(kK1Block)
+    k1_extremes(const double2* __restrict__ pts, std::uint64_t n,
+                std::uint64_t base, K1Partial* partials, unsigned* ticket,
+                ohx_extremes_rec* out) {
+  ArgState<8, 4> st;
+  st.init();
+  const std::uint64_t stride = std::uint64_t(gridDim.x) * kK1Block;
+  std::uint64_t j = std::uint64_t(blockIdx.x) * kK1Block + threadIdx.x;
+  for (; j + (kK1Unroll - 1) * stride < n; j += kK1Unroll * stride) {
+    double2 v[kK1Unroll];
+#pragma unroll
+    for (int u = 0; u < kK1Unroll; ++u) v[u] = ld_stream(pts + j + u * stride);
+#pragma unroll
+    for (int u = 0; u < kK1Unroll; ++u) K1Visit::visit(st, v[u], j + u * stride);
+  }
+  for (; j < n; j += stride) K1Visit::visit(st, ld_stream(pts + j), j);
+
+  block_reduce<8, 4, kK1Block>(st);
+  if (!grid_combine<8, 4, kK1Block>(st, partials, ticket)) return;
+  if (threadIdx.x < 8) {
+    // lane a of warp 0 publishes slot a with its winner's coordinates
+    const int a = threadIdx.x;
+    double k = 0, s = 0;
+    std::uint64_t i = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (b == a) {
+        k = st.k[b];
+        i = st.i[b];
+        if (b >= 4) s = st.s[b - 4];
+      }
+    const double2 p = pts[i];
+    out->key[a] = k;
+    out->idx[a] = base + i;
+    out->x[a] = p.x;
+    out->y[a] = p.y;
+    if (a >= 4) out->second[a - 4] = s;
+    if (a == 0) out->n = n;
+  }
+}
+
+// ==================================================================== K1b ==
+// slot k: argmax of -(|x - cx| + |y - cy|) = the reference argmin of
+// manhattan(p, corner) (geometry.hpp:35-37), corners ne, nw, sw, se.
+__global__ void __launch_bounds__(kK1Block)
+    k1b_corners(const double2* __restrict__ pts, std::uint64_t n,
+                std::uint64_t base, double xmax, double ymax, double xmin,
+                double ymin, K1Partial* partials, unsigned* ticket,
+                ohx_corner_rec* out) {
+  ArgState<4, 0> st;
+  st.init();
+  const double cx[4] = {xmax, xmin, xmin, xmax};
+  const double cy[4] = {ymax, ymax, ymin, ymin};
+  const std::uint64_t stride = std::uint64_t(gridDim.x) * kK1Block;
+  std::uint64_t j = std::uint64_t(blockIdx.x) * kK1Block + threadIdx.x;
+  auto visit = [&](double2 p, std::uint64_t jj) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const double m = __dadd_rn(fabs(__dsub_rn(p.x, cx[a])), fabs(__dsub_rn(p.y, cy[a])));
+      upd(st.k[a], st.i[a], -m, jj);
+    }
+  };
+  for (; j + (kK1Unroll - 1) * stride < n; j += kK1Unroll * stride) {
+    double2 v[kK1Unroll];
+#pragma unroll
+    for (int u = 0; u < kK1Unroll; ++u) v[u] = ld_stream(pts + j + u * stride);
+#pragma unroll
+    for (int u = 0; u < kK1Unroll; ++u) visit(v[u], j + u * stride);
+  }
+  for (; j < n; j += stride) visit(ld_stream(pts + j), j);
+
+  block_reduce<4, 0, kK1Block>(st);
+  if (!grid_combine<4, 0, kK1Block>(st, partials, ticket)) return;
+  if (threadIdx.x < 4) {
+    const int a = threadIdx.x;
+    double k = 0;
+    std::uint64_t i = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (b == a) {
+        k = st.k[b];
+        i = st.i[b];
+      }
+    const double2 p = pts[i];
+    out->key[a] = -k;
+    out->idx[a] = base + i;
+    out->x[a] = p.x;
+    out->y[a] = p.y;
+    if (a == 0) out->n = n;
+  }
+}
+
+// ===================================================================== K2 ==
+constexpr std::uint64_t kFlagA = 1ull << 62;  // aggregate published
+constexpr std::uint64_t kFlagP = 2ull << 62;  // inclusive prefix published
+constexpr std::uint64_t kValMask = (1ull << 62) - 1;
+
+// orientation(a, b, p) < 0 with the edge constants A = fl(b.x-a.x),
+// C = fl(b.y-a.y): det = fl(fl(A*fl(p.y-a.y)) - fl(C*fl(p.x-a.x))) is
+// negative exactly when the first rounded product is below the second
+// (geometry.hpp:27-32).
+__device__ __forceinline__ bool right_of(double px, double py, double ax,
+                                         double ay, double A, double C) {
+  return __dmul_rn(A, __dsub_rn(py, ay)) < __dmul_rn(C, __dsub_rn(px, ax));
+}
+
+__device__ __forceinline__ std::uint32_t classify(const KPlan& P, double2 p,
+                                                  std::uint64_t j,
+                                                  bool tile_has_kept) {
+  if (tile_has_kept) {
+    // kept overrides, first match wins (filter.cpp:108-124)
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (j == P.kept[k]) return P.kept_label[k];
+  }
+  // certified interior box: every edge determinant provably > 0 there
+  if (p.x >= P.box[0] && p.x <= P.box[1] && p.y >= P.box[2] && p.y <= P.box[3])
+    return 0;
+  bool outside = P.m < 3;  // degenerate octagon filters nothing (filter.cpp:125)
+  if (!outside) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      outside |= right_of(p.x, p.y, P.ax[e], P.ay[e], P.ea[e], P.ec[e]);
+  }
+  if (!outside) return 0;
+  // find_queue (filter.cpp:88-102): first strictly-right edge, else 1
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (right_of(p.x, p.y, P.qax[q], P.qay[q], P.qa[q], P.qc[q])) return q + 1;
+  return 1;
+}
+
+// One warp walks back over predecessor tiles' status words of one quadrant
+// and returns the exclusive prefix (decoupled look-back).
+__device__ __forceinline__ std::uint64_t look_back(const std::uint64_t* st,
+                                                   std::uint64_t tile) {
+  const int lane = threadIdx.x & 31;
+  std::uint64_t excl = 0;
+  long long pos = static_cast<long long>(tile) - 1;
+  for (;;) {
+    const long long at = pos - lane;
+    std::uint64_t w = kFlagP;  // before tile 0: a virtual zero prefix
+    if (at >= 0) {
+      do {
+        w = ld_relaxed(st + at);
+      } while ((w >> 62) == 0);
+    }
+    const unsigned pmask = __ballot_sync(kFull, (w & kFlagP) != 0);
+    std::uint64_t v = w & kValMask;
+    if (pmask) {
+      const int first = __ffs(pmask) - 1;  // nearest inclusive prefix
+      if (lane > first) v = 0;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+    excl += v;
+    if (pmask) return excl;
+    pos -= 32;
+  }
+}
+
+template <typename IdxT>
+__global__ void __launch_bounds__(kK2Block)
+    k2_filter(const double2* __restrict__ pts, std::uint64_t n,
+              const __grid_constant__ KPlan plan, std::uint64_t* status,
+              std::uint64_t ntiles, unsigned* tile_counter, IdxT* queues,
+              std::uint64_t cap, std::uint8_t* labels,
+              unsigned long long* counts) {
+  constexpr int W = kK2Block / 32;
+  constexpr int SEG = kK2Items * W;  // (item, warp) segments of a tile
+  __shared__ std::uint32_t s_tile;
+  __shared__ std::uint32_t s_off[4][SEG];
+  __shared__ std::uint64_t s_excl[4];
+  __shared__ std::uint32_t s_agg[4];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const std::uint64_t tile = s_tile;
+  const std::uint64_t t0 = tile * kK2Tile;
+
+  bool has_kept = false;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) has_kept |= (plan.kept[k] - t0) < kK2Tile;
+
+  double2 v[kK2Items];
+#pragma unroll
+  for (int it = 0; it < kK2Items; ++it) {
+    const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
+    v[it] = j < n ? ld_stream(pts + j) : make_double2(0.0, 0.0);
+  }
+  std::uint32_t lab[kK2Items];
+  std::uint32_t any = 0;
+#pragma unroll
+  for (int it = 0; it < kK2Items; ++it) {
+    const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
+    lab[it] = j < n ? classify(plan, v[it], j, has_kept) : 0u;
+    any |= lab[it];
+    if (labels != nullptr && j < n) labels[j] = static_cast<std::uint8_t>(lab[it]);
+  }
+
+  const bool last = tile == ntiles - 1;
+  if (!__syncthreads_or(any != 0)) {
+    // nothing survives here: publish a zero aggregate (a prefix for tile 0)
+    if (threadIdx.x < 4)
+      st_relaxed(status + threadIdx.x * ntiles + tile, tile == 0 ? kFlagP : kFlagA);
+    if (!last) return;
+    // the final tile always resolves its prefix: it reports the counts
+    if (tile == 0) {
+      if (threadIdx.x < 4) counts[threadIdx.x] = 0;
+      return;
+    }
+    if (warp < 4) {
+      const std::uint64_t excl = look_back(status + warp * ntiles, tile);
+      if (lane == 0) counts[warp] = excl;
+    }
+    return;
+  }
+
+  // per (item, warp, quadrant) survivor counts
+#pragma unroll
+  for (int it = 0; it < kK2Items; ++it) {
+    const unsigned live = __ballot_sync(kFull, lab[it] != 0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const unsigned mq = live ? __ballot_sync(kFull, lab[it] == unsigned(q + 1)) : 0u;
+      if (lane == 0) s_off[q][it * W + warp] = __popc(mq);
+    }
+  }
+  __syncthreads();
+  // exclusive scan of each quadrant's SEG counts by warp q
+  if (warp < 4) {
+    constexpr int PER = SEG / 32;
+    std::uint32_t c[PER];
+    std::uint32_t sum = 0;
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      c[r] = s_off[warp][lane * PER + r];
+      sum += c[r];
+    }
+    std::uint32_t incl = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const std::uint32_t o = __shfl_up_sync(kFull, incl, off);
+      if (lane >= off) incl += o;
+    }
+    std::uint32_t run = incl - sum;
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      s_off[warp][lane * PER + r] = run;
+      run += c[r];
+    }
+    const std::uint32_t agg = __shfl_sync(kFull, incl, 31);
+    std::uint64_t excl = 0;
+    if (tile == 0) {
+      if (lane == 0) st_relaxed(status + warp * ntiles, kFlagP | agg);
+    } else {
+      if (lane == 0) st_relaxed(status + warp * ntiles + tile, kFlagA | agg);
+      excl = look_back(status + warp * ntiles, tile);
+      if (lane == 0) st_relaxed(status + warp * ntiles + tile, kFlagP | (excl + agg));
+    }
+    if (lane == 0) {
+      s_excl[warp] = excl;
+      s_agg[warp] = agg;
+      if (last) counts[warp] = excl + agg;
+    }
+  }
+  __syncthreads();
+
+  // scatter survivors in index order: (item, warp, lane)
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int it = 0; it < kK2Items; ++it) {
+    const unsigned live = __ballot_sync(kFull, lab[it] != 0);
+    if (!live) continue;
+    const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const unsigned mq = __ballot_sync(kFull, lab[it] == unsigned(q + 1));
+      if (lab[it] == unsigned(q + 1)) {
+        const std::uint64_t pos = s_excl[q] + s_off[q][it * W + warp] + __popc(mq & lt);
+        if (pos < cap) queues[std::uint64_t(q) * cap + pos] = static_cast<IdxT>(j);
+      }
+    }
+  }
+}
+
+template <typename IdxT>
+__global__ void gather_xy(const double2* __restrict__ pts,
+                          const IdxT* __restrict__ idx, std::uint64_t count,
+                          double2* __restrict__ out) {
+  for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+       k < count; k += std::uint64_t(gridDim.x) * blockDim.x)
+    out[k] = pts[idx[k]];
+}
+
+}  // namespace
+
+// ============================================================ launchers ==
+int k1_grid(int device, std::uint64_t n) {
+  int sms = 0, per_sm = 0;
+  check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device),
+             "cudaDeviceGetAttribute");
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_extremes,
+                                                           kK1Block, 0),
+             "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  if (per_sm < 1) per_sm = 1;
+  const std::uint64_t full = std::uint64_t(sms) * per_sm;
+  const std::uint64_t need = (n + kK1Block * kK1Unroll - 1) / (kK1Block * kK1Unroll);
+  return static_cast<int>(need < full ? (need > 0 ? need : 1) : full);
+}
+
+void launch_k1(const double* d_xy, std::uint64_t n, std::uint64_t base,
+               K1Partial* partials, int grid, unsigned* ticket,
+               ohx_extremes_rec* d_out, cudaStream_t stream) {
+  k1_extremes<<<grid, kK1Block, 0, stream>>>(reinterpret_cast<const double2*>(d_xy),
+                                              n, base, partials, ticket, d_out);
+  check_cuda(cudaGetLastError(), "k1_extremes launch");
+}
+
+void launch_k1b(const double* d_xy, std::uint64_t n, std::uint64_t base,
+                const double bbox[4], K1Partial* partials, int grid,
+                unsigned* ticket, ohx_corner_rec* d_out, cudaStream_t stream) {
+  k1b_corners<<<grid, kK1Block, 0, stream>>>(
+      reinterpret_cast<const double2*>(d_xy), n, base, bbox[0], bbox[1], bbox[2],
+      bbox[3], partials, ticket, d_out);
+  check_cuda(cudaGetLastError(), "k1b_corners launch");
+}
+
+void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan,
+               std::uint64_t* d_status, std::uint64_t ntiles, void* d_queues,
+               int idx_bytes, std::uint64_t cap, std::uint8_t* d_labels,
+               unsigned long long* d_counts, cudaStream_t stream) {
+  // the tile counter lives right after the 4*ntiles status words, so one
+  // memset re-arms both (the allocation holds k2_status_bytes(ntiles))
+  auto* d_tile_counter = reinterpret_cast<unsigned*>(d_status + 4 * ntiles);
+  check_cuda(cudaMemsetAsync(d_status, 0, k2_status_bytes(ntiles), stream),
+             "cudaMemsetAsync(status)");
+  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  if (idx_bytes == 4) {
+    k2_filter<std::uint32_t><<<static_cast<unsigned>(ntiles), kK2Block, 0, stream>>>(
+        pts, n, plan, d_status, ntiles, d_tile_counter,
+        static_cast<std::uint32_t*>(d_queues), cap, d_labels, d_counts);
+  } else {
+    k2_filter<std::uint64_t><<<static_cast<unsigned>(ntiles), kK2Block, 0, stream>>>(
+        pts, n, plan, d_status, ntiles, d_tile_counter,
+        static_cast<std::uint64_t*>(d_queues), cap, d_labels, d_counts);
+  }
+  check_cuda(cudaGetLastError(), "k2_filter launch");
+}
+
+void launch_gather(const double* d_xy, const void* d_idx, int idx_bytes,
+                   std::uint64_t count, double* d_out, cudaStream_t stream) {
+  if (count == 0) return;
+  const unsigned grid = static_cast<unsigned>(count < 148ull * 2048 ? (count + 255) / 256 : 148 * 8);
+  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  if (idx_bytes == 4)
+    gather_xy<<<grid, 256, 0, stream>>>(pts, static_cast<const std::uint32_t*>(d_idx), count,
+                                        reinterpret_cast<double2*>(d_out));
+  else
+    gather_xy<<<grid, 256, 0, stream>>>(pts, static_cast<const std::uint64_t*>(d_idx), count,
+                                        reinterpret_cast<double2*>(d_out));
+  check_cuda(cudaGetLastError(), "gather_xy launch");
+}
+
+}  // namespace ohx

@@ -1,0 +1,177 @@
+// pipeline.cpp -- pipeline-level C ABI (include/ohx.h): the entry points the
+// reference binds to Python (python/module.cpp:40-108), each a thin
+// exception-safe wrapper over the C++ API of octohull_api.cpp, plus the
+// device-resident variant used for the kernel-level throughput numbers.
+#include <chrono>
+#include <cstring>
+#include <span>
+#include <string>
+
+#include "internal.hpp"
+#include "octohull/filter.hpp"
+#include "octohull/hull.hpp"
+#include "octohull/pointgen.hpp"
+#include "ohx.h"
+#include "pipeline.hpp"
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+double ms(Clock::time_point a, Clock::time_point b) {
+  return std::chrono::duration<double, std::milli>(b - a).count();
+}
+
+std::span<const octohull::Point2D> pts_of(const double* xy, std::uint64_t n) {
+  return {reinterpret_cast<const octohull::Point2D*>(xy), static_cast<std::size_t>(n)};
+}
+
+void copy_hull(const std::vector<octohull::Point2D>& v, double* out, std::uint64_t cap,
+               std::uint64_t* h) {
+  *h = v.size();
+  if (v.size() > cap) throw std::invalid_argument("hull output capacity too small");
+  std::memcpy(out, v.data(), v.size() * sizeof(octohull::Point2D));
+}
+
+}  // namespace
+
+using ohx::guard;
+
+extern "C" {
+
+int ohx_heaphull(const double* h_xy, uint64_t n, double* h_hull, uint64_t cap, uint64_t* h,
+                 double* timings) {
+  return guard([&] {
+    const auto t0 = Clock::now();
+    octohull::ReduceEngine engine;
+    const octohull::HullPolygon hull = octohull::heaphull(pts_of(h_xy, n), engine);
+    copy_hull(hull.vertices, h_hull, cap, h);
+    if (timings) {
+      timings[0] = timings[1] = timings[3] = 0.0;
+      timings[2] = ms(t0, Clock::now());
+    }
+  });
+}
+
+int ohx_heaphull_device(ohx_ctx* ctx, const double* d_xy, uint64_t n, double* h_hull,
+                        uint64_t cap, uint64_t* h, double* timings) {
+  return guard([&] {
+    if (n == 0) throw std::invalid_argument("heaphull: empty point set");
+    std::lock_guard<std::mutex> g(ohx::ctx_mutex(ctx));
+    ohx::ctx_bind(ctx);
+    cudaStream_t s = ohx::ctx_stream(ctx);
+    const auto t0 = Clock::now();
+    const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
+    const auto t1 = Clock::now();
+    std::vector<ohx::P2> q[4];
+    const ohx::P2* qp[4];
+    for (int k = 0; k < 4; ++k) {
+      q[k].resize(f.counts[k]);
+      ohx::queue_fetch(ctx, k + 1, nullptr, reinterpret_cast<double*>(q[k].data()),
+                       f.counts[k], s);
+      qp[k] = q[k].data();
+    }
+    const ohx::P2 anchors[4] = {{f.ext.x[OHX_EAST], f.ext.y[OHX_EAST]},
+                                {f.ext.x[OHX_NORTH], f.ext.y[OHX_NORTH]},
+                                {f.ext.x[OHX_WEST], f.ext.y[OHX_WEST]},
+                                {f.ext.x[OHX_SOUTH], f.ext.y[OHX_SOUTH]}};
+    const std::vector<ohx::P2> cyc = ohx::hull_from_queue_points(anchors, qp, f.counts);
+    *h = cyc.size();
+    if (cyc.size() > cap) throw std::invalid_argument("hull output capacity too small");
+    std::memcpy(h_hull, cyc.data(), cyc.size() * sizeof(ohx::P2));
+    const auto t2 = Clock::now();
+    if (timings) {
+      timings[0] = ms(t0, t1);
+      timings[1] = ms(t1, t2);
+      timings[2] = ms(t0, t2);
+      timings[3] = 0.0;
+    }
+  });
+}
+
+int ohx_classify(const double* h_xy, uint64_t n, uint8_t* h_labels) {
+  return guard([&] {
+    octohull::ReduceEngine engine;
+    const auto pts = pts_of(h_xy, n);
+    const octohull::ExtremeSet ext = octohull::find_extremes(pts, engine);
+    const octohull::Octagon oct = octohull::build_octagon(pts, ext);
+    const octohull::LabelArray l = octohull::classify_points(pts, oct, ext, engine);
+    std::memcpy(h_labels, l.data(), l.size());
+  });
+}
+
+int ohx_heaphull_run(const double* h_xy, uint64_t n, double* h_hull, uint64_t cap,
+                     uint64_t* h, uint8_t* h_labels, double* timings) {
+  return guard([&] {
+    octohull::ReduceEngine engine;
+    const octohull::HeaphullRun run = octohull::heaphull_run(pts_of(h_xy, n), engine);
+    copy_hull(run.hull.vertices, h_hull, cap, h);
+    if (h_labels) std::memcpy(h_labels, run.labels.data(), run.labels.size());
+    if (timings) {
+      timings[0] = run.filter_ms;
+      timings[1] = run.hull_ms;
+      timings[2] = run.total_ms;
+      timings[3] = 0.0;
+    }
+  });
+}
+
+int ohx_find_extremes(const double* h_xy, uint64_t n, uint64_t ext[8]) {
+  return guard([&] {
+    octohull::ReduceEngine engine;
+    const octohull::ExtremeSet e = octohull::find_extremes(pts_of(h_xy, n), engine);
+    const uint64_t v[8] = {e.axis.east, e.axis.north, e.axis.west, e.axis.south,
+                           e.corner.ne, e.corner.nw,  e.corner.sw, e.corner.se};
+    std::memcpy(ext, v, sizeof(v));
+  });
+}
+
+int ohx_monotone_chain(const double* h_xy, uint64_t n, double* h_hull, uint64_t cap,
+                       uint64_t* h) {
+  return guard([&] {
+    const octohull::HullPolygon hull = octohull::monotone_chain_hull(pts_of(h_xy, n));
+    copy_hull(hull.vertices, h_hull, cap, h);
+  });
+}
+
+int ohx_generate(int dist, uint64_t n, uint64_t seed, double distort_pct, double* h_xy,
+                 int threads) {
+  return guard([&] { ohx::generate_points(dist, n, seed, distort_pct, h_xy, threads); });
+}
+
+int ohx_hull_from_queues(const double* h_xy, const uint64_t ext_axis[4],
+                         const uint64_t* const q_idx[4], const uint64_t q_len[4],
+                         double* h_hull, uint64_t cap, uint64_t* h) {
+  return guard([&] {
+    const auto* P = reinterpret_cast<const ohx::P2*>(h_xy);
+    std::vector<ohx::P2> q[4];
+    const ohx::P2* qp[4];
+    for (int k = 0; k < 4; ++k) {
+      q[k].resize(q_len[k]);
+      for (uint64_t i = 0; i < q_len[k]; ++i) q[k][i] = P[q_idx[k][i]];
+      qp[k] = q[k].data();
+    }
+    const ohx::P2 anchors[4] = {P[ext_axis[0]], P[ext_axis[1]], P[ext_axis[2]],
+                                P[ext_axis[3]]};
+    const std::vector<ohx::P2> cyc = ohx::hull_from_queue_points(anchors, qp, q_len);
+    *h = cyc.size();
+    if (cyc.size() > cap) throw std::invalid_argument("hull output capacity too small");
+    std::memcpy(h_hull, cyc.data(), cyc.size() * sizeof(ohx::P2));
+  });
+}
+
+int ohx_hull_from_queue_points(const double anchors_xy[8], const double* const q_xy[4],
+                               const uint64_t q_len[4], double* h_hull, uint64_t cap,
+                               uint64_t* h) {
+  return guard([&] {
+    const ohx::P2* qp[4];
+    for (int k = 0; k < 4; ++k) qp[k] = reinterpret_cast<const ohx::P2*>(q_xy[k]);
+    const auto* A = reinterpret_cast<const ohx::P2*>(anchors_xy);
+    const std::vector<ohx::P2> cyc = ohx::hull_from_queue_points(A, qp, q_len);
+    *h = cyc.size();
+    if (cyc.size() > cap) throw std::invalid_argument("hull output capacity too small");
+    std::memcpy(h_hull, cyc.data(), cyc.size() * sizeof(ohx::P2));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// pipeline.hpp -- internal orchestration shared by the pipeline-level C ABI
+// (pipeline.cpp) and the C++ API (octohull_api.cpp).  Functions throw
+// std::invalid_argument for contract violations and ohx::Error otherwise;
+// callers hold ctx_mutex(ctx) and have bound the context's device.
+#pragma once
+
+#include <cstdint>
+#include <mutex>
+
+#include "internal.hpp"
+#include "ohx.h"
+
+namespace ohx {
+
+struct FilterOut {
+  ohx_extreme_set ext;  // resolved ExtremeSet (+ coordinates)
+  double oct[16];       // octagon (build_octagon) ...
+  int m;                // ... and its vertex count
+  ohx_filter_plan plan;
+  std::uint64_t counts[4];
+  bool corner_pass;  // the certificate failed and K1b ran
+};
+
+ohx_ctx* create_ctx(int device);
+void destroy_ctx(ohx_ctx* c);
+ohx_ctx* default_ctx(int device = -1);
+cudaStream_t ctx_stream(ohx_ctx* c);
+std::mutex& ctx_mutex(ohx_ctx* c);
+void ctx_bind(ohx_ctx* c);
+
+const double* stage_points(ohx_ctx* c, const double* h_xy, std::uint64_t n,
+                           cudaStream_t s);
+std::uint8_t* stage_labels(ohx_ctx* c, std::uint64_t n);
+
+void extremes(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+              ohx_extremes_rec* out, cudaStream_t s);
+void corners_exact(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                   std::uint64_t base, const double bbox[4], ohx_corner_rec* out,
+                   cudaStream_t s);
+void combine_extremes(const ohx_extremes_rec* recs, int k, ohx_extremes_rec* out);
+void combine_corners(const ohx_corner_rec* recs, int k, ohx_corner_rec* out);
+std::uint32_t resolve_extremes(const ohx_extremes_rec& r, ohx_extreme_set* out);
+void apply_corners(const ohx_corner_rec& c, ohx_extreme_set* ext);
+int build_octagon(const double cand[16], double oct[16]);
+void make_plan(const ohx_extreme_set& e, const double* oct, int m,
+               ohx_filter_plan* p);
+void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+            const ohx_filter_plan& plan, std::uint8_t* d_labels,
+            std::uint64_t counts[4], cudaStream_t s);
+void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
+                 std::uint64_t cap, cudaStream_t s);
+
+// K1 -> certificate -> (K1b) -> octagon -> plan -> K2 on one device
+FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                        std::uint8_t* d_labels, cudaStream_t s);
+
+}  // namespace ohx

@@ -1,0 +1,203 @@
+"""Parity of the sm_100a path against the oracle and the reference's golden
+fixtures, through the C ABI (ctypes).  Bit-exact everywhere: extreme
+indices, labels, the four queues in order, hull coordinates."""
+
+import numpy as np
+import pytest
+
+import paper_2209_12310_b200 as P
+from paper_2209_12310_b200 import _lib
+from conftest import sha
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    c = P.Context(0)
+    yield c
+    c.close()
+
+
+def dev(pts):
+    return torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+
+
+def ext_set(pts, ext):
+    s = _lib.ExtremeSet()
+    for k, j in enumerate(ext):
+        s.ext[k], s.x[k], s.y[k] = int(j), pts[int(j), 0], pts[int(j), 1]
+    return s
+
+
+def run_kernels(ctx, pts, oracle, base=0):
+    """K1 -> certificate -> K1b -> octagon -> K2 through the kernel-level ABI."""
+    d = dev(pts)
+    n = len(pts)
+    rec = ctx.extremes(d, n, base)
+    ext, mask = P.resolve_extremes(rec)
+    if mask:
+        bbox = (rec.x[0], rec.y[1], rec.x[2], rec.y[3])
+        ext = P.apply_corners(ext, ctx.corners_exact(d, n, bbox, base))
+    octg = P.build_octagon_from_set(ext)
+    plan = P.make_plan(ext, octg)
+    labels = torch.empty(n, dtype=torch.uint8, device="cuda")
+    counts = ctx.filter(d, n, plan, base, d_labels=labels)
+    queues = [ctx.queue(q + 1, counts[q])[0] for q in range(4)]
+    return rec, ext, mask, octg, labels.cpu().numpy(), counts, queues
+
+
+# ------------------------------------------------------------- golden ----
+@pytest.mark.parametrize("k", range(23))
+def test_api_matches_reference_golden(golden, k):
+    c = golden["cases"][k]
+    pts = P.generate(c["dist"], c["n"], c["seed"], c["distort"])
+    assert sha(pts) == c["points_sha256"]
+    assert [int(v) for v in P.find_extremes(pts)] == c["ext"]
+    hull, labels, t = P.heaphull_run(pts)
+    assert [int((labels == v).sum()) for v in range(5)] == c["label_hist"]
+    assert sha(labels) == c["labels_sha256"]
+    assert len(hull) == c["h"] and sha(hull) == c["hull_sha256"]
+    if "hull" in c:
+        assert hull.tolist() == c["hull"]
+    assert np.array_equal(P.heaphull(pts), hull)
+    assert np.array_equal(P.classify(pts), labels)
+    assert P.filter_rate(labels) == c["filter_rate"]
+
+
+@pytest.mark.parametrize("k", range(23))
+def test_kernels_match_oracle(ctx, oracle, golden, k):
+    c = golden["cases"][k]
+    pts = P.generate(c["dist"], c["n"], c["seed"], c["distort"])
+    rec, ext, mask, octg, labels, counts, queues = run_kernels(ctx, pts, oracle)
+    # K1 axis slots and diagonal winners/seconds against a host scan
+    x, y = pts[:, 0], pts[:, 1]
+    keys = [x, y, -x, -y, x + y, y - x, -(x + y), x - y]
+    for a, kk in enumerate(keys):
+        j = int(np.flatnonzero(kk == kk.max())[0])
+        assert rec.idx[a] == j and rec.x[a] == x[j] and rec.y[a] == y[j]
+        if a >= 4:
+            rest = np.delete(kk, j)
+            assert rec.second[a - 4] == (rest.max() if rest.size else -np.inf)
+    assert [int(v) for v in ext.ext] == c["ext"]
+    assert octg.tolist() == c["octagon"]
+    assert sha(labels) == c["labels_sha256"]
+    assert counts == c["queue_len"]
+    assert sha(np.concatenate(queues)) == c["queues_sha256"]
+    assert np.array_equal(labels, oracle.classify(pts))
+
+
+def test_degenerate_grids_match_reference(grid_trials):
+    # test_hull.cpp:223-249, 5000 tiny integer grids: ties, duplicates, lines
+    for t in grid_trials:
+        a = np.array(t["pts"], dtype=float)
+        assert [int(v) for v in P.find_extremes(a)] == t["ext"]
+        hull, labels, _ = P.heaphull_run(a)
+        assert labels.tolist() == t["labels"]
+        assert hull.tolist() == t["hull"]
+
+
+def test_exact_corner_kernel_matches_oracle(ctx, oracle):
+    rng = np.random.default_rng(11)
+    for n in (1, 5, 1000, 70001):
+        pts = (rng.integers(-5, 6, size=(n, 2)) / 4.0).astype(float)
+        axis = oracle.find_extremes(pts)[:4]
+        bbox = (pts[axis[0], 0], pts[axis[1], 1], pts[axis[2], 0], pts[axis[3], 1])
+        crec = ctx.corners_exact(dev(pts), n, bbox)
+        assert [int(v) for v in crec.idx] == [int(v) for v in oracle.corner_extremes(pts, axis)]
+
+
+# ---------------------------------------------------- shapes and tiles ----
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 32, 33, 255, 256, 2047, 2048, 2049,
+                               4095, 4096, 4097, 3 * 2048 + 5, 65537, 300007])
+def test_tile_boundaries_ragged_sizes(ctx, oracle, n):
+    rng = np.random.default_rng(n)
+    # coarse grid: heavy ties, duplicates, collinear runs, and plenty of survivors
+    pts = (rng.integers(-40, 41, size=(n, 2)) / 8.0).astype(float)
+    rec, ext, mask, octg, labels, counts, queues = run_kernels(ctx, pts, oracle)
+    assert np.array_equal(ext.ext, oracle.find_extremes(pts))
+    want = oracle.classify(pts)
+    assert np.array_equal(labels, want)
+    for q in range(4):
+        assert np.array_equal(queues[q], np.flatnonzero(want == q + 1))
+    hull = P.heaphull(pts)
+    assert np.array_equal(hull, oracle.heaphull(pts))
+
+
+def test_all_points_survive_circle(ctx, oracle):
+    pts = P.generate("circle", 500000, 21)
+    rec, ext, mask, octg, labels, counts, queues = run_kernels(ctx, pts, oracle)
+    want = oracle.classify(pts)
+    assert np.array_equal(labels, want)
+    assert sum(counts) == int((want != 0).sum()) and sum(counts) > 0.99 * len(pts)
+    assert np.array_equal(P.heaphull(pts), oracle.heaphull(pts))
+
+
+def test_degenerate_octagon_filters_nothing(ctx, oracle):
+    # collinear input: octagon has 2 vertices, every point goes to a queue
+    n = 10000
+    t = np.linspace(-1, 1, n)
+    pts = np.stack([t, 0.5 * t], axis=1)
+    rec, ext, mask, octg, labels, counts, queues = run_kernels(ctx, pts, oracle)
+    assert len(octg) < 3
+    assert np.array_equal(labels, oracle.classify(pts))
+    assert (labels != 0).all()
+
+
+# ------------------------------------------------------------ sharding ----
+@pytest.mark.parametrize("shards", [2, 3, 7])
+def test_shard_records_combine_to_whole(ctx, oracle, shards):
+    pts = P.generate("disk", 200001, 17)
+    n = len(pts)
+    bounds = np.linspace(0, n, shards + 1).astype(int)
+    recs = [ctx.extremes(dev(pts[b0:b1]), b1 - b0, b0) for b0, b1 in zip(bounds[:-1], bounds[1:])]
+    whole = ctx.extremes(dev(pts), n)
+    g = P.combine_extremes(recs)
+    assert list(g.idx) == list(whole.idx) and list(g.second) == list(whole.second)
+    ext, mask = P.resolve_extremes(g)
+    if mask:
+        bbox = (g.x[0], g.y[1], g.x[2], g.y[3])
+        crecs = [ctx.corners_exact(dev(pts[b0:b1]), b1 - b0, bbox, b0)
+                 for b0, b1 in zip(bounds[:-1], bounds[1:])]
+        ext = P.apply_corners(ext, P.combine_corners(crecs))
+    assert np.array_equal(ext.ext, oracle.find_extremes(pts))
+    plan = P.make_plan(ext, P.build_octagon_from_set(ext))
+    want = oracle.classify(pts)
+    for b0, b1 in zip(bounds[:-1], bounds[1:]):
+        counts = ctx.filter(dev(pts[b0:b1]), b1 - b0, plan, b0)
+        for q in range(4):
+            got = ctx.queue(q + 1, counts[q])[0]
+            assert np.array_equal(got, b0 + np.flatnonzero(want[b0:b1] == q + 1))
+
+
+# ---------------------------------------------------------- large sizes ----
+def test_normal_1e8_matches_oracle(ctx, oracle):
+    pts = P.generate("normal", 100_000_000, 7)
+    d = dev(pts)
+    rec = ctx.extremes(d, len(pts))
+    ext, mask = P.resolve_extremes(rec)
+    assert mask == 0  # certified on the normal corpus
+    want_ext = oracle.find_extremes(pts)
+    assert np.array_equal(ext.ext, want_ext)
+    octg = P.build_octagon_from_set(ext)
+    plan = P.make_plan(ext, octg)
+    counts = ctx.filter(d, len(pts), plan)
+    want = oracle.classify(pts, want_ext, octg)
+    nz = np.flatnonzero(want)
+    assert sum(counts) == len(nz)
+    for q in range(4):
+        got = ctx.queue(q + 1, counts[q])[0]
+        assert np.array_equal(got, nz[want[nz] == q + 1])
+    hull, _ = ctx.heaphull_device(d, len(pts))
+    del d
+    assert np.array_equal(hull, oracle.heaphull(pts))
+
+
+def test_launch_counter_proves_native_path(ctx):
+    before = ctx.launches
+    pts = P.generate("square", 10000, 3)
+    run_kernels(ctx, pts, None)
+    assert ctx.launches >= before + 2

@@ -1,0 +1,262 @@
+"""CPU-side tests of the product library (no GPU needed): the C ABI loads and
+exports everything include/ohx.h declares, the host stages between and after
+the kernels (generator, extremes combine + corner certificate, build_octagon,
+the K2 plan and its certified box, the host hull) match the oracle, and the
+device entry points fail loudly when there is no GPU."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2209_12310_b200 as P
+from paper_2209_12310_b200 import _lib
+from conftest import ROOT, sha
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "ohx.h")).read()
+    return sorted(set(re.findall(r"\b(ohx_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r" T (ohx_\w+)", out))
+    declared = declared_symbols()
+    assert len(declared) >= 25
+    missing = [s for s in declared if s not in exported]
+    assert not missing, missing
+    # and the ctypes stub binds every one of them
+    bound = {name for name, _, _ in _lib.PROTOTYPES}
+    assert set(declared) <= bound
+    assert P.lib.ohx_abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+@pytest.mark.parametrize("dist,n,seed,d", [
+    ("normal", 1, 0, 0.0), ("normal", 300001, 9, 0.0), ("square", 262145, 4, 0.0),
+    ("disk", 300000, 5, 0.0), ("circle", 300000, 6, 3.5), ("circle", 70000, 6, 0.0)])
+def test_generator_bit_exact(oracle, dist, n, seed, d):
+    a = P.generate(dist, n, seed, d)
+    assert np.array_equal(a, oracle.generate(dist, n, seed, d))
+    assert np.array_equal(a, P.generate(dist, n, seed, d, threads=3))
+
+
+def test_generator_errors():
+    with pytest.raises(ValueError):
+        P.generate("triangle", 10)
+    with pytest.raises(ValueError):
+        P.generate("normal", 10, distort=2.0)
+    with pytest.raises(ValueError):
+        P.generate("circle", 10, distort=-1.0)
+    with pytest.raises(ValueError):
+        P.generate("normal", 0)
+
+
+def test_monotone_chain_matches_oracle(oracle, golden):
+    for c in golden["cases"][:12]:
+        pts = oracle.generate(c["dist"], c["n"], c["seed"], c["distort"])
+        assert np.array_equal(P.monotone_chain(pts), oracle.monotone_chain(pts))
+
+
+# ---------------------------------------------------------------- host hull
+def hull_via_library(oracle, pts):
+    """Oracle labels -> queues -> the product's host hull stage."""
+    ext = oracle.find_extremes(pts)
+    lab = oracle.classify(pts)
+    anchors = pts[ext[:4].astype(np.int64)]
+    queues = [pts[np.flatnonzero(lab == q)] for q in (1, 2, 3, 4)]
+    return P.hull_from_queue_points(anchors, queues)
+
+
+def test_host_hull_matches_oracle_on_golden(oracle, golden):
+    for c in golden["cases"]:
+        pts = oracle.generate(c["dist"], c["n"], c["seed"], c["distort"])
+        hull = hull_via_library(oracle, pts)
+        assert len(hull) == c["h"] and sha(hull) == c["hull_sha256"], c
+
+
+def test_host_hull_matches_oracle_on_degenerate_grids(oracle, grid_trials):
+    for t in grid_trials:
+        a = np.array(t["pts"], dtype=float)
+        assert hull_via_library(oracle, a).tolist() == t["hull"]
+
+
+# ------------------------------------------------- extremes combine + cert
+def emulate_k1(pts, base=0):
+    """Reference-semantics emulation of one shard's K1 record (test-side):
+    argmax of the 8 maximised keys, smallest index on ties, plus the second
+    largest diagonal key."""
+    x, y = pts[:, 0], pts[:, 1]
+    t = x + y
+    d = x - y
+    keys = [x, y, -x, -y, t, -d, -t, d]
+    rec = _lib.ExtremesRec()
+    for a, k in enumerate(keys):
+        j = int(np.flatnonzero(k == k.max())[0])
+        rec.key[a] = k[j]
+        rec.idx[a] = base + j
+        rec.x[a] = x[j]
+        rec.y[a] = y[j]
+        if a >= 4:
+            rest = np.delete(k, j)
+            rec.second[a - 4] = rest.max() if rest.size else -np.inf
+    rec.n = len(pts)
+    return rec
+
+
+def emulate_corners(pts, bbox, base=0):
+    xmax, ymax, xmin, ymin = bbox
+    rec = _lib.CornerRec()
+    for a, (cx, cy) in enumerate([(xmax, ymax), (xmin, ymax), (xmin, ymin), (xmax, ymin)]):
+        m = np.abs(pts[:, 0] - cx) + np.abs(pts[:, 1] - cy)
+        j = int(np.flatnonzero(m == m.min())[0])
+        rec.key[a], rec.idx[a], rec.x[a], rec.y[a] = m[j], base + j, pts[j, 0], pts[j, 1]
+    rec.n = len(pts)
+    return rec
+
+
+def resolve_like_pipeline(pts, shards):
+    """Shard -> K1 records -> combine -> certificate -> (exact corners)."""
+    bounds = np.linspace(0, len(pts), shards + 1).astype(int)
+    recs = [emulate_k1(pts[b0:b1], b0) for b0, b1 in zip(bounds[:-1], bounds[1:]) if b1 > b0]
+    g = P.combine_extremes(recs)
+    ext, mask = P.resolve_extremes(g)
+    if mask:
+        bbox = (g.x[0], g.y[1], g.x[2], g.y[3])
+        crecs = [emulate_corners(pts[b0:b1], bbox, b0)
+                 for b0, b1 in zip(bounds[:-1], bounds[1:]) if b1 > b0]
+        ext = P.apply_corners(ext, P.combine_corners(crecs))
+    return [int(v) for v in ext.ext], mask
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3, 8])
+def test_certificate_and_combine_match_reference_extremes(oracle, golden, shards):
+    for c in golden["cases"]:
+        if c["n"] > 300000:
+            continue
+        pts = oracle.generate(c["dist"], c["n"], c["seed"], c["distort"])
+        got, _ = resolve_like_pipeline(pts, shards)
+        assert got == c["ext"], c
+
+
+def test_certificate_on_degenerate_grids(grid_trials):
+    uncertified = 0
+    for t in grid_trials[:2000]:
+        a = np.array(t["pts"], dtype=float)
+        got, mask = resolve_like_pipeline(a, 1 + len(a) % 3)
+        uncertified += mask != 0
+        assert got == t["ext"]
+    assert uncertified > 0  # ties on grids must exercise the exact fallback
+
+
+def test_certificate_never_certifies_a_wrong_corner(oracle):
+    # adversarial near-ties: points on a line x + y = const, perturbed by ulps
+    rng = np.random.default_rng(1)
+    for trial in range(200):
+        n = 50
+        base = rng.uniform(-1e3, 1e3)
+        x = rng.uniform(-1, 1, n) * 10.0 ** rng.integers(-3, 4)
+        y = base - x
+        y = y + rng.integers(-3, 4, n) * np.spacing(np.abs(y) + 1e-300)
+        pts = np.stack([x, y], axis=1)
+        ext, mask = resolve_like_pipeline(pts, 1)
+        assert ext == [int(v) for v in oracle.find_extremes(pts)]
+
+
+# ----------------------------------------------------- octagon and K2 plan
+def test_build_octagon_matches_oracle(oracle, golden, grid_trials):
+    for c in golden["cases"]:
+        pts = oracle.generate(c["dist"], c["n"], c["seed"], c["distort"])
+        rec = emulate_k1(pts)
+        ext, _ = P.resolve_extremes(rec)
+        for k in range(8):  # use the reference's extremes
+            j = c["ext"][k]
+            ext.ext[k], ext.x[k], ext.y[k] = j, pts[j, 0], pts[j, 1]
+        assert P.build_octagon_from_set(ext).tolist() == c["octagon"]
+    for t in grid_trials[:500]:
+        a = np.array(t["pts"], dtype=float)
+        ext = _lib.ExtremeSet()
+        for k, j in enumerate(t["ext"]):
+            ext.ext[k], ext.x[k], ext.y[k] = j, a[j, 0], a[j, 1]
+        e = np.array(t["ext"], dtype=np.uint64)
+        assert np.array_equal(P.build_octagon_from_set(ext), oracle.build_octagon(a, e))
+
+
+def orientation(a, b, c):
+    det = (b[0] - a[0]) * (c[1] - a[1]) - (b[1] - a[1]) * (c[0] - a[0])
+    return int(det > 0) - int(det < 0)
+
+
+def test_certified_box_is_strictly_inside(oracle):
+    rng = np.random.default_rng(3)
+    for dist, n, seed, d in [("normal", 100000, 7, 0.0), ("square", 100000, 7, 0.0),
+                             ("disk", 100000, 7, 0.0), ("circle", 20000, 7, 5.0)]:
+        pts = oracle.generate(dist, n, seed, d)
+        e = oracle.find_extremes(pts)
+        octg = oracle.build_octagon(pts, e)
+        ext = _lib.ExtremeSet()
+        for k, j in enumerate(e):
+            ext.ext[k], ext.x[k], ext.y[k] = int(j), pts[j, 0], pts[j, 1]
+        plan = P.make_plan(ext, octg)
+        x0, x1, y0, y1 = plan.box
+        assert x0 < x1 and y0 < y1, dist
+        # corners, edges of the box and random interior points: every
+        # reference orientation strictly positive
+        xs = np.concatenate([[x0, x1], rng.uniform(x0, x1, 300)])
+        ys = np.concatenate([[y0, y1], rng.uniform(y0, y1, 300)])
+        m = len(octg)
+        for px in xs[:40]:
+            for py in ys[:40]:
+                for i in range(m):
+                    assert orientation(octg[i], octg[(i + 1) % m], (px, py)) == 1
+        # plan edge constants are the reference's (b - a) differences
+        for i in range(m):
+            b = octg[(i + 1) % m]
+            assert plan.ea[i] == b[0] - octg[i][0] and plan.ec[i] == b[1] - octg[i][1]
+        # coverage: the box must catch most interior points of these corpora
+        inside = ((pts[:, 0] >= x0) & (pts[:, 0] <= x1) & (pts[:, 1] >= y0) & (pts[:, 1] <= y1))
+        floor = {"normal": 0.99, "square": 0.9, "disk": 0.6}.get(dist, 0.0)
+        assert inside.mean() > floor, (dist, inside.mean())
+
+
+def test_device_entry_points_fail_loudly_without_gpu():
+    if P.device_count() if _has_driver() else 0:
+        pytest.skip("a GPU is visible")
+    pts = P.generate("normal", 100, 1)
+    with pytest.raises(RuntimeError):
+        P.heaphull(pts)
+    with pytest.raises(RuntimeError):
+        P.classify(pts)
+    with pytest.raises(RuntimeError):
+        P.Context(0)
+
+
+def _has_driver():
+    try:
+        P.device_count()
+        return True
+    except RuntimeError:
+        return False
+
+
+def test_bad_input_raises_value_error():
+    # tests/python/test_smoke.py:54-60
+    with pytest.raises(ValueError):
+        P.heaphull(np.zeros((3, 3)))
+    with pytest.raises(ValueError):
+        P.heaphull(np.array([[0.0, np.nan]]))
+    with pytest.raises(ValueError):
+        P.heaphull(np.zeros((0, 2)))
+    with pytest.raises(ValueError):
+        P.classify(np.zeros((4, 2)), threads=0)
