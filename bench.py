@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 heaphull filter (arXiv 2209.12310).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
+    (N > 1: launched by torch.distributed.run, one rank per GPU, NCCL)
+
+Workload: BASELINE.json configs[2] -- normal-distribution 2D points,
+N = 1e9 per GPU (16 GB of AoS binary64 points, larger than the 126 MB L2,
+so no flush is needed), seed 7 + rank.  Weak scaling: every rank owns a
+1e9-point shard of the global index range; the shards are filtered
+independently and only the ~300 B extremes records and the survivors
+cross GPUs (sharded.py).
+
+A step is one full hull of the whole job's points:
+  value  -- inputs resident in HBM: K1 -> certificate -> (K1b) -> octagon ->
+            K2 -> survivors D2H -> host hull, Gpoints/s over all ranks,
+  e2e    -- the same through the reference-facing API with host buffers:
+            N = 1 the C ABI call ohx_heaphull (octohull::heaphull) on
+            pinned host points, N > 1 the sharded API with each rank's
+            pinned shard uploaded inside the step.
+Steps are timed with CUDA events after a barrier + synchronize on both
+sides, max over ranks.  roofline: the dominant kernel's algorithmic bytes
+per launch (16 B per point read, + 4 B per survivor index written for K2)
+over its CUDA-event duration on the launching stream, against the measured
+HBM copy bandwidth in MEASURED_PEAKS.json.  cpu_baseline: the reference
+library itself (oracle/_ref, compiled from the reference sources) timed on
+the host cores on a bounded 1e8-point sample.
+
+`--impl reference` times that reference CPU implementation on the same
+metric (rank 0 only), each step a bounded sample of the workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gpoints/s end-to-end hull and filter HBM GB/s vs peak at 1/2/4/8 B200"
+UNIT = "Gpoints/s"
+WORKLOAD = "normal-distribution 2D points, 1e9 per GPU (BASELINE configs[2]; C5 shape at N>1)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--dist", default="normal")
+    ap.add_argument("--n", type=float, default=1e9, help="points per GPU")
+    ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--cpu-sample", type=float, default=1e8)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi samples (200 ms) while the timed region runs."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per point of K1/K2 from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------- CPU reference ----
+def cpu_reference(n_sample: int, reps: int, seed: int, dist: str):
+    """The reference heaphull_run (oracle/_ref) on all host cores."""
+    import numpy as np
+
+    import paper_2209_12310_b200 as P
+    from oracle import Oracle, Reference
+
+    pts = P.generate(dist, n_sample, seed)
+    cores = os.cpu_count() or 1
+    if Reference.available():
+        eng = Reference().engine(cores, 32)
+        kind = "reference"
+        run = eng.heaphull
+    else:  # the C restatement, single-threaded
+        o = Oracle()
+        kind, cores = "port", 1
+
+        def run(a):
+            t0 = time.perf_counter()
+            h = o.heaphull(a)
+            return len(h), {"total_ms": (time.perf_counter() - t0) * 1e3}
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        run(pts)
+        times.append(time.perf_counter() - t0)
+    del np
+    return {"kind": kind, "cores": cores, "times": times, "n": n_sample}
+
+
+def run_reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = int(a.cpu_sample)
+    r = cpu_reference(n, a.warmup + a.steps, a.seed, a.dist)
+    timed = r["times"][a.warmup:]
+    ms = 1e3 * sum(timed) / len(timed)
+    value = n / (ms * 1e-3) / 1e9
+    sample = f"{a.dist} n={n} seed={a.seed} (bounded sample of the {WORKLOAD} workload), full heaphull_run"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator, seed 7)",
+        "config": {"workload": WORKLOAD, "dist": a.dist, "sample_points": n,
+                   "parallelism": f"ReduceEngine({{32, {r['cores']}}}) host lanes"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- B200 arm --
+def run_b200_arm(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2209_12310_b200 as P
+    from paper_2209_12310_b200.sharded import CudaShard, sharded_heaphull
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.gpus != world:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    n = int(a.n)
+    base = rank * n
+    t0 = time.perf_counter()
+    host = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+    hp = host.numpy()
+    P.check(P.lib.ohx_generate(P.DISTS[a.dist], n, a.seed + rank, 0.0,
+                               hp.ctypes.data_as(P._dp), 0))
+    d = host.to(dev)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    ctx = P.Context(local)
+    shard = CudaShard(ctx, d, n, base)
+
+    def step_device(stats=None):
+        if world == 1:
+            hull, _ = ctx.heaphull_device(d, n)
+            return hull
+        return sharded_heaphull(shard, device=dev, stats=stats)
+
+    # correctness gate on this very workload: the sharded / single pipeline
+    # must equal the kernel-level path (and K1/K2 are oracle-checked in tests)
+    stats = {}
+    hull0 = sharded_heaphull(shard, device=dev, stats=stats)
+    if rank == 0 and world == 1:
+        hull1 = step_device()
+        assert np.array_equal(hull0, hull1), "pipeline disagreement"
+
+    # ---------------- device-resident timed region
+    for _ in range(a.warmup):
+        step_device()
+    k1, k2 = [], []
+    launches0 = ctx.launches
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        start.record()
+        for _ in range(a.steps):
+            step_device()
+            km = ctx.kernel_ms()
+            k1.append(km["k1"])
+            k2.append(km["k2"])
+        stop.record()
+        barrier()
+    launches = ctx.launches - launches0
+    ms = max_over_ranks(start.elapsed_time(stop) / a.steps)
+    value = world * n / (ms * 1e-3) / 1e9
+
+    # ---------------- e2e through the host-buffer API
+    e2e = None
+    if not a.no_e2e:
+        s_local = sum(stats["counts"])
+        if world == 1:
+            out = np.empty((n + 8, 2), dtype=np.float64) if n < 10_000_000 else np.empty((s_local + 8 + 64, 2))
+            h = P.C.c_uint64(0)
+
+            def step_e2e():
+                P.check(P.lib.ohx_heaphull(hp.ctypes.data_as(P._dp), n, out.ctypes.data_as(P._dp),
+                                           len(out), P.C.byref(h), None))
+        else:
+            d2 = torch.empty_like(d)
+
+            def step_e2e():
+                d2.copy_(host, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                sharded_heaphull(CudaShard(ctx, d2, n, base), device=dev)
+        for _ in range(a.warmup):
+            step_e2e()
+        with ClockSampler(local) as clocks_e2e:
+            barrier()
+            start.record()
+            for _ in range(a.steps):
+                step_e2e()
+            stop.record()
+            barrier()
+        ms_e2e = max_over_ranks(start.elapsed_time(stop) / a.steps)
+        e2e = {"value": world * n / (ms_e2e * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": world * n * 16,
+               "d2h_bytes_per_step": sum(stats["counts"]) * 16 * world + 2 * 320,
+               "api": "ohx_heaphull (C ABI) on pinned host points" if world == 1
+               else "sharded_heaphull with per-rank pinned shard H2D"}
+        clocks_e2e_summary = clocks_e2e.summary()
+    else:
+        clocks_e2e_summary = None
+
+    # ---------------- roofline of the dominant kernel
+    peak, peak_src = measured_peak()
+    s_local = sum(stats["counts"])
+    k1_ms, k2_ms = statistics.mean(k1), statistics.mean(k2)
+    kern = {
+        "k1_extremes": {"ms": k1_ms, "bytes": 16 * n},
+        "k2_filter": {"ms": k2_ms, "bytes": 16 * n + 4 * s_local},
+    }
+    for v in kern.values():
+        v["gbs"] = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+        v["frac"] = v["gbs"] / peak
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    traffic = None
+    tr = ncu_traffic()
+    if tr and dom in tr:
+        traffic = tr[dom]["dram_bytes_per_point"] * n
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak,
+                "unit": "GB/s", "frac": kern[dom]["gbs"] / peak, "traffic": traffic,
+                "peak_source": peak_src,
+                "algorithmic_bytes": kern[dom]["bytes"],
+                "kernels": kern}
+
+    # ---------------- CPU baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        ns = int(a.cpu_sample)
+        r = cpu_reference(ns, 2, a.seed, a.dist)
+        t = statistics.mean(r["times"])
+        cpu = {"value": ns / t / 1e9, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+               "sample": f"{a.dist} n={ns} seed={a.seed}, reference heaphull_run x2 "
+                         f"(ReduceEngine chunk 32, {r['cores']} workers), mean {t:.3f} s"}
+
+    if rank == 0:
+        clk = clocks.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic: reference generator ({a.dist}, seed {a.seed}+rank), bit-identical",
+            "config": {"workload": WORKLOAD, "dist": a.dist, "points_per_gpu": n,
+                       "points_total": world * n, "parallelism": f"index-range shards x{world}",
+                       "l2": "inputs 16 GB/GPU >> 126 MB L2 (no flush needed)",
+                       "survivors": stats["counts"], "corner_certificate": "pass" if not
+                       stats["uncertified"] else f"fallback mask {stats['uncertified']}"},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+            "clocks_e2e": clocks_e2e_summary, "gpu_launches": launches,
+            "setup_s": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference_arm(a)
+    else:
+        run_b200_arm(a)
+
+
+if __name__ == "__main__":
+    main()
