@@ -66,46 +66,64 @@ def parse():
 
 # ---------------------------------------------------------------- clocks --
 class ClockSampler:
-    """nvidia-smi samples (200 ms) while the timed region runs."""
+    """SM clock + clock-event reasons sampled DURING the timed region.
 
-    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NVML is polled every 5 ms from a thread (the device-resident timed
+    region of a 1e9-point run lasts only ~60 ms, too short for
+    `nvidia-smi -lms 200`); `nvidia-smi` is the fallback."""
 
-    def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40,
+               "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4,
+               "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period, self.rows = index, period_s, []
+        self._stop = threading.Event()
+        self.nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (pynvml, h)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([v.strip() for v in line.split(",")])
+    def _poll(self):
+        while not self._stop.is_set():
+            try:
+                if self.nvml:
+                    pynvml, h = self.nvml
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((sm, self.max_mhz, rs))
+                else:
+                    out = subprocess.run(
+                        ["nvidia-smi", "-i", str(self.index),
+                         "--query-gpu=clocks.sm,clocks.max.sm", "--format=csv,noheader,nounits"],
+                        capture_output=True, text=True, timeout=5).stdout.split(",")
+                    self.rows.append((float(out[0]), float(out[1]), 0))
+            except Exception:
+                pass
+            self._stop.wait(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            self.proc.wait(timeout=5)
+        self._stop.set()
+        self.t.join(timeout=5)
 
     def summary(self):
-        rows = [r for r in self.rows if len(r) >= 8]
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(rows)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({k for r in self.rows for k, bit in self.REASONS.items() if r[2] & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.rows[0][1],
+                "reasons": reasons, "samples": len(self.rows),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def measured_peak():

@@ -136,22 +136,26 @@ bool certify_corner(const ohx_extremes_rec& r, int k) {
 // corner c of it has E(c) > 8u(|A||c.y-a.y| + |C||c.x-a.x|) (8u > g2 leaves
 // room for the long double evaluation), and then every point of the box has
 // det > 0 on every edge.
-struct EdgeL {
-  long double ax, ay, A, C;
+// The search runs in double with a 16u margin (double evaluation of E is
+// within ~4u of exact, so 16u in double implies > 8u exactly); the final
+// box is re-verified in long double at 8u before it is used.
+template <typename R>
+struct EdgeT {
+  R ax, ay, A, C;
 };
 
-bool box_ok(const std::vector<EdgeL>& edges, long double x0, long double x1,
-            long double y0, long double y1) {
+template <typename R>
+bool box_ok(const std::vector<EdgeT<R>>& edges, R x0, R x1, R y0, R y1, R factor) {
   if (!(x0 <= x1) || !(y0 <= y1)) return false;
-  const long double u8 = 8.0L * 0x1p-53L;
-  const long double xs[2] = {x0, x1}, ys[2] = {y0, y1};
-  for (const EdgeL& e : edges) {
-    for (long double cx : xs)
-      for (long double cy : ys) {
-        const long double dy = cy - e.ay, dx = cx - e.ax;
-        const long double E = e.A * dy - e.C * dx;
-        const long double margin =
-            u8 * (std::fabs(e.A) * std::fabs(dy) + std::fabs(e.C) * std::fabs(dx)) + 0x1p-1000L;
+  const R uf = factor * R(0x1p-53);
+  const R xs[2] = {x0, x1}, ys[2] = {y0, y1};
+  for (const EdgeT<R>& e : edges) {
+    for (R cx : xs)
+      for (R cy : ys) {
+        const R dy = cy - e.ay, dx = cx - e.ax;
+        const R E = e.A * dy - e.C * dx;
+        const R margin = uf * (std::fabs(e.A) * std::fabs(dy) + std::fabs(e.C) * std::fabs(dx)) +
+                         R(0x1p-1000);
         if (!(E > margin)) return false;
       }
   }
@@ -165,58 +169,59 @@ void fit_box(const double* oct, int m, const double* ea, const double* ec,
   box[2] = 1.0;
   box[3] = 0.0;  // empty
   if (m < 3) return;
-  std::vector<EdgeL> edges;
-  long double vx0 = oct[0], vx1 = oct[0], vy0 = oct[1], vy1 = oct[1];
-  long double cx = 0, cy = 0;
+  std::vector<EdgeT<double>> edges;
+  std::vector<EdgeT<long double>> edges_l;
+  double vx0 = oct[0], vx1 = oct[0], vy0 = oct[1], vy1 = oct[1];
+  double cx = 0, cy = 0;
   for (int i = 0; i < m; ++i) {
     edges.push_back({oct[2 * i], oct[2 * i + 1], ea[i], ec[i]});
-    vx0 = std::min<long double>(vx0, oct[2 * i]);
-    vx1 = std::max<long double>(vx1, oct[2 * i]);
-    vy0 = std::min<long double>(vy0, oct[2 * i + 1]);
-    vy1 = std::max<long double>(vy1, oct[2 * i + 1]);
+    edges_l.push_back({oct[2 * i], oct[2 * i + 1], ea[i], ec[i]});
+    vx0 = std::min(vx0, oct[2 * i]);
+    vx1 = std::max(vx1, oct[2 * i]);
+    vy0 = std::min(vy0, oct[2 * i + 1]);
+    vy1 = std::max(vy1, oct[2 * i + 1]);
     cx += oct[2 * i];
     cy += oct[2 * i + 1];
   }
   cx /= m;
   cy /= m;
-  const long double hx = (vx1 - vx0) / 2, hy = (vy1 - vy0) / 2;
+  const double hx = (vx1 - vx0) / 2, hy = (vy1 - vy0) / 2;
+  auto ok = [&](const double* t) { return box_ok(edges, t[0], t[1], t[2], t[3], 16.0); };
   // 1) the largest centred box with the octagon's aspect ratio
-  long double lo = 0, hi = 1;
-  if (!box_ok(edges, cx - 1e-9L * hx, cx + 1e-9L * hx, cy - 1e-9L * hy, cy + 1e-9L * hy))
-    return;  // sliver octagon: no certified box, every point takes the full test
-  for (int it = 0; it < 60; ++it) {
-    const long double s = (lo + hi) / 2;
-    if (box_ok(edges, cx - s * hx, cx + s * hx, cy - s * hy, cy + s * hy)) lo = s;
+  double b[4] = {cx - 1e-9 * hx, cx + 1e-9 * hx, cy - 1e-9 * hy, cy + 1e-9 * hy};
+  if (!ok(b)) return;  // sliver octagon: no certified box, every point takes the full test
+  double lo = 0, hi = 1;
+  for (int it = 0; it < 40; ++it) {
+    const double s = (lo + hi) / 2;
+    const double t[4] = {cx - s * hx, cx + s * hx, cy - s * hy, cy + s * hy};
+    if (ok(t)) lo = s;
     else hi = s;
   }
-  long double b[4] = {cx - lo * hx, cx + lo * hx, cy - lo * hy, cy + lo * hy};
-  // 2) grow the sides together: each round moves every side half way to the
-  //    furthest position it could reach alone, so no side pins a corner
-  //    early (a greedy one-side-at-a-time push gets stuck on near-flat
-  //    octagon edges); the last round takes the full step
-  const long double lim[4] = {vx0, vx1, vy0, vy1};
-  for (int round = 0; round < 24; ++round) {
-    const long double step = round == 23 ? 1.0L : 0.5L;
+  b[0] = cx - lo * hx;
+  b[1] = cx + lo * hx;
+  b[2] = cy - lo * hy;
+  b[3] = cy + lo * hy;
+  // 2) grow the sides together: each round moves every side part of the
+  //    way to the furthest position it could reach alone, so no side pins a
+  //    corner early (a greedy one-side-at-a-time push gets stuck on
+  //    near-flat octagon edges); the last round takes the full step
+  const double lim[4] = {vx0, vx1, vy0, vy1};
+  constexpr int kRounds = 10;
+  for (int round = 0; round < kRounds; ++round) {
+    const double step = round == kRounds - 1 ? 1.0 : 0.6;
     for (int side = 0; side < 4; ++side) {
-      long double good = b[side], bad = lim[side];
-      for (int it = 0; it < 48; ++it) {
-        const long double mid = (good + bad) / 2;
-        long double t[4] = {b[0], b[1], b[2], b[3]};
-        t[side] = mid;
-        if (box_ok(edges, t[0], t[1], t[2], t[3])) good = mid;
-        else bad = mid;
+      double good = b[side], bad = lim[side];
+      for (int it = 0; it < 32; ++it) {
+        double t[4] = {b[0], b[1], b[2], b[3]};
+        t[side] = (good + bad) / 2;
+        if (ok(t)) good = t[side];
+        else bad = t[side];
       }
       b[side] += step * (good - b[side]);
     }
   }
-  // round inwards to doubles, then re-verify the exact double box
-  double d[4] = {static_cast<double>(b[0]), static_cast<double>(b[1]),
-                 static_cast<double>(b[2]), static_cast<double>(b[3])};
-  if (static_cast<long double>(d[0]) < b[0]) d[0] = std::nextafter(d[0], INFINITY);
-  if (static_cast<long double>(d[1]) > b[1]) d[1] = std::nextafter(d[1], -INFINITY);
-  if (static_cast<long double>(d[2]) < b[2]) d[2] = std::nextafter(d[2], INFINITY);
-  if (static_cast<long double>(d[3]) > b[3]) d[3] = std::nextafter(d[3], -INFINITY);
-  if (box_ok(edges, d[0], d[1], d[2], d[3])) std::memcpy(box, d, sizeof(d));
+  // certify the exact double box in long double before using it
+  if (box_ok<long double>(edges_l, b[0], b[1], b[2], b[3], 8.0L)) std::memcpy(box, b, sizeof(b));
 }
 
 }  // namespace
@@ -501,6 +506,39 @@ void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
       for (std::uint64_t k = 0; k < cnt; ++k) h_idx[k] += c->last_base;
   }
   check_cuda(cudaStreamSynchronize(s), "queue fetch");
+}
+
+void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s) {
+  if (c->last_n == 0) throw std::invalid_argument("no filter result in this context");
+  const std::uint64_t total =
+      c->last_counts[0] + c->last_counts[1] + c->last_counts[2] + c->last_counts[3];
+  if (total == 0) return;
+  dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, total * 16, "gather");
+  launch_gather4(c->last_xy, c->d_queues, c->last_idx_bytes, c->last_cap, c->last_counts,
+                 c->d_gather, s);
+  ++c->launches;
+  check_cuda(cudaMemcpyAsync(h_xy, c->d_gather, total * 16, cudaMemcpyDeviceToHost, s),
+             "cudaMemcpyAsync(queues xy)");
+  check_cuda(cudaStreamSynchronize(s), "queues fetch");
+}
+
+std::vector<P2> device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s) {
+  // reference hull.cpp:164-183 on the device queues: one gather launch and
+  // one D2H of the survivors' coordinates, then the host hull stage
+  const std::uint64_t total = f.counts[0] + f.counts[1] + f.counts[2] + f.counts[3];
+  std::vector<P2> packed(total);
+  queues_fetch_xy(c, reinterpret_cast<double*>(packed.data()), s);
+  const P2* qp[4];
+  std::uint64_t off = 0;
+  for (int k = 0; k < 4; ++k) {
+    qp[k] = packed.data() + off;
+    off += f.counts[k];
+  }
+  const P2 anchors[4] = {{f.ext.x[OHX_EAST], f.ext.y[OHX_EAST]},
+                         {f.ext.x[OHX_NORTH], f.ext.y[OHX_NORTH]},
+                         {f.ext.x[OHX_WEST], f.ext.y[OHX_WEST]},
+                         {f.ext.x[OHX_SOUTH], f.ext.y[OHX_SOUTH]}};
+  return hull_from_queue_points(anchors, qp, f.counts);
 }
 
 FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,

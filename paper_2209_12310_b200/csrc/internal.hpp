@@ -56,6 +56,9 @@ void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan,
                std::uint64_t* d_status, std::uint64_t ntiles, void* d_queues,
                int idx_bytes, std::uint64_t cap, std::uint8_t* d_labels,
                unsigned long long* d_counts, cudaStream_t stream);
+void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
+                    std::uint64_t cap, const std::uint64_t counts[4], double* d_out,
+                    cudaStream_t stream);
 void launch_gather(const double* d_xy, const void* d_idx, int idx_bytes,
                    std::uint64_t count, double* d_out, cudaStream_t stream);
 

@@ -210,38 +210,55 @@ constexpr int kK1Unroll = 4;
 // Slots (ohx.h): 0 east x, 1 north y, 2 west -x, 3 south -y,
 //                4 ne fl(x+y), 5 nw fl(y-x), 6 sw -fl(x+y), 7 se fl(x-y);
 // slots 4..7 also keep their second-best key.
+//
+// Fast path: a point changes the thread's state only if some key beats the
+// current best (axis slots) or the current second (diagonal slots; beating
+// the best implies beating the second).  After the first few hundred points
+// of a thread that is rare (~ln(m) record breaks per key), so the common
+// path is 2 DADD + 8 DSETP + a predicate reduction, and the selects of the
+// full update run only on the rare divergent slow path.
 struct K1Visit {
-  __device__ __forceinline__ static void visit(ArgState<8, 4>& st, double2 p,
-                                               std::uint64_t j) {
-    const double t = __dadd_rn(p.x, p.y);
-    const double d = __dsub_rn(p.x, p.y);
-    upd(st.k[0], st.i[0], p.x, j);
-    upd(st.k[1], st.i[1], p.y, j);
-    upd(st.k[2], st.i[2], -p.x, j);
-    upd(st.k[3], st.i[3], -p.y, j);
+  __device__ __forceinline__ static void slow(ArgState<8, 4>& st, double x, double y,
+                                              double t, double d, std::uint64_t j) {
+    upd(st.k[0], st.i[0], x, j);
+    upd(st.k[1], st.i[1], y, j);
+    upd(st.k[2], st.i[2], -x, j);
+    upd(st.k[3], st.i[3], -y, j);
     upd2(st.k[4], st.i[4], st.s[0], t, j);
     upd2(st.k[5], st.i[5], st.s[1], -d, j);
     upd2(st.k[6], st.i[6], st.s[2], -t, j);
     upd2(st.k[7], st.i[7], st.s[3], d, j);
   }
+  __device__ __forceinline__ static void visit(ArgState<8, 4>& st, double2 p,
+                                               std::uint64_t j) {
+    const double t = __dadd_rn(p.x, p.y);
+    const double d = __dsub_rn(p.x, p.y);
+    const bool hit = (p.x > st.k[0]) | (p.y > st.k[1]) | (-p.x > st.k[2]) |
+                     (-p.y > st.k[3]) | (t > st.s[0]) | (-d > st.s[1]) |
+                     (-t > st.s[2]) | (d > st.s[3]);
+    if (hit) slow(st, p.x, p.y, t, d, j);
+  }
 };
 
+template <typename IdxT>
 __global__ void __launch_bounds__(kK1Block)
     k1_extremes(const double2* __restrict__ pts, std::uint64_t n,
                 std::uint64_t base, K1Partial* partials, unsigned* ticket,
                 ohx_extremes_rec* out) {
   ArgState<8, 4> st;
   st.init();
-  const std::uint64_t stride = std::uint64_t(gridDim.x) * kK1Block;
-  std::uint64_t j = std::uint64_t(blockIdx.x) * kK1Block + threadIdx.x;
-  for (; j + (kK1Unroll - 1) * stride < n; j += kK1Unroll * stride) {
+  const IdxT stride = static_cast<IdxT>(gridDim.x) * kK1Block;
+  IdxT j = static_cast<IdxT>(blockIdx.x) * kK1Block + threadIdx.x;
+  const IdxT nn = static_cast<IdxT>(n);
+  // j + (U-1)*stride cannot wrap: the grid never exceeds n/U threads
+  for (; j + (kK1Unroll - 1) * stride < nn; j += kK1Unroll * stride) {
     double2 v[kK1Unroll];
 #pragma unroll
     for (int u = 0; u < kK1Unroll; ++u) v[u] = ld_stream(pts + j + u * stride);
 #pragma unroll
     for (int u = 0; u < kK1Unroll; ++u) K1Visit::visit(st, v[u], j + u * stride);
   }
-  for (; j < n; j += stride) K1Visit::visit(st, ld_stream(pts + j), j);
+  for (; j < nn; j += stride) K1Visit::visit(st, ld_stream(pts + j), j);
 
   block_reduce<8, 4, kK1Block>(st);
   if (!grid_combine<8, 4, kK1Block>(st, partials, ticket)) return;
@@ -282,10 +299,16 @@ __global__ void __launch_bounds__(kK1Block)
   const std::uint64_t stride = std::uint64_t(gridDim.x) * kK1Block;
   std::uint64_t j = std::uint64_t(blockIdx.x) * kK1Block + threadIdx.x;
   auto visit = [&](double2 p, std::uint64_t jj) {
+    double m[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const double m = __dadd_rn(fabs(__dsub_rn(p.x, cx[a])), fabs(__dsub_rn(p.y, cy[a])));
-      upd(st.k[a], st.i[a], -m, jj);
+    for (int a = 0; a < 4; ++a)
+      m[a] = __dadd_rn(fabs(__dsub_rn(p.x, cx[a])), fabs(__dsub_rn(p.y, cy[a])));
+    // fast path as in K1: only a strictly closer point touches the state
+    const bool hit = (-m[0] > st.k[0]) | (-m[1] > st.k[1]) | (-m[2] > st.k[2]) |
+                     (-m[3] > st.k[3]);
+    if (hit) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a) upd(st.k[a], st.i[a], -m[a], jj);
     }
   };
   for (; j + (kK1Unroll - 1) * stride < n; j += kK1Unroll * stride) {
@@ -522,6 +545,19 @@ __global__ void gather_xy(const double2* __restrict__ pts,
     out[k] = pts[idx[k]];
 }
 
+// All four queues in one launch, packed back to back: out = [q1|q2|q3|q4].
+template <typename IdxT>
+__global__ void gather_xy4(const double2* __restrict__ pts, const IdxT* __restrict__ queues,
+                           std::uint64_t cap, ulonglong4 ends, double2* __restrict__ out) {
+  const std::uint64_t total = ends.w;
+  for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += std::uint64_t(gridDim.x) * blockDim.x) {
+    const int q = (k >= ends.x) + (k >= ends.y) + (k >= ends.z);
+    const std::uint64_t start = q == 0 ? 0 : (q == 1 ? ends.x : (q == 2 ? ends.y : ends.z));
+    out[k] = pts[queues[std::uint64_t(q) * cap + (k - start)]];
+  }
+}
+
 }  // namespace
 
 // ============================================================ launchers ==
@@ -529,7 +565,7 @@ int k1_grid(int device, std::uint64_t n) {
   int sms = 0, per_sm = 0;
   check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device),
              "cudaDeviceGetAttribute");
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_extremes,
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_extremes<std::uint64_t>,
                                                            kK1Block, 0),
              "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
   if (per_sm < 1) per_sm = 1;
@@ -541,8 +577,13 @@ int k1_grid(int device, std::uint64_t n) {
 void launch_k1(const double* d_xy, std::uint64_t n, std::uint64_t base,
                K1Partial* partials, int grid, unsigned* ticket,
                ohx_extremes_rec* d_out, cudaStream_t stream) {
-  k1_extremes<<<grid, kK1Block, 0, stream>>>(reinterpret_cast<const double2*>(d_xy),
-                                              n, base, partials, ticket, d_out);
+  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  // 32-bit in-loop indices whenever the shard (plus a full grid stride of
+  // overshoot) fits: one SEL per index update instead of two
+  if (n + std::uint64_t(grid) * kK1Block * kK1Unroll < 0xffffffffull)
+    k1_extremes<std::uint32_t><<<grid, kK1Block, 0, stream>>>(pts, n, base, partials, ticket, d_out);
+  else
+    k1_extremes<std::uint64_t><<<grid, kK1Block, 0, stream>>>(pts, n, base, partials, ticket, d_out);
   check_cuda(cudaGetLastError(), "k1_extremes launch");
 }
 
@@ -575,6 +616,24 @@ void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan,
         static_cast<std::uint64_t*>(d_queues), cap, d_labels, d_counts);
   }
   check_cuda(cudaGetLastError(), "k2_filter launch");
+}
+
+void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
+                    std::uint64_t cap, const std::uint64_t counts[4], double* d_out,
+                    cudaStream_t stream) {
+  const ulonglong4 ends = make_ulonglong4(counts[0], counts[0] + counts[1],
+                                          counts[0] + counts[1] + counts[2],
+                                          counts[0] + counts[1] + counts[2] + counts[3]);
+  if (ends.w == 0) return;
+  const unsigned grid = static_cast<unsigned>(ends.w < 148ull * 2048 ? (ends.w + 255) / 256 : 148 * 8);
+  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  if (idx_bytes == 4)
+    gather_xy4<<<grid, 256, 0, stream>>>(pts, static_cast<const std::uint32_t*>(d_queues), cap,
+                                         ends, reinterpret_cast<double2*>(d_out));
+  else
+    gather_xy4<<<grid, 256, 0, stream>>>(pts, static_cast<const std::uint64_t*>(d_queues), cap,
+                                         ends, reinterpret_cast<double2*>(d_out));
+  check_cuda(cudaGetLastError(), "gather_xy4 launch");
 }
 
 void launch_gather(const double* d_xy, const void* d_idx, int idx_bytes,

@@ -66,19 +66,7 @@ ExtremeSet from_set(const ohx_extreme_set& s) {
 // hull.cpp:164-183): survivor coordinates are gathered on the device in
 // queue (= index) order and copied back, then chained on the host.
 HullPolygon hull_from_device(Device& d, const ohx::FilterOut& f) {
-  std::vector<ohx::P2> q[4];
-  const ohx::P2* qp[4];
-  for (int k = 0; k < 4; ++k) {
-    q[k].resize(f.counts[k]);
-    ohx::queue_fetch(d.c, k + 1, nullptr, reinterpret_cast<double*>(q[k].data()),
-                     f.counts[k], d.s);
-    qp[k] = q[k].data();
-  }
-  const ohx::P2 anchors[4] = {{f.ext.x[OHX_EAST], f.ext.y[OHX_EAST]},
-                              {f.ext.x[OHX_NORTH], f.ext.y[OHX_NORTH]},
-                              {f.ext.x[OHX_WEST], f.ext.y[OHX_WEST]},
-                              {f.ext.x[OHX_SOUTH], f.ext.y[OHX_SOUTH]}};
-  const std::vector<ohx::P2> cyc = ohx::hull_from_queue_points(anchors, qp, f.counts);
+  const std::vector<ohx::P2> cyc = ohx::device_queues_hull(d.c, f, d.s);
   HullPolygon h;
   h.vertices.resize(cyc.size());
   std::memcpy(static_cast<void*>(h.vertices.data()), cyc.data(), cyc.size() * sizeof(Point2D));

@@ -63,19 +63,7 @@ int ohx_heaphull_device(ohx_ctx* ctx, const double* d_xy, uint64_t n, double* h_
     const auto t0 = Clock::now();
     const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
     const auto t1 = Clock::now();
-    std::vector<ohx::P2> q[4];
-    const ohx::P2* qp[4];
-    for (int k = 0; k < 4; ++k) {
-      q[k].resize(f.counts[k]);
-      ohx::queue_fetch(ctx, k + 1, nullptr, reinterpret_cast<double*>(q[k].data()),
-                       f.counts[k], s);
-      qp[k] = q[k].data();
-    }
-    const ohx::P2 anchors[4] = {{f.ext.x[OHX_EAST], f.ext.y[OHX_EAST]},
-                                {f.ext.x[OHX_NORTH], f.ext.y[OHX_NORTH]},
-                                {f.ext.x[OHX_WEST], f.ext.y[OHX_WEST]},
-                                {f.ext.x[OHX_SOUTH], f.ext.y[OHX_SOUTH]}};
-    const std::vector<ohx::P2> cyc = ohx::hull_from_queue_points(anchors, qp, f.counts);
+    const std::vector<ohx::P2> cyc = ohx::device_queues_hull(ctx, f, s);
     *h = cyc.size();
     if (cyc.size() > cap) throw std::invalid_argument("hull output capacity too small");
     std::memcpy(h_hull, cyc.data(), cyc.size() * sizeof(ohx::P2));

@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <mutex>
+#include <vector>
 
 #include "internal.hpp"
 #include "ohx.h"
@@ -49,6 +50,13 @@ void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
             std::uint64_t counts[4], cudaStream_t s);
 void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
                  std::uint64_t cap, cudaStream_t s);
+
+// survivor coordinates of all four queues, packed [q1|q2|q3|q4], one launch
+void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s);
+
+// host hull stage on the queues of the last filter (survivors gathered and
+// copied back in one launch)
+std::vector<P2> device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s);
 
 // K1 -> certificate -> (K1b) -> octagon -> plan -> K2 on one device
 FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
