@@ -55,17 +55,17 @@ __device__ __forceinline__ void st_relaxed(std::uint64_t* p, std::uint64_t v) {
 // is argmax of its exact negation).  Within a thread indices only grow, so
 // a strict '>' keeps the earliest index.
 
-template <int NK, int NS>
+template <int NK, int NS, typename I = std::uint64_t>
 struct ArgState {
   double k[NK];
-  std::uint64_t i[NK];
+  I i[NK];
   double s[NS > 0 ? NS : 1];
 
   __device__ __forceinline__ void init() {
 #pragma unroll
     for (int a = 0; a < NK; ++a) {
       k[a] = __longlong_as_double(0xfff0000000000000ll);  // -inf
-      i[a] = ~0ull;
+      i[a] = ~I(0);
     }
 #pragma unroll
     for (int a = 0; a < (NS > 0 ? NS : 1); ++a) s[a] = __longlong_as_double(0xfff0000000000000ll);
@@ -73,16 +73,16 @@ struct ArgState {
 };
 
 // in-thread update: strict improvement only
-__device__ __forceinline__ void upd(double& bk, std::uint64_t& bi, double key,
-                                    std::uint64_t j) {
+template <typename I>
+__device__ __forceinline__ void upd(double& bk, I& bi, double key, I j) {
   const bool take = key > bk;
   bk = take ? key : bk;
   bi = take ? j : bi;
 }
 
 // in-thread update tracking the second-largest key of the multiset
-__device__ __forceinline__ void upd2(double& bk, std::uint64_t& bi, double& s2,
-                                     double key, std::uint64_t j) {
+template <typename I>
+__device__ __forceinline__ void upd2(double& bk, I& bi, double& s2, double key, I j) {
   const bool take = key > bk;
   const double lo = take ? bk : key;  // the value that does not become best
   s2 = lo > s2 ? lo : s2;
@@ -205,7 +205,22 @@ __device__ __forceinline__ bool grid_combine(ArgState<NK, NS>& st,
 }
 
 constexpr int kK1Block = 256;
-constexpr int kK1Unroll = 4;
+constexpr int kK1Unroll = 8;
+constexpr int kK1MinBlocks = 3;
+
+// widen a streaming-phase state (32- or 64-bit indices) for the reductions
+template <int NK, int NS, typename I>
+__device__ __forceinline__ ArgState<NK, NS> widen(const ArgState<NK, NS, I>& t) {
+  ArgState<NK, NS> st;
+#pragma unroll
+  for (int a = 0; a < NK; ++a) {
+    st.k[a] = t.k[a];
+    st.i[a] = t.i[a] == ~I(0) ? ~0ull : static_cast<std::uint64_t>(t.i[a]);
+  }
+#pragma unroll
+  for (int a = 0; a < (NS > 0 ? NS : 1); ++a) st.s[a] = t.s[a];
+  return st;
+}
 
 // Slots (ohx.h): 0 east x, 1 north y, 2 west -x, 3 south -y,
 //                4 ne fl(x+y), 5 nw fl(y-x), 6 sw -fl(x+y), 7 se fl(x-y);
@@ -218,8 +233,9 @@ constexpr int kK1Unroll = 4;
 // path is 2 DADD + 8 DSETP + a predicate reduction, and the selects of the
 // full update run only on the rare divergent slow path.
 struct K1Visit {
-  __device__ __forceinline__ static void slow(ArgState<8, 4>& st, double x, double y,
-                                              double t, double d, std::uint64_t j) {
+  template <typename I>
+  __device__ __forceinline__ static void slow(ArgState<8, 4, I>& st, double x, double y,
+                                              double t, double d, I j) {
     upd(st.k[0], st.i[0], x, j);
     upd(st.k[1], st.i[1], y, j);
     upd(st.k[2], st.i[2], -x, j);
@@ -229,8 +245,8 @@ struct K1Visit {
     upd2(st.k[6], st.i[6], st.s[2], -t, j);
     upd2(st.k[7], st.i[7], st.s[3], d, j);
   }
-  __device__ __forceinline__ static void visit(ArgState<8, 4>& st, double2 p,
-                                               std::uint64_t j) {
+  template <typename I>
+  __device__ __forceinline__ static void visit(ArgState<8, 4, I>& st, double2 p, I j) {
     const double t = __dadd_rn(p.x, p.y);
     const double d = __dsub_rn(p.x, p.y);
     const bool hit = (p.x > st.k[0]) | (p.y > st.k[1]) | (-p.x > st.k[2]) |
@@ -241,12 +257,12 @@ struct K1Visit {
 };
 
 template <typename IdxT>
-__global__ void __launch_bounds__(kK1Block)
+__global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
     k1_extremes(const double2* __restrict__ pts, std::uint64_t n,
                 std::uint64_t base, K1Partial* partials, unsigned* ticket,
                 ohx_extremes_rec* out) {
-  ArgState<8, 4> st;
-  st.init();
+  ArgState<8, 4, IdxT> ts;
+  ts.init();
   const IdxT stride = static_cast<IdxT>(gridDim.x) * kK1Block;
   IdxT j = static_cast<IdxT>(blockIdx.x) * kK1Block + threadIdx.x;
   const IdxT nn = static_cast<IdxT>(n);
@@ -256,10 +272,11 @@ __global__ void __launch_bounds__(kK1Block)
 #pragma unroll
     for (int u = 0; u < kK1Unroll; ++u) v[u] = ld_stream(pts + j + u * stride);
 #pragma unroll
-    for (int u = 0; u < kK1Unroll; ++u) K1Visit::visit(st, v[u], j + u * stride);
+    for (int u = 0; u < kK1Unroll; ++u) K1Visit::visit(ts, v[u], IdxT(j + u * stride));
   }
-  for (; j < nn; j += stride) K1Visit::visit(st, ld_stream(pts + j), j);
+  for (; j < nn; j += stride) K1Visit::visit(ts, ld_stream(pts + j), j);
 
+  ArgState<8, 4> st = widen(ts);
   block_reduce<8, 4, kK1Block>(st);
   if (!grid_combine<8, 4, kK1Block>(st, partials, ticket)) return;
   if (threadIdx.x < 8) {
@@ -287,7 +304,7 @@ __global__ void __launch_bounds__(kK1Block)
 // ==================================================================== K1b ==
 // slot k: argmax of -(|x - cx| + |y - cy|) = the reference argmin of
 // manhattan(p, corner) (geometry.hpp:35-37), corners ne, nw, sw, se.
-__global__ void __launch_bounds__(kK1Block)
+__global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
     k1b_corners(const double2* __restrict__ pts, std::uint64_t n,
                 std::uint64_t base, double xmax, double ymax, double xmin,
                 double ymin, K1Partial* partials, unsigned* ticket,
@@ -565,7 +582,7 @@ int k1_grid(int device, std::uint64_t n) {
   int sms = 0, per_sm = 0;
   check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device),
              "cudaDeviceGetAttribute");
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_extremes<std::uint64_t>,
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_extremes<std::uint32_t>,
                                                            kK1Block, 0),
              "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
   if (per_sm < 1) per_sm = 1;
