@@ -13,6 +13,7 @@ import pytest
 import paper_2209_12310_b200 as P
 from paper_2209_12310_b200 import _lib
 from conftest import ROOT, sha
+from emulate import emulate_corners, emulate_k1
 
 
 def declared_symbols():
@@ -93,39 +94,6 @@ def test_host_hull_matches_oracle_on_degenerate_grids(oracle, grid_trials):
 
 
 # ------------------------------------------------- extremes combine + cert
-def emulate_k1(pts, base=0):
-    """Reference-semantics emulation of one shard's K1 record (test-side):
-    argmax of the 8 maximised keys, smallest index on ties, plus the second
-    largest diagonal key."""
-    x, y = pts[:, 0], pts[:, 1]
-    t = x + y
-    d = x - y
-    keys = [x, y, -x, -y, t, -d, -t, d]
-    rec = _lib.ExtremesRec()
-    for a, k in enumerate(keys):
-        j = int(np.flatnonzero(k == k.max())[0])
-        rec.key[a] = k[j]
-        rec.idx[a] = base + j
-        rec.x[a] = x[j]
-        rec.y[a] = y[j]
-        if a >= 4:
-            rest = np.delete(k, j)
-            rec.second[a - 4] = rest.max() if rest.size else -np.inf
-    rec.n = len(pts)
-    return rec
-
-
-def emulate_corners(pts, bbox, base=0):
-    xmax, ymax, xmin, ymin = bbox
-    rec = _lib.CornerRec()
-    for a, (cx, cy) in enumerate([(xmax, ymax), (xmin, ymax), (xmin, ymin), (xmax, ymin)]):
-        m = np.abs(pts[:, 0] - cx) + np.abs(pts[:, 1] - cy)
-        j = int(np.flatnonzero(m == m.min())[0])
-        rec.key[a], rec.idx[a], rec.x[a], rec.y[a] = m[j], base + j, pts[j, 0], pts[j, 1]
-    rec.n = len(pts)
-    return rec
-
-
 def resolve_like_pipeline(pts, shards):
     """Shard -> K1 records -> combine -> certificate -> (exact corners)."""
     bounds = np.linspace(0, len(pts), shards + 1).astype(int)

@@ -1,0 +1,74 @@
+"""The multi-GPU orchestration (paper_2209_12310_b200/sharded.py) on CPU:
+world_size 2 (and 3) over gloo, every rank owning a contiguous index range,
+the per-shard kernels emulated with reference semantics (tests/emulate.py).
+The sharded result must equal the single-process oracle bit for bit."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+CORPORA = [("normal", 20000, 7, 0.0), ("circle", 3000, 12, 2.0), ("square", 5001, 3, 0.0),
+           ("disk", 4000, 55, 0.0)]
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    sys.path.insert(0, os.path.dirname(HERE))
+    sys.path.insert(0, HERE)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from emulate import EmulatedShard
+    from oracle import Oracle
+    from paper_2209_12310_b200.sharded import shard_range, sharded_heaphull
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o = Oracle()
+        out = []
+        cases = CORPORA + [("grid", 0, 0, 0.0)]
+        for dist_name, n, seed, d in cases:
+            if dist_name == "grid":  # ties and duplicates across the shard seam
+                rng = np.random.default_rng(1)
+                pts = (rng.integers(-3, 4, size=(61, 2)) / 2.0).astype(float)
+            else:
+                pts = o.generate(dist_name, n, seed, d)
+            b0, cnt = shard_range(len(pts), world, rank)
+            stats = {}
+            hull = sharded_heaphull(EmulatedShard(o, pts, b0, cnt), device="cpu", stats=stats)
+            if rank == 0:
+                want, labels = o.heaphull(pts, with_labels=True)
+                out.append((dist_name, hull.tolist() == want.tolist(),
+                            stats["ext"] == [int(v) for v in o.find_extremes(pts)],
+                            stats["n_total"] == len(pts)))
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_pipeline_matches_oracle(world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for name, hull_ok, ext_ok, n_ok in res:
+        assert hull_ok and ext_ok and n_ok, name
