@@ -105,6 +105,8 @@ typedef struct {
   double box[4];         /* certified interior box xlo,xhi,ylo,yhi (empty if xlo>xhi) */
   uint64_t kept[8];      /* kept indices in override order E,NE,N,NW,W,SW,S,SE */
   uint8_t kept_label[8]; /* 1,1,2,2,3,3,4,4 */
+  uint8_t facing[16];    /* per box-side code (bit0 E, bit1 N, bit2 W, bit3 S):
+                            the octagon edge facing that side, tested first */
   int32_t m;             /* octagon vertices; < 3 = degenerate (filter nothing) */
   int32_t pad;
 } ohx_filter_plan;

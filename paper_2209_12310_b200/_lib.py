@@ -50,7 +50,8 @@ class FilterPlan(C.Structure):
                 ("qax", C.c_double * 4), ("qay", C.c_double * 4),
                 ("qa", C.c_double * 4), ("qc", C.c_double * 4),
                 ("box", C.c_double * 4), ("kept", _u64 * 8),
-                ("kept_label", C.c_uint8 * 8), ("m", C.c_int32), ("pad", C.c_int32)]
+                ("kept_label", C.c_uint8 * 8), ("facing", C.c_uint8 * 16),
+                ("m", C.c_int32), ("pad", C.c_int32)]
 
 
 # (name, restype, argtypes) of every entry point declared in include/ohx.h

@@ -414,6 +414,23 @@ void make_plan(const ohx_extreme_set& e, const double* oct, int m,
     p->kept_label[k] = static_cast<std::uint8_t>(1 + k / 2);
   }
   fit_box(oct, m, p->ea, p->ec, p->box);
+  // facing table: for each combination of box sides a point lies beyond,
+  // the edge whose outward normal (C, -A) best matches that direction
+  for (int code = 0; code < 16; ++code) {
+    const double dx = ((code & 1) ? 1.0 : 0.0) - ((code & 4) ? 1.0 : 0.0);
+    const double dy = ((code & 2) ? 1.0 : 0.0) - ((code & 8) ? 1.0 : 0.0);
+    int best = 0;
+    double best_v = -INFINITY;
+    for (int i = 0; i < (m >= 3 ? m : 0); ++i) {
+      const double len = std::hypot(p->ea[i], p->ec[i]);
+      const double v = len > 0 ? (p->ec[i] * dx - p->ea[i] * dy) / len : -INFINITY;
+      if (v > best_v) {
+        best_v = v;
+        best = i;
+      }
+    }
+    p->facing[code] = static_cast<std::uint8_t>(best);
+  }
 }
 
 void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
@@ -435,6 +452,9 @@ void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
     kp.kept[k] = (g >= base && g - base < n) ? g - base : ~0ull;
     kp.kept_label[k] = plan.kept_label[k];
   }
+  std::memcpy(kp.facing, plan.facing, sizeof(kp.facing));
+  for (int code = 0; code < 16; ++code)
+    if (plan.m >= 3 && kp.facing[code] >= plan.m) throw std::invalid_argument("bad facing table");
   kp.m = plan.m;
 
   const std::uint64_t ntiles = (n + kK2Tile - 1) / kK2Tile;

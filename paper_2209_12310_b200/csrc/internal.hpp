@@ -23,6 +23,7 @@ struct KPlan {
   double box[4];
   std::uint64_t kept[8];  // shard-local, ~0 when not in this shard
   std::uint32_t kept_label[8];
+  std::uint8_t facing[16];  // first octagon edge to test per box-side code
   std::int32_t m;
 };
 

@@ -362,39 +362,50 @@ __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
 constexpr std::uint64_t kFlagA = 1ull << 62;  // aggregate published
 constexpr std::uint64_t kFlagP = 2ull << 62;  // inclusive prefix published
 constexpr std::uint64_t kValMask = (1ull << 62) - 1;
+constexpr int kK2Warps = kK2Block / 32;
+constexpr int kK2Seg = kK2Items * kK2Warps;  // (item, warp) segments of a tile
 
 // orientation(a, b, p) < 0 with the edge constants A = fl(b.x-a.x),
 // C = fl(b.y-a.y): det = fl(fl(A*fl(p.y-a.y)) - fl(C*fl(p.x-a.x))) is
 // negative exactly when the first rounded product is below the second
 // (geometry.hpp:27-32).
-__device__ __forceinline__ bool right_of(double px, double py, double ax,
-                                         double ay, double A, double C) {
-  return __dmul_rn(A, __dsub_rn(py, ay)) < __dmul_rn(C, __dsub_rn(px, ax));
+__device__ __forceinline__ bool right_of(double px, double py, const double4& e) {
+  return __dmul_rn(e.z, __dsub_rn(py, e.y)) < __dmul_rn(e.w, __dsub_rn(px, e.x));
 }
 
-__device__ __forceinline__ std::uint32_t classify(const KPlan& P, double2 p,
-                                                  std::uint64_t j,
-                                                  bool tile_has_kept) {
-  if (tile_has_kept) {
-    // kept overrides, first match wins (filter.cpp:108-124)
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (j == P.kept[k]) return P.kept_label[k];
+struct K2Shared {
+  double4 edge[8];    // octagon edges {a.x, a.y, A, C}
+  double4 qedge[4];   // find_queue edges E->N, N->W, W->S, S->E
+  std::uint8_t facing[16];
+  std::uint32_t tile;
+  std::uint32_t off[4][kK2Seg];
+  std::uint64_t excl[4];
+  // per warp: the warp's hard points, densely packed, and their labels
+  double2 stage[kK2Warps][kK2Items * 32];
+  std::uint8_t code[kK2Warps][kK2Items * 32];
+};
+
+// Full classification of a point outside the certified box: the octagon test
+// (filter.cpp:125-128, geometry.cpp:16-22) starting at the edge that faces
+// the point's side of the box (any order yields the same "some edge < 0"),
+// then find_queue in its fixed order (filter.cpp:94-101).
+__device__ __forceinline__ std::uint32_t classify_hard(const K2Shared& S, int m, double2 p,
+                                                       int code) {
+  if (m >= 3) {
+    int e = S.facing[code];
+    bool out = false;
+    for (int k = 0; k < m; ++k) {
+      if (right_of(p.x, p.y, S.edge[e])) {
+        out = true;
+        break;
+      }
+      e = (e + 1 == m) ? 0 : e + 1;
+    }
+    if (!out) return 0;
   }
-  // certified interior box: every edge determinant provably > 0 there
-  if (p.x >= P.box[0] && p.x <= P.box[1] && p.y >= P.box[2] && p.y <= P.box[3])
-    return 0;
-  bool outside = P.m < 3;  // degenerate octagon filters nothing (filter.cpp:125)
-  if (!outside) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e)
-      outside |= right_of(p.x, p.y, P.ax[e], P.ay[e], P.ea[e], P.ec[e]);
-  }
-  if (!outside) return 0;
-  // find_queue (filter.cpp:88-102): first strictly-right edge, else 1
 #pragma unroll
   for (int q = 0; q < 4; ++q)
-    if (right_of(p.x, p.y, P.qax[q], P.qay[q], P.qa[q], P.qc[q])) return q + 1;
+    if (right_of(p.x, p.y, S.qedge[q])) return q + 1;
   return 1;
 }
 
@@ -434,22 +445,24 @@ __global__ void __launch_bounds__(kK2Block)
               std::uint64_t ntiles, unsigned* tile_counter, IdxT* queues,
               std::uint64_t cap, std::uint8_t* labels,
               unsigned long long* counts) {
-  constexpr int W = kK2Block / 32;
-  constexpr int SEG = kK2Items * W;  // (item, warp) segments of a tile
-  __shared__ std::uint32_t s_tile;
-  __shared__ std::uint32_t s_off[4][SEG];
-  __shared__ std::uint64_t s_excl[4];
-  __shared__ std::uint32_t s_agg[4];
-
+  constexpr int W = kK2Warps;
+  extern __shared__ __align__(16) unsigned char k2_smem[];
+  K2Shared& S = *reinterpret_cast<K2Shared*>(k2_smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
-  __syncthreads();
-  const std::uint64_t tile = s_tile;
-  const std::uint64_t t0 = tile * kK2Tile;
+  const unsigned lt = (1u << lane) - 1u;
 
-  bool has_kept = false;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) has_kept |= (plan.kept[k] - t0) < kK2Tile;
+  if (threadIdx.x == 0) S.tile = atomicAdd(tile_counter, 1u);
+  if (threadIdx.x < 8)
+    S.edge[threadIdx.x] = make_double4(plan.ax[threadIdx.x], plan.ay[threadIdx.x],
+                                       plan.ea[threadIdx.x], plan.ec[threadIdx.x]);
+  else if (threadIdx.x < 12)
+    S.qedge[threadIdx.x - 8] = make_double4(plan.qax[threadIdx.x - 8], plan.qay[threadIdx.x - 8],
+                                            plan.qa[threadIdx.x - 8], plan.qc[threadIdx.x - 8]);
+  else if (threadIdx.x < 28)
+    S.facing[threadIdx.x - 12] = plan.facing[threadIdx.x - 12];
+  __syncthreads();
+  const std::uint64_t tile = S.tile;
+  const std::uint64_t t0 = tile * kK2Tile;
 
   double2 v[kK2Items];
 #pragma unroll
@@ -457,13 +470,60 @@ __global__ void __launch_bounds__(kK2Block)
     const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
     v[it] = j < n ? ld_stream(pts + j) : make_double2(0.0, 0.0);
   }
+
+  bool has_kept = false;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) has_kept |= (plan.kept[k] - t0) < kK2Tile;
+
+  // 1) kept overrides and the certified box; everything else is "hard"
   std::uint32_t lab[kK2Items];
-  std::uint32_t any = 0;
+  unsigned hard_ballot[kK2Items];
+  std::uint32_t hbase[kK2Items];
+  std::uint32_t H = 0;
 #pragma unroll
   for (int it = 0; it < kK2Items; ++it) {
     const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
-    lab[it] = j < n ? classify(plan, v[it], j, has_kept) : 0u;
+    lab[it] = 0;
+    bool kept = false;
+    if (has_kept) {
+#pragma unroll
+      for (int k = 7; k >= 0; --k)  // first match wins (filter.cpp:122-124)
+        if (j == plan.kept[k]) {
+          lab[it] = plan.kept_label[k];
+          kept = true;
+        }
+    }
+    const bool e = v[it].x > plan.box[1], w = v[it].x < plan.box[0];
+    const bool nn = v[it].y > plan.box[3], s = v[it].y < plan.box[2];
+    const bool hard = j < n && !kept && (e | w | nn | s);
+    hard_ballot[it] = __ballot_sync(kFull, hard);
+    hbase[it] = H;
+    H += __popc(hard_ballot[it]);
+    if (hard) {
+      const std::uint32_t slot = hbase[it] + __popc(hard_ballot[it] & lt);
+      S.stage[warp][slot] = v[it];
+      S.code[warp][slot] = static_cast<std::uint8_t>(e | (nn << 1) | (w << 2) | (s << 3));
+    }
+  }
+
+  // 2) dense classification of the warp's hard points, 32 at a time
+  if (H) {
+    __syncwarp();
+    for (std::uint32_t slot = lane; slot < H; slot += 32)
+      S.code[warp][slot] = static_cast<std::uint8_t>(
+          classify_hard(S, plan.m, S.stage[warp][slot], S.code[warp][slot]));
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < kK2Items; ++it)
+      if (hard_ballot[it] >> lane & 1u)
+        lab[it] = S.code[warp][hbase[it] + __popc(hard_ballot[it] & lt)];
+  }
+
+  std::uint32_t any = 0;
+#pragma unroll
+  for (int it = 0; it < kK2Items; ++it) {
     any |= lab[it];
+    const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
     if (labels != nullptr && j < n) labels[j] = static_cast<std::uint8_t>(lab[it]);
   }
 
@@ -485,25 +545,31 @@ __global__ void __launch_bounds__(kK2Block)
     return;
   }
 
-  // per (item, warp, quadrant) survivor counts
+  // 3) per (item, warp, quadrant) survivor counts; a lane's own quadrant
+  //    mask comes from two ballots of the label bits
+  unsigned live_b[kK2Items], b0_b[kK2Items], b1_b[kK2Items];
 #pragma unroll
   for (int it = 0; it < kK2Items; ++it) {
-    const unsigned live = __ballot_sync(kFull, lab[it] != 0);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const unsigned mq = live ? __ballot_sync(kFull, lab[it] == unsigned(q + 1)) : 0u;
-      if (lane == 0) s_off[q][it * W + warp] = __popc(mq);
+    const std::uint32_t code = lab[it] - 1u;  // 0..3 for survivors
+    live_b[it] = __ballot_sync(kFull, lab[it] != 0);
+    b0_b[it] = __ballot_sync(kFull, code & 1u);
+    b1_b[it] = __ballot_sync(kFull, code & 2u);
+    if (lane < 4) {
+      const unsigned m0 = (lane & 1) ? b0_b[it] : ~b0_b[it];
+      const unsigned m1 = (lane & 2) ? b1_b[it] : ~b1_b[it];
+      S.off[lane][it * W + warp] = __popc(live_b[it] & m0 & m1);
     }
   }
   __syncthreads();
-  // exclusive scan of each quadrant's SEG counts by warp q
+  // exclusive scan of each quadrant's segment counts by warp q, then the
+  // decoupled look-back across tiles
   if (warp < 4) {
-    constexpr int PER = SEG / 32;
+    constexpr int PER = kK2Seg / 32;
     std::uint32_t c[PER];
     std::uint32_t sum = 0;
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
-      c[r] = s_off[warp][lane * PER + r];
+      c[r] = S.off[warp][lane * PER + r];
       sum += c[r];
     }
     std::uint32_t incl = sum;
@@ -515,7 +581,7 @@ __global__ void __launch_bounds__(kK2Block)
     std::uint32_t run = incl - sum;
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
-      s_off[warp][lane * PER + r] = run;
+      S.off[warp][lane * PER + r] = run;
       run += c[r];
     }
     const std::uint32_t agg = __shfl_sync(kFull, incl, 31);
@@ -528,28 +594,22 @@ __global__ void __launch_bounds__(kK2Block)
       if (lane == 0) st_relaxed(status + warp * ntiles + tile, kFlagP | (excl + agg));
     }
     if (lane == 0) {
-      s_excl[warp] = excl;
-      s_agg[warp] = agg;
+      S.excl[warp] = excl;
       if (last) counts[warp] = excl + agg;
     }
   }
   __syncthreads();
 
-  // scatter survivors in index order: (item, warp, lane)
-  const unsigned lt = (1u << lane) - 1u;
+  // 4) scatter survivors in index order (item, warp, lane): one store each
 #pragma unroll
   for (int it = 0; it < kK2Items; ++it) {
-    const unsigned live = __ballot_sync(kFull, lab[it] != 0);
-    if (!live) continue;
+    if (!live_b[it] || lab[it] == 0) continue;
+    const std::uint32_t q = lab[it] - 1u;
+    const unsigned mine = live_b[it] & ((q & 1u) ? b0_b[it] : ~b0_b[it]) &
+                          ((q & 2u) ? b1_b[it] : ~b1_b[it]);
+    const std::uint64_t pos = S.excl[q] + S.off[q][it * W + warp] + __popc(mine & lt);
     const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const unsigned mq = __ballot_sync(kFull, lab[it] == unsigned(q + 1));
-      if (lab[it] == unsigned(q + 1)) {
-        const std::uint64_t pos = s_excl[q] + s_off[q][it * W + warp] + __popc(mq & lt);
-        if (pos < cap) queues[std::uint64_t(q) * cap + pos] = static_cast<IdxT>(j);
-      }
-    }
+    if (pos < cap) queues[std::uint64_t(q) * cap + pos] = static_cast<IdxT>(j);
   }
 }
 
@@ -623,12 +683,23 @@ void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan,
   check_cuda(cudaMemsetAsync(d_status, 0, k2_status_bytes(ntiles), stream),
              "cudaMemsetAsync(status)");
   const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  constexpr int smem = sizeof(K2Shared);
+  static bool configured = false;  // opt in to > 48 KB dynamic smem once
+  if (!configured) {
+    check_cuda(cudaFuncSetAttribute(k2_filter<std::uint32_t>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+               "cudaFuncSetAttribute");
+    check_cuda(cudaFuncSetAttribute(k2_filter<std::uint64_t>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+               "cudaFuncSetAttribute");
+    configured = true;
+  }
   if (idx_bytes == 4) {
-    k2_filter<std::uint32_t><<<static_cast<unsigned>(ntiles), kK2Block, 0, stream>>>(
+    k2_filter<std::uint32_t><<<static_cast<unsigned>(ntiles), kK2Block, smem, stream>>>(
         pts, n, plan, d_status, ntiles, d_tile_counter,
         static_cast<std::uint32_t*>(d_queues), cap, d_labels, d_counts);
   } else {
-    k2_filter<std::uint64_t><<<static_cast<unsigned>(ntiles), kK2Block, 0, stream>>>(
+    k2_filter<std::uint64_t><<<static_cast<unsigned>(ntiles), kK2Block, smem, stream>>>(
         pts, n, plan, d_status, ntiles, d_tile_counter,
         static_cast<std::uint64_t*>(d_queues), cap, d_labels, d_counts);
   }
