@@ -364,49 +364,41 @@ constexpr std::uint64_t kFlagP = 2ull << 62;  // inclusive prefix published
 constexpr std::uint64_t kValMask = (1ull << 62) - 1;
 constexpr int kK2Warps = kK2Block / 32;
 constexpr int kK2Seg = kK2Items * kK2Warps;  // (item, warp) segments of a tile
+constexpr int kK2Stage = 128;  // staged hard points per warp (half its items)
 
 // orientation(a, b, p) < 0 with the edge constants A = fl(b.x-a.x),
 // C = fl(b.y-a.y): det = fl(fl(A*fl(p.y-a.y)) - fl(C*fl(p.x-a.x))) is
 // negative exactly when the first rounded product is below the second
 // (geometry.hpp:27-32).
-__device__ __forceinline__ bool right_of(double px, double py, const double4& e) {
+__device__ __forceinline__ bool right_of(double px, double py, double4 e) {
   return __dmul_rn(e.z, __dsub_rn(py, e.y)) < __dmul_rn(e.w, __dsub_rn(px, e.x));
 }
 
 struct K2Shared {
-  double4 edge[8];    // octagon edges {a.x, a.y, A, C}
-  double4 qedge[4];   // find_queue edges E->N, N->W, W->S, S->E
-  std::uint8_t facing[16];
   std::uint32_t tile;
   std::uint32_t off[4][kK2Seg];
   std::uint64_t excl[4];
-  // per warp: the warp's hard points, densely packed, and their labels
-  double2 stage[kK2Warps][kK2Items * 32];
-  std::uint8_t code[kK2Warps][kK2Items * 32];
+  // per warp: up to kK2Stage of the warp's points outside the certified
+  // box, densely packed, then their labels
+  double2 stage[kK2Warps][kK2Stage];
+  std::uint8_t lab[kK2Warps][kK2Stage];
 };
 
 // Full classification of a point outside the certified box: the octagon test
-// (filter.cpp:125-128, geometry.cpp:16-22) starting at the edge that faces
-// the point's side of the box (any order yields the same "some edge < 0"),
-// then find_queue in its fixed order (filter.cpp:94-101).
-__device__ __forceinline__ std::uint32_t classify_hard(const K2Shared& S, int m, double2 p,
-                                                       int code) {
-  if (m >= 3) {
-    int e = S.facing[code];
-    bool out = false;
-    for (int k = 0; k < m; ++k) {
-      if (right_of(p.x, p.y, S.edge[e])) {
-        out = true;
-        break;
-      }
-      e = (e + 1 == m) ? 0 : e + 1;
-    }
-    if (!out) return 0;
-  }
+// (filter.cpp:125-128, geometry.cpp:16-22; "some edge < 0" in any order, so
+// all edges are evaluated branch-free with warp-uniform constants) and then
+// find_queue in its fixed first-match order (filter.cpp:94-101).
+__device__ __forceinline__ std::uint32_t classify_hard(const KPlan& P, double2 p) {
+  bool out = P.m < 3;  // degenerate octagon filters nothing (filter.cpp:125)
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (right_of(p.x, p.y, S.qedge[q])) return q + 1;
-  return 1;
+  for (int e = 0; e < 8; ++e)
+    out |= right_of(p.x, p.y, make_double4(P.ax[e], P.ay[e], P.ea[e], P.ec[e]));
+  if (!out) return 0;
+  std::uint32_t q = 1;  // default queue (filter.cpp:101)
+#pragma unroll
+  for (int k = 3; k >= 0; --k)  // the lowest matching edge wins
+    if (right_of(p.x, p.y, make_double4(P.qax[k], P.qay[k], P.qa[k], P.qc[k]))) q = k + 1;
+  return q;
 }
 
 // One warp walks back over predecessor tiles' status words of one quadrant
@@ -439,7 +431,7 @@ __device__ __forceinline__ std::uint64_t look_back(const std::uint64_t* st,
 }
 
 template <typename IdxT>
-__global__ void __launch_bounds__(kK2Block)
+__global__ void __launch_bounds__(kK2Block, 4)
     k2_filter(const double2* __restrict__ pts, std::uint64_t n,
               const __grid_constant__ KPlan plan, std::uint64_t* status,
               std::uint64_t ntiles, unsigned* tile_counter, IdxT* queues,
@@ -452,80 +444,95 @@ __global__ void __launch_bounds__(kK2Block)
   const unsigned lt = (1u << lane) - 1u;
 
   if (threadIdx.x == 0) S.tile = atomicAdd(tile_counter, 1u);
-  if (threadIdx.x < 8)
-    S.edge[threadIdx.x] = make_double4(plan.ax[threadIdx.x], plan.ay[threadIdx.x],
-                                       plan.ea[threadIdx.x], plan.ec[threadIdx.x]);
-  else if (threadIdx.x < 12)
-    S.qedge[threadIdx.x - 8] = make_double4(plan.qax[threadIdx.x - 8], plan.qay[threadIdx.x - 8],
-                                            plan.qa[threadIdx.x - 8], plan.qc[threadIdx.x - 8]);
-  else if (threadIdx.x < 28)
-    S.facing[threadIdx.x - 12] = plan.facing[threadIdx.x - 12];
   __syncthreads();
   const std::uint64_t tile = S.tile;
   const std::uint64_t t0 = tile * kK2Tile;
+  const bool full = t0 + kK2Tile <= n;  // block-uniform: only the last tile is ragged
 
   double2 v[kK2Items];
+  if (full) {
 #pragma unroll
-  for (int it = 0; it < kK2Items; ++it) {
-    const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
-    v[it] = j < n ? ld_stream(pts + j) : make_double2(0.0, 0.0);
+    for (int it = 0; it < kK2Items; ++it) v[it] = ld_stream(pts + t0 + it * kK2Block + threadIdx.x);
+  } else {
+#pragma unroll
+    for (int it = 0; it < kK2Items; ++it) {
+      const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
+      v[it] = j < n ? ld_stream(pts + j) : make_double2(0.0, 0.0);
+    }
   }
 
   bool has_kept = false;
 #pragma unroll
   for (int k = 0; k < 8; ++k) has_kept |= (plan.kept[k] - t0) < kK2Tile;
 
-  // 1) kept overrides and the certified box; everything else is "hard"
-  std::uint32_t lab[kK2Items];
-  unsigned hard_ballot[kK2Items];
-  std::uint32_t hbase[kK2Items];
-  std::uint32_t H = 0;
+  // 1) kept overrides and the certified box; everything else is "hard".
+  //    Labels live packed in one register, 4 bits per item.
+  std::uint32_t labs = 0;
+  std::uint32_t hard = 0;  // bit it: item it needs the full test
 #pragma unroll
   for (int it = 0; it < kK2Items; ++it) {
-    const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
-    lab[it] = 0;
-    bool kept = false;
+    const std::uint32_t jl = it * kK2Block + threadIdx.x;  // offset in the tile
+    const bool inbox = v[it].x >= plan.box[0] && v[it].x <= plan.box[1] &&
+                       v[it].y >= plan.box[2] && v[it].y <= plan.box[3];
+    bool h = !inbox && (full || t0 + jl < n);
     if (has_kept) {
+      const std::uint64_t j = t0 + jl;
+      std::uint32_t kl = 0;
 #pragma unroll
       for (int k = 7; k >= 0; --k)  // first match wins (filter.cpp:122-124)
-        if (j == plan.kept[k]) {
-          lab[it] = plan.kept_label[k];
-          kept = true;
-        }
+        if (j == plan.kept[k]) kl = plan.kept_label[k];
+      if (kl) {
+        labs |= kl << (4 * it);
+        h = false;
+      }
     }
-    const bool e = v[it].x > plan.box[1], w = v[it].x < plan.box[0];
-    const bool nn = v[it].y > plan.box[3], s = v[it].y < plan.box[2];
-    const bool hard = j < n && !kept && (e | w | nn | s);
-    hard_ballot[it] = __ballot_sync(kFull, hard);
-    hbase[it] = H;
-    H += __popc(hard_ballot[it]);
-    if (hard) {
-      const std::uint32_t slot = hbase[it] + __popc(hard_ballot[it] & lt);
-      S.stage[warp][slot] = v[it];
-      S.code[warp][slot] = static_cast<std::uint8_t>(e | (nn << 1) | (w << 2) | (s << 3));
-    }
+    hard |= std::uint32_t(h) << it;
   }
 
-  // 2) dense classification of the warp's hard points, 32 at a time
-  if (H) {
-    __syncwarp();
-    for (std::uint32_t slot = lane; slot < H; slot += 32)
-      S.code[warp][slot] = static_cast<std::uint8_t>(
-          classify_hard(S, plan.m, S.stage[warp][slot], S.code[warp][slot]));
-    __syncwarp();
+  // 2) a warp with few hard points packs them into shared memory and
+  //    classifies them 32 at a time, so a few out-of-box lanes do not make
+  //    every item of the warp pay for the full test; a warp with many
+  //    (> kK2Stage, e.g. points on a circle) is dense already and tests
+  //    item by item
+  if (__any_sync(kFull, hard != 0)) {
+    std::uint32_t H = 0;
 #pragma unroll
-    for (int it = 0; it < kK2Items; ++it)
-      if (hard_ballot[it] >> lane & 1u)
-        lab[it] = S.code[warp][hbase[it] + __popc(hard_ballot[it] & lt)];
+    for (int it = 0; it < kK2Items; ++it) H += __popc(__ballot_sync(kFull, hard >> it & 1u));
+    if (H <= kK2Stage) {
+      H = 0;
+#pragma unroll
+      for (int it = 0; it < kK2Items; ++it) {
+        const unsigned hb = __ballot_sync(kFull, hard >> it & 1u);
+        if (hard >> it & 1u) S.stage[warp][H + __popc(hb & lt)] = v[it];
+        H += __popc(hb);
+      }
+      __syncwarp();
+      for (std::uint32_t slot = lane; slot < H; slot += 32)
+        S.lab[warp][slot] = static_cast<std::uint8_t>(classify_hard(plan, S.stage[warp][slot]));
+      __syncwarp();
+      H = 0;
+#pragma unroll
+      for (int it = 0; it < kK2Items; ++it) {
+        const unsigned hb = __ballot_sync(kFull, hard >> it & 1u);
+        if (hard >> it & 1u) labs |= std::uint32_t(S.lab[warp][H + __popc(hb & lt)]) << (4 * it);
+        H += __popc(hb);
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < kK2Items; ++it)
+        if (hard >> it & 1u) labs |= classify_hard(plan, v[it]) << (4 * it);
+    }
   }
+#define LAB(it) ((labs >> (4 * (it))) & 0xFu)
 
-  std::uint32_t any = 0;
+  if (labels != nullptr) {
 #pragma unroll
-  for (int it = 0; it < kK2Items; ++it) {
-    any |= lab[it];
-    const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
-    if (labels != nullptr && j < n) labels[j] = static_cast<std::uint8_t>(lab[it]);
+    for (int it = 0; it < kK2Items; ++it) {
+      const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
+      if (full || j < n) labels[j] = static_cast<std::uint8_t>(LAB(it));
+    }
   }
+  const std::uint32_t any = labs;
 
   const bool last = tile == ntiles - 1;
   if (!__syncthreads_or(any != 0)) {
@@ -547,17 +554,16 @@ __global__ void __launch_bounds__(kK2Block)
 
   // 3) per (item, warp, quadrant) survivor counts; a lane's own quadrant
   //    mask comes from two ballots of the label bits
-  unsigned live_b[kK2Items], b0_b[kK2Items], b1_b[kK2Items];
 #pragma unroll
   for (int it = 0; it < kK2Items; ++it) {
-    const std::uint32_t code = lab[it] - 1u;  // 0..3 for survivors
-    live_b[it] = __ballot_sync(kFull, lab[it] != 0);
-    b0_b[it] = __ballot_sync(kFull, code & 1u);
-    b1_b[it] = __ballot_sync(kFull, code & 2u);
+    const std::uint32_t code = LAB(it) - 1u;  // 0..3 for survivors
+    const unsigned live = __ballot_sync(kFull, LAB(it) != 0);
+    const unsigned b0 = __ballot_sync(kFull, code & 1u);
+    const unsigned b1 = __ballot_sync(kFull, code & 2u);
     if (lane < 4) {
-      const unsigned m0 = (lane & 1) ? b0_b[it] : ~b0_b[it];
-      const unsigned m1 = (lane & 2) ? b1_b[it] : ~b1_b[it];
-      S.off[lane][it * W + warp] = __popc(live_b[it] & m0 & m1);
+      const unsigned m0 = (lane & 1) ? b0 : ~b0;
+      const unsigned m1 = (lane & 2) ? b1 : ~b1;
+      S.off[lane][it * W + warp] = __popc(live & m0 & m1);
     }
   }
   __syncthreads();
@@ -603,14 +609,18 @@ __global__ void __launch_bounds__(kK2Block)
   // 4) scatter survivors in index order (item, warp, lane): one store each
 #pragma unroll
   for (int it = 0; it < kK2Items; ++it) {
-    if (!live_b[it] || lab[it] == 0) continue;
-    const std::uint32_t q = lab[it] - 1u;
-    const unsigned mine = live_b[it] & ((q & 1u) ? b0_b[it] : ~b0_b[it]) &
-                          ((q & 2u) ? b1_b[it] : ~b1_b[it]);
+    const std::uint32_t q = LAB(it) - 1u;
+    const unsigned live = __ballot_sync(kFull, LAB(it) != 0);
+    if (!live) continue;
+    const unsigned b0 = __ballot_sync(kFull, q & 1u);
+    const unsigned b1 = __ballot_sync(kFull, q & 2u);
+    if (LAB(it) == 0) continue;
+    const unsigned mine = live & ((q & 1u) ? b0 : ~b0) & ((q & 2u) ? b1 : ~b1);
     const std::uint64_t pos = S.excl[q] + S.off[q][it * W + warp] + __popc(mine & lt);
     const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
     if (pos < cap) queues[std::uint64_t(q) * cap + pos] = static_cast<IdxT>(j);
   }
+#undef LAB
 }
 
 template <typename IdxT>
