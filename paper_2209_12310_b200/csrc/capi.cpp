@@ -459,7 +459,7 @@ void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
 
   const std::uint64_t ntiles = (n + kK2Tile - 1) / kK2Tile;
   dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes,
-           k2_status_bytes(ntiles), "look-back status");
+           k2_work_bytes(ntiles), "k2 work area");
   const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
   // queue capacity: a quarter of the shard plus slack; grown and re-run on
   // overflow (counts are exact even when stores are dropped)
@@ -470,10 +470,10 @@ void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
     dev_grow(&c->d_queues, &c->queue_bytes, 4ull * idx_bytes * cap, "queues");
     check_cuda(cudaEventRecord(c->ev[2][0], s), "cudaEventRecord");
     launch_k2(d_xy, n, kp, c->d_status, ntiles, c->d_queues, idx_bytes, cap,
-              d_labels, c->d_counts, s);
+              d_labels, c->d_counts, s);  // k2_filter + k2_compact
     check_cuda(cudaEventRecord(c->ev[2][1], s), "cudaEventRecord");
     c->timed[2] = true;
-    ++c->launches;
+    c->launches += 2;
     check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
     check_cuda(cudaStreamSynchronize(s), "k2_filter");

@@ -47,16 +47,47 @@ void launch_k1(const double* d_xy, std::uint64_t n, std::uint64_t base,
 void launch_k1b(const double* d_xy, std::uint64_t n, std::uint64_t base,
                 const double bbox[4], K1Partial* partials, int grid,
                 unsigned* ticket, ohx_corner_rec* d_out, cudaStream_t stream);
-// K2 scratch: 4*ntiles look-back status words followed by the tile counter.
-inline std::uint64_t k2_status_bytes(std::uint64_t ntiles) {
-  return ntiles * 4 * sizeof(std::uint64_t) + 64;
+// K2 work area: [2 counters | k2_compact look-back words (4 per group of 256
+// tiles) | per-tile queue counts (4 x u32 per tile) | survivor scratch
+// (one 16-bit slot per point)].  Only the first part is cleared per launch.
+constexpr std::uint64_t kK2GroupTiles = 256;
+struct K2Work {
+  unsigned* tile_counter;
+  unsigned* group_counter;
+  std::uint64_t* status;
+  std::uint32_t* tile_counts;
+  std::uint16_t* scratch;
+  std::uint64_t clear_bytes;
+  std::uint64_t total_bytes;
+};
+inline K2Work k2_work_layout(void* base, std::uint64_t ntiles) {
+  const std::uint64_t ngroups = (ntiles + kK2GroupTiles - 1) / kK2GroupTiles;
+  auto* b = static_cast<unsigned char*>(base);
+  K2Work w;
+  std::uint64_t off = 0;
+  w.tile_counter = reinterpret_cast<unsigned*>(b + off);
+  w.group_counter = reinterpret_cast<unsigned*>(b + off + 4);
+  off += 256;
+  w.status = reinterpret_cast<std::uint64_t*>(b + off);
+  off += 4 * ngroups * 8;
+  w.clear_bytes = off;
+  off = (off + 255) & ~std::uint64_t(255);
+  w.tile_counts = reinterpret_cast<std::uint32_t*>(b + off);
+  off += 4 * ntiles * 4;
+  off = (off + 255) & ~std::uint64_t(255);
+  w.scratch = reinterpret_cast<std::uint16_t*>(b + off);
+  off += ntiles * kK2Tile * 2;
+  w.total_bytes = off;
+  return w;
 }
-// K2 (re-arms its scratch with one memset on `stream` first).  d_queues
-// holds 4 queues of `cap` shard-local indices of idx_bytes each.
-void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan,
-               std::uint64_t* d_status, std::uint64_t ntiles, void* d_queues,
-               int idx_bytes, std::uint64_t cap, std::uint8_t* d_labels,
-               unsigned long long* d_counts, cudaStream_t stream);
+inline std::uint64_t k2_work_bytes(std::uint64_t ntiles) {
+  return k2_work_layout(nullptr, ntiles).total_bytes;
+}
+// K2 (k2_filter + k2_compact; re-arms its work area first).  d_queues holds
+// 4 queues of `cap` shard-local indices of idx_bytes each.
+void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_work,
+               std::uint64_t ntiles, void* d_queues, int idx_bytes, std::uint64_t cap,
+               std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream);
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
                     std::uint64_t cap, const std::uint64_t counts[4], double* d_out,
                     cudaStream_t stream);

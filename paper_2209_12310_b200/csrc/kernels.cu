@@ -359,6 +359,18 @@ __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
 }
 
 // ===================================================================== K2 ==
+// Two launches:
+//   k2_filter   labels every point of a 2048-point tile and writes the tile's
+//               survivors, ordered (quadrant, index), as 16-bit tile offsets
+//               into the tile's own slice of a scratch buffer, plus the
+//               tile's four queue counts.  No cross-tile dependency, one
+//               block barrier per tile.
+//   k2_compact  one thread per tile: scans the tile counts (block scan +
+//               decoupled look-back over groups of 256 tiles) and copies each
+//               tile's survivors into the four queues as global indices.
+// Survivors cost 2 B (scratch write) + 2 B (read) + the index write, which is
+// negligible for filtered inputs and keeps the fully-surviving circle case
+// free of per-tile serialisation.
 constexpr std::uint64_t kFlagA = 1ull << 62;  // aggregate published
 constexpr std::uint64_t kFlagP = 2ull << 62;  // inclusive prefix published
 constexpr std::uint64_t kValMask = (1ull << 62) - 1;
@@ -375,42 +387,54 @@ __device__ __forceinline__ bool right_of(double px, double py, double4 e) {
 }
 
 struct K2Shared {
+  double4 edge[12];  // octagon edges 0..7, then find_queue edges E->N, N->W, W->S, S->E
   std::uint32_t tile;
+  std::uint32_t has_kept;
   std::uint32_t off[4][kK2Seg];
-  std::uint64_t excl[4];
+  std::uint32_t qbase[4];
   // per warp: up to kK2Stage of the warp's points outside the certified
   // box, densely packed, then their labels
   double2 stage[kK2Warps][kK2Stage];
   std::uint8_t lab[kK2Warps][kK2Stage];
 };
 
+// Edge constants are re-read from shared memory at every use (volatile):
+// hoisting all twelve edges into registers would spill.
+__device__ __forceinline__ double4 edge_at(const double4* e) {
+  double4 r;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(e))));
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+16];" : "=d"(r.z), "=d"(r.w)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(e))));
+  return r;
+}
+
 // Full classification of a point outside the certified box: the octagon test
 // (filter.cpp:125-128, geometry.cpp:16-22; "some edge < 0" in any order, so
-// all edges are evaluated branch-free with warp-uniform constants) and then
-// find_queue in its fixed first-match order (filter.cpp:94-101).
-__device__ __forceinline__ std::uint32_t classify_hard(const KPlan& P, double2 p) {
-  bool out = P.m < 3;  // degenerate octagon filters nothing (filter.cpp:125)
+// all edges are evaluated branch-free) and then find_queue in its fixed
+// first-match order (filter.cpp:94-101).
+__device__ __forceinline__ std::uint32_t classify_hard(const double4* E, int m, double2 p) {
+  bool out = m < 3;  // degenerate octagon filters nothing (filter.cpp:125)
 #pragma unroll
-  for (int e = 0; e < 8; ++e)
-    out |= right_of(p.x, p.y, make_double4(P.ax[e], P.ay[e], P.ea[e], P.ec[e]));
+  for (int e = 0; e < 8; ++e) out |= right_of(p.x, p.y, edge_at(E + e));
   if (!out) return 0;
   std::uint32_t q = 1;  // default queue (filter.cpp:101)
 #pragma unroll
   for (int k = 3; k >= 0; --k)  // the lowest matching edge wins
-    if (right_of(p.x, p.y, make_double4(P.qax[k], P.qay[k], P.qa[k], P.qc[k]))) q = k + 1;
+    if (right_of(p.x, p.y, edge_at(E + 8 + k))) q = k + 1;
   return q;
 }
 
-// One warp walks back over predecessor tiles' status words of one quadrant
-// and returns the exclusive prefix (decoupled look-back).
+// One warp walks back over predecessor status words of one quadrant and
+// returns the exclusive prefix (decoupled look-back).
 __device__ __forceinline__ std::uint64_t look_back(const std::uint64_t* st,
-                                                   std::uint64_t tile) {
+                                                   std::uint64_t unit) {
   const int lane = threadIdx.x & 31;
   std::uint64_t excl = 0;
-  long long pos = static_cast<long long>(tile) - 1;
+  long long pos = static_cast<long long>(unit) - 1;
   for (;;) {
     const long long at = pos - lane;
-    std::uint64_t w = kFlagP;  // before tile 0: a virtual zero prefix
+    std::uint64_t w = kFlagP;  // before unit 0: a virtual zero prefix
     if (at >= 0) {
       do {
         w = ld_relaxed(st + at);
@@ -430,51 +454,28 @@ __device__ __forceinline__ std::uint64_t look_back(const std::uint64_t* st,
   }
 }
 
-template <typename IdxT>
-__global__ void __launch_bounds__(kK2Block, 4)
-    k2_filter(const double2* __restrict__ pts, std::uint64_t n,
-              const __grid_constant__ KPlan plan, std::uint64_t* status,
-              std::uint64_t ntiles, unsigned* tile_counter, IdxT* queues,
-              std::uint64_t cap, std::uint8_t* labels,
-              unsigned long long* counts) {
-  constexpr int W = kK2Warps;
-  extern __shared__ __align__(16) unsigned char k2_smem[];
-  K2Shared& S = *reinterpret_cast<K2Shared*>(k2_smem);
+template <bool kFull_>
+__device__ __forceinline__ std::uint32_t k2_label_tile(const KPlan& plan, const double2* pts,
+                                                       std::uint64_t n, std::uint64_t t0,
+                                                       bool has_kept, K2Shared& S) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-
-  if (threadIdx.x == 0) S.tile = atomicAdd(tile_counter, 1u);
-  __syncthreads();
-  const std::uint64_t tile = S.tile;
-  const std::uint64_t t0 = tile * kK2Tile;
-  const bool full = t0 + kK2Tile <= n;  // block-uniform: only the last tile is ragged
-
   double2 v[kK2Items];
-  if (full) {
 #pragma unroll
-    for (int it = 0; it < kK2Items; ++it) v[it] = ld_stream(pts + t0 + it * kK2Block + threadIdx.x);
-  } else {
-#pragma unroll
-    for (int it = 0; it < kK2Items; ++it) {
-      const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
-      v[it] = j < n ? ld_stream(pts + j) : make_double2(0.0, 0.0);
-    }
+  for (int it = 0; it < kK2Items; ++it) {
+    const std::uint32_t jl = it * kK2Block + threadIdx.x;
+    v[it] = (kFull_ || t0 + jl < n) ? ld_stream(pts + t0 + jl) : make_double2(0.0, 0.0);
   }
-
-  bool has_kept = false;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) has_kept |= (plan.kept[k] - t0) < kK2Tile;
-
   // 1) kept overrides and the certified box; everything else is "hard".
   //    Labels live packed in one register, 4 bits per item.
   std::uint32_t labs = 0;
   std::uint32_t hard = 0;  // bit it: item it needs the full test
 #pragma unroll
   for (int it = 0; it < kK2Items; ++it) {
-    const std::uint32_t jl = it * kK2Block + threadIdx.x;  // offset in the tile
     const bool inbox = v[it].x >= plan.box[0] && v[it].x <= plan.box[1] &&
                        v[it].y >= plan.box[2] && v[it].y <= plan.box[3];
-    bool h = !inbox && (full || t0 + jl < n);
+    const std::uint32_t jl = it * kK2Block + threadIdx.x;
+    bool h = !inbox && (kFull_ || t0 + jl < n);
     if (has_kept) {
       const std::uint64_t j = t0 + jl;
       std::uint32_t kl = 0;
@@ -488,70 +489,82 @@ __global__ void __launch_bounds__(kK2Block, 4)
     }
     hard |= std::uint32_t(h) << it;
   }
-
-  // 2) a warp with few hard points packs them into shared memory and
-  //    classifies them 32 at a time, so a few out-of-box lanes do not make
-  //    every item of the warp pay for the full test; a warp with many
-  //    (> kK2Stage, e.g. points on a circle) is dense already and tests
-  //    item by item
+  // 2) the warp's hard points are packed into shared memory, four items at
+  //    a time, and classified 32 at a time: a few out-of-box lanes do not
+  //    make every item of the warp pay for the full test, and the full test
+  //    is instantiated once (a rolled loop) instead of per item
   if (__any_sync(kFull, hard != 0)) {
-    std::uint32_t H = 0;
 #pragma unroll
-    for (int it = 0; it < kK2Items; ++it) H += __popc(__ballot_sync(kFull, hard >> it & 1u));
-    if (H <= kK2Stage) {
-      H = 0;
+    for (int half = 0; half < kK2Items / 4; ++half) {
+      std::uint32_t H = 0;
 #pragma unroll
-      for (int it = 0; it < kK2Items; ++it) {
+      for (int it = 4 * half; it < 4 * half + 4; ++it) {
         const unsigned hb = __ballot_sync(kFull, hard >> it & 1u);
         if (hard >> it & 1u) S.stage[warp][H + __popc(hb & lt)] = v[it];
         H += __popc(hb);
       }
+      if (H == 0) continue;
       __syncwarp();
       for (std::uint32_t slot = lane; slot < H; slot += 32)
-        S.lab[warp][slot] = static_cast<std::uint8_t>(classify_hard(plan, S.stage[warp][slot]));
+        S.lab[warp][slot] = static_cast<std::uint8_t>(classify_hard(S.edge, plan.m, S.stage[warp][slot]));
       __syncwarp();
       H = 0;
 #pragma unroll
-      for (int it = 0; it < kK2Items; ++it) {
+      for (int it = 4 * half; it < 4 * half + 4; ++it) {
         const unsigned hb = __ballot_sync(kFull, hard >> it & 1u);
         if (hard >> it & 1u) labs |= std::uint32_t(S.lab[warp][H + __popc(hb & lt)]) << (4 * it);
         H += __popc(hb);
       }
-    } else {
-#pragma unroll
-      for (int it = 0; it < kK2Items; ++it)
-        if (hard >> it & 1u) labs |= classify_hard(plan, v[it]) << (4 * it);
+      __syncwarp();  // the next half reuses the stage
     }
   }
-#define LAB(it) ((labs >> (4 * (it))) & 0xFu)
+  return labs;
+}
 
+template <int kUnused = 0>
+__global__ void __launch_bounds__(kK2Block, 4)
+    k2_filter(const double2* __restrict__ pts, std::uint64_t n,
+              const __grid_constant__ KPlan plan, unsigned* tile_counter,
+              std::uint32_t* tile_counts, std::uint64_t ntiles,
+              std::uint16_t* scratch, std::uint8_t* labels) {
+  constexpr int W = kK2Warps;
+  extern __shared__ __align__(16) unsigned char k2_smem[];
+  K2Shared& S = *reinterpret_cast<K2Shared*>(k2_smem);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+
+  if (threadIdx.x < 8)
+    S.edge[threadIdx.x] = make_double4(plan.ax[threadIdx.x], plan.ay[threadIdx.x],
+                                       plan.ea[threadIdx.x], plan.ec[threadIdx.x]);
+  else if (threadIdx.x < 12)
+    S.edge[threadIdx.x] = make_double4(plan.qax[threadIdx.x - 8], plan.qay[threadIdx.x - 8],
+                                       plan.qa[threadIdx.x - 8], plan.qc[threadIdx.x - 8]);
+  if (threadIdx.x == 32) {
+    const std::uint32_t t = atomicAdd(tile_counter, 1u);
+    S.tile = t;
+    bool hk = false;
+    for (int k = 0; k < 8; ++k) hk |= (plan.kept[k] - std::uint64_t(t) * kK2Tile) < kK2Tile;
+    S.has_kept = hk;
+  }
+  __syncthreads();
+  const std::uint64_t tile = S.tile;
+  const std::uint64_t t0 = tile * kK2Tile;
+  const bool has_kept = S.has_kept;
+  const std::uint32_t labs = (t0 + kK2Tile <= n)
+                                 ? k2_label_tile<true>(plan, pts, n, t0, has_kept, S)
+                                 : k2_label_tile<false>(plan, pts, n, t0, has_kept, S);
+#define LAB(it) ((labs >> (4 * (it))) & 0xFu)
   if (labels != nullptr) {
 #pragma unroll
     for (int it = 0; it < kK2Items; ++it) {
       const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
-      if (full || j < n) labels[j] = static_cast<std::uint8_t>(LAB(it));
+      if (j < n) labels[j] = static_cast<std::uint8_t>(LAB(it));
     }
   }
-  const std::uint32_t any = labs;
-
-  const bool last = tile == ntiles - 1;
-  if (!__syncthreads_or(any != 0)) {
-    // nothing survives here: publish a zero aggregate (a prefix for tile 0)
-    if (threadIdx.x < 4)
-      st_relaxed(status + threadIdx.x * ntiles + tile, tile == 0 ? kFlagP : kFlagA);
-    if (!last) return;
-    // the final tile always resolves its prefix: it reports the counts
-    if (tile == 0) {
-      if (threadIdx.x < 4) counts[threadIdx.x] = 0;
-      return;
-    }
-    if (warp < 4) {
-      const std::uint64_t excl = look_back(status + warp * ntiles, tile);
-      if (lane == 0) counts[warp] = excl;
-    }
+  if (!__syncthreads_or(labs != 0)) {
+    if (threadIdx.x < 4) tile_counts[threadIdx.x * ntiles + tile] = 0;
     return;
   }
-
   // 3) per (item, warp, quadrant) survivor counts; a lane's own quadrant
   //    mask comes from two ballots of the label bits
 #pragma unroll
@@ -567,8 +580,8 @@ __global__ void __launch_bounds__(kK2Block, 4)
     }
   }
   __syncthreads();
-  // exclusive scan of each quadrant's segment counts by warp q, then the
-  // decoupled look-back across tiles
+  // exclusive scan of each quadrant's segment counts (warp q), then the
+  // quadrant bases inside the tile's scratch slice (q-major order)
   if (warp < 4) {
     constexpr int PER = kK2Seg / 32;
     std::uint32_t c[PER];
@@ -590,23 +603,16 @@ __global__ void __launch_bounds__(kK2Block, 4)
       S.off[warp][lane * PER + r] = run;
       run += c[r];
     }
-    const std::uint32_t agg = __shfl_sync(kFull, incl, 31);
-    std::uint64_t excl = 0;
-    if (tile == 0) {
-      if (lane == 0) st_relaxed(status + warp * ntiles, kFlagP | agg);
-    } else {
-      if (lane == 0) st_relaxed(status + warp * ntiles + tile, kFlagA | agg);
-      excl = look_back(status + warp * ntiles, tile);
-      if (lane == 0) st_relaxed(status + warp * ntiles + tile, kFlagP | (excl + agg));
-    }
-    if (lane == 0) {
-      S.excl[warp] = excl;
-      if (last) counts[warp] = excl + agg;
+    if (lane == 31) {
+      tile_counts[warp * ntiles + tile] = incl;
+      S.qbase[warp] = incl;  // the quadrant total, turned into a base below
     }
   }
   __syncthreads();
-
-  // 4) scatter survivors in index order (item, warp, lane): one store each
+  const std::uint32_t tot0 = S.qbase[0], tot1 = S.qbase[1], tot2 = S.qbase[2];
+  const std::uint32_t tot01 = tot0 + tot1, tot012 = tot01 + tot2;
+  std::uint16_t* slice = scratch + t0;
+  // 4) scatter survivors in (quadrant, index) order: one 16-bit store each
 #pragma unroll
   for (int it = 0; it < kK2Items; ++it) {
     const std::uint32_t q = LAB(it) - 1u;
@@ -616,11 +622,89 @@ __global__ void __launch_bounds__(kK2Block, 4)
     const unsigned b1 = __ballot_sync(kFull, q & 2u);
     if (LAB(it) == 0) continue;
     const unsigned mine = live & ((q & 1u) ? b0 : ~b0) & ((q & 2u) ? b1 : ~b1);
-    const std::uint64_t pos = S.excl[q] + S.off[q][it * W + warp] + __popc(mine & lt);
-    const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
-    if (pos < cap) queues[std::uint64_t(q) * cap + pos] = static_cast<IdxT>(j);
+    const std::uint32_t qb = q == 0 ? 0u : (q == 1 ? tot0 : (q == 2 ? tot01 : tot012));
+    const std::uint32_t pos = qb + S.off[q][it * W + warp] + __popc(mine & lt);
+    slice[pos] = static_cast<std::uint16_t>(it * kK2Block + threadIdx.x);
   }
 #undef LAB
+}
+
+constexpr int kK2cBlock = static_cast<int>(kK2GroupTiles);  // tiles per compaction block
+
+template <typename IdxT>
+__global__ void __launch_bounds__(kK2cBlock)
+    k2_compact(const std::uint32_t* __restrict__ tile_counts, std::uint64_t ntiles,
+               const std::uint16_t* __restrict__ scratch, std::uint64_t* status,
+               unsigned* group_counter, IdxT* queues, std::uint64_t cap,
+               unsigned long long* counts) {
+  __shared__ std::uint32_t s_group;
+  __shared__ std::uint64_t s_excl[4];
+  __shared__ std::uint32_t s_cnt[4][kK2cBlock];  // exclusive prefix inside the group
+  __shared__ std::uint32_t s_warp[4][kK2cBlock / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const std::uint64_t ngroups = (ntiles + kK2cBlock - 1) / kK2cBlock;
+  if (threadIdx.x == 0) s_group = atomicAdd(group_counter, 1u);
+  __syncthreads();
+  const std::uint64_t g = s_group;
+  const std::uint64_t tile = g * kK2cBlock + threadIdx.x;
+  std::uint32_t c[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) c[q] = tile < ntiles ? tile_counts[q * ntiles + tile] : 0u;
+  // block-wide exclusive scan of the four counts
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    std::uint32_t incl = c[q];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const std::uint32_t o = __shfl_up_sync(kFull, incl, off);
+      if (lane >= off) incl += o;
+    }
+    if (lane == 31) s_warp[q][warp] = incl;
+    s_cnt[q][threadIdx.x] = incl - c[q];
+  }
+  __syncthreads();
+  if (warp < 4) {
+    const int q = warp;
+    std::uint32_t wsum = lane < kK2cBlock / 32 ? s_warp[q][lane] : 0u;
+    std::uint32_t incl = wsum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const std::uint32_t o = __shfl_up_sync(kFull, incl, off);
+      if (lane >= off) incl += o;
+    }
+    if (lane < kK2cBlock / 32) s_warp[q][lane] = incl - wsum;
+    const std::uint64_t agg = __shfl_sync(kFull, incl, 31);
+    std::uint64_t excl = 0;
+    if (g == 0) {
+      if (lane == 0) st_relaxed(status + q * ngroups, kFlagP | agg);
+    } else {
+      if (lane == 0) st_relaxed(status + q * ngroups + g, kFlagA | agg);
+      excl = look_back(status + q * ngroups, g);
+      if (lane == 0) st_relaxed(status + q * ngroups + g, kFlagP | (excl + agg));
+    }
+    if (lane == 0) {
+      s_excl[q] = excl;
+      if (g == ngroups - 1) counts[q] = excl + agg;
+    }
+  }
+  __syncthreads();
+  // each warp copies the survivors of its 32 tiles, one tile at a time
+  for (int k = 0; k < 32; ++k) {
+    const int tl = warp * 32 + k;
+    const std::uint64_t t = g * kK2cBlock + tl;
+    if (t >= ntiles) break;
+    const std::uint16_t* slice = scratch + t * kK2Tile;
+    std::uint32_t src = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const std::uint32_t cnt = __shfl_sync(kFull, c[q], k);
+      const std::uint64_t dst = s_excl[q] + s_warp[q][warp] + s_cnt[q][tl];
+      IdxT* out = queues + std::uint64_t(q) * cap;
+      for (std::uint32_t e = lane; e < cnt; e += 32)
+        if (dst + e < cap) out[dst + e] = static_cast<IdxT>(t * kK2Tile + slice[src + e]);
+      src += cnt;
+    }
+  }
 }
 
 template <typename IdxT>
@@ -683,37 +767,34 @@ void launch_k1b(const double* d_xy, std::uint64_t n, std::uint64_t base,
   check_cuda(cudaGetLastError(), "k1b_corners launch");
 }
 
-void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan,
-               std::uint64_t* d_status, std::uint64_t ntiles, void* d_queues,
-               int idx_bytes, std::uint64_t cap, std::uint8_t* d_labels,
-               unsigned long long* d_counts, cudaStream_t stream) {
-  // the tile counter lives right after the 4*ntiles status words, so one
-  // memset re-arms both (the allocation holds k2_status_bytes(ntiles))
-  auto* d_tile_counter = reinterpret_cast<unsigned*>(d_status + 4 * ntiles);
-  check_cuda(cudaMemsetAsync(d_status, 0, k2_status_bytes(ntiles), stream),
-             "cudaMemsetAsync(status)");
+void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_work,
+               std::uint64_t ntiles, void* d_queues, int idx_bytes, std::uint64_t cap,
+               std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream) {
+  const K2Work w = k2_work_layout(d_work, ntiles);
+  // re-arm the two work counters and the look-back words of k2_compact
+  check_cuda(cudaMemsetAsync(d_work, 0, w.clear_bytes, stream), "cudaMemsetAsync(k2 work)");
   const auto* pts = reinterpret_cast<const double2*>(d_xy);
   constexpr int smem = sizeof(K2Shared);
   static bool configured = false;  // opt in to > 48 KB dynamic smem once
   if (!configured) {
-    check_cuda(cudaFuncSetAttribute(k2_filter<std::uint32_t>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-               "cudaFuncSetAttribute");
-    check_cuda(cudaFuncSetAttribute(k2_filter<std::uint64_t>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+    check_cuda(cudaFuncSetAttribute(k2_filter<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem),
                "cudaFuncSetAttribute");
     configured = true;
   }
-  if (idx_bytes == 4) {
-    k2_filter<std::uint32_t><<<static_cast<unsigned>(ntiles), kK2Block, smem, stream>>>(
-        pts, n, plan, d_status, ntiles, d_tile_counter,
-        static_cast<std::uint32_t*>(d_queues), cap, d_labels, d_counts);
-  } else {
-    k2_filter<std::uint64_t><<<static_cast<unsigned>(ntiles), kK2Block, smem, stream>>>(
-        pts, n, plan, d_status, ntiles, d_tile_counter,
-        static_cast<std::uint64_t*>(d_queues), cap, d_labels, d_counts);
-  }
+  k2_filter<0><<<static_cast<unsigned>(ntiles), kK2Block, smem, stream>>>(
+      pts, n, plan, w.tile_counter, w.tile_counts, ntiles, w.scratch, d_labels);
   check_cuda(cudaGetLastError(), "k2_filter launch");
+  const unsigned ngroups = static_cast<unsigned>((ntiles + kK2cBlock - 1) / kK2cBlock);
+  if (idx_bytes == 4)
+    k2_compact<std::uint32_t><<<ngroups, kK2cBlock, 0, stream>>>(
+        w.tile_counts, ntiles, w.scratch, w.status, w.group_counter,
+        static_cast<std::uint32_t*>(d_queues), cap, d_counts);
+  else
+    k2_compact<std::uint64_t><<<ngroups, kK2cBlock, 0, stream>>>(
+        w.tile_counts, ntiles, w.scratch, w.status, w.group_counter,
+        static_cast<std::uint64_t*>(d_queues), cap, d_counts);
+  check_cuda(cudaGetLastError(), "k2_compact launch");
 }
 
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
