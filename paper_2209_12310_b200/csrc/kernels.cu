@@ -639,7 +639,9 @@ __global__ void __launch_bounds__(kK2cBlock)
                unsigned long long* counts) {
   __shared__ std::uint32_t s_group;
   __shared__ std::uint64_t s_excl[4];
-  __shared__ std::uint32_t s_cnt[4][kK2cBlock];  // exclusive prefix inside the group
+  __shared__ std::uint32_t s_tot[4];
+  __shared__ std::uint32_t s_pre[4][kK2cBlock];  // group-level exclusive prefix per tile
+  __shared__ std::uint16_t s_src[4][kK2cBlock];  // quadrant offset inside each tile slice
   __shared__ std::uint32_t s_warp[4][kK2cBlock / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const std::uint64_t ngroups = (ntiles + kK2cBlock - 1) / kK2cBlock;
@@ -650,7 +652,12 @@ __global__ void __launch_bounds__(kK2cBlock)
   std::uint32_t c[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) c[q] = tile < ntiles ? tile_counts[q * ntiles + tile] : 0u;
-  // block-wide exclusive scan of the four counts
+  s_src[0][threadIdx.x] = 0;
+  s_src[1][threadIdx.x] = static_cast<std::uint16_t>(c[0]);
+  s_src[2][threadIdx.x] = static_cast<std::uint16_t>(c[0] + c[1]);
+  s_src[3][threadIdx.x] = static_cast<std::uint16_t>(c[0] + c[1] + c[2]);
+  // block-wide exclusive scan of the four counts: warp scans ...
+  std::uint32_t wex[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     std::uint32_t incl = c[q];
@@ -660,12 +667,13 @@ __global__ void __launch_bounds__(kK2cBlock)
       if (lane >= off) incl += o;
     }
     if (lane == 31) s_warp[q][warp] = incl;
-    s_cnt[q][threadIdx.x] = incl - c[q];
+    wex[q] = incl - c[q];
   }
   __syncthreads();
+  // ... then the warp totals (warp q), and the look-back across groups
   if (warp < 4) {
     const int q = warp;
-    std::uint32_t wsum = lane < kK2cBlock / 32 ? s_warp[q][lane] : 0u;
+    const std::uint32_t wsum = lane < kK2cBlock / 32 ? s_warp[q][lane] : 0u;
     std::uint32_t incl = wsum;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -673,7 +681,7 @@ __global__ void __launch_bounds__(kK2cBlock)
       if (lane >= off) incl += o;
     }
     if (lane < kK2cBlock / 32) s_warp[q][lane] = incl - wsum;
-    const std::uint64_t agg = __shfl_sync(kFull, incl, 31);
+    const std::uint32_t agg = __shfl_sync(kFull, incl, 31);
     std::uint64_t excl = 0;
     if (g == 0) {
       if (lane == 0) st_relaxed(status + q * ngroups, kFlagP | agg);
@@ -684,25 +692,32 @@ __global__ void __launch_bounds__(kK2cBlock)
     }
     if (lane == 0) {
       s_excl[q] = excl;
+      s_tot[q] = agg;
       if (g == ngroups - 1) counts[q] = excl + agg;
     }
   }
   __syncthreads();
-  // each warp copies the survivors of its 32 tiles, one tile at a time
-  for (int k = 0; k < 32; ++k) {
-    const int tl = warp * 32 + k;
-    const std::uint64_t t = g * kK2cBlock + tl;
-    if (t >= ntiles) break;
-    const std::uint16_t* slice = scratch + t * kK2Tile;
-    std::uint32_t src = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const std::uint32_t cnt = __shfl_sync(kFull, c[q], k);
-      const std::uint64_t dst = s_excl[q] + s_warp[q][warp] + s_cnt[q][tl];
-      IdxT* out = queues + std::uint64_t(q) * cap;
-      for (std::uint32_t e = lane; e < cnt; e += 32)
-        if (dst + e < cap) out[dst + e] = static_cast<IdxT>(t * kK2Tile + slice[src + e]);
-      src += cnt;
+  for (int q = 0; q < 4; ++q) s_pre[q][threadIdx.x] = s_warp[q][warp] + wex[q];
+  __syncthreads();
+  // flattened copy: survivor k of quadrant q in this group lives in the tile
+  // found by binary search over the prefix, so all loads are independent
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    const std::uint32_t total = s_tot[q];
+    IdxT* out = queues + std::uint64_t(q) * cap + s_excl[q];
+    const std::uint64_t room = cap > s_excl[q] ? cap - s_excl[q] : 0;
+    for (std::uint32_t k = threadIdx.x; k < total; k += kK2cBlock) {
+      int lo = 0, hi = kK2cBlock - 1;  // the last tile whose prefix is <= k
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_pre[q][mid] <= k) lo = mid;
+        else hi = mid - 1;
+      }
+      const std::uint64_t t = g * kK2cBlock + lo;
+      const std::uint32_t e = k - s_pre[q][lo];
+      if (k < room)
+        out[k] = static_cast<IdxT>(t * kK2Tile + scratch[t * kK2Tile + s_src[q][lo] + e]);
     }
   }
 }
