@@ -47,10 +47,10 @@ void launch_k1(const double* d_xy, std::uint64_t n, std::uint64_t base,
 void launch_k1b(const double* d_xy, std::uint64_t n, std::uint64_t base,
                 const double bbox[4], K1Partial* partials, int grid,
                 unsigned* ticket, ohx_corner_rec* d_out, cudaStream_t stream);
-// K2 work area: [2 counters | k2_compact look-back words (4 per group of 256
+// K2 work area: [2 counters | k2_compact look-back words (4 per group of 64
 // tiles) | per-tile queue counts (4 x u32 per tile) | survivor scratch
 // (one 16-bit slot per point)].  Only the first part is cleared per launch.
-constexpr std::uint64_t kK2GroupTiles = 256;
+constexpr std::uint64_t kK2GroupTiles = 64;
 struct K2Work {
   unsigned* tile_counter;
   unsigned* group_counter;

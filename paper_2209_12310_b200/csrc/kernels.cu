@@ -629,7 +629,8 @@ __global__ void __launch_bounds__(kK2Block, 4)
 #undef LAB
 }
 
-constexpr int kK2cBlock = static_cast<int>(kK2GroupTiles);  // tiles per compaction block
+constexpr int kK2cBlock = 256;  // threads per compaction block
+constexpr int kK2cTiles = static_cast<int>(kK2GroupTiles);  // tiles per compaction group
 
 template <typename IdxT>
 __global__ void __launch_bounds__(kK2cBlock)
@@ -637,51 +638,45 @@ __global__ void __launch_bounds__(kK2cBlock)
                const std::uint16_t* __restrict__ scratch, std::uint64_t* status,
                unsigned* group_counter, IdxT* queues, std::uint64_t cap,
                unsigned long long* counts) {
+  constexpr int G = kK2cTiles;  // tiles per group: threads [0, G) hold one tile each
+  static_assert(G == 64 && kK2cBlock >= 128, "scan below assumes two warps of tiles");
   __shared__ std::uint32_t s_group;
   __shared__ std::uint64_t s_excl[4];
   __shared__ std::uint32_t s_tot[4];
-  __shared__ std::uint32_t s_pre[4][kK2cBlock];  // group-level exclusive prefix per tile
-  __shared__ std::uint16_t s_src[4][kK2cBlock];  // quadrant offset inside each tile slice
-  __shared__ std::uint32_t s_warp[4][kK2cBlock / 32];
+  __shared__ std::uint32_t s_pre[4][G];  // group-level exclusive prefix per tile
+  __shared__ std::uint16_t s_src[4][G];  // quadrant offset inside each tile slice
+  __shared__ std::uint32_t s_w0[4];      // warp 0's totals
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const std::uint64_t ngroups = (ntiles + kK2cBlock - 1) / kK2cBlock;
+  const std::uint64_t ngroups = (ntiles + G - 1) / G;
   if (threadIdx.x == 0) s_group = atomicAdd(group_counter, 1u);
   __syncthreads();
   const std::uint64_t g = s_group;
-  const std::uint64_t tile = g * kK2cBlock + threadIdx.x;
-  std::uint32_t c[4];
+  if (threadIdx.x < G) {
+    const std::uint64_t tile = g * G + threadIdx.x;
+    std::uint32_t c[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) c[q] = tile < ntiles ? tile_counts[q * ntiles + tile] : 0u;
-  s_src[0][threadIdx.x] = 0;
-  s_src[1][threadIdx.x] = static_cast<std::uint16_t>(c[0]);
-  s_src[2][threadIdx.x] = static_cast<std::uint16_t>(c[0] + c[1]);
-  s_src[3][threadIdx.x] = static_cast<std::uint16_t>(c[0] + c[1] + c[2]);
-  // block-wide exclusive scan of the four counts: warp scans ...
-  std::uint32_t wex[4];
+    for (int q = 0; q < 4; ++q) c[q] = tile < ntiles ? tile_counts[q * ntiles + tile] : 0u;
+    s_src[0][threadIdx.x] = 0;
+    s_src[1][threadIdx.x] = static_cast<std::uint16_t>(c[0]);
+    s_src[2][threadIdx.x] = static_cast<std::uint16_t>(c[0] + c[1]);
+    s_src[3][threadIdx.x] = static_cast<std::uint16_t>(c[0] + c[1] + c[2]);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    std::uint32_t incl = c[q];
+    for (int q = 0; q < 4; ++q) {
+      std::uint32_t incl = c[q];
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const std::uint32_t o = __shfl_up_sync(kFull, incl, off);
-      if (lane >= off) incl += o;
+      for (int off = 1; off < 32; off <<= 1) {
+        const std::uint32_t o = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl += o;
+      }
+      s_pre[q][threadIdx.x] = incl - c[q];  // warp-local for now
+      if (warp == 0 && lane == 31) s_w0[q] = incl;
+      if (warp == 1 && lane == 31) s_tot[q] = incl;  // warp 1's total, fixed up below
     }
-    if (lane == 31) s_warp[q][warp] = incl;
-    wex[q] = incl - c[q];
   }
   __syncthreads();
-  // ... then the warp totals (warp q), and the look-back across groups
   if (warp < 4) {
     const int q = warp;
-    const std::uint32_t wsum = lane < kK2cBlock / 32 ? s_warp[q][lane] : 0u;
-    std::uint32_t incl = wsum;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const std::uint32_t o = __shfl_up_sync(kFull, incl, off);
-      if (lane >= off) incl += o;
-    }
-    if (lane < kK2cBlock / 32) s_warp[q][lane] = incl - wsum;
-    const std::uint32_t agg = __shfl_sync(kFull, incl, 31);
+    const std::uint32_t agg = s_w0[q] + s_tot[q];
     std::uint64_t excl = 0;
     if (g == 0) {
       if (lane == 0) st_relaxed(status + q * ngroups, kFlagP | agg);
@@ -690,15 +685,15 @@ __global__ void __launch_bounds__(kK2cBlock)
       excl = look_back(status + q * ngroups, g);
       if (lane == 0) st_relaxed(status + q * ngroups + g, kFlagP | (excl + agg));
     }
+    // the second warp's tiles come after the first warp's
+    s_pre[q][32 + lane] += s_w0[q];
+    __syncwarp();
     if (lane == 0) {
       s_excl[q] = excl;
       s_tot[q] = agg;
       if (g == ngroups - 1) counts[q] = excl + agg;
     }
   }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < 4; ++q) s_pre[q][threadIdx.x] = s_warp[q][warp] + wex[q];
   __syncthreads();
   // flattened copy: survivor k of quadrant q in this group lives in the tile
   // found by binary search over the prefix, so all loads are independent
@@ -708,13 +703,14 @@ __global__ void __launch_bounds__(kK2cBlock)
     IdxT* out = queues + std::uint64_t(q) * cap + s_excl[q];
     const std::uint64_t room = cap > s_excl[q] ? cap - s_excl[q] : 0;
     for (std::uint32_t k = threadIdx.x; k < total; k += kK2cBlock) {
-      int lo = 0, hi = kK2cBlock - 1;  // the last tile whose prefix is <= k
-      while (lo < hi) {
+      int lo = 0, hi = G - 1;  // the last tile whose prefix is <= k
+#pragma unroll
+      for (int step = 0; step < 6; ++step) {
         const int mid = (lo + hi + 1) >> 1;
         if (s_pre[q][mid] <= k) lo = mid;
         else hi = mid - 1;
       }
-      const std::uint64_t t = g * kK2cBlock + lo;
+      const std::uint64_t t = g * G + lo;
       const std::uint32_t e = k - s_pre[q][lo];
       if (k < room)
         out[k] = static_cast<IdxT>(t * kK2Tile + scratch[t * kK2Tile + s_src[q][lo] + e]);
@@ -800,7 +796,7 @@ void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_w
   k2_filter<0><<<static_cast<unsigned>(ntiles), kK2Block, smem, stream>>>(
       pts, n, plan, w.tile_counter, w.tile_counts, ntiles, w.scratch, d_labels);
   check_cuda(cudaGetLastError(), "k2_filter launch");
-  const unsigned ngroups = static_cast<unsigned>((ntiles + kK2cBlock - 1) / kK2cBlock);
+  const unsigned ngroups = static_cast<unsigned>((ntiles + kK2cTiles - 1) / kK2cTiles);
   if (idx_bytes == 4)
     k2_compact<std::uint32_t><<<ngroups, kK2cBlock, 0, stream>>>(
         w.tile_counts, ntiles, w.scratch, w.status, w.group_counter,
