@@ -320,7 +320,7 @@ def run_b200_arm(a):
     k1_ms, k2_ms = statistics.mean(k1), statistics.mean(k2)
     kern = {
         "k1_extremes": {"ms": k1_ms, "bytes": 16 * n},
-        "k2_filter": {"ms": k2_ms, "bytes": 16 * n + 4 * s_local},
+        "k2_filter_compact": {"ms": k2_ms, "bytes": 16 * n + 4 * s_local},
     }
     for v in kern.values():
         v["gbs"] = v["bytes"] / (v["ms"] * 1e-3) / 1e9
