@@ -191,7 +191,7 @@ void fit_box(const double* oct, int m, const double* ea, const double* ec,
   double b[4] = {cx - 1e-9 * hx, cx + 1e-9 * hx, cy - 1e-9 * hy, cy + 1e-9 * hy};
   if (!ok(b)) return;  // sliver octagon: no certified box, every point takes the full test
   double lo = 0, hi = 1;
-  for (int it = 0; it < 40; ++it) {
+  for (int it = 0; it < 24; ++it) {
     const double s = (lo + hi) / 2;
     const double t[4] = {cx - s * hx, cx + s * hx, cy - s * hy, cy + s * hy};
     if (ok(t)) lo = s;
@@ -206,12 +206,12 @@ void fit_box(const double* oct, int m, const double* ea, const double* ec,
   //    corner early (a greedy one-side-at-a-time push gets stuck on
   //    near-flat octagon edges); the last round takes the full step
   const double lim[4] = {vx0, vx1, vy0, vy1};
-  constexpr int kRounds = 10;
+  constexpr int kRounds = 6;
   for (int round = 0; round < kRounds; ++round) {
     const double step = round == kRounds - 1 ? 1.0 : 0.6;
     for (int side = 0; side < 4; ++side) {
       double good = b[side], bad = lim[side];
-      for (int it = 0; it < 32; ++it) {
+      for (int it = 0; it < 20; ++it) {
         double t[4] = {b[0], b[1], b[2], b[3]};
         t[side] = (good + bad) / 2;
         if (ok(t)) good = t[side];

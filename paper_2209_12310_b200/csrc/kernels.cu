@@ -263,18 +263,26 @@ __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
                 ohx_extremes_rec* out) {
   ArgState<8, 4, IdxT> ts;
   ts.init();
-  const IdxT stride = static_cast<IdxT>(gridDim.x) * kK1Block;
-  IdxT j = static_cast<IdxT>(blockIdx.x) * kK1Block + threadIdx.x;
-  const IdxT nn = static_cast<IdxT>(n);
-  // j + (U-1)*stride cannot wrap: the grid never exceeds n/U threads
-  for (; j + (kK1Unroll - 1) * stride < nn; j += kK1Unroll * stride) {
-    double2 v[kK1Unroll];
+  // each block streams one contiguous range of 2048-point chunks (32 KB of
+  // consecutive addresses per block step, 8 loads in flight per thread)
+  constexpr std::uint64_t kChunk = std::uint64_t(kK1Block) * kK1Unroll;
+  const std::uint64_t nchunks = (n + kChunk - 1) / kChunk;
+  const std::uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+  const std::uint64_t c_end = min(nchunks, (blockIdx.x + 1) * per);
+  for (std::uint64_t c = blockIdx.x * per; c < c_end; ++c) {
+    const IdxT j0 = static_cast<IdxT>(c * kChunk + threadIdx.x);
+    if ((c + 1) * kChunk <= n) {
+      double2 v[kK1Unroll];
 #pragma unroll
-    for (int u = 0; u < kK1Unroll; ++u) v[u] = ld_stream(pts + j + u * stride);
+      for (int u = 0; u < kK1Unroll; ++u) v[u] = ld_stream(pts + j0 + u * kK1Block);
 #pragma unroll
-    for (int u = 0; u < kK1Unroll; ++u) K1Visit::visit(ts, v[u], IdxT(j + u * stride));
+      for (int u = 0; u < kK1Unroll; ++u) K1Visit::visit(ts, v[u], IdxT(j0 + u * kK1Block));
+    } else {
+      for (int u = 0; u < kK1Unroll; ++u)
+        if (std::uint64_t(j0) + u * kK1Block < n)
+          K1Visit::visit(ts, ld_stream(pts + j0 + u * kK1Block), IdxT(j0 + u * kK1Block));
+    }
   }
-  for (; j < nn; j += stride) K1Visit::visit(ts, ld_stream(pts + j), j);
 
   ArgState<8, 4> st = widen(ts);
   block_reduce<8, 4, kK1Block>(st);
@@ -762,7 +770,7 @@ void launch_k1(const double* d_xy, std::uint64_t n, std::uint64_t base,
   const auto* pts = reinterpret_cast<const double2*>(d_xy);
   // 32-bit in-loop indices whenever the shard (plus a full grid stride of
   // overshoot) fits: one SEL per index update instead of two
-  if (n + std::uint64_t(grid) * kK1Block * kK1Unroll < 0xffffffffull)
+  if (n + std::uint64_t(kK1Block) * kK1Unroll < 0xffffffffull)
     k1_extremes<std::uint32_t><<<grid, kK1Block, 0, stream>>>(pts, n, base, partials, ticket, d_out);
   else
     k1_extremes<std::uint64_t><<<grid, kK1Block, 0, stream>>>(pts, n, base, partials, ticket, d_out);
