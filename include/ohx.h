@@ -105,8 +105,6 @@ typedef struct {
   double box[4];         /* certified interior box xlo,xhi,ylo,yhi (empty if xlo>xhi) */
   uint64_t kept[8];      /* kept indices in override order E,NE,N,NW,W,SW,S,SE */
   uint8_t kept_label[8]; /* 1,1,2,2,3,3,4,4 */
-  uint8_t facing[16];    /* per box-side code (bit0 E, bit1 N, bit2 W, bit3 S):
-                            the octagon edge facing that side, tested first */
   int32_t m;             /* octagon vertices; < 3 = degenerate (filter nothing) */
   int32_t pad;
 } ohx_filter_plan;
@@ -127,6 +125,14 @@ int ohx_ctx_default(int device, ohx_ctx** out);
 int ohx_ctx_device(const ohx_ctx* ctx);
 /* Kernels launched by this context since creation (evidence counter). */
 uint64_t ohx_ctx_launches(const ohx_ctx* ctx);
+/* How the last pipeline-level call on this context ran. */
+typedef struct {
+  uint32_t fused;       /* 1: single pass (KF) + K2 on the candidates only */
+  uint32_t corner_pass; /* 1: the corner certificate failed and K1b ran */
+  uint64_t candidates;  /* points K2 examined in fused mode */
+  uint64_t counts[4];   /* queue lengths */
+} ohx_run_info;
+int ohx_ctx_last_run(const ohx_ctx* ctx, ohx_run_info* info);
 /* Device duration (CUDA events on the launching stream) of the last launch
  * of K1, K1b and K2 in this context; -1 for a kernel not yet launched. */
 int ohx_ctx_kernel_ms(ohx_ctx* ctx, double ms[3]);

@@ -21,7 +21,7 @@ import ctypes as C
 import numpy as np
 
 from ._lib import (DISTS, SLOTS, CornerRec, ExtremeSet, ExtremesRec, FilterPlan, OhxError,
-                   check, lib)
+                   RunInfo, check, lib)
 
 __all__ = ["classify", "filter_rate", "generate", "heaphull", "monotone_chain",
            "heaphull_run", "find_extremes", "Context", "OhxError", "device_count"]
@@ -181,6 +181,14 @@ class Context:
         out = (C.c_double * 3)()
         check(lib.ohx_ctx_kernel_ms(self.h, out))
         return {"k1": out[0], "k1b": out[1], "k2": out[2]}
+
+    def last_run(self) -> dict:
+        """How the last pipeline call on this context ran (fused single pass
+        or two passes, corner fallback, candidates, queue lengths)."""
+        r = RunInfo()
+        check(lib.ohx_ctx_last_run(self.h, C.byref(r)))
+        return {"fused": bool(r.fused), "corner_pass": bool(r.corner_pass),
+                "candidates": int(r.candidates), "counts": [int(v) for v in r.counts]}
 
     # ---- kernel level --------------------------------------------------
     def extremes(self, d_xy, n: int, index_base: int = 0, stream=None) -> ExtremesRec:

@@ -44,14 +44,18 @@ class ExtremeSet(C.Structure):
     _fields_ = [("ext", _u64 * 8), ("x", C.c_double * 8), ("y", C.c_double * 8)]
 
 
+class RunInfo(C.Structure):
+    _fields_ = [("fused", C.c_uint32), ("corner_pass", C.c_uint32), ("candidates", _u64),
+                ("counts", _u64 * 4)]
+
+
 class FilterPlan(C.Structure):
     _fields_ = [("ax", C.c_double * 8), ("ay", C.c_double * 8),
                 ("ea", C.c_double * 8), ("ec", C.c_double * 8),
                 ("qax", C.c_double * 4), ("qay", C.c_double * 4),
                 ("qa", C.c_double * 4), ("qc", C.c_double * 4),
                 ("box", C.c_double * 4), ("kept", _u64 * 8),
-                ("kept_label", C.c_uint8 * 8), ("facing", C.c_uint8 * 16),
-                ("m", C.c_int32), ("pad", C.c_int32)]
+                ("kept_label", C.c_uint8 * 8), ("m", C.c_int32), ("pad", C.c_int32)]
 
 
 # (name, restype, argtypes) of every entry point declared in include/ohx.h
@@ -65,6 +69,7 @@ PROTOTYPES = [
     ("ohx_ctx_device", C.c_int, [_vp]),
     ("ohx_ctx_launches", _u64, [_vp]),
     ("ohx_ctx_kernel_ms", C.c_int, [_vp, _dp]),
+    ("ohx_ctx_last_run", C.c_int, [_vp, C.POINTER(RunInfo)]),
     ("ohx_extremes", C.c_int, [_vp, _vp, _u64, _u64, C.POINTER(ExtremesRec), _vp]),
     ("ohx_extremes_combine", C.c_int, [C.POINTER(ExtremesRec), C.c_int, C.POINTER(ExtremesRec)]),
     ("ohx_extremes_resolve", C.c_int, [C.POINTER(ExtremesRec), C.POINTER(ExtremeSet),

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -59,6 +60,16 @@ struct ohx_ctx {
   std::uint64_t labels_bytes = 0;
   double* d_gather = nullptr;
   std::uint64_t gather_bytes = 0;
+
+  // fused single-pass mode: sample, candidate list, coverage counter
+  double* d_sample = nullptr;
+  std::uint64_t sample_bytes = 0;
+  void* d_cand = nullptr;
+  std::uint64_t cand_bytes = 0;
+  unsigned long long* d_cnt = nullptr;
+  unsigned long long* h_cnt = nullptr;  // pinned
+
+  ohx_run_info last_run = {};
 
   // CUDA events bracketing the last launch of each kernel (K1, K1b, K2)
   cudaEvent_t ev[3][2] = {};
@@ -414,29 +425,11 @@ void make_plan(const ohx_extreme_set& e, const double* oct, int m,
     p->kept_label[k] = static_cast<std::uint8_t>(1 + k / 2);
   }
   fit_box(oct, m, p->ea, p->ec, p->box);
-  // facing table: for each combination of box sides a point lies beyond,
-  // the edge whose outward normal (C, -A) best matches that direction
-  for (int code = 0; code < 16; ++code) {
-    const double dx = ((code & 1) ? 1.0 : 0.0) - ((code & 4) ? 1.0 : 0.0);
-    const double dy = ((code & 2) ? 1.0 : 0.0) - ((code & 8) ? 1.0 : 0.0);
-    int best = 0;
-    double best_v = -INFINITY;
-    for (int i = 0; i < (m >= 3 ? m : 0); ++i) {
-      const double len = std::hypot(p->ea[i], p->ec[i]);
-      const double v = len > 0 ? (p->ec[i] * dx - p->ea[i] * dy) / len : -INFINITY;
-      if (v > best_v) {
-        best_v = v;
-        best = i;
-      }
-    }
-    p->facing[code] = static_cast<std::uint8_t>(best);
-  }
 }
 
-void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
-            const ohx_filter_plan& plan, std::uint8_t* d_labels,
-            std::uint64_t counts[4], cudaStream_t s) {
-  if (n == 0) throw std::invalid_argument("classify_points: empty point set");
+namespace {
+
+KPlan make_kplan(const ohx_filter_plan& plan, std::uint64_t base, std::uint64_t n) {
   KPlan kp;
   std::memcpy(kp.ax, plan.ax, sizeof(kp.ax));
   std::memcpy(kp.ay, plan.ay, sizeof(kp.ay));
@@ -452,46 +445,73 @@ void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
     kp.kept[k] = (g >= base && g - base < n) ? g - base : ~0ull;
     kp.kept_label[k] = plan.kept_label[k];
   }
-  std::memcpy(kp.facing, plan.facing, sizeof(kp.facing));
-  for (int code = 0; code < 16; ++code)
-    if (plan.m >= 3 && kp.facing[code] >= plan.m) throw std::invalid_argument("bad facing table");
   kp.m = plan.m;
+  return kp;
+}
 
-  const std::uint64_t ntiles = (n + kK2Tile - 1) / kK2Tile;
-  dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes,
-           k2_work_bytes(ntiles), "k2 work area");
+// K2 over the n points of a shard, or (d_cand != null) over the n_cand
+// candidates listed there (shard-local indices, same width as the queues).
+void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+                 const ohx_filter_plan& plan, std::uint8_t* d_labels, std::uint64_t counts[4],
+                 cudaStream_t s, const void* d_cand, std::uint64_t n_cand) {
+  const KPlan kp = make_kplan(plan, base, n);
+  const std::uint64_t items = d_cand ? n_cand : n;
   const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
-  // queue capacity: a quarter of the shard plus slack; grown and re-run on
-  // overflow (counts are exact even when stores are dropped)
-  std::uint64_t cap = std::min<std::uint64_t>(n, std::max<std::uint64_t>(4096, n / 4 + n / 16));
-  if (c->queue_bytes / (4ull * idx_bytes) > cap)
-    cap = std::min<std::uint64_t>(n, c->queue_bytes / (4ull * idx_bytes));
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    dev_grow(&c->d_queues, &c->queue_bytes, 4ull * idx_bytes * cap, "queues");
-    check_cuda(cudaEventRecord(c->ev[2][0], s), "cudaEventRecord");
-    launch_k2(d_xy, n, kp, c->d_status, ntiles, c->d_queues, idx_bytes, cap,
-              d_labels, c->d_counts, s);  // k2_filter + k2_compact
-    check_cuda(cudaEventRecord(c->ev[2][1], s), "cudaEventRecord");
-    c->timed[2] = true;
-    c->launches += 2;
-    check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
-    check_cuda(cudaStreamSynchronize(s), "k2_filter");
-    std::uint64_t mx = 0;
-    for (int q = 0; q < 4; ++q) {
-      counts[q] = c->h_counts[q];
-      mx = std::max<std::uint64_t>(mx, counts[q]);
+  if (items == 0) {  // no candidates at all
+    for (int q = 0; q < 4; ++q) counts[q] = 0;
+  } else {
+    const std::uint64_t ntiles = (items + kK2Tile - 1) / kK2Tile;
+    dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes,
+             k2_work_bytes(ntiles), "k2 work area");
+    // queue capacity: a quarter of the items plus slack; grown and re-run on
+    // overflow (counts are exact even when stores are dropped)
+    std::uint64_t cap =
+        std::min<std::uint64_t>(items, std::max<std::uint64_t>(4096, items / 4 + items / 16));
+    if (c->queue_bytes / (4ull * idx_bytes) > cap)
+      cap = std::min<std::uint64_t>(items, c->queue_bytes / (4ull * idx_bytes));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      dev_grow(&c->d_queues, &c->queue_bytes, 4ull * idx_bytes * cap, "queues");
+      check_cuda(cudaEventRecord(c->ev[2][0], s), "cudaEventRecord");
+      launch_k2(d_xy, items, kp, c->d_status, ntiles, c->d_queues, idx_bytes, cap, d_labels,
+                c->d_counts, s, d_cand);  // k2_filter + k2_compact
+      check_cuda(cudaEventRecord(c->ev[2][1], s), "cudaEventRecord");
+      c->timed[2] = true;
+      c->launches += 2;
+      check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
+      check_cuda(cudaStreamSynchronize(s), "k2_filter");
+      std::uint64_t mx = 0;
+      for (int q = 0; q < 4; ++q) {
+        counts[q] = c->h_counts[q];
+        mx = std::max<std::uint64_t>(mx, counts[q]);
+      }
+      if (mx <= cap) break;
+      if (attempt == 1) throw Error(OHX_E_INTERNAL, "k2_filter: queue overflow after regrow");
+      cap = std::min<std::uint64_t>(items, mx + mx / 8 + 1024);
     }
-    if (mx <= cap) break;
-    if (attempt == 1) throw Error(OHX_E_INTERNAL, "k2_filter: queue overflow after regrow");
-    cap = std::min<std::uint64_t>(n, mx + mx / 8 + 1024);
+    c->last_cap = cap;
   }
   c->last_xy = d_xy;
   c->last_n = n;
   c->last_base = base;
-  c->last_cap = cap;
   c->last_idx_bytes = idx_bytes;
   for (int q = 0; q < 4; ++q) c->last_counts[q] = counts[q];
+}
+
+}  // namespace
+
+void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+            const ohx_filter_plan& plan, std::uint8_t* d_labels, std::uint64_t counts[4],
+            cudaStream_t s) {
+  if (n == 0) throw std::invalid_argument("classify_points: empty point set");
+  filter_core(c, d_xy, n, base, plan, d_labels, counts, s, nullptr, 0);
+}
+
+bool box_certified(const ohx_filter_plan& plan, const double box[4]) {
+  if (plan.m < 3 || !(box[0] <= box[1]) || !(box[2] <= box[3])) return false;
+  std::vector<EdgeT<long double>> edges;
+  for (int i = 0; i < plan.m; ++i) edges.push_back({plan.ax[i], plan.ay[i], plan.ea[i], plan.ec[i]});
+  return box_ok<long double>(edges, box[0], box[1], box[2], box[3], 8.0L);
 }
 
 void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
@@ -561,11 +581,10 @@ std::vector<P2> device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t 
   return hull_from_queue_points(anchors, qp, f.counts);
 }
 
-FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
-                        std::uint8_t* d_labels, cudaStream_t s) {
-  FilterOut f{};
-  ohx_extremes_rec rec;
-  extremes(c, d_xy, n, 0, &rec, s);
+namespace {
+
+void finish_extremes(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                     const ohx_extremes_rec& rec, FilterOut& f, cudaStream_t s) {
   const std::uint32_t mask = resolve_extremes(rec, &f.ext);
   f.corner_pass = mask != 0;
   if (mask) {
@@ -584,9 +603,142 @@ FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
   }
   f.m = build_octagon(cand, f.oct);
   make_plan(f.ext, f.oct, f.m, &f.plan);
+}
+
+constexpr std::uint64_t kFuseMinPoints = 1ull << 23;  // below: both passes are cheap
+
+// OHX_FUSE: unset/"auto" = fused pass when it pays, "0" = always two passes,
+// "fallback" = run the fused pass but reject its box (exercises the
+// verification-failure path; tests only).
+int fuse_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("OHX_FUSE");
+    if (!e || !*e || std::string(e) == "auto") return 1;
+    if (std::string(e) == "0") return 0;
+    if (std::string(e) == "fallback") return 2;
+    return 1;
+  }();
+  return mode;
+}
+constexpr int kSampleSegs = 256, kSampleLen = 4096;
+constexpr double kFuseMinCoverage = 0.97;
+
+// The provisional box of the fused pass, from a 1M-point sample: the
+// sample's eight extremes -> octagon -> certified box.  Returns false when
+// fusing does not pay (small input, no box, poor sample coverage).
+bool provisional_box(ohx_ctx* c, const double* d_xy, std::uint64_t n, double box[4],
+                     cudaStream_t s) {
+  if (n < kFuseMinPoints || fuse_mode() == 0) return false;
+  const std::uint64_t ns = std::uint64_t(kSampleSegs) * kSampleLen;
+  dev_grow(reinterpret_cast<void**>(&c->d_sample), &c->sample_bytes, ns * 16, "sample");
+  launch_sample(d_xy, n, kSampleSegs, kSampleLen, c->d_sample, s);
+  ++c->launches;
+  ohx_extremes_rec rs;
+  const int grid = k1_grid(c->device, ns);
+  ensure_partials(c, grid);
+  launch_k1(c->d_sample, ns, 0, c->d_partials, grid, c->d_ticket, c->d_rec, s);
+  ++c->launches;
+  check_cuda(cudaMemcpyAsync(&rs, c->d_rec, sizeof(rs), cudaMemcpyDeviceToHost, s),
+             "cudaMemcpyAsync(sample rec)");
+  check_cuda(cudaStreamSynchronize(s), "sample extremes");
+  ohx_extreme_set es;
+  resolve_extremes(rs, &es);  // a heuristic octagon: the diagonal winners need no certificate
+  const int slot[8] = {OHX_EAST, OHX_NE, OHX_NORTH, OHX_NW,
+                       OHX_WEST, OHX_SW, OHX_SOUTH, OHX_SE};
+  double cand[16], oct[16];
+  for (int k = 0; k < 8; ++k) {
+    cand[2 * k] = es.x[slot[k]];
+    cand[2 * k + 1] = es.y[slot[k]];
+  }
+  const int m = build_octagon(cand, oct);
+  if (m < 3) return false;
+  ohx_filter_plan ps;
+  make_plan(es, oct, m, &ps);
+  std::memcpy(box, ps.box, sizeof(ps.box));
+  if (!(box[0] <= box[1])) return false;
+  launch_count_in_box(c->d_sample, ns, box, c->d_cnt, s);
+  ++c->launches;
+  check_cuda(cudaMemcpyAsync(c->h_cnt, c->d_cnt, 8, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
+  check_cuda(cudaStreamSynchronize(s), "sample coverage");
+  return double(*c->h_cnt) >= kFuseMinCoverage * double(ns);
+}
+
+}  // namespace
+
+namespace {
+FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                             std::uint8_t* d_labels, cudaStream_t s);
+}
+
+FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                        std::uint8_t* d_labels, cudaStream_t s) {
+  const FilterOut f = device_filter_impl(c, d_xy, n, d_labels, s);
+  c->last_run.fused = f.fused;
+  c->last_run.corner_pass = f.corner_pass;
+  c->last_run.candidates = f.candidates;
+  for (int q = 0; q < 4; ++q) c->last_run.counts[q] = f.counts[q];
+  return f;
+}
+
+namespace {
+FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                             std::uint8_t* d_labels, cudaStream_t s) {
+  if (n == 0) throw std::invalid_argument("heaphull: empty point set");
+  FilterOut f{};
+  double box[4];
+  if (provisional_box(c, d_xy, n, box, s)) {
+    // ---- fused: one pass for the extremes and the provisional filter
+    const std::uint64_t ntiles = (n + kK2Tile - 1) / kK2Tile;
+    dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes, k2_work_bytes(ntiles),
+             "k2 work area");
+    const int grid = kf_grid(c->device, n);
+    ensure_partials(c, grid);
+    check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
+    launch_kf(d_xy, n, 0, box, c->d_partials, grid, c->d_ticket, c->d_rec, c->d_status, ntiles, s);
+    check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
+    c->timed[0] = true;
+    ++c->launches;
+    check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
+                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec)");
+    check_cuda(cudaStreamSynchronize(s), "kf_extremes_prefilter");
+    const ohx_extremes_rec rec = *c->h_rec;
+    finish_extremes(c, d_xy, n, rec, f, s);
+    // the dropped points are label 0 iff B is certified inside the true
+    // octagon and holds none of the eight kept points
+    bool ok = box_certified(f.plan, box) && fuse_mode() != 2;
+    for (int a = 0; a < 8 && ok; ++a)
+      ok = !(f.ext.x[a] >= box[0] && f.ext.x[a] <= box[1] && f.ext.y[a] >= box[2] &&
+             f.ext.y[a] <= box[3]);
+    if (ok) {
+      const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
+      const std::uint64_t cap = std::max<std::uint64_t>(1u << 20, n / 16);
+      dev_grow(&c->d_cand, &c->cand_bytes, cap * idx_bytes, "candidates");
+      launch_candidates(c->d_status, ntiles, c->d_cand, idx_bytes, cap, c->d_counts, s);
+      ++c->launches;
+      check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
+      check_cuda(cudaStreamSynchronize(s), "candidates");
+      const std::uint64_t n_cand = c->h_counts[0];
+      if (n_cand <= cap) {
+        if (d_labels) check_cuda(cudaMemsetAsync(d_labels, 0, n, s), "cudaMemsetAsync(labels)");
+        filter_core(c, d_xy, n, 0, f.plan, d_labels, f.counts, s, c->d_cand, n_cand);
+        f.fused = true;
+        f.candidates = n_cand;
+        return f;
+      }
+    }
+    // not certified (or too many candidates): the regular second pass
+    filter(c, d_xy, n, 0, f.plan, d_labels, f.counts, s);
+    return f;
+  }
+  // ---- two passes: K1, then K2
+  ohx_extremes_rec rec;
+  extremes(c, d_xy, n, 0, &rec, s);
+  finish_extremes(c, d_xy, n, rec, f, s);
   filter(c, d_xy, n, 0, f.plan, d_labels, f.counts, s);
   return f;
 }
+}  // namespace
 
 ohx_ctx* create_ctx(int device) {
   int ndev = 0;
@@ -611,6 +763,8 @@ ohx_ctx* create_ctx(int device) {
   check_cuda(cudaMallocHost(&c->h_rec, sizeof(ohx_extremes_rec)), "cudaMallocHost");
   check_cuda(cudaMallocHost(&c->h_crec, sizeof(ohx_corner_rec)), "cudaMallocHost");
   check_cuda(cudaMallocHost(&c->h_counts, 64), "cudaMallocHost");
+  check_cuda(cudaMalloc(&c->d_cnt, 64), "cudaMalloc(cnt)");
+  check_cuda(cudaMallocHost(&c->h_cnt, 64), "cudaMallocHost");
   for (auto& pair : c->ev)
     for (auto& e : pair) check_cuda(cudaEventCreate(&e), "cudaEventCreate");
   return c.release();
@@ -624,10 +778,11 @@ void destroy_ctx(ohx_ctx* c) {
                   static_cast<void*>(c->d_rec), static_cast<void*>(c->d_crec),
                   static_cast<void*>(c->d_counts), static_cast<void*>(c->d_status),
                   c->d_queues, static_cast<void*>(c->d_pts),
-                  static_cast<void*>(c->d_labels), static_cast<void*>(c->d_gather)})
+                  static_cast<void*>(c->d_labels), static_cast<void*>(c->d_gather),
+                  static_cast<void*>(c->d_sample), c->d_cand, static_cast<void*>(c->d_cnt)})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_crec),
-                  static_cast<void*>(c->h_counts)})
+                  static_cast<void*>(c->h_counts), static_cast<void*>(c->h_cnt)})
     if (p) cudaFreeHost(p);
   for (auto& pair : c->ev)
     for (auto& e : pair)
@@ -683,6 +838,10 @@ int ohx_ctx_default(int device, ohx_ctx** out) {
 int ohx_ctx_device(const ohx_ctx* ctx) { return ctx ? ctx->device : -1; }
 
 uint64_t ohx_ctx_launches(const ohx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ohx_ctx_last_run(const ohx_ctx* ctx, ohx_run_info* info) {
+  return guard([&] { *info = ctx->last_run; });
+}
 
 int ohx_ctx_kernel_ms(ohx_ctx* ctx, double ms[3]) {
   return guard([&] {

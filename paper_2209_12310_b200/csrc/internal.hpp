@@ -23,7 +23,6 @@ struct KPlan {
   double box[4];
   std::uint64_t kept[8];  // shard-local, ~0 when not in this shard
   std::uint32_t kept_label[8];
-  std::uint8_t facing[16];  // first octagon edge to test per box-side code
   std::int32_t m;
 };
 
@@ -85,9 +84,25 @@ inline std::uint64_t k2_work_bytes(std::uint64_t ntiles) {
 }
 // K2 (k2_filter + k2_compact; re-arms its work area first).  d_queues holds
 // 4 queues of `cap` shard-local indices of idx_bytes each.
+// d_gather (nullable): gather mode over a candidate list of n shard-local
+// indices (same width as the queues); labels are then scattered.
 void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_work,
                std::uint64_t ntiles, void* d_queues, int idx_bytes, std::uint64_t cap,
-               std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream);
+               std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream,
+               const void* d_gather = nullptr);
+// KF: fused extremes + provisional box filter (see kernels.cu).  Re-arms the
+// work area; leaves candidate tile counts/scratch in it.
+int kf_grid(int device, std::uint64_t n);
+void launch_kf(const double* d_xy, std::uint64_t n, std::uint64_t base, const double box[4],
+               K1Partial* partials, int grid, unsigned* ticket, ohx_extremes_rec* d_out,
+               void* d_work, std::uint64_t ntiles, cudaStream_t stream);
+// ordered candidate list from KF's work area (queue 0 of k2_compact)
+void launch_candidates(void* d_work, std::uint64_t ntiles, void* d_cand, int idx_bytes,
+                       std::uint64_t cap, unsigned long long* d_counts, cudaStream_t stream);
+void launch_sample(const double* d_xy, std::uint64_t n, int segs, int len, double* d_sample,
+                   cudaStream_t stream);
+void launch_count_in_box(const double* d_xy, std::uint64_t n, const double box[4],
+                         unsigned long long* d_count, cudaStream_t stream);
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
                     std::uint64_t cap, const std::uint64_t counts[4], double* d_out,
                     cudaStream_t stream);

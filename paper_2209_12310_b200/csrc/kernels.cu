@@ -23,6 +23,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <type_traits>
 
 #include "internal.hpp"
 
@@ -462,17 +463,27 @@ __device__ __forceinline__ std::uint64_t look_back(const std::uint64_t* st,
   }
 }
 
-template <bool kFull_>
+// Gather mode (GIdx != void): the tile's items are the points gidx[t0 + jl]
+// of a candidate list rather than consecutive points.
+template <typename GIdx>
+__device__ __forceinline__ std::uint64_t item_index(const GIdx* gidx, std::uint64_t k) {
+  if constexpr (std::is_void_v<GIdx>) return k;
+  else return static_cast<std::uint64_t>(__ldg(gidx + k));
+}
+
+template <bool kFull_, typename GIdx>
 __device__ __forceinline__ std::uint32_t k2_label_tile(const KPlan& plan, const double2* pts,
-                                                       std::uint64_t n, std::uint64_t t0,
-                                                       bool has_kept, K2Shared& S) {
+                                                       const GIdx* gidx, std::uint64_t n,
+                                                       std::uint64_t t0, bool has_kept,
+                                                       K2Shared& S) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   double2 v[kK2Items];
 #pragma unroll
   for (int it = 0; it < kK2Items; ++it) {
     const std::uint32_t jl = it * kK2Block + threadIdx.x;
-    v[it] = (kFull_ || t0 + jl < n) ? ld_stream(pts + t0 + jl) : make_double2(0.0, 0.0);
+    v[it] = (kFull_ || t0 + jl < n) ? ld_stream(pts + item_index(gidx, t0 + jl))
+                                    : make_double2(0.0, 0.0);
   }
   // 1) kept overrides and the certified box; everything else is "hard".
   //    Labels live packed in one register, 4 bits per item.
@@ -484,8 +495,8 @@ __device__ __forceinline__ std::uint32_t k2_label_tile(const KPlan& plan, const 
                        v[it].y >= plan.box[2] && v[it].y <= plan.box[3];
     const std::uint32_t jl = it * kK2Block + threadIdx.x;
     bool h = !inbox && (kFull_ || t0 + jl < n);
-    if (has_kept) {
-      const std::uint64_t j = t0 + jl;
+    if (has_kept && (kFull_ || t0 + jl < n)) {
+      const std::uint64_t j = item_index(gidx, t0 + jl);
       std::uint32_t kl = 0;
 #pragma unroll
       for (int k = 7; k >= 0; --k)  // first match wins (filter.cpp:122-124)
@@ -529,9 +540,9 @@ __device__ __forceinline__ std::uint32_t k2_label_tile(const KPlan& plan, const 
   return labs;
 }
 
-template <int kUnused = 0>
+template <typename GIdx>
 __global__ void __launch_bounds__(kK2Block, 4)
-    k2_filter(const double2* __restrict__ pts, std::uint64_t n,
+    k2_filter(const double2* __restrict__ pts, const GIdx* __restrict__ gidx, std::uint64_t n,
               const __grid_constant__ KPlan plan, unsigned* tile_counter,
               std::uint32_t* tile_counts, std::uint64_t ntiles,
               std::uint16_t* scratch, std::uint8_t* labels) {
@@ -550,7 +561,7 @@ __global__ void __launch_bounds__(kK2Block, 4)
   if (threadIdx.x == 32) {
     const std::uint32_t t = atomicAdd(tile_counter, 1u);
     S.tile = t;
-    bool hk = false;
+    bool hk = !std::is_void_v<GIdx>;  // gather mode: a candidate may be any point
     for (int k = 0; k < 8; ++k) hk |= (plan.kept[k] - std::uint64_t(t) * kK2Tile) < kK2Tile;
     S.has_kept = hk;
   }
@@ -559,14 +570,14 @@ __global__ void __launch_bounds__(kK2Block, 4)
   const std::uint64_t t0 = tile * kK2Tile;
   const bool has_kept = S.has_kept;
   const std::uint32_t labs = (t0 + kK2Tile <= n)
-                                 ? k2_label_tile<true>(plan, pts, n, t0, has_kept, S)
-                                 : k2_label_tile<false>(plan, pts, n, t0, has_kept, S);
+                                 ? k2_label_tile<true>(plan, pts, gidx, n, t0, has_kept, S)
+                                 : k2_label_tile<false>(plan, pts, gidx, n, t0, has_kept, S);
 #define LAB(it) ((labs >> (4 * (it))) & 0xFu)
   if (labels != nullptr) {
 #pragma unroll
     for (int it = 0; it < kK2Items; ++it) {
       const std::uint64_t j = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
-      if (j < n) labels[j] = static_cast<std::uint8_t>(LAB(it));
+      if (j < n) labels[item_index(gidx, j)] = static_cast<std::uint8_t>(LAB(it));
     }
   }
   if (!__syncthreads_or(labs != 0)) {
@@ -640,12 +651,12 @@ __global__ void __launch_bounds__(kK2Block, 4)
 constexpr int kK2cBlock = 256;  // threads per compaction block
 constexpr int kK2cTiles = static_cast<int>(kK2GroupTiles);  // tiles per compaction group
 
-template <typename IdxT>
+template <typename IdxT, bool kGather>
 __global__ void __launch_bounds__(kK2cBlock)
     k2_compact(const std::uint32_t* __restrict__ tile_counts, std::uint64_t ntiles,
                const std::uint16_t* __restrict__ scratch, std::uint64_t* status,
                unsigned* group_counter, IdxT* queues, std::uint64_t cap,
-               unsigned long long* counts) {
+               unsigned long long* counts, const IdxT* __restrict__ gidx) {
   constexpr int G = kK2cTiles;  // tiles per group: threads [0, G) hold one tile each
   static_assert(G == 64 && kK2cBlock >= 128, "scan below assumes two warps of tiles");
   __shared__ std::uint32_t s_group;
@@ -720,10 +731,158 @@ __global__ void __launch_bounds__(kK2cBlock)
       }
       const std::uint64_t t = g * G + lo;
       const std::uint32_t e = k - s_pre[q][lo];
-      if (k < room)
-        out[k] = static_cast<IdxT>(t * kK2Tile + scratch[t * kK2Tile + s_src[q][lo] + e]);
+      if (k < room) {
+        const std::uint64_t item = t * kK2Tile + scratch[t * kK2Tile + s_src[q][lo] + e];
+        out[k] = kGather ? gidx[item] : static_cast<IdxT>(item);
+      }
     }
   }
+}
+
+// ===================================================================== KF ==
+// Fused single pass (K1 + provisional filter).  While streaming the points
+// for the eight extremes, every point inside a provisional box B (fitted on
+// a sample's octagon before the pass) is dropped and every other point is
+// recorded as a candidate: tile-local 16-bit offsets in the tile's scratch
+// slice plus the tile's candidate count (queue row 0 of the K2 work area).
+// After the pass the host checks that B is certified inside the TRUE
+// octagon (exact edge margins, ohx::box_certified) and contains no kept
+// index; then every dropped point provably has the reference label 0 and
+// only the candidates need the full test (K2 in gather mode).  Otherwise the
+// regular K2 pass runs and nothing from this pass but the extremes is used.
+constexpr int kKFBlock = 256;
+constexpr int kKFMinBlocks = 3;
+
+template <typename IdxT>
+__global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
+    kf_extremes_prefilter(const double2* __restrict__ pts, std::uint64_t n, std::uint64_t base,
+                          double bx0, double bx1, double by0, double by1,
+                          K1Partial* partials, unsigned* ticket, ohx_extremes_rec* out,
+                          unsigned* tile_counter, std::uint32_t* tile_counts,
+                          std::uint64_t ntiles, std::uint16_t* scratch) {
+  static_assert(kKFBlock == kK2Block, "KF tiles are K2 tiles");
+  constexpr int W = kKFBlock / 32;
+  __shared__ std::uint32_t s_tile[2];
+  __shared__ std::uint32_t s_off[kK2Seg];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  ArgState<8, 4, IdxT> ts;
+  ts.init();
+  if (threadIdx.x == 0) s_tile[0] = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  for (int iter = 0;; ++iter) {
+    const std::uint64_t tile = s_tile[iter & 1];
+    if (tile >= ntiles) break;
+    // prefetch the next tile id; the barrier below publishes it
+    if (threadIdx.x == 0) s_tile[(iter + 1) & 1] = atomicAdd(tile_counter, 1u);
+    const std::uint64_t t0 = tile * kK2Tile;
+    const bool full = t0 + kK2Tile <= n;
+    double2 v[kK2Items];
+#pragma unroll
+    for (int it = 0; it < kK2Items; ++it) {
+      const std::uint32_t jl = it * kKFBlock + threadIdx.x;
+      v[it] = (full || t0 + jl < n) ? ld_stream(pts + t0 + jl) : make_double2(0.0, 0.0);
+    }
+    std::uint32_t cand = 0;
+#pragma unroll
+    for (int it = 0; it < kK2Items; ++it) {
+      const std::uint32_t jl = it * kKFBlock + threadIdx.x;
+      const bool valid = full || t0 + jl < n;
+      if (valid) K1Visit::visit(ts, v[it], static_cast<IdxT>(t0 + jl));
+      const bool inbox = v[it].x >= bx0 && v[it].x <= bx1 && v[it].y >= by0 && v[it].y <= by1;
+      cand |= std::uint32_t(valid && !inbox) << it;
+    }
+    if (!__syncthreads_or(cand != 0)) {
+      if (threadIdx.x < 4) tile_counts[threadIdx.x * ntiles + tile] = 0;
+      continue;
+    }
+#pragma unroll
+    for (int it = 0; it < kK2Items; ++it) {
+      const unsigned b = __ballot_sync(kFull, cand >> it & 1u);
+      if (lane == 0) s_off[it * W + warp] = __popc(b);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      constexpr int PER = kK2Seg / 32;
+      std::uint32_t c[PER], sum = 0;
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        c[r] = s_off[lane * PER + r];
+        sum += c[r];
+      }
+      std::uint32_t incl = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const std::uint32_t o = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl += o;
+      }
+      std::uint32_t run = incl - sum;
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        s_off[lane * PER + r] = run;
+        run += c[r];
+      }
+      if (lane == 31) tile_counts[tile] = incl;
+      if (lane >= 1 && lane < 4) tile_counts[lane * ntiles + tile] = 0;
+    }
+    __syncthreads();
+    std::uint16_t* slice = scratch + t0;
+#pragma unroll
+    for (int it = 0; it < kK2Items; ++it) {
+      const unsigned b = __ballot_sync(kFull, cand >> it & 1u);
+      if (cand >> it & 1u)
+        slice[s_off[it * W + warp] + __popc(b & lt)] =
+            static_cast<std::uint16_t>(it * kKFBlock + threadIdx.x);
+    }
+    __syncthreads();  // s_off is reused by the next tile
+  }
+
+  ArgState<8, 4> st = widen(ts);
+  block_reduce<8, 4, kKFBlock>(st);
+  if (!grid_combine<8, 4, kKFBlock>(st, partials, ticket)) return;
+  if (threadIdx.x < 8) {
+    const int a = threadIdx.x;
+    double k = 0, s2 = 0;
+    std::uint64_t i = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (b == a) {
+        k = st.k[b];
+        i = st.i[b];
+        if (b >= 4) s2 = st.s[b - 4];
+      }
+    const double2 p = pts[i];
+    out->key[a] = k;
+    out->idx[a] = base + i;
+    out->x[a] = p.x;
+    out->y[a] = p.y;
+    if (a >= 4) out->second[a - 4] = s2;
+    if (a == 0) out->n = n;
+  }
+}
+
+// A sample for the provisional box: `segs` runs of `len` consecutive points
+// at evenly spaced offsets (coalesced reads, 16 MB for the default 256 x 4096).
+__global__ void gather_sample(const double2* __restrict__ pts, std::uint64_t n, int len,
+                              double2* __restrict__ out) {
+  const std::uint64_t segs = gridDim.x;
+  const std::uint64_t start = (n - len) * blockIdx.x / (segs > 1 ? segs - 1 : 1);
+  for (int k = threadIdx.x; k < len; k += blockDim.x)
+    out[std::uint64_t(blockIdx.x) * len + k] = pts[start + k];
+}
+
+// Number of points of `pts` inside the box (sample coverage estimate).
+__global__ void count_in_box(const double2* __restrict__ pts, std::uint64_t n, double bx0,
+                             double bx1, double by0, double by1, unsigned long long* count) {
+  unsigned c = 0;
+  for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += std::uint64_t(gridDim.x) * blockDim.x) {
+    const double2 p = pts[k];
+    c += p.x >= bx0 && p.x <= bx1 && p.y >= by0 && p.y <= by1;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(kFull, c, off);
+  if ((threadIdx.x & 31) == 0) atomicAdd(count, static_cast<unsigned long long>(c));
 }
 
 template <typename IdxT>
@@ -786,34 +945,114 @@ void launch_k1b(const double* d_xy, std::uint64_t n, std::uint64_t base,
   check_cuda(cudaGetLastError(), "k1b_corners launch");
 }
 
-void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_work,
-               std::uint64_t ntiles, void* d_queues, int idx_bytes, std::uint64_t cap,
-               std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream) {
-  const K2Work w = k2_work_layout(d_work, ntiles);
-  // re-arm the two work counters and the look-back words of k2_compact
-  check_cuda(cudaMemsetAsync(d_work, 0, w.clear_bytes, stream), "cudaMemsetAsync(k2 work)");
-  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+template <typename GIdx>
+static void k2_filter_launch(const double2* pts, const GIdx* gidx, std::uint64_t n,
+                             const KPlan& plan, const K2Work& w, std::uint64_t ntiles,
+                             std::uint8_t* d_labels, cudaStream_t stream) {
   constexpr int smem = sizeof(K2Shared);
-  static bool configured = false;  // opt in to > 48 KB dynamic smem once
+  static bool configured = false;  // opt in to > 48 KB dynamic smem once per instantiation
   if (!configured) {
-    check_cuda(cudaFuncSetAttribute(k2_filter<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    check_cuda(cudaFuncSetAttribute(k2_filter<GIdx>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem),
                "cudaFuncSetAttribute");
     configured = true;
   }
-  k2_filter<0><<<static_cast<unsigned>(ntiles), kK2Block, smem, stream>>>(
-      pts, n, plan, w.tile_counter, w.tile_counts, ntiles, w.scratch, d_labels);
+  k2_filter<GIdx><<<static_cast<unsigned>(ntiles), kK2Block, smem, stream>>>(
+      pts, gidx, n, plan, w.tile_counter, w.tile_counts, ntiles, w.scratch, d_labels);
   check_cuda(cudaGetLastError(), "k2_filter launch");
+}
+
+template <typename IdxT, bool kGather>
+static void k2_compact_launch(const K2Work& w, std::uint64_t ntiles, IdxT* queues,
+                              std::uint64_t cap, unsigned long long* d_counts,
+                              const IdxT* gidx, cudaStream_t stream) {
   const unsigned ngroups = static_cast<unsigned>((ntiles + kK2cTiles - 1) / kK2cTiles);
-  if (idx_bytes == 4)
-    k2_compact<std::uint32_t><<<ngroups, kK2cBlock, 0, stream>>>(
-        w.tile_counts, ntiles, w.scratch, w.status, w.group_counter,
-        static_cast<std::uint32_t*>(d_queues), cap, d_counts);
-  else
-    k2_compact<std::uint64_t><<<ngroups, kK2cBlock, 0, stream>>>(
-        w.tile_counts, ntiles, w.scratch, w.status, w.group_counter,
-        static_cast<std::uint64_t*>(d_queues), cap, d_counts);
+  k2_compact<IdxT, kGather><<<ngroups, kK2cBlock, 0, stream>>>(
+      w.tile_counts, ntiles, w.scratch, w.status, w.group_counter, queues, cap, d_counts, gidx);
   check_cuda(cudaGetLastError(), "k2_compact launch");
+}
+
+void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_work,
+               std::uint64_t ntiles, void* d_queues, int idx_bytes, std::uint64_t cap,
+               std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream,
+               const void* d_gather) {
+  const K2Work w = k2_work_layout(d_work, ntiles);
+  // re-arm the two work counters and the look-back words of k2_compact
+  check_cuda(cudaMemsetAsync(d_work, 0, w.clear_bytes, stream), "cudaMemsetAsync(k2 work)");
+  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  if (idx_bytes == 4) {
+    const auto* g = static_cast<const std::uint32_t*>(d_gather);
+    if (g) k2_filter_launch(pts, g, n, plan, w, ntiles, d_labels, stream);
+    else k2_filter_launch<void>(pts, nullptr, n, plan, w, ntiles, d_labels, stream);
+    auto* q = static_cast<std::uint32_t*>(d_queues);
+    if (g) k2_compact_launch<std::uint32_t, true>(w, ntiles, q, cap, d_counts, g, stream);
+    else k2_compact_launch<std::uint32_t, false>(w, ntiles, q, cap, d_counts, nullptr, stream);
+  } else {
+    const auto* g = static_cast<const std::uint64_t*>(d_gather);
+    if (g) k2_filter_launch(pts, g, n, plan, w, ntiles, d_labels, stream);
+    else k2_filter_launch<void>(pts, nullptr, n, plan, w, ntiles, d_labels, stream);
+    auto* q = static_cast<std::uint64_t*>(d_queues);
+    if (g) k2_compact_launch<std::uint64_t, true>(w, ntiles, q, cap, d_counts, g, stream);
+    else k2_compact_launch<std::uint64_t, false>(w, ntiles, q, cap, d_counts, nullptr, stream);
+  }
+}
+
+int kf_grid(int device, std::uint64_t n) {
+  int sms = 0, per_sm = 0;
+  check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device),
+             "cudaDeviceGetAttribute");
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                 &per_sm, kf_extremes_prefilter<std::uint32_t>, kKFBlock, 0),
+             "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  if (per_sm < 1) per_sm = 1;
+  const std::uint64_t ntiles = (n + kK2Tile - 1) / kK2Tile;
+  const std::uint64_t full = std::uint64_t(sms) * per_sm;
+  return static_cast<int>(ntiles < full ? ntiles : full);
+}
+
+void launch_kf(const double* d_xy, std::uint64_t n, std::uint64_t base, const double box[4],
+               K1Partial* partials, int grid, unsigned* ticket, ohx_extremes_rec* d_out,
+               void* d_work, std::uint64_t ntiles, cudaStream_t stream) {
+  const K2Work w = k2_work_layout(d_work, ntiles);
+  check_cuda(cudaMemsetAsync(d_work, 0, w.clear_bytes, stream), "cudaMemsetAsync(kf work)");
+  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  if (n + kK2Tile < 0xffffffffull)
+    kf_extremes_prefilter<std::uint32_t><<<grid, kKFBlock, 0, stream>>>(
+        pts, n, base, box[0], box[1], box[2], box[3], partials, ticket, d_out, w.tile_counter,
+        w.tile_counts, ntiles, w.scratch);
+  else
+    kf_extremes_prefilter<std::uint64_t><<<grid, kKFBlock, 0, stream>>>(
+        pts, n, base, box[0], box[1], box[2], box[3], partials, ticket, d_out, w.tile_counter,
+        w.tile_counts, ntiles, w.scratch);
+  check_cuda(cudaGetLastError(), "kf_extremes_prefilter launch");
+}
+
+void launch_candidates(void* d_work, std::uint64_t ntiles, void* d_cand, int idx_bytes,
+                       std::uint64_t cap, unsigned long long* d_counts, cudaStream_t stream) {
+  // KF left the candidates' tile counts in queue row 0: one ordered list
+  const K2Work w = k2_work_layout(d_work, ntiles);
+  if (idx_bytes == 4)
+    k2_compact_launch<std::uint32_t, false>(w, ntiles, static_cast<std::uint32_t*>(d_cand), cap,
+                                            d_counts, nullptr, stream);
+  else
+    k2_compact_launch<std::uint64_t, false>(w, ntiles, static_cast<std::uint64_t*>(d_cand), cap,
+                                            d_counts, nullptr, stream);
+}
+
+void launch_sample(const double* d_xy, std::uint64_t n, int segs, int len, double* d_sample,
+                   cudaStream_t stream) {
+  gather_sample<<<segs, 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n, len,
+                                          reinterpret_cast<double2*>(d_sample));
+  check_cuda(cudaGetLastError(), "gather_sample launch");
+}
+
+void launch_count_in_box(const double* d_xy, std::uint64_t n, const double box[4],
+                         unsigned long long* d_count, cudaStream_t stream) {
+  check_cuda(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), stream), "cudaMemsetAsync");
+  const unsigned grid = static_cast<unsigned>(n / (256 * 16) + 1 < 1184 ? n / (256 * 16) + 1 : 1184);
+  count_in_box<<<grid, 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n, box[0], box[1],
+                                         box[2], box[3], d_count);
+  check_cuda(cudaGetLastError(), "count_in_box launch");
 }
 
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,

@@ -20,6 +20,8 @@ struct FilterOut {
   ohx_filter_plan plan;
   std::uint64_t counts[4];
   bool corner_pass;  // the certificate failed and K1b ran
+  bool fused;        // single pass: K2 ran on the fused pass's candidates only
+  std::uint64_t candidates;
 };
 
 ohx_ctx* create_ctx(int device);

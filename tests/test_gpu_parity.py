@@ -2,12 +2,14 @@
 fixtures, through the C ABI (ctypes).  Bit-exact everywhere: extreme
 indices, labels, the four queues in order, hull coordinates."""
 
+import os
+
 import numpy as np
 import pytest
 
 import paper_2209_12310_b200 as P
 from paper_2209_12310_b200 import _lib
-from conftest import sha
+from conftest import ROOT, sha
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -201,3 +203,55 @@ def test_launch_counter_proves_native_path(ctx):
     pts = P.generate("square", 10000, 3)
     run_kernels(ctx, pts, None)
     assert ctx.launches >= before + 2
+
+
+# ------------------------------------------------------- fused single pass ----
+FUSED_CASES = [("normal", 10_000_000, 7, 0.0, True), ("square", 9_000_000, 3, 0.0, True),
+               ("disk", 9_000_000, 5, 0.0, False), ("circle", 9_000_000, 9, 1.0, False)]
+
+
+@pytest.mark.parametrize("dist,n,seed,d,fused", FUSED_CASES)
+def test_fused_pipeline_matches_oracle(ctx, oracle, dist, n, seed, d, fused):
+    pts = P.generate(dist, n, seed, d)
+    dpts = dev(pts)
+    hull, _ = ctx.heaphull_device(dpts, n)
+    info = ctx.last_run()
+    assert info["fused"] == fused, info
+    want_hull, want_labels = oracle.heaphull(pts, with_labels=True)
+    assert np.array_equal(hull, want_hull)
+    assert info["counts"] == [int((want_labels == q).sum()) for q in (1, 2, 3, 4)]
+    # the queues themselves, in order
+    for q in range(4):
+        idx, _ = ctx.queue(q + 1, info["counts"][q])
+        assert np.array_equal(idx, np.flatnonzero(want_labels == q + 1))
+    if fused:
+        assert 0 < info["candidates"] < n // 20
+
+
+def test_fused_labels_through_the_host_api(oracle):
+    pts = P.generate("normal", 9_000_000, 21)
+    hull, labels, _ = P.heaphull_run(pts)
+    want_hull, want_labels = oracle.heaphull(pts, with_labels=True)
+    assert np.array_equal(labels, want_labels)
+    assert np.array_equal(hull, want_hull)
+
+
+def test_fused_verification_failure_falls_back(tmp_path):
+    # OHX_FUSE=fallback rejects the provisional box after the fused pass:
+    # the result must still be exact (the regular second pass runs)
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, paper_2209_12310_b200 as P\n"
+        "from oracle import Oracle\n"
+        "pts = P.generate('normal', 9_000_000, 5)\n"
+        "ctx = P.Context(0)\n"
+        "hull, _ = ctx.heaphull_device(torch.from_numpy(pts).cuda(), len(pts))\n"
+        "info = ctx.last_run()\n"
+        "assert not info['fused'], info\n"
+        "assert np.array_equal(hull, Oracle().heaphull(pts))\n"
+        "print('fallback ok')\n")
+    env = dict(os.environ, OHX_FUSE="fallback", PYTHONPATH=ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=600)
+    assert r.returncode == 0 and "fallback ok" in r.stdout, r.stderr[-3000:]
