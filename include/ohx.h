@@ -131,6 +131,11 @@ typedef struct {
   uint32_t corner_pass; /* 1: the corner certificate failed and K1b ran */
   uint64_t candidates;  /* points K2 examined in fused mode */
   uint64_t counts[4];   /* queue lengths */
+  uint32_t fuse_state;  /* 0 not tried (small n / disabled), 1 fused, 2 no
+                           sample box, 3 sample coverage too low, 4 box not
+                           certified in the true octagon, 5 too many candidates */
+  uint32_t pad;
+  double sample_coverage; /* fraction of the sample inside the provisional box */
 } ohx_run_info;
 int ohx_ctx_last_run(const ohx_ctx* ctx, ohx_run_info* info);
 /* Device duration (CUDA events on the launching stream) of the last launch

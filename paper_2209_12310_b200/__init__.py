@@ -188,7 +188,10 @@ class Context:
         r = RunInfo()
         check(lib.ohx_ctx_last_run(self.h, C.byref(r)))
         return {"fused": bool(r.fused), "corner_pass": bool(r.corner_pass),
-                "candidates": int(r.candidates), "counts": [int(v) for v in r.counts]}
+                "candidates": int(r.candidates), "counts": [int(v) for v in r.counts],
+                "fuse_state": ("off", "fused", "no-sample-box", "low-sample-coverage",
+                               "box-not-certified", "too-many-candidates")[r.fuse_state],
+                "sample_coverage": float(r.sample_coverage)}
 
     # ---- kernel level --------------------------------------------------
     def extremes(self, d_xy, n: int, index_base: int = 0, stream=None) -> ExtremesRec:

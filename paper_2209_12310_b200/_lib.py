@@ -46,7 +46,8 @@ class ExtremeSet(C.Structure):
 
 class RunInfo(C.Structure):
     _fields_ = [("fused", C.c_uint32), ("corner_pass", C.c_uint32), ("candidates", _u64),
-                ("counts", _u64 * 4)]
+                ("counts", _u64 * 4), ("fuse_state", C.c_uint32), ("pad", C.c_uint32),
+                ("sample_coverage", C.c_double)]
 
 
 class FilterPlan(C.Structure):

@@ -627,8 +627,9 @@ constexpr double kFuseMinCoverage = 0.97;
 // sample's eight extremes -> octagon -> certified box.  Returns false when
 // fusing does not pay (small input, no box, poor sample coverage).
 bool provisional_box(ohx_ctx* c, const double* d_xy, std::uint64_t n, double box[4],
-                     cudaStream_t s) {
+                     cudaStream_t s, FilterOut& f) {
   if (n < kFuseMinPoints || fuse_mode() == 0) return false;
+  f.fuse_state = 2;
   const std::uint64_t ns = std::uint64_t(kSampleSegs) * kSampleLen;
   dev_grow(reinterpret_cast<void**>(&c->d_sample), &c->sample_bytes, ns * 16, "sample");
   launch_sample(d_xy, n, kSampleSegs, kSampleLen, c->d_sample, s);
@@ -660,7 +661,9 @@ bool provisional_box(ohx_ctx* c, const double* d_xy, std::uint64_t n, double box
   ++c->launches;
   check_cuda(cudaMemcpyAsync(c->h_cnt, c->d_cnt, 8, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
   check_cuda(cudaStreamSynchronize(s), "sample coverage");
-  return double(*c->h_cnt) >= kFuseMinCoverage * double(ns);
+  f.sample_coverage = double(*c->h_cnt) / double(ns);
+  f.fuse_state = 3;
+  return f.sample_coverage >= kFuseMinCoverage;
 }
 
 }  // namespace
@@ -676,6 +679,8 @@ FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
   c->last_run.fused = f.fused;
   c->last_run.corner_pass = f.corner_pass;
   c->last_run.candidates = f.candidates;
+  c->last_run.fuse_state = f.fuse_state;
+  c->last_run.sample_coverage = f.sample_coverage;
   for (int q = 0; q < 4; ++q) c->last_run.counts[q] = f.counts[q];
   return f;
 }
@@ -686,15 +691,14 @@ FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
   if (n == 0) throw std::invalid_argument("heaphull: empty point set");
   FilterOut f{};
   double box[4];
-  if (provisional_box(c, d_xy, n, box, s)) {
+  if (provisional_box(c, d_xy, n, box, s, f)) {
     // ---- fused: one pass for the extremes and the provisional filter
-    const std::uint64_t ntiles = (n + kK2Tile - 1) / kK2Tile;
-    dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes, k2_work_bytes(ntiles),
-             "k2 work area");
+    dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes,
+             kf_work_layout(nullptr, n).total_bytes, "kf work area");
     const int grid = kf_grid(c->device, n);
     ensure_partials(c, grid);
     check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
-    launch_kf(d_xy, n, 0, box, c->d_partials, grid, c->d_ticket, c->d_rec, c->d_status, ntiles, s);
+    launch_kf(d_xy, n, 0, box, c->d_partials, grid, c->d_ticket, c->d_rec, c->d_status, s);
     check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
     c->timed[0] = true;
     ++c->launches;
@@ -706,6 +710,7 @@ FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
     // the dropped points are label 0 iff B is certified inside the true
     // octagon and holds none of the eight kept points
     bool ok = box_certified(f.plan, box) && fuse_mode() != 2;
+    f.fuse_state = 4;
     for (int a = 0; a < 8 && ok; ++a)
       ok = !(f.ext.x[a] >= box[0] && f.ext.x[a] <= box[1] && f.ext.y[a] >= box[2] &&
              f.ext.y[a] <= box[3]);
@@ -713,13 +718,15 @@ FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
       const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
       const std::uint64_t cap = std::max<std::uint64_t>(1u << 20, n / 16);
       dev_grow(&c->d_cand, &c->cand_bytes, cap * idx_bytes, "candidates");
-      launch_candidates(c->d_status, ntiles, c->d_cand, idx_bytes, cap, c->d_counts, s);
+      launch_candidates(c->d_status, n, c->d_cand, idx_bytes, cap, c->d_counts, s);
       ++c->launches;
       check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
       check_cuda(cudaStreamSynchronize(s), "candidates");
       const std::uint64_t n_cand = c->h_counts[0];
+      f.fuse_state = 5;
       if (n_cand <= cap) {
+        f.fuse_state = 1;
         if (d_labels) check_cuda(cudaMemsetAsync(d_labels, 0, n, s), "cudaMemsetAsync(labels)");
         filter_core(c, d_xy, n, 0, f.plan, d_labels, f.counts, s, c->d_cand, n_cand);
         f.fused = true;

@@ -90,14 +90,49 @@ void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_w
                std::uint64_t ntiles, void* d_queues, int idx_bytes, std::uint64_t cap,
                std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream,
                const void* d_gather = nullptr);
-// KF: fused extremes + provisional box filter (see kernels.cu).  Re-arms the
-// work area; leaves candidate tile counts/scratch in it.
+// KF work area: [2 counters | kf_compact look-back words (1 per group of
+// 1024 warp tiles) | per-warp-tile candidate counts (u32 per 256 points) |
+// 8-bit candidate offsets (one slot per point)].
+constexpr std::uint64_t kKFWarpTile = 256, kKFGroupTiles = 1024;
+struct KFWork {
+  unsigned* ticket_unused;
+  unsigned* group_counter;
+  std::uint64_t* status;
+  std::uint32_t* wt_counts;
+  std::uint8_t* scratch;
+  std::uint64_t nwt;
+  std::uint64_t clear_bytes;
+  std::uint64_t total_bytes;
+};
+inline KFWork kf_work_layout(void* base, std::uint64_t n) {
+  KFWork w;
+  w.nwt = (n + kKFWarpTile - 1) / kKFWarpTile;
+  const std::uint64_t ngroups = (w.nwt + kKFGroupTiles - 1) / kKFGroupTiles;
+  auto* b = static_cast<unsigned char*>(base);
+  std::uint64_t off = 0;
+  w.ticket_unused = reinterpret_cast<unsigned*>(b);
+  w.group_counter = reinterpret_cast<unsigned*>(b + 4);
+  off += 256;
+  w.status = reinterpret_cast<std::uint64_t*>(b + off);
+  off += ngroups * 8;
+  w.clear_bytes = off;
+  off = (off + 255) & ~std::uint64_t(255);
+  w.wt_counts = reinterpret_cast<std::uint32_t*>(b + off);
+  off += w.nwt * 4;
+  off = (off + 255) & ~std::uint64_t(255);
+  w.scratch = b + off;
+  off += w.nwt * kKFWarpTile;
+  w.total_bytes = off;
+  return w;
+}
+// KF: fused extremes + provisional box filter (see kernels.cu).  Re-arms its
+// work area and leaves the candidates' tile counts/offsets in it.
 int kf_grid(int device, std::uint64_t n);
 void launch_kf(const double* d_xy, std::uint64_t n, std::uint64_t base, const double box[4],
                K1Partial* partials, int grid, unsigned* ticket, ohx_extremes_rec* d_out,
-               void* d_work, std::uint64_t ntiles, cudaStream_t stream);
-// ordered candidate list from KF's work area (queue 0 of k2_compact)
-void launch_candidates(void* d_work, std::uint64_t ntiles, void* d_cand, int idx_bytes,
+               void* d_work, cudaStream_t stream);
+// the ordered candidate list from KF's work area; d_counts[0] = its length
+void launch_candidates(void* d_work, std::uint64_t n, void* d_cand, int idx_bytes,
                        std::uint64_t cap, unsigned long long* d_counts, cudaStream_t stream);
 void launch_sample(const double* d_xy, std::uint64_t n, int segs, int len, double* d_sample,
                    cudaStream_t stream);

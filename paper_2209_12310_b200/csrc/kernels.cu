@@ -743,98 +743,60 @@ __global__ void __launch_bounds__(kK2cBlock)
 // Fused single pass (K1 + provisional filter).  While streaming the points
 // for the eight extremes, every point inside a provisional box B (fitted on
 // a sample's octagon before the pass) is dropped and every other point is
-// recorded as a candidate: tile-local 16-bit offsets in the tile's scratch
-// slice plus the tile's candidate count (queue row 0 of the K2 work area).
-// After the pass the host checks that B is certified inside the TRUE
-// octagon (exact edge margins, ohx::box_certified) and contains no kept
-// index; then every dropped point provably has the reference label 0 and
-// only the candidates need the full test (K2 in gather mode).  Otherwise the
-// regular K2 pass runs and nothing from this pass but the extremes is used.
+// recorded as a candidate.  Each warp owns 256-point warp tiles (grid-stride,
+// so a thread's indices only grow, as K1's tie rule needs) and compacts its
+// candidates with ballots alone -- no block barrier in the loop: 8-bit tile
+// offsets into the tile's slice of a scratch buffer plus a per-tile count.
+// kf_compact turns those into one ordered candidate list.  After the pass
+// the host checks that B is certified inside the TRUE octagon (exact edge
+// margins) and holds no kept point; then every dropped point provably has
+// the reference label 0 and only the candidates need K2 (gather mode).
+// Otherwise the regular K2 pass runs and only the extremes are used.
 constexpr int kKFBlock = 256;
 constexpr int kKFMinBlocks = 3;
+constexpr int kWT = 256;  // points per warp tile (8 items x 32 lanes)
 
 template <typename IdxT>
 __global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
     kf_extremes_prefilter(const double2* __restrict__ pts, std::uint64_t n, std::uint64_t base,
                           double bx0, double bx1, double by0, double by1,
                           K1Partial* partials, unsigned* ticket, ohx_extremes_rec* out,
-                          unsigned* tile_counter, std::uint32_t* tile_counts,
-                          std::uint64_t ntiles, std::uint16_t* scratch) {
-  static_assert(kKFBlock == kK2Block, "KF tiles are K2 tiles");
-  constexpr int W = kKFBlock / 32;
-  __shared__ std::uint32_t s_tile[2];
-  __shared__ std::uint32_t s_off[kK2Seg];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                          std::uint32_t* wt_counts, std::uint64_t nwt,
+                          std::uint8_t* scratch) {
+  const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   ArgState<8, 4, IdxT> ts;
   ts.init();
-  if (threadIdx.x == 0) s_tile[0] = atomicAdd(tile_counter, 1u);
-  __syncthreads();
-  for (int iter = 0;; ++iter) {
-    const std::uint64_t tile = s_tile[iter & 1];
-    if (tile >= ntiles) break;
-    // prefetch the next tile id; the barrier below publishes it
-    if (threadIdx.x == 0) s_tile[(iter + 1) & 1] = atomicAdd(tile_counter, 1u);
-    const std::uint64_t t0 = tile * kK2Tile;
-    const bool full = t0 + kK2Tile <= n;
-    double2 v[kK2Items];
+  const std::uint64_t warps = std::uint64_t(gridDim.x) * (kKFBlock / 32);
+  for (std::uint64_t wt = std::uint64_t(blockIdx.x) * (kKFBlock / 32) + (threadIdx.x >> 5);
+       wt < nwt; wt += warps) {
+    const std::uint64_t t0 = wt * kWT;
+    const bool full = t0 + kWT <= n;
+    double2 v[8];
 #pragma unroll
-    for (int it = 0; it < kK2Items; ++it) {
-      const std::uint32_t jl = it * kKFBlock + threadIdx.x;
+    for (int it = 0; it < 8; ++it) {
+      const std::uint32_t jl = it * 32 + lane;
       v[it] = (full || t0 + jl < n) ? ld_stream(pts + t0 + jl) : make_double2(0.0, 0.0);
     }
     std::uint32_t cand = 0;
 #pragma unroll
-    for (int it = 0; it < kK2Items; ++it) {
-      const std::uint32_t jl = it * kKFBlock + threadIdx.x;
+    for (int it = 0; it < 8; ++it) {
+      const std::uint32_t jl = it * 32 + lane;
       const bool valid = full || t0 + jl < n;
       if (valid) K1Visit::visit(ts, v[it], static_cast<IdxT>(t0 + jl));
       const bool inbox = v[it].x >= bx0 && v[it].x <= bx1 && v[it].y >= by0 && v[it].y <= by1;
       cand |= std::uint32_t(valid && !inbox) << it;
     }
-    if (!__syncthreads_or(cand != 0)) {
-      if (threadIdx.x < 4) tile_counts[threadIdx.x * ntiles + tile] = 0;
-      continue;
-    }
+    std::uint32_t c = 0;
+    if (__any_sync(kFull, cand != 0)) {
 #pragma unroll
-    for (int it = 0; it < kK2Items; ++it) {
-      const unsigned b = __ballot_sync(kFull, cand >> it & 1u);
-      if (lane == 0) s_off[it * W + warp] = __popc(b);
-    }
-    __syncthreads();
-    if (warp == 0) {
-      constexpr int PER = kK2Seg / 32;
-      std::uint32_t c[PER], sum = 0;
-#pragma unroll
-      for (int r = 0; r < PER; ++r) {
-        c[r] = s_off[lane * PER + r];
-        sum += c[r];
+      for (int it = 0; it < 8; ++it) {
+        const unsigned b = __ballot_sync(kFull, cand >> it & 1u);
+        if (cand >> it & 1u) scratch[t0 + c + __popc(b & lt)] = static_cast<std::uint8_t>(it * 32 + lane);
+        c += __popc(b);
       }
-      std::uint32_t incl = sum;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const std::uint32_t o = __shfl_up_sync(kFull, incl, off);
-        if (lane >= off) incl += o;
-      }
-      std::uint32_t run = incl - sum;
-#pragma unroll
-      for (int r = 0; r < PER; ++r) {
-        s_off[lane * PER + r] = run;
-        run += c[r];
-      }
-      if (lane == 31) tile_counts[tile] = incl;
-      if (lane >= 1 && lane < 4) tile_counts[lane * ntiles + tile] = 0;
     }
-    __syncthreads();
-    std::uint16_t* slice = scratch + t0;
-#pragma unroll
-    for (int it = 0; it < kK2Items; ++it) {
-      const unsigned b = __ballot_sync(kFull, cand >> it & 1u);
-      if (cand >> it & 1u)
-        slice[s_off[it * W + warp] + __popc(b & lt)] =
-            static_cast<std::uint16_t>(it * kKFBlock + threadIdx.x);
-    }
-    __syncthreads();  // s_off is reused by the next tile
+    if (lane == 0) wt_counts[wt] = c;
   }
 
   ArgState<8, 4> st = widen(ts);
@@ -858,6 +820,94 @@ __global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
     out->y[a] = p.y;
     if (a >= 4) out->second[a - 4] = s2;
     if (a == 0) out->n = n;
+  }
+}
+
+// Ordered candidate list from KF's warp-tile counts: groups of 1024 tiles
+// (4 per thread), block scan + decoupled look-back across groups, then a
+// flattened copy (binary search over the group's tile prefix).
+constexpr int kKFcBlock = 256;
+constexpr int kKFcTiles = 4 * kKFcBlock;
+
+template <typename IdxT>
+__global__ void __launch_bounds__(kKFcBlock)
+    kf_compact(const std::uint32_t* __restrict__ wt_counts, std::uint64_t nwt,
+               const std::uint8_t* __restrict__ scratch, std::uint64_t* status,
+               unsigned* group_counter, IdxT* cand, std::uint64_t cap,
+               unsigned long long* counts) {
+  __shared__ std::uint32_t s_group;
+  __shared__ std::uint32_t s_pre[kKFcTiles];
+  __shared__ std::uint32_t s_warp[kKFcBlock / 32];
+  __shared__ std::uint64_t s_excl;
+  __shared__ std::uint32_t s_total;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const std::uint64_t ngroups = (nwt + kKFcTiles - 1) / kKFcTiles;
+  if (threadIdx.x == 0) s_group = atomicAdd(group_counter, 1u);
+  __syncthreads();
+  const std::uint64_t g = s_group;
+  std::uint32_t c[4], sum = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const std::uint64_t t = g * kKFcTiles + threadIdx.x * 4 + r;
+    c[r] = t < nwt ? wt_counts[t] : 0u;
+    sum += c[r];
+  }
+  std::uint32_t incl = sum;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const std::uint32_t o = __shfl_up_sync(kFull, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const std::uint32_t w = lane < kKFcBlock / 32 ? s_warp[lane] : 0u;
+    std::uint32_t wi = w;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const std::uint32_t o = __shfl_up_sync(kFull, wi, off);
+      if (lane >= off) wi += o;
+    }
+    if (lane < kKFcBlock / 32) s_warp[lane] = wi - w;
+    const std::uint32_t agg = __shfl_sync(kFull, wi, 31);
+    std::uint64_t excl = 0;
+    if (g == 0) {
+      if (lane == 0) st_relaxed(status, kFlagP | agg);
+    } else {
+      if (lane == 0) st_relaxed(status + g, kFlagA | agg);
+      excl = look_back(status, g);
+      if (lane == 0) st_relaxed(status + g, kFlagP | (excl + agg));
+    }
+    if (lane == 0) {
+      s_excl = excl;
+      s_total = agg;
+      if (g == ngroups - 1) {
+        counts[0] = excl + agg;
+        counts[1] = counts[2] = counts[3] = 0;
+      }
+    }
+  }
+  __syncthreads();
+  std::uint32_t run = s_warp[warp] + incl - sum;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    s_pre[threadIdx.x * 4 + r] = run;
+    run += c[r];
+  }
+  __syncthreads();
+  const std::uint32_t total = s_total;
+  const std::uint64_t excl = s_excl;
+  for (std::uint32_t k = threadIdx.x; k < total; k += kKFcBlock) {
+    int lo = 0, hi = kKFcTiles - 1;  // the last tile whose prefix is <= k
+#pragma unroll
+    for (int step = 0; step < 10; ++step) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pre[mid] <= k) lo = mid;
+      else hi = mid - 1;
+    }
+    const std::uint64_t t = g * kKFcTiles + lo;
+    const std::uint32_t e = k - s_pre[lo];
+    if (excl + k < cap) cand[excl + k] = static_cast<IdxT>(t * kWT + scratch[t * kWT + e]);
   }
 }
 
@@ -1005,38 +1055,42 @@ int kf_grid(int device, std::uint64_t n) {
                  &per_sm, kf_extremes_prefilter<std::uint32_t>, kKFBlock, 0),
              "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
   if (per_sm < 1) per_sm = 1;
-  const std::uint64_t ntiles = (n + kK2Tile - 1) / kK2Tile;
+  const std::uint64_t nwt = (n + kWT - 1) / kWT;
+  const std::uint64_t need = (nwt + kKFBlock / 32 - 1) / (kKFBlock / 32);
   const std::uint64_t full = std::uint64_t(sms) * per_sm;
-  return static_cast<int>(ntiles < full ? ntiles : full);
+  return static_cast<int>(need < full ? need : full);
 }
 
 void launch_kf(const double* d_xy, std::uint64_t n, std::uint64_t base, const double box[4],
                K1Partial* partials, int grid, unsigned* ticket, ohx_extremes_rec* d_out,
-               void* d_work, std::uint64_t ntiles, cudaStream_t stream) {
-  const K2Work w = k2_work_layout(d_work, ntiles);
+               void* d_work, cudaStream_t stream) {
+  const KFWork w = kf_work_layout(d_work, n);
   check_cuda(cudaMemsetAsync(d_work, 0, w.clear_bytes, stream), "cudaMemsetAsync(kf work)");
   const auto* pts = reinterpret_cast<const double2*>(d_xy);
-  if (n + kK2Tile < 0xffffffffull)
+  if (n + kWT < 0xffffffffull)
     kf_extremes_prefilter<std::uint32_t><<<grid, kKFBlock, 0, stream>>>(
-        pts, n, base, box[0], box[1], box[2], box[3], partials, ticket, d_out, w.tile_counter,
-        w.tile_counts, ntiles, w.scratch);
+        pts, n, base, box[0], box[1], box[2], box[3], partials, ticket, d_out, w.wt_counts,
+        w.nwt, w.scratch);
   else
     kf_extremes_prefilter<std::uint64_t><<<grid, kKFBlock, 0, stream>>>(
-        pts, n, base, box[0], box[1], box[2], box[3], partials, ticket, d_out, w.tile_counter,
-        w.tile_counts, ntiles, w.scratch);
+        pts, n, base, box[0], box[1], box[2], box[3], partials, ticket, d_out, w.wt_counts,
+        w.nwt, w.scratch);
   check_cuda(cudaGetLastError(), "kf_extremes_prefilter launch");
 }
 
-void launch_candidates(void* d_work, std::uint64_t ntiles, void* d_cand, int idx_bytes,
+void launch_candidates(void* d_work, std::uint64_t n, void* d_cand, int idx_bytes,
                        std::uint64_t cap, unsigned long long* d_counts, cudaStream_t stream) {
-  // KF left the candidates' tile counts in queue row 0: one ordered list
-  const K2Work w = k2_work_layout(d_work, ntiles);
+  const KFWork w = kf_work_layout(d_work, n);
+  const unsigned ngroups = static_cast<unsigned>((w.nwt + kKFcTiles - 1) / kKFcTiles);
   if (idx_bytes == 4)
-    k2_compact_launch<std::uint32_t, false>(w, ntiles, static_cast<std::uint32_t*>(d_cand), cap,
-                                            d_counts, nullptr, stream);
+    kf_compact<std::uint32_t><<<ngroups, kKFcBlock, 0, stream>>>(
+        w.wt_counts, w.nwt, w.scratch, w.status, w.group_counter,
+        static_cast<std::uint32_t*>(d_cand), cap, d_counts);
   else
-    k2_compact_launch<std::uint64_t, false>(w, ntiles, static_cast<std::uint64_t*>(d_cand), cap,
-                                            d_counts, nullptr, stream);
+    kf_compact<std::uint64_t><<<ngroups, kKFcBlock, 0, stream>>>(
+        w.wt_counts, w.nwt, w.scratch, w.status, w.group_counter,
+        static_cast<std::uint64_t*>(d_cand), cap, d_counts);
+  check_cuda(cudaGetLastError(), "kf_compact launch");
 }
 
 void launch_sample(const double* d_xy, std::uint64_t n, int segs, int len, double* d_sample,

@@ -22,6 +22,8 @@ struct FilterOut {
   bool corner_pass;  // the certificate failed and K1b ran
   bool fused;        // single pass: K2 ran on the fused pass's candidates only
   std::uint64_t candidates;
+  std::uint32_t fuse_state;  // ohx_run_info.fuse_state
+  double sample_coverage;
 };
 
 ohx_ctx* create_ctx(int device);
