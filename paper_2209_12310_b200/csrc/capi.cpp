@@ -173,8 +173,9 @@ bool box_ok(const std::vector<EdgeT<R>>& edges, R x0, R x1, R y0, R y1, R factor
   return true;
 }
 
-void fit_box(const double* oct, int m, const double* ea, const double* ec,
-             double box[4]) {
+// Fallback search: centred box, then the sides grown together.
+void fit_box_ascent(const double* oct, int m, const double* ea, const double* ec,
+                    double box[4]) {
   box[0] = 1.0;
   box[1] = 0.0;
   box[2] = 1.0;
@@ -233,6 +234,114 @@ void fit_box(const double* oct, int m, const double* ea, const double* ec,
   }
   // certify the exact double box in long double before using it
   if (box_ok<long double>(edges_l, b[0], b[1], b[2], b[3], 8.0L)) std::memcpy(box, b, sizeof(b));
+}
+
+// Horizontal chord [left, right] of the convex polygon at height y.
+bool chord(const double* oct, int m, double y, double& left, double& right) {
+  left = INFINITY;
+  right = -INFINITY;
+  for (int i = 0; i < m; ++i) {
+    const int j = i + 1 == m ? 0 : i + 1;
+    const double ax = oct[2 * i], ay = oct[2 * i + 1], bx = oct[2 * j], by = oct[2 * j + 1];
+    if (ay == by) {
+      if (y == ay) {
+        left = std::min(left, std::min(ax, bx));
+        right = std::max(right, std::max(ax, bx));
+      }
+      continue;
+    }
+    if (y < std::min(ay, by) || y > std::max(ay, by)) continue;
+    const double x = ax + (y - ay) * (bx - ax) / (by - ay);
+    left = std::min(left, x);
+    right = std::max(right, x);
+  }
+  return left <= right;
+}
+
+// The certified interior box: the largest-area axis-aligned rectangle in the
+// (convex) octagon -- for heights y0 < y1 the widest rectangle spans the
+// intersection of the two chords -- found by a grid search over (y0, y1)
+// and a local refinement, then pulled inwards until box_ok certifies it.
+// Area is the coverage proxy (exact for uniform data, near-centred boxes for
+// normal data).  Falls back to fit_box_ascent.
+void fit_box(const double* oct, int m, const double* ea, const double* ec, double box[4]) {
+  box[0] = 1.0;
+  box[1] = 0.0;
+  box[2] = 1.0;
+  box[3] = 0.0;  // empty
+  if (m < 3) return;
+  double vy0 = oct[1], vy1 = oct[1], vx0 = oct[0], vx1 = oct[0];
+  for (int i = 1; i < m; ++i) {
+    vy0 = std::min(vy0, oct[2 * i + 1]);
+    vy1 = std::max(vy1, oct[2 * i + 1]);
+    vx0 = std::min(vx0, oct[2 * i]);
+    vx1 = std::max(vx1, oct[2 * i]);
+  }
+  if (!(vy1 > vy0) || !(vx1 > vx0)) return;
+  auto area = [&](double y0, double y1, double* b) {
+    double l0, r0, l1, r1;
+    if (!(y1 > y0) || !chord(oct, m, y0, l0, r0) || !chord(oct, m, y1, l1, r1)) return -1.0;
+    b[0] = std::max(l0, l1);
+    b[1] = std::min(r0, r1);
+    b[2] = y0;
+    b[3] = y1;
+    return b[1] > b[0] ? (b[1] - b[0]) * (y1 - y0) : -1.0;
+  };
+  constexpr int G = 40;
+  const double dy = (vy1 - vy0) / G;
+  double gy[G + 1], gl[G + 1], gr[G + 1];
+  for (int i = 0; i <= G; ++i) {
+    gy[i] = i == G ? vy1 : vy0 + i * dy;
+    if (!chord(oct, m, gy[i], gl[i], gr[i])) gl[i] = INFINITY, gr[i] = -INFINITY;
+  }
+  double best = -1, by0 = 0, by1 = 0, tmp[4];
+  for (int i = 0; i <= G; ++i)
+    for (int k = i + 1; k <= G; ++k) {
+      const double w = std::min(gr[i], gr[k]) - std::max(gl[i], gl[k]);
+      const double a = w > 0 ? w * (gy[k] - gy[i]) : -1.0;
+      if (a > best) {
+        best = a;
+        by0 = gy[i];
+        by1 = gy[k];
+      }
+    }
+  // local refinement: shrinking pattern search on (y0, y1)
+  for (double step = dy; step > (vy1 - vy0) * 1e-9; step *= 0.5) {
+    for (bool moved = true; moved;) {
+      moved = false;
+      const double cand[4][2] = {{by0 - step, by1}, {by0 + step, by1}, {by0, by1 - step},
+                                 {by0, by1 + step}};
+      for (const auto& c : cand) {
+        if (c[0] < vy0 || c[1] > vy1) continue;
+        const double a = area(c[0], c[1], tmp);
+        if (a > best) {
+          best = a;
+          by0 = c[0];
+          by1 = c[1];
+          moved = true;
+        }
+      }
+    }
+  }
+  double b[4];
+  if (best > 0 && area(by0, by1, b) > 0) {
+    std::vector<EdgeT<double>> edges;
+    std::vector<EdgeT<long double>> edges_l;
+    for (int i = 0; i < m; ++i) {
+      edges.push_back({oct[2 * i], oct[2 * i + 1], ea[i], ec[i]});
+      edges_l.push_back({oct[2 * i], oct[2 * i + 1], ea[i], ec[i]});
+    }
+    const double ex = vx1 - vx0, ey = vy1 - vy0;
+    for (double eps = 1e-12; eps < 1e-3; eps *= 8) {
+      const double t[4] = {b[0] + eps * ex, b[1] - eps * ex, b[2] + eps * ey, b[3] - eps * ey};
+      if (box_ok(edges, t[0], t[1], t[2], t[3], 16.0) &&
+          box_ok<long double>(edges_l, t[0], t[1], t[2], t[3], 8.0L)) {
+        std::memcpy(box, t, sizeof(t));
+        return;
+      }
+    }
+  }
+  fit_box_ascent(oct, m, ea, ec, box);
 }
 
 }  // namespace
