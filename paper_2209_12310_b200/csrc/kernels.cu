@@ -92,15 +92,16 @@ __device__ __forceinline__ void upd2(double& bk, I& bi, double& s2, double key, 
 }
 
 // cross-thread merge of (ak,ai) with (bk,bi): argmax, ties -> smaller index
-__device__ __forceinline__ void merge(double& ak, std::uint64_t& ai, double bk,
-                                      std::uint64_t bi) {
+template <typename I>
+__device__ __forceinline__ void merge(double& ak, I& ai, double bk, I bi) {
   const bool take = bk > ak || (bk == ak && bi < ai);
   ak = take ? bk : ak;
   ai = take ? bi : ai;
 }
 
-__device__ __forceinline__ void merge2(double& ak, std::uint64_t& ai, double& as,
-                                       double bk, std::uint64_t bi, double bs) {
+template <typename I>
+__device__ __forceinline__ void merge2(double& ak, I& ai, double& as, double bk, I bi,
+                                       double bs) {
   // second of the union = max(both seconds, the smaller of the two bests)
   const double lo = ak < bk ? ak : bk;
   double s = as > bs ? as : bs;
@@ -127,15 +128,18 @@ __device__ __forceinline__ void warp_reduce(ArgState<NK, NS>& st) {
   }
 }
 
-// Block-wide reduction; the result is valid in warp 0.
-template <int NK, int NS, int BLOCK>
+// Block-wide reduction; the result is valid in warp 0.  kUniform: every
+// warp's lanes already hold one identical (warp-reduced) state -- reducing
+// those copies again would count each diagonal winner twice in its
+// second-best key.
+template <int NK, int NS, int BLOCK, bool kUniform = false>
 __device__ __forceinline__ void block_reduce(ArgState<NK, NS>& st) {
   constexpr int W = BLOCK / 32;
   __shared__ double sk[W][NK];
   __shared__ std::uint64_t si[W][NK];
   __shared__ double ss[W][NS > 0 ? NS : 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  warp_reduce(st);
+  if (!kUniform) warp_reduce(st);
   __syncthreads();  // smem may be reused by a previous call
   if (lane == 0) {
 #pragma unroll
@@ -227,41 +231,101 @@ __device__ __forceinline__ ArgState<NK, NS> widen(const ArgState<NK, NS, I>& t) 
 //                4 ne fl(x+y), 5 nw fl(y-x), 6 sw -fl(x+y), 7 se fl(x-y);
 // slots 4..7 also keep their second-best key.
 //
-// Fast path: a point changes the thread's state only if some key beats the
-// current best (axis slots) or the current second (diagonal slots; beating
-// the best implies beating the second).  After the first few hundred points
-// of a thread that is rare (~ln(m) record breaks per key), so the common
-// path is 2 DADD + 8 DSETP + a predicate reduction, and the selects of the
-// full update run only on the rare divergent slow path.
+// The state is warp-uniform: all 32 lanes hold the warp's best (and second)
+// of every slot.  Fast path: a point can change the state only if one of its
+// keys beats the warp's best (axis slots) or second (diagonal slots), which
+// after a warp has seen m points happens with probability ~1/m per key; the
+// common path is therefore 2 DADD + 8 DSETP + one vote per point.  On a hit
+// the slots that some lane improves are reduced across the warp (argmax
+// with ties to the smaller index; multiset top-2 for the diagonals) and
+// merged.  A per-lane state would take its divergent update path 32x more
+// often (every lane's own record breaks stall the whole warp).
 struct K1Visit {
   template <typename I>
-  __device__ __forceinline__ static void slow(ArgState<8, 4, I>& st, double x, double y,
-                                              double t, double d, I j) {
-    upd(st.k[0], st.i[0], x, j);
-    upd(st.k[1], st.i[1], y, j);
-    upd(st.k[2], st.i[2], -x, j);
-    upd(st.k[3], st.i[3], -y, j);
-    upd2(st.k[4], st.i[4], st.s[0], t, j);
-    upd2(st.k[5], st.i[5], st.s[1], -d, j);
-    upd2(st.k[6], st.i[6], st.s[2], -t, j);
-    upd2(st.k[7], st.i[7], st.s[3], d, j);
+  __device__ __forceinline__ static void reduce1(double& bk, I& bi, double key, I j) {
+    double k = key;
+    I i = j;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ok = __shfl_xor_sync(kFull, k, off);
+      const I oi = __shfl_xor_sync(kFull, i, off);
+      merge(k, i, ok, oi);
+    }
+    merge(bk, bi, k, i);
   }
   template <typename I>
-  __device__ __forceinline__ static void visit(ArgState<8, 4, I>& st, double2 p, I j) {
+  __device__ __forceinline__ static void reduce2(double& bk, I& bi, double& bs, double key, I j) {
+    double k = key, s2 = __longlong_as_double(0xfff0000000000000ll);
+    I i = j;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ok = __shfl_xor_sync(kFull, k, off);
+      const I oi = __shfl_xor_sync(kFull, i, off);
+      const double os = __shfl_xor_sync(kFull, s2, off);
+      merge2(k, i, s2, ok, oi, os);
+    }
+    merge2(bk, bi, bs, k, i, s2);
+  }
+  // Can point p change the warp's state?  (per lane, no vote)
+  template <typename I>
+  __device__ __forceinline__ static bool hits(const ArgState<8, 4, I>& st, double2 p) {
     const double t = __dadd_rn(p.x, p.y);
     const double d = __dsub_rn(p.x, p.y);
-    const bool hit = (p.x > st.k[0]) | (p.y > st.k[1]) | (-p.x > st.k[2]) |
-                     (-p.y > st.k[3]) | (t > st.s[0]) | (-d > st.s[1]) |
-                     (-t > st.s[2]) | (d > st.s[3]);
-    if (hit) slow(st, p.x, p.y, t, d, j);
+    return (p.x > st.k[0]) | (p.y > st.k[1]) | (-p.x > st.k[2]) | (-p.y > st.k[3]) |
+           (t > st.s[0]) | (-d > st.s[1]) | (-t > st.s[2]) | (d > st.s[3]);
+  }
+  // Called by all 32 lanes of the warp; `valid` lanes contribute point j.
+  template <typename I>
+  __device__ __forceinline__ static void update(ArgState<8, 4, I>& st, double2 p, I j, bool valid) {
+    const double t = __dadd_rn(p.x, p.y);
+    const double d = __dsub_rn(p.x, p.y);
+    double key[8] = {p.x, p.y, -p.x, -p.y, t, -d, -t, d};
+    if (!valid) {
+#pragma unroll
+      for (int a = 0; a < 8; ++a) key[a] = __longlong_as_double(0xfff0000000000000ll);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+      if (__any_sync(kFull, key[a] > st.k[a])) reduce1(st.k[a], st.i[a], key[a], j);
+#pragma unroll
+    for (int a = 4; a < 8; ++a)
+      if (__any_sync(kFull, key[a] > st.s[a - 4]))
+        reduce2(st.k[a], st.i[a], st.s[a - 4], key[a], j);
   }
 };
+
+// Visit the 8 points v[u] (index j0 + u * step) of every lane of a warp.
+// Fast path: no lane's point can change the state -> one vote for all 8.
+// Otherwise the points go through a per-warp shared-memory stage so that the
+// update path is instantiated once (a rolled loop), not per item.
+template <typename I>
+__device__ __forceinline__ void visit8(ArgState<8, 4, I>& st, const double2 (&v)[8], I j0,
+                                       I step, std::uint64_t n, bool all_valid,
+                                       double2* stage) {
+  bool any = false;
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    any |= (all_valid || std::uint64_t(j0) + u * std::uint64_t(step) < n) && K1Visit::hits(st, v[u]);
+  if (!__any_sync(kFull, any)) return;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) stage[u * 32 + lane] = v[u];
+  __syncwarp();
+#pragma unroll 1
+  for (int u = 0; u < 8; ++u) {
+    const I j = j0 + static_cast<I>(u) * step;
+    K1Visit::update(st, stage[u * 32 + lane], j, all_valid || std::uint64_t(j) < n);
+  }
+  __syncwarp();
+}
 
 template <typename IdxT>
 __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
     k1_extremes(const double2* __restrict__ pts, std::uint64_t n,
                 std::uint64_t base, K1Partial* partials, unsigned* ticket,
                 ohx_extremes_rec* out) {
+  static_assert(kK1Unroll == 8, "visit8 takes 8 points per lane");
+  __shared__ double2 k1_stage[kK1Block / 32][8 * 32];
   ArgState<8, 4, IdxT> ts;
   ts.init();
   // each block streams one contiguous range of 2048-point chunks (32 KB of
@@ -276,17 +340,19 @@ __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
       double2 v[kK1Unroll];
 #pragma unroll
       for (int u = 0; u < kK1Unroll; ++u) v[u] = ld_stream(pts + j0 + u * kK1Block);
-#pragma unroll
-      for (int u = 0; u < kK1Unroll; ++u) K1Visit::visit(ts, v[u], IdxT(j0 + u * kK1Block));
+      visit8(ts, v, j0, IdxT(kK1Block), n, true, k1_stage[threadIdx.x >> 5]);
     } else {
+      double2 v[kK1Unroll];
+#pragma unroll
       for (int u = 0; u < kK1Unroll; ++u)
-        if (std::uint64_t(j0) + u * kK1Block < n)
-          K1Visit::visit(ts, ld_stream(pts + j0 + u * kK1Block), IdxT(j0 + u * kK1Block));
+        v[u] = std::uint64_t(j0) + u * kK1Block < n ? ld_stream(pts + j0 + u * kK1Block)
+                                                    : make_double2(0.0, 0.0);
+      visit8(ts, v, j0, IdxT(kK1Block), n, false, k1_stage[threadIdx.x >> 5]);
     }
   }
 
   ArgState<8, 4> st = widen(ts);
-  block_reduce<8, 4, kK1Block>(st);
+  block_reduce<8, 4, kK1Block, true>(st);
   if (!grid_combine<8, 4, kK1Block>(st, partials, ticket)) return;
   if (threadIdx.x < 8) {
     // lane a of warp 0 publishes slot a with its winner's coordinates
@@ -765,6 +831,7 @@ __global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
                           std::uint8_t* scratch) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
+  __shared__ double2 kf_stage[kKFBlock / 32][8 * 32];
   ArgState<8, 4, IdxT> ts;
   ts.init();
   const std::uint64_t warps = std::uint64_t(gridDim.x) * (kKFBlock / 32);
@@ -778,12 +845,12 @@ __global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
       const std::uint32_t jl = it * 32 + lane;
       v[it] = (full || t0 + jl < n) ? ld_stream(pts + t0 + jl) : make_double2(0.0, 0.0);
     }
+    visit8(ts, v, static_cast<IdxT>(t0 + lane), IdxT(32), n, full, kf_stage[threadIdx.x >> 5]);
     std::uint32_t cand = 0;
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
       const std::uint32_t jl = it * 32 + lane;
       const bool valid = full || t0 + jl < n;
-      if (valid) K1Visit::visit(ts, v[it], static_cast<IdxT>(t0 + jl));
       const bool inbox = v[it].x >= bx0 && v[it].x <= bx1 && v[it].y >= by0 && v[it].y <= by1;
       cand |= std::uint32_t(valid && !inbox) << it;
     }
@@ -800,7 +867,7 @@ __global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
   }
 
   ArgState<8, 4> st = widen(ts);
-  block_reduce<8, 4, kKFBlock>(st);
+  block_reduce<8, 4, kKFBlock, true>(st);
   if (!grid_combine<8, 4, kKFBlock>(st, partials, ticket)) return;
   if (threadIdx.x < 8) {
     const int a = threadIdx.x;
