@@ -764,8 +764,16 @@ bool provisional_box(ohx_ctx* c, const double* d_xy, std::uint64_t n, double box
   if (m < 3) return false;
   ohx_filter_plan ps;
   make_plan(es, oct, m, &ps);
-  std::memcpy(box, ps.box, sizeof(ps.box));
-  if (!(box[0] <= box[1])) return false;
+  if (!(ps.box[0] <= ps.box[1])) return false;
+  // the sample octagon only approximates the true one: pull the box 2 %
+  // towards its centre so that it still fits after the true extremes move
+  // the edges a little (verified exactly after the pass)
+  const double cx = 0.5 * (ps.box[0] + ps.box[1]), cy = 0.5 * (ps.box[2] + ps.box[3]);
+  const double hx = 0.49 * (ps.box[1] - ps.box[0]), hy = 0.49 * (ps.box[3] - ps.box[2]);
+  box[0] = cx - hx;
+  box[1] = cx + hx;
+  box[2] = cy - hy;
+  box[3] = cy + hy;
   launch_count_in_box(c->d_sample, ns, box, c->d_cnt, s);
   ++c->launches;
   check_cuda(cudaMemcpyAsync(c->h_cnt, c->d_cnt, 8, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");

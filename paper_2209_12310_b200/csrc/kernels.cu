@@ -240,6 +240,14 @@ __device__ __forceinline__ ArgState<NK, NS> widen(const ArgState<NK, NS, I>& t) 
 // with ties to the smaller index; multiset top-2 for the diagonals) and
 // merged.  A per-lane state would take its divergent update path 32x more
 // often (every lane's own record breaks stall the whole warp).
+// The warp-uniform extremes state, one per warp in shared memory (only the
+// eight thresholds live in registers).
+struct WarpExt {
+  double k[8];
+  double s[4];
+  std::uint64_t i[8];
+};
+
 struct K1Visit {
   template <typename I>
   __device__ __forceinline__ static void reduce1(double& bk, I& bi, double key, I j) {
@@ -266,17 +274,18 @@ struct K1Visit {
     }
     merge2(bk, bi, bs, k, i, s2);
   }
-  // Can point p change the warp's state?  (per lane, no vote)
-  template <typename I>
-  __device__ __forceinline__ static bool hits(const ArgState<8, 4, I>& st, double2 p) {
+  // Can point p change the warp's state?  th[a] is the value a key must beat:
+  // the best for the axis slots, the second for the diagonal ones.
+  __device__ __forceinline__ static bool hits(const double (&th)[8], double2 p) {
     const double t = __dadd_rn(p.x, p.y);
     const double d = __dsub_rn(p.x, p.y);
-    return (p.x > st.k[0]) | (p.y > st.k[1]) | (-p.x > st.k[2]) | (-p.y > st.k[3]) |
-           (t > st.s[0]) | (-d > st.s[1]) | (-t > st.s[2]) | (d > st.s[3]);
+    return (p.x > th[0]) | (p.y > th[1]) | (-p.x > th[2]) | (-p.y > th[3]) | (t > th[4]) |
+           (-d > th[5]) | (-t > th[6]) | (d > th[7]);
   }
   // Called by all 32 lanes of the warp; `valid` lanes contribute point j.
-  template <typename I>
-  __device__ __forceinline__ static void update(ArgState<8, 4, I>& st, double2 p, I j, bool valid) {
+  __device__ __forceinline__ static void update(WarpExt& w, double (&th)[8], double2 p,
+                                                std::uint64_t j, bool valid) {
+    const int lane = threadIdx.x & 31;
     const double t = __dadd_rn(p.x, p.y);
     const double d = __dsub_rn(p.x, p.y);
     double key[8] = {p.x, p.y, -p.x, -p.y, t, -d, -t, d};
@@ -285,27 +294,69 @@ struct K1Visit {
       for (int a = 0; a < 8; ++a) key[a] = __longlong_as_double(0xfff0000000000000ll);
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
-      if (__any_sync(kFull, key[a] > st.k[a])) reduce1(st.k[a], st.i[a], key[a], j);
-#pragma unroll
-    for (int a = 4; a < 8; ++a)
-      if (__any_sync(kFull, key[a] > st.s[a - 4]))
-        reduce2(st.k[a], st.i[a], st.s[a - 4], key[a], j);
+    for (int a = 0; a < 8; ++a) {
+      if (!__any_sync(kFull, key[a] > th[a])) continue;
+      double bk = w.k[a];
+      std::uint64_t bi = w.i[a];
+      if (a < 4) {
+        reduce1(bk, bi, key[a], j);
+        th[a] = bk;
+      } else {
+        double bs = w.s[a - 4];
+        reduce2(bk, bi, bs, key[a], j);
+        th[a] = bs;
+        __syncwarp();
+        if (lane == 0) w.s[a - 4] = bs;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        w.k[a] = bk;
+        w.i[a] = bi;
+      }
+      __syncwarp();
+    }
   }
 };
+
+__device__ __forceinline__ void warp_ext_init(WarpExt& w, double (&th)[8]) {
+  const double ninf = __longlong_as_double(0xfff0000000000000ll);
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      w.k[a] = ninf;
+      w.i[a] = ~0ull;
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) w.s[a] = ninf;
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a) th[a] = ninf;
+  __syncwarp();
+}
+
+__device__ __forceinline__ ArgState<8, 4> warp_ext_state(const WarpExt& w) {
+  ArgState<8, 4> st;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    st.k[a] = w.k[a];
+    st.i[a] = w.i[a];
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) st.s[a] = w.s[a];
+  return st;
+}
 
 // Visit the 8 points v[u] (index j0 + u * step) of every lane of a warp.
 // Fast path: no lane's point can change the state -> one vote for all 8.
 // Otherwise the points go through a per-warp shared-memory stage so that the
 // update path is instantiated once (a rolled loop), not per item.
-template <typename I>
-__device__ __forceinline__ void visit8(ArgState<8, 4, I>& st, const double2 (&v)[8], I j0,
-                                       I step, std::uint64_t n, bool all_valid,
-                                       double2* stage) {
+template <bool all_valid, typename I>
+__device__ __forceinline__ void visit8(WarpExt& w, double (&th)[8], const double2 (&v)[8], I j0,
+                                       I step, std::uint64_t n, double2* stage) {
   bool any = false;
 #pragma unroll
   for (int u = 0; u < 8; ++u)
-    any |= (all_valid || std::uint64_t(j0) + u * std::uint64_t(step) < n) && K1Visit::hits(st, v[u]);
+    any |= (all_valid || std::uint64_t(j0) + u * std::uint64_t(step) < n) && K1Visit::hits(th, v[u]);
   if (!__any_sync(kFull, any)) return;
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -313,8 +364,8 @@ __device__ __forceinline__ void visit8(ArgState<8, 4, I>& st, const double2 (&v)
   __syncwarp();
 #pragma unroll 1
   for (int u = 0; u < 8; ++u) {
-    const I j = j0 + static_cast<I>(u) * step;
-    K1Visit::update(st, stage[u * 32 + lane], j, all_valid || std::uint64_t(j) < n);
+    const std::uint64_t j = std::uint64_t(j0) + std::uint64_t(u) * std::uint64_t(step);
+    K1Visit::update(w, th, stage[u * 32 + lane], j, all_valid || j < n);
   }
   __syncwarp();
 }
@@ -326,8 +377,10 @@ __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
                 ohx_extremes_rec* out) {
   static_assert(kK1Unroll == 8, "visit8 takes 8 points per lane");
   __shared__ double2 k1_stage[kK1Block / 32][8 * 32];
-  ArgState<8, 4, IdxT> ts;
-  ts.init();
+  __shared__ WarpExt k1_ext[kK1Block / 32];
+  WarpExt& we = k1_ext[threadIdx.x >> 5];
+  double th[8];
+  warp_ext_init(we, th);
   // each block streams one contiguous range of 2048-point chunks (32 KB of
   // consecutive addresses per block step, 8 loads in flight per thread)
   constexpr std::uint64_t kChunk = std::uint64_t(kK1Block) * kK1Unroll;
@@ -340,18 +393,19 @@ __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
       double2 v[kK1Unroll];
 #pragma unroll
       for (int u = 0; u < kK1Unroll; ++u) v[u] = ld_stream(pts + j0 + u * kK1Block);
-      visit8(ts, v, j0, IdxT(kK1Block), n, true, k1_stage[threadIdx.x >> 5]);
+      visit8<true>(we, th, v, j0, IdxT(kK1Block), n, k1_stage[threadIdx.x >> 5]);
     } else {
       double2 v[kK1Unroll];
 #pragma unroll
       for (int u = 0; u < kK1Unroll; ++u)
         v[u] = std::uint64_t(j0) + u * kK1Block < n ? ld_stream(pts + j0 + u * kK1Block)
                                                     : make_double2(0.0, 0.0);
-      visit8(ts, v, j0, IdxT(kK1Block), n, false, k1_stage[threadIdx.x >> 5]);
+      visit8<false>(we, th, v, j0, IdxT(kK1Block), n, k1_stage[threadIdx.x >> 5]);
     }
   }
 
-  ArgState<8, 4> st = widen(ts);
+  __syncwarp();
+  ArgState<8, 4> st = warp_ext_state(we);
   block_reduce<8, 4, kK1Block, true>(st);
   if (!grid_combine<8, 4, kK1Block>(st, partials, ticket)) return;
   if (threadIdx.x < 8) {
@@ -819,8 +873,44 @@ __global__ void __launch_bounds__(kK2cBlock)
 // the reference label 0 and only the candidates need K2 (gather mode).
 // Otherwise the regular K2 pass runs and only the extremes are used.
 constexpr int kKFBlock = 256;
-constexpr int kKFMinBlocks = 3;
+constexpr int kKFMinBlocks = 2;
 constexpr int kWT = 256;  // points per warp tile (8 items x 32 lanes)
+
+// One 256-point warp tile of KF: extremes + provisional box + candidates.
+template <bool kFullTile>
+__device__ __forceinline__ void kf_tile(const double2* __restrict__ pts, std::uint64_t n,
+                                        std::uint64_t wt, double bx0, double bx1, double by0,
+                                        double by1, WarpExt& we, double (&th)[8],
+                                        std::uint32_t* wt_counts, std::uint8_t* scratch,
+                                        double2* stage) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const std::uint64_t t0 = wt * kWT;
+  double2 v[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const std::uint32_t jl = it * 32 + lane;
+    v[it] = (kFullTile || t0 + jl < n) ? ld_stream(pts + t0 + jl) : make_double2(0.0, 0.0);
+  }
+  visit8<kFullTile>(we, th, v, t0 + lane, std::uint64_t(32), n, stage);
+  std::uint32_t cand = 0;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const bool valid = kFullTile || t0 + it * 32 + lane < n;
+    const bool inbox = v[it].x >= bx0 && v[it].x <= bx1 && v[it].y >= by0 && v[it].y <= by1;
+    cand |= std::uint32_t(valid && !inbox) << it;
+  }
+  std::uint32_t c = 0;
+  if (__any_sync(kFull, cand != 0)) {
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const unsigned b = __ballot_sync(kFull, cand >> it & 1u);
+      if (cand >> it & 1u) scratch[t0 + c + __popc(b & lt)] = static_cast<std::uint8_t>(it * 32 + lane);
+      c += __popc(b);
+    }
+  }
+  if (lane == 0) wt_counts[wt] = c;
+}
 
 template <typename IdxT>
 __global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
@@ -829,44 +919,29 @@ __global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
                           K1Partial* partials, unsigned* ticket, ohx_extremes_rec* out,
                           std::uint32_t* wt_counts, std::uint64_t nwt,
                           std::uint8_t* scratch) {
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
   __shared__ double2 kf_stage[kKFBlock / 32][8 * 32];
-  ArgState<8, 4, IdxT> ts;
-  ts.init();
-  const std::uint64_t warps = std::uint64_t(gridDim.x) * (kKFBlock / 32);
-  for (std::uint64_t wt = std::uint64_t(blockIdx.x) * (kKFBlock / 32) + (threadIdx.x >> 5);
-       wt < nwt; wt += warps) {
-    const std::uint64_t t0 = wt * kWT;
-    const bool full = t0 + kWT <= n;
-    double2 v[8];
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const std::uint32_t jl = it * 32 + lane;
-      v[it] = (full || t0 + jl < n) ? ld_stream(pts + t0 + jl) : make_double2(0.0, 0.0);
-    }
-    visit8(ts, v, static_cast<IdxT>(t0 + lane), IdxT(32), n, full, kf_stage[threadIdx.x >> 5]);
-    std::uint32_t cand = 0;
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const std::uint32_t jl = it * 32 + lane;
-      const bool valid = full || t0 + jl < n;
-      const bool inbox = v[it].x >= bx0 && v[it].x <= bx1 && v[it].y >= by0 && v[it].y <= by1;
-      cand |= std::uint32_t(valid && !inbox) << it;
-    }
-    std::uint32_t c = 0;
-    if (__any_sync(kFull, cand != 0)) {
-#pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const unsigned b = __ballot_sync(kFull, cand >> it & 1u);
-        if (cand >> it & 1u) scratch[t0 + c + __popc(b & lt)] = static_cast<std::uint8_t>(it * 32 + lane);
-        c += __popc(b);
-      }
-    }
-    if (lane == 0) wt_counts[wt] = c;
+  __shared__ WarpExt kf_ext[kKFBlock / 32];
+  WarpExt& we = kf_ext[threadIdx.x >> 5];
+  double th[8];
+  warp_ext_init(we, th);
+  // each block streams one contiguous range of 2048-point chunks, warp w
+  // taking the chunk's w-th 256-point warp tile (32 KB of consecutive
+  // addresses per block step, as in K1)
+  constexpr std::uint64_t kChunkTiles = kKFBlock / 32;
+  const std::uint64_t nchunks = (nwt + kChunkTiles - 1) / kChunkTiles;
+  const std::uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+  const std::uint64_t c_end = min(nchunks, (blockIdx.x + 1) * per);
+  const std::uint64_t nfull = n / kWT;  // every warp tile but possibly the last is full
+  for (std::uint64_t ch = blockIdx.x * per; ch < c_end; ++ch) {
+    const std::uint64_t wt = ch * kChunkTiles + (threadIdx.x >> 5);
+    if (wt < nfull) kf_tile<true>(pts, n, wt, bx0, bx1, by0, by1, we, th, wt_counts, scratch,
+                                   kf_stage[threadIdx.x >> 5]);
+    else if (wt < nwt) kf_tile<false>(pts, n, wt, bx0, bx1, by0, by1, we, th, wt_counts, scratch,
+                                       kf_stage[threadIdx.x >> 5]);
   }
 
-  ArgState<8, 4> st = widen(ts);
+  __syncwarp();
+  ArgState<8, 4> st = warp_ext_state(we);
   block_reduce<8, 4, kKFBlock, true>(st);
   if (!grid_combine<8, 4, kKFBlock>(st, partials, ticket)) return;
   if (threadIdx.x < 8) {

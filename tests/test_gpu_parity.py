@@ -216,7 +216,7 @@ def test_fused_pipeline_matches_oracle(ctx, oracle, dist, n, seed, d, fused):
     dpts = dev(pts)
     hull, _ = ctx.heaphull_device(dpts, n)
     info = ctx.last_run()
-    assert info["fused"] == fused, info
+    assert info["fused"] == fused, info["fuse_state"]
     want_hull, want_labels = oracle.heaphull(pts, with_labels=True)
     assert np.array_equal(hull, want_hull)
     assert info["counts"] == [int((want_labels == q).sum()) for q in (1, 2, 3, 4)]
