@@ -730,7 +730,7 @@ int fuse_mode() {
   return mode;
 }
 constexpr int kSampleSegs = 256, kSampleLen = 4096;
-constexpr double kFuseMinCoverage = 0.97;
+constexpr double kFuseMinCoverage = 0.95;
 
 // The provisional box of the fused pass, from a 1M-point sample: the
 // sample's eight extremes -> octagon -> certified box.  Returns false when
@@ -765,11 +765,11 @@ bool provisional_box(ohx_ctx* c, const double* d_xy, std::uint64_t n, double box
   ohx_filter_plan ps;
   make_plan(es, oct, m, &ps);
   if (!(ps.box[0] <= ps.box[1])) return false;
-  // the sample octagon only approximates the true one: pull the box 2 %
+  // the sample octagon only approximates the true one: pull the box 0.5 %
   // towards its centre so that it still fits after the true extremes move
   // the edges a little (verified exactly after the pass)
   const double cx = 0.5 * (ps.box[0] + ps.box[1]), cy = 0.5 * (ps.box[2] + ps.box[3]);
-  const double hx = 0.49 * (ps.box[1] - ps.box[0]), hy = 0.49 * (ps.box[3] - ps.box[2]);
+  const double hx = 0.4975 * (ps.box[1] - ps.box[0]), hy = 0.4975 * (ps.box[3] - ps.box[2]);
   box[0] = cx - hx;
   box[1] = cx + hx;
   box[2] = cy - hy;
