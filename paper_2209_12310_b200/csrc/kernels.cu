@@ -50,6 +50,46 @@ __device__ __forceinline__ void st_relaxed(std::uint64_t* p, std::uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+
+// ---- TMA bulk copies (cp.async.bulk) + mbarrier, for the streaming kernels
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// one arrival that also announces `bytes` of incoming async-proxy writes
+__device__ __forceinline__ void mbar_arrive_expect(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
 // ===================================================================== K1 ==
 // Every slot is an argmax of a maximised key; ties keep the smaller index
 // (combine_max / combine_min, reference parallel.hpp:34-43; argmin of a key
@@ -1053,6 +1093,128 @@ __global__ void __launch_bounds__(kKFcBlock)
   }
 }
 
+// ============================================================= K1 / KF (TMA) ==
+// The streaming pass of K1 (kPrefilter = false) and of the fused KF
+// (kPrefilter = true) fed by TMA bulk copies: each block owns a contiguous
+// range of 2048-point (32 KB) chunks and keeps kSStages of them in flight in
+// shared memory (cp.async.bulk + mbarrier), so the bytes in flight no longer
+// depend on registers.  Warp w processes the chunk's w-th 256-point tile
+// straight from shared memory (conflict-free 16-byte loads); the warp-
+// uniform extremes update reads its points from the same buffer.
+constexpr int kSBlock = 256;
+constexpr int kSChunk = 2048;
+constexpr int kSStages = 3;
+
+struct StreamSmem {
+  double2 buf[kSStages][kSChunk];
+  unsigned long long bar[kSStages];
+  WarpExt ext[kSBlock / 32];
+};
+
+template <bool kPrefilter, bool kFullTile>
+__device__ __forceinline__ void stream_tile(const double2* tile, std::uint64_t t0, std::uint64_t n,
+                                            std::uint64_t wt, double bx0, double bx1, double by0,
+                                            double by1, WarpExt& we, double (&th)[8],
+                                            std::uint32_t* wt_counts, std::uint8_t* scratch) {
+  const int lane = threadIdx.x & 31;
+  double2 v[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) v[it] = tile[it * 32 + lane];
+  visit8<kFullTile>(we, th, v, t0 + lane, std::uint64_t(32), n, const_cast<double2*>(tile));
+  if constexpr (kPrefilter) {
+    const unsigned lt = (1u << lane) - 1u;
+    std::uint32_t cand = 0;
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const bool valid = kFullTile || t0 + it * 32 + lane < n;
+      const bool inbox = v[it].x >= bx0 && v[it].x <= bx1 && v[it].y >= by0 && v[it].y <= by1;
+      cand |= std::uint32_t(valid && !inbox) << it;
+    }
+    std::uint32_t c = 0;
+    if (__any_sync(kFull, cand != 0)) {
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const unsigned b = __ballot_sync(kFull, cand >> it & 1u);
+        if (cand >> it & 1u)
+          scratch[t0 + c + __popc(b & lt)] = static_cast<std::uint8_t>(it * 32 + lane);
+        c += __popc(b);
+      }
+    }
+    if (lane == 0) wt_counts[wt] = c;
+  }
+}
+
+template <bool kPrefilter>
+__global__ void __launch_bounds__(kSBlock, 2)
+    k_stream(const double2* __restrict__ pts, std::uint64_t n, std::uint64_t base, double bx0,
+             double bx1, double by0, double by1, K1Partial* partials, unsigned* ticket,
+             ohx_extremes_rec* out, std::uint32_t* wt_counts, std::uint8_t* scratch) {
+  extern __shared__ __align__(128) unsigned char k_stream_smem[];
+  StreamSmem& S = *reinterpret_cast<StreamSmem*>(k_stream_smem);
+  const int warp = threadIdx.x >> 5;
+  WarpExt& we = S.ext[warp];
+  double th[8];
+  warp_ext_init(we, th);
+  const std::uint64_t nchunks = (n + kSChunk - 1) / kSChunk;
+  const std::uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+  const std::uint64_t c0 = min(nchunks, std::uint64_t(blockIdx.x) * per);
+  const std::uint64_t c1 = min(nchunks, c0 + per);
+  auto issue = [&](std::uint64_t c, int st) {
+    const std::uint64_t p0 = c * kSChunk;
+    const unsigned bytes = static_cast<unsigned>((min(n, p0 + kSChunk) - p0) * sizeof(double2));
+    mbar_arrive_expect(&S.bar[st], bytes);
+    bulk_g2s(S.buf[st], pts + p0, bytes, &S.bar[st]);
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kSStages; ++st) mbar_init(&S.bar[st], 1);
+    mbar_fence_init();
+    for (int st = 0; st < kSStages && c0 + st < c1; ++st) issue(c0 + st, st);
+  }
+  __syncthreads();
+  for (std::uint64_t c = c0, k = 0; c < c1; ++c, ++k) {
+    const int st = static_cast<int>(k % kSStages);
+    mbar_wait(&S.bar[st], static_cast<unsigned>((k / kSStages) & 1));
+    const std::uint64_t t0 = c * kSChunk + std::uint64_t(warp) * 256;  // this warp's tile
+    const std::uint64_t wt = c * (kSChunk / 256) + warp;
+    const double2* tile = S.buf[st] + warp * 256;
+    if (t0 + 256 <= n)
+      stream_tile<kPrefilter, true>(tile, t0, n, wt, bx0, bx1, by0, by1, we, th, wt_counts, scratch);
+    else if (t0 < n)
+      stream_tile<kPrefilter, false>(tile, t0, n, wt, bx0, bx1, by0, by1, we, th, wt_counts,
+                                     scratch);
+    else if (kPrefilter && (threadIdx.x & 31) == 0 && wt < (n + 255) / 256)
+      wt_counts[wt] = 0;
+    __syncthreads();  // every warp is done with stage st
+    if (threadIdx.x == 0 && c + kSStages < c1) {
+      fence_proxy_async_smem();  // order the generic reads before the async refill
+      issue(c + kSStages, st);
+    }
+  }
+  __syncwarp();
+  ArgState<8, 4> res = warp_ext_state(we);
+  block_reduce<8, 4, kSBlock, true>(res);
+  if (!grid_combine<8, 4, kSBlock>(res, partials, ticket)) return;
+  if (threadIdx.x < 8) {
+    const int a = threadIdx.x;
+    double kk = 0, s2 = 0;
+    std::uint64_t i = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (b == a) {
+        kk = res.k[b];
+        i = res.i[b];
+        if (b >= 4) s2 = res.s[b - 4];
+      }
+    const double2 p = pts[i];
+    out->key[a] = kk;
+    out->idx[a] = base + i;
+    out->x[a] = p.x;
+    out->y[a] = p.y;
+    if (a >= 4) out->second[a - 4] = s2;
+    if (a == 0) out->n = n;
+  }
+}
+
 // A sample for the provisional box: `segs` runs of `len` consecutive points
 // at evenly spaced offsets (coalesced reads, 16 MB for the default 256 x 4096).
 __global__ void gather_sample(const double2* __restrict__ pts, std::uint64_t n, int len,
@@ -1102,30 +1264,41 @@ __global__ void gather_xy4(const double2* __restrict__ pts, const IdxT* __restri
 }  // namespace
 
 // ============================================================ launchers ==
-int k1_grid(int device, std::uint64_t n) {
-  int sms = 0, per_sm = 0;
+static int stream_grid(int device, std::uint64_t n) {
+  int sms = 0;
   check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device),
              "cudaDeviceGetAttribute");
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_extremes<std::uint32_t>,
-                                                           kK1Block, 0),
-             "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-  if (per_sm < 1) per_sm = 1;
-  const std::uint64_t full = std::uint64_t(sms) * per_sm;
-  const std::uint64_t need = (n + kK1Block * kK1Unroll - 1) / (kK1Block * kK1Unroll);
-  return static_cast<int>(need < full ? (need > 0 ? need : 1) : full);
+  const std::uint64_t nchunks = (n + kSChunk - 1) / kSChunk;
+  const std::uint64_t full = std::uint64_t(sms) * 2;  // two 98 KB blocks per SM
+  return static_cast<int>(nchunks < full ? (nchunks > 0 ? nchunks : 1) : full);
 }
+
+template <bool kPrefilter>
+static void stream_launch(const double* d_xy, std::uint64_t n, std::uint64_t base,
+                          const double box[4], K1Partial* partials, int grid, unsigned* ticket,
+                          ohx_extremes_rec* d_out, std::uint32_t* wt_counts,
+                          std::uint8_t* scratch, cudaStream_t stream) {
+  constexpr int smem = sizeof(StreamSmem);
+  static bool configured = false;
+  if (!configured) {
+    check_cuda(cudaFuncSetAttribute(k_stream<kPrefilter>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+               "cudaFuncSetAttribute(k_stream)");
+    configured = true;
+  }
+  k_stream<kPrefilter><<<grid, kSBlock, smem, stream>>>(
+      reinterpret_cast<const double2*>(d_xy), n, base, box ? box[0] : 0.0, box ? box[1] : 0.0,
+      box ? box[2] : 0.0, box ? box[3] : 0.0, partials, ticket, d_out, wt_counts, scratch);
+  check_cuda(cudaGetLastError(), "k_stream launch");
+}
+
+int k1_grid(int device, std::uint64_t n) { return stream_grid(device, n); }
 
 void launch_k1(const double* d_xy, std::uint64_t n, std::uint64_t base,
                K1Partial* partials, int grid, unsigned* ticket,
                ohx_extremes_rec* d_out, cudaStream_t stream) {
-  const auto* pts = reinterpret_cast<const double2*>(d_xy);
-  // 32-bit in-loop indices whenever the shard (plus a full grid stride of
-  // overshoot) fits: one SEL per index update instead of two
-  if (n + std::uint64_t(kK1Block) * kK1Unroll < 0xffffffffull)
-    k1_extremes<std::uint32_t><<<grid, kK1Block, 0, stream>>>(pts, n, base, partials, ticket, d_out);
-  else
-    k1_extremes<std::uint64_t><<<grid, kK1Block, 0, stream>>>(pts, n, base, partials, ticket, d_out);
-  check_cuda(cudaGetLastError(), "k1_extremes launch");
+  stream_launch<false>(d_xy, n, base, nullptr, partials, grid, ticket, d_out, nullptr, nullptr,
+                       stream);
 }
 
 void launch_k1b(const double* d_xy, std::uint64_t n, std::uint64_t base,
@@ -1189,35 +1362,15 @@ void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_w
   }
 }
 
-int kf_grid(int device, std::uint64_t n) {
-  int sms = 0, per_sm = 0;
-  check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device),
-             "cudaDeviceGetAttribute");
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                 &per_sm, kf_extremes_prefilter<std::uint32_t>, kKFBlock, 0),
-             "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-  if (per_sm < 1) per_sm = 1;
-  const std::uint64_t nwt = (n + kWT - 1) / kWT;
-  const std::uint64_t need = (nwt + kKFBlock / 32 - 1) / (kKFBlock / 32);
-  const std::uint64_t full = std::uint64_t(sms) * per_sm;
-  return static_cast<int>(need < full ? need : full);
-}
+int kf_grid(int device, std::uint64_t n) { return stream_grid(device, n); }
 
 void launch_kf(const double* d_xy, std::uint64_t n, std::uint64_t base, const double box[4],
                K1Partial* partials, int grid, unsigned* ticket, ohx_extremes_rec* d_out,
                void* d_work, cudaStream_t stream) {
   const KFWork w = kf_work_layout(d_work, n);
   check_cuda(cudaMemsetAsync(d_work, 0, w.clear_bytes, stream), "cudaMemsetAsync(kf work)");
-  const auto* pts = reinterpret_cast<const double2*>(d_xy);
-  if (n + kWT < 0xffffffffull)
-    kf_extremes_prefilter<std::uint32_t><<<grid, kKFBlock, 0, stream>>>(
-        pts, n, base, box[0], box[1], box[2], box[3], partials, ticket, d_out, w.wt_counts,
-        w.nwt, w.scratch);
-  else
-    kf_extremes_prefilter<std::uint64_t><<<grid, kKFBlock, 0, stream>>>(
-        pts, n, base, box[0], box[1], box[2], box[3], partials, ticket, d_out, w.wt_counts,
-        w.nwt, w.scratch);
-  check_cuda(cudaGetLastError(), "kf_extremes_prefilter launch");
+  stream_launch<true>(d_xy, n, base, box, partials, grid, ticket, d_out, w.wt_counts, w.scratch,
+                      stream);
 }
 
 void launch_candidates(void* d_work, std::uint64_t n, void* d_cand, int idx_bytes,
