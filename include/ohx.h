@@ -129,18 +129,22 @@ uint64_t ohx_ctx_launches(const ohx_ctx* ctx);
 typedef struct {
   uint32_t fused;       /* 1: single pass (KF) + K2 on the candidates only */
   uint32_t corner_pass; /* 1: the corner certificate failed and K1b ran */
-  uint64_t candidates;  /* points K2 examined in fused mode */
+  uint64_t candidates;  /* points outside the provisional region (fused pass) */
   uint64_t counts[4];   /* queue lengths */
   uint32_t fuse_state;  /* 0 not tried (small n / disabled), 1 fused, 2 no
-                           sample box, 3 sample coverage too low, 4 box not
-                           certified in the true octagon, 5 too many candidates */
+                           sample region, 3 sample coverage too low, 4 region
+                           not certified in the true octagon, 5 too many
+                           candidates */
   uint32_t pad;
-  double sample_coverage; /* fraction of the sample inside the provisional box */
+  double sample_coverage; /* fraction of the sample inside the provisional region */
 } ohx_run_info;
 int ohx_ctx_last_run(const ohx_ctx* ctx, ohx_run_info* info);
 /* Device duration (CUDA events on the launching stream) of the last launch
- * of K1, K1b and K2 in this context; -1 for a kernel not yet launched. */
-int ohx_ctx_kernel_ms(ohx_ctx* ctx, double ms[3]);
+ * of each stage in this context: ms[0] K1 (or, fused, the KF filter pass),
+ * ms[1] K1b, ms[2] K2, ms[3] the fused path's candidate stage (ordered
+ * compaction + K1 over the candidates); -1 for a stage that did not run
+ * (a pipeline call resets all four). */
+int ohx_ctx_kernel_ms(ohx_ctx* ctx, double ms[4]);
 
 /* ---- kernel-level (one shard, device-resident points) ------------------ */
 

@@ -177,10 +177,11 @@ class Context:
         return int(lib.ohx_ctx_launches(self.h))
 
     def kernel_ms(self) -> dict:
-        """CUDA-event durations of the last K1 / K1b / K2 launches (ms)."""
-        out = (C.c_double * 3)()
+        """CUDA-event durations (ms) of the last launch of each stage: K1 (or
+        the fused KF filter pass), K1b, K2, and the fused candidate stage."""
+        out = (C.c_double * 4)()
         check(lib.ohx_ctx_kernel_ms(self.h, out))
-        return {"k1": out[0], "k1b": out[1], "k2": out[2]}
+        return {"k1": out[0], "k1b": out[1], "k2": out[2], "kc": out[3]}
 
     def last_run(self) -> dict:
         """How the last pipeline call on this context ran (fused single pass
@@ -189,8 +190,8 @@ class Context:
         check(lib.ohx_ctx_last_run(self.h, C.byref(r)))
         return {"fused": bool(r.fused), "corner_pass": bool(r.corner_pass),
                 "candidates": int(r.candidates), "counts": [int(v) for v in r.counts],
-                "fuse_state": ("off", "fused", "no-sample-box", "low-sample-coverage",
-                               "box-not-certified", "too-many-candidates")[r.fuse_state],
+                "fuse_state": ("off", "fused", "no-sample-region", "low-sample-coverage",
+                               "region-not-certified", "too-many-candidates")[r.fuse_state],
                 "sample_coverage": float(r.sample_coverage)}
 
     # ---- kernel level --------------------------------------------------

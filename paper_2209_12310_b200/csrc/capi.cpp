@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -71,9 +72,10 @@ struct ohx_ctx {
 
   ohx_run_info last_run = {};
 
-  // CUDA events bracketing the last launch of each kernel (K1, K1b, K2)
-  cudaEvent_t ev[3][2] = {};
-  bool timed[3] = {false, false, false};
+  // CUDA events bracketing the last launch of each stage: K1 (or KF), K1b,
+  // K2, and the fused path's candidate stage (compaction + candidate K1)
+  cudaEvent_t ev[4][2] = {};
+  bool timed[4] = {false, false, false, false};
 };
 
 namespace ohx {
@@ -616,11 +618,65 @@ void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
   filter_core(c, d_xy, n, base, plan, d_labels, counts, s, nullptr, 0);
 }
 
-bool box_certified(const ohx_filter_plan& plan, const double box[4]) {
-  if (plan.m < 3 || !(box[0] <= box[1]) || !(box[2] <= box[3])) return false;
-  std::vector<EdgeT<long double>> edges;
-  for (int i = 0; i < plan.m; ++i) edges.push_back({plan.ax[i], plan.ay[i], plan.ea[i], plan.ec[i]});
-  return box_ok<long double>(edges, box[0], box[1], box[2], box[3], 8.0L);
+// Vertices of the convex polygon {p : key_a(p) <= b[a], a = 0..7} (the slot
+// keys x, y, -x, -y, x+y, y-x, -(x+y), x-y), in long double: the axis box
+// clipped by the four diagonal half-planes.
+std::vector<std::pair<long double, long double>> region_vertices(const long double b[8]) {
+  using V = std::pair<long double, long double>;
+  std::vector<V> poly = {{-b[2], -b[3]}, {b[0], -b[3]}, {b[0], b[1]}, {-b[2], b[1]}};
+  static const int dx[4] = {1, -1, -1, 1}, dy[4] = {1, 1, -1, -1};
+  for (int k = 0; k < 4 && poly.size() >= 3; ++k) {
+    std::vector<V> out;
+    auto val = [&](const V& p) { return dx[k] * p.first + dy[k] * p.second - b[4 + k]; };
+    for (std::size_t i = 0; i < poly.size(); ++i) {
+      const V p = poly[i], q = poly[(i + 1) % poly.size()];
+      const long double vp = val(p), vq = val(q);
+      if (vp <= 0) out.push_back(p);
+      if ((vp <= 0) != (vq <= 0)) {
+        const long double t = vp / (vp - vq);
+        out.push_back({p.first + t * (q.first - p.first), p.second + t * (q.second - p.second)});
+      }
+    }
+    poly = out;
+  }
+  return poly;
+}
+
+// Is every point the fused pass dropped (in_region true) strictly inside the
+// true octagon, i.e. reference label 0?  The accepted set is within Q with
+// its diagonal bounds widened by the rounding of fl(x+y), fl(x-y)
+// (|fl(s) - s| <= u(|x| + |y|)); every vertex of that widened polygon must
+// clear every octagon edge by the determinant's error bound (the bound is
+// concave, see box_ok, so vertices suffice).
+bool region_certified(const ohx_filter_plan& plan, const KFRegion& q) {
+  if (plan.m < 3) return false;
+  if (!(q.x0 <= q.x1) || !(q.y0 <= q.y1) || !(q.t0 <= q.t1) || !(q.d0 <= q.d1)) return false;
+  const long double X = std::max(std::fabs((long double)q.x0), std::fabs((long double)q.x1));
+  const long double Y = std::max(std::fabs((long double)q.y0), std::fabs((long double)q.y1));
+  const long double w = 4.0L * 0x1p-53L * (X + Y) + 0x1p-1000L;
+  const long double b[8] = {q.x1, q.y1, -(long double)q.x0, -(long double)q.y0,
+                            q.t1 + w, -(long double)q.d0 + w, -(long double)q.t0 + w, q.d1 + w};
+  const auto verts = region_vertices(b);
+  if (verts.size() < 3) return false;
+  const long double uf = 8.0L * 0x1p-53L;
+  for (int i = 0; i < plan.m; ++i) {
+    const long double ax = plan.ax[i], ay = plan.ay[i], A = plan.ea[i], C = plan.ec[i];
+    for (const auto& v : verts) {
+      const long double dy = v.second - ay, dx = v.first - ax;
+      const long double E = A * dy - C * dx;
+      const long double margin = uf * (std::fabs(A) * std::fabs(dy) + std::fabs(C) * std::fabs(dx)) +
+                                 0x1p-1000L;
+      if (!(E > margin)) return false;
+    }
+  }
+  return true;
+}
+
+// The fused pass's own test, on the host (same binary64 operations).
+bool in_region_host(const KFRegion& q, double x, double y) {
+  const double t = x + y, d = x - y;
+  return x >= q.x0 && x <= q.x1 && y >= q.y0 && y <= q.y1 && t >= q.t0 && t <= q.t1 &&
+         d >= q.d0 && d <= q.d1;
 }
 
 void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
@@ -717,70 +773,218 @@ void finish_extremes(ohx_ctx* c, const double* d_xy, std::uint64_t n,
 constexpr std::uint64_t kFuseMinPoints = 1ull << 23;  // below: both passes are cheap
 
 // OHX_FUSE: unset/"auto" = fused pass when it pays, "0" = always two passes,
-// "fallback" = run the fused pass but reject its box (exercises the
-// verification-failure path; tests only).
+// "fallback" = run the fused pass but reject its region (exercises the
+// verification-failure path), "force" = fuse whatever the sample coverage
+// (exercises heavy candidate lists).  The last two are for tests.
 int fuse_mode() {
   static const int mode = [] {
     const char* e = std::getenv("OHX_FUSE");
     if (!e || !*e || std::string(e) == "auto") return 1;
     if (std::string(e) == "0") return 0;
     if (std::string(e) == "fallback") return 2;
+    if (std::string(e) == "force") return 3;
     return 1;
   }();
   return mode;
 }
 constexpr int kSampleSegs = 256, kSampleLen = 4096;
-constexpr double kFuseMinCoverage = 0.95;
+constexpr int kSubSamples = 8;  // disjoint sub-samples of kSampleSegs / 8 runs each
+constexpr double kFuseMinCoverage = 0.8;
 
-// The provisional box of the fused pass, from a 1M-point sample: the
-// sample's eight extremes -> octagon -> certified box.  Returns false when
-// fusing does not pay (small input, no box, poor sample coverage).
-bool provisional_box(ohx_ctx* c, const double* d_xy, std::uint64_t n, double box[4],
-                     cudaStream_t s, FilterOut& f) {
+// Part of the convex polygon `poly` on the left of a -> b (Sutherland-Hodgman
+// step; heuristic geometry, the box is certified exactly after the pass).
+std::vector<P2> clip_left(const std::vector<P2>& poly, P2 a, P2 b) {
+  std::vector<P2> out;
+  const std::size_t m = poly.size();
+  auto side = [&](P2 p) { return (b.x - a.x) * (p.y - a.y) - (b.y - a.y) * (p.x - a.x); };
+  for (std::size_t i = 0; i < m; ++i) {
+    const P2 p = poly[i], q = poly[(i + 1) % m];
+    const double sp = side(p), sq = side(q);
+    if (sp >= 0) out.push_back(p);
+    if ((sp >= 0) != (sq >= 0)) {
+      const double t = sp / (sp - sq);
+      out.push_back({p.x + t * (q.x - p.x), p.y + t * (q.y - p.y)});
+    }
+  }
+  return out;
+}
+
+// key of slot a (ohx.h slot order: x, y, -x, -y, x+y, y-x, -(x+y), x-y)
+double slot_key(int a, double x, double y) {
+  switch (a) {
+    case 0: return x;
+    case 1: return y;
+    case 2: return -x;
+    case 3: return -y;
+    case 4: return x + y;
+    case 5: return y - x;
+    case 6: return -(x + y);
+    default: return x - y;
+  }
+}
+
+// Is the region {key_a <= b[a]} inside the convex CCW polygon R?  (R is
+// convex, so the region's vertices decide.)  Heuristic geometry in double,
+// no allocation: it runs a few hundred times per fit.
+bool region_inside(const double b[8], const std::vector<P2>& R) {
+  P2 poly[16], out[16];
+  int m = 4;
+  poly[0] = {-b[2], -b[3]};
+  poly[1] = {b[0], -b[3]};
+  poly[2] = {b[0], b[1]};
+  poly[3] = {-b[2], b[1]};
+  static const int dx[4] = {1, -1, -1, 1}, dy[4] = {1, 1, -1, -1};
+  for (int k = 0; k < 4 && m >= 3; ++k) {
+    int o = 0;
+    for (int i = 0; i < m; ++i) {
+      const P2 p = poly[i], q = poly[i + 1 == m ? 0 : i + 1];
+      const double vp = dx[k] * p.x + dy[k] * p.y - b[4 + k];
+      const double vq = dx[k] * q.x + dy[k] * q.y - b[4 + k];
+      if (vp <= 0) out[o++] = p;
+      if ((vp <= 0) != (vq <= 0)) {
+        const double t = vp / (vp - vq);
+        out[o++] = {p.x + t * (q.x - p.x), p.y + t * (q.y - p.y)};
+      }
+    }
+    m = o;
+    for (int i = 0; i < m; ++i) poly[i] = out[i];
+  }
+  if (m < 3) return false;
+  const std::size_t r = R.size();
+  for (int v = 0; v < m; ++v)
+    for (std::size_t i = 0; i < r; ++i) {
+      const P2 a = R[i], c = R[i + 1 == r ? 0 : i + 1];
+      if ((c.x - a.x) * (poly[v].y - a.y) - (c.y - a.y) * (poly[v].x - a.x) < 0) return false;
+    }
+  return true;
+}
+
+// The fused pass's region Q: an octagon with the slot directions as edge
+// normals, fitted inside the convex polygon R.  Start from R's own slot
+// support values scaled towards R's centroid until the octagon fits, then
+// push each bound out on its own (a few rounds), then pull everything 0.2 %
+// back towards the centre.  Finally every bound is clamped strictly below
+// lim[a] (the sample's best / second key of the slot).
+bool fit_region(const std::vector<P2>& R, const double lim[8], KFRegion* q) {
+  if (R.size() < 3) return false;
+  double cx = 0, cy = 0;
+  for (const P2& p : R) {
+    cx += p.x;
+    cy += p.y;
+  }
+  cx /= double(R.size());
+  cy /= double(R.size());
+  double h[8], c0[8], b[8];
+  for (int a = 0; a < 8; ++a) {
+    h[a] = -INFINITY;
+    for (const P2& p : R) h[a] = std::max(h[a], slot_key(a, p.x, p.y));
+    c0[a] = slot_key(a, cx, cy);
+    if (!(h[a] > c0[a])) return false;
+  }
+  auto at = [&](double sc, double* out) {
+    for (int a = 0; a < 8; ++a) out[a] = c0[a] + sc * (h[a] - c0[a]);
+  };
+  double lo = 0, hi = 1;
+  at(1e-6, b);
+  if (!region_inside(b, R)) return false;
+  for (int it = 0; it < 24; ++it) {
+    const double mid = (lo + hi) / 2;
+    at(mid, b);
+    if (region_inside(b, R)) lo = mid;
+    else hi = mid;
+  }
+  at(lo, b);
+  for (int round = 0; round < 2; ++round)
+    for (int a = 0; a < 8; ++a) {
+      double good = b[a], bad = h[a];
+      for (int it = 0; it < 16; ++it) {
+        double t[8];
+        std::memcpy(t, b, sizeof(t));
+        t[a] = (good + bad) / 2;
+        if (region_inside(t, R)) good = t[a];
+        else bad = t[a];
+      }
+      b[a] = good;
+    }
+  double r[8];
+  for (int a = 0; a < 8; ++a) {
+    r[a] = c0[a] + 0.998 * (b[a] - c0[a]);
+    const double below = std::nextafter(lim[a], -INFINITY);
+    if (r[a] > below) r[a] = below;
+  }
+  *q = KFRegion{-r[2], r[0], -r[3], r[1], -r[6], r[4], -r[5], r[7]};
+  return q->x0 < q->x1 && q->y0 < q->y1 && q->t0 < q->t1 && q->d0 < q->d1;
+}
+
+// The provisional region of the fused pass.  A 1M-point sample (kSampleSegs
+// runs of kSampleLen consecutive points) is split into kSubSamples disjoint
+// sub-samples; each one's eight extremes give an octagon, and Q is fitted
+// inside the INTERSECTION of those octagons.  The sub-sample octagons
+// scatter the way the true octagon may sit relative to any one sample's, so
+// a region inside all of them rarely leaves the true octagon (checked
+// exactly after the pass; a miss costs the regular second pass).  Q's bounds
+// are also kept strictly below the whole sample's extremes keys, which is
+// what lets the fused pass skip the extremes test for points inside Q.
+// Returns false when fusing does not pay (small input, no region, sample
+// coverage below kFuseMinCoverage).
+bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegion* q,
+                        cudaStream_t s, FilterOut& f) {
   if (n < kFuseMinPoints || fuse_mode() == 0) return false;
   f.fuse_state = 2;
   const std::uint64_t ns = std::uint64_t(kSampleSegs) * kSampleLen;
-  dev_grow(reinterpret_cast<void**>(&c->d_sample), &c->sample_bytes, ns * 16, "sample");
+  const std::uint64_t nsub = ns / kSubSamples;
+  dev_grow(reinterpret_cast<void**>(&c->d_sample), &c->sample_bytes,
+           ns * 16 + kSubSamples * sizeof(ohx_extremes_rec), "sample");
+  auto* d_recs = reinterpret_cast<ohx_extremes_rec*>(c->d_sample + 2 * ns);
   launch_sample(d_xy, n, kSampleSegs, kSampleLen, c->d_sample, s);
   ++c->launches;
-  ohx_extremes_rec rs;
-  const int grid = k1_grid(c->device, ns);
+  const int grid = k1_grid(c->device, nsub);
   ensure_partials(c, grid);
-  launch_k1(c->d_sample, ns, 0, c->d_partials, grid, c->d_ticket, c->d_rec, s);
-  ++c->launches;
-  check_cuda(cudaMemcpyAsync(&rs, c->d_rec, sizeof(rs), cudaMemcpyDeviceToHost, s),
-             "cudaMemcpyAsync(sample rec)");
+  for (int g = 0; g < kSubSamples; ++g) {
+    launch_k1(c->d_sample + 2 * nsub * g, nsub, 0, c->d_partials, grid, c->d_ticket, d_recs + g,
+              s);
+    ++c->launches;
+  }
+  ohx_extremes_rec rs[kSubSamples];
+  check_cuda(cudaMemcpyAsync(rs, d_recs, sizeof(rs), cudaMemcpyDeviceToHost, s),
+             "cudaMemcpyAsync(sample recs)");
   check_cuda(cudaStreamSynchronize(s), "sample extremes");
-  ohx_extreme_set es;
-  resolve_extremes(rs, &es);  // a heuristic octagon: the diagonal winners need no certificate
   const int slot[8] = {OHX_EAST, OHX_NE, OHX_NORTH, OHX_NW,
                        OHX_WEST, OHX_SW, OHX_SOUTH, OHX_SE};
-  double cand[16], oct[16];
-  for (int k = 0; k < 8; ++k) {
-    cand[2 * k] = es.x[slot[k]];
-    cand[2 * k + 1] = es.y[slot[k]];
+  std::vector<P2> region;
+  for (int g = 0; g < kSubSamples; ++g) {
+    ohx_extreme_set es;
+    resolve_extremes(rs[g], &es);  // heuristic octagons: diagonal winners need no certificate
+    double cand[16], oct[16];
+    for (int k = 0; k < 8; ++k) {
+      cand[2 * k] = es.x[slot[k]];
+      cand[2 * k + 1] = es.y[slot[k]];
+    }
+    const int m = build_octagon(cand, oct);
+    if (m < 3) return false;
+    if (g == 0) {
+      for (int i = 0; i < m; ++i) region.push_back({oct[2 * i], oct[2 * i + 1]});
+      continue;
+    }
+    for (int i = 0; i < m && region.size() >= 3; ++i) {
+      const int j = i + 1 == m ? 0 : i + 1;
+      region = clip_left(region, {oct[2 * i], oct[2 * i + 1]}, {oct[2 * j], oct[2 * j + 1]});
+    }
+    if (region.size() < 3) return false;
   }
-  const int m = build_octagon(cand, oct);
-  if (m < 3) return false;
-  ohx_filter_plan ps;
-  make_plan(es, oct, m, &ps);
-  if (!(ps.box[0] <= ps.box[1])) return false;
-  // the sample octagon only approximates the true one: pull the box 0.5 %
-  // towards its centre so that it still fits after the true extremes move
-  // the edges a little (verified exactly after the pass)
-  const double cx = 0.5 * (ps.box[0] + ps.box[1]), cy = 0.5 * (ps.box[2] + ps.box[3]);
-  const double hx = 0.4975 * (ps.box[1] - ps.box[0]), hy = 0.4975 * (ps.box[3] - ps.box[2]);
-  box[0] = cx - hx;
-  box[1] = cx + hx;
-  box[2] = cy - hy;
-  box[3] = cy + hy;
-  launch_count_in_box(c->d_sample, ns, box, c->d_cnt, s);
+  // the whole sample's best (axis) / second (diagonal) keys
+  ohx_extremes_rec all;
+  combine_extremes(rs, kSubSamples, &all);
+  double lim[8];
+  for (int a = 0; a < 8; ++a) lim[a] = a < 4 ? all.key[a] : all.second[a - 4];
+  if (!fit_region(region, lim, q)) return false;
+  launch_count_in_region(c->d_sample, ns, *q, c->d_cnt, s);
   ++c->launches;
   check_cuda(cudaMemcpyAsync(c->h_cnt, c->d_cnt, 8, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
   check_cuda(cudaStreamSynchronize(s), "sample coverage");
   f.sample_coverage = double(*c->h_cnt) / double(ns);
   f.fuse_state = 3;
-  return f.sample_coverage >= kFuseMinCoverage;
+  return f.sample_coverage >= kFuseMinCoverage || fuse_mode() == 3;
 }
 
 }  // namespace
@@ -803,57 +1007,95 @@ FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
 }
 
 namespace {
+// OHX_TRACE=1: host wall time of each pipeline phase on stderr
+struct Trace {
+  bool on = [] {
+    const char* e = std::getenv("OHX_TRACE");
+    return e && *e && std::string(e) != "0";
+  }();
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ohx] %-14s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
                              std::uint8_t* d_labels, cudaStream_t s) {
   if (n == 0) throw std::invalid_argument("heaphull: empty point set");
   FilterOut f{};
-  double box[4];
-  if (provisional_box(c, d_xy, n, box, s, f)) {
-    // ---- fused: one pass for the extremes and the provisional filter
-    dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes,
-             kf_work_layout(nullptr, n).total_bytes, "kf work area");
-    const int grid = kf_grid(c->device, n);
-    ensure_partials(c, grid);
+  for (bool& t : c->timed) t = false;  // kernel_ms reports this pipeline's stages
+  Trace tr;
+  KFRegion q;
+  const bool fuse = provisional_region(c, d_xy, n, &q, s, f);
+  tr.mark("region");
+  if (fuse) {
+    // ---- fused: one streaming pass filters Q; the extremes come from the
+    // candidates (the points outside Q) alone
+    const KFWork wl = kf_work_layout(nullptr, n);
+    dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes, wl.total_bytes,
+             "kf work area");
+    const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
+    // room for 1.5x the sample's miss rate (+1M); more candidates than that
+    // fall back to the two-pass path
+    const std::uint64_t cap = std::min<std::uint64_t>(
+        n, (1u << 20) + static_cast<std::uint64_t>(1.5 * (1.0 - f.sample_coverage) * double(n)));
+    dev_grow(&c->d_cand, &c->cand_bytes, cap * idx_bytes, "candidates");
     check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
-    launch_kf(d_xy, n, 0, box, c->d_partials, grid, c->d_ticket, c->d_rec, c->d_status, s);
+    launch_kf(d_xy, n, q, kf_grid(c->device, n), c->d_status, s);
     check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
     c->timed[0] = true;
     ++c->launches;
-    check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
-                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec)");
-    check_cuda(cudaStreamSynchronize(s), "kf_extremes_prefilter");
-    const ohx_extremes_rec rec = *c->h_rec;
-    finish_extremes(c, d_xy, n, rec, f, s);
-    // the dropped points are label 0 iff B is certified inside the true
-    // octagon and holds none of the eight kept points
-    bool ok = box_certified(f.plan, box) && fuse_mode() != 2;
-    f.fuse_state = 4;
-    for (int a = 0; a < 8 && ok; ++a)
-      ok = !(f.ext.x[a] >= box[0] && f.ext.x[a] <= box[1] && f.ext.y[a] >= box[2] &&
-             f.ext.y[a] <= box[3]);
-    if (ok) {
-      const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
-      const std::uint64_t cap = std::max<std::uint64_t>(1u << 20, n / 16);
-      dev_grow(&c->d_cand, &c->cand_bytes, cap * idx_bytes, "candidates");
-      launch_candidates(c->d_status, n, c->d_cand, idx_bytes, cap, c->d_counts, s);
-      ++c->launches;
-      check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
-      check_cuda(cudaStreamSynchronize(s), "candidates");
-      const std::uint64_t n_cand = c->h_counts[0];
-      f.fuse_state = 5;
-      if (n_cand <= cap) {
+    check_cuda(cudaEventRecord(c->ev[3][0], s), "cudaEventRecord");
+    launch_candidates(c->d_status, n, c->d_cand, idx_bytes, cap, c->d_counts, s);
+    ++c->launches;
+    check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
+    check_cuda(cudaStreamSynchronize(s), "kf candidates");
+    tr.mark("kf+compact");
+    const std::uint64_t n_cand = c->h_counts[0];
+    f.candidates = n_cand;
+    if (n_cand >= 1 && n_cand <= cap) {
+      // K1 over the gathered candidates, record indices mapped back
+      dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, n_cand * 16,
+               "candidate points");
+      launch_gather(d_xy, c->d_cand, idx_bytes, n_cand, c->d_gather, s);
+      const int grid = k1_grid(c->device, n_cand);
+      ensure_partials(c, grid);
+      launch_k1(c->d_gather, n_cand, 0, c->d_partials, grid, c->d_ticket, c->d_rec, s);
+      launch_map_rec(c->d_rec, c->d_cand, idx_bytes, 0, s);
+      c->launches += 3;
+      check_cuda(cudaEventRecord(c->ev[3][1], s), "cudaEventRecord");
+      c->timed[3] = true;
+      check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
+                                 cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec)");
+      check_cuda(cudaStreamSynchronize(s), "candidate extremes");
+      tr.mark("cand-k1");
+      ohx_extremes_rec rec = *c->h_rec;
+      rec.n = n;
+      finish_extremes(c, d_xy, n, rec, f, s);
+      tr.mark("octagon+plan");
+      // the dropped points are label 0 iff Q is certified inside the true
+      // octagon and holds none of the eight kept points
+      bool ok = region_certified(f.plan, q) && fuse_mode() != 2;
+      f.fuse_state = 4;
+      for (int a = 0; a < 8 && ok; ++a) ok = !in_region_host(q, f.ext.x[a], f.ext.y[a]);
+      if (ok) {
         f.fuse_state = 1;
         if (d_labels) check_cuda(cudaMemsetAsync(d_labels, 0, n, s), "cudaMemsetAsync(labels)");
         filter_core(c, d_xy, n, 0, f.plan, d_labels, f.counts, s, c->d_cand, n_cand);
+        tr.mark("k2-gather");
         f.fused = true;
-        f.candidates = n_cand;
         return f;
       }
+      // not certified: the regular K2 pass over all points
+      filter(c, d_xy, n, 0, f.plan, d_labels, f.counts, s);
+      return f;
     }
-    // not certified (or too many candidates): the regular second pass
-    filter(c, d_xy, n, 0, f.plan, d_labels, f.counts, s);
-    return f;
+    f.fuse_state = 5;  // candidate list overflow: the two-pass path
   }
   // ---- two passes: K1, then K2
   ohx_extremes_rec rec;
@@ -967,11 +1209,11 @@ int ohx_ctx_last_run(const ohx_ctx* ctx, ohx_run_info* info) {
   return guard([&] { *info = ctx->last_run; });
 }
 
-int ohx_ctx_kernel_ms(ohx_ctx* ctx, double ms[3]) {
+int ohx_ctx_kernel_ms(ohx_ctx* ctx, double ms[4]) {
   return guard([&] {
     std::lock_guard<std::mutex> g(ctx->mu);
     bind(ctx);
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < 4; ++k) {
       ms[k] = -1.0;
       if (!ctx->timed[k]) continue;
       float v = 0.f;

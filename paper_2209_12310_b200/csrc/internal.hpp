@@ -98,8 +98,9 @@ struct KFWork {
   unsigned* ticket_unused;
   unsigned* group_counter;
   std::uint64_t* status;
-  std::uint32_t* wt_counts;
-  std::uint8_t* scratch;
+  void* slots;  // 16 B per warp tile: count + first 15 candidate offsets
+  std::uint32_t* wt_counts;  // exact counts of tiles with > 15 candidates
+  std::uint8_t* scratch;     // all offsets of tiles with > 15 candidates
   std::uint64_t nwt;
   std::uint64_t clear_bytes;
   std::uint64_t total_bytes;
@@ -117,6 +118,8 @@ inline KFWork kf_work_layout(void* base, std::uint64_t n) {
   off += ngroups * 8;
   w.clear_bytes = off;
   off = (off + 255) & ~std::uint64_t(255);
+  w.slots = b + off;
+  off += w.nwt * 16;
   w.wt_counts = reinterpret_cast<std::uint32_t*>(b + off);
   off += w.nwt * 4;
   off = (off + 255) & ~std::uint64_t(255);
@@ -128,16 +131,25 @@ inline KFWork kf_work_layout(void* base, std::uint64_t n) {
 // KF: fused extremes + provisional box filter (see kernels.cu).  Re-arms its
 // work area and leaves the candidates' tile counts/offsets in it.
 int kf_grid(int device, std::uint64_t n);
-void launch_kf(const double* d_xy, std::uint64_t n, std::uint64_t base, const double box[4],
-               K1Partial* partials, int grid, unsigned* ticket, ohx_extremes_rec* d_out,
-               void* d_work, cudaStream_t stream);
+// The fused pass's provisional region Q (heuristic; certified inside the
+// true octagon after the pass): x0 <= x <= x1, y0 <= y <= y1,
+// t0 <= fl(x+y) <= t1, d0 <= fl(x-y) <= d1.
+struct KFRegion {
+  double x0, x1, y0, y1, t0, t1, d0, d1;
+};
+
+void launch_kf(const double* d_xy, std::uint64_t n, const KFRegion& q, int grid, void* d_work,
+               cudaStream_t stream);
+// K1 record indices of a gathered candidate buffer -> candidate indices + base
+void launch_map_rec(ohx_extremes_rec* d_rec, const void* d_cand, int idx_bytes,
+                    std::uint64_t base, cudaStream_t stream);
 // the ordered candidate list from KF's work area; d_counts[0] = its length
 void launch_candidates(void* d_work, std::uint64_t n, void* d_cand, int idx_bytes,
                        std::uint64_t cap, unsigned long long* d_counts, cudaStream_t stream);
 void launch_sample(const double* d_xy, std::uint64_t n, int segs, int len, double* d_sample,
                    cudaStream_t stream);
-void launch_count_in_box(const double* d_xy, std::uint64_t n, const double box[4],
-                         unsigned long long* d_count, cudaStream_t stream);
+void launch_count_in_region(const double* d_xy, std::uint64_t n, const KFRegion& q,
+                            unsigned long long* d_count, cudaStream_t stream);
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
                     std::uint64_t cap, const std::uint64_t counts[4], double* d_out,
                     cudaStream_t stream);

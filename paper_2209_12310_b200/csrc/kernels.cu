@@ -23,6 +23,8 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 #include <type_traits>
 
 #include "internal.hpp"
@@ -410,11 +412,30 @@ __device__ __forceinline__ void visit8(WarpExt& w, double (&th)[8], const double
   __syncwarp();
 }
 
+// The chunks a block streams: one contiguous range per block (stride =
+// false), or grid-strided so that the whole grid sweeps the array front to
+// back (stride = true).
+struct ChunkRange {
+  std::uint64_t begin, end, step;
+  __device__ __forceinline__ ChunkRange(std::uint64_t nchunks, bool stride) {
+    if (stride) {
+      begin = blockIdx.x;
+      end = nchunks;
+      step = gridDim.x;
+    } else {
+      const std::uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+      begin = min(nchunks, std::uint64_t(blockIdx.x) * per);
+      end = min(nchunks, begin + per);
+      step = 1;
+    }
+  }
+};
+
 template <typename IdxT>
 __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
     k1_extremes(const double2* __restrict__ pts, std::uint64_t n,
                 std::uint64_t base, K1Partial* partials, unsigned* ticket,
-                ohx_extremes_rec* out) {
+                ohx_extremes_rec* out, bool stride) {
   static_assert(kK1Unroll == 8, "visit8 takes 8 points per lane");
   __shared__ double2 k1_stage[kK1Block / 32][8 * 32];
   __shared__ WarpExt k1_ext[kK1Block / 32];
@@ -425,9 +446,8 @@ __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
   // consecutive addresses per block step, 8 loads in flight per thread)
   constexpr std::uint64_t kChunk = std::uint64_t(kK1Block) * kK1Unroll;
   const std::uint64_t nchunks = (n + kChunk - 1) / kChunk;
-  const std::uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
-  const std::uint64_t c_end = min(nchunks, (blockIdx.x + 1) * per);
-  for (std::uint64_t c = blockIdx.x * per; c < c_end; ++c) {
+  ChunkRange cr(nchunks, stride);
+  for (std::uint64_t c = cr.begin; c < cr.end; c += cr.step) {
     const IdxT j0 = static_cast<IdxT>(c * kChunk + threadIdx.x);
     if ((c + 1) * kChunk <= n) {
       double2 v[kK1Unroll];
@@ -900,31 +920,48 @@ __global__ void __launch_bounds__(kK2cBlock)
 }
 
 // ===================================================================== KF ==
-// Fused single pass (K1 + provisional filter).  While streaming the points
-// for the eight extremes, every point inside a provisional box B (fitted on
-// a sample's octagon before the pass) is dropped and every other point is
-// recorded as a candidate.  Each warp owns 256-point warp tiles (grid-stride,
-// so a thread's indices only grow, as K1's tie rule needs) and compacts its
-// candidates with ballots alone -- no block barrier in the loop: 8-bit tile
-// offsets into the tile's slice of a scratch buffer plus a per-tile count.
-// kf_compact turns those into one ordered candidate list.  After the pass
-// the host checks that B is certified inside the TRUE octagon (exact edge
-// margins) and holds no kept point; then every dropped point provably has
-// the reference label 0 and only the candidates need K2 (gather mode).
-// Otherwise the regular K2 pass runs and only the extremes are used.
+// Fused single pass.  Before the pass the host fits a provisional region Q
+// (an octagon with the slot directions as edge normals) from a sample, with
+// every bound of Q strictly below the sample's value of the matching
+// extremes key (the best for the axis slots, the second for the diagonal
+// ones).  The whole input's best / second can only be larger, so a point
+// inside Q can be neither an extreme, nor tied with one, nor a second-best:
+// the eight extremes and the second-best keys are exactly those of the
+// points OUTSIDE Q (the candidates).  KF therefore only streams the points
+// once, tests Q (2 DADD + 8 DSETP per point, the same rounded keys as K1)
+// and records the candidates, in index order, as 8-bit offsets within each
+// 256-point warp tile (a dense 16-byte slot per tile).  kf_compact turns
+// those into one ordered candidate list, K1 runs on the gathered
+// candidates, and after the octagon is known the host checks that Q lies
+// inside it (exact error bounds) and holds no kept point; then every
+// dropped point has the reference label 0 and only the candidates need K2
+// (gather mode).  Otherwise the regular K2 pass runs over all points.
 constexpr int kKFBlock = 256;
-constexpr int kKFMinBlocks = 2;
+constexpr int kKFMinBlocks = 4;
 constexpr int kWT = 256;  // points per warp tile (8 items x 32 lanes)
 
-// One 256-point warp tile of KF: extremes + provisional box + candidates.
+// Is p inside the provisional region Q?
+__device__ __forceinline__ bool in_region(const KFRegion& q, double2 p) {
+  const double t = __dadd_rn(p.x, p.y);
+  const double d = __dsub_rn(p.x, p.y);
+  return (p.x >= q.x0) & (p.x <= q.x1) & (p.y >= q.y0) & (p.y <= q.y1) & (t >= q.t0) &
+         (t <= q.t1) & (d >= q.d0) & (d <= q.d1);
+}
+
+// One 256-point warp tile (point t0 + it * 32 + lane in item it).  Its
+// candidates' tile offsets, in index order, go to a 16-byte slot per tile
+// (byte 0 the count, bytes 1..15 the first 15 offsets): every tile writes
+// its slot, so the slot array is written densely, in full sectors.  A tile
+// with more than 15 candidates marks its slot 0xFF and spills all offsets to
+// its 256-byte slice of `scratch` and the count to wt_counts (rare unless the
+// region covers the data poorly).  `buf` is the warp's 16 + 256 byte stage.
 template <bool kFullTile>
 __device__ __forceinline__ void kf_tile(const double2* __restrict__ pts, std::uint64_t n,
-                                        std::uint64_t wt, double bx0, double bx1, double by0,
-                                        double by1, WarpExt& we, double (&th)[8],
-                                        std::uint32_t* wt_counts, std::uint8_t* scratch,
-                                        double2* stage) {
+                                        std::uint64_t wt, const KFRegion& q,
+                                        uint4* __restrict__ slots,
+                                        std::uint32_t* __restrict__ wt_counts,
+                                        std::uint8_t* __restrict__ scratch, std::uint8_t* buf) {
   const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
   const std::uint64_t t0 = wt * kWT;
   double2 v[8];
 #pragma unroll
@@ -932,80 +969,69 @@ __device__ __forceinline__ void kf_tile(const double2* __restrict__ pts, std::ui
     const std::uint32_t jl = it * 32 + lane;
     v[it] = (kFullTile || t0 + jl < n) ? ld_stream(pts + t0 + jl) : make_double2(0.0, 0.0);
   }
-  visit8<kFullTile>(we, th, v, t0 + lane, std::uint64_t(32), n, stage);
   std::uint32_t cand = 0;
 #pragma unroll
   for (int it = 0; it < 8; ++it) {
     const bool valid = kFullTile || t0 + it * 32 + lane < n;
-    const bool inbox = v[it].x >= bx0 && v[it].x <= bx1 && v[it].y >= by0 && v[it].y <= by1;
-    cand |= std::uint32_t(valid && !inbox) << it;
+    cand |= std::uint32_t(valid && !in_region(q, v[it])) << it;
   }
-  std::uint32_t c = 0;
-  if (__any_sync(kFull, cand != 0)) {
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const unsigned b = __ballot_sync(kFull, cand >> it & 1u);
-      if (cand >> it & 1u) scratch[t0 + c + __popc(b & lt)] = static_cast<std::uint8_t>(it * 32 + lane);
+  std::uint32_t items = __reduce_or_sync(kFull, cand), c = 0;
+  if (items) {
+    const unsigned lt = (1u << lane) - 1u;
+    while (items) {
+      const int it = __ffs(items) - 1;
+      items &= items - 1;
+      const bool mine = cand >> it & 1u;
+      const unsigned b = __ballot_sync(kFull, mine);
+      if (mine) {
+        const std::uint32_t pos = c + __popc(b & lt);
+        const auto off = static_cast<std::uint8_t>(it * 32 + lane);
+        buf[16 + pos] = off;
+        if (pos < 15) buf[1 + pos] = off;
+      }
       c += __popc(b);
     }
+    __syncwarp();
+    if (c > 15) {
+      for (std::uint32_t k = lane; k < c; k += 32) scratch[t0 + k] = buf[16 + k];
+      if (lane == 0) wt_counts[wt] = c;
+    }
   }
-  if (lane == 0) wt_counts[wt] = c;
+  if (lane == 0) {
+    buf[0] = static_cast<std::uint8_t>(c > 15 ? 0xFF : c);
+    slots[wt] = *reinterpret_cast<const uint4*>(buf);
+  }
+  __syncwarp();  // buf is reused by the next tile
 }
 
-template <typename IdxT>
 __global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
-    kf_extremes_prefilter(const double2* __restrict__ pts, std::uint64_t n, std::uint64_t base,
-                          double bx0, double bx1, double by0, double by1,
-                          K1Partial* partials, unsigned* ticket, ohx_extremes_rec* out,
-                          std::uint32_t* wt_counts, std::uint64_t nwt,
-                          std::uint8_t* scratch) {
-  __shared__ double2 kf_stage[kKFBlock / 32][8 * 32];
-  __shared__ WarpExt kf_ext[kKFBlock / 32];
-  WarpExt& we = kf_ext[threadIdx.x >> 5];
-  double th[8];
-  warp_ext_init(we, th);
-  // each block streams one contiguous range of 2048-point chunks, warp w
-  // taking the chunk's w-th 256-point warp tile (32 KB of consecutive
-  // addresses per block step, as in K1)
+    kf_filter(const double2* __restrict__ pts, std::uint64_t n, const KFRegion q,
+              uint4* __restrict__ slots, std::uint32_t* __restrict__ wt_counts, std::uint64_t nwt,
+              std::uint8_t* __restrict__ scratch, bool stride) {
+  __shared__ __align__(16) std::uint8_t kf_buf[kKFBlock / 32][16 + kWT];
+  std::uint8_t* buf = kf_buf[threadIdx.x >> 5];
+  // blocks stream 2048-point chunks, warp w taking the chunk's w-th warp tile
   constexpr std::uint64_t kChunkTiles = kKFBlock / 32;
   const std::uint64_t nchunks = (nwt + kChunkTiles - 1) / kChunkTiles;
-  const std::uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
-  const std::uint64_t c_end = min(nchunks, (blockIdx.x + 1) * per);
   const std::uint64_t nfull = n / kWT;  // every warp tile but possibly the last is full
-  for (std::uint64_t ch = blockIdx.x * per; ch < c_end; ++ch) {
+  ChunkRange cr(nchunks, stride);
+  for (std::uint64_t ch = cr.begin; ch < cr.end; ch += cr.step) {
     const std::uint64_t wt = ch * kChunkTiles + (threadIdx.x >> 5);
-    if (wt < nfull) kf_tile<true>(pts, n, wt, bx0, bx1, by0, by1, we, th, wt_counts, scratch,
-                                   kf_stage[threadIdx.x >> 5]);
-    else if (wt < nwt) kf_tile<false>(pts, n, wt, bx0, bx1, by0, by1, we, th, wt_counts, scratch,
-                                       kf_stage[threadIdx.x >> 5]);
-  }
-
-  __syncwarp();
-  ArgState<8, 4> st = warp_ext_state(we);
-  block_reduce<8, 4, kKFBlock, true>(st);
-  if (!grid_combine<8, 4, kKFBlock>(st, partials, ticket)) return;
-  if (threadIdx.x < 8) {
-    const int a = threadIdx.x;
-    double k = 0, s2 = 0;
-    std::uint64_t i = 0;
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-      if (b == a) {
-        k = st.k[b];
-        i = st.i[b];
-        if (b >= 4) s2 = st.s[b - 4];
-      }
-    const double2 p = pts[i];
-    out->key[a] = k;
-    out->idx[a] = base + i;
-    out->x[a] = p.x;
-    out->y[a] = p.y;
-    if (a >= 4) out->second[a - 4] = s2;
-    if (a == 0) out->n = n;
+    if (wt < nfull) kf_tile<true>(pts, n, wt, q, slots, wt_counts, scratch, buf);
+    else if (wt < nwt) kf_tile<false>(pts, n, wt, q, slots, wt_counts, scratch, buf);
   }
 }
 
-// Ordered candidate list from KF's warp-tile counts: groups of 1024 tiles
+// K1's record indices refer to the gathered candidate buffer: map them back
+// to the candidates' (shard-local) indices, + base.
+template <typename IdxT>
+__global__ void map_rec_idx(ohx_extremes_rec* rec, const IdxT* __restrict__ cand,
+                            std::uint64_t base) {
+  const int a = threadIdx.x;
+  if (a < 8) rec->idx[a] = base + static_cast<std::uint64_t>(cand[rec->idx[a]]);
+}
+
+// Ordered candidate list from KF's per-tile slots: groups of 1024 tiles
 // (4 per thread), block scan + decoupled look-back across groups, then a
 // flattened copy (binary search over the group's tile prefix).
 constexpr int kKFcBlock = 256;
@@ -1013,12 +1039,13 @@ constexpr int kKFcTiles = 4 * kKFcBlock;
 
 template <typename IdxT>
 __global__ void __launch_bounds__(kKFcBlock)
-    kf_compact(const std::uint32_t* __restrict__ wt_counts, std::uint64_t nwt,
-               const std::uint8_t* __restrict__ scratch, std::uint64_t* status,
-               unsigned* group_counter, IdxT* cand, std::uint64_t cap,
+    kf_compact(const uint4* __restrict__ slots, const std::uint32_t* __restrict__ wt_counts,
+               std::uint64_t nwt, const std::uint8_t* __restrict__ scratch,
+               std::uint64_t* status, unsigned* group_counter, IdxT* cand, std::uint64_t cap,
                unsigned long long* counts) {
   __shared__ std::uint32_t s_group;
   __shared__ std::uint32_t s_pre[kKFcTiles];
+  __shared__ uint4 s_slot[kKFcTiles];
   __shared__ std::uint32_t s_warp[kKFcBlock / 32];
   __shared__ std::uint64_t s_excl;
   __shared__ std::uint32_t s_total;
@@ -1031,7 +1058,10 @@ __global__ void __launch_bounds__(kKFcBlock)
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const std::uint64_t t = g * kKFcTiles + threadIdx.x * 4 + r;
-    c[r] = t < nwt ? wt_counts[t] : 0u;
+    const uint4 sl = t < nwt ? slots[t] : make_uint4(0, 0, 0, 0);
+    s_slot[threadIdx.x * 4 + r] = sl;
+    const std::uint32_t b0 = sl.x & 0xFFu;
+    c[r] = b0 == 0xFFu ? wt_counts[t] : b0;
     sum += c[r];
   }
   std::uint32_t incl = sum;
@@ -1079,6 +1109,7 @@ __global__ void __launch_bounds__(kKFcBlock)
   __syncthreads();
   const std::uint32_t total = s_total;
   const std::uint64_t excl = s_excl;
+  const auto* sb = reinterpret_cast<const std::uint8_t*>(s_slot);
   for (std::uint32_t k = threadIdx.x; k < total; k += kKFcBlock) {
     int lo = 0, hi = kKFcTiles - 1;  // the last tile whose prefix is <= k
 #pragma unroll
@@ -1089,18 +1120,20 @@ __global__ void __launch_bounds__(kKFcBlock)
     }
     const std::uint64_t t = g * kKFcTiles + lo;
     const std::uint32_t e = k - s_pre[lo];
-    if (excl + k < cap) cand[excl + k] = static_cast<IdxT>(t * kWT + scratch[t * kWT + e]);
+    const std::uint8_t* sl = sb + 16 * lo;
+    const std::uint32_t off = sl[0] == 0xFFu ? scratch[t * kWT + e] : sl[1 + e];
+    if (excl + k < cap) cand[excl + k] = static_cast<IdxT>(t * kWT + off);
   }
 }
 
-// ============================================================= K1 / KF (TMA) ==
-// The streaming pass of K1 (kPrefilter = false) and of the fused KF
-// (kPrefilter = true) fed by TMA bulk copies: each block owns a contiguous
-// range of 2048-point (32 KB) chunks and keeps kSStages of them in flight in
-// shared memory (cp.async.bulk + mbarrier), so the bytes in flight no longer
-// depend on registers.  Warp w processes the chunk's w-th 256-point tile
-// straight from shared memory (conflict-free 16-byte loads); the warp-
-// uniform extremes update reads its points from the same buffer.
+// ====================================================== K1 (TMA variant) ==
+// K1's streaming pass fed by TMA bulk copies (OHX_STREAM=tma; the register-
+// staged k1_extremes is the default -- it measured faster on B200): each
+// block owns a contiguous range of 2048-point (32 KB) chunks and keeps
+// kSStages of them in flight in shared memory (cp.async.bulk + mbarrier).
+// Warp w processes the chunk's w-th 256-point tile straight from shared
+// memory; the warp-uniform extremes update reads its points from the same
+// buffer.
 constexpr int kSBlock = 256;
 constexpr int kSChunk = 2048;
 constexpr int kSStages = 3;
@@ -1111,47 +1144,12 @@ struct StreamSmem {
   WarpExt ext[kSBlock / 32];
 };
 
-template <bool kPrefilter, bool kFullTile>
-__device__ __forceinline__ void stream_tile(const double2* tile, std::uint64_t t0, std::uint64_t n,
-                                            std::uint64_t wt, double bx0, double bx1, double by0,
-                                            double by1, WarpExt& we, double (&th)[8],
-                                            std::uint32_t* wt_counts, std::uint8_t* scratch) {
-  const int lane = threadIdx.x & 31;
-  double2 v[8];
-#pragma unroll
-  for (int it = 0; it < 8; ++it) v[it] = tile[it * 32 + lane];
-  visit8<kFullTile>(we, th, v, t0 + lane, std::uint64_t(32), n, const_cast<double2*>(tile));
-  if constexpr (kPrefilter) {
-    const unsigned lt = (1u << lane) - 1u;
-    std::uint32_t cand = 0;
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const bool valid = kFullTile || t0 + it * 32 + lane < n;
-      const bool inbox = v[it].x >= bx0 && v[it].x <= bx1 && v[it].y >= by0 && v[it].y <= by1;
-      cand |= std::uint32_t(valid && !inbox) << it;
-    }
-    std::uint32_t c = 0;
-    if (__any_sync(kFull, cand != 0)) {
-#pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const unsigned b = __ballot_sync(kFull, cand >> it & 1u);
-        if (cand >> it & 1u)
-          scratch[t0 + c + __popc(b & lt)] = static_cast<std::uint8_t>(it * 32 + lane);
-        c += __popc(b);
-      }
-    }
-    if (lane == 0) wt_counts[wt] = c;
-  }
-}
-
-template <bool kPrefilter>
 __global__ void __launch_bounds__(kSBlock, 2)
-    k_stream(const double2* __restrict__ pts, std::uint64_t n, std::uint64_t base, double bx0,
-             double bx1, double by0, double by1, K1Partial* partials, unsigned* ticket,
-             ohx_extremes_rec* out, std::uint32_t* wt_counts, std::uint8_t* scratch) {
+    k1_stream_tma(const double2* __restrict__ pts, std::uint64_t n, std::uint64_t base,
+                  K1Partial* partials, unsigned* ticket, ohx_extremes_rec* out) {
   extern __shared__ __align__(128) unsigned char k_stream_smem[];
   StreamSmem& S = *reinterpret_cast<StreamSmem*>(k_stream_smem);
-  const int warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpExt& we = S.ext[warp];
   double th[8];
   warp_ext_init(we, th);
@@ -1175,15 +1173,14 @@ __global__ void __launch_bounds__(kSBlock, 2)
     const int st = static_cast<int>(k % kSStages);
     mbar_wait(&S.bar[st], static_cast<unsigned>((k / kSStages) & 1));
     const std::uint64_t t0 = c * kSChunk + std::uint64_t(warp) * 256;  // this warp's tile
-    const std::uint64_t wt = c * (kSChunk / 256) + warp;
-    const double2* tile = S.buf[st] + warp * 256;
-    if (t0 + 256 <= n)
-      stream_tile<kPrefilter, true>(tile, t0, n, wt, bx0, bx1, by0, by1, we, th, wt_counts, scratch);
-    else if (t0 < n)
-      stream_tile<kPrefilter, false>(tile, t0, n, wt, bx0, bx1, by0, by1, we, th, wt_counts,
-                                     scratch);
-    else if (kPrefilter && (threadIdx.x & 31) == 0 && wt < (n + 255) / 256)
-      wt_counts[wt] = 0;
+    double2* tile = S.buf[st] + warp * 256;
+    if (t0 < n) {
+      double2 v[8];
+#pragma unroll
+      for (int it = 0; it < 8; ++it) v[it] = tile[it * 32 + lane];
+      if (t0 + 256 <= n) visit8<true>(we, th, v, t0 + lane, std::uint64_t(32), n, tile);
+      else visit8<false>(we, th, v, t0 + lane, std::uint64_t(32), n, tile);
+    }
     __syncthreads();  // every warp is done with stage st
     if (threadIdx.x == 0 && c + kSStages < c1) {
       fence_proxy_async_smem();  // order the generic reads before the async refill
@@ -1215,7 +1212,7 @@ __global__ void __launch_bounds__(kSBlock, 2)
   }
 }
 
-// A sample for the provisional box: `segs` runs of `len` consecutive points
+// A sample for the provisional region: `segs` runs of `len` consecutive points
 // at evenly spaced offsets (coalesced reads, 16 MB for the default 256 x 4096).
 __global__ void gather_sample(const double2* __restrict__ pts, std::uint64_t n, int len,
                               double2* __restrict__ out) {
@@ -1225,15 +1222,13 @@ __global__ void gather_sample(const double2* __restrict__ pts, std::uint64_t n, 
     out[std::uint64_t(blockIdx.x) * len + k] = pts[start + k];
 }
 
-// Number of points of `pts` inside the box (sample coverage estimate).
-__global__ void count_in_box(const double2* __restrict__ pts, std::uint64_t n, double bx0,
-                             double bx1, double by0, double by1, unsigned long long* count) {
+// Number of points of `pts` inside the region Q (sample coverage estimate).
+__global__ void count_in_region(const double2* __restrict__ pts, std::uint64_t n,
+                                const KFRegion q, unsigned long long* count) {
   unsigned c = 0;
   for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
-       k += std::uint64_t(gridDim.x) * blockDim.x) {
-    const double2 p = pts[k];
-    c += p.x >= bx0 && p.x <= bx1 && p.y >= by0 && p.y <= by1;
-  }
+       k += std::uint64_t(gridDim.x) * blockDim.x)
+    c += in_region(q, pts[k]);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(kFull, c, off);
   if ((threadIdx.x & 31) == 0) atomicAdd(count, static_cast<unsigned long long>(c));
@@ -1264,7 +1259,22 @@ __global__ void gather_xy4(const double2* __restrict__ pts, const IdxT* __restri
 }  // namespace
 
 // ============================================================ launchers ==
-static int stream_grid(int device, std::uint64_t n) {
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+
+// OHX_ORDER=stride: grid-strided chunk order for K1/KF (default: one
+// contiguous range per block).  Experiment switches.
+static bool chunk_stride() {
+  static const bool v = [] {
+    const char* e = std::getenv("OHX_ORDER");
+    return e && std::string(e) == "stride";
+  }();
+  return v;
+}
+
+static int tma_grid(int device, std::uint64_t n) {
   int sms = 0;
   check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device),
              "cudaDeviceGetAttribute");
@@ -1273,32 +1283,67 @@ static int stream_grid(int device, std::uint64_t n) {
   return static_cast<int>(nchunks < full ? (nchunks > 0 ? nchunks : 1) : full);
 }
 
-template <bool kPrefilter>
-static void stream_launch(const double* d_xy, std::uint64_t n, std::uint64_t base,
-                          const double box[4], K1Partial* partials, int grid, unsigned* ticket,
-                          ohx_extremes_rec* d_out, std::uint32_t* wt_counts,
-                          std::uint8_t* scratch, cudaStream_t stream) {
+static void k1_tma_launch(const double* d_xy, std::uint64_t n, std::uint64_t base,
+                          K1Partial* partials, int grid, unsigned* ticket,
+                          ohx_extremes_rec* d_out, cudaStream_t stream) {
   constexpr int smem = sizeof(StreamSmem);
   static bool configured = false;
   if (!configured) {
-    check_cuda(cudaFuncSetAttribute(k_stream<kPrefilter>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-               "cudaFuncSetAttribute(k_stream)");
+    check_cuda(cudaFuncSetAttribute(k1_stream_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem),
+               "cudaFuncSetAttribute(k1_stream_tma)");
     configured = true;
   }
-  k_stream<kPrefilter><<<grid, kSBlock, smem, stream>>>(
-      reinterpret_cast<const double2*>(d_xy), n, base, box ? box[0] : 0.0, box ? box[1] : 0.0,
-      box ? box[2] : 0.0, box ? box[3] : 0.0, partials, ticket, d_out, wt_counts, scratch);
-  check_cuda(cudaGetLastError(), "k_stream launch");
+  k1_stream_tma<<<grid, kSBlock, smem, stream>>>(reinterpret_cast<const double2*>(d_xy), n, base,
+                                                 partials, ticket, d_out);
+  check_cuda(cudaGetLastError(), "k1_stream_tma launch");
 }
 
-int k1_grid(int device, std::uint64_t n) { return stream_grid(device, n); }
+// OHX_STREAM selects K1's streaming implementation: unset/"reg" = the
+// register-staged loads (default), "tma" = the cp.async.bulk pipeline.
+static bool stream_tma() {
+  static const bool tma = [] {
+    const char* e = std::getenv("OHX_STREAM");
+    return e && std::string(e) == "tma";
+  }();
+  return tma;
+}
+
+template <typename K>
+static int occupancy_grid(int device, K kernel, int block, std::uint64_t need) {
+  int sms = 0, per_sm = 0;
+  check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device),
+             "cudaDeviceGetAttribute");
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0),
+             "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  if (per_sm < 1) per_sm = 1;
+  const std::uint64_t full = std::uint64_t(sms) * per_sm;
+  return static_cast<int>(need < full ? (need > 0 ? need : 1) : full);
+}
+
+int k1_grid(int device, std::uint64_t n) {
+  if (stream_tma()) return tma_grid(device, n);
+  return occupancy_grid(device, k1_extremes<std::uint32_t>, kK1Block,
+                        (n + kK1Block * kK1Unroll - 1) / (kK1Block * kK1Unroll));
+}
 
 void launch_k1(const double* d_xy, std::uint64_t n, std::uint64_t base,
                K1Partial* partials, int grid, unsigned* ticket,
                ohx_extremes_rec* d_out, cudaStream_t stream) {
-  stream_launch<false>(d_xy, n, base, nullptr, partials, grid, ticket, d_out, nullptr, nullptr,
-                       stream);
+  if (stream_tma()) {
+    k1_tma_launch(d_xy, n, base, partials, grid, ticket, d_out, stream);
+    return;
+  }
+  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  // 32-bit in-loop indices whenever the shard (plus a full grid stride of
+  // overshoot) fits
+  if (n + std::uint64_t(kK1Block) * kK1Unroll < 0xffffffffull)
+    k1_extremes<std::uint32_t><<<grid, kK1Block, 0, stream>>>(pts, n, base, partials, ticket, d_out,
+                                                              chunk_stride());
+  else
+    k1_extremes<std::uint64_t><<<grid, kK1Block, 0, stream>>>(pts, n, base, partials, ticket, d_out,
+                                                              chunk_stride());
+  check_cuda(cudaGetLastError(), "k1_extremes launch");
 }
 
 void launch_k1b(const double* d_xy, std::uint64_t n, std::uint64_t base,
@@ -1362,15 +1407,35 @@ void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_w
   }
 }
 
-int kf_grid(int device, std::uint64_t n) { return stream_grid(device, n); }
+int kf_grid(int device, std::uint64_t n) {
+  const std::uint64_t nwt = (n + kWT - 1) / kWT;
+  int g = occupancy_grid(device, kf_filter, kKFBlock, (nwt + kKFBlock / 32 - 1) / (kKFBlock / 32));
+  static const int bps = env_int("OHX_KF_BPS", 0);  // cap on blocks per SM
+  if (bps > 0) {
+    int sms = 0;
+    check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    g = std::min(g, sms * bps);
+  }
+  return g;
+}
 
-void launch_kf(const double* d_xy, std::uint64_t n, std::uint64_t base, const double box[4],
-               K1Partial* partials, int grid, unsigned* ticket, ohx_extremes_rec* d_out,
-               void* d_work, cudaStream_t stream) {
+void launch_kf(const double* d_xy, std::uint64_t n, const KFRegion& q, int grid, void* d_work,
+               cudaStream_t stream) {
   const KFWork w = kf_work_layout(d_work, n);
   check_cuda(cudaMemsetAsync(d_work, 0, w.clear_bytes, stream), "cudaMemsetAsync(kf work)");
-  stream_launch<true>(d_xy, n, base, box, partials, grid, ticket, d_out, w.wt_counts, w.scratch,
-                      stream);
+  kf_filter<<<grid, kKFBlock, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n, q,
+                                           reinterpret_cast<uint4*>(w.slots), w.wt_counts, w.nwt,
+                                           w.scratch, chunk_stride());
+  check_cuda(cudaGetLastError(), "kf_filter launch");
+}
+
+void launch_map_rec(ohx_extremes_rec* d_rec, const void* d_cand, int idx_bytes,
+                    std::uint64_t base, cudaStream_t stream) {
+  if (idx_bytes == 4)
+    map_rec_idx<<<1, 32, 0, stream>>>(d_rec, static_cast<const std::uint32_t*>(d_cand), base);
+  else
+    map_rec_idx<<<1, 32, 0, stream>>>(d_rec, static_cast<const std::uint64_t*>(d_cand), base);
+  check_cuda(cudaGetLastError(), "map_rec_idx launch");
 }
 
 void launch_candidates(void* d_work, std::uint64_t n, void* d_cand, int idx_bytes,
@@ -1379,11 +1444,11 @@ void launch_candidates(void* d_work, std::uint64_t n, void* d_cand, int idx_byte
   const unsigned ngroups = static_cast<unsigned>((w.nwt + kKFcTiles - 1) / kKFcTiles);
   if (idx_bytes == 4)
     kf_compact<std::uint32_t><<<ngroups, kKFcBlock, 0, stream>>>(
-        w.wt_counts, w.nwt, w.scratch, w.status, w.group_counter,
+        reinterpret_cast<const uint4*>(w.slots), w.wt_counts, w.nwt, w.scratch, w.status, w.group_counter,
         static_cast<std::uint32_t*>(d_cand), cap, d_counts);
   else
     kf_compact<std::uint64_t><<<ngroups, kKFcBlock, 0, stream>>>(
-        w.wt_counts, w.nwt, w.scratch, w.status, w.group_counter,
+        reinterpret_cast<const uint4*>(w.slots), w.wt_counts, w.nwt, w.scratch, w.status, w.group_counter,
         static_cast<std::uint64_t*>(d_cand), cap, d_counts);
   check_cuda(cudaGetLastError(), "kf_compact launch");
 }
@@ -1395,13 +1460,12 @@ void launch_sample(const double* d_xy, std::uint64_t n, int segs, int len, doubl
   check_cuda(cudaGetLastError(), "gather_sample launch");
 }
 
-void launch_count_in_box(const double* d_xy, std::uint64_t n, const double box[4],
-                         unsigned long long* d_count, cudaStream_t stream) {
+void launch_count_in_region(const double* d_xy, std::uint64_t n, const KFRegion& q,
+                            unsigned long long* d_count, cudaStream_t stream) {
   check_cuda(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), stream), "cudaMemsetAsync");
   const unsigned grid = static_cast<unsigned>(n / (256 * 16) + 1 < 1184 ? n / (256 * 16) + 1 : 1184);
-  count_in_box<<<grid, 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n, box[0], box[1],
-                                         box[2], box[3], d_count);
-  check_cuda(cudaGetLastError(), "count_in_box launch");
+  count_in_region<<<grid, 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n, q, d_count);
+  check_cuda(cudaGetLastError(), "count_in_region launch");
 }
 
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,

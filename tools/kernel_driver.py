@@ -21,11 +21,25 @@ ap.add_argument("--n", type=float, default=1e8)
 ap.add_argument("--seed", type=int, default=7)
 ap.add_argument("--distort", type=float, default=0.0)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--pipeline", action="store_true",
+                help="time the whole device pipeline (fused pass when it applies)")
 a = ap.parse_args()
 n = int(a.n)
 pts = P.generate(a.dist, n, a.seed, a.distort)
 d = torch.from_numpy(pts).cuda()
 ctx = P.Context(0)
+if a.pipeline:
+    import time
+    for _ in range(a.reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hull, _ = ctx.heaphull_device(d, n)
+        t1 = time.perf_counter()
+        info = ctx.last_run()
+        print(a.dist, n, "pipeline ms %.3f" % ((t1 - t0) * 1e3), "h", len(hull), "fused", info["fused"],
+              info["fuse_state"], "cand", info["candidates"], "cov %.4f" % info["sample_coverage"],
+              ctx.kernel_ms(), flush=True)
+    sys.exit(0)
 for _ in range(a.reps):
     rec = ctx.extremes(d, n)
     ext, mask = P.resolve_extremes(rec)
