@@ -67,6 +67,10 @@ struct ohx_ctx {
   std::uint64_t sample_bytes = 0;
   void* d_cand = nullptr;
   std::uint64_t cand_bytes = 0;
+  void* d_regions = nullptr;  // KF per-warp candidate regions
+  std::uint64_t regions_bytes = 0;
+  double* d_cpts = nullptr;  // gathered candidate coordinates
+  std::uint64_t cpts_bytes = 0;
   unsigned long long* d_cnt = nullptr;
   unsigned long long* h_cnt = nullptr;  // pinned
 
@@ -564,7 +568,8 @@ KPlan make_kplan(const ohx_filter_plan& plan, std::uint64_t base, std::uint64_t 
 // candidates listed there (shard-local indices, same width as the queues).
 void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
                  const ohx_filter_plan& plan, std::uint8_t* d_labels, std::uint64_t counts[4],
-                 cudaStream_t s, const void* d_cand, std::uint64_t n_cand) {
+                 cudaStream_t s, const void* d_cand, std::uint64_t n_cand,
+                 const double* d_cpts) {
   const KPlan kp = make_kplan(plan, base, n);
   const std::uint64_t items = d_cand ? n_cand : n;
   const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
@@ -584,7 +589,7 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
       dev_grow(&c->d_queues, &c->queue_bytes, 4ull * idx_bytes * cap, "queues");
       check_cuda(cudaEventRecord(c->ev[2][0], s), "cudaEventRecord");
       launch_k2(d_xy, items, kp, c->d_status, ntiles, c->d_queues, idx_bytes, cap, d_labels,
-                c->d_counts, s, d_cand);  // k2_filter + k2_compact
+                c->d_counts, s, d_cand, d_cpts);  // k2_filter + k2_compact
       check_cuda(cudaEventRecord(c->ev[2][1], s), "cudaEventRecord");
       c->timed[2] = true;
       c->launches += 2;
@@ -615,7 +620,7 @@ void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
             const ohx_filter_plan& plan, std::uint8_t* d_labels, std::uint64_t counts[4],
             cudaStream_t s) {
   if (n == 0) throw std::invalid_argument("classify_points: empty point set");
-  filter_core(c, d_xy, n, base, plan, d_labels, counts, s, nullptr, 0);
+  filter_core(c, d_xy, n, base, plan, d_labels, counts, s, nullptr, 0, nullptr);
 }
 
 // Vertices of the convex polygon {p : key_a(p) <= b[a], a = 0..7} (the slot
@@ -918,6 +923,7 @@ bool fit_region(const std::vector<P2>& R, const double lim[8], KFRegion* q) {
 
 // The provisional region of the fused pass.  A 1M-point sample (kSampleSegs
 // runs of kSampleLen consecutive points) is split into kSubSamples disjoint
+// (interleaved: run b goes to sub-sample b % kSubSamples)
 // sub-samples; each one's eight extremes give an octagon, and Q is fitted
 // inside the INTERSECTION of those octagons.  The sub-sample octagons
 // scatter the way the true octagon may sit relative to any one sample's, so
@@ -936,7 +942,7 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   dev_grow(reinterpret_cast<void**>(&c->d_sample), &c->sample_bytes,
            ns * 16 + kSubSamples * sizeof(ohx_extremes_rec), "sample");
   auto* d_recs = reinterpret_cast<ohx_extremes_rec*>(c->d_sample + 2 * ns);
-  launch_sample(d_xy, n, kSampleSegs, kSampleLen, c->d_sample, s);
+  launch_sample(d_xy, n, kSampleSegs, kSampleLen, kSubSamples, c->d_sample, s);
   ++c->launches;
   const int grid = k1_grid(c->device, nsub);
   ensure_partials(c, grid);
@@ -1035,37 +1041,43 @@ FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
   if (fuse) {
     // ---- fused: one streaming pass filters Q; the extremes come from the
     // candidates (the points outside Q) alone
-    const KFWork wl = kf_work_layout(nullptr, n);
-    dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes, wl.total_bytes,
-             "kf work area");
     const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
-    // room for 1.5x the sample's miss rate (+1M); more candidates than that
-    // fall back to the two-pass path
-    const std::uint64_t cap = std::min<std::uint64_t>(
-        n, (1u << 20) + static_cast<std::uint64_t>(1.5 * (1.0 - f.sample_coverage) * double(n)));
-    dev_grow(&c->d_cand, &c->cand_bytes, cap * idx_bytes, "candidates");
+    const int grid = kf_grid(c->device);
+    const std::uint64_t nw = std::uint64_t(grid) * kKFWarpsPerBlock;
+    const std::uint64_t per = ((n + 255) / 256 + nw - 1) / nw * 256;  // points per warp
+    // room for 1.5x the sample's miss rate (+256) per warp region; a region
+    // that overflows sends the call down the two-pass path
+    const std::uint64_t cap_w = std::min<std::uint64_t>(
+        per, 256 + static_cast<std::uint64_t>(1.5 * (1.0 - f.sample_coverage) * double(per)));
+    dev_grow(&c->d_regions, &c->regions_bytes, nw * cap_w * idx_bytes, "kf regions");
+    dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes, nw * 12 + 16,
+             "kf counts");
+    auto* d_wcounts = reinterpret_cast<std::uint32_t*>(c->d_status);
+    auto* d_offsets = c->d_status + (nw + 1) / 2;  // 8-byte aligned after the u32 counts
     check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
-    launch_kf(d_xy, n, q, kf_grid(c->device, n), c->d_status, s);
+    launch_kf(d_xy, n, q, grid, c->d_regions, idx_bytes, cap_w, d_wcounts, s);
     check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
     c->timed[0] = true;
     ++c->launches;
     check_cuda(cudaEventRecord(c->ev[3][0], s), "cudaEventRecord");
-    launch_candidates(c->d_status, n, c->d_cand, idx_bytes, cap, c->d_counts, s);
+    launch_kf_scan(d_wcounts, nw, cap_w, d_offsets, c->d_counts, s);
     ++c->launches;
     check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
     check_cuda(cudaStreamSynchronize(s), "kf candidates");
-    tr.mark("kf+compact");
+    tr.mark("kf+scan");
     const std::uint64_t n_cand = c->h_counts[0];
     f.candidates = n_cand;
-    if (n_cand >= 1 && n_cand <= cap) {
-      // K1 over the gathered candidates, record indices mapped back
-      dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, n_cand * 16,
+    if (n_cand >= 1 && c->h_counts[1] == 0) {
+      // ordered candidate list + coordinates; K1 over them, indices mapped back
+      dev_grow(&c->d_cand, &c->cand_bytes, n_cand * idx_bytes, "candidates");
+      dev_grow(reinterpret_cast<void**>(&c->d_cpts), &c->cpts_bytes, n_cand * 16,
                "candidate points");
-      launch_gather(d_xy, c->d_cand, idx_bytes, n_cand, c->d_gather, s);
-      const int grid = k1_grid(c->device, n_cand);
-      ensure_partials(c, grid);
-      launch_k1(c->d_gather, n_cand, 0, c->d_partials, grid, c->d_ticket, c->d_rec, s);
+      launch_kf_gather(d_xy, c->d_regions, idx_bytes, cap_w, d_wcounts, d_offsets, nw, c->d_cand,
+                       c->d_cpts, s);
+      const int k1g = k1_grid(c->device, n_cand);
+      ensure_partials(c, k1g);
+      launch_k1(c->d_cpts, n_cand, 0, c->d_partials, k1g, c->d_ticket, c->d_rec, s);
       launch_map_rec(c->d_rec, c->d_cand, idx_bytes, 0, s);
       c->launches += 3;
       check_cuda(cudaEventRecord(c->ev[3][1], s), "cudaEventRecord");
@@ -1086,7 +1098,7 @@ FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
       if (ok) {
         f.fuse_state = 1;
         if (d_labels) check_cuda(cudaMemsetAsync(d_labels, 0, n, s), "cudaMemsetAsync(labels)");
-        filter_core(c, d_xy, n, 0, f.plan, d_labels, f.counts, s, c->d_cand, n_cand);
+        filter_core(c, d_xy, n, 0, f.plan, d_labels, f.counts, s, c->d_cand, n_cand, c->d_cpts);
         tr.mark("k2-gather");
         f.fused = true;
         return f;
@@ -1095,7 +1107,7 @@ FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
       filter(c, d_xy, n, 0, f.plan, d_labels, f.counts, s);
       return f;
     }
-    f.fuse_state = 5;  // candidate list overflow: the two-pass path
+    f.fuse_state = 5;  // a warp region overflowed: the two-pass path
   }
   // ---- two passes: K1, then K2
   ohx_extremes_rec rec;
@@ -1145,7 +1157,8 @@ void destroy_ctx(ohx_ctx* c) {
                   static_cast<void*>(c->d_counts), static_cast<void*>(c->d_status),
                   c->d_queues, static_cast<void*>(c->d_pts),
                   static_cast<void*>(c->d_labels), static_cast<void*>(c->d_gather),
-                  static_cast<void*>(c->d_sample), c->d_cand, static_cast<void*>(c->d_cnt)})
+                  static_cast<void*>(c->d_sample), c->d_cand, static_cast<void*>(c->d_cnt),
+                  c->d_regions, static_cast<void*>(c->d_cpts)})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_crec),
                   static_cast<void*>(c->h_counts), static_cast<void*>(c->h_cnt)})

@@ -89,48 +89,7 @@ inline std::uint64_t k2_work_bytes(std::uint64_t ntiles) {
 void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_work,
                std::uint64_t ntiles, void* d_queues, int idx_bytes, std::uint64_t cap,
                std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream,
-               const void* d_gather = nullptr);
-// KF work area: [2 counters | kf_compact look-back words (1 per group of
-// 1024 warp tiles) | per-warp-tile candidate counts (u32 per 256 points) |
-// 8-bit candidate offsets (one slot per point)].
-constexpr std::uint64_t kKFWarpTile = 256, kKFGroupTiles = 1024;
-struct KFWork {
-  unsigned* ticket_unused;
-  unsigned* group_counter;
-  std::uint64_t* status;
-  void* slots;  // 16 B per warp tile: count + first 15 candidate offsets
-  std::uint32_t* wt_counts;  // exact counts of tiles with > 15 candidates
-  std::uint8_t* scratch;     // all offsets of tiles with > 15 candidates
-  std::uint64_t nwt;
-  std::uint64_t clear_bytes;
-  std::uint64_t total_bytes;
-};
-inline KFWork kf_work_layout(void* base, std::uint64_t n) {
-  KFWork w;
-  w.nwt = (n + kKFWarpTile - 1) / kKFWarpTile;
-  const std::uint64_t ngroups = (w.nwt + kKFGroupTiles - 1) / kKFGroupTiles;
-  auto* b = static_cast<unsigned char*>(base);
-  std::uint64_t off = 0;
-  w.ticket_unused = reinterpret_cast<unsigned*>(b);
-  w.group_counter = reinterpret_cast<unsigned*>(b + 4);
-  off += 256;
-  w.status = reinterpret_cast<std::uint64_t*>(b + off);
-  off += ngroups * 8;
-  w.clear_bytes = off;
-  off = (off + 255) & ~std::uint64_t(255);
-  w.slots = b + off;
-  off += w.nwt * 16;
-  w.wt_counts = reinterpret_cast<std::uint32_t*>(b + off);
-  off += w.nwt * 4;
-  off = (off + 255) & ~std::uint64_t(255);
-  w.scratch = b + off;
-  off += w.nwt * kKFWarpTile;
-  w.total_bytes = off;
-  return w;
-}
-// KF: fused extremes + provisional box filter (see kernels.cu).  Re-arms its
-// work area and leaves the candidates' tile counts/offsets in it.
-int kf_grid(int device, std::uint64_t n);
+               const void* d_gather = nullptr, const double* d_gather_xy = nullptr);
 // The fused pass's provisional region Q (heuristic; certified inside the
 // true octagon after the pass): x0 <= x <= x1, y0 <= y <= y1,
 // t0 <= fl(x+y) <= t1, d0 <= fl(x-y) <= d1.
@@ -138,16 +97,24 @@ struct KFRegion {
   double x0, x1, y0, y1, t0, t1, d0, d1;
 };
 
-void launch_kf(const double* d_xy, std::uint64_t n, const KFRegion& q, int grid, void* d_work,
+// KF: blocks of the fused filter pass (occupancy-sized, one warp per range)
+int kf_grid(int device);
+constexpr int kKFWarpsPerBlock = 8;
+void launch_kf(const double* d_xy, std::uint64_t n, const KFRegion& q, int grid, void* d_regions,
+               int idx_bytes, std::uint64_t cap_w, std::uint32_t* d_warp_counts,
                cudaStream_t stream);
+// d_counts[0] = candidates, d_counts[1] = 1 if some warp region overflowed
+void launch_kf_scan(const std::uint32_t* d_warp_counts, std::uint64_t nw, std::uint64_t cap_w,
+                    std::uint64_t* d_offsets, unsigned long long* d_counts, cudaStream_t stream);
+void launch_kf_gather(const double* d_xy, const void* d_regions, int idx_bytes,
+                      std::uint64_t cap_w, const std::uint32_t* d_warp_counts,
+                      const std::uint64_t* d_offsets, std::uint64_t nw, void* d_cand,
+                      double* d_cpts, cudaStream_t stream);
 // K1 record indices of a gathered candidate buffer -> candidate indices + base
 void launch_map_rec(ohx_extremes_rec* d_rec, const void* d_cand, int idx_bytes,
                     std::uint64_t base, cudaStream_t stream);
-// the ordered candidate list from KF's work area; d_counts[0] = its length
-void launch_candidates(void* d_work, std::uint64_t n, void* d_cand, int idx_bytes,
-                       std::uint64_t cap, unsigned long long* d_counts, cudaStream_t stream);
-void launch_sample(const double* d_xy, std::uint64_t n, int segs, int len, double* d_sample,
-                   cudaStream_t stream);
+void launch_sample(const double* d_xy, std::uint64_t n, int segs, int len, int subs,
+                   double* d_sample, cudaStream_t stream);
 void launch_count_in_region(const double* d_xy, std::uint64_t n, const KFRegion& q,
                             unsigned long long* d_count, cudaStream_t stream);
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,

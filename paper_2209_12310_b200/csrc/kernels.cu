@@ -412,30 +412,11 @@ __device__ __forceinline__ void visit8(WarpExt& w, double (&th)[8], const double
   __syncwarp();
 }
 
-// The chunks a block streams: one contiguous range per block (stride =
-// false), or grid-strided so that the whole grid sweeps the array front to
-// back (stride = true).
-struct ChunkRange {
-  std::uint64_t begin, end, step;
-  __device__ __forceinline__ ChunkRange(std::uint64_t nchunks, bool stride) {
-    if (stride) {
-      begin = blockIdx.x;
-      end = nchunks;
-      step = gridDim.x;
-    } else {
-      const std::uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
-      begin = min(nchunks, std::uint64_t(blockIdx.x) * per);
-      end = min(nchunks, begin + per);
-      step = 1;
-    }
-  }
-};
-
 template <typename IdxT>
 __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
     k1_extremes(const double2* __restrict__ pts, std::uint64_t n,
                 std::uint64_t base, K1Partial* partials, unsigned* ticket,
-                ohx_extremes_rec* out, bool stride) {
+                ohx_extremes_rec* out) {
   static_assert(kK1Unroll == 8, "visit8 takes 8 points per lane");
   __shared__ double2 k1_stage[kK1Block / 32][8 * 32];
   __shared__ WarpExt k1_ext[kK1Block / 32];
@@ -446,8 +427,9 @@ __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
   // consecutive addresses per block step, 8 loads in flight per thread)
   constexpr std::uint64_t kChunk = std::uint64_t(kK1Block) * kK1Unroll;
   const std::uint64_t nchunks = (n + kChunk - 1) / kChunk;
-  ChunkRange cr(nchunks, stride);
-  for (std::uint64_t c = cr.begin; c < cr.end; c += cr.step) {
+  const std::uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+  const std::uint64_t c_end = min(nchunks, (blockIdx.x + 1) * per);
+  for (std::uint64_t c = blockIdx.x * per; c < c_end; ++c) {
     const IdxT j0 = static_cast<IdxT>(c * kChunk + threadIdx.x);
     if ((c + 1) * kChunk <= n) {
       double2 v[kK1Unroll];
@@ -651,19 +633,22 @@ __device__ __forceinline__ std::uint64_t item_index(const GIdx* gidx, std::uint6
   else return static_cast<std::uint64_t>(__ldg(gidx + k));
 }
 
+// In gather mode `cpts` (when set) holds the candidates' coordinates already
+// gathered, cpts[k] = pts[gidx[k]]: contiguous loads instead of a gather.
 template <bool kFull_, typename GIdx>
 __device__ __forceinline__ std::uint32_t k2_label_tile(const KPlan& plan, const double2* pts,
-                                                       const GIdx* gidx, std::uint64_t n,
-                                                       std::uint64_t t0, bool has_kept,
-                                                       K2Shared& S) {
+                                                       const GIdx* gidx, const double2* cpts,
+                                                       std::uint64_t n, std::uint64_t t0,
+                                                       bool has_kept, K2Shared& S) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   double2 v[kK2Items];
 #pragma unroll
   for (int it = 0; it < kK2Items; ++it) {
     const std::uint32_t jl = it * kK2Block + threadIdx.x;
-    v[it] = (kFull_ || t0 + jl < n) ? ld_stream(pts + item_index(gidx, t0 + jl))
-                                    : make_double2(0.0, 0.0);
+    v[it] = (kFull_ || t0 + jl < n)
+                ? ld_stream(cpts != nullptr ? cpts + t0 + jl : pts + item_index(gidx, t0 + jl))
+                : make_double2(0.0, 0.0);
   }
   // 1) kept overrides and the certified box; everything else is "hard".
   //    Labels live packed in one register, 4 bits per item.
@@ -722,7 +707,8 @@ __device__ __forceinline__ std::uint32_t k2_label_tile(const KPlan& plan, const 
 
 template <typename GIdx>
 __global__ void __launch_bounds__(kK2Block, 4)
-    k2_filter(const double2* __restrict__ pts, const GIdx* __restrict__ gidx, std::uint64_t n,
+    k2_filter(const double2* __restrict__ pts, const GIdx* __restrict__ gidx,
+              const double2* __restrict__ cpts, std::uint64_t n,
               const __grid_constant__ KPlan plan, unsigned* tile_counter,
               std::uint32_t* tile_counts, std::uint64_t ntiles,
               std::uint16_t* scratch, std::uint8_t* labels) {
@@ -750,8 +736,8 @@ __global__ void __launch_bounds__(kK2Block, 4)
   const std::uint64_t t0 = tile * kK2Tile;
   const bool has_kept = S.has_kept;
   const std::uint32_t labs = (t0 + kK2Tile <= n)
-                                 ? k2_label_tile<true>(plan, pts, gidx, n, t0, has_kept, S)
-                                 : k2_label_tile<false>(plan, pts, gidx, n, t0, has_kept, S);
+                                 ? k2_label_tile<true>(plan, pts, gidx, cpts, n, t0, has_kept, S)
+                                 : k2_label_tile<false>(plan, pts, gidx, cpts, n, t0, has_kept, S);
 #define LAB(it) ((labs >> (4 * (it))) & 0xFu)
   if (labels != nullptr) {
 #pragma unroll
@@ -929,10 +915,9 @@ __global__ void __launch_bounds__(kK2cBlock)
 // the eight extremes and the second-best keys are exactly those of the
 // points OUTSIDE Q (the candidates).  KF therefore only streams the points
 // once, tests Q (2 DADD + 8 DSETP per point, the same rounded keys as K1)
-// and records the candidates, in index order, as 8-bit offsets within each
-// 256-point warp tile (a dense 16-byte slot per tile).  kf_compact turns
-// those into one ordered candidate list, K1 runs on the gathered
-// candidates, and after the octagon is known the host checks that Q lies
+// and appends the candidates' indices to per-warp regions; kf_scan +
+// kf_gather turn those into one ordered candidate list with the candidates'
+// coordinates gathered next to it, K1 runs on the gathered candidates, and after the octagon is known the host checks that Q lies
 // inside it (exact error bounds) and holds no kept point; then every
 // dropped point has the reference label 0 and only the candidates need K2
 // (gather mode).  Otherwise the regular K2 pass runs over all points.
@@ -940,85 +925,166 @@ constexpr int kKFBlock = 256;
 constexpr int kKFMinBlocks = 4;
 constexpr int kWT = 256;  // points per warp tile (8 items x 32 lanes)
 
-// Is p inside the provisional region Q?
+// Is p inside the provisional region Q?  (a predicate chain: 2 DADD +
+// 8 DSETP, no integer select per comparison)
 __device__ __forceinline__ bool in_region(const KFRegion& q, double2 p) {
-  const double t = __dadd_rn(p.x, p.y);
-  const double d = __dsub_rn(p.x, p.y);
-  return (p.x >= q.x0) & (p.x <= q.x1) & (p.y >= q.y0) & (p.y <= q.y1) & (t >= q.t0) &
-         (t <= q.t1) & (d >= q.d0) & (d <= q.d1);
+  std::uint32_t r;
+  asm("{\n\t.reg .pred p;\n\t.reg .f64 t, d;\n\t"
+      "add.rn.f64 t, %1, %2;\n\t"
+      "sub.rn.f64 d, %1, %2;\n\t"
+      "setp.ge.f64 p, %1, %3;\n\t"
+      "setp.le.and.f64 p, %1, %4, p;\n\t"
+      "setp.ge.and.f64 p, %2, %5, p;\n\t"
+      "setp.le.and.f64 p, %2, %6, p;\n\t"
+      "setp.ge.and.f64 p, t, %7, p;\n\t"
+      "setp.le.and.f64 p, t, %8, p;\n\t"
+      "setp.ge.and.f64 p, d, %9, p;\n\t"
+      "setp.le.and.f64 p, d, %10, p;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(r)
+      : "d"(p.x), "d"(p.y), "d"(q.x0), "d"(q.x1), "d"(q.y0), "d"(q.y1), "d"(q.t0), "d"(q.t1),
+        "d"(q.d0), "d"(q.d1));
+  return r != 0;
 }
 
-// One 256-point warp tile (point t0 + it * 32 + lane in item it).  Its
-// candidates' tile offsets, in index order, go to a 16-byte slot per tile
-// (byte 0 the count, bytes 1..15 the first 15 offsets): every tile writes
-// its slot, so the slot array is written densely, in full sectors.  A tile
-// with more than 15 candidates marks its slot 0xFF and spills all offsets to
-// its 256-byte slice of `scratch` and the count to wt_counts (rare unless the
-// region covers the data poorly).  `buf` is the warp's 16 + 256 byte stage.
-template <bool kFullTile>
+__device__ __forceinline__ std::uint64_t l2_evict_last_policy() {
+  std::uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// candidate stores stay in L2 (they are read back right after the pass)
+__device__ __forceinline__ void st_keep(std::uint32_t* p, std::uint32_t v, std::uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep(std::uint64_t* p, std::uint64_t v, std::uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+
+// Every warp streams its own contiguous range of 256-point tiles (point
+// t0 + it * 32 + lane in item it) and appends its candidates' indices, in
+// index order, to a private region of cap_w entries: the only stores of the
+// pass are the candidates themselves, written densely (the measured cost of
+// any per-tile record -- counts, slots or bit masks -- is 10x its share of
+// the bytes: writes interleaved with the read stream).  The exact count is
+// kept even past cap_w (the host then falls back to two passes).
+template <bool kFullTile, typename IdxT>
 __device__ __forceinline__ void kf_tile(const double2* __restrict__ pts, std::uint64_t n,
-                                        std::uint64_t wt, const KFRegion& q,
-                                        uint4* __restrict__ slots,
-                                        std::uint32_t* __restrict__ wt_counts,
-                                        std::uint8_t* __restrict__ scratch, std::uint8_t* buf) {
+                                        std::uint64_t t0, const KFRegion& q, IdxT* reg,
+                                        std::uint64_t cap_w, std::uint64_t pol,
+                                        std::uint32_t& c) {
   const int lane = threadIdx.x & 31;
-  const std::uint64_t t0 = wt * kWT;
   double2 v[8];
 #pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const std::uint32_t jl = it * 32 + lane;
-    v[it] = (kFullTile || t0 + jl < n) ? ld_stream(pts + t0 + jl) : make_double2(0.0, 0.0);
-  }
+  for (int it = 0; it < 8; ++it)
+    v[it] = (kFullTile || t0 + it * 32 + lane < n) ? ld_stream(pts + t0 + it * 32 + lane)
+                                                   : make_double2(0.0, 0.0);
   std::uint32_t cand = 0;
 #pragma unroll
   for (int it = 0; it < 8; ++it) {
-    const bool valid = kFullTile || t0 + it * 32 + lane < n;
-    cand |= std::uint32_t(valid && !in_region(q, v[it])) << it;
+    if (!in_region(q, v[it]) && (kFullTile || t0 + it * 32 + lane < n)) cand |= 1u << it;
   }
-  std::uint32_t items = __reduce_or_sync(kFull, cand), c = 0;
-  if (items) {
-    const unsigned lt = (1u << lane) - 1u;
-    while (items) {
-      const int it = __ffs(items) - 1;
-      items &= items - 1;
-      const bool mine = cand >> it & 1u;
-      const unsigned b = __ballot_sync(kFull, mine);
-      if (mine) {
-        const std::uint32_t pos = c + __popc(b & lt);
-        const auto off = static_cast<std::uint8_t>(it * 32 + lane);
-        buf[16 + pos] = off;
-        if (pos < 15) buf[1 + pos] = off;
-      }
-      c += __popc(b);
+  std::uint32_t items = __reduce_or_sync(kFull, cand);
+  if (items == 0) return;
+  const unsigned lt = (1u << lane) - 1u;
+  do {
+    const int it = __ffs(items) - 1;
+    items &= items - 1;
+    const bool mine = cand >> it & 1u;
+    const unsigned b = __ballot_sync(kFull, mine);
+    if (mine) {
+      const std::uint32_t pos = c + __popc(b & lt);
+      if (pos < cap_w) st_keep(reg + pos, static_cast<IdxT>(t0 + it * 32 + lane), pol);
     }
-    __syncwarp();
-    if (c > 15) {
-      for (std::uint32_t k = lane; k < c; k += 32) scratch[t0 + k] = buf[16 + k];
-      if (lane == 0) wt_counts[wt] = c;
-    }
-  }
-  if (lane == 0) {
-    buf[0] = static_cast<std::uint8_t>(c > 15 ? 0xFF : c);
-    slots[wt] = *reinterpret_cast<const uint4*>(buf);
-  }
-  __syncwarp();  // buf is reused by the next tile
+    c += __popc(b);
+  } while (items);
 }
 
+template <typename IdxT>
 __global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
     kf_filter(const double2* __restrict__ pts, std::uint64_t n, const KFRegion q,
-              uint4* __restrict__ slots, std::uint32_t* __restrict__ wt_counts, std::uint64_t nwt,
-              std::uint8_t* __restrict__ scratch, bool stride) {
-  __shared__ __align__(16) std::uint8_t kf_buf[kKFBlock / 32][16 + kWT];
-  std::uint8_t* buf = kf_buf[threadIdx.x >> 5];
-  // blocks stream 2048-point chunks, warp w taking the chunk's w-th warp tile
-  constexpr std::uint64_t kChunkTiles = kKFBlock / 32;
-  const std::uint64_t nchunks = (nwt + kChunkTiles - 1) / kChunkTiles;
-  const std::uint64_t nfull = n / kWT;  // every warp tile but possibly the last is full
-  ChunkRange cr(nchunks, stride);
-  for (std::uint64_t ch = cr.begin; ch < cr.end; ch += cr.step) {
-    const std::uint64_t wt = ch * kChunkTiles + (threadIdx.x >> 5);
-    if (wt < nfull) kf_tile<true>(pts, n, wt, q, slots, wt_counts, scratch, buf);
-    else if (wt < nwt) kf_tile<false>(pts, n, wt, q, slots, wt_counts, scratch, buf);
+              IdxT* __restrict__ regions, std::uint64_t cap_w,
+              std::uint32_t* __restrict__ warp_counts) {
+  const std::uint64_t nt = (n + kWT - 1) / kWT;
+  const std::uint64_t nw = std::uint64_t(gridDim.x) * (kKFBlock / 32);
+  const std::uint64_t gw = std::uint64_t(blockIdx.x) * (kKFBlock / 32) + (threadIdx.x >> 5);
+  const std::uint64_t per = (nt + nw - 1) / nw;
+  const std::uint64_t b0 = min(nt, gw * per), b1 = min(nt, b0 + per);
+  const std::uint64_t bf = max(b0, min(b1, n / kWT));  // tiles [b0, bf) are full
+  IdxT* reg = regions + gw * cap_w;
+  const std::uint64_t pol = l2_evict_last_policy();
+  std::uint32_t c = 0;  // a warp range holds < 2^32 points
+  for (std::uint64_t t = b0; t < bf; ++t) kf_tile<true>(pts, n, t * kWT, q, reg, cap_w, pol, c);
+  if (bf < b1) kf_tile<false>(pts, n, bf * kWT, q, reg, cap_w, pol, c);
+  if ((threadIdx.x & 31) == 0) warp_counts[gw] = c;
+}
+
+// Exclusive scan of the per-warp counts (one block): offsets, the total and
+// whether any region overflowed -> counts[0] = total, counts[1] = overflow.
+constexpr int kScanBlock = 1024;
+__global__ void __launch_bounds__(kScanBlock)
+    kf_scan(const std::uint32_t* __restrict__ warp_counts, std::uint64_t nw, std::uint64_t cap_w,
+            std::uint64_t* __restrict__ offsets, unsigned long long* counts) {
+  __shared__ std::uint64_t s_warp[kScanBlock / 32];
+  __shared__ std::uint64_t s_carry;
+  __shared__ int s_over;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    s_carry = 0;
+    s_over = 0;
+  }
+  __syncthreads();
+  for (std::uint64_t base = 0; base < nw; base += kScanBlock) {
+    const std::uint64_t i = base + threadIdx.x;
+    const std::uint64_t v = i < nw ? warp_counts[i] : 0;
+    if (v > cap_w) s_over = 1;
+    std::uint64_t incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const std::uint64_t o = __shfl_up_sync(kFull, incl, off);
+      if (lane >= off) incl += o;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const std::uint64_t w = s_warp[lane];
+      std::uint64_t wi = w;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const std::uint64_t o = __shfl_up_sync(kFull, wi, off);
+        if (lane >= off) wi += o;
+      }
+      s_warp[lane] = wi - w;
+    }
+    __syncthreads();
+    const std::uint64_t carry = s_carry;
+    if (i < nw) offsets[i] = carry + s_warp[warp] + incl - v;
+    __syncthreads();
+    if (threadIdx.x == kScanBlock - 1) s_carry = carry + s_warp[warp] + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    counts[0] = s_carry;
+    counts[1] = s_over;
+  }
+}
+
+// One block per warp region: copies its candidates to the ordered list and
+// gathers their coordinates (cpts[k] = pts[cand[k]]) for the candidate K1
+// and the gather-mode K2.
+template <typename IdxT>
+__global__ void __launch_bounds__(256)
+    kf_gather(const double2* __restrict__ pts, const IdxT* __restrict__ regions,
+              std::uint64_t cap_w, const std::uint32_t* __restrict__ warp_counts,
+              const std::uint64_t* __restrict__ offsets, IdxT* __restrict__ cand,
+              double2* __restrict__ cpts) {
+  const std::uint64_t w = blockIdx.x;
+  const std::uint64_t cnt = warp_counts[w];
+  const std::uint64_t o = offsets[w];
+  const IdxT* r = regions + w * cap_w;
+  for (std::uint64_t k = threadIdx.x; k < cnt; k += blockDim.x) {
+    const IdxT j = r[k];
+    cand[o + k] = j;
+    cpts[o + k] = pts[j];
   }
 }
 
@@ -1029,101 +1095,6 @@ __global__ void map_rec_idx(ohx_extremes_rec* rec, const IdxT* __restrict__ cand
                             std::uint64_t base) {
   const int a = threadIdx.x;
   if (a < 8) rec->idx[a] = base + static_cast<std::uint64_t>(cand[rec->idx[a]]);
-}
-
-// Ordered candidate list from KF's per-tile slots: groups of 1024 tiles
-// (4 per thread), block scan + decoupled look-back across groups, then a
-// flattened copy (binary search over the group's tile prefix).
-constexpr int kKFcBlock = 256;
-constexpr int kKFcTiles = 4 * kKFcBlock;
-
-template <typename IdxT>
-__global__ void __launch_bounds__(kKFcBlock)
-    kf_compact(const uint4* __restrict__ slots, const std::uint32_t* __restrict__ wt_counts,
-               std::uint64_t nwt, const std::uint8_t* __restrict__ scratch,
-               std::uint64_t* status, unsigned* group_counter, IdxT* cand, std::uint64_t cap,
-               unsigned long long* counts) {
-  __shared__ std::uint32_t s_group;
-  __shared__ std::uint32_t s_pre[kKFcTiles];
-  __shared__ uint4 s_slot[kKFcTiles];
-  __shared__ std::uint32_t s_warp[kKFcBlock / 32];
-  __shared__ std::uint64_t s_excl;
-  __shared__ std::uint32_t s_total;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const std::uint64_t ngroups = (nwt + kKFcTiles - 1) / kKFcTiles;
-  if (threadIdx.x == 0) s_group = atomicAdd(group_counter, 1u);
-  __syncthreads();
-  const std::uint64_t g = s_group;
-  std::uint32_t c[4], sum = 0;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const std::uint64_t t = g * kKFcTiles + threadIdx.x * 4 + r;
-    const uint4 sl = t < nwt ? slots[t] : make_uint4(0, 0, 0, 0);
-    s_slot[threadIdx.x * 4 + r] = sl;
-    const std::uint32_t b0 = sl.x & 0xFFu;
-    c[r] = b0 == 0xFFu ? wt_counts[t] : b0;
-    sum += c[r];
-  }
-  std::uint32_t incl = sum;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const std::uint32_t o = __shfl_up_sync(kFull, incl, off);
-    if (lane >= off) incl += o;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const std::uint32_t w = lane < kKFcBlock / 32 ? s_warp[lane] : 0u;
-    std::uint32_t wi = w;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const std::uint32_t o = __shfl_up_sync(kFull, wi, off);
-      if (lane >= off) wi += o;
-    }
-    if (lane < kKFcBlock / 32) s_warp[lane] = wi - w;
-    const std::uint32_t agg = __shfl_sync(kFull, wi, 31);
-    std::uint64_t excl = 0;
-    if (g == 0) {
-      if (lane == 0) st_relaxed(status, kFlagP | agg);
-    } else {
-      if (lane == 0) st_relaxed(status + g, kFlagA | agg);
-      excl = look_back(status, g);
-      if (lane == 0) st_relaxed(status + g, kFlagP | (excl + agg));
-    }
-    if (lane == 0) {
-      s_excl = excl;
-      s_total = agg;
-      if (g == ngroups - 1) {
-        counts[0] = excl + agg;
-        counts[1] = counts[2] = counts[3] = 0;
-      }
-    }
-  }
-  __syncthreads();
-  std::uint32_t run = s_warp[warp] + incl - sum;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    s_pre[threadIdx.x * 4 + r] = run;
-    run += c[r];
-  }
-  __syncthreads();
-  const std::uint32_t total = s_total;
-  const std::uint64_t excl = s_excl;
-  const auto* sb = reinterpret_cast<const std::uint8_t*>(s_slot);
-  for (std::uint32_t k = threadIdx.x; k < total; k += kKFcBlock) {
-    int lo = 0, hi = kKFcTiles - 1;  // the last tile whose prefix is <= k
-#pragma unroll
-    for (int step = 0; step < 10; ++step) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_pre[mid] <= k) lo = mid;
-      else hi = mid - 1;
-    }
-    const std::uint64_t t = g * kKFcTiles + lo;
-    const std::uint32_t e = k - s_pre[lo];
-    const std::uint8_t* sl = sb + 16 * lo;
-    const std::uint32_t off = sl[0] == 0xFFu ? scratch[t * kWT + e] : sl[1 + e];
-    if (excl + k < cap) cand[excl + k] = static_cast<IdxT>(t * kWT + off);
-  }
 }
 
 // ====================================================== K1 (TMA variant) ==
@@ -1212,14 +1183,17 @@ __global__ void __launch_bounds__(kSBlock, 2)
   }
 }
 
-// A sample for the provisional region: `segs` runs of `len` consecutive points
-// at evenly spaced offsets (coalesced reads, 16 MB for the default 256 x 4096).
-__global__ void gather_sample(const double2* __restrict__ pts, std::uint64_t n, int len,
+// A sample for the provisional region: `segs` runs of `len` consecutive
+// points at evenly spaced offsets (coalesced reads, 16 MB for the default
+// 256 x 4096).  Run b is stored as run b / subs of sub-sample b % subs, so
+// every sub-sample spans the whole index range.
+__global__ void gather_sample(const double2* __restrict__ pts, std::uint64_t n, int len, int subs,
                               double2* __restrict__ out) {
   const std::uint64_t segs = gridDim.x;
-  const std::uint64_t start = (n - len) * blockIdx.x / (segs > 1 ? segs - 1 : 1);
-  for (int k = threadIdx.x; k < len; k += blockDim.x)
-    out[std::uint64_t(blockIdx.x) * len + k] = pts[start + k];
+  const std::uint64_t b = blockIdx.x;
+  const std::uint64_t start = (n - len) * b / (segs > 1 ? segs - 1 : 1);
+  const std::uint64_t slot = (b % subs) * (segs / subs) + b / subs;
+  for (int k = threadIdx.x; k < len; k += blockDim.x) out[slot * len + k] = pts[start + k];
 }
 
 // Number of points of `pts` inside the region Q (sample coverage estimate).
@@ -1259,21 +1233,6 @@ __global__ void gather_xy4(const double2* __restrict__ pts, const IdxT* __restri
 }  // namespace
 
 // ============================================================ launchers ==
-static int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e && *e ? std::atoi(e) : dflt;
-}
-
-// OHX_ORDER=stride: grid-strided chunk order for K1/KF (default: one
-// contiguous range per block).  Experiment switches.
-static bool chunk_stride() {
-  static const bool v = [] {
-    const char* e = std::getenv("OHX_ORDER");
-    return e && std::string(e) == "stride";
-  }();
-  return v;
-}
-
 static int tma_grid(int device, std::uint64_t n) {
   int sms = 0;
   check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device),
@@ -1338,11 +1297,9 @@ void launch_k1(const double* d_xy, std::uint64_t n, std::uint64_t base,
   // 32-bit in-loop indices whenever the shard (plus a full grid stride of
   // overshoot) fits
   if (n + std::uint64_t(kK1Block) * kK1Unroll < 0xffffffffull)
-    k1_extremes<std::uint32_t><<<grid, kK1Block, 0, stream>>>(pts, n, base, partials, ticket, d_out,
-                                                              chunk_stride());
+    k1_extremes<std::uint32_t><<<grid, kK1Block, 0, stream>>>(pts, n, base, partials, ticket, d_out);
   else
-    k1_extremes<std::uint64_t><<<grid, kK1Block, 0, stream>>>(pts, n, base, partials, ticket, d_out,
-                                                              chunk_stride());
+    k1_extremes<std::uint64_t><<<grid, kK1Block, 0, stream>>>(pts, n, base, partials, ticket, d_out);
   check_cuda(cudaGetLastError(), "k1_extremes launch");
 }
 
@@ -1356,7 +1313,8 @@ void launch_k1b(const double* d_xy, std::uint64_t n, std::uint64_t base,
 }
 
 template <typename GIdx>
-static void k2_filter_launch(const double2* pts, const GIdx* gidx, std::uint64_t n,
+static void k2_filter_launch(const double2* pts, const GIdx* gidx, const double2* cpts,
+                             std::uint64_t n,
                              const KPlan& plan, const K2Work& w, std::uint64_t ntiles,
                              std::uint8_t* d_labels, cudaStream_t stream) {
   constexpr int smem = sizeof(K2Shared);
@@ -1368,7 +1326,7 @@ static void k2_filter_launch(const double2* pts, const GIdx* gidx, std::uint64_t
     configured = true;
   }
   k2_filter<GIdx><<<static_cast<unsigned>(ntiles), kK2Block, smem, stream>>>(
-      pts, gidx, n, plan, w.tile_counter, w.tile_counts, ntiles, w.scratch, d_labels);
+      pts, gidx, cpts, n, plan, w.tile_counter, w.tile_counts, ntiles, w.scratch, d_labels);
   check_cuda(cudaGetLastError(), "k2_filter launch");
 }
 
@@ -1385,48 +1343,67 @@ static void k2_compact_launch(const K2Work& w, std::uint64_t ntiles, IdxT* queue
 void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_work,
                std::uint64_t ntiles, void* d_queues, int idx_bytes, std::uint64_t cap,
                std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream,
-               const void* d_gather) {
+               const void* d_gather, const double* d_gather_xy) {
   const K2Work w = k2_work_layout(d_work, ntiles);
+  const auto* cp = reinterpret_cast<const double2*>(d_gather_xy);
   // re-arm the two work counters and the look-back words of k2_compact
   check_cuda(cudaMemsetAsync(d_work, 0, w.clear_bytes, stream), "cudaMemsetAsync(k2 work)");
   const auto* pts = reinterpret_cast<const double2*>(d_xy);
   if (idx_bytes == 4) {
     const auto* g = static_cast<const std::uint32_t*>(d_gather);
-    if (g) k2_filter_launch(pts, g, n, plan, w, ntiles, d_labels, stream);
-    else k2_filter_launch<void>(pts, nullptr, n, plan, w, ntiles, d_labels, stream);
+    if (g) k2_filter_launch(pts, g, cp, n, plan, w, ntiles, d_labels, stream);
+    else k2_filter_launch<void>(pts, nullptr, nullptr, n, plan, w, ntiles, d_labels, stream);
     auto* q = static_cast<std::uint32_t*>(d_queues);
     if (g) k2_compact_launch<std::uint32_t, true>(w, ntiles, q, cap, d_counts, g, stream);
     else k2_compact_launch<std::uint32_t, false>(w, ntiles, q, cap, d_counts, nullptr, stream);
   } else {
     const auto* g = static_cast<const std::uint64_t*>(d_gather);
-    if (g) k2_filter_launch(pts, g, n, plan, w, ntiles, d_labels, stream);
-    else k2_filter_launch<void>(pts, nullptr, n, plan, w, ntiles, d_labels, stream);
+    if (g) k2_filter_launch(pts, g, cp, n, plan, w, ntiles, d_labels, stream);
+    else k2_filter_launch<void>(pts, nullptr, nullptr, n, plan, w, ntiles, d_labels, stream);
     auto* q = static_cast<std::uint64_t*>(d_queues);
     if (g) k2_compact_launch<std::uint64_t, true>(w, ntiles, q, cap, d_counts, g, stream);
     else k2_compact_launch<std::uint64_t, false>(w, ntiles, q, cap, d_counts, nullptr, stream);
   }
 }
 
-int kf_grid(int device, std::uint64_t n) {
-  const std::uint64_t nwt = (n + kWT - 1) / kWT;
-  int g = occupancy_grid(device, kf_filter, kKFBlock, (nwt + kKFBlock / 32 - 1) / (kKFBlock / 32));
-  static const int bps = env_int("OHX_KF_BPS", 0);  // cap on blocks per SM
-  if (bps > 0) {
-    int sms = 0;
-    check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
-    g = std::min(g, sms * bps);
-  }
-  return g;
+int kf_grid(int device) {
+  return occupancy_grid(device, kf_filter<std::uint32_t>, kKFBlock, ~0ull);
 }
 
-void launch_kf(const double* d_xy, std::uint64_t n, const KFRegion& q, int grid, void* d_work,
+void launch_kf(const double* d_xy, std::uint64_t n, const KFRegion& q, int grid, void* d_regions,
+               int idx_bytes, std::uint64_t cap_w, std::uint32_t* d_warp_counts,
                cudaStream_t stream) {
-  const KFWork w = kf_work_layout(d_work, n);
-  check_cuda(cudaMemsetAsync(d_work, 0, w.clear_bytes, stream), "cudaMemsetAsync(kf work)");
-  kf_filter<<<grid, kKFBlock, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n, q,
-                                           reinterpret_cast<uint4*>(w.slots), w.wt_counts, w.nwt,
-                                           w.scratch, chunk_stride());
+  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  if (idx_bytes == 4)
+    kf_filter<std::uint32_t><<<grid, kKFBlock, 0, stream>>>(
+        pts, n, q, static_cast<std::uint32_t*>(d_regions), cap_w, d_warp_counts);
+  else
+    kf_filter<std::uint64_t><<<grid, kKFBlock, 0, stream>>>(
+        pts, n, q, static_cast<std::uint64_t*>(d_regions), cap_w, d_warp_counts);
   check_cuda(cudaGetLastError(), "kf_filter launch");
+}
+
+void launch_kf_scan(const std::uint32_t* d_warp_counts, std::uint64_t nw, std::uint64_t cap_w,
+                    std::uint64_t* d_offsets, unsigned long long* d_counts, cudaStream_t stream) {
+  kf_scan<<<1, kScanBlock, 0, stream>>>(d_warp_counts, nw, cap_w, d_offsets, d_counts);
+  check_cuda(cudaGetLastError(), "kf_scan launch");
+}
+
+void launch_kf_gather(const double* d_xy, const void* d_regions, int idx_bytes,
+                      std::uint64_t cap_w, const std::uint32_t* d_warp_counts,
+                      const std::uint64_t* d_offsets, std::uint64_t nw, void* d_cand,
+                      double* d_cpts, cudaStream_t stream) {
+  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  auto* cp = reinterpret_cast<double2*>(d_cpts);
+  if (idx_bytes == 4)
+    kf_gather<<<static_cast<unsigned>(nw), 256, 0, stream>>>(
+        pts, static_cast<const std::uint32_t*>(d_regions), cap_w, d_warp_counts, d_offsets,
+        static_cast<std::uint32_t*>(d_cand), cp);
+  else
+    kf_gather<<<static_cast<unsigned>(nw), 256, 0, stream>>>(
+        pts, static_cast<const std::uint64_t*>(d_regions), cap_w, d_warp_counts, d_offsets,
+        static_cast<std::uint64_t*>(d_cand), cp);
+  check_cuda(cudaGetLastError(), "kf_gather launch");
 }
 
 void launch_map_rec(ohx_extremes_rec* d_rec, const void* d_cand, int idx_bytes,
@@ -1438,24 +1415,9 @@ void launch_map_rec(ohx_extremes_rec* d_rec, const void* d_cand, int idx_bytes,
   check_cuda(cudaGetLastError(), "map_rec_idx launch");
 }
 
-void launch_candidates(void* d_work, std::uint64_t n, void* d_cand, int idx_bytes,
-                       std::uint64_t cap, unsigned long long* d_counts, cudaStream_t stream) {
-  const KFWork w = kf_work_layout(d_work, n);
-  const unsigned ngroups = static_cast<unsigned>((w.nwt + kKFcTiles - 1) / kKFcTiles);
-  if (idx_bytes == 4)
-    kf_compact<std::uint32_t><<<ngroups, kKFcBlock, 0, stream>>>(
-        reinterpret_cast<const uint4*>(w.slots), w.wt_counts, w.nwt, w.scratch, w.status, w.group_counter,
-        static_cast<std::uint32_t*>(d_cand), cap, d_counts);
-  else
-    kf_compact<std::uint64_t><<<ngroups, kKFcBlock, 0, stream>>>(
-        reinterpret_cast<const uint4*>(w.slots), w.wt_counts, w.nwt, w.scratch, w.status, w.group_counter,
-        static_cast<std::uint64_t*>(d_cand), cap, d_counts);
-  check_cuda(cudaGetLastError(), "kf_compact launch");
-}
-
-void launch_sample(const double* d_xy, std::uint64_t n, int segs, int len, double* d_sample,
-                   cudaStream_t stream) {
-  gather_sample<<<segs, 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n, len,
+void launch_sample(const double* d_xy, std::uint64_t n, int segs, int len, int subs,
+                   double* d_sample, cudaStream_t stream) {
+  gather_sample<<<segs, 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n, len, subs,
                                           reinterpret_cast<double2*>(d_sample));
   check_cuda(cudaGetLastError(), "gather_sample launch");
 }
