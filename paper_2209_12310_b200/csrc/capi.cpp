@@ -792,7 +792,8 @@ int fuse_mode() {
   }();
   return mode;
 }
-constexpr int kSampleSegs = 256, kSampleLen = 4096;
+constexpr int kSampleLen = 8192;     // points per sample run
+constexpr int kSampleMaxSegs = 1024;  // runs (8M points, 128 MB) for n >= 2^27
 constexpr int kSubSamples = 8;  // disjoint sub-samples of kSampleSegs / 8 runs each
 constexpr double kFuseMinCoverage = 0.8;
 
@@ -921,10 +922,11 @@ bool fit_region(const std::vector<P2>& R, const double lim[8], KFRegion* q) {
   return q->x0 < q->x1 && q->y0 < q->y1 && q->t0 < q->t1 && q->d0 < q->d1;
 }
 
-// The provisional region of the fused pass.  A 1M-point sample (kSampleSegs
-// runs of kSampleLen consecutive points) is split into kSubSamples disjoint
-// (interleaved: run b goes to sub-sample b % kSubSamples)
-// sub-samples; each one's eight extremes give an octagon, and Q is fitted
+// The provisional region of the fused pass.  A sample of about n/16 points
+// (up to 8M: runs of kSampleLen consecutive points at evenly spaced offsets,
+// read in place) is split into kSubSamples disjoint sub-samples (run b goes
+// to sub-sample b % kSubSamples, so each spans the whole index range); each
+// one's eight extremes (one batched launch) give an octagon, and Q is fitted
 // inside the INTERSECTION of those octagons.  The sub-sample octagons
 // scatter the way the true octagon may sit relative to any one sample's, so
 // a region inside all of them rarely leaves the true octagon (checked
@@ -937,20 +939,16 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
                         cudaStream_t s, FilterOut& f) {
   if (n < kFuseMinPoints || fuse_mode() == 0) return false;
   f.fuse_state = 2;
-  const std::uint64_t ns = std::uint64_t(kSampleSegs) * kSampleLen;
-  const std::uint64_t nsub = ns / kSubSamples;
+  // about n/16 sampled points, 64..1024 runs, a multiple of kSubSamples
+  const int segs = static_cast<int>(std::clamp<std::uint64_t>(
+                       n / (16ull * kSampleLen), 64, kSampleMaxSegs)) / kSubSamples * kSubSamples;
+  const std::uint64_t ns = std::uint64_t(segs) * kSampleLen;
   dev_grow(reinterpret_cast<void**>(&c->d_sample), &c->sample_bytes,
-           ns * 16 + kSubSamples * sizeof(ohx_extremes_rec), "sample");
-  auto* d_recs = reinterpret_cast<ohx_extremes_rec*>(c->d_sample + 2 * ns);
-  launch_sample(d_xy, n, kSampleSegs, kSampleLen, kSubSamples, c->d_sample, s);
+           kSubSamples * sizeof(ohx_extremes_rec), "sample records");
+  auto* d_recs = reinterpret_cast<ohx_extremes_rec*>(c->d_sample);
+  ensure_partials(c, segs);
+  launch_k1_sample(d_xy, n, segs, kSampleLen, kSubSamples, c->d_partials, c->d_ticket, d_recs, s);
   ++c->launches;
-  const int grid = k1_grid(c->device, nsub);
-  ensure_partials(c, grid);
-  for (int g = 0; g < kSubSamples; ++g) {
-    launch_k1(c->d_sample + 2 * nsub * g, nsub, 0, c->d_partials, grid, c->d_ticket, d_recs + g,
-              s);
-    ++c->launches;
-  }
   ohx_extremes_rec rs[kSubSamples];
   check_cuda(cudaMemcpyAsync(rs, d_recs, sizeof(rs), cudaMemcpyDeviceToHost, s),
              "cudaMemcpyAsync(sample recs)");
@@ -984,7 +982,7 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   double lim[8];
   for (int a = 0; a < 8; ++a) lim[a] = a < 4 ? all.key[a] : all.second[a - 4];
   if (!fit_region(region, lim, q)) return false;
-  launch_count_in_region(c->d_sample, ns, *q, c->d_cnt, s);
+  launch_count_in_region(d_xy, n, segs, kSampleLen, *q, c->d_cnt, s);
   ++c->launches;
   check_cuda(cudaMemcpyAsync(c->h_cnt, c->d_cnt, 8, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
   check_cuda(cudaStreamSynchronize(s), "sample coverage");
@@ -1075,9 +1073,9 @@ FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
                "candidate points");
       launch_kf_gather(d_xy, c->d_regions, idx_bytes, cap_w, d_wcounts, d_offsets, nw, c->d_cand,
                        c->d_cpts, s);
-      const int k1g = k1_grid(c->device, n_cand);
+      const int k1g = k1_list_grid(n_cand);
       ensure_partials(c, k1g);
-      launch_k1(c->d_cpts, n_cand, 0, c->d_partials, k1g, c->d_ticket, c->d_rec, s);
+      launch_k1_list(c->d_cpts, n_cand, c->d_partials, k1g, c->d_ticket, c->d_rec, s);
       launch_map_rec(c->d_rec, c->d_cand, idx_bytes, 0, s);
       c->launches += 3;
       check_cuda(cudaEventRecord(c->ev[3][1], s), "cudaEventRecord");

@@ -113,10 +113,19 @@ void launch_kf_gather(const double* d_xy, const void* d_regions, int idx_bytes,
 // K1 record indices of a gathered candidate buffer -> candidate indices + base
 void launch_map_rec(ohx_extremes_rec* d_rec, const void* d_cand, int idx_bytes,
                     std::uint64_t base, cudaStream_t stream);
-void launch_sample(const double* d_xy, std::uint64_t n, int segs, int len, int subs,
-                   double* d_sample, cudaStream_t stream);
-void launch_count_in_region(const double* d_xy, std::uint64_t n, const KFRegion& q,
-                            unsigned long long* d_count, cudaStream_t stream);
+// K1 over the provisional region's sample, read in place: `segs` runs of
+// `len` points at evenly spaced offsets, run b belonging to sub-sample
+// b % subs; one record per sub-sample (global indices).  Partials: subs x
+// (segs / subs) entries, tickets: subs.
+void launch_k1_sample(const double* d_xy, std::uint64_t n, int segs, int len, int subs,
+                      K1Partial* partials, unsigned* ticket, ohx_extremes_rec* d_recs,
+                      cudaStream_t stream);
+// K1 over a short contiguous list (the fused pass's candidates)
+int k1_list_grid(std::uint64_t n);
+void launch_k1_list(const double* d_xy, std::uint64_t n, K1Partial* partials, int grid,
+                    unsigned* ticket, ohx_extremes_rec* d_rec, cudaStream_t stream);
+void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int len,
+                            const KFRegion& q, unsigned long long* d_count, cudaStream_t stream);
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
                     std::uint64_t cap, const std::uint64_t counts[4], double* d_out,
                     cudaStream_t stream);

@@ -472,6 +472,85 @@ __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
   }
 }
 
+// ============================================================ K1 (small) ==
+// K1 for small inputs -- the provisional region's sample and the fused
+// pass's candidate list.  With few points per warp nearly every point would
+// take the warp-uniform update path of k1_extremes, so here every thread
+// keeps its own state (register compare-and-select per point) and the
+// states are reduced once per warp / block / grid.  blockIdx.y selects an
+// independent input (a sub-sample), each with its own partials, ticket and
+// record.
+//   sampled: input g is the sample runs b = s * subs + g (s = 0..segs/subs-1)
+//            of `len` consecutive points starting at (n - len) * b /
+//            (segs - 1); reported indices are global.
+//   list:    input 0 is pts[0, n).
+struct SampleMap {
+  std::uint64_t n;
+  int segs, len, subs;
+  __device__ __forceinline__ std::uint64_t run_start(std::uint64_t b) const {
+    return (n - std::uint64_t(len)) * b / std::uint64_t(segs > 1 ? segs - 1 : 1);
+  }
+};
+
+__device__ __forceinline__ void k1_visit(ArgState<8, 4>& st, double2 p, std::uint64_t j) {
+  const double t = __dadd_rn(p.x, p.y);
+  const double d = __dsub_rn(p.x, p.y);
+  upd(st.k[0], st.i[0], p.x, j);
+  upd(st.k[1], st.i[1], p.y, j);
+  upd(st.k[2], st.i[2], -p.x, j);
+  upd(st.k[3], st.i[3], -p.y, j);
+  upd2(st.k[4], st.i[4], st.s[0], t, j);
+  upd2(st.k[5], st.i[5], st.s[1], -d, j);
+  upd2(st.k[6], st.i[6], st.s[2], -t, j);
+  upd2(st.k[7], st.i[7], st.s[3], d, j);
+}
+
+template <bool kSampled>
+__global__ void __launch_bounds__(256)
+    k1_small(const double2* __restrict__ pts, std::uint64_t n, const SampleMap sm,
+             K1Partial* partials, unsigned* ticket, ohx_extremes_rec* out) {
+  const int g = blockIdx.y;
+  partials += std::uint64_t(g) * gridDim.x;
+  ticket += g;
+  out += g;
+  ArgState<8, 4> st;
+  st.init();
+  if constexpr (kSampled) {
+    // global indices only grow along a thread's runs (run b increases with s)
+    const int nrun = sm.segs / sm.subs;
+    for (int r = blockIdx.x; r < nrun; r += gridDim.x) {
+      const std::uint64_t start = sm.run_start(std::uint64_t(r) * sm.subs + g);
+      for (int k = threadIdx.x; k < sm.len; k += 256)
+        k1_visit(st, ld_stream(pts + start + k), start + k);
+    }
+  } else {
+    for (std::uint64_t j = std::uint64_t(blockIdx.x) * 256 + threadIdx.x; j < n;
+         j += std::uint64_t(gridDim.x) * 256)
+      k1_visit(st, ld_stream(pts + j), j);
+  }
+  block_reduce<8, 4, 256>(st);
+  if (!grid_combine<8, 4, 256>(st, partials, ticket)) return;
+  if (threadIdx.x < 8) {
+    const int a = threadIdx.x;
+    double k = 0, s2 = 0;
+    std::uint64_t i = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (b == a) {
+        k = st.k[b];
+        i = st.i[b];
+        if (b >= 4) s2 = st.s[b - 4];
+      }
+    const double2 p = pts[i];
+    out->key[a] = k;
+    out->idx[a] = i;
+    out->x[a] = p.x;
+    out->y[a] = p.y;
+    if (a >= 4) out->second[a - 4] = s2;
+    if (a == 0) out->n = kSampled ? std::uint64_t(sm.segs / sm.subs) * sm.len : n;
+  }
+}
+
 // ==================================================================== K1b ==
 // slot k: argmax of -(|x - cx| + |y - cy|) = the reference argmin of
 // manhattan(p, corner) (geometry.hpp:35-37), corners ne, nw, sw, se.
@@ -1183,28 +1262,15 @@ __global__ void __launch_bounds__(kSBlock, 2)
   }
 }
 
-// A sample for the provisional region: `segs` runs of `len` consecutive
-// points at evenly spaced offsets (coalesced reads, 16 MB for the default
-// 256 x 4096).  Run b is stored as run b / subs of sub-sample b % subs, so
-// every sub-sample spans the whole index range.
-__global__ void gather_sample(const double2* __restrict__ pts, std::uint64_t n, int len, int subs,
-                              double2* __restrict__ out) {
-  const std::uint64_t segs = gridDim.x;
-  const std::uint64_t b = blockIdx.x;
-  const std::uint64_t start = (n - len) * b / (segs > 1 ? segs - 1 : 1);
-  const std::uint64_t slot = (b % subs) * (segs / subs) + b / subs;
-  for (int k = threadIdx.x; k < len; k += blockDim.x) out[slot * len + k] = pts[start + k];
-}
-
-// Number of points of `pts` inside the region Q (sample coverage estimate).
-__global__ void count_in_region(const double2* __restrict__ pts, std::uint64_t n,
-                                const KFRegion q, unsigned long long* count) {
+// Number of the sample's points inside the region Q (sample coverage
+// estimate): block b counts run b.
+__global__ void __launch_bounds__(256)
+    count_in_region(const double2* __restrict__ pts, const SampleMap sm, const KFRegion q,
+                    unsigned long long* count) {
+  const std::uint64_t start = sm.run_start(blockIdx.x);
   unsigned c = 0;
-  for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
-       k += std::uint64_t(gridDim.x) * blockDim.x)
-    c += in_region(q, pts[k]);
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(kFull, c, off);
+  for (int k = threadIdx.x; k < sm.len; k += 256) c += in_region(q, ld_stream(pts + start + k));
+  c = __reduce_add_sync(kFull, c);
   if ((threadIdx.x & 31) == 0) atomicAdd(count, static_cast<unsigned long long>(c));
 }
 
@@ -1415,18 +1481,33 @@ void launch_map_rec(ohx_extremes_rec* d_rec, const void* d_cand, int idx_bytes,
   check_cuda(cudaGetLastError(), "map_rec_idx launch");
 }
 
-void launch_sample(const double* d_xy, std::uint64_t n, int segs, int len, int subs,
-                   double* d_sample, cudaStream_t stream) {
-  gather_sample<<<segs, 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n, len, subs,
-                                          reinterpret_cast<double2*>(d_sample));
-  check_cuda(cudaGetLastError(), "gather_sample launch");
+void launch_k1_sample(const double* d_xy, std::uint64_t n, int segs, int len, int subs,
+                      K1Partial* partials, unsigned* ticket, ohx_extremes_rec* d_recs,
+                      cudaStream_t stream) {
+  const SampleMap sm{n, segs, len, subs};
+  k1_small<true><<<dim3(segs / subs, subs), 256, 0, stream>>>(
+      reinterpret_cast<const double2*>(d_xy), 0, sm, partials, ticket, d_recs);
+  check_cuda(cudaGetLastError(), "k1_small<sample> launch");
 }
 
-void launch_count_in_region(const double* d_xy, std::uint64_t n, const KFRegion& q,
-                            unsigned long long* d_count, cudaStream_t stream) {
+int k1_list_grid(std::uint64_t n) {
+  const std::uint64_t b = (n + 256 * 16 - 1) / (256 * 16);
+  return static_cast<int>(b < 1 ? 1 : (b > 148 * 4 ? 148 * 4 : b));
+}
+
+void launch_k1_list(const double* d_xy, std::uint64_t n, K1Partial* partials, int grid,
+                    unsigned* ticket, ohx_extremes_rec* d_rec, cudaStream_t stream) {
+  k1_small<false><<<dim3(grid, 1), 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n,
+                                                    SampleMap{0, 1, 1, 1}, partials, ticket,
+                                                    d_rec);
+  check_cuda(cudaGetLastError(), "k1_small<list> launch");
+}
+
+void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int len,
+                            const KFRegion& q, unsigned long long* d_count, cudaStream_t stream) {
   check_cuda(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), stream), "cudaMemsetAsync");
-  const unsigned grid = static_cast<unsigned>(n / (256 * 16) + 1 < 1184 ? n / (256 * 16) + 1 : 1184);
-  count_in_region<<<grid, 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n, q, d_count);
+  count_in_region<<<segs, 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy),
+                                            SampleMap{n, segs, len, 1}, q, d_count);
   check_cuda(cudaGetLastError(), "count_in_region launch");
 }
 
