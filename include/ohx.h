@@ -168,6 +168,27 @@ int ohx_extremes_combine(const ohx_extremes_rec* recs, int k,
 int ohx_extremes_resolve(const ohx_extremes_rec* rec, ohx_extreme_set* out,
                          uint32_t* uncertified_mask);
 
+/* Fused single pass over one shard (replaces K1 + the K2 read of every
+ * point; SURVEY §8f "one read").  Samples the shard, fits a provisional
+ * region Q, streams the points once (KF) keeping only those outside Q, and
+ * runs K1 over those candidates.  *fused = 1: h_rec is the shard's extremes
+ * record, exactly what ohx_extremes returns (global indices).  *fused = 0:
+ * nothing usable (small shard, poor sample coverage, candidate overflow) --
+ * call ohx_extremes.  The candidates stay in the context for
+ * ohx_filter_fused. */
+int ohx_fused_extremes(ohx_ctx* ctx, const double* d_xy, uint64_t n, uint64_t index_base,
+                       ohx_extremes_rec* h_rec, int* fused, void* stream);
+/* Second half of the fused pass, same points: classify with the global
+ * ExtremeSet and plan (filter.cpp:104-131, hull.cpp:124-131).  K2 runs over
+ * the candidates only when Q is certified inside the plan's octagon and
+ * holds none of the kept points (*fused = 1), else over all n points
+ * (*fused = 0).  Same outputs as ohx_filter (queues via ohx_queue_fetch;
+ * labels of dropped points 0).  OHX_E_INVALID without a pending
+ * ohx_fused_extremes over (d_xy, n, index_base) in this context. */
+int ohx_filter_fused(ohx_ctx* ctx, const double* d_xy, uint64_t n, uint64_t index_base,
+                     const ohx_extreme_set* ext, const ohx_filter_plan* plan, uint8_t* d_labels,
+                     uint64_t h_counts[4], int* fused, void* stream);
+
 /* K1b. Exact corner argmins against the bounding box
  * bbox = {x_max, y_max, x_min, y_min} (filter.cpp:28-43). */
 int ohx_corners_exact(ohx_ctx* ctx, const double* d_xy, uint64_t n,

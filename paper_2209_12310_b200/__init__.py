@@ -200,6 +200,27 @@ class Context:
         check(lib.ohx_extremes(self.h, _ptr(d_xy), n, index_base, C.byref(rec), _stream(stream)))
         return rec
 
+    def fused_extremes(self, d_xy, n: int, index_base: int = 0, stream=None):
+        """Fused single pass over a shard: the extremes record from one read
+        (KF + K1 over the candidates), or None when the pass did not apply
+        (then use `extremes`).  Pair with `filter_fused`."""
+        rec = ExtremesRec()
+        fused = C.c_int(0)
+        check(lib.ohx_fused_extremes(self.h, _ptr(d_xy), n, index_base, C.byref(rec),
+                                     C.byref(fused), _stream(stream)))
+        return rec if fused.value else None
+
+    def filter_fused(self, d_xy, n: int, ext: ExtremeSet, plan: FilterPlan, index_base: int = 0,
+                     d_labels=None, stream=None):
+        """Second half of the fused pass -> (queue counts, K2 ran on the
+        candidates only)."""
+        counts = (C.c_uint64 * 4)()
+        fused = C.c_int(0)
+        check(lib.ohx_filter_fused(self.h, _ptr(d_xy), n, index_base, C.byref(ext), C.byref(plan),
+                                   None if d_labels is None else _ptr(d_labels), counts,
+                                   C.byref(fused), _stream(stream)))
+        return [int(c) for c in counts], bool(fused.value)
+
     def corners_exact(self, d_xy, n: int, bbox, index_base: int = 0, stream=None) -> CornerRec:
         b = (C.c_double * 4)(*bbox)
         rec = CornerRec()

@@ -72,6 +72,10 @@ PROTOTYPES = [
     ("ohx_ctx_kernel_ms", C.c_int, [_vp, _dp]),
     ("ohx_ctx_last_run", C.c_int, [_vp, C.POINTER(RunInfo)]),
     ("ohx_extremes", C.c_int, [_vp, _vp, _u64, _u64, C.POINTER(ExtremesRec), _vp]),
+    ("ohx_fused_extremes", C.c_int, [_vp, _vp, _u64, _u64, C.POINTER(ExtremesRec),
+                                     C.POINTER(C.c_int), _vp]),
+    ("ohx_filter_fused", C.c_int, [_vp, _vp, _u64, _u64, C.POINTER(ExtremeSet),
+                                   C.POINTER(FilterPlan), _vp, _u64p, C.POINTER(C.c_int), _vp]),
     ("ohx_extremes_combine", C.c_int, [C.POINTER(ExtremesRec), C.c_int, C.POINTER(ExtremesRec)]),
     ("ohx_extremes_resolve", C.c_int, [C.POINTER(ExtremesRec), C.POINTER(ExtremeSet),
                                        C.POINTER(C.c_uint32)]),

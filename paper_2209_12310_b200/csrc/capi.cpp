@@ -76,6 +76,14 @@ struct ohx_ctx {
 
   ohx_run_info last_run = {};
 
+  // the last fused pass (fused_begin) awaiting its fused_finish
+  struct {
+    bool active = false;
+    ohx::KFRegion q{};
+    const double* d_xy = nullptr;
+    std::uint64_t n = 0, base = 0, n_cand = 0;
+  } fz;
+
   // CUDA events bracketing the last launch of each stage: K1 (or KF), K1b,
   // K2, and the fused path's candidate stage (compaction + candidate K1)
   cudaEvent_t ev[4][2] = {};
@@ -1027,88 +1035,110 @@ struct Trace {
   }
 };
 
+// Fused pass, first half, over the n points of one shard (global indices
+// base + j): provisional region -> KF -> ordered candidate list -> K1 over
+// the candidates.  Returns true with the shard's extremes record in *rec
+// (what K1 over all points would have produced) when the fused pass ran;
+// false (f.fuse_state says why) when the caller must run K1 instead.
+bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+                 FilterOut& f, ohx_extremes_rec* rec, cudaStream_t s, Trace& tr) {
+  c->fz.active = false;
+  KFRegion q;
+  const bool fuse = provisional_region(c, d_xy, n, &q, s, f);
+  tr.mark("region");
+  if (!fuse) return false;
+  const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
+  const int grid = kf_grid(c->device);
+  const std::uint64_t nw = std::uint64_t(grid) * kKFWarpsPerBlock;
+  const std::uint64_t per = ((n + 255) / 256 + nw - 1) / nw * 256;  // points per warp
+  // room for 1.5x the sample's miss rate (+256) per warp region; a region
+  // that overflows sends the call down the two-pass path
+  const std::uint64_t cap_w = std::min<std::uint64_t>(
+      per, 256 + static_cast<std::uint64_t>(1.5 * (1.0 - f.sample_coverage) * double(per)));
+  dev_grow(&c->d_regions, &c->regions_bytes, nw * cap_w * idx_bytes, "kf regions");
+  dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes, nw * 12 + 16, "kf counts");
+  auto* d_wcounts = reinterpret_cast<std::uint32_t*>(c->d_status);
+  auto* d_offsets = c->d_status + (nw + 1) / 2;  // 8-byte aligned after the u32 counts
+  check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
+  launch_kf(d_xy, n, q, grid, c->d_regions, idx_bytes, cap_w, d_wcounts, s);
+  check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
+  c->timed[0] = true;
+  ++c->launches;
+  check_cuda(cudaEventRecord(c->ev[3][0], s), "cudaEventRecord");
+  launch_kf_scan(d_wcounts, nw, cap_w, d_offsets, c->d_counts, s);
+  ++c->launches;
+  check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
+  check_cuda(cudaStreamSynchronize(s), "kf candidates");
+  tr.mark("kf+scan");
+  const std::uint64_t n_cand = c->h_counts[0];
+  f.candidates = n_cand;
+  if (n_cand == 0 || c->h_counts[1] != 0) {
+    f.fuse_state = 5;  // a warp region overflowed: the two-pass path
+    return false;
+  }
+  // ordered candidate list + coordinates; K1 over them, indices mapped back
+  dev_grow(&c->d_cand, &c->cand_bytes, n_cand * idx_bytes, "candidates");
+  dev_grow(reinterpret_cast<void**>(&c->d_cpts), &c->cpts_bytes, n_cand * 16, "candidate points");
+  launch_kf_gather(d_xy, c->d_regions, idx_bytes, cap_w, d_wcounts, d_offsets, nw, c->d_cand,
+                   c->d_cpts, s);
+  const int k1g = k1_list_grid(n_cand);
+  ensure_partials(c, k1g);
+  launch_k1_list(c->d_cpts, n_cand, c->d_partials, k1g, c->d_ticket, c->d_rec, s);
+  launch_map_rec(c->d_rec, c->d_cand, idx_bytes, base, s);
+  c->launches += 3;
+  check_cuda(cudaEventRecord(c->ev[3][1], s), "cudaEventRecord");
+  c->timed[3] = true;
+  check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
+                             cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec)");
+  check_cuda(cudaStreamSynchronize(s), "candidate extremes");
+  tr.mark("cand-k1");
+  *rec = *c->h_rec;
+  rec->n = n;
+  c->fz = {true, q, d_xy, n, base, n_cand};
+  return true;
+}
+
+// Fused pass, second half: with the (global) ExtremeSet and plan, the
+// points KF dropped have the reference label 0 iff Q lies inside the
+// octagon (exact error bounds) and holds none of the eight kept points;
+// then K2 runs over the candidates only, otherwise over all n points.
+void fused_finish(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+                  const ohx_extreme_set& ext, const ohx_filter_plan& plan,
+                  std::uint8_t* d_labels, std::uint64_t counts[4], FilterOut& f,
+                  cudaStream_t s) {
+  if (!c->fz.active || c->fz.d_xy != d_xy || c->fz.n != n || c->fz.base != base)
+    throw std::invalid_argument("filter_fused: no fused pass over these points in this context");
+  c->fz.active = false;
+  const KFRegion& q = c->fz.q;
+  bool ok = region_certified(plan, q) && fuse_mode() != 2;
+  f.fuse_state = 4;
+  for (int a = 0; a < 8 && ok; ++a) ok = !in_region_host(q, ext.x[a], ext.y[a]);
+  if (!ok) {  // not certified: the regular K2 pass over all points
+    filter(c, d_xy, n, base, plan, d_labels, counts, s);
+    return;
+  }
+  f.fuse_state = 1;
+  f.fused = true;
+  if (d_labels) check_cuda(cudaMemsetAsync(d_labels, 0, n, s), "cudaMemsetAsync(labels)");
+  filter_core(c, d_xy, n, base, plan, d_labels, counts, s, c->d_cand, c->fz.n_cand, c->d_cpts);
+}
+
 FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
                              std::uint8_t* d_labels, cudaStream_t s) {
   if (n == 0) throw std::invalid_argument("heaphull: empty point set");
   FilterOut f{};
   for (bool& t : c->timed) t = false;  // kernel_ms reports this pipeline's stages
   Trace tr;
-  KFRegion q;
-  const bool fuse = provisional_region(c, d_xy, n, &q, s, f);
-  tr.mark("region");
-  if (fuse) {
-    // ---- fused: one streaming pass filters Q; the extremes come from the
-    // candidates (the points outside Q) alone
-    const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
-    const int grid = kf_grid(c->device);
-    const std::uint64_t nw = std::uint64_t(grid) * kKFWarpsPerBlock;
-    const std::uint64_t per = ((n + 255) / 256 + nw - 1) / nw * 256;  // points per warp
-    // room for 1.5x the sample's miss rate (+256) per warp region; a region
-    // that overflows sends the call down the two-pass path
-    const std::uint64_t cap_w = std::min<std::uint64_t>(
-        per, 256 + static_cast<std::uint64_t>(1.5 * (1.0 - f.sample_coverage) * double(per)));
-    dev_grow(&c->d_regions, &c->regions_bytes, nw * cap_w * idx_bytes, "kf regions");
-    dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes, nw * 12 + 16,
-             "kf counts");
-    auto* d_wcounts = reinterpret_cast<std::uint32_t*>(c->d_status);
-    auto* d_offsets = c->d_status + (nw + 1) / 2;  // 8-byte aligned after the u32 counts
-    check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
-    launch_kf(d_xy, n, q, grid, c->d_regions, idx_bytes, cap_w, d_wcounts, s);
-    check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
-    c->timed[0] = true;
-    ++c->launches;
-    check_cuda(cudaEventRecord(c->ev[3][0], s), "cudaEventRecord");
-    launch_kf_scan(d_wcounts, nw, cap_w, d_offsets, c->d_counts, s);
-    ++c->launches;
-    check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
-    check_cuda(cudaStreamSynchronize(s), "kf candidates");
-    tr.mark("kf+scan");
-    const std::uint64_t n_cand = c->h_counts[0];
-    f.candidates = n_cand;
-    if (n_cand >= 1 && c->h_counts[1] == 0) {
-      // ordered candidate list + coordinates; K1 over them, indices mapped back
-      dev_grow(&c->d_cand, &c->cand_bytes, n_cand * idx_bytes, "candidates");
-      dev_grow(reinterpret_cast<void**>(&c->d_cpts), &c->cpts_bytes, n_cand * 16,
-               "candidate points");
-      launch_kf_gather(d_xy, c->d_regions, idx_bytes, cap_w, d_wcounts, d_offsets, nw, c->d_cand,
-                       c->d_cpts, s);
-      const int k1g = k1_list_grid(n_cand);
-      ensure_partials(c, k1g);
-      launch_k1_list(c->d_cpts, n_cand, c->d_partials, k1g, c->d_ticket, c->d_rec, s);
-      launch_map_rec(c->d_rec, c->d_cand, idx_bytes, 0, s);
-      c->launches += 3;
-      check_cuda(cudaEventRecord(c->ev[3][1], s), "cudaEventRecord");
-      c->timed[3] = true;
-      check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
-                                 cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec)");
-      check_cuda(cudaStreamSynchronize(s), "candidate extremes");
-      tr.mark("cand-k1");
-      ohx_extremes_rec rec = *c->h_rec;
-      rec.n = n;
-      finish_extremes(c, d_xy, n, rec, f, s);
-      tr.mark("octagon+plan");
-      // the dropped points are label 0 iff Q is certified inside the true
-      // octagon and holds none of the eight kept points
-      bool ok = region_certified(f.plan, q) && fuse_mode() != 2;
-      f.fuse_state = 4;
-      for (int a = 0; a < 8 && ok; ++a) ok = !in_region_host(q, f.ext.x[a], f.ext.y[a]);
-      if (ok) {
-        f.fuse_state = 1;
-        if (d_labels) check_cuda(cudaMemsetAsync(d_labels, 0, n, s), "cudaMemsetAsync(labels)");
-        filter_core(c, d_xy, n, 0, f.plan, d_labels, f.counts, s, c->d_cand, n_cand, c->d_cpts);
-        tr.mark("k2-gather");
-        f.fused = true;
-        return f;
-      }
-      // not certified: the regular K2 pass over all points
-      filter(c, d_xy, n, 0, f.plan, d_labels, f.counts, s);
-      return f;
-    }
-    f.fuse_state = 5;  // a warp region overflowed: the two-pass path
+  ohx_extremes_rec rec;
+  if (fused_begin(c, d_xy, n, 0, f, &rec, s, tr)) {
+    finish_extremes(c, d_xy, n, rec, f, s);
+    tr.mark("octagon+plan");
+    fused_finish(c, d_xy, n, 0, f.ext, f.plan, d_labels, f.counts, f, s);
+    tr.mark("k2");
+    return f;
   }
   // ---- two passes: K1, then K2
-  ohx_extremes_rec rec;
   extremes(c, d_xy, n, 0, &rec, s);
   finish_extremes(c, d_xy, n, rec, f, s);
   filter(c, d_xy, n, 0, f.plan, d_labels, f.counts, s);
@@ -1241,6 +1271,38 @@ int ohx_extremes(ohx_ctx* ctx, const double* d_xy, uint64_t n, uint64_t index_ba
     std::lock_guard<std::mutex> g(ctx->mu);
     bind(ctx);
     extremes(ctx, d_xy, n, index_base, h_rec, pick(ctx, stream));
+  });
+}
+
+int ohx_fused_extremes(ohx_ctx* ctx, const double* d_xy, uint64_t n, uint64_t index_base,
+                       ohx_extremes_rec* h_rec, int* fused, void* stream) {
+  return guard([&] {
+    if (n == 0) throw std::invalid_argument("find_extremes: empty point set");
+    std::lock_guard<std::mutex> g(ctx->mu);
+    bind(ctx);
+    for (bool& t : ctx->timed) t = false;
+    FilterOut f{};
+    Trace tr;
+    *fused = fused_begin(ctx, d_xy, n, index_base, f, h_rec, pick(ctx, stream), tr) ? 1 : 0;
+    ctx->last_run = {};
+    ctx->last_run.candidates = f.candidates;
+    ctx->last_run.fuse_state = f.fuse_state;
+    ctx->last_run.sample_coverage = f.sample_coverage;
+  });
+}
+
+int ohx_filter_fused(ohx_ctx* ctx, const double* d_xy, uint64_t n, uint64_t index_base,
+                     const ohx_extreme_set* ext, const ohx_filter_plan* plan, uint8_t* d_labels,
+                     uint64_t h_counts[4], int* fused, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> g(ctx->mu);
+    bind(ctx);
+    FilterOut f{};
+    fused_finish(ctx, d_xy, n, index_base, *ext, *plan, d_labels, h_counts, f, pick(ctx, stream));
+    *fused = f.fused ? 1 : 0;
+    ctx->last_run.fused = f.fused;
+    ctx->last_run.fuse_state = f.fuse_state;
+    for (int q = 0; q < 4; ++q) ctx->last_run.counts[q] = h_counts[q];
   });
 }
 

@@ -6,12 +6,17 @@ tests).  Rank r owns the contiguous global index range
 of the reference (parallel.hpp:34-43) holds across shards.
 
   1. K1 on every shard                       -> one ~300 B extremes record
+     (or the fused pass: KF streams the shard once against a provisional
+     region fitted on the shard's own sample and K1 runs on the points
+     outside it -- the same record from one read)
   2. all_gather of the records + the same associative combine on every rank
      (NCCL has no arg-min over (f64, u64) pairs; the combine is exact and
      order-independent, so every rank derives the identical ExtremeSet)
   3. corner certificate; only if it fails: K1b per shard + all_gather
   4. build_octagon + K2 plan (host, identical on every rank)
-  5. K2 on every shard -> four index-ordered queues per shard
+  5. K2 on every shard -> four index-ordered queues per shard (fused: on the
+     shard's candidates only, once its region is certified inside the
+     global octagon)
   6. survivor coordinates gathered to the root in rank order (= global
      index order, so the concatenation equals build_queues of the whole)
   7. the root runs the host hull stage (reference semantics) on them.
@@ -41,6 +46,13 @@ class CudaShard:
 
     def extremes(self) -> ExtremesRec:
         return self.ctx.extremes(self.d_xy, self.n, self.base)
+
+    def fused_extremes(self):
+        return self.ctx.fused_extremes(self.d_xy, self.n, self.base)
+
+    def filter_fused(self, ext, plan):
+        self.counts, _ = self.ctx.filter_fused(self.d_xy, self.n, ext, plan, self.base)
+        return self.counts
 
     def corners_exact(self, bbox) -> CornerRec:
         return self.ctx.corners_exact(self.d_xy, self.n, bbox, self.base)
@@ -109,7 +121,11 @@ def sharded_heaphull(shard, device=None, root: int = 0, stats: dict | None = Non
     elsewhere.  `stats` (optional) receives counts / certificate info."""
     dist = _dist()
     rank = dist.get_rank() if dist else 0
-    rec = shard.extremes()
+    # one read per shard when the fused pass applies (its record equals K1's)
+    rec = shard.fused_extremes() if hasattr(shard, "fused_extremes") else None
+    fused = rec is not None
+    if not fused:
+        rec = shard.extremes()
     g = combine_extremes(_allgather_structs(rec, ExtremesRec, device))
     ext, mask = resolve_extremes(g)
     if mask:
@@ -118,10 +134,11 @@ def sharded_heaphull(shard, device=None, root: int = 0, stats: dict | None = Non
         ext = apply_corners(ext, combine_corners(_allgather_structs(crec, CornerRec, device)))
     octagon = build_octagon_from_set(ext)
     plan = make_plan(ext, octagon)
-    counts = shard.filter(plan)
+    counts = shard.filter_fused(ext, plan) if fused else shard.filter(plan)
     queues = [shard.queue_xy(q + 1, counts[q]) for q in range(4)]
     if stats is not None:
-        stats.update(counts=list(counts), uncertified=mask, ext=[int(v) for v in ext.ext],
+        stats.update(counts=list(counts), uncertified=mask, fused=fused,
+                     ext=[int(v) for v in ext.ext],
                      octagon=octagon.tolist(), n_total=int(g.n))
     gathered = _gather_queues(queues, device, root)
     if rank != root:

@@ -175,6 +175,44 @@ def test_shard_records_combine_to_whole(ctx, oracle, shards):
             assert np.array_equal(got, b0 + np.flatnonzero(want[b0:b1] == q + 1))
 
 
+@pytest.mark.parametrize("dist,shards", [("normal", 3), ("square", 2)])
+def test_fused_shards_match_whole(oracle, dist, shards):
+    # the fused pass per shard (each with its own context, region and
+    # candidates) combines to the reference result of the whole input: the
+    # records equal K1's, the per-shard queues equal build_queues' slices
+    pts = P.generate(dist, 30_000_000, 11)
+    n = len(pts)
+    bounds = np.linspace(0, n, shards + 1).astype(int)
+    ctxs = [P.Context(0) for _ in range(shards)]
+    devs = [dev(pts[b0:b1]) for b0, b1 in zip(bounds[:-1], bounds[1:])]
+    recs = []
+    for c, d, b0, b1 in zip(ctxs, devs, bounds[:-1], bounds[1:]):
+        rec = c.fused_extremes(d, b1 - b0, b0)
+        assert rec is not None, c.last_run()
+        k1 = c.extremes(d, b1 - b0, b0)
+        assert list(rec.idx) == list(k1.idx) and list(rec.second) == list(k1.second)
+        assert list(rec.key) == list(k1.key)
+        recs.append(rec)
+    g = P.combine_extremes(recs)
+    ext, mask = P.resolve_extremes(g)
+    assert mask == 0
+    want_ext = oracle.find_extremes(pts)
+    assert np.array_equal(ext.ext, want_ext)
+    octg = P.build_octagon_from_set(ext)
+    plan = P.make_plan(ext, octg)
+    want = oracle.classify(pts, want_ext, octg)
+    for c, d, b0, b1 in zip(ctxs, devs, bounds[:-1], bounds[1:]):
+        counts, fused = c.filter_fused(d, b1 - b0, ext, plan, b0)
+        assert fused
+        for q in range(4):
+            got = c.queue(q + 1, counts[q])[0]
+            assert np.array_equal(got, b0 + np.flatnonzero(want[b0:b1] == q + 1))
+    with pytest.raises(ValueError):  # no pending fused pass any more
+        ctxs[0].filter_fused(devs[0], bounds[1], ext, plan, 0)
+    for c in ctxs:
+        c.close()
+
+
 # ---------------------------------------------------------- large sizes ----
 def test_normal_1e8_matches_oracle(ctx, oracle):
     pts = P.generate("normal", 100_000_000, 7)
