@@ -12,18 +12,21 @@ independently and only the ~300 B extremes records and the survivors
 cross GPUs (sharded.py).
 
 A step is one full hull of the whole job's points:
-  value  -- inputs resident in HBM: K1 -> certificate -> (K1b) -> octagon ->
-            K2 -> survivors D2H -> host hull, Gpoints/s over all ranks,
+  value  -- inputs resident in HBM: the fused single pass (sample ->
+            provisional region -> KF filter pass -> K1 over the candidates)
+            or, when it does not apply, K1; certificate -> (K1b) ->
+            octagon -> K2 (candidates only when fused) -> survivors D2H ->
+            host hull, Gpoints/s over all ranks,
   e2e    -- the same through the reference-facing API with host buffers:
             N = 1 the C ABI call ohx_heaphull (octohull::heaphull) on
             pinned host points, N > 1 the sharded API with each rank's
             pinned shard uploaded inside the step.
 Steps are timed with CUDA events after a barrier + synchronize on both
 sides, max over ranks.  roofline: the dominant kernel's algorithmic bytes
-per launch (16 B per point read, + 4 B per survivor index written for K2)
-over its CUDA-event duration on the launching stream, against the measured
-HBM copy bandwidth in MEASURED_PEAKS.json.  cpu_baseline: the reference
-library itself (oracle/_ref, compiled from the reference sources) timed on
+per launch (16 B per point read; the fused KF pass also writes 4 B per
+candidate index) over its CUDA-event duration on the launching stream,
+against the measured HBM copy bandwidth in MEASURED_PEAKS.json.
+cpu_baseline: the reference library itself (oracle/_ref, compiled from the reference sources) timed on
 the host cores on a bounded 1e8-point sample.
 
 `--impl reference` times that reference CPU implementation on the same
@@ -260,7 +263,7 @@ def run_b200_arm(a):
     # ---------------- device-resident timed region
     for _ in range(a.warmup):
         step_device()
-    k1, k2 = [], []
+    k1, k2, kc, runs = [], [], [], []
     launches0 = ctx.launches
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -271,6 +274,8 @@ def run_b200_arm(a):
             km = ctx.kernel_ms()
             k1.append(km["k1"])
             k2.append(km["k2"])
+            kc.append(km["kc"])
+            runs.append(ctx.last_run())
         stop.record()
         barrier()
     launches = ctx.launches - launches0
@@ -315,13 +320,30 @@ def run_b200_arm(a):
         clocks_e2e_summary = None
 
     # ---------------- roofline of the dominant kernel
+    # algorithmic bytes per launch: every point read once by the
+    # streaming pass (16 B); fused, KF also writes its candidates' indices
+    # (idx B each) and the candidate stage / K2 touch only the candidates
     peak, peak_src = measured_peak()
     s_local = sum(stats["counts"])
+    idx_b = 4 if n < 2**32 else 8
+    fused = bool(runs) and all(r["fused"] for r in runs)
+    cand = runs[-1]["candidates"] if runs else 0
     k1_ms, k2_ms = statistics.mean(k1), statistics.mean(k2)
-    kern = {
-        "k1_extremes": {"ms": k1_ms, "bytes": 16 * n},
-        "k2_filter_compact": {"ms": k2_ms, "bytes": 16 * n + 4 * s_local},
-    }
+    if fused:
+        kern = {
+            "kf_filter": {"ms": k1_ms, "bytes": 16 * n + idx_b * cand,
+                          "note": "fused pass: region test + candidate append"},
+            "candidate_stage": {"ms": statistics.mean(kc),
+                                "bytes": cand * (idx_b * 2 + 16 * 2 + 16),
+                                "note": "scan + gather + K1 over candidates (+ host sync)"},
+            "k2_gather": {"ms": k2_ms, "bytes": cand * (idx_b + 16) + idx_b * s_local,
+                          "note": "K2 on the candidates only"},
+        }
+    else:
+        kern = {
+            "k1_extremes": {"ms": k1_ms, "bytes": 16 * n},
+            "k2_filter_compact": {"ms": k2_ms, "bytes": 16 * n + idx_b * s_local},
+        }
     for v in kern.values():
         v["gbs"] = v["bytes"] / (v["ms"] * 1e-3) / 1e9
         v["frac"] = v["gbs"] / peak
@@ -334,7 +356,9 @@ def run_b200_arm(a):
                 "unit": "GB/s", "frac": kern[dom]["gbs"] / peak, "traffic": traffic,
                 "peak_source": peak_src,
                 "algorithmic_bytes": kern[dom]["bytes"],
-                "kernels": kern}
+                "kernels": kern,
+                "pipeline": "fused single pass (KF)" if fused else "two passes (K1, K2)",
+                "candidates": cand}
 
     # ---------------- CPU baseline (rank 0, N = 1)
     cpu = None
