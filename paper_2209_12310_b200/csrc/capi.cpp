@@ -71,6 +71,10 @@ struct ohx_ctx {
   std::uint64_t regions_bytes = 0;
   double* d_cpts = nullptr;  // gathered candidate coordinates
   std::uint64_t cpts_bytes = 0;
+  void* d_hsort = nullptr;  // hull stage: device sweep sort work + sorted arcs
+  std::uint64_t hsort_bytes = 0;
+  void* h_sorted = nullptr;  // pinned: the sorted arcs on the host
+  std::uint64_t h_sorted_bytes = 0;
   unsigned long long* d_cnt = nullptr;
   unsigned long long* h_cnt = nullptr;  // pinned
 
@@ -740,10 +744,55 @@ void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s) {
   check_cuda(cudaStreamSynchronize(s), "queues fetch");
 }
 
-std::vector<P2> device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s) {
-  // reference hull.cpp:164-183 on the device queues: one gather launch and
-  // one D2H of the survivors' coordinates, then the host hull stage
+// Survivor counts from which the hull stage's sweep sort runs on the device
+constexpr std::uint64_t kDeviceSortMin = 8192;
+
+void host_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what) {
+  if (*have >= need && *p) return;
+  if (*p) check_cuda(cudaFreeHost(*p), "cudaFreeHost");
+  *p = nullptr;
+  *have = 0;
+  check_cuda(cudaMallocHost(p, need), what);
+  *have = need;
+}
+
+PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s) {
+  // reference hull.cpp:164-183 on the device queues
   const std::uint64_t total = f.counts[0] + f.counts[1] + f.counts[2] + f.counts[3];
+  const P2 anchors[4] = {{f.ext.x[OHX_EAST], f.ext.y[OHX_EAST]},
+                         {f.ext.x[OHX_NORTH], f.ext.y[OHX_NORTH]},
+                         {f.ext.x[OHX_WEST], f.ext.y[OHX_WEST]},
+                         {f.ext.x[OHX_SOUTH], f.ext.y[OHX_SOUTH]}};
+  if (total >= kDeviceSortMin) {
+    // large survivor sets: the arcs are built and sorted on the device and
+    // come back in sweep order; the chains and the clean-up run on the host
+    dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, total * 16, "gather");
+    launch_gather4(c->last_xy, c->d_queues, c->last_idx_bytes, c->last_cap, c->last_counts,
+                   c->d_gather, s);
+    ++c->launches;
+    const std::uint64_t arcs_n = total + 8;
+    dev_grow(&c->d_hsort, &c->hsort_bytes, sort_arcs_work_bytes(f.counts) + arcs_n * 16,
+             "hull sort work");
+    auto* d_sorted = reinterpret_cast<double*>(static_cast<unsigned char*>(c->d_hsort) +
+                                               sort_arcs_work_bytes(f.counts));
+    sort_arcs(c->d_gather, f.counts, reinterpret_cast<const double*>(anchors), c->d_hsort,
+              d_sorted, s);
+    c->launches += 2 + 4 * 4;  // build/gather + four radix sorts
+    host_grow(&c->h_sorted, &c->h_sorted_bytes, arcs_n * 16, "cudaMallocHost(sorted arcs)");
+    check_cuda(cudaMemcpyAsync(c->h_sorted, d_sorted, arcs_n * 16, cudaMemcpyDeviceToHost, s),
+               "cudaMemcpyAsync(sorted arcs)");
+    check_cuda(cudaStreamSynchronize(s), "hull sort");
+    const P2* arcs[4];
+    std::uint64_t len[4], off = 0;
+    for (int q = 0; q < 4; ++q) {
+      arcs[q] = static_cast<const P2*>(c->h_sorted) + off;
+      len[q] = f.counts[q] + 2;
+      off += len[q];
+    }
+    return hull_from_sorted_arcs(arcs, len);
+  }
+  // one gather launch and one D2H of the survivors' coordinates, then the
+  // host hull stage
   std::vector<P2> packed(total);
   queues_fetch_xy(c, reinterpret_cast<double*>(packed.data()), s);
   const P2* qp[4];
@@ -752,10 +801,6 @@ std::vector<P2> device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t 
     qp[k] = packed.data() + off;
     off += f.counts[k];
   }
-  const P2 anchors[4] = {{f.ext.x[OHX_EAST], f.ext.y[OHX_EAST]},
-                         {f.ext.x[OHX_NORTH], f.ext.y[OHX_NORTH]},
-                         {f.ext.x[OHX_WEST], f.ext.y[OHX_WEST]},
-                         {f.ext.x[OHX_SOUTH], f.ext.y[OHX_SOUTH]}};
   return hull_from_queue_points(anchors, qp, f.counts);
 }
 
@@ -1186,10 +1231,10 @@ void destroy_ctx(ohx_ctx* c) {
                   c->d_queues, static_cast<void*>(c->d_pts),
                   static_cast<void*>(c->d_labels), static_cast<void*>(c->d_gather),
                   static_cast<void*>(c->d_sample), c->d_cand, static_cast<void*>(c->d_cnt),
-                  c->d_regions, static_cast<void*>(c->d_cpts)})
+                  c->d_regions, static_cast<void*>(c->d_cpts), c->d_hsort})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_crec),
-                  static_cast<void*>(c->h_counts), static_cast<void*>(c->h_cnt)})
+                  static_cast<void*>(c->h_counts), static_cast<void*>(c->h_cnt), c->h_sorted})
     if (p) cudaFreeHost(p);
   for (auto& pair : c->ev)
     for (auto& e : pair)

@@ -5,15 +5,32 @@
 // strict-left-turn chain, then cycle clean-up (de-duplication, collinear
 // collapse, strict_cycle peeling, rotation to the east-most vertex).
 // Outputs are coordinate-identical to the reference for every input; the
-// implementation differs where that cannot change the result: the four
-// quadrant chains run concurrently and large sorts use the libstdc++
-// parallel sort (equal points are indistinguishable, so any sort order of
-// ties yields the same chain).
+// implementation differs where that cannot change the result:
+//  * large survivor sets arrive already sorted from the device
+//    (hullsort.cu); smaller ones use the libstdc++ (parallel) sort -- equal
+//    points are indistinguishable, so any order of ties yields the same
+//    chain;
+//  * the four quadrant chains run concurrently (each chain is the
+//    reference's sequential stack loop: its decisions are the reference's
+//    predicate sequence, which a parallel hull would not reproduce on
+//    near-degenerate inputs);
+//  * the clean-up's linear passes (de-duplication, collinearity test,
+//    compaction, rotation) run in parallel, and the peel replays the
+//    reference's LIFO worklist exactly while skipping the vertices whose
+//    test cannot change (see peel).
+#include <omp.h>
 #include <parallel/algorithm>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
 #include <thread>
+#include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "internal.hpp"
@@ -27,6 +44,20 @@ int orient(const P2& a, const P2& b, const P2& c) {
 }
 
 namespace {
+
+// OHX_TRACE=1: wall time of the hull phases on stderr
+bool trace_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("OHX_TRACE");
+    return e && *e && std::string(e) != "0";
+  }();
+  return on;
+}
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
 
 bool same(const P2& a, const P2& b) { return a.x == b.x && a.y == b.y; }
 
@@ -45,104 +76,343 @@ struct SweepLess {
 
 bool lex(const P2& a, const P2& b) { return a.x != b.x ? a.x < b.x : a.y < b.y; }
 
-template <class Cmp>
-void big_sort(std::vector<P2>& v, Cmp cmp) {
+// the reference's preferred first vertex: max x, ties to the smaller y
+bool starts_before(const P2& a, const P2& b) { return a.x != b.x ? a.x > b.x : a.y < b.y; }
+
+template <class V, class Cmp>
+void big_sort(V& v, Cmp cmp) {
   if (v.size() >= (1u << 17)) __gnu_parallel::sort(v.begin(), v.end(), cmp);
   else std::sort(v.begin(), v.end(), cmp);
 }
 
-// Peel every vertex that does not turn strictly left, re-examining the
-// neighbours of each removal (LIFO worklist, reference hull.cpp:54-92; the
-// visiting order is kept so degenerate cycles reduce identically).
-std::vector<P2> peel(const std::vector<P2>& cyc) {
-  const std::size_t m = cyc.size();
-  std::vector<std::size_t> prv(m), nxt(m), stack;
-  std::vector<unsigned char> alive(m, 1), pending(m, 1);
-  stack.reserve(m);
-  for (std::size_t i = 0; i < m; ++i) {
-    prv[i] = (i + m - 1) % m;
-    nxt[i] = (i + 1) % m;
-    stack.push_back(i);
+constexpr std::size_t kParMin = 1u << 16;  // below: serial loops
+
+// Parallel stream compaction: the elements i of `in` with keep(i), in order.
+template <class Keep>
+PVec compact(const P2* in, std::size_t n, Keep keep) {
+  PVec out;
+  if (n < kParMin) {
+    out.reserve(n);
+    for (std::size_t i = 0; i < n; ++i)
+      if (keep(i)) out.push_back(in[i]);
+    return out;
   }
-  std::size_t live = m;
-  while (!stack.empty() && live > 2) {
-    const std::size_t i = stack.back();
-    stack.pop_back();
-    pending[i] = 0;
-    if (!alive[i] || orient(cyc[prv[i]], cyc[i], cyc[nxt[i]]) > 0) continue;
-    alive[i] = 0;
-    --live;
-    nxt[prv[i]] = nxt[i];
-    prv[nxt[i]] = prv[i];
-    for (std::size_t nb : {prv[i], nxt[i]})
-      if (alive[nb] && !pending[nb]) {
-        stack.push_back(nb);
-        pending[nb] = 1;
-      }
+  const int T = omp_get_max_threads();
+  std::vector<std::size_t> cnt(T + 1, 0);
+#pragma omp parallel num_threads(T)
+  {
+    const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+    const std::size_t b = n * t / nt, e = n * (t + 1) / nt;
+    std::size_t c = 0;
+    for (std::size_t i = b; i < e; ++i) c += keep(i) ? 1 : 0;
+    cnt[t + 1] = c;
+#pragma omp barrier
+#pragma omp single
+    {
+      for (int k = 0; k < nt; ++k) cnt[k + 1] += cnt[k];
+      out.resize(cnt[nt]);
+    }
+    std::size_t o = cnt[t];
+    for (std::size_t i = b; i < e; ++i)
+      if (keep(i)) out[o++] = in[i];
   }
-  std::vector<P2> out;
-  out.reserve(live);
-  std::size_t s = 0;
-  while (!alive[s]) ++s;
-  std::size_t i = s;
-  do {
-    out.push_back(cyc[i]);
-    i = nxt[i];
-  } while (i != s);
   return out;
+}
+
+// Peel every vertex that does not turn strictly left, re-examining the
+// neighbours of each removal: the reference's LIFO worklist
+// (hull.cpp:54-92) replayed exactly, so degenerate cycles reduce
+// identically.  The worklist initially holds every vertex (m-1 on top);
+// popping a vertex that turns strictly left and whose neighbours never
+// changed is a no-op (its only effect, clearing its pending flag, is
+// implicit here: "pending" = below the scan pointer or on the explicit
+// stack), so the scan jumps from one vertex that needs a test -- a
+// non-strict turn (all found in parallel up front) or a pending vertex
+// whose neighbour was removed -- to the next.  Links of the cyclic list
+// are stored only where they changed (few removals: hash maps; many:
+// arrays).  Returns false when nothing is removed (`cyc` is the answer).
+template <class Links>
+bool peel_with(PVec& cyc, std::vector<std::size_t> todo, Links& L) {
+  const std::size_t m = cyc.size();
+  std::make_heap(todo.begin(), todo.end());  // pending tests, max first
+  std::vector<std::size_t> stack;            // explicit pushes (above the scan)
+  std::size_t ptr = m;                       // scan entries [0, ptr) still pending
+  std::size_t live = m;
+  bool removed = false;
+  while (live > 2) {
+    std::size_t i;
+    if (!stack.empty()) {
+      i = stack.back();
+      stack.pop_back();
+      L.set_on_stack(i, false);
+    } else {
+      if (todo.empty()) break;  // the rest of the scan is no-ops
+      std::pop_heap(todo.begin(), todo.end());
+      i = todo.back();
+      todo.pop_back();
+      L.set_queued(i, false);
+      ptr = i;  // every scan entry above i was popped as a no-op
+    }
+    const std::size_t a = L.prv(i), c = L.nxt(i);
+    if (!L.alive(i) || orient(cyc[a], cyc[i], cyc[c]) > 0) continue;
+    L.kill(i);
+    removed = true;
+    --live;
+    L.set_nxt(a, c);
+    L.set_prv(c, a);
+    for (std::size_t nb : {a, c}) {
+      if (!L.alive(nb)) continue;
+      if (nb < ptr) {  // still pending in the scan: test it when reached
+        if (!L.queued(nb)) {
+          L.set_queued(nb, true);
+          todo.push_back(nb);
+          std::push_heap(todo.begin(), todo.end());
+        }
+      } else if (!L.on_stack(nb)) {
+        stack.push_back(nb);
+        L.set_on_stack(nb, true);
+      }
+    }
+  }
+  if (removed) {
+    // unlinking keeps the cyclic index order: the survivors in index order
+    // (the reference walks the list from the first alive vertex)
+    PVec out = compact(cyc.data(), m, [&](std::size_t k) { return L.alive(k); });
+    cyc.swap(out);
+  }
+  return removed;
+}
+
+struct SparseLinks {
+  std::size_t m;
+  std::unordered_map<std::size_t, std::size_t> p, n;
+  std::unordered_set<std::size_t> dead, stacked, que;
+  std::size_t prv(std::size_t i) const {
+    const auto it = p.find(i);
+    return it != p.end() ? it->second : (i == 0 ? m - 1 : i - 1);
+  }
+  std::size_t nxt(std::size_t i) const {
+    const auto it = n.find(i);
+    return it != n.end() ? it->second : (i + 1 == m ? 0 : i + 1);
+  }
+  void set_prv(std::size_t i, std::size_t v) { p[i] = v; }
+  void set_nxt(std::size_t i, std::size_t v) { n[i] = v; }
+  bool alive(std::size_t i) const { return !dead.count(i); }
+  void kill(std::size_t i) { dead.insert(i); }
+  bool on_stack(std::size_t i) const { return stacked.count(i); }
+  void set_on_stack(std::size_t i, bool v) { v ? (void)stacked.insert(i) : (void)stacked.erase(i); }
+  bool queued(std::size_t i) const { return que.count(i); }
+  void set_queued(std::size_t i, bool v) { v ? (void)que.insert(i) : (void)que.erase(i); }
+};
+
+struct DenseLinks {
+  std::vector<std::size_t> p, n;
+  std::vector<std::uint8_t> flags;  // 1 dead, 2 on stack, 4 queued
+  explicit DenseLinks(std::size_t m) : p(m), n(m), flags(m, 0) {
+#pragma omp parallel for schedule(static) if (m >= kParMin)
+    for (std::int64_t i = 0; i < static_cast<std::int64_t>(m); ++i) {
+      p[i] = i == 0 ? m - 1 : i - 1;
+      n[i] = i + 1 == static_cast<std::int64_t>(m) ? 0 : i + 1;
+    }
+  }
+  std::size_t prv(std::size_t i) const { return p[i]; }
+  std::size_t nxt(std::size_t i) const { return n[i]; }
+  void set_prv(std::size_t i, std::size_t v) { p[i] = v; }
+  void set_nxt(std::size_t i, std::size_t v) { n[i] = v; }
+  bool alive(std::size_t i) const { return !(flags[i] & 1); }
+  void kill(std::size_t i) { flags[i] |= 1; }
+  bool on_stack(std::size_t i) const { return flags[i] & 2; }
+  void set_on_stack(std::size_t i, bool v) { flags[i] = v ? (flags[i] | 2) : (flags[i] & ~2); }
+  bool queued(std::size_t i) const { return flags[i] & 4; }
+  void set_queued(std::size_t i, bool v) { flags[i] = v ? (flags[i] | 4) : (flags[i] & ~4); }
+};
+
+void peel(PVec& cyc) {
+  const std::size_t m = cyc.size();
+  // the non-strict turns, ascending
+  const int T = omp_get_max_threads();
+  std::vector<std::vector<std::size_t>> part(m >= kParMin ? T : 1);
+#pragma omp parallel num_threads(static_cast<int>(part.size())) if (m >= kParMin)
+  {
+    const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+    const std::size_t b = m * t / nt, e = m * (t + 1) / nt;
+    for (std::size_t i = b; i < e; ++i) {
+      const std::size_t a = i == 0 ? m - 1 : i - 1, c = i + 1 == m ? 0 : i + 1;
+      if (orient(cyc[a], cyc[i], cyc[c]) <= 0) part[t].push_back(i);
+    }
+  }
+  std::vector<std::size_t> todo;
+  for (auto& v : part) todo.insert(todo.end(), v.begin(), v.end());
+  if (todo.empty()) return;
+  if (todo.size() * 64 < m) {
+    SparseLinks L{m, {}, {}, {}, {}, {}};
+    for (std::size_t i : todo) L.que.insert(i);
+    peel_with(cyc, std::move(todo), L);
+  } else {
+    DenseLinks L(m);
+    for (std::size_t i : todo) L.flags[i] |= 4;
+    peel_with(cyc, std::move(todo), L);
+  }
 }
 
 }  // namespace
 
-std::vector<P2> quadrant_chain(std::vector<P2> pts, int quadrant) {
-  // reference hull.cpp:133-150
-  if (pts.empty()) return {};
-  big_sort(pts, SweepLess{quadrant});
-  std::vector<P2> chain;
-  chain.reserve(std::min<std::size_t>(pts.size(), 1u << 20));
-  for (const P2& p : pts) {
-    while (chain.size() >= 2 && orient(chain[chain.size() - 2], chain.back(), p) <= 0)
-      chain.pop_back();
-    chain.push_back(p);
+void copy_points(P2* dst, const P2* src, std::size_t n) {
+  if (n < kParMin) {
+    std::memcpy(static_cast<void*>(dst), src, n * sizeof(P2));
+    return;
   }
-  chain.pop_back();  // the sweep's last point is the next arc's entry
+#pragma omp parallel
+  {
+    const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+    const std::size_t b = n * t / nt, e = n * (t + 1) / nt;
+    std::memcpy(static_cast<void*>(dst + b), src + b, (e - b) * sizeof(P2));
+  }
+}
+
+// The strict-left-turn chain of an arc already in sweep order (reference
+// hull.cpp:140-149); the sweep's last point is dropped (it is the next
+// arc's entry).  The top edge's differences are kept in registers: the
+// determinant is evaluated with exactly the reference's operations.
+PVec chain_sorted(const P2* pts, std::size_t n) {
+  if (n == 0) return {};
+  PVec chain(n);
+  P2* ch = chain.data();
+  std::size_t top = 0;  // chain[0, top)
+  for (std::size_t k = 0; k < n; ++k) {
+    const P2 p = pts[k];
+    while (top >= 2) {
+      const P2 a = ch[top - 2], b = ch[top - 1];
+      const double det = (b.x - a.x) * (p.y - a.y) - (b.y - a.y) * (p.x - a.x);
+      if (det > 0.0) break;
+      --top;
+    }
+    ch[top++] = p;
+  }
+  chain.resize(top - 1);
   return chain;
 }
 
-std::vector<P2> finalize_cycle(std::vector<P2> cycle) {
-  // reference hull.cpp:94-120
-  std::vector<P2> d;
-  d.reserve(cycle.size());
-  for (const P2& p : cycle)
-    if (d.empty() || !same(d.back(), p)) d.push_back(p);
+PVec quadrant_chain(std::vector<P2> pts, int quadrant) {
+  // reference hull.cpp:133-150
+  if (pts.empty()) return {};
+  const double t0 = now_ms();
+  big_sort(pts, SweepLess{quadrant});
+  const double t1 = now_ms();
+  PVec chain = chain_sorted(pts.data(), pts.size());
+  if (trace_on())
+    std::fprintf(stderr, "[ohx] hull q%d: %zu pts sort %.3f ms chain %.3f ms\n", quadrant,
+                 pts.size(), t1 - t0, now_ms() - t1);
+  return chain;
+}
+
+PVec finalize_cycle(PVec cycle) {
+  // reference hull.cpp:94-120.  Consecutive duplicates collapse first (a
+  // point is dropped iff it equals its predecessor: the last kept point
+  // always equals the predecessor), then equal front/back pairs.
+  double tt = now_ms();
+  auto tmark = [&](const char* w) {
+    if (trace_on()) std::fprintf(stderr, "[ohx]   finalize %-8s %.3f ms\n", w, now_ms() - tt);
+    tt = now_ms();
+  };
+  bool dups = false;
+  const std::size_t n0 = cycle.size();
+#pragma omp parallel for schedule(static) reduction(|| : dups) if (n0 >= kParMin)
+  for (std::int64_t k = 1; k < static_cast<std::int64_t>(n0); ++k)
+    dups = dups || same(cycle[k - 1], cycle[k]);
+  PVec d;
+  if (dups) {
+    const P2* c = cycle.data();
+    d = compact(c, n0, [&](std::size_t k) { return k == 0 || !same(c[k - 1], c[k]); });
+    PVec().swap(cycle);
+  } else {
+    d.swap(cycle);
+  }
+  tmark("dedup");
   while (d.size() > 1 && same(d.front(), d.back())) d.pop_back();
-  if (d.size() > 2) {
+  const std::size_t m = d.size();
+  if (m > 2) {
     bool flat = true;
-    for (std::size_t k = 2; k < d.size() && flat; ++k) flat = orient(d[0], d[1], d[k]) == 0;
+#pragma omp parallel for schedule(static) reduction(&& : flat) if (m >= kParMin)
+    for (std::int64_t k = 2; k < static_cast<std::int64_t>(m); ++k)
+      flat = flat && orient(d[0], d[1], d[k]) == 0;
+    tmark("flat");
     if (flat) {
       const auto mm = std::minmax_element(d.begin(), d.end(), lex);
       d = {*mm.first, *mm.second};
     } else {
-      d = peel(d);
+      peel(d);
     }
+    tmark("peel");
   }
   if (d.size() >= 2) {
-    // start at max x, ties to the smaller y (reference hull.cpp:35-49)
+    // start at the first vertex with max x, ties to the smaller y
+    // (reference hull.cpp:35-49)
+    const std::size_t sz = d.size();
     std::size_t best = 0;
-    for (std::size_t i = 1; i < d.size(); ++i) {
-      const P2 &a = d[i], &b = d[best];
-      if (a.x != b.x ? a.x > b.x : a.y < b.y) best = i;
+    if (sz < kParMin) {
+      for (std::size_t i = 1; i < sz; ++i)
+        if (starts_before(d[i], d[best])) best = i;
+    } else {
+      const int T = omp_get_max_threads();
+      std::vector<std::size_t> pb(T, 0);
+#pragma omp parallel num_threads(T)
+      {
+        const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+        const std::size_t b = sz * t / nt, e = sz * (t + 1) / nt;
+        std::size_t bi = b;
+        for (std::size_t i = b + 1; i < e; ++i)
+          if (starts_before(d[i], d[bi])) bi = i;
+        pb[t] = bi;
+      }
+      best = pb[0];
+      for (int t = 1; t < T; ++t)
+        if (pb[t] < sz && starts_before(d[pb[t]], d[best])) best = pb[t];
     }
-    std::rotate(d.begin(), d.begin() + static_cast<std::ptrdiff_t>(best), d.end());
+    tmark("best");
+    if (best != 0) {
+      PVec r(sz);
+      copy_points(r.data(), d.data() + best, sz - best);
+      copy_points(r.data() + (sz - best), d.data(), best);
+      d.swap(r);
+    }
+    tmark("rotate");
   }
   return d;
 }
 
-std::vector<P2> hull_from_queue_points(const P2 anchors[4], const P2* const q_pts[4],
-                                       const std::uint64_t q_len[4]) {
+PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4]) {
+  PVec chains[4];
+  const std::uint64_t total = len[0] + len[1] + len[2] + len[3];
+  const double t0 = now_ms();
+  if (total >= (1u << 16)) {
+    std::vector<std::thread> th;
+    for (int q = 0; q < 4; ++q)
+      th.emplace_back([&, q] { chains[q] = chain_sorted(arcs[q], len[q]); });
+    for (auto& t : th) t.join();
+  } else {
+    for (int q = 0; q < 4; ++q) chains[q] = chain_sorted(arcs[q], len[q]);
+  }
+  std::size_t h = 0;
+  for (int q = 0; q < 4; ++q) h += chains[q].size();
+  PVec cycle(h);
+  for (std::size_t q = 0, off = 0; q < 4; off += chains[q].size(), ++q)
+    copy_points(cycle.data() + off, chains[q].data(), chains[q].size());
+  for (auto& c : chains) PVec().swap(c);
+  const double t1 = now_ms();
+  PVec out = finalize_cycle(std::move(cycle));
+  if (trace_on())
+    std::fprintf(stderr,
+                 "[ohx] hull chains (sorted arcs, %llu pts) %.3f ms, finalize %zu vertices %.3f ms\n",
+                 static_cast<unsigned long long>(total), t1 - t0, out.size(), now_ms() - t1);
+  return out;
+}
+
+PVec hull_from_queue_points(const P2 anchors[4], const P2* const q_pts[4],
+                            const std::uint64_t q_len[4]) {
   // reference hull.cpp:164-183: arc q runs from anchor q-1 (entry) to
   // anchor q (exit) over the queue's members, in queue order
-  std::vector<P2> chains[4];
+  PVec chains[4];
   auto arc = [&](int q) {
     std::vector<P2> cand;
     cand.reserve(q_len[q] + 2);
@@ -159,18 +429,22 @@ std::vector<P2> hull_from_queue_points(const P2 anchors[4], const P2* const q_pt
   } else {
     for (int q = 0; q < 4; ++q) arc(q);
   }
-  std::vector<P2> cycle;
+  PVec cycle;
   for (int q = 0; q < 4; ++q) cycle.insert(cycle.end(), chains[q].begin(), chains[q].end());
-  return finalize_cycle(std::move(cycle));
+  const double t0 = now_ms();
+  PVec out = finalize_cycle(std::move(cycle));
+  if (trace_on())
+    std::fprintf(stderr, "[ohx] hull finalize: %zu vertices %.3f ms\n", out.size(), now_ms() - t0);
+  return out;
 }
 
-std::vector<P2> monotone_chain(const P2* pts, std::uint64_t n) {
+PVec monotone_chain(const P2* pts, std::uint64_t n) {
   // reference hull.cpp:205-232
   std::vector<P2> s(pts, pts + n);
   big_sort(s, lex);
   s.erase(std::unique(s.begin(), s.end(), same), s.end());
-  if (s.size() <= 2) return s;
-  std::vector<P2> lo, hi;
+  if (s.size() <= 2) return PVec(s.begin(), s.end());
+  PVec lo, hi;
   for (const P2& p : s) {
     while (lo.size() >= 2 && orient(lo[lo.size() - 2], lo.back(), p) <= 0) lo.pop_back();
     lo.push_back(p);
@@ -179,7 +453,7 @@ std::vector<P2> monotone_chain(const P2* pts, std::uint64_t n) {
     while (hi.size() >= 2 && orient(hi[hi.size() - 2], hi.back(), *it) <= 0) hi.pop_back();
     hi.push_back(*it);
   }
-  std::vector<P2> cyc(lo.begin(), lo.end() - 1);
+  PVec cyc(lo.begin(), lo.end() - 1);
   cyc.insert(cyc.end(), hi.begin(), hi.end() - 1);
   return cyc;
 }

@@ -10,6 +10,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "ohx.h"
@@ -170,12 +171,48 @@ int guard(F&& f) {
 struct P2 {
   double x, y;
 };
-std::vector<P2> quadrant_chain(std::vector<P2> pts, int quadrant);
-std::vector<P2> finalize_cycle(std::vector<P2> cycle);
-std::vector<P2> hull_from_queue_points(const P2 anchors[4],
-                                       const P2* const q_pts[4],
-                                       const std::uint64_t q_len[4]);
-std::vector<P2> monotone_chain(const P2* pts, std::uint64_t n);
+// A std::vector whose resize leaves new elements default-initialised: the
+// hull stage's buffers (up to ~1.6 GB) are written once, in parallel, with
+// no zero-fill pass over freshly mapped pages first.
+template <class T>
+struct DefaultInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = DefaultInitAlloc<U>;
+  };
+  DefaultInitAlloc() noexcept = default;
+  template <class U>
+  DefaultInitAlloc(const DefaultInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+};
+using PVec = std::vector<P2, DefaultInitAlloc<P2>>;
+// Parallel copy of n points (OpenMP above a size threshold)
+void copy_points(P2* dst, const P2* src, std::size_t n);
+
+PVec quadrant_chain(std::vector<P2> pts, int quadrant);
+// chain of an arc already in sweep order (the arc's last point dropped)
+PVec chain_sorted(const P2* pts, std::size_t n);
+// The hull stage's sweep sort on the device (hullsort.cu): the four arcs
+// [anchor q, queue q (packed [q1|q2|q3|q4] coordinates), anchor q+1], each
+// sorted in its quadrant's sweep order, written back to back to d_sorted
+// (sum(counts) + 8 points).
+std::size_t sort_arcs_work_bytes(const std::uint64_t counts[4]);
+void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const double anchors[8],
+               void* d_work, double* d_sorted, cudaStream_t s);
+// hull stage from the four arcs [anchor q, queue q, anchor q+1] already in
+// sweep order (device-sorted)
+PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4]);
+PVec finalize_cycle(PVec cycle);
+PVec hull_from_queue_points(const P2 anchors[4], const P2* const q_pts[4],
+                            const std::uint64_t q_len[4]);
+PVec monotone_chain(const P2* pts, std::uint64_t n);
 int orient(const P2& a, const P2& b, const P2& c);
 
 // ---- host generator (pointgen.cpp)

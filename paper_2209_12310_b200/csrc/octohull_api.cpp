@@ -66,10 +66,10 @@ ExtremeSet from_set(const ohx_extreme_set& s) {
 // hull.cpp:164-183): survivor coordinates are gathered on the device in
 // queue (= index) order and copied back, then chained on the host.
 HullPolygon hull_from_device(Device& d, const ohx::FilterOut& f) {
-  const std::vector<ohx::P2> cyc = ohx::device_queues_hull(d.c, f, d.s);
+  const ohx::PVec cyc = ohx::device_queues_hull(d.c, f, d.s);
   HullPolygon h;
   h.vertices.resize(cyc.size());
-  std::memcpy(static_cast<void*>(h.vertices.data()), cyc.data(), cyc.size() * sizeof(Point2D));
+  ohx::copy_points(reinterpret_cast<ohx::P2*>(h.vertices.data()), cyc.data(), cyc.size());
   return h;
 }
 
@@ -302,7 +302,7 @@ QuadQueues build_queues(const LabelArray& labels) {
 std::vector<Point2D> quadrant_hull(std::vector<Point2D> pts, int quadrant) {
   std::vector<ohx::P2> p(pts.size());
   std::memcpy(p.data(), pts.data(), pts.size() * sizeof(Point2D));
-  const std::vector<ohx::P2> c = ohx::quadrant_chain(std::move(p), quadrant);
+  const ohx::PVec c = ohx::quadrant_chain(std::move(p), quadrant);
   std::vector<Point2D> out(c.size());
   std::memcpy(static_cast<void*>(out.data()), c.data(), c.size() * sizeof(Point2D));
   return out;
@@ -348,7 +348,7 @@ HullPolygon heaphull(std::span<const Point2D> pts, ReduceConfig cfg) {
 HullPolygon monotone_chain_hull(std::span<const Point2D> pts) {
   // reference hull.cpp:205-232 (host; the independent check)
   if (pts.empty()) throw std::invalid_argument("monotone_chain_hull: empty point set");
-  const std::vector<ohx::P2> c =
+  const ohx::PVec c =
       ohx::monotone_chain(reinterpret_cast<const ohx::P2*>(pts.data()), pts.size());
   HullPolygon h;
   h.vertices.resize(c.size());

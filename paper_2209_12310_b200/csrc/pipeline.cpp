@@ -30,7 +30,8 @@ void copy_hull(const std::vector<octohull::Point2D>& v, double* out, std::uint64
                std::uint64_t* h) {
   *h = v.size();
   if (v.size() > cap) throw std::invalid_argument("hull output capacity too small");
-  std::memcpy(out, v.data(), v.size() * sizeof(octohull::Point2D));
+  ohx::copy_points(reinterpret_cast<ohx::P2*>(out), reinterpret_cast<const ohx::P2*>(v.data()),
+                   v.size());
 }
 
 }  // namespace
@@ -63,10 +64,10 @@ int ohx_heaphull_device(ohx_ctx* ctx, const double* d_xy, uint64_t n, double* h_
     const auto t0 = Clock::now();
     const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
     const auto t1 = Clock::now();
-    const std::vector<ohx::P2> cyc = ohx::device_queues_hull(ctx, f, s);
+    const ohx::PVec cyc = ohx::device_queues_hull(ctx, f, s);
     *h = cyc.size();
     if (cyc.size() > cap) throw std::invalid_argument("hull output capacity too small");
-    std::memcpy(h_hull, cyc.data(), cyc.size() * sizeof(ohx::P2));
+    ohx::copy_points(reinterpret_cast<ohx::P2*>(h_hull), cyc.data(), cyc.size());
     const auto t2 = Clock::now();
     if (timings) {
       timings[0] = ms(t0, t1);
@@ -141,10 +142,10 @@ int ohx_hull_from_queues(const double* h_xy, const uint64_t ext_axis[4],
     }
     const ohx::P2 anchors[4] = {P[ext_axis[0]], P[ext_axis[1]], P[ext_axis[2]],
                                 P[ext_axis[3]]};
-    const std::vector<ohx::P2> cyc = ohx::hull_from_queue_points(anchors, qp, q_len);
+    const ohx::PVec cyc = ohx::hull_from_queue_points(anchors, qp, q_len);
     *h = cyc.size();
     if (cyc.size() > cap) throw std::invalid_argument("hull output capacity too small");
-    std::memcpy(h_hull, cyc.data(), cyc.size() * sizeof(ohx::P2));
+    ohx::copy_points(reinterpret_cast<ohx::P2*>(h_hull), cyc.data(), cyc.size());
   });
 }
 
@@ -155,10 +156,10 @@ int ohx_hull_from_queue_points(const double anchors_xy[8], const double* const q
     const ohx::P2* qp[4];
     for (int k = 0; k < 4; ++k) qp[k] = reinterpret_cast<const ohx::P2*>(q_xy[k]);
     const auto* A = reinterpret_cast<const ohx::P2*>(anchors_xy);
-    const std::vector<ohx::P2> cyc = ohx::hull_from_queue_points(A, qp, q_len);
+    const ohx::PVec cyc = ohx::hull_from_queue_points(A, qp, q_len);
     *h = cyc.size();
     if (cyc.size() > cap) throw std::invalid_argument("hull output capacity too small");
-    std::memcpy(h_hull, cyc.data(), cyc.size() * sizeof(ohx::P2));
+    ohx::copy_points(reinterpret_cast<ohx::P2*>(h_hull), cyc.data(), cyc.size());
   });
 }
 

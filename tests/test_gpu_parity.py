@@ -376,3 +376,15 @@ def test_sorted_input_overflows_warp_regions_and_stays_exact():
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=600)
     assert r.returncode == 0 and "sorted ok" in r.stdout, r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("scale", [50.0, 3000.0, 1e6])
+def test_device_sorted_hull_on_degenerate_survivors(oracle, scale):
+    # survivor sets past the device sweep-sort threshold, full of duplicates,
+    # collinear runs and -0.0 / +0.0 coordinates (np.round(-0.3) == -0.0)
+    rng = np.random.default_rng(int(scale))
+    t = rng.uniform(0, 2 * np.pi, 300_000)
+    pts = np.ascontiguousarray(np.round(np.stack([np.cos(t), np.sin(t)], 1) * scale))
+    assert np.signbit(pts).any() and (scale > 1e4 or (pts == 0).any())
+    hull = P.heaphull(pts)
+    assert np.array_equal(hull, oracle.heaphull(pts))

@@ -93,6 +93,24 @@ def test_host_hull_matches_oracle_on_degenerate_grids(oracle, grid_trials):
         assert hull_via_library(oracle, a).tolist() == t["hull"]
 
 
+def test_host_hull_large_degenerate_sets(oracle):
+    # sizes past the parallel thresholds of the host hull stage (compaction,
+    # collinearity reduction, the scan-skipping peel) on inputs full of
+    # duplicates, collinear runs and non-strict seams
+    rng = np.random.default_rng(5)
+    cases = []
+    for g in (3, 7, 40, 1000):
+        cases.append(rng.integers(0, g, size=(150_000, 2)).astype(float))
+    t = rng.uniform(0, 2 * np.pi, 200_000)
+    for scale in (50.0, 3000.0):  # circle points snapped to a grid: collinear chords
+        cases.append(np.round(np.stack([np.cos(t), np.sin(t)], 1) * scale))
+    line = np.stack([np.arange(100_000.0), 2 * np.arange(100_000.0)], 1)
+    cases.append(np.concatenate([line, line[::-1]]))  # fully collinear
+    for a in cases:
+        a = np.ascontiguousarray(a)
+        assert np.array_equal(hull_via_library(oracle, a), oracle.heaphull(a))
+
+
 # ------------------------------------------------- extremes combine + cert
 def resolve_like_pipeline(pts, shards):
     """Shard -> K1 records -> combine -> certificate -> (exact corners)."""
