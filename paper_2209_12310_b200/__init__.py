@@ -20,8 +20,8 @@ import ctypes as C
 
 import numpy as np
 
-from ._lib import (DISTS, SLOTS, CornerRec, ExtremeSet, ExtremesRec, FilterPlan, OhxError,
-                   RunInfo, check, lib)
+from ._lib import (DISTS, OHX_E_INVALID, SLOTS, CornerRec, ExtremeSet, ExtremesRec, FilterPlan,
+                   OhxError, RunInfo, check, lib)
 
 __all__ = ["classify", "filter_rate", "generate", "heaphull", "monotone_chain",
            "heaphull_run", "find_extremes", "Context", "OhxError", "device_count"]
@@ -247,12 +247,18 @@ class Context:
 
     def heaphull_device(self, d_xy, n: int):
         """Full pipeline on device-resident points -> (hull, timings)."""
-        hull = np.empty((n + 8, 2), dtype=np.float64)
-        h = C.c_uint64(0)
-        t = np.zeros(4, dtype=np.float64)
-        check(lib.ohx_heaphull_device(self.h, _ptr(d_xy), n, hull.ctypes.data_as(_dp),
-                                      len(hull), C.byref(h), t.ctypes.data_as(_dp)))
-        return hull[: h.value].copy(), dict(filter_ms=t[0], hull_ms=t[1], total_ms=t[2])
+        cap = min(n + 8, 1 << 24)
+        while True:
+            hull = np.empty((cap, 2), dtype=np.float64)
+            h = C.c_uint64(0)
+            t = np.zeros(4, dtype=np.float64)
+            rc = lib.ohx_heaphull_device(self.h, _ptr(d_xy), n, hull.ctypes.data_as(_dp),
+                                         len(hull), C.byref(h), t.ctypes.data_as(_dp))
+            if rc == OHX_E_INVALID and h.value > cap:  # the hull outgrew the buffer
+                cap = h.value
+                continue
+            check(rc)
+            return hull[: h.value].copy(), dict(filter_ms=t[0], hull_ms=t[1], total_ms=t[2])
 
 
 # ---- host-only helpers of the C ABI (pure functions, no device) ---------

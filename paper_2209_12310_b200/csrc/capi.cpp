@@ -591,10 +591,11 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
     const std::uint64_t ntiles = (items + kK2Tile - 1) / kK2Tile;
     dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes,
              k2_work_bytes(ntiles), "k2 work area");
-    // queue capacity: a quarter of the items plus slack; grown and re-run on
-    // overflow (counts are exact even when stores are dropped)
+    // queue capacity: 1/16 of the items (at least 1M); grown to the exact
+    // counts and re-run on overflow (counts are exact even when stores are
+    // dropped)
     std::uint64_t cap =
-        std::min<std::uint64_t>(items, std::max<std::uint64_t>(4096, items / 4 + items / 16));
+        std::min<std::uint64_t>(items, std::max<std::uint64_t>(1u << 20, items / 16));
     if (c->queue_bytes / (4ull * idx_bytes) > cap)
       cap = std::min<std::uint64_t>(items, c->queue_bytes / (4ull * idx_bytes));
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -745,7 +746,7 @@ void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s) {
 }
 
 // Survivor counts from which the hull stage's sweep sort runs on the device
-constexpr std::uint64_t kDeviceSortMin = 8192;
+constexpr std::uint64_t kDeviceSortMin = 1u << 17;
 
 void host_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what) {
   if (*have >= need && *p) return;
@@ -846,6 +847,8 @@ int fuse_mode() {
   return mode;
 }
 constexpr int kSampleLen = 8192;     // points per sample run
+static_assert(kSampleLen % 2048 == 0, "k1_small reads sample runs 2048 points at a time");
+constexpr int kCoverageStep = 4;      // coverage counted on every 4th run
 constexpr int kSampleMaxSegs = 1024;  // runs (8M points, 128 MB) for n >= 2^27
 constexpr int kSubSamples = 8;  // disjoint sub-samples of kSampleSegs / 8 runs each
 constexpr double kFuseMinCoverage = 0.8;
@@ -995,7 +998,6 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   // about n/16 sampled points, 64..1024 runs, a multiple of kSubSamples
   const int segs = static_cast<int>(std::clamp<std::uint64_t>(
                        n / (16ull * kSampleLen), 64, kSampleMaxSegs)) / kSubSamples * kSubSamples;
-  const std::uint64_t ns = std::uint64_t(segs) * kSampleLen;
   dev_grow(reinterpret_cast<void**>(&c->d_sample), &c->sample_bytes,
            kSubSamples * sizeof(ohx_extremes_rec), "sample records");
   auto* d_recs = reinterpret_cast<ohx_extremes_rec*>(c->d_sample);
@@ -1035,11 +1037,12 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   double lim[8];
   for (int a = 0; a < 8; ++a) lim[a] = a < 4 ? all.key[a] : all.second[a - 4];
   if (!fit_region(region, lim, q)) return false;
-  launch_count_in_region(d_xy, n, segs, kSampleLen, *q, c->d_cnt, s);
+  launch_count_in_region(d_xy, n, segs, kSampleLen, kCoverageStep, *q, c->d_cnt, s);
   ++c->launches;
   check_cuda(cudaMemcpyAsync(c->h_cnt, c->d_cnt, 8, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
   check_cuda(cudaStreamSynchronize(s), "sample coverage");
-  f.sample_coverage = double(*c->h_cnt) / double(ns);
+  f.sample_coverage =
+      double(*c->h_cnt) / double(std::uint64_t((segs + kCoverageStep - 1) / kCoverageStep) * kSampleLen);
   f.fuse_state = 3;
   return f.sample_coverage >= kFuseMinCoverage || fuse_mode() == 3;
 }

@@ -385,7 +385,7 @@ PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4]) 
   PVec chains[4];
   const std::uint64_t total = len[0] + len[1] + len[2] + len[3];
   const double t0 = now_ms();
-  if (total >= (1u << 16)) {
+  if (total >= (1u << 12)) {  // one thread per arc
     std::vector<std::thread> th;
     for (int q = 0; q < 4; ++q)
       th.emplace_back([&, q] { chains[q] = chain_sorted(arcs[q], len[q]); });
@@ -422,7 +422,7 @@ PVec hull_from_queue_points(const P2 anchors[4], const P2* const q_pts[4],
     chains[q] = quadrant_chain(std::move(cand), q + 1);
   };
   const std::uint64_t total = q_len[0] + q_len[1] + q_len[2] + q_len[3];
-  if (total >= (1u << 16)) {
+  if (total >= (1u << 12)) {  // one thread per arc
     std::vector<std::thread> th;
     for (int q = 0; q < 4; ++q) th.emplace_back(arc, q);
     for (auto& t : th) t.join();

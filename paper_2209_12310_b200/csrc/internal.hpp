@@ -125,7 +125,8 @@ void launch_k1_sample(const double* d_xy, std::uint64_t n, int segs, int len, in
 int k1_list_grid(std::uint64_t n);
 void launch_k1_list(const double* d_xy, std::uint64_t n, K1Partial* partials, int grid,
                     unsigned* ticket, ohx_extremes_rec* d_rec, cudaStream_t stream);
-void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int len,
+// points of the sample runs 0, step, 2 step, ... inside Q
+void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int len, int step,
                             const KFRegion& q, unsigned long long* d_count, cudaStream_t stream);
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
                     std::uint64_t cap, const std::uint64_t counts[4], double* d_out,

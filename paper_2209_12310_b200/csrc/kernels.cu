@@ -516,17 +516,30 @@ __global__ void __launch_bounds__(256)
   ArgState<8, 4> st;
   st.init();
   if constexpr (kSampled) {
-    // global indices only grow along a thread's runs (run b increases with s)
+    // global indices only grow along a thread's runs (run b increases with
+    // s); 8 loads in flight per thread (runs are multiples of 2048 points)
     const int nrun = sm.segs / sm.subs;
     for (int r = blockIdx.x; r < nrun; r += gridDim.x) {
       const std::uint64_t start = sm.run_start(std::uint64_t(r) * sm.subs + g);
-      for (int k = threadIdx.x; k < sm.len; k += 256)
-        k1_visit(st, ld_stream(pts + start + k), start + k);
+      for (int k0 = threadIdx.x; k0 < sm.len; k0 += 256 * 8) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_stream(pts + start + k0 + u * 256);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) k1_visit(st, v[u], start + k0 + u * 256);
+      }
     }
   } else {
-    for (std::uint64_t j = std::uint64_t(blockIdx.x) * 256 + threadIdx.x; j < n;
-         j += std::uint64_t(gridDim.x) * 256)
-      k1_visit(st, ld_stream(pts + j), j);
+    const std::uint64_t stride = std::uint64_t(gridDim.x) * 256;
+    std::uint64_t j = std::uint64_t(blockIdx.x) * 256 + threadIdx.x;
+    for (; j + 3 * stride < n; j += 4 * stride) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = ld_stream(pts + j + u * stride);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) k1_visit(st, v[u], j + u * stride);
+    }
+    for (; j < n; j += stride) k1_visit(st, ld_stream(pts + j), j);
   }
   block_reduce<8, 4, 256>(st);
   if (!grid_combine<8, 4, 256>(st, partials, ticket)) return;
@@ -1263,13 +1276,19 @@ __global__ void __launch_bounds__(kSBlock, 2)
 }
 
 // Number of the sample's points inside the region Q (sample coverage
-// estimate): block b counts run b.
+// estimate): block b counts run b * step.
 __global__ void __launch_bounds__(256)
-    count_in_region(const double2* __restrict__ pts, const SampleMap sm, const KFRegion q,
-                    unsigned long long* count) {
-  const std::uint64_t start = sm.run_start(blockIdx.x);
+    count_in_region(const double2* __restrict__ pts, const SampleMap sm, int step,
+                    const KFRegion q, unsigned long long* count) {
+  const std::uint64_t start = sm.run_start(std::uint64_t(blockIdx.x) * step);
   unsigned c = 0;
-  for (int k = threadIdx.x; k < sm.len; k += 256) c += in_region(q, ld_stream(pts + start + k));
+  for (int k0 = threadIdx.x; k0 < sm.len; k0 += 256 * 8) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = ld_stream(pts + start + k0 + u * 256);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) c += in_region(q, v[u]);
+  }
   c = __reduce_add_sync(kFull, c);
   if ((threadIdx.x & 31) == 0) atomicAdd(count, static_cast<unsigned long long>(c));
 }
@@ -1503,11 +1522,11 @@ void launch_k1_list(const double* d_xy, std::uint64_t n, K1Partial* partials, in
   check_cuda(cudaGetLastError(), "k1_small<list> launch");
 }
 
-void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int len,
+void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int len, int step,
                             const KFRegion& q, unsigned long long* d_count, cudaStream_t stream) {
   check_cuda(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), stream), "cudaMemsetAsync");
-  count_in_region<<<segs, 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy),
-                                            SampleMap{n, segs, len, 1}, q, d_count);
+  count_in_region<<<(segs + step - 1) / step, 256, 0, stream>>>(
+      reinterpret_cast<const double2*>(d_xy), SampleMap{n, segs, len, 1}, step, q, d_count);
   check_cuda(cudaGetLastError(), "count_in_region launch");
 }
 

@@ -388,3 +388,59 @@ def test_device_sorted_hull_on_degenerate_survivors(oracle, scale):
     assert np.signbit(pts).any() and (scale > 1e4 or (pts == 0).any())
     hull = P.heaphull(pts)
     assert np.array_equal(hull, oracle.heaphull(pts))
+
+
+def test_u64_indices_on_a_tiled_4p5e9_point_input(ctx):
+    # 4.5e9 points (72 GB of HBM) = the same 9e8-point block tiled 5 times:
+    # every shard-local index needs 64 bits (K1/K2/KF/queues take their u64
+    # paths).  Size-independent properties: the extremes are the block's
+    # (first occurrence wins), the hull is the block's hull, and every queue
+    # is the block's queue repeated with offsets t*B -- except that in the
+    # later tiles the copies of the eight kept points are plain boundary
+    # points of the octagon (reference label 0: only the kept INDICES carry
+    # the override, filter.cpp:108-124).
+    free, _ = torch.cuda.mem_get_info()
+    B, T = 900_000_000, 5
+    if free < (B * T * 16) * 1.25:
+        pytest.skip(f"needs ~{B * T * 16 * 1.25 / 2**30:.0f} GiB of free device memory")
+    n = B * T
+    blk = P.generate("normal", B, 3)
+    d = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    d[:B].copy_(torch.from_numpy(blk))
+    del blk
+    for t in range(1, T):
+        d[t * B:(t + 1) * B].copy_(d[:B])
+    # the block alone (u32 paths)
+    hull_b, _ = ctx.heaphull_device(d[:B], B)
+    info_b = ctx.last_run()
+    qb = [ctx.queue(q + 1, info_b["counts"][q])[0] for q in range(4)]
+    rec_b = ctx.extremes(d[:B], B)
+    ext_b, mask_b = P.resolve_extremes(rec_b)
+    if mask_b:
+        ext_b = P.apply_corners(ext_b, ctx.corners_exact(
+            d[:B], B, (rec_b.x[0], rec_b.y[1], rec_b.x[2], rec_b.y[3])))
+    kept = np.array(list(ext_b.ext), dtype=np.uint64)
+    want = [np.concatenate([qb[q]] + [qb[q][~np.isin(qb[q], kept)] + np.uint64(t * B)
+                                      for t in range(1, T)]) for q in range(4)]
+    # fused pipeline over the tiled input
+    hull, _ = ctx.heaphull_device(d, n)
+    info = ctx.last_run()
+    assert info["fused"], info
+    assert np.array_equal(hull, hull_b)
+    assert info["counts"] == [len(w) for w in want]
+    for q in range(4):
+        assert np.array_equal(ctx.queue(q + 1, info["counts"][q])[0], want[q]), q
+    # two-pass kernels (K1, K2) over the tiled input
+    rec = ctx.extremes(d, n)
+    assert list(rec.idx) == list(rec_b.idx) and rec.n == n
+    ext, mask = P.resolve_extremes(rec)
+    if mask:
+        ext = P.apply_corners(ext, ctx.corners_exact(d, n, (rec.x[0], rec.y[1], rec.x[2], rec.y[3])))
+    assert list(ext.ext) == list(ext_b.ext)
+    plan = P.make_plan(ext, P.build_octagon_from_set(ext))
+    counts = ctx.filter(d, n, plan)
+    assert counts == info["counts"]
+    for q in range(4):
+        assert np.array_equal(ctx.queue(q + 1, counts[q])[0], want[q]), q
+    del d
+    torch.cuda.empty_cache()
