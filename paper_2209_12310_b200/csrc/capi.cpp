@@ -8,6 +8,8 @@
 // and no -march, like the reference objects.
 #include <cuda_runtime.h>
 
+#include <omp.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -87,6 +89,11 @@ struct ohx_ctx {
     const double* d_xy = nullptr;
     std::uint64_t n = 0, base = 0, n_cand = 0;
   } fz;
+
+  // pinned staging ring for host copies of pageable user buffers
+  static constexpr int kStageBufs = 4;
+  void* h_stage[kStageBufs] = {};
+  cudaEvent_t stage_ev[kStageBufs] = {};
 
   // CUDA events bracketing the last launch of each stage: K1 (or KF), K1b,
   // K2, and the fused path's candidate stage (compaction + candidate K1)
@@ -384,13 +391,103 @@ cudaStream_t ctx_stream(ohx_ctx* c) { return c->stream; }
 std::mutex& ctx_mutex(ohx_ctx* c) { return c->mu; }
 void ctx_bind(ohx_ctx* c) { bind(c); }
 
+// ---- host <-> device copies of user buffers.  Page-locked memory is
+// copied directly; pageable memory (std::vector, numpy: what the reference's
+// API and bindings pass) would go through the driver's staging at ~11 GB/s,
+// so it goes through the context's ring of pinned chunks instead: host
+// threads copy chunk k into a pinned buffer while the copy engine moves
+// chunk k-1 (PCIe-bound, ~55 GB/s).
+constexpr std::uint64_t kStageChunk = 64ull << 20;  // bytes per pinned chunk
+constexpr std::uint64_t kStageMin = 1ull << 20;     // smaller copies go direct
+
+bool is_pinned(const void* h) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+void ensure_stage(ohx_ctx* c) {
+  if (c->h_stage[0]) return;
+  for (int b = 0; b < ohx_ctx::kStageBufs; ++b) {
+    check_cuda(cudaMallocHost(&c->h_stage[b], kStageChunk), "cudaMallocHost(staging)");
+    check_cuda(cudaEventCreateWithFlags(&c->stage_ev[b], cudaEventDisableTiming),
+               "cudaEventCreate(staging)");
+  }
+}
+
+void host_memcpy(void* dst, const void* src, std::uint64_t bytes) {
+  if (bytes < (8ull << 20)) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+#pragma omp parallel
+  {
+    const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+    const std::uint64_t b = bytes * t / nt, e = bytes * (t + 1) / nt;
+    std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
+  }
+}
+
+void copy_h2d(ohx_ctx* c, void* d, const void* h, std::uint64_t bytes, cudaStream_t s) {
+  if (bytes < kStageMin || is_pinned(h)) {
+    check_cuda(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(H2D)");
+    return;
+  }
+  ensure_stage(c);
+  const std::uint64_t chunks = (bytes + kStageChunk - 1) / kStageChunk;
+  for (std::uint64_t k = 0; k < chunks; ++k) {
+    const int b = static_cast<int>(k % ohx_ctx::kStageBufs);
+    const std::uint64_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    if (k >= ohx_ctx::kStageBufs)
+      check_cuda(cudaEventSynchronize(c->stage_ev[b]), "cudaEventSynchronize(staging)");
+    host_memcpy(c->h_stage[b], static_cast<const char*>(h) + off, len);
+    check_cuda(cudaMemcpyAsync(static_cast<char*>(d) + off, c->h_stage[b], len,
+                               cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(H2D chunk)");
+    check_cuda(cudaEventRecord(c->stage_ev[b], s), "cudaEventRecord(staging)");
+  }
+}
+
+void copy_d2h(ohx_ctx* c, void* h, const void* d, std::uint64_t bytes, cudaStream_t s) {
+  if (bytes < kStageMin || is_pinned(h)) {
+    check_cuda(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(D2H)");
+    check_cuda(cudaStreamSynchronize(s), "D2H");
+    return;
+  }
+  ensure_stage(c);
+  const std::uint64_t chunks = (bytes + kStageChunk - 1) / kStageChunk;
+  auto drain = [&](std::uint64_t k) {  // chunk k has been issued: copy it out
+    const int b = static_cast<int>(k % ohx_ctx::kStageBufs);
+    const std::uint64_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    check_cuda(cudaEventSynchronize(c->stage_ev[b]), "cudaEventSynchronize(staging)");
+    host_memcpy(static_cast<char*>(h) + off, c->h_stage[b], len);
+  };
+  for (std::uint64_t k = 0; k < chunks; ++k) {
+    const int b = static_cast<int>(k % ohx_ctx::kStageBufs);
+    if (k >= ohx_ctx::kStageBufs) drain(k - ohx_ctx::kStageBufs);
+    const std::uint64_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    check_cuda(cudaMemcpyAsync(c->h_stage[b], static_cast<const char*>(d) + off, len,
+                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(D2H chunk)");
+    check_cuda(cudaEventRecord(c->stage_ev[b], s), "cudaEventRecord(staging)");
+  }
+  for (std::uint64_t k = chunks > ohx_ctx::kStageBufs ? chunks - ohx_ctx::kStageBufs : 0;
+       k < chunks; ++k)
+    drain(k);
+}
+
 const double* stage_points(ohx_ctx* c, const double* h_xy, std::uint64_t n,
                            cudaStream_t s) {
   const std::uint64_t bytes = n * 16;
   dev_grow(reinterpret_cast<void**>(&c->d_pts), &c->pts_bytes, bytes, "points");
-  check_cuda(cudaMemcpyAsync(c->d_pts, h_xy, bytes, cudaMemcpyHostToDevice, s),
-             "cudaMemcpyAsync(points H2D)");
+  copy_h2d(c, c->d_pts, h_xy, bytes, s);
   return c->d_pts;
+}
+
+void fetch_labels(ohx_ctx* c, std::uint8_t* h_labels, const std::uint8_t* d_labels,
+                  std::uint64_t n, cudaStream_t s) {
+  copy_d2h(c, h_labels, d_labels, n, s);
 }
 
 std::uint8_t* stage_labels(ohx_ctx* c, std::uint64_t n) {
@@ -1239,6 +1336,10 @@ void destroy_ctx(ohx_ctx* c) {
   for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_crec),
                   static_cast<void*>(c->h_counts), static_cast<void*>(c->h_cnt), c->h_sorted})
     if (p) cudaFreeHost(p);
+  for (int b = 0; b < ohx_ctx::kStageBufs; ++b) {
+    if (c->h_stage[b]) cudaFreeHost(c->h_stage[b]);
+    if (c->stage_ev[b]) cudaEventDestroy(c->stage_ev[b]);
+  }
   for (auto& pair : c->ev)
     for (auto& e : pair)
       if (e) cudaEventDestroy(e);

@@ -284,8 +284,7 @@ LabelArray classify_points(std::span<const Point2D> pts, const Octagon& oct,
   std::uint64_t counts[4];
   ohx::filter(d.c, dx, pts.size(), 0, plan, dl, counts, d.s);
   LabelArray labels(pts.size());
-  ohx::check_cuda(cudaMemcpyAsync(labels.data(), dl, pts.size(), cudaMemcpyDeviceToHost, d.s),
-                  "cudaMemcpyAsync(labels)");
+  ohx::fetch_labels(d.c, labels.data(), dl, pts.size(), d.s);
   ohx::check_cuda(cudaStreamSynchronize(d.s), "classify_points");
   return labels;
 }
@@ -318,8 +317,7 @@ HeaphullRun heaphull_run(std::span<const Point2D> pts, ReduceEngine&) {
   const ohx::FilterOut f = ohx::device_filter(d.c, dx, pts.size(), dl, d.s);
   HeaphullRun run;
   run.labels.resize(pts.size());
-  ohx::check_cuda(cudaMemcpyAsync(run.labels.data(), dl, pts.size(), cudaMemcpyDeviceToHost, d.s),
-                  "cudaMemcpyAsync(labels)");
+  ohx::fetch_labels(d.c, run.labels.data(), dl, pts.size(), d.s);
   ohx::check_cuda(cudaStreamSynchronize(d.s), "heaphull_run");
   const auto t1 = Clock::now();
   run.hull = hull_from_device(d, f);

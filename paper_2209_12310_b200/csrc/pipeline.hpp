@@ -36,6 +36,9 @@ void ctx_bind(ohx_ctx* c);
 const double* stage_points(ohx_ctx* c, const double* h_xy, std::uint64_t n,
                            cudaStream_t s);
 std::uint8_t* stage_labels(ohx_ctx* c, std::uint64_t n);
+// labels back into a (possibly pageable) host buffer; synchronous
+void fetch_labels(ohx_ctx* c, std::uint8_t* h_labels, const std::uint8_t* d_labels,
+                  std::uint64_t n, cudaStream_t s);
 
 void extremes(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
               ohx_extremes_rec* out, cudaStream_t s);
