@@ -72,3 +72,59 @@ def test_sharded_pipeline_matches_oracle(world):
         assert p.exitcode == 0
     for name, hull_ok, ext_ok, n_ok in res:
         assert hull_ok and ext_ok and n_ok, name
+
+
+def _gpu_worker(rank, world, port, q):
+    sys.path.insert(0, os.path.dirname(HERE))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    import paper_2209_12310_b200 as P
+    from oracle import Oracle
+    from paper_2209_12310_b200.sharded import CudaShard, shard_range, sharded_heaphull
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o = Oracle()
+        ctx = P.Context(0)
+        out = []
+        for dist_name, n, seed in [("normal", 24_000_000, 5), ("square", 20_000_000, 8),
+                                   ("disk", 3_000_000, 2)]:
+            pts = P.generate(dist_name, n, seed)
+            b0, cnt = shard_range(n, world, rank)
+            d = torch.from_numpy(pts[b0:b0 + cnt]).cuda()
+            stats = {}
+            hull = sharded_heaphull(CudaShard(ctx, d, cnt, b0), device="cpu", stats=stats)
+            if rank == 0:
+                want = o.heaphull(pts)
+                out.append((dist_name, hull.tolist() == want.tolist(), stats["fused"]))
+        if rank == 0:
+            q.put(out)
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_cuda_shards_over_gloo_on_one_gpu():
+    # the real per-shard backend (CudaShard: fused pass on each shard's own
+    # sample, filter_fused against the global plan) in 2 processes sharing
+    # cuda:0, exchanging records and survivors over gloo
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("needs a CUDA device")
+    import torch.multiprocessing as mp
+    mctx = mp.get_context("spawn")
+    q = mctx.Queue()
+    port = _free_port()
+    procs = [mctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for name, hull_ok, fused in res:
+        assert hull_ok, name
+    assert [fused for _, _, fused in res] == [True, True, False]
