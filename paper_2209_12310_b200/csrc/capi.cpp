@@ -968,6 +968,22 @@ std::vector<P2> clip_left(const std::vector<P2>& poly, P2 a, P2 b) {
   return out;
 }
 
+// OHX_TRACE=1: host wall time of each pipeline phase on stderr
+struct Trace {
+  bool on = [] {
+    const char* e = std::getenv("OHX_TRACE");
+    return e && *e && std::string(e) != "0";
+  }();
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ohx] %-14s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 // key of slot a (ohx.h slot order: x, y, -x, -y, x+y, y-x, -(x+y), x-y)
 double slot_key(int a, double x, double y) {
   switch (a) {
@@ -1046,7 +1062,8 @@ bool fit_region(const std::vector<P2>& R, const double lim[8], KFRegion* q) {
   double lo = 0, hi = 1;
   at(1e-6, b);
   if (!region_inside(b, R)) return false;
-  for (int it = 0; it < 24; ++it) {
+  // bisections to ~1e-4 of the span: Q is pulled 0.2 % inwards afterwards
+  for (int it = 0; it < 14; ++it) {
     const double mid = (lo + hi) / 2;
     at(mid, b);
     if (region_inside(b, R)) lo = mid;
@@ -1056,7 +1073,7 @@ bool fit_region(const std::vector<P2>& R, const double lim[8], KFRegion* q) {
   for (int round = 0; round < 2; ++round)
     for (int a = 0; a < 8; ++a) {
       double good = b[a], bad = h[a];
-      for (int it = 0; it < 16; ++it) {
+      for (int it = 0; it < 10; ++it) {
         double t[8];
         std::memcpy(t, b, sizeof(t));
         t[a] = (good + bad) / 2;
@@ -1089,7 +1106,7 @@ bool fit_region(const std::vector<P2>& R, const double lim[8], KFRegion* q) {
 // Returns false when fusing does not pay (small input, no region, sample
 // coverage below kFuseMinCoverage).
 bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegion* q,
-                        cudaStream_t s, FilterOut& f) {
+                        std::uint64_t* sampled, cudaStream_t s, FilterOut& f, Trace& tr) {
   if (n < kFuseMinPoints || fuse_mode() == 0) return false;
   f.fuse_state = 2;
   // about n/16 sampled points, 64..1024 runs, a multiple of kSubSamples
@@ -1105,6 +1122,7 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   check_cuda(cudaMemcpyAsync(rs, d_recs, sizeof(rs), cudaMemcpyDeviceToHost, s),
              "cudaMemcpyAsync(sample recs)");
   check_cuda(cudaStreamSynchronize(s), "sample extremes");
+  tr.mark("sample k1");
   const int slot[8] = {OHX_EAST, OHX_NE, OHX_NORTH, OHX_NW,
                        OHX_WEST, OHX_SW, OHX_SOUTH, OHX_SE};
   std::vector<P2> region;
@@ -1134,14 +1152,14 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   double lim[8];
   for (int a = 0; a < 8; ++a) lim[a] = a < 4 ? all.key[a] : all.second[a - 4];
   if (!fit_region(region, lim, q)) return false;
+  tr.mark("region fit");
+  // the coverage count stays on the device: KF reads it and runs only when
+  // enough of the sample falls inside Q (no host round trip here)
   launch_count_in_region(d_xy, n, segs, kSampleLen, kCoverageStep, *q, c->d_cnt, s);
   ++c->launches;
-  check_cuda(cudaMemcpyAsync(c->h_cnt, c->d_cnt, 8, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
-  check_cuda(cudaStreamSynchronize(s), "sample coverage");
-  f.sample_coverage =
-      double(*c->h_cnt) / double(std::uint64_t((segs + kCoverageStep - 1) / kCoverageStep) * kSampleLen);
+  *sampled = std::uint64_t((segs + kCoverageStep - 1) / kCoverageStep) * kSampleLen;
   f.fuse_state = 3;
-  return f.sample_coverage >= kFuseMinCoverage || fuse_mode() == 3;
+  return true;
 }
 
 }  // namespace
@@ -1164,21 +1182,6 @@ FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
 }
 
 namespace {
-// OHX_TRACE=1: host wall time of each pipeline phase on stderr
-struct Trace {
-  bool on = [] {
-    const char* e = std::getenv("OHX_TRACE");
-    return e && *e && std::string(e) != "0";
-  }();
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void mark(const char* what) {
-    if (!on) return;
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[ohx] %-14s %8.3f ms\n", what,
-                 std::chrono::duration<double, std::milli>(now - t).count());
-    t = now;
-  }
-};
 
 // Fused pass, first half, over the n points of one shard (global indices
 // base + j): provisional region -> KF -> ordered candidate list -> K1 over
@@ -1189,55 +1192,67 @@ bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
                  FilterOut& f, ohx_extremes_rec* rec, cudaStream_t s, Trace& tr) {
   c->fz.active = false;
   KFRegion q;
-  const bool fuse = provisional_region(c, d_xy, n, &q, s, f);
-  tr.mark("region");
-  if (!fuse) return false;
+  std::uint64_t sampled = 0;
+  if (!provisional_region(c, d_xy, n, &q, &sampled, s, f, tr)) return false;
   const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
   const int grid = kf_grid(c->device);
   const std::uint64_t nw = std::uint64_t(grid) * kKFWarpsPerBlock;
   const std::uint64_t per = ((n + 255) / 256 + nw - 1) / nw * 256;  // points per warp
-  // room for 1.5x the sample's miss rate (+256) per warp region; a region
-  // that overflows sends the call down the two-pass path
+  // KF runs (device-side gate) when >= kFuseMinCoverage of the sample is in
+  // Q; each warp region has room for 1.5x the miss rate that allows (+256).
+  // A region that overflows sends the call down the two-pass path.
+  const double min_cov = fuse_mode() == 3 ? 0.0 : kFuseMinCoverage;
+  const auto gate_min = static_cast<std::uint64_t>(std::ceil(min_cov * double(sampled)));
   const std::uint64_t cap_w = std::min<std::uint64_t>(
-      per, 256 + static_cast<std::uint64_t>(1.5 * (1.0 - f.sample_coverage) * double(per)));
+      per, 256 + static_cast<std::uint64_t>(1.5 * (1.0 - min_cov) * double(per)));
   dev_grow(&c->d_regions, &c->regions_bytes, nw * cap_w * idx_bytes, "kf regions");
   dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes, nw * 12 + 16, "kf counts");
   auto* d_wcounts = reinterpret_cast<std::uint32_t*>(c->d_status);
   auto* d_offsets = c->d_status + (nw + 1) / 2;  // 8-byte aligned after the u32 counts
   check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
-  launch_kf(d_xy, n, q, grid, c->d_regions, idx_bytes, cap_w, d_wcounts, s);
+  launch_kf(d_xy, n, q, grid, c->d_regions, idx_bytes, cap_w, d_wcounts, c->d_cnt, gate_min, s);
   check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
   c->timed[0] = true;
   ++c->launches;
+  // candidate list + coordinates and K1 over them, sized on the device: the
+  // list buffers hold cap_c candidates (more: regrown and redone below)
   check_cuda(cudaEventRecord(c->ev[3][0], s), "cudaEventRecord");
-  launch_kf_scan(d_wcounts, nw, cap_w, d_offsets, c->d_counts, s);
-  ++c->launches;
-  check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
-  check_cuda(cudaStreamSynchronize(s), "kf candidates");
-  tr.mark("kf+scan");
+  launch_kf_scan(d_wcounts, nw, cap_w, d_offsets, c->d_cnt, c->d_counts, s);
+  std::uint64_t cap_c = std::max<std::uint64_t>(c->cpts_bytes / 16,
+                                                std::max<std::uint64_t>(1u << 20, n / 32));
+  auto candidates = [&](std::uint64_t cap) {
+    dev_grow(&c->d_cand, &c->cand_bytes, cap * idx_bytes, "candidates");
+    dev_grow(reinterpret_cast<void**>(&c->d_cpts), &c->cpts_bytes, cap * 16, "candidate points");
+    launch_kf_gather(d_xy, c->d_regions, idx_bytes, cap_w, d_wcounts, d_offsets, nw, c->d_cand,
+                     c->d_cpts, cap, s);
+    const int k1g = k1_list_grid(cap);
+    ensure_partials(c, k1g);
+    launch_k1_list(c->d_cpts, cap, c->d_counts, c->d_partials, k1g, c->d_ticket, c->d_rec, s);
+    launch_map_rec(c->d_rec, c->d_cand, idx_bytes, base, s);
+    c->launches += 3;
+    check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
+    check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
+                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec)");
+    check_cuda(cudaStreamSynchronize(s), "kf + candidate extremes");
+  };
+  candidates(cap_c);
+  ++c->launches;  // kf_scan
+  tr.mark("kf+cand-k1");
+  f.sample_coverage = double(c->h_counts[2]) / double(sampled);
   const std::uint64_t n_cand = c->h_counts[0];
   f.candidates = n_cand;
+  if (c->h_counts[2] < gate_min) return false;  // KF did not run: low coverage
   if (n_cand == 0 || c->h_counts[1] != 0) {
     f.fuse_state = 5;  // a warp region overflowed: the two-pass path
     return false;
   }
-  // ordered candidate list + coordinates; K1 over them, indices mapped back
-  dev_grow(&c->d_cand, &c->cand_bytes, n_cand * idx_bytes, "candidates");
-  dev_grow(reinterpret_cast<void**>(&c->d_cpts), &c->cpts_bytes, n_cand * 16, "candidate points");
-  launch_kf_gather(d_xy, c->d_regions, idx_bytes, cap_w, d_wcounts, d_offsets, nw, c->d_cand,
-                   c->d_cpts, s);
-  const int k1g = k1_list_grid(n_cand);
-  ensure_partials(c, k1g);
-  launch_k1_list(c->d_cpts, n_cand, c->d_partials, k1g, c->d_ticket, c->d_rec, s);
-  launch_map_rec(c->d_rec, c->d_cand, idx_bytes, base, s);
-  c->launches += 3;
+  if (n_cand > cap_c) {  // more candidates than the list buffers held
+    cap_c = n_cand;
+    candidates(cap_c);
+  }
   check_cuda(cudaEventRecord(c->ev[3][1], s), "cudaEventRecord");
   c->timed[3] = true;
-  check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
-                             cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec)");
-  check_cuda(cudaStreamSynchronize(s), "candidate extremes");
-  tr.mark("cand-k1");
   *rec = *c->h_rec;
   rec->n = n;
   c->fz = {true, q, d_xy, n, base, n_cand};

@@ -507,8 +507,9 @@ __device__ __forceinline__ void k1_visit(ArgState<8, 4>& st, double2 p, std::uin
 
 template <bool kSampled>
 __global__ void __launch_bounds__(256)
-    k1_small(const double2* __restrict__ pts, std::uint64_t n, const SampleMap sm,
-             K1Partial* partials, unsigned* ticket, ohx_extremes_rec* out) {
+    k1_small(const double2* __restrict__ pts, std::uint64_t n, const unsigned long long* d_n,
+             const SampleMap sm, K1Partial* partials, unsigned* ticket, ohx_extremes_rec* out) {
+  if (d_n != nullptr && *d_n < n) n = *d_n;  // list length counted on the device
   const int g = blockIdx.y;
   partials += std::uint64_t(g) * gridDim.x;
   ticket += g;
@@ -554,13 +555,14 @@ __global__ void __launch_bounds__(256)
         i = st.i[b];
         if (b >= 4) s2 = st.s[b - 4];
       }
-    const double2 p = pts[i];
+    const std::uint64_t cnt = kSampled ? std::uint64_t(sm.segs / sm.subs) * sm.len : n;
+    const double2 p = cnt ? pts[i] : make_double2(0.0, 0.0);  // an empty list has no winner
     out->key[a] = k;
     out->idx[a] = i;
     out->x[a] = p.x;
     out->y[a] = p.y;
     if (a >= 4) out->second[a - 4] = s2;
-    if (a == 0) out->n = kSampled ? std::uint64_t(sm.segs / sm.subs) * sm.len : n;
+    if (a == 0) out->n = cnt;
   }
 }
 
@@ -1095,10 +1097,15 @@ template <typename IdxT>
 __global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
     kf_filter(const double2* __restrict__ pts, std::uint64_t n, const KFRegion q,
               IdxT* __restrict__ regions, std::uint64_t cap_w,
-              std::uint32_t* __restrict__ warp_counts) {
+              std::uint32_t* __restrict__ warp_counts, const unsigned long long* __restrict__ gate,
+              unsigned long long gate_min) {
   const std::uint64_t nt = (n + kWT - 1) / kWT;
   const std::uint64_t nw = std::uint64_t(gridDim.x) * (kKFBlock / 32);
   const std::uint64_t gw = std::uint64_t(blockIdx.x) * (kKFBlock / 32) + (threadIdx.x >> 5);
+  if (*gate < gate_min) {  // the sample's coverage of Q is too low: no pass
+    if ((threadIdx.x & 31) == 0) warp_counts[gw] = 0;
+    return;
+  }
   const std::uint64_t per = (nt + nw - 1) / nw;
   const std::uint64_t b0 = min(nt, gw * per), b1 = min(nt, b0 + per);
   const std::uint64_t bf = max(b0, min(b1, n / kWT));  // tiles [b0, bf) are full
@@ -1111,11 +1118,13 @@ __global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
 }
 
 // Exclusive scan of the per-warp counts (one block): offsets, the total and
-// whether any region overflowed -> counts[0] = total, counts[1] = overflow.
+// whether any region overflowed -> counts[0] = total, counts[1] = overflow,
+// counts[2] = the coverage count KF was gated on.
 constexpr int kScanBlock = 1024;
 __global__ void __launch_bounds__(kScanBlock)
     kf_scan(const std::uint32_t* __restrict__ warp_counts, std::uint64_t nw, std::uint64_t cap_w,
-            std::uint64_t* __restrict__ offsets, unsigned long long* counts) {
+            std::uint64_t* __restrict__ offsets, const unsigned long long* gate,
+            unsigned long long* counts) {
   __shared__ std::uint64_t s_warp[kScanBlock / 32];
   __shared__ std::uint64_t s_carry;
   __shared__ int s_over;
@@ -1157,26 +1166,29 @@ __global__ void __launch_bounds__(kScanBlock)
   if (threadIdx.x == 0) {
     counts[0] = s_carry;
     counts[1] = s_over;
+    counts[2] = *gate;
   }
 }
 
-// One block per warp region: copies its candidates to the ordered list and
-// gathers their coordinates (cpts[k] = pts[cand[k]]) for the candidate K1
-// and the gather-mode K2.
+// One warp per KF warp region: copies its candidates to the ordered list
+// and gathers their coordinates (cpts[k] = pts[cand[k]]) for the candidate
+// K1 and the gather-mode K2.
 template <typename IdxT>
 __global__ void __launch_bounds__(256)
     kf_gather(const double2* __restrict__ pts, const IdxT* __restrict__ regions,
-              std::uint64_t cap_w, const std::uint32_t* __restrict__ warp_counts,
+              std::uint64_t cap_w, std::uint64_t nw, const std::uint32_t* __restrict__ warp_counts,
               const std::uint64_t* __restrict__ offsets, IdxT* __restrict__ cand,
-              double2* __restrict__ cpts) {
-  const std::uint64_t w = blockIdx.x;
-  const std::uint64_t cnt = warp_counts[w];
+              double2* __restrict__ cpts, std::uint64_t cap_c) {
+  const std::uint64_t w = std::uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (w >= nw) return;
   const std::uint64_t o = offsets[w];
+  if (o >= cap_c) return;
+  const std::uint64_t cnt = min(std::uint64_t(warp_counts[w]), cap_c - o);
   const IdxT* r = regions + w * cap_w;
-  for (std::uint64_t k = threadIdx.x; k < cnt; k += blockDim.x) {
+  for (std::uint64_t k = threadIdx.x & 31; k < cnt; k += 32) {
     const IdxT j = r[k];
     cand[o + k] = j;
-    cpts[o + k] = pts[j];
+    cpts[o + k] = ld_stream(pts + j);
   }
 }
 
@@ -1186,7 +1198,7 @@ template <typename IdxT>
 __global__ void map_rec_idx(ohx_extremes_rec* rec, const IdxT* __restrict__ cand,
                             std::uint64_t base) {
   const int a = threadIdx.x;
-  if (a < 8) rec->idx[a] = base + static_cast<std::uint64_t>(cand[rec->idx[a]]);
+  if (a < 8 && rec->n > 0) rec->idx[a] = base + static_cast<std::uint64_t>(cand[rec->idx[a]]);
 }
 
 // ====================================================== K1 (TMA variant) ==
@@ -1457,37 +1469,39 @@ int kf_grid(int device) {
 
 void launch_kf(const double* d_xy, std::uint64_t n, const KFRegion& q, int grid, void* d_regions,
                int idx_bytes, std::uint64_t cap_w, std::uint32_t* d_warp_counts,
-               cudaStream_t stream) {
+               const unsigned long long* d_gate, std::uint64_t gate_min, cudaStream_t stream) {
   const auto* pts = reinterpret_cast<const double2*>(d_xy);
   if (idx_bytes == 4)
     kf_filter<std::uint32_t><<<grid, kKFBlock, 0, stream>>>(
-        pts, n, q, static_cast<std::uint32_t*>(d_regions), cap_w, d_warp_counts);
+        pts, n, q, static_cast<std::uint32_t*>(d_regions), cap_w, d_warp_counts, d_gate, gate_min);
   else
     kf_filter<std::uint64_t><<<grid, kKFBlock, 0, stream>>>(
-        pts, n, q, static_cast<std::uint64_t*>(d_regions), cap_w, d_warp_counts);
+        pts, n, q, static_cast<std::uint64_t*>(d_regions), cap_w, d_warp_counts, d_gate, gate_min);
   check_cuda(cudaGetLastError(), "kf_filter launch");
 }
 
 void launch_kf_scan(const std::uint32_t* d_warp_counts, std::uint64_t nw, std::uint64_t cap_w,
-                    std::uint64_t* d_offsets, unsigned long long* d_counts, cudaStream_t stream) {
-  kf_scan<<<1, kScanBlock, 0, stream>>>(d_warp_counts, nw, cap_w, d_offsets, d_counts);
+                    std::uint64_t* d_offsets, const unsigned long long* d_gate,
+                    unsigned long long* d_counts, cudaStream_t stream) {
+  kf_scan<<<1, kScanBlock, 0, stream>>>(d_warp_counts, nw, cap_w, d_offsets, d_gate, d_counts);
   check_cuda(cudaGetLastError(), "kf_scan launch");
 }
 
 void launch_kf_gather(const double* d_xy, const void* d_regions, int idx_bytes,
                       std::uint64_t cap_w, const std::uint32_t* d_warp_counts,
                       const std::uint64_t* d_offsets, std::uint64_t nw, void* d_cand,
-                      double* d_cpts, cudaStream_t stream) {
+                      double* d_cpts, std::uint64_t cap_c, cudaStream_t stream) {
   const auto* pts = reinterpret_cast<const double2*>(d_xy);
   auto* cp = reinterpret_cast<double2*>(d_cpts);
+  const unsigned grid = static_cast<unsigned>((nw + 7) / 8);
   if (idx_bytes == 4)
-    kf_gather<<<static_cast<unsigned>(nw), 256, 0, stream>>>(
-        pts, static_cast<const std::uint32_t*>(d_regions), cap_w, d_warp_counts, d_offsets,
-        static_cast<std::uint32_t*>(d_cand), cp);
+    kf_gather<<<grid, 256, 0, stream>>>(
+        pts, static_cast<const std::uint32_t*>(d_regions), cap_w, nw, d_warp_counts, d_offsets,
+        static_cast<std::uint32_t*>(d_cand), cp, cap_c);
   else
-    kf_gather<<<static_cast<unsigned>(nw), 256, 0, stream>>>(
-        pts, static_cast<const std::uint64_t*>(d_regions), cap_w, d_warp_counts, d_offsets,
-        static_cast<std::uint64_t*>(d_cand), cp);
+    kf_gather<<<grid, 256, 0, stream>>>(
+        pts, static_cast<const std::uint64_t*>(d_regions), cap_w, nw, d_warp_counts, d_offsets,
+        static_cast<std::uint64_t*>(d_cand), cp, cap_c);
   check_cuda(cudaGetLastError(), "kf_gather launch");
 }
 
@@ -1505,7 +1519,7 @@ void launch_k1_sample(const double* d_xy, std::uint64_t n, int segs, int len, in
                       cudaStream_t stream) {
   const SampleMap sm{n, segs, len, subs};
   k1_small<true><<<dim3(segs / subs, subs), 256, 0, stream>>>(
-      reinterpret_cast<const double2*>(d_xy), 0, sm, partials, ticket, d_recs);
+      reinterpret_cast<const double2*>(d_xy), 0, nullptr, sm, partials, ticket, d_recs);
   check_cuda(cudaGetLastError(), "k1_small<sample> launch");
 }
 
@@ -1514,10 +1528,11 @@ int k1_list_grid(std::uint64_t n) {
   return static_cast<int>(b < 1 ? 1 : (b > 148 * 4 ? 148 * 4 : b));
 }
 
-void launch_k1_list(const double* d_xy, std::uint64_t n, K1Partial* partials, int grid,
-                    unsigned* ticket, ohx_extremes_rec* d_rec, cudaStream_t stream) {
+void launch_k1_list(const double* d_xy, std::uint64_t n, const unsigned long long* d_n,
+                    K1Partial* partials, int grid, unsigned* ticket, ohx_extremes_rec* d_rec,
+                    cudaStream_t stream) {
   k1_small<false><<<dim3(grid, 1), 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n,
-                                                    SampleMap{0, 1, 1, 1}, partials, ticket,
+                                                    d_n, SampleMap{0, 1, 1, 1}, partials, ticket,
                                                     d_rec);
   check_cuda(cudaGetLastError(), "k1_small<list> launch");
 }

@@ -352,30 +352,19 @@ def test_forced_fusion_heavy_candidates_match_oracle():
     assert r.returncode == 0 and "force ok" in r.stdout, r.stderr[-3000:]
 
 
-def test_sorted_input_overflows_warp_regions_and_stays_exact():
-    # points sorted by x put every candidate into the first and last warps'
-    # ranges: their KF regions overflow and the call takes the two-pass path
-    # (OHX_FUSE=force: the sorted sample's coverage alone would already
-    # decline the fused pass)
-    import subprocess
-    import sys
-    code = (
-        "import numpy as np, torch, paper_2209_12310_b200 as P\n"
-        "from oracle import Oracle\n"
-        "pts = P.generate('normal', 9_000_000, 13)\n"
-        "pts = np.ascontiguousarray(pts[np.argsort(pts[:, 0], kind='stable')])\n"
-        "ctx = P.Context(0)\n"
-        "hull, _ = ctx.heaphull_device(torch.from_numpy(pts).cuda(), len(pts))\n"
-        "info = ctx.last_run()\n"
-        "assert not info['fused'] and info['fuse_state'] == 'too-many-candidates', info\n"
-        "want_hull, want_labels = Oracle().heaphull(pts, with_labels=True)\n"
-        "assert np.array_equal(hull, want_hull)\n"
-        "assert info['counts'] == [int((want_labels == q).sum()) for q in (1, 2, 3, 4)]\n"
-        "print('sorted ok')\n")
-    env = dict(os.environ, OHX_FUSE="force", PYTHONPATH=ROOT)
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
-                       timeout=600)
-    assert r.returncode == 0 and "sorted ok" in r.stdout, r.stderr[-3000:]
+def test_sorted_input_overflows_warp_regions_and_stays_exact(ctx, oracle):
+    # points sorted by radius: the sample still covers the region well (the
+    # fused pass runs), but every candidate sits in the last warps' ranges,
+    # whose KF regions overflow -> the call takes the two-pass path
+    pts = P.generate("normal", 9_000_000, 13)
+    pts = np.ascontiguousarray(pts[np.argsort(np.hypot(pts[:, 0], pts[:, 1]), kind="stable")])
+    n = len(pts)
+    hull, _ = ctx.heaphull_device(dev(pts), n)
+    info = ctx.last_run()
+    assert not info["fused"] and info["fuse_state"] == "too-many-candidates", info
+    want_hull, want_labels = oracle.heaphull(pts, with_labels=True)
+    assert np.array_equal(hull, want_hull)
+    assert info["counts"] == [int((want_labels == q).sum()) for q in (1, 2, 3, 4)]
 
 
 @pytest.mark.parametrize("scale", [50.0, 3000.0, 1e6])
@@ -388,6 +377,7 @@ def test_device_sorted_hull_on_degenerate_survivors(oracle, scale):
     assert np.signbit(pts).any() and (scale > 1e4 or (pts == 0).any())
     hull = P.heaphull(pts)
     assert np.array_equal(hull, oracle.heaphull(pts))
+
 
 
 def test_u64_indices_on_a_tiled_4p5e9_point_input(ctx):
