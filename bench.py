@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=float, default=1e8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the full-size parity gate against the reference library")
     return ap.parse_args()
 
 
@@ -370,6 +372,36 @@ def run_b200_arm(a):
                "sample": f"{a.dist} n={ns} seed={a.seed}, reference heaphull_run x2 "
                          f"(ReduceEngine chunk 32, {r['cores']} workers), mean {t:.3f} s"}
 
+    # ---------------- full-size parity gate (rank 0, N = 1): the reference
+    # library's own heaphull_run / find_extremes on these very points
+    parity = None
+    if rank == 0 and world == 1 and not a.no_parity:
+        from oracle import Reference
+        if Reference.available():
+            ref = Reference()
+            cores = os.cpu_count() or 1
+            t0 = time.perf_counter()
+            ref_hull, ref_labels, _ = ref.heaphull_run(hp, cores, 32)
+            ref_ext = ref.find_extremes(hp, cores, 32)
+            ref_s = time.perf_counter() - t0
+            hull_dev = step_device()
+            info = ctx.last_run()
+            queues_ok = True
+            for q in range(4):
+                want = np.flatnonzero(ref_labels == q + 1)
+                got = ctx.queue(q + 1, info["counts"][q])[0]
+                queues_ok &= bool(np.array_equal(got, want))
+            parity = {"checked_against": f"reference heaphull_run + find_extremes (oracle/_ref, "
+                                         f"{cores} workers) on the same {n} points",
+                      "hull_equal": bool(np.array_equal(hull_dev, ref_hull)),
+                      "extremes_equal": stats["ext"] == [int(v) for v in ref_ext],
+                      "queues_equal": queues_ok,
+                      "survivors": int((ref_labels != 0).sum()), "h": int(len(ref_hull)),
+                      "reference_s": ref_s}
+            del ref_labels
+        else:
+            parity = {"checked_against": None, "why": "oracle/_ref not built"}
+
     if rank == 0:
         clk = clocks.summary()
         line = {
@@ -382,7 +414,7 @@ def run_b200_arm(a):
                        "l2": "inputs 16 GB/GPU >> 126 MB L2 (no flush needed)",
                        "survivors": stats["counts"], "corner_certificate": "pass" if not
                        stats["uncertified"] else f"fallback mask {stats['uncertified']}"},
-            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity, "clocks": clk,
             "clocks_e2e": clocks_e2e_summary, "gpu_launches": launches,
             "setup_s": setup_s,
         }
