@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--dist", default="normal")
-    ap.add_argument("--n", type=float, default=1e9, help="points per GPU")
+    ap.add_argument("--points", "--n", dest="n", type=float, default=1e9, help="points per GPU")
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--cpu-sample", type=float, default=1e8)
     ap.add_argument("--no-e2e", action="store_true")
@@ -218,10 +218,19 @@ def run_b200_arm(a):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if a.gpus != world:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # OHX_BENCH_BACKEND=gloo: a test mode for the N > 1 code path on a box
+    # with fewer GPUs than ranks (ranks share devices, exchanges go through
+    # host memory); the measured configuration is always NCCL
+    backend = os.environ.get("OHX_BENCH_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
+    xdev = dev if backend == "nccl" else torch.device("cpu")  # collective buffers
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
@@ -231,7 +240,7 @@ def run_b200_arm(a):
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=xdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -245,19 +254,19 @@ def run_b200_arm(a):
     d = host.to(dev)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
-    ctx = P.Context(local)
+    ctx = P.Context(local_dev)
     shard = CudaShard(ctx, d, n, base)
 
     def step_device(stats=None):
         if world == 1:
             hull, _ = ctx.heaphull_device(d, n)
             return hull
-        return sharded_heaphull(shard, device=dev, stats=stats)
+        return sharded_heaphull(shard, device=xdev, stats=stats)
 
     # correctness gate on this very workload: the sharded / single pipeline
     # must equal the kernel-level path (and K1/K2 are oracle-checked in tests)
     stats = {}
-    hull0 = sharded_heaphull(shard, device=dev, stats=stats)
+    hull0 = sharded_heaphull(shard, device=xdev, stats=stats)
     if rank == 0 and world == 1:
         hull1 = step_device()
         assert np.array_equal(hull0, hull1), "pipeline disagreement"
@@ -268,7 +277,7 @@ def run_b200_arm(a):
     k1, k2, kc, runs = [], [], [], []
     launches0 = ctx.launches
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local_dev) as clocks:
         barrier()
         start.record()
         for _ in range(a.steps):
@@ -301,10 +310,10 @@ def run_b200_arm(a):
             def step_e2e():
                 d2.copy_(host, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
-                sharded_heaphull(CudaShard(ctx, d2, n, base), device=dev)
+                sharded_heaphull(CudaShard(ctx, d2, n, base), device=xdev)
         for _ in range(a.warmup):
             step_e2e()
-        with ClockSampler(local) as clocks_e2e:
+        with ClockSampler(local_dev) as clocks_e2e:
             barrier()
             start.record()
             for _ in range(a.steps):

@@ -128,3 +128,23 @@ def test_sharded_cuda_shards_over_gloo_on_one_gpu():
     for name, hull_ok, fused in res:
         assert hull_ok, name
     assert [fused for _, _, fused in res] == [True, True, False]
+
+
+@pytest.mark.gpu
+def test_bench_multi_rank_path_on_one_gpu(tmp_path):
+    # bench.py's N > 1 code path (barriers, max over ranks, sharded fused
+    # pipeline, e2e with per-rank H2D) as 2 torchrun ranks sharing cuda:0;
+    # OHX_BENCH_BACKEND=gloo only swaps the collective backend
+    import json
+    import subprocess
+    root = os.path.dirname(HERE)
+    env = dict(os.environ, OHX_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(root, "bench.py"), "--gpus", "2", "--points", "1.2e7", "--steps", "3",
+           "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["points_total"] == 24_000_000
+    assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
