@@ -61,16 +61,15 @@ double now_ms() {
 
 bool same(const P2& a, const P2& b) { return a.x == b.x && a.y == b.y; }
 
-// CCW sweep keys of the four quadrant arcs (reference hull.cpp:18-30)
+// CCW sweep keys of the four quadrant arcs (reference hull.cpp:18-30),
+// one comparator type per quadrant so the sort inlines a branch-light key
+template <int Q>
 struct SweepLess {
-  int q;
   bool operator()(const P2& a, const P2& b) const {
-    switch (q) {
-      case 1: return a.x != b.x ? a.x > b.x : a.y < b.y;
-      case 2: return a.y != b.y ? a.y > b.y : a.x > b.x;
-      case 3: return a.x != b.x ? a.x < b.x : a.y > b.y;
-      default: return a.y != b.y ? a.y < b.y : a.x < b.x;
-    }
+    if constexpr (Q == 1) return a.x != b.x ? a.x > b.x : a.y < b.y;
+    else if constexpr (Q == 2) return a.y != b.y ? a.y > b.y : a.x > b.x;
+    else if constexpr (Q == 3) return a.x != b.x ? a.x < b.x : a.y > b.y;
+    else return a.y != b.y ? a.y < b.y : a.x < b.x;
   }
 };
 
@@ -86,6 +85,63 @@ void big_sort(V& v, Cmp cmp) {
 }
 
 constexpr std::size_t kParMin = 1u << 16;  // below: serial loops
+
+// Order-preserving u64 of a coordinate (-0.0 folded onto +0.0: the
+// reference's comparator sees them equal); hullsort.cu uses the same map.
+inline std::uint64_t asc_key(double v) {
+  if (v == 0.0) v = 0.0;
+  std::uint64_t u;
+  std::memcpy(&u, &v, 8);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// Sweep sort of a mid-sized arc: LSD radix sort (11-bit digits, digits all
+// keys share skipped) on the primary key, then runs of equal primary key
+// sorted by the comparator (rare: equal coordinates).  Linear passes
+// instead of ~n log n mispredicted comparisons (~50 ns per point on the
+// box's host for random arcs).  Equal points may come out in any order, as
+// with std::sort.
+template <int Q>
+void radix_sweep_sort(std::vector<P2>& pts) {
+  struct E {
+    std::uint64_t k;
+    std::uint32_t i;
+  };
+  const std::size_t n = pts.size();
+  std::vector<E> a(n), b(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    const P2& p = pts[i];
+    const std::uint64_t k = Q == 1 ? ~asc_key(p.x) : Q == 2 ? ~asc_key(p.y)
+                          : Q == 3 ? asc_key(p.x) : asc_key(p.y);
+    a[i] = {k, static_cast<std::uint32_t>(i)};
+  }
+  constexpr int kBits = 11, kBuckets = 1 << kBits;
+  std::vector<std::uint32_t> cnt(kBuckets + 1);
+  for (int shift = 0; shift < 64; shift += kBits) {
+    auto digit = [&](const E& e) { return static_cast<std::uint32_t>((e.k >> shift) & (kBuckets - 1)); };
+    std::fill(cnt.begin(), cnt.end(), 0u);
+    for (const E& e : a) ++cnt[digit(e) + 1];
+    if (cnt[digit(a[0]) + 1] == n) continue;  // every key has this digit
+    for (int d = 0; d < kBuckets; ++d) cnt[d + 1] += cnt[d];
+    for (const E& e : a) b[cnt[digit(e)]++] = e;
+    a.swap(b);
+  }
+  std::vector<P2> out(n);
+  for (std::size_t i = 0; i < n; ++i) out[i] = pts[a[i].i];
+  for (std::size_t r = 0; r < n;) {  // equal primary keys: secondary order
+    std::size_t e = r + 1;
+    while (e < n && a[e].k == a[r].k) ++e;
+    if (e - r > 1) std::sort(out.begin() + r, out.begin() + e, SweepLess<Q>{});
+    r = e;
+  }
+  pts.swap(out);
+}
+
+template <int Q>
+void sweep_sort(std::vector<P2>& pts) {
+  if (pts.size() >= 512 && pts.size() < (1u << 17)) radix_sweep_sort<Q>(pts);
+  else big_sort(pts, SweepLess<Q>{});
+}
 
 // Parallel stream compaction: the elements i of `in` with keep(i), in order.
 template <class Keep>
@@ -297,7 +353,12 @@ PVec quadrant_chain(std::vector<P2> pts, int quadrant) {
   // reference hull.cpp:133-150
   if (pts.empty()) return {};
   const double t0 = now_ms();
-  big_sort(pts, SweepLess{quadrant});
+  switch (quadrant) {
+    case 1: sweep_sort<1>(pts); break;
+    case 2: sweep_sort<2>(pts); break;
+    case 3: sweep_sort<3>(pts); break;
+    default: sweep_sort<4>(pts); break;
+  }
   const double t1 = now_ms();
   PVec chain = chain_sorted(pts.data(), pts.size());
   if (trace_on())

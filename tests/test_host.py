@@ -106,6 +106,11 @@ def test_host_hull_large_degenerate_sets(oracle):
         cases.append(np.round(np.stack([np.cos(t), np.sin(t)], 1) * scale))
     line = np.stack([np.arange(100_000.0), 2 * np.arange(100_000.0)], 1)
     cases.append(np.concatenate([line, line[::-1]]))  # fully collinear
+    # mid-sized arcs (the radix sweep sort): duplicates and +/-0.0 ties
+    for g in (5, 60):
+        cases.append(rng.integers(-g, g + 1, size=(20_000, 2)).astype(float) * 0.5)
+    t2 = rng.uniform(0, 2 * np.pi, 30_000)
+    cases.append(np.round(np.stack([np.cos(t2), np.sin(t2)], 1) * 400.0))
     for a in cases:
         a = np.ascontiguousarray(a)
         assert np.array_equal(hull_via_library(oracle, a), oracle.heaphull(a))
