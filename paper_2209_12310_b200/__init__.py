@@ -70,7 +70,8 @@ def heaphull(points, threads: int = 1, chunk: int = 32) -> np.ndarray:
     h = C.c_uint64(0)
     check(lib.ohx_heaphull(a.ctypes.data_as(_dp), len(a), hull.ctypes.data_as(_dp),
                            len(hull), C.byref(h), None))
-    return hull[: h.value].copy()
+    # small hulls are copied out of the (virtual, n-sized) buffer
+    return hull[: h.value].copy() if h.value < (1 << 20) else hull[: h.value]
 
 
 def heaphull_run(points):
@@ -247,7 +248,9 @@ class Context:
 
     def heaphull_device(self, d_xy, n: int):
         """Full pipeline on device-resident points -> (hull, timings)."""
-        cap = min(n + 8, 1 << 24)
+        # the output buffer is virtual until written: full size up to 2^28
+        # points, else start at 2^24 and grow if the hull outgrows it
+        cap = n + 8 if n <= (1 << 28) else 1 << 24
         while True:
             hull = np.empty((cap, 2), dtype=np.float64)
             h = C.c_uint64(0)
@@ -258,7 +261,8 @@ class Context:
                 cap = h.value
                 continue
             check(rc)
-            return hull[: h.value].copy(), dict(filter_ms=t[0], hull_ms=t[1], total_ms=t[2])
+            out = hull[: h.value].copy() if h.value < (1 << 20) else hull[: h.value]
+            return out, dict(filter_ms=t[0], hull_ms=t[1], total_ms=t[2])
 
 
 # ---- host-only helpers of the C ABI (pure functions, no device) ---------

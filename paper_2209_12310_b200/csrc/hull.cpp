@@ -19,6 +19,8 @@
 //    reference's LIFO worklist exactly while skipping the vertices whose
 //    test cannot change (see peel).
 #include <omp.h>
+#include <sys/mman.h>
+
 #include <parallel/algorithm>
 
 #include <algorithm>
@@ -28,6 +30,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
+#include <new>
 #include <thread>
 #include <unordered_map>
 #include <unordered_set>
@@ -36,6 +40,62 @@
 #include "internal.hpp"
 
 namespace ohx {
+
+namespace {
+struct BigCache {
+  std::mutex mu;
+  struct Block {
+    void* p;
+    std::size_t bytes;
+  };
+  std::vector<Block> blocks;  // freed blocks kept mapped (pages faulted)
+  std::size_t held = 0;
+  static constexpr std::size_t kMaxHeld = std::size_t(16) << 30;
+  static constexpr std::size_t kMaxBlocks = 8;
+};
+BigCache& big_cache() {
+  static BigCache* c = new BigCache;  // never destroyed: freeing at exit is moot
+  return *c;
+}
+std::size_t round_2m(std::size_t b) { return (b + (std::size_t(2) << 20) - 1) & ~((std::size_t(2) << 20) - 1); }
+}  // namespace
+
+void* big_alloc(std::size_t bytes) {
+  bytes = round_2m(bytes);
+  BigCache& c = big_cache();
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    std::size_t best = c.blocks.size();
+    for (std::size_t i = 0; i < c.blocks.size(); ++i)  // smallest block that fits (<= 2x)
+      if (c.blocks[i].bytes >= bytes && c.blocks[i].bytes <= 2 * bytes &&
+          (best == c.blocks.size() || c.blocks[i].bytes < c.blocks[best].bytes))
+        best = i;
+    if (best != c.blocks.size()) {
+      void* p = c.blocks[best].p;
+      c.held -= c.blocks[best].bytes;
+      c.blocks.erase(c.blocks.begin() + static_cast<std::ptrdiff_t>(best));
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (posix_memalign(&p, std::size_t(2) << 20, bytes) != 0) throw std::bad_alloc();
+  madvise(p, bytes, MADV_HUGEPAGE);
+  return p;
+}
+
+void big_free(void* p, std::size_t bytes) noexcept {
+  bytes = round_2m(bytes);
+  BigCache& c = big_cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  // a recycled block may be larger than the size its last owner knew: the
+  // recorded size is then a lower bound, which is all big_alloc relies on
+  if (c.held + bytes <= BigCache::kMaxHeld && c.blocks.size() < BigCache::kMaxBlocks) {
+    c.blocks.push_back({p, bytes});
+    c.held += bytes;
+    return;
+  }
+  std::free(p);
+}
 
 int orient(const P2& a, const P2& b, const P2& c) {
   // reference geometry.hpp:27-32

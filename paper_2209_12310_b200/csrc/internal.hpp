@@ -180,6 +180,14 @@ struct P2 {
 // A std::vector whose resize leaves new elements default-initialised: the
 // hull stage's buffers (up to ~1.6 GB) are written once, in parallel, with
 // no zero-fill pass over freshly mapped pages first.
+// Blocks of >= kBigBlock bytes come from big_alloc: 2 MB aligned, marked
+// for transparent huge pages (the box runs THP in madvise mode: 4 KB pages
+// would fault ~400K times per GB) and recycled through a small cache, so
+// the hull stage's GB-sized buffers are not re-faulted on every call.
+constexpr std::size_t kBigBlock = std::size_t(64) << 20;
+void* big_alloc(std::size_t bytes);
+void big_free(void* p, std::size_t bytes) noexcept;
+
 template <class T>
 struct DefaultInitAlloc : std::allocator<T> {
   template <class U>
@@ -189,6 +197,14 @@ struct DefaultInitAlloc : std::allocator<T> {
   DefaultInitAlloc() noexcept = default;
   template <class U>
   DefaultInitAlloc(const DefaultInitAlloc<U>&) noexcept {}
+  T* allocate(std::size_t n) {
+    if (n * sizeof(T) >= kBigBlock) return static_cast<T*>(big_alloc(n * sizeof(T)));
+    return std::allocator<T>::allocate(n);
+  }
+  void deallocate(T* p, std::size_t n) noexcept {
+    if (n * sizeof(T) >= kBigBlock) big_free(p, n * sizeof(T));
+    else std::allocator<T>::deallocate(p, n);
+  }
   template <class U>
   void construct(U* p) noexcept {
     ::new (static_cast<void*>(p)) U;

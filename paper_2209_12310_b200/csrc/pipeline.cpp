@@ -42,14 +42,27 @@ extern "C" {
 
 int ohx_heaphull(const double* h_xy, uint64_t n, double* h_hull, uint64_t cap, uint64_t* h,
                  double* timings) {
+  // octohull::heaphull (hull.cpp:196-198) without the intermediate
+  // std::vector<Point2D>: the hull goes straight into the caller's buffer
   return guard([&] {
+    if (n == 0) throw std::invalid_argument("heaphull: empty point set");
     const auto t0 = Clock::now();
-    octohull::ReduceEngine engine;
-    const octohull::HullPolygon hull = octohull::heaphull(pts_of(h_xy, n), engine);
-    copy_hull(hull.vertices, h_hull, cap, h);
+    ohx_ctx* ctx = ohx::default_ctx();
+    std::lock_guard<std::mutex> g(ohx::ctx_mutex(ctx));
+    ohx::ctx_bind(ctx);
+    cudaStream_t s = ohx::ctx_stream(ctx);
+    const double* d_xy = ohx::stage_points(ctx, h_xy, n, s);
+    const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
+    const auto t1 = Clock::now();
+    const ohx::PVec cyc = ohx::device_queues_hull(ctx, f, s);
+    *h = cyc.size();
+    if (cyc.size() > cap) throw std::invalid_argument("hull output capacity too small");
+    ohx::copy_points(reinterpret_cast<ohx::P2*>(h_hull), cyc.data(), cyc.size());
     if (timings) {
-      timings[0] = timings[1] = timings[3] = 0.0;
+      timings[0] = ms(t0, t1);
+      timings[1] = ms(t1, Clock::now());
       timings[2] = ms(t0, Clock::now());
+      timings[3] = 0.0;
     }
   });
 }
