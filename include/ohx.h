@@ -45,7 +45,8 @@ enum {
   OHX_E_CUDA = -2,     /* CUDA runtime error (std::runtime_error) */
   OHX_E_NODEVICE = -3, /* no sm_100 device visible */
   OHX_E_NOMEM = -4,    /* device or pinned allocation failed */
-  OHX_E_INTERNAL = -5
+  OHX_E_INTERNAL = -5,
+  OHX_E_IO = -6        /* file error (std::runtime_error in the reference's io) */
 };
 
 /* Distributions of pointgen.hpp:10 (generate, pointgen.cpp:44-88). */
@@ -240,6 +241,21 @@ int ohx_classify(const double* h_xy, uint64_t n, uint8_t* h_labels);
 int ohx_heaphull_run(const double* h_xy, uint64_t n, double* h_hull,
                      uint64_t cap, uint64_t* h, uint8_t* h_labels,
                      double* timings);
+/* ---- point files (io.cpp:87-124, the binary PTS2 layout) -------------- */
+/* Validated header -> point count (OHX_E_IO with the reference's message:
+ * bad magic, count 0, size mismatch, cannot open). */
+int ohx_pts2_count(const char* path, uint64_t* n);
+/* The file's points straight into device memory d_xy (capacity cap
+ * points): pread into pinned chunks overlapped with the H2D copies, then a
+ * device scan rejects the first non-finite point ("non-finite coordinate in
+ * point i at byte 12+16i", OHX_E_IO). */
+int ohx_pts2_load_device(ohx_ctx* ctx, const char* path, double* d_xy, uint64_t cap,
+                         uint64_t* n, void* stream);
+/* read_points(path, Binary) + heaphull (tools/octohull_main.cpp) with the
+ * file loaded straight into device memory; timings[3] = file -> device ms. */
+int ohx_heaphull_pts2(const char* path, double* h_hull, uint64_t cap, uint64_t* h,
+                      double* timings);
+
 /* find_extremes (filter.cpp:47-52) from host points: ext[8] slot order. */
 int ohx_find_extremes(const double* h_xy, uint64_t n, uint64_t ext[8]);
 

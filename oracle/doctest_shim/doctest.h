@@ -3,8 +3,9 @@
 // The reference's unit suites (/root/reference/proj/tests/test_*.cpp) are
 // written against doctest, which is not vendored (proj/README.md:34).  This
 // header provides the subset they use -- TEST_CASE, SUBCASE, CHECK[_FALSE],
-// REQUIRE[_FALSE], CHECK_THROWS_AS, CHECK_THROWS_WITH_AS, CHECK_NOTHROW,
-// doctest::Approx(...).epsilon() -- so the UNMODIFIED suites can be
+// REQUIRE[_FALSE], CHECK_THROWS_AS, CHECK_THROWS_WITH_AS (a message or
+// doctest::Contains), CHECK_NOTHROW, doctest::Approx(...).epsilon() -- so
+// the UNMODIFIED suites can be
 // compiled against the B200 library (oracle/Makefile target `reftests`).
 // SUBCASEs run once each, in order, inside their test case.
 #pragma once
@@ -35,7 +36,17 @@ class Approx {
   double eps_ = 1e-7;
 };
 
+// substring matcher of CHECK_THROWS_WITH_AS
+struct Contains {
+  std::string s;
+  explicit Contains(const char* p) : s(p) {}
+};
+
 namespace shim {
+inline bool msg_ok(const char* what, const char* m) { return std::strstr(what, m) != nullptr; }
+inline bool msg_ok(const char* what, const Contains& c) {
+  return std::strstr(what, c.s.c_str()) != nullptr;
+}
 struct Case {
   const char* name;
   void (*fn)();
@@ -112,9 +123,9 @@ inline int run_all() {
   do {                                                                            \
     bool ds_ok = false;                                                           \
     try { (void)(expr); } catch (const __VA_ARGS__& e) {                          \
-      ds_ok = std::strstr(e.what(), msg) != nullptr;                              \
+      ds_ok = doctest::shim::msg_ok(e.what(), msg);                               \
     } catch (...) {}                                                              \
-    doctest::shim::report(ds_ok, "throws " #__VA_ARGS__ " with \"" msg "\": " #expr, \
+    doctest::shim::report(ds_ok, "throws " #__VA_ARGS__ " with " #msg ": " #expr,   \
                           __FILE__, __LINE__);                                    \
   } while (0)
 #define CHECK_NOTHROW(...)                                                        \

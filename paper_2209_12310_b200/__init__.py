@@ -17,13 +17,15 @@ benchmarks and the multi-GPU sharded path (``sharded.py``) use.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
 from ._lib import (DISTS, OHX_E_INVALID, SLOTS, CornerRec, ExtremeSet, ExtremesRec, FilterPlan,
                    OhxError, RunInfo, check, lib)
 
-__all__ = ["classify", "filter_rate", "generate", "heaphull", "monotone_chain",
+__all__ = ["classify", "filter_rate", "generate", "heaphull", "heaphull_file", "write_pts2",
+           "monotone_chain",
            "heaphull_run", "find_extremes", "Context", "OhxError", "device_count"]
 
 _dp = C.POINTER(C.c_double)
@@ -85,6 +87,27 @@ def heaphull_run(points):
                                len(hull), C.byref(h), labels.ctypes.data_as(_u8p),
                                t.ctypes.data_as(_dp)))
     return hull[: h.value].copy(), labels, dict(filter_ms=t[0], hull_ms=t[1], total_ms=t[2])
+
+
+def heaphull_file(path) -> np.ndarray:
+    """heaphull of a PTS2 point file (reference io.cpp binary layout), the
+    file streamed straight into device memory."""
+    n = C.c_uint64(0)
+    check(lib.ohx_pts2_count(os.fsencode(path), C.byref(n)))
+    hull = np.empty((n.value + 8, 2), dtype=np.float64)
+    h = C.c_uint64(0)
+    check(lib.ohx_heaphull_pts2(os.fsencode(path), hull.ctypes.data_as(_dp), len(hull),
+                                C.byref(h), None))
+    return hull[: h.value].copy() if h.value < (1 << 20) else hull[: h.value]
+
+
+def write_pts2(points, path) -> None:
+    """Write a PTS2 file (magic, u64 LE count, LE (x, y) doubles); like the
+    reference's write_points it does not validate the values."""
+    a = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+    with open(path, "wb") as f:
+        f.write(b"PTS2" + len(a).to_bytes(8, "little"))
+        f.write(a.astype("<f8", copy=False).tobytes())
 
 
 def monotone_chain(points) -> np.ndarray:
@@ -245,6 +268,18 @@ class Context:
                                   None if xy is None else xy.ctypes.data_as(_dp), count,
                                   _stream(stream)))
         return idx, xy
+
+    def load_pts2(self, path, d_xy=None, stream=None):
+        """A PTS2 file into device memory -> (n, tensor or the given buffer)."""
+        n = C.c_uint64(0)
+        check(lib.ohx_pts2_count(os.fsencode(path), C.byref(n)))
+        if d_xy is None:
+            import torch
+            d_xy = torch.empty((n.value, 2), dtype=torch.float64, device=f"cuda:{self.device}")
+        cap = d_xy.numel() // 2
+        check(lib.ohx_pts2_load_device(self.h, os.fsencode(path), _ptr(d_xy), cap, C.byref(n),
+                                       _stream(stream)))
+        return n.value, d_xy
 
     def heaphull_device(self, d_xy, n: int):
         """Full pipeline on device-resident points -> (hull, timings)."""

@@ -19,6 +19,7 @@ OHX_E_CUDA = -2
 OHX_E_NODEVICE = -3
 OHX_E_NOMEM = -4
 OHX_E_INTERNAL = -5
+OHX_E_IO = -6
 
 DISTS = {"normal": 0, "square": 1, "disk": 2, "circle": 3}
 SLOTS = ("east", "north", "west", "south", "ne", "nw", "sw", "se")
@@ -92,6 +93,9 @@ PROTOTYPES = [
     ("ohx_heaphull_device", C.c_int, [_vp, _vp, _u64, _dp, _u64, _u64p, _dp]),
     ("ohx_classify", C.c_int, [_dp, _u64, _u8p]),
     ("ohx_heaphull_run", C.c_int, [_dp, _u64, _dp, _u64, _u64p, _u8p, _dp]),
+    ("ohx_pts2_count", C.c_int, [C.c_char_p, _u64p]),
+    ("ohx_pts2_load_device", C.c_int, [_vp, C.c_char_p, _vp, _u64, _u64p, _vp]),
+    ("ohx_heaphull_pts2", C.c_int, [C.c_char_p, _dp, _u64, _u64p, _dp]),
     ("ohx_find_extremes", C.c_int, [_dp, _u64, _u64p]),
     ("ohx_monotone_chain", C.c_int, [_dp, _u64, _dp, _u64, _u64p]),
     ("ohx_generate", C.c_int, [C.c_int, _u64, _u64, C.c_double, _dp, C.c_int]),

@@ -7,6 +7,8 @@
 // edge constants) is plain binary64 in a TU built with -ffp-contract=off
 // and no -march, like the reference objects.
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <unistd.h>
 
 #include <omp.h>
 
@@ -475,6 +477,65 @@ void copy_d2h(ohx_ctx* c, void* h, const void* d, std::uint64_t bytes, cudaStrea
   for (std::uint64_t k = chunks > ohx_ctx::kStageBufs ? chunks - ohx_ctx::kStageBufs : 0;
        k < chunks; ++k)
     drain(k);
+}
+
+// A PTS2 file straight into device memory: the payload
+// streams through the pinned staging ring -- host threads pread chunk k
+// while the copy engine moves chunk k-1 -- and a device scan finds the
+// first non-finite point (reference io.cpp:87-124 semantics and messages).
+std::uint64_t load_pts2_device(ohx_ctx* c, const std::string& path, double* d_xy,
+                               std::uint64_t cap, cudaStream_t s) {
+  const std::uint64_t n = pts2_count(path);
+  if (n > cap) throw std::invalid_argument(path + ": " + std::to_string(n) +
+                                           " points exceed the device buffer (" +
+                                           std::to_string(cap) + ")");
+  const int fd = ::open(path.c_str(), O_RDONLY);
+  if (fd < 0) io_fail(path, "cannot open for reading");
+  ensure_stage(c);
+  const std::uint64_t bytes = 16 * n;
+  const std::uint64_t chunks = (bytes + kStageChunk - 1) / kStageChunk;
+  bool ok = true;
+  for (std::uint64_t k = 0; k < chunks && ok; ++k) {
+    const int b = static_cast<int>(k % ohx_ctx::kStageBufs);
+    const std::uint64_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    if (k >= ohx_ctx::kStageBufs)
+      check_cuda(cudaEventSynchronize(c->stage_ev[b]), "cudaEventSynchronize(staging)");
+    char* dst = static_cast<char*>(c->h_stage[b]);
+#pragma omp parallel num_threads(len >= (16u << 20) ? 8 : 1) reduction(&& : ok)
+    {
+      const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+      std::uint64_t p = len * t / nt, e = len * (t + 1) / nt;
+      while (p < e && ok) {
+        const ssize_t r = ::pread(fd, dst + p, static_cast<std::size_t>(e - p),
+                                  static_cast<off_t>(12 + off + p));
+        if (r <= 0) ok = false;
+        else p += static_cast<std::uint64_t>(r);
+      }
+    }
+    if (!ok) break;
+    check_cuda(cudaMemcpyAsync(reinterpret_cast<char*>(d_xy) + off, dst, len,
+                               cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(PTS2 chunk)");
+    check_cuda(cudaEventRecord(c->stage_ev[b], s), "cudaEventRecord(staging)");
+  }
+  ::close(fd);
+  if (!ok) {
+    check_cuda(cudaStreamSynchronize(s), "PTS2 load");
+    io_fail(path, "read error");
+  }
+  launch_first_nonfinite(d_xy, n, c->d_cnt, s);
+  ++c->launches;
+  check_cuda(cudaMemcpyAsync(c->h_cnt, c->d_cnt, 8, cudaMemcpyDeviceToHost, s),
+             "cudaMemcpyAsync(non-finite)");
+  check_cuda(cudaStreamSynchronize(s), "PTS2 load");
+  if (*c->h_cnt < n) io_fail(path, nonfinite_message(*c->h_cnt));
+  return n;
+}
+
+const double* stage_pts2(ohx_ctx* c, const std::string& path, std::uint64_t* n, cudaStream_t s) {
+  const std::uint64_t count = pts2_count(path);
+  dev_grow(reinterpret_cast<void**>(&c->d_pts), &c->pts_bytes, count * 16, "points");
+  *n = load_pts2_device(c, path, c->d_pts, count, s);
+  return c->d_pts;
 }
 
 const double* stage_points(ohx_ctx* c, const double* h_xy, std::uint64_t n,
@@ -1435,6 +1496,19 @@ int ohx_extremes(ohx_ctx* ctx, const double* d_xy, uint64_t n, uint64_t index_ba
     std::lock_guard<std::mutex> g(ctx->mu);
     bind(ctx);
     extremes(ctx, d_xy, n, index_base, h_rec, pick(ctx, stream));
+  });
+}
+
+int ohx_pts2_count(const char* path, uint64_t* n) {
+  return guard([&] { *n = pts2_count(path); });
+}
+
+int ohx_pts2_load_device(ohx_ctx* ctx, const char* path, double* d_xy, uint64_t cap, uint64_t* n,
+                         void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> g(ctx->mu);
+    bind(ctx);
+    *n = load_pts2_device(ctx, path, d_xy, cap, pick(ctx, stream));
   });
 }
 

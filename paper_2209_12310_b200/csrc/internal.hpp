@@ -133,6 +133,9 @@ void launch_k1_list(const double* d_xy, std::uint64_t n, const unsigned long lon
 // points of the sample runs 0, step, 2 step, ... inside Q
 void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int len, int step,
                             const KFRegion& q, unsigned long long* d_count, cudaStream_t stream);
+// *d_first = the smallest index with a non-finite coordinate, else ~0
+void launch_first_nonfinite(const double* d_xy, std::uint64_t n, unsigned long long* d_first,
+                            cudaStream_t stream);
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
                     std::uint64_t cap, const std::uint64_t counts[4], double* d_out,
                     cudaStream_t stream);
@@ -236,6 +239,12 @@ PVec hull_from_queue_points(const P2 anchors[4], const P2* const q_pts[4],
                             const std::uint64_t q_len[4]);
 PVec monotone_chain(const P2* pts, std::uint64_t n);
 int orient(const P2& a, const P2& b, const P2& c);
+
+// ---- point files (io.cpp)
+[[noreturn]] void io_fail(const std::string& path, const std::string& what);
+// validated PTS2 header -> point count (reference io.cpp:87-107 messages)
+std::uint64_t pts2_count(const std::string& path);
+std::string nonfinite_message(std::uint64_t i);
 
 // ---- host generator (pointgen.cpp)
 void generate_points(int dist, std::uint64_t n, std::uint64_t seed,

@@ -1305,6 +1305,26 @@ __global__ void __launch_bounds__(256)
   if ((threadIdx.x & 31) == 0) atomicAdd(count, static_cast<unsigned long long>(c));
 }
 
+// The smallest index of a point with a non-finite coordinate (the PTS2
+// loader's validation, reference io.cpp:117-120), or leaves *first as is.
+__global__ void first_nonfinite(const double2* __restrict__ pts, std::uint64_t n,
+                                unsigned long long* first) {
+  unsigned long long mine = ~0ull;
+  for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += std::uint64_t(gridDim.x) * blockDim.x) {
+    const double2 p = ld_stream(pts + k);
+    if (!isfinite(p.x) || !isfinite(p.y)) {
+      mine = k;
+      break;  // a thread's later indices are larger
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(kFull, mine, off);
+    mine = o < mine ? o : mine;
+  }
+  if ((threadIdx.x & 31) == 0 && mine != ~0ull) atomicMin(first, mine);
+}
+
 template <typename IdxT>
 __global__ void gather_xy(const double2* __restrict__ pts,
                           const IdxT* __restrict__ idx, std::uint64_t count,
@@ -1543,6 +1563,14 @@ void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int l
   count_in_region<<<(segs + step - 1) / step, 256, 0, stream>>>(
       reinterpret_cast<const double2*>(d_xy), SampleMap{n, segs, len, 1}, step, q, d_count);
   check_cuda(cudaGetLastError(), "count_in_region launch");
+}
+
+void launch_first_nonfinite(const double* d_xy, std::uint64_t n, unsigned long long* d_first,
+                            cudaStream_t stream) {
+  check_cuda(cudaMemsetAsync(d_first, 0xFF, sizeof(unsigned long long), stream), "cudaMemsetAsync");
+  const unsigned grid = static_cast<unsigned>(n / (256 * 16) + 1 < 148 * 8 ? n / (256 * 16) + 1 : 148 * 8);
+  first_nonfinite<<<grid, 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n, d_first);
+  check_cuda(cudaGetLastError(), "first_nonfinite launch");
 }
 
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,

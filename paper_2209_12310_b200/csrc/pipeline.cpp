@@ -91,6 +91,34 @@ int ohx_heaphull_device(ohx_ctx* ctx, const double* d_xy, uint64_t n, double* h_
   });
 }
 
+int ohx_heaphull_pts2(const char* path, double* h_hull, uint64_t cap, uint64_t* h,
+                      double* timings) {
+  // the reference CLI's read_points(Binary) + heaphull (tools/octohull_main
+  // .cpp), with the file streamed straight into device memory
+  return guard([&] {
+    const auto t0 = Clock::now();
+    ohx_ctx* ctx = ohx::default_ctx();
+    std::lock_guard<std::mutex> g(ohx::ctx_mutex(ctx));
+    ohx::ctx_bind(ctx);
+    cudaStream_t s = ohx::ctx_stream(ctx);
+    std::uint64_t n = 0;
+    const double* d_xy = ohx::stage_pts2(ctx, path, &n, s);
+    const auto tl = Clock::now();
+    const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
+    const auto t1 = Clock::now();
+    const ohx::PVec cyc = ohx::device_queues_hull(ctx, f, s);
+    *h = cyc.size();
+    if (cyc.size() > cap) throw std::invalid_argument("hull output capacity too small");
+    ohx::copy_points(reinterpret_cast<ohx::P2*>(h_hull), cyc.data(), cyc.size());
+    if (timings) {
+      timings[0] = ms(tl, t1);
+      timings[1] = ms(t1, Clock::now());
+      timings[2] = ms(t0, Clock::now());
+      timings[3] = ms(t0, tl);  // file -> device
+    }
+  });
+}
+
 int ohx_classify(const double* h_xy, uint64_t n, uint8_t* h_labels) {
   return guard([&] {
     octohull::ReduceEngine engine;

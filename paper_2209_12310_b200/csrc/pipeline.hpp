@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "internal.hpp"
@@ -36,6 +37,8 @@ void ctx_bind(ohx_ctx* c);
 const double* stage_points(ohx_ctx* c, const double* h_xy, std::uint64_t n,
                            cudaStream_t s);
 std::uint8_t* stage_labels(ohx_ctx* c, std::uint64_t n);
+// a PTS2 file into the context's device point buffer (*n points)
+const double* stage_pts2(ohx_ctx* c, const std::string& path, std::uint64_t* n, cudaStream_t s);
 // labels back into a (possibly pageable) host buffer; synchronous
 void fetch_labels(ohx_ctx* c, std::uint8_t* h_labels, const std::uint8_t* d_labels,
                   std::uint64_t n, cudaStream_t s);

@@ -434,3 +434,24 @@ def test_u64_indices_on_a_tiled_4p5e9_point_input(ctx):
         assert np.array_equal(ctx.queue(q + 1, counts[q])[0], want[q]), q
     del d
     torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------ PTS2 files
+def test_pts2_straight_to_device(ctx, oracle, tmp_path):
+    # file -> pinned chunks -> device, bit-exact; the first non-finite point
+    # is reported with its index and byte offset (reference io.cpp:117-120)
+    pts = P.generate("normal", 9_000_017, 19)  # > one 64 MB staging chunk
+    f = tmp_path / "p.bin"
+    P.write_pts2(pts, f)
+    n, d = ctx.load_pts2(f)
+    assert n == len(pts)
+    assert np.array_equal(d.cpu().numpy(), pts)
+    hull = P.heaphull_file(f)
+    assert np.array_equal(hull, oracle.heaphull(pts))
+    for bad in (8_999_999, 4_194_305, 0):
+        q = pts.copy()
+        q[bad, bad % 2] = np.inf if bad else np.nan
+        q[bad + 7, 0] = np.nan  # a later one must not be the one reported
+        P.write_pts2(q, f)
+        with pytest.raises(P.OhxError, match=f"point {bad} at byte {12 + 16 * bad}"):
+            ctx.load_pts2(f)

@@ -251,3 +251,25 @@ def test_bad_input_raises_value_error():
         P.heaphull(np.zeros((0, 2)))
     with pytest.raises(ValueError):
         P.classify(np.zeros((4, 2)), threads=0)
+
+
+# ------------------------------------------------------------ PTS2 files
+def test_pts2_header_validation(tmp_path, oracle):
+    import ctypes as C
+    pts = oracle.generate("disk", 1000, 3)
+    f = tmp_path / "p.bin"
+    P.write_pts2(pts, f)
+    assert f.stat().st_size == 12 + 16 * 1000
+    n = C.c_uint64(0)
+    P.check(P.lib.ohx_pts2_count(os.fsencode(f), C.byref(n)))
+    assert n.value == 1000
+    cases = {b"XXXX" + (3).to_bytes(8, "little"): "magic",
+             b"PTS2" + (0).to_bytes(8, "little"): "empty",
+             b"PTS2" + (2).to_bytes(8, "little") + b"\0" * 27: "size mismatch",
+             b"PTS2": "truncated header"}
+    for raw, what in cases.items():
+        f.write_bytes(raw)
+        assert P.lib.ohx_pts2_count(os.fsencode(f), C.byref(n)) == _lib.OHX_E_IO
+        assert what in P.lib.ohx_last_error().decode()
+    assert P.lib.ohx_pts2_count(os.fsencode(tmp_path / "nope.bin"), C.byref(n)) == _lib.OHX_E_IO
+    assert "nope.bin" in P.lib.ohx_last_error().decode()

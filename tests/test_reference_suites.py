@@ -1,8 +1,8 @@
 """The reference's own unit suites (tests/test_{geometry,parallel,pointgen,
-filter,hull}.cpp of /root/reference/proj), UNMODIFIED, compiled by
+io,filter,hull}.cpp of /root/reference/proj), UNMODIFIED, compiled by
 oracle/Makefile (`reftests`) against this library's drop-in headers and
-linked to libocto_b200.so.  geometry / parallel / pointgen exercise host
-code only; filter and hull drive the sm_100a kernels and need the GPU."""
+linked to libocto_b200.so.  geometry / parallel / pointgen / io exercise
+host code only; filter and hull drive the sm_100a kernels and need the GPU."""
 
 import os
 import re
@@ -26,7 +26,7 @@ def run_suite(name):
     assert m and m.group(1) == m.group(2), summary
 
 
-@pytest.mark.parametrize("suite", ["geometry", "parallel", "pointgen"])
+@pytest.mark.parametrize("suite", ["geometry", "parallel", "pointgen", "io"])
 def test_reference_host_suites(suite):
     run_suite(suite)
 
