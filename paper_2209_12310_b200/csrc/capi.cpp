@@ -1008,6 +1008,15 @@ constexpr int kSampleLen = 8192;     // points per sample run
 static_assert(kSampleLen % 2048 == 0, "k1_small reads sample runs 2048 points at a time");
 constexpr int kCoverageStep = 4;      // coverage counted on every 4th run
 constexpr int kSampleMaxSegs = 1024;  // runs (8M points, 128 MB) for n >= 2^27
+// OHX_SAMPLE_SEGS overrides the cap (experiment switch)
+int sample_max_segs() {
+  static const int v = [] {
+    const char* e = std::getenv("OHX_SAMPLE_SEGS");
+    const int k = e ? std::atoi(e) : 0;
+    return k >= 64 ? k : kSampleMaxSegs;
+  }();
+  return v;
+}
 constexpr int kSubSamples = 8;  // disjoint sub-samples of kSampleSegs / 8 runs each
 constexpr double kFuseMinCoverage = 0.8;
 
@@ -1172,7 +1181,7 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   f.fuse_state = 2;
   // about n/16 sampled points, 64..1024 runs, a multiple of kSubSamples
   const int segs = static_cast<int>(std::clamp<std::uint64_t>(
-                       n / (16ull * kSampleLen), 64, kSampleMaxSegs)) / kSubSamples * kSubSamples;
+                       n / (16ull * kSampleLen), 64, sample_max_segs())) / kSubSamples * kSubSamples;
   dev_grow(reinterpret_cast<void**>(&c->d_sample), &c->sample_bytes,
            kSubSamples * sizeof(ohx_extremes_rec), "sample records");
   auto* d_recs = reinterpret_cast<ohx_extremes_rec*>(c->d_sample);
