@@ -455,3 +455,27 @@ def test_pts2_straight_to_device(ctx, oracle, tmp_path):
         P.write_pts2(q, f)
         with pytest.raises(P.OhxError, match=f"point {bad} at byte {12 + 16 * bad}"):
             ctx.load_pts2(f)
+
+
+@pytest.mark.parametrize("shape", ["same", "line", "two", "grid"])
+def test_degenerate_large_inputs(ctx, oracle, shape):
+    # large inputs (past the fused-pass threshold) whose octagon degenerates
+    # or whose extremes tie massively: every pipeline stage must agree with
+    # the oracle (fused or not)
+    n = 9_000_000
+    rng = np.random.default_rng(7)
+    if shape == "same":
+        pts = np.full((n, 2), 1.5)
+    elif shape == "line":
+        t = rng.uniform(-1, 1, n)
+        pts = np.stack([t, 3 * t + 0.25], 1)
+    elif shape == "two":
+        pts = np.where(rng.random((n, 1)) < 0.5, [[0.0, 0.0]], [[1.0, -2.0]])
+    else:
+        pts = rng.integers(-40, 41, size=(n, 2)).astype(float)
+    pts = np.ascontiguousarray(pts)
+    hull, _ = ctx.heaphull_device(dev(pts), n)
+    want_hull, want_labels = oracle.heaphull(pts, with_labels=True)
+    assert np.array_equal(hull, want_hull), shape
+    info = ctx.last_run()
+    assert info["counts"] == [int((want_labels == q).sum()) for q in (1, 2, 3, 4)], (shape, info)
