@@ -269,6 +269,12 @@ int ohx_monotone_chain(const double* h_xy, uint64_t n, double* h_hull,
 int ohx_generate(int dist, uint64_t n, uint64_t seed, double distort_pct,
                  double* h_xy, int threads);
 
+/* The strict-left-turn chain of an arc already in sweep order (the loop of
+ * quadrant_hull, hull.cpp:140-149, without its sort): h_out receives the
+ * chain without the arc's last point (*m entries; capacity n).  Long arcs
+ * run in parallel chunks with the reference loop's exact decisions. */
+int ohx_chain(const double* h_xy, uint64_t n, double* h_out, uint64_t* m);
+
 /* Host hull stage of heaphull_run (hull.cpp:164-183) on given queues:
  * pts = all points (host), queues as global indices. */
 int ohx_hull_from_queues(const double* h_xy, const uint64_t ext_axis[4],

@@ -13,6 +13,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -79,6 +80,7 @@ struct ohx_ctx {
   std::uint64_t hsort_bytes = 0;
   void* h_sorted = nullptr;  // pinned: the sorted arcs on the host
   std::uint64_t h_sorted_bytes = 0;
+  cudaEvent_t arc_ev[4] = {};  // their per-arc copies
   unsigned long long* d_cnt = nullptr;
   unsigned long long* h_cnt = nullptr;  // pinned
 
@@ -903,6 +905,24 @@ void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s) {
   check_cuda(cudaStreamSynchronize(s), "queues fetch");
 }
 
+namespace {
+// OHX_TRACE=1: host wall time of each pipeline phase on stderr
+struct Trace {
+  bool on = [] {
+    const char* e = std::getenv("OHX_TRACE");
+    return e && *e && std::string(e) != "0";
+  }();
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ohx] %-14s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+}  // namespace
+
 // Survivor counts from which the hull stage's sweep sort runs on the device
 constexpr std::uint64_t kDeviceSortMin = 1u << 17;
 
@@ -934,21 +954,38 @@ PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s) {
              "hull sort work");
     auto* d_sorted = reinterpret_cast<double*>(static_cast<unsigned char*>(c->d_hsort) +
                                                sort_arcs_work_bytes(f.counts));
+    Trace tr;
     sort_arcs(c->d_gather, f.counts, reinterpret_cast<const double*>(anchors), c->d_hsort,
               d_sorted, s);
     c->launches += 2 + 4 * 4;  // build/gather + four radix sorts
+    if (tr.on) {
+      check_cuda(cudaStreamSynchronize(s), "hull sort");
+      tr.mark("hull dev sort");
+    }
     host_grow(&c->h_sorted, &c->h_sorted_bytes, arcs_n * 16, "cudaMallocHost(sorted arcs)");
-    check_cuda(cudaMemcpyAsync(c->h_sorted, d_sorted, arcs_n * 16, cudaMemcpyDeviceToHost, s),
-               "cudaMemcpyAsync(sorted arcs)");
-    check_cuda(cudaStreamSynchronize(s), "hull sort");
+    // one copy per arc: arc q's chain starts as soon as its copy lands
+    if (!c->arc_ev[0])
+      for (auto& e : c->arc_ev)
+        check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate(arc)");
     const P2* arcs[4];
     std::uint64_t len[4], off = 0;
     for (int q = 0; q < 4; ++q) {
       arcs[q] = static_cast<const P2*>(c->h_sorted) + off;
       len[q] = f.counts[q] + 2;
+      check_cuda(cudaMemcpyAsync(static_cast<P2*>(c->h_sorted) + off,
+                                 reinterpret_cast<const P2*>(d_sorted) + off, len[q] * 16,
+                                 cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(sorted arc)");
+      check_cuda(cudaEventRecord(c->arc_ev[q], s), "cudaEventRecord(arc)");
       off += len[q];
     }
-    return hull_from_sorted_arcs(arcs, len);
+    std::atomic<int> failed{cudaSuccess};  // set by the arc threads (no throwing there)
+    PVec cyc = hull_from_sorted_arcs(arcs, len, [&](int q) {
+      const cudaError_t e = cudaEventSynchronize(c->arc_ev[q]);
+      if (e != cudaSuccess) failed = e;
+    });
+    check_cuda(static_cast<cudaError_t>(failed.load()), "cudaEventSynchronize(sorted arc)");
+    tr.mark("hull D2H + host");
+    return cyc;
   }
   // one gather launch and one D2H of the survivors' coordinates, then the
   // host hull stage
@@ -1038,21 +1075,6 @@ std::vector<P2> clip_left(const std::vector<P2>& poly, P2 a, P2 b) {
   return out;
 }
 
-// OHX_TRACE=1: host wall time of each pipeline phase on stderr
-struct Trace {
-  bool on = [] {
-    const char* e = std::getenv("OHX_TRACE");
-    return e && *e && std::string(e) != "0";
-  }();
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void mark(const char* what) {
-    if (!on) return;
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[ohx] %-14s %8.3f ms\n", what,
-                 std::chrono::duration<double, std::milli>(now - t).count());
-    t = now;
-  }
-};
 
 // key of slot a (ohx.h slot order: x, y, -x, -y, x+y, y-x, -(x+y), x-y)
 double slot_key(int a, double x, double y) {
@@ -1425,6 +1447,8 @@ void destroy_ctx(ohx_ctx* c) {
     if (c->h_stage[b]) cudaFreeHost(c->h_stage[b]);
     if (c->stage_ev[b]) cudaEventDestroy(c->stage_ev[b]);
   }
+  for (auto& e : c->arc_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& pair : c->ev)
     for (auto& e : pair)
       if (e) cudaEventDestroy(e);

@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <functional>
 #include <mutex>
 #include <new>
 #include <thread>
@@ -343,9 +344,9 @@ struct DenseLinks {
   void set_queued(std::size_t i, bool v) { flags[i] = v ? (flags[i] | 4) : (flags[i] & ~4); }
 };
 
-void peel(PVec& cyc) {
+// the non-strict turns of the cyclic sequence, ascending
+std::vector<std::size_t> non_strict_turns(const PVec& cyc) {
   const std::size_t m = cyc.size();
-  // the non-strict turns, ascending
   const int T = omp_get_max_threads();
   std::vector<std::vector<std::size_t>> part(m >= kParMin ? T : 1);
 #pragma omp parallel num_threads(static_cast<int>(part.size())) if (m >= kParMin)
@@ -359,16 +360,99 @@ void peel(PVec& cyc) {
   }
   std::vector<std::size_t> todo;
   for (auto& v : part) todo.insert(todo.end(), v.begin(), v.end());
-  if (todo.empty()) return;
+  return todo;
+}
+
+// returns whether anything was removed
+bool peel(PVec& cyc, std::vector<std::size_t> todo) {
+  const std::size_t m = cyc.size();
+  if (todo.empty()) return false;
   if (todo.size() * 64 < m) {
     SparseLinks L{m, {}, {}, {}, {}, {}};
     for (std::size_t i : todo) L.que.insert(i);
-    peel_with(cyc, std::move(todo), L);
-  } else {
-    DenseLinks L(m);
-    for (std::size_t i : todo) L.flags[i] |= 4;
-    peel_with(cyc, std::move(todo), L);
+    return peel_with(cyc, std::move(todo), L);
   }
+  DenseLinks L(m);
+  for (std::size_t i : todo) L.flags[i] |= 4;
+  return peel_with(cyc, std::move(todo), L);
+}
+
+// the first vertex with max x, ties to the smaller y (reference
+// hull.cpp:35-49)
+std::size_t start_vertex(const PVec& d) {
+  const std::size_t sz = d.size();
+  std::size_t best = 0;
+  if (sz < kParMin) {
+    for (std::size_t i = 1; i < sz; ++i)
+      if (starts_before(d[i], d[best])) best = i;
+    return best;
+  }
+  const int T = omp_get_max_threads();
+  std::vector<std::size_t> pb(T, sz);
+#pragma omp parallel num_threads(T)
+  {
+    const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+    const std::size_t b = sz * t / nt, e = sz * (t + 1) / nt;
+    std::size_t bi = b;
+    for (std::size_t i = b + 1; i < e; ++i)
+      if (starts_before(d[i], d[bi])) bi = i;
+    if (b < e) pb[t] = bi;
+  }
+  best = pb[0];
+  for (int t = 1; t < T; ++t)
+    if (pb[t] < sz && starts_before(d[pb[t]], d[best])) best = pb[t];
+  return best;
+}
+
+// One parallel pass over a cycle that the fast path of finalize_cycle
+// needs: consecutive duplicates?  all collinear with (c0, c1)?  its
+// non-strict turns, and its start vertex.
+struct CycleScan {
+  bool dups = false, flat = true;
+  std::vector<std::size_t> bad;
+  std::size_t best = 0;
+};
+
+CycleScan scan_cycle(const PVec& c) {
+  CycleScan r;
+  const std::size_t m = c.size();
+  const int T = m >= kParMin ? omp_get_max_threads() : 1;
+  std::vector<std::vector<std::size_t>> part(T);
+  std::vector<std::size_t> pb(T, m);
+  std::vector<unsigned char> dups(T, 0), flat(T, 1);
+#pragma omp parallel num_threads(T)
+  {
+    const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+    const std::size_t b = m * t / nt, e = m * (t + 1) / nt;
+    bool du = false, fl = true;
+    std::size_t bi = b;
+    for (std::size_t i = b; i < e; ++i) {
+      const std::size_t a = i == 0 ? m - 1 : i - 1, n = i + 1 == m ? 0 : i + 1;
+      if (i > 0) du = du || same(c[a], c[i]);
+      if (i >= 2) fl = fl && orient(c[0], c[1], c[i]) == 0;
+      if (orient(c[a], c[i], c[n]) <= 0) part[t].push_back(i);
+      if (i > b && starts_before(c[i], c[bi])) bi = i;
+    }
+    dups[t] = du;
+    flat[t] = fl;
+    if (b < e) pb[t] = bi;
+  }
+  for (int t = 0; t < T; ++t) {
+    r.dups = r.dups || dups[t];
+    r.flat = r.flat && flat[t];
+    r.bad.insert(r.bad.end(), part[t].begin(), part[t].end());
+    if (pb[t] < m && (t == 0 || starts_before(c[pb[t]], c[r.best]))) r.best = pb[t];
+  }
+  return r;
+}
+
+void rotate_to(PVec& d, std::size_t best) {
+  if (best == 0) return;
+  const std::size_t sz = d.size();
+  PVec r(sz);
+  copy_points(r.data(), d.data() + best, sz - best);
+  copy_points(r.data() + (sz - best), d.data(), best);
+  d.swap(r);
 }
 
 }  // namespace
@@ -386,23 +470,234 @@ void copy_points(P2* dst, const P2* src, std::size_t n) {
   }
 }
 
-// The strict-left-turn chain of an arc already in sweep order (reference
+namespace {
+
+inline bool strict_left(const P2& a, const P2& b, const P2& p) {
+  // orientation(a, b, p) > 0 with the reference's operations (geometry.hpp:27-32)
+  return (b.x - a.x) * (p.y - a.y) - (b.y - a.y) * (p.x - a.x) > 0.0;
+}
+
+// OHX_CHAIN_PAR_MIN / OHX_CHAIN_CHUNKS: size from which an arc's chain runs
+// in parallel, and its number of chunks (test hooks; defaults 2^22, 16).
+// Smaller arcs (and arcs whose chunks rarely coincide, like a disk's) are
+// cheaper with the plain loop.
+std::size_t env_size(const char* name, std::size_t dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? static_cast<std::size_t>(std::atoll(e)) : dflt;
+}
+std::size_t chain_par_min() {
+  static const std::size_t v = env_size("OHX_CHAIN_PAR_MIN", std::size_t(1) << 22);
+  return v;
+}
+
+// Chains computed in parallel with IDENTICAL decisions.  Every chunk of an
+// arc first runs the loop on its own (empty stack); then, chunk by chunk,
+// the true loop resumes from the true stack G and replays the chunk's first
+// points until it provably coincides with the chunk's own run: the part of
+// G pushed in this chunk (C) equals the top |C| >= 2 entries of the local
+// stack after the same point, and the local run never again drops below
+// those entries' base + 2 (so every later test and pop touches only entries
+// both runs share).  From there the chunk's local final stack above that
+// base is the true result.  A chunk that does not coincide within
+// kSyncWindow points is finished by the plain loop on a flattened copy of G.
+constexpr std::size_t kSyncWindow = 64;
+
+struct ChunkRun {
+  std::size_t b, e, height;          // points [b, e) of the arc, local stack height
+  std::uint32_t low[kSyncWindow];    // stack height after point k's pops (k < window)
+  std::uint32_t low_rest;            // min of that height over the later points
+};
+
+struct ArcChain {
+  const P2* pts = nullptr;
+  std::size_t n = 0;
+  PVec loc;                          // the chunks' local stacks, each in place
+  std::vector<ChunkRun> runs;
+  struct Slice {
+    const P2* base;
+    std::size_t from, to;
+  };
+  std::vector<Slice> G;              // the true stack, as slices
+  std::size_t gsize = 0;
+  PVec extra;                        // entries pushed by replayed points
+
+  void local_run(std::size_t j) {  // phase A, one chunk (any thread)
+    ChunkRun& r = runs[j];
+    const P2* in = pts + r.b;
+    P2* ch = loc.data() + r.b;
+    const std::size_t len = r.e - r.b;
+    std::size_t top = 0;
+    std::uint32_t rest = ~0u;
+    for (std::size_t k = 0; k < len; ++k) {
+      const P2 p = in[k];
+      while (top >= 2 && !strict_left(ch[top - 2], ch[top - 1], p)) --top;
+      if (k < kSyncWindow) r.low[k] = static_cast<std::uint32_t>(top);
+      else rest = std::min(rest, static_cast<std::uint32_t>(top));
+      ch[top++] = p;
+    }
+    r.height = top;
+    r.low_rest = rest;
+  }
+
+  const P2& at(std::size_t d) const {  // d-th entry from the top of G
+    for (std::size_t s = G.size(); s-- > 0;) {
+      const std::size_t len = G[s].to - G[s].from;
+      if (d < len) return G[s].base[G[s].to - 1 - d];
+      d -= len;
+    }
+    return G[0].base[0];  // unreachable: callers keep d < gsize
+  }
+  void pop() {
+    if (--G.back().to == G.back().from) G.pop_back();
+    --gsize;
+  }
+  void push_extra(const P2& p) {
+    extra.push_back(p);  // reserved: never moves
+    const std::size_t i = extra.size() - 1;
+    if (!G.empty() && G.back().base == extra.data() && G.back().to == i) ++G.back().to;
+    else G.push_back({extra.data(), i, i + 1});
+    ++gsize;
+  }
+
+  void resolve() {  // phase B (sequential per arc)
+    extra.reserve(n + 1);
+    G.push_back({loc.data() + runs[0].b, 0, runs[0].height});  // chunk 0 is the true run
+    gsize = runs[0].height;
+    for (std::size_t j = 1; j < runs.size(); ++j) {
+      const ChunkRun& r = runs[j];
+      const std::size_t len = r.e - r.b;
+      std::vector<std::size_t> C;  // chunk-local indices of G's chunk part
+      std::size_t t = 0;
+      bool synced = false;
+      for (; t < std::min(len, kSyncWindow) && !synced; ++t) {
+        const P2 p = pts[r.b + t];
+        while (gsize >= 2 && !strict_left(at(1), at(0), p)) {
+          pop();  // the chunk's own entries sit on top of the earlier ones
+          if (!C.empty()) C.pop_back();
+        }
+        push_extra(p);
+        C.push_back(t);
+        const std::size_t h = r.low[t] + 1, c = C.size();
+        std::uint32_t later = r.low_rest;  // min height after pops, later points
+        for (std::size_t k = t + 1; k < std::min(len, kSyncWindow); ++k) later = std::min(later, r.low[k]);
+        if (c < 2 || c > h || std::size_t(later) < h - c + 2) continue;
+        bool same_top = true;  // local entry at level l = last point k <= t pushed at l
+        for (std::size_t i = 0; i < c && same_top; ++i) {
+          const std::size_t level = h - c + i;
+          std::size_t k = t;
+          while (r.low[k] != level) --k;
+          same_top = k == C[i];
+        }
+        if (!same_top) continue;
+        for (std::size_t i = 0; i < c; ++i) pop();
+        G.push_back({loc.data() + r.b, h - c, r.height});
+        gsize += r.height - (h - c);
+        synced = true;
+      }
+      if (synced || t == len) continue;
+      // no coincidence within the window: flatten G and run the plain loop
+      PVec flat(gsize + (len - t));
+      std::size_t top = 0;
+      for (const Slice& sl : G) {
+        std::memcpy(static_cast<void*>(flat.data() + top), sl.base + sl.from,
+                    (sl.to - sl.from) * sizeof(P2));
+        top += sl.to - sl.from;
+      }
+      for (std::size_t k = t; k < len; ++k) {
+        const P2 p = pts[r.b + k];
+        while (top >= 2 && !strict_left(flat[top - 2], flat[top - 1], p)) --top;
+        flat[top++] = p;
+      }
+      flat.resize(top);
+      extra.clear();  // nothing in G refers to it any more
+      G.clear();
+      gsize = top;
+      flats.push_back(std::move(flat));
+      G.push_back({flats.back().data(), 0, top});
+    }
+  }
+  std::vector<PVec> flats;
+};
+
+}  // namespace
+
+// The chains of the four arcs (already in sweep order), concatenated in arc
+// order, each without its last point (the next arc's entry): the cycle the
+// clean-up takes (reference hull.cpp:164-183).  Arcs of >= par_min points
+// run in parallel chunks (all arcs' chunks in one parallel loop); wait_arc(q)
+// is called before arc q is read.
+PVec chain_arcs(const P2* const arcs[4], const std::uint64_t len[4],
+                const std::function<void(int)>& wait_arc) {
+  const std::size_t par_min = chain_par_min();
+  static const std::size_t chunks = std::max<std::size_t>(2, env_size("OHX_CHAIN_CHUNKS", 16));
+  ArcChain A[4];
+  struct Task {
+    int q;
+    std::size_t j;
+  };
+  std::vector<Task> tasks;
+  for (int q = 0; q < 4; ++q) {
+    A[q].pts = arcs[q];
+    A[q].n = len[q];
+    const std::size_t n = len[q];
+    const std::size_t K = n >= par_min && n >= 2 * chunks ? chunks : 1;
+    const std::size_t step = n ? (n + K - 1) / K : 0;
+    for (std::size_t b = 0; b < n; b += step) A[q].runs.push_back({b, std::min(n, b + step), 0, {}, 0});
+    A[q].loc.resize(n);
+    for (std::size_t j = 0; j < A[q].runs.size(); ++j) tasks.push_back({q, j});
+  }
+  std::sort(tasks.begin(), tasks.end(), [&](const Task& x, const Task& y) {  // long runs first
+    return A[x.q].runs[x.j].e - A[x.q].runs[x.j].b > A[y.q].runs[y.j].e - A[y.q].runs[y.j].b;
+  });
+  const std::uint64_t total = len[0] + len[1] + len[2] + len[3];
+#pragma omp parallel for schedule(dynamic, 1) if (total >= (1u << 12))
+  for (std::int64_t i = 0; i < static_cast<std::int64_t>(tasks.size()); ++i) {
+    if (wait_arc) wait_arc(tasks[i].q);
+    A[tasks[i].q].local_run(tasks[i].j);
+  }
+#pragma omp parallel for schedule(dynamic, 1) if (total >= (1u << 12))
+  for (int q = 0; q < 4; ++q)
+    if (A[q].n) A[q].resolve();
+  // assembly: every arc's slices, minus its last entry, straight into the cycle
+  struct Piece {
+    const P2* src;
+    std::size_t len, dst;
+  };
+  std::vector<Piece> pieces;
+  std::size_t h = 0;
+  for (int q = 0; q < 4; ++q) {
+    if (A[q].gsize == 0) continue;
+    std::size_t keep = A[q].gsize - 1;
+    for (const auto& sl : A[q].G) {
+      const std::size_t l = std::min(keep, sl.to - sl.from);
+      if (l) pieces.push_back({sl.base + sl.from, l, h});
+      h += l;
+      keep -= l;
+    }
+  }
+  PVec cycle(h);
+#pragma omp parallel for schedule(dynamic, 1) if (h >= kParMin)
+  for (std::int64_t i = 0; i < static_cast<std::int64_t>(pieces.size()); ++i)
+    copy_points(cycle.data() + pieces[i].dst, pieces[i].src, pieces[i].len);
+  return cycle;
+}
+
+// The strict-left-turn chain of one arc already in sweep order (reference
 // hull.cpp:140-149); the sweep's last point is dropped (it is the next
-// arc's entry).  The top edge's differences are kept in registers: the
-// determinant is evaluated with exactly the reference's operations.
+// arc's entry).  Long arcs run in parallel chunks with the same decisions.
 PVec chain_sorted(const P2* pts, std::size_t n) {
   if (n == 0) return {};
-  PVec chain(n);
+  if (n >= chain_par_min()) {
+    const P2* arcs[4] = {pts, pts, pts, pts};
+    const std::uint64_t len[4] = {n, 0, 0, 0};
+    return chain_arcs(arcs, len, {});
+  }
+  PVec chain(n);  // the plain loop
   P2* ch = chain.data();
-  std::size_t top = 0;  // chain[0, top)
+  std::size_t top = 0;
   for (std::size_t k = 0; k < n; ++k) {
     const P2 p = pts[k];
-    while (top >= 2) {
-      const P2 a = ch[top - 2], b = ch[top - 1];
-      const double det = (b.x - a.x) * (p.y - a.y) - (b.y - a.y) * (p.x - a.x);
-      if (det > 0.0) break;
-      --top;
-    }
+    while (top >= 2 && !strict_left(ch[top - 2], ch[top - 1], p)) --top;
     ch[top++] = p;
   }
   chain.resize(top - 1);
@@ -430,24 +725,39 @@ PVec quadrant_chain(std::vector<P2> pts, int quadrant) {
 PVec finalize_cycle(PVec cycle) {
   // reference hull.cpp:94-120.  Consecutive duplicates collapse first (a
   // point is dropped iff it equals its predecessor: the last kept point
-  // always equals the predecessor), then equal front/back pairs.
+  // always equals the predecessor), then equal front/back pairs; a fully
+  // collinear cycle reduces to its two extreme points, any other is peeled
+  // to strict left turns; the result starts at the east-most vertex.
   double tt = now_ms();
   auto tmark = [&](const char* w) {
     if (trace_on()) std::fprintf(stderr, "[ohx]   finalize %-8s %.3f ms\n", w, now_ms() - tt);
     tt = now_ms();
   };
-  bool dups = false;
   const std::size_t n0 = cycle.size();
-#pragma omp parallel for schedule(static) reduction(|| : dups) if (n0 >= kParMin)
-  for (std::int64_t k = 1; k < static_cast<std::int64_t>(n0); ++k)
-    dups = dups || same(cycle[k - 1], cycle[k]);
+  if (n0 > 2 && !same(cycle.front(), cycle.back())) {
+    // fast path: one fused parallel scan; valid as is when the cycle has no
+    // duplicates (the usual case: chains of strict turns)
+    CycleScan sc = scan_cycle(cycle);
+    tmark("scan");
+    if (!sc.dups) {
+      if (sc.flat) {
+        const auto mm = std::minmax_element(cycle.begin(), cycle.end(), lex);
+        PVec d = {*mm.first, *mm.second};
+        rotate_to(d, start_vertex(d));
+        return d;
+      }
+      const bool removed = peel(cycle, std::move(sc.bad));
+      tmark("peel");
+      rotate_to(cycle, removed ? start_vertex(cycle) : sc.best);
+      tmark("rotate");
+      return cycle;
+    }
+  }
   PVec d;
-  if (dups) {
+  {
     const P2* c = cycle.data();
     d = compact(c, n0, [&](std::size_t k) { return k == 0 || !same(c[k - 1], c[k]); });
     PVec().swap(cycle);
-  } else {
-    d.swap(cycle);
   }
   tmark("dedup");
   while (d.size() > 1 && same(d.front(), d.back())) d.pop_back();
@@ -457,69 +767,24 @@ PVec finalize_cycle(PVec cycle) {
 #pragma omp parallel for schedule(static) reduction(&& : flat) if (m >= kParMin)
     for (std::int64_t k = 2; k < static_cast<std::int64_t>(m); ++k)
       flat = flat && orient(d[0], d[1], d[k]) == 0;
-    tmark("flat");
     if (flat) {
       const auto mm = std::minmax_element(d.begin(), d.end(), lex);
       d = {*mm.first, *mm.second};
     } else {
-      peel(d);
+      peel(d, non_strict_turns(d));
     }
     tmark("peel");
   }
-  if (d.size() >= 2) {
-    // start at the first vertex with max x, ties to the smaller y
-    // (reference hull.cpp:35-49)
-    const std::size_t sz = d.size();
-    std::size_t best = 0;
-    if (sz < kParMin) {
-      for (std::size_t i = 1; i < sz; ++i)
-        if (starts_before(d[i], d[best])) best = i;
-    } else {
-      const int T = omp_get_max_threads();
-      std::vector<std::size_t> pb(T, 0);
-#pragma omp parallel num_threads(T)
-      {
-        const int t = omp_get_thread_num(), nt = omp_get_num_threads();
-        const std::size_t b = sz * t / nt, e = sz * (t + 1) / nt;
-        std::size_t bi = b;
-        for (std::size_t i = b + 1; i < e; ++i)
-          if (starts_before(d[i], d[bi])) bi = i;
-        pb[t] = bi;
-      }
-      best = pb[0];
-      for (int t = 1; t < T; ++t)
-        if (pb[t] < sz && starts_before(d[pb[t]], d[best])) best = pb[t];
-    }
-    tmark("best");
-    if (best != 0) {
-      PVec r(sz);
-      copy_points(r.data(), d.data() + best, sz - best);
-      copy_points(r.data() + (sz - best), d.data(), best);
-      d.swap(r);
-    }
-    tmark("rotate");
-  }
+  if (d.size() >= 2) rotate_to(d, start_vertex(d));
+  tmark("rotate");
   return d;
 }
 
-PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4]) {
-  PVec chains[4];
+PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
+                           const std::function<void(int)>& wait_arc) {
   const std::uint64_t total = len[0] + len[1] + len[2] + len[3];
   const double t0 = now_ms();
-  if (total >= (1u << 12)) {  // one thread per arc
-    std::vector<std::thread> th;
-    for (int q = 0; q < 4; ++q)
-      th.emplace_back([&, q] { chains[q] = chain_sorted(arcs[q], len[q]); });
-    for (auto& t : th) t.join();
-  } else {
-    for (int q = 0; q < 4; ++q) chains[q] = chain_sorted(arcs[q], len[q]);
-  }
-  std::size_t h = 0;
-  for (int q = 0; q < 4; ++q) h += chains[q].size();
-  PVec cycle(h);
-  for (std::size_t q = 0, off = 0; q < 4; off += chains[q].size(), ++q)
-    copy_points(cycle.data() + off, chains[q].data(), chains[q].size());
-  for (auto& c : chains) PVec().swap(c);
+  PVec cycle = chain_arcs(arcs, len, wait_arc);
   const double t1 = now_ms();
   PVec out = finalize_cycle(std::move(cycle));
   if (trace_on())

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -224,6 +225,9 @@ void copy_points(P2* dst, const P2* src, std::size_t n);
 PVec quadrant_chain(std::vector<P2> pts, int quadrant);
 // chain of an arc already in sweep order (the arc's last point dropped)
 PVec chain_sorted(const P2* pts, std::size_t n);
+// the four arcs' chains concatenated (the cycle of hull.cpp:164-183)
+PVec chain_arcs(const P2* const arcs[4], const std::uint64_t len[4],
+                const std::function<void(int)>& wait_arc);
 // The hull stage's sweep sort on the device (hullsort.cu): the four arcs
 // [anchor q, queue q (packed [q1|q2|q3|q4] coordinates), anchor q+1], each
 // sorted in its quadrant's sweep order, written back to back to d_sorted
@@ -233,7 +237,10 @@ void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const doub
                void* d_work, double* d_sorted, cudaStream_t s);
 // hull stage from the four arcs [anchor q, queue q, anchor q+1] already in
 // sweep order (device-sorted)
-PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4]);
+// (wait_arc(q), when set, is called by arc q's thread before it reads the
+// arc: the arcs may still be arriving from the device)
+PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
+                           const std::function<void(int)>& wait_arc = {});
 PVec finalize_cycle(PVec cycle);
 PVec hull_from_queue_points(const P2 anchors[4], const P2* const q_pts[4],
                             const std::uint64_t q_len[4]);

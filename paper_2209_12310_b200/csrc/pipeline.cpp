@@ -156,6 +156,14 @@ int ohx_find_extremes(const double* h_xy, uint64_t n, uint64_t ext[8]) {
   });
 }
 
+int ohx_chain(const double* h_xy, uint64_t n, double* h_out, uint64_t* m) {
+  return guard([&] {
+    const ohx::PVec c = ohx::chain_sorted(reinterpret_cast<const ohx::P2*>(h_xy), n);
+    *m = c.size();
+    ohx::copy_points(reinterpret_cast<ohx::P2*>(h_out), c.data(), c.size());
+  });
+}
+
 int ohx_monotone_chain(const double* h_xy, uint64_t n, double* h_hull, uint64_t cap,
                        uint64_t* h) {
   return guard([&] {

@@ -273,3 +273,77 @@ def test_pts2_header_validation(tmp_path, oracle):
         assert what in P.lib.ohx_last_error().decode()
     assert P.lib.ohx_pts2_count(os.fsencode(tmp_path / "nope.bin"), C.byref(n)) == _lib.OHX_E_IO
     assert "nope.bin" in P.lib.ohx_last_error().decode()
+
+
+@pytest.mark.parametrize("chunks", ["2", "7", "64"])
+def test_parallel_chain_matches_the_sequential_loop(chunks):
+    # the host hull tests again with every arc of >= 64 points chained in
+    # parallel chunks (OHX_CHAIN_PAR_MIN / OHX_CHAIN_CHUNKS test hooks):
+    # golden corpora, the reference's degenerate grids, large degenerate sets
+    import subprocess
+    import sys
+    env = dict(os.environ, OHX_CHAIN_PAR_MIN="64", OHX_CHAIN_CHUNKS=chunks)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_host.py"), "-k",
+                        "host_hull and not parallel_chain"],
+                       capture_output=True, text=True, env=env, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+CHAIN_SCRIPT = r"""
+import sys, numpy as np, ctypes as C
+sys.path.insert(0, ROOT_DIR)
+import paper_2209_12310_b200 as P
+dp = C.POINTER(C.c_double)
+
+def seq_chain(a):  # the reference loop (hull.cpp:140-149), Python doubles
+    st = []
+    for x, y in a.tolist():
+        while len(st) >= 2:
+            (ax, ay), (bx, by) = st[-2], st[-1]
+            if (bx - ax) * (y - ay) - (by - ay) * (x - ax) > 0.0:
+                break
+            st.pop()
+        st.append((x, y))
+    return np.array(st[:-1], dtype=np.float64).reshape(-1, 2)
+
+def lib_chain(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    out = np.empty_like(a); m = C.c_uint64()
+    P.check(P.lib.ohx_chain(a.ctypes.data_as(dp), len(a), out.ctypes.data_as(dp), C.byref(m)))
+    return out[: m.value]
+
+rng = np.random.default_rng(11)
+seqs = []
+t = np.sort(rng.uniform(0, np.pi / 2, 20000))[::-1]          # convex arc (nearly no pops)
+seqs.append(np.stack([np.cos(t), np.sin(t)], 1))
+seqs.append(np.stack([np.cos(t), np.sin(t)], 1) * (1 + rng.normal(0, 1e-3, (20000, 1))))
+x = np.sort(rng.uniform(0, 1, 20000))[::-1]                   # random cloud, many pops
+seqs.append(np.stack([x, rng.uniform(0, 1, 20000)], 1))
+z = np.arange(20000.0)                                        # zigzag: pops across chunks
+seqs.append(np.stack([-z, (z % 2) * 3.0 + z * 1e-3], 1))
+seqs.append(np.stack([-z, np.where(z % 1000 < 500, 0.0, 1e6 - z)], 1))
+g = rng.integers(0, 30, size=(20000, 2)).astype(float)        # grid: duplicates, collinear
+seqs.append(g[np.lexsort((g[:, 1], -g[:, 0]))])
+line = np.stack([-z, 2 * z], 1)                               # collinear
+seqs.append(line)
+w = np.cumsum(rng.normal(0, 1, (20000, 2)), 0)               # random walk
+seqs.append(w[np.argsort(-w[:, 0], kind="stable")])
+bad = 0
+for a in seqs:
+    a = np.ascontiguousarray(a)
+    if not np.array_equal(lib_chain(a), seq_chain(a)):
+        bad += 1
+print("chains ok" if bad == 0 else f"{bad} mismatches")
+"""
+
+
+@pytest.mark.parametrize("chunks", ["2", "5", "16", "300"])
+def test_parallel_chain_equals_the_reference_loop_directly(chunks):
+    import subprocess
+    import sys
+    env = dict(os.environ, OHX_CHAIN_PAR_MIN="64", OHX_CHAIN_CHUNKS=chunks)
+    code = CHAIN_SCRIPT.replace("ROOT_DIR", repr(ROOT))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=900)
+    assert r.returncode == 0 and "chains ok" in r.stdout, r.stdout + r.stderr[-3000:]
