@@ -1,0 +1,516 @@
+// device.cpp -- the filter pipeline on one device: K1 / K1b / K2 launches
+// and their host steps, the fused single pass (provisional region, KF,
+// candidate extremes, certified K2 on the candidates), the queues and the
+// hull stage's device sweep sort.
+#include <cuda_runtime.h>
+#include <fcntl.h>
+#include <omp.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "host.hpp"
+#include "internal.hpp"
+#include "ohx.h"
+#include "pipeline.hpp"
+
+namespace ohx {
+
+void extremes(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+              ohx_extremes_rec* out, cudaStream_t s) {
+  if (n == 0) throw std::invalid_argument("find_axis_extremes: empty point set");
+  const int grid = k1_grid(c->device, n);
+  ensure_partials(c, grid);
+  check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
+  launch_k1(d_xy, n, base, c->d_partials, grid, c->d_ticket, c->d_rec, s);
+  check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
+  c->timed[0] = true;
+  ++c->launches;
+  check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
+                             cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec)");
+  check_cuda(cudaStreamSynchronize(s), "k1_extremes");
+  *out = *c->h_rec;
+}
+
+void corners_exact(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                   std::uint64_t base, const double bbox[4], ohx_corner_rec* out,
+                   cudaStream_t s) {
+  if (n == 0) throw std::invalid_argument("find_corner_extremes: empty point set");
+  const int grid = k1_grid(c->device, n);
+  ensure_partials(c, grid);
+  check_cuda(cudaEventRecord(c->ev[1][0], s), "cudaEventRecord");
+  launch_k1b(d_xy, n, base, bbox, c->d_partials, grid, c->d_ticket, c->d_crec, s);
+  check_cuda(cudaEventRecord(c->ev[1][1], s), "cudaEventRecord");
+  c->timed[1] = true;
+  ++c->launches;
+  check_cuda(cudaMemcpyAsync(c->h_crec, c->d_crec, sizeof(ohx_corner_rec),
+                             cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(crec)");
+  check_cuda(cudaStreamSynchronize(s), "k1b_corners");
+  *out = *c->h_crec;
+}
+KPlan make_kplan(const ohx_filter_plan& plan, std::uint64_t base, std::uint64_t n) {
+  KPlan kp;
+  std::memcpy(kp.ax, plan.ax, sizeof(kp.ax));
+  std::memcpy(kp.ay, plan.ay, sizeof(kp.ay));
+  std::memcpy(kp.ea, plan.ea, sizeof(kp.ea));
+  std::memcpy(kp.ec, plan.ec, sizeof(kp.ec));
+  std::memcpy(kp.qax, plan.qax, sizeof(kp.qax));
+  std::memcpy(kp.qay, plan.qay, sizeof(kp.qay));
+  std::memcpy(kp.qa, plan.qa, sizeof(kp.qa));
+  std::memcpy(kp.qc, plan.qc, sizeof(kp.qc));
+  std::memcpy(kp.box, plan.box, sizeof(kp.box));
+  for (int k = 0; k < 8; ++k) {
+    const std::uint64_t g = plan.kept[k];
+    kp.kept[k] = (g >= base && g - base < n) ? g - base : ~0ull;
+    kp.kept_label[k] = plan.kept_label[k];
+  }
+  kp.m = plan.m;
+  return kp;
+}
+
+// K2 over the n points of a shard, or (d_cand != null) over the n_cand
+// candidates listed there (shard-local indices, same width as the queues).
+void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+                 const ohx_filter_plan& plan, std::uint8_t* d_labels, std::uint64_t counts[4],
+                 cudaStream_t s, const void* d_cand, std::uint64_t n_cand,
+                 const double* d_cpts) {
+  const KPlan kp = make_kplan(plan, base, n);
+  const std::uint64_t items = d_cand ? n_cand : n;
+  const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
+  if (items == 0) {  // no candidates at all
+    for (int q = 0; q < 4; ++q) counts[q] = 0;
+  } else {
+    const std::uint64_t ntiles = (items + kK2Tile - 1) / kK2Tile;
+    dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes,
+             k2_work_bytes(ntiles), "k2 work area");
+    // queue capacity: 1/16 of the items (at least 1M); grown to the exact
+    // counts and re-run on overflow (counts are exact even when stores are
+    // dropped)
+    std::uint64_t cap =
+        std::min<std::uint64_t>(items, std::max<std::uint64_t>(1u << 20, items / 16));
+    if (c->queue_bytes / (4ull * idx_bytes) > cap)
+      cap = std::min<std::uint64_t>(items, c->queue_bytes / (4ull * idx_bytes));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      dev_grow(&c->d_queues, &c->queue_bytes, 4ull * idx_bytes * cap, "queues");
+      check_cuda(cudaEventRecord(c->ev[2][0], s), "cudaEventRecord");
+      launch_k2(d_xy, items, kp, c->d_status, ntiles, c->d_queues, idx_bytes, cap, d_labels,
+                c->d_counts, s, d_cand, d_cpts);  // k2_filter + k2_compact
+      check_cuda(cudaEventRecord(c->ev[2][1], s), "cudaEventRecord");
+      c->timed[2] = true;
+      c->launches += 2;
+      check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
+      check_cuda(cudaStreamSynchronize(s), "k2_filter");
+      std::uint64_t mx = 0;
+      for (int q = 0; q < 4; ++q) {
+        counts[q] = c->h_counts[q];
+        mx = std::max<std::uint64_t>(mx, counts[q]);
+      }
+      if (mx <= cap) break;
+      if (attempt == 1) throw Error(OHX_E_INTERNAL, "k2_filter: queue overflow after regrow");
+      cap = std::min<std::uint64_t>(items, mx + mx / 8 + 1024);
+    }
+    c->last_cap = cap;
+  }
+  c->last_xy = d_xy;
+  c->last_n = n;
+  c->last_base = base;
+  c->last_idx_bytes = idx_bytes;
+  for (int q = 0; q < 4; ++q) c->last_counts[q] = counts[q];
+}
+
+
+void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+            const ohx_filter_plan& plan, std::uint8_t* d_labels, std::uint64_t counts[4],
+            cudaStream_t s) {
+  if (n == 0) throw std::invalid_argument("classify_points: empty point set");
+  filter_core(c, d_xy, n, base, plan, d_labels, counts, s, nullptr, 0, nullptr);
+}
+void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
+                 std::uint64_t cap, cudaStream_t s) {
+  if (q < 1 || q > 4) throw std::invalid_argument("queue must be 1..4");
+  if (c->last_n == 0) throw std::invalid_argument("no filter result in this context");
+  const std::uint64_t cnt = c->last_counts[q - 1];
+  if (cnt > cap) throw std::invalid_argument("queue larger than the output capacity");
+  if (cnt == 0) return;
+  const auto* qbase = static_cast<const char*>(c->d_queues) +
+                      std::uint64_t(q - 1) * c->last_cap * c->last_idx_bytes;
+  if (h_xy) {
+    dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, cnt * 16, "gather");
+    launch_gather(c->last_xy, qbase, c->last_idx_bytes, cnt, c->d_gather, s);
+    ++c->launches;
+    check_cuda(cudaMemcpyAsync(h_xy, c->d_gather, cnt * 16, cudaMemcpyDeviceToHost, s),
+               "cudaMemcpyAsync(queue xy)");
+  }
+  if (h_idx) {
+    if (c->last_idx_bytes == 8) {
+      check_cuda(cudaMemcpyAsync(h_idx, qbase, cnt * 8, cudaMemcpyDeviceToHost, s),
+                 "cudaMemcpyAsync(queue idx)");
+      check_cuda(cudaStreamSynchronize(s), "queue fetch");
+    } else {
+      std::vector<std::uint32_t> tmp(cnt);
+      check_cuda(cudaMemcpyAsync(tmp.data(), qbase, cnt * 4, cudaMemcpyDeviceToHost, s),
+                 "cudaMemcpyAsync(queue idx)");
+      check_cuda(cudaStreamSynchronize(s), "queue fetch");
+      for (std::uint64_t k = 0; k < cnt; ++k) h_idx[k] = c->last_base + tmp[k];
+    }
+    if (c->last_idx_bytes == 8 && c->last_base)
+      for (std::uint64_t k = 0; k < cnt; ++k) h_idx[k] += c->last_base;
+  }
+  check_cuda(cudaStreamSynchronize(s), "queue fetch");
+}
+
+void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s) {
+  if (c->last_n == 0) throw std::invalid_argument("no filter result in this context");
+  const std::uint64_t total =
+      c->last_counts[0] + c->last_counts[1] + c->last_counts[2] + c->last_counts[3];
+  if (total == 0) return;
+  dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, total * 16, "gather");
+  launch_gather4(c->last_xy, c->d_queues, c->last_idx_bytes, c->last_cap, c->last_counts,
+                 c->d_gather, s);
+  ++c->launches;
+  check_cuda(cudaMemcpyAsync(h_xy, c->d_gather, total * 16, cudaMemcpyDeviceToHost, s),
+             "cudaMemcpyAsync(queues xy)");
+  check_cuda(cudaStreamSynchronize(s), "queues fetch");
+}
+// Survivor counts from which the hull stage's sweep sort runs on the device
+constexpr std::uint64_t kDeviceSortMin = 1u << 17;
+PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s) {
+  // reference hull.cpp:164-183 on the device queues
+  const std::uint64_t total = f.counts[0] + f.counts[1] + f.counts[2] + f.counts[3];
+  const P2 anchors[4] = {{f.ext.x[OHX_EAST], f.ext.y[OHX_EAST]},
+                         {f.ext.x[OHX_NORTH], f.ext.y[OHX_NORTH]},
+                         {f.ext.x[OHX_WEST], f.ext.y[OHX_WEST]},
+                         {f.ext.x[OHX_SOUTH], f.ext.y[OHX_SOUTH]}};
+  if (total >= kDeviceSortMin) {
+    // large survivor sets: the arcs are built and sorted on the device and
+    // come back in sweep order; the chains and the clean-up run on the host
+    dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, total * 16, "gather");
+    launch_gather4(c->last_xy, c->d_queues, c->last_idx_bytes, c->last_cap, c->last_counts,
+                   c->d_gather, s);
+    ++c->launches;
+    const std::uint64_t arcs_n = total + 8;
+    dev_grow(&c->d_hsort, &c->hsort_bytes, sort_arcs_work_bytes(f.counts) + arcs_n * 16,
+             "hull sort work");
+    auto* d_sorted = reinterpret_cast<double*>(static_cast<unsigned char*>(c->d_hsort) +
+                                               sort_arcs_work_bytes(f.counts));
+    Trace tr;
+    sort_arcs(c->d_gather, f.counts, reinterpret_cast<const double*>(anchors), c->d_hsort,
+              d_sorted, s);
+    c->launches += 2 + 4 * 4;  // build/gather + four radix sorts
+    if (tr.on) {
+      check_cuda(cudaStreamSynchronize(s), "hull sort");
+      tr.mark("hull dev sort");
+    }
+    host_grow(&c->h_sorted, &c->h_sorted_bytes, arcs_n * 16, "cudaMallocHost(sorted arcs)");
+    // one copy per arc: arc q's chain starts as soon as its copy lands
+    if (!c->arc_ev[0])
+      for (auto& e : c->arc_ev)
+        check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate(arc)");
+    const P2* arcs[4];
+    std::uint64_t len[4], off = 0;
+    for (int q = 0; q < 4; ++q) {
+      arcs[q] = static_cast<const P2*>(c->h_sorted) + off;
+      len[q] = f.counts[q] + 2;
+      check_cuda(cudaMemcpyAsync(static_cast<P2*>(c->h_sorted) + off,
+                                 reinterpret_cast<const P2*>(d_sorted) + off, len[q] * 16,
+                                 cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(sorted arc)");
+      check_cuda(cudaEventRecord(c->arc_ev[q], s), "cudaEventRecord(arc)");
+      off += len[q];
+    }
+    std::atomic<int> failed{cudaSuccess};  // set by the arc threads (no throwing there)
+    PVec cyc = hull_from_sorted_arcs(arcs, len, [&](int q) {
+      const cudaError_t e = cudaEventSynchronize(c->arc_ev[q]);
+      if (e != cudaSuccess) failed = e;
+    });
+    check_cuda(static_cast<cudaError_t>(failed.load()), "cudaEventSynchronize(sorted arc)");
+    tr.mark("hull D2H + host");
+    return cyc;
+  }
+  // one gather launch and one D2H of the survivors' coordinates, then the
+  // host hull stage
+  std::vector<P2> packed(total);
+  queues_fetch_xy(c, reinterpret_cast<double*>(packed.data()), s);
+  const P2* qp[4];
+  std::uint64_t off = 0;
+  for (int k = 0; k < 4; ++k) {
+    qp[k] = packed.data() + off;
+    off += f.counts[k];
+  }
+  return hull_from_queue_points(anchors, qp, f.counts);
+}
+void finish_extremes(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                     const ohx_extremes_rec& rec, FilterOut& f, cudaStream_t s) {
+  const std::uint32_t mask = resolve_extremes(rec, &f.ext);
+  f.corner_pass = mask != 0;
+  if (mask) {
+    const double bbox[4] = {rec.x[OHX_EAST], rec.y[OHX_NORTH], rec.x[OHX_WEST],
+                            rec.y[OHX_SOUTH]};
+    ohx_corner_rec cr;
+    corners_exact(c, d_xy, n, 0, bbox, &cr, s);
+    apply_corners(cr, &f.ext);
+  }
+  const int slot[8] = {OHX_EAST, OHX_NE, OHX_NORTH, OHX_NW,
+                       OHX_WEST, OHX_SW, OHX_SOUTH, OHX_SE};
+  double cand[16];
+  for (int k = 0; k < 8; ++k) {
+    cand[2 * k] = f.ext.x[slot[k]];
+    cand[2 * k + 1] = f.ext.y[slot[k]];
+  }
+  f.m = build_octagon(cand, f.oct);
+  make_plan(f.ext, f.oct, f.m, &f.plan);
+}
+
+constexpr std::uint64_t kFuseMinPoints = 1ull << 23;  // below: both passes are cheap
+
+// OHX_FUSE: unset/"auto" = fused pass when it pays, "0" = always two passes,
+// "fallback" = run the fused pass but reject its region (exercises the
+// verification-failure path), "force" = fuse whatever the sample coverage
+// (exercises heavy candidate lists).  The last two are for tests.
+int fuse_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("OHX_FUSE");
+    if (!e || !*e || std::string(e) == "auto") return 1;
+    if (std::string(e) == "0") return 0;
+    if (std::string(e) == "fallback") return 2;
+    if (std::string(e) == "force") return 3;
+    return 1;
+  }();
+  return mode;
+}
+constexpr int kSampleLen = 8192;     // points per sample run
+static_assert(kSampleLen % 2048 == 0, "k1_small reads sample runs 2048 points at a time");
+constexpr int kCoverageStep = 4;      // coverage counted on every 4th run
+constexpr int kSampleMaxSegs = 1024;  // runs (8M points, 128 MB) for n >= 2^27
+// OHX_SAMPLE_SEGS overrides the cap (experiment switch)
+int sample_max_segs() {
+  static const int v = [] {
+    const char* e = std::getenv("OHX_SAMPLE_SEGS");
+    const int k = e ? std::atoi(e) : 0;
+    return k >= 64 ? k : kSampleMaxSegs;
+  }();
+  return v;
+}
+constexpr int kSubSamples = 8;  // disjoint sub-samples of kSampleSegs / 8 runs each
+constexpr double kFuseMinCoverage = 0.8;
+// The provisional region of the fused pass.  A sample of about n/16 points
+// (up to 8M: runs of kSampleLen consecutive points at evenly spaced offsets,
+// read in place) is split into kSubSamples disjoint sub-samples (run b goes
+// to sub-sample b % kSubSamples, so each spans the whole index range); each
+// one's eight extremes (one batched launch) give an octagon, and Q is fitted
+// inside the INTERSECTION of those octagons.  The sub-sample octagons
+// scatter the way the true octagon may sit relative to any one sample's, so
+// a region inside all of them rarely leaves the true octagon (checked
+// exactly after the pass; a miss costs the regular second pass).  Q's bounds
+// are also kept strictly below the whole sample's extremes keys, which is
+// what lets the fused pass skip the extremes test for points inside Q.
+// Returns false when fusing does not pay (small input, no region, sample
+// coverage below kFuseMinCoverage).
+bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegion* q,
+                        std::uint64_t* sampled, cudaStream_t s, FilterOut& f, Trace& tr) {
+  if (n < kFuseMinPoints || fuse_mode() == 0) return false;
+  f.fuse_state = 2;
+  // about n/16 sampled points, 64..1024 runs, a multiple of kSubSamples
+  const int segs = static_cast<int>(std::clamp<std::uint64_t>(
+                       n / (16ull * kSampleLen), 64, sample_max_segs())) / kSubSamples * kSubSamples;
+  dev_grow(reinterpret_cast<void**>(&c->d_sample), &c->sample_bytes,
+           kSubSamples * sizeof(ohx_extremes_rec), "sample records");
+  auto* d_recs = reinterpret_cast<ohx_extremes_rec*>(c->d_sample);
+  ensure_partials(c, segs);
+  launch_k1_sample(d_xy, n, segs, kSampleLen, kSubSamples, c->d_partials, c->d_ticket, d_recs, s);
+  ++c->launches;
+  ohx_extremes_rec rs[kSubSamples];
+  check_cuda(cudaMemcpyAsync(rs, d_recs, sizeof(rs), cudaMemcpyDeviceToHost, s),
+             "cudaMemcpyAsync(sample recs)");
+  check_cuda(cudaStreamSynchronize(s), "sample extremes");
+  tr.mark("sample k1");
+  const int slot[8] = {OHX_EAST, OHX_NE, OHX_NORTH, OHX_NW,
+                       OHX_WEST, OHX_SW, OHX_SOUTH, OHX_SE};
+  std::vector<P2> region;
+  for (int g = 0; g < kSubSamples; ++g) {
+    ohx_extreme_set es;
+    resolve_extremes(rs[g], &es);  // heuristic octagons: diagonal winners need no certificate
+    double cand[16], oct[16];
+    for (int k = 0; k < 8; ++k) {
+      cand[2 * k] = es.x[slot[k]];
+      cand[2 * k + 1] = es.y[slot[k]];
+    }
+    const int m = build_octagon(cand, oct);
+    if (m < 3) return false;
+    if (g == 0) {
+      for (int i = 0; i < m; ++i) region.push_back({oct[2 * i], oct[2 * i + 1]});
+      continue;
+    }
+    for (int i = 0; i < m && region.size() >= 3; ++i) {
+      const int j = i + 1 == m ? 0 : i + 1;
+      region = clip_left(region, {oct[2 * i], oct[2 * i + 1]}, {oct[2 * j], oct[2 * j + 1]});
+    }
+    if (region.size() < 3) return false;
+  }
+  // the whole sample's best (axis) / second (diagonal) keys
+  ohx_extremes_rec all;
+  combine_extremes(rs, kSubSamples, &all);
+  double lim[8];
+  for (int a = 0; a < 8; ++a) lim[a] = a < 4 ? all.key[a] : all.second[a - 4];
+  if (!fit_region(region, lim, q)) return false;
+  tr.mark("region fit");
+  // the coverage count stays on the device: KF reads it and runs only when
+  // enough of the sample falls inside Q (no host round trip here)
+  launch_count_in_region(d_xy, n, segs, kSampleLen, kCoverageStep, *q, c->d_cnt, s);
+  ++c->launches;
+  *sampled = std::uint64_t((segs + kCoverageStep - 1) / kCoverageStep) * kSampleLen;
+  f.fuse_state = 3;
+  return true;
+}
+
+
+FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                             std::uint8_t* d_labels, cudaStream_t s);
+
+FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                        std::uint8_t* d_labels, cudaStream_t s) {
+  const FilterOut f = device_filter_impl(c, d_xy, n, d_labels, s);
+  c->last_run.fused = f.fused;
+  c->last_run.corner_pass = f.corner_pass;
+  c->last_run.candidates = f.candidates;
+  c->last_run.fuse_state = f.fuse_state;
+  c->last_run.sample_coverage = f.sample_coverage;
+  for (int q = 0; q < 4; ++q) c->last_run.counts[q] = f.counts[q];
+  return f;
+}
+
+
+// Fused pass, first half, over the n points of one shard (global indices
+// base + j): provisional region -> KF -> ordered candidate list -> K1 over
+// the candidates.  Returns true with the shard's extremes record in *rec
+// (what K1 over all points would have produced) when the fused pass ran;
+// false (f.fuse_state says why) when the caller must run K1 instead.
+bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+                 FilterOut& f, ohx_extremes_rec* rec, cudaStream_t s, Trace& tr) {
+  c->fz.active = false;
+  KFRegion q;
+  std::uint64_t sampled = 0;
+  if (!provisional_region(c, d_xy, n, &q, &sampled, s, f, tr)) return false;
+  const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
+  const int grid = kf_grid(c->device);
+  const std::uint64_t nw = std::uint64_t(grid) * kKFWarpsPerBlock;
+  const std::uint64_t per = ((n + 255) / 256 + nw - 1) / nw * 256;  // points per warp
+  // KF runs (device-side gate) when >= kFuseMinCoverage of the sample is in
+  // Q; each warp region has room for 1.5x the miss rate that allows (+256).
+  // A region that overflows sends the call down the two-pass path.
+  const double min_cov = fuse_mode() == 3 ? 0.0 : kFuseMinCoverage;
+  const auto gate_min = static_cast<std::uint64_t>(std::ceil(min_cov * double(sampled)));
+  const std::uint64_t cap_w = std::min<std::uint64_t>(
+      per, 256 + static_cast<std::uint64_t>(1.5 * (1.0 - min_cov) * double(per)));
+  dev_grow(&c->d_regions, &c->regions_bytes, nw * cap_w * idx_bytes, "kf regions");
+  dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes, nw * 12 + 16, "kf counts");
+  auto* d_wcounts = reinterpret_cast<std::uint32_t*>(c->d_status);
+  auto* d_offsets = c->d_status + (nw + 1) / 2;  // 8-byte aligned after the u32 counts
+  check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
+  launch_kf(d_xy, n, q, grid, c->d_regions, idx_bytes, cap_w, d_wcounts, c->d_cnt, gate_min, s);
+  check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
+  c->timed[0] = true;
+  ++c->launches;
+  // candidate list + coordinates and K1 over them, sized on the device: the
+  // list buffers hold cap_c candidates (more: regrown and redone below)
+  check_cuda(cudaEventRecord(c->ev[3][0], s), "cudaEventRecord");
+  launch_kf_scan(d_wcounts, nw, cap_w, d_offsets, c->d_cnt, c->d_counts, s);
+  std::uint64_t cap_c = std::max<std::uint64_t>(c->cpts_bytes / 16,
+                                                std::max<std::uint64_t>(1u << 20, n / 32));
+  auto candidates = [&](std::uint64_t cap) {
+    dev_grow(&c->d_cand, &c->cand_bytes, cap * idx_bytes, "candidates");
+    dev_grow(reinterpret_cast<void**>(&c->d_cpts), &c->cpts_bytes, cap * 16, "candidate points");
+    launch_kf_gather(d_xy, c->d_regions, idx_bytes, cap_w, d_wcounts, d_offsets, nw, c->d_cand,
+                     c->d_cpts, cap, s);
+    const int k1g = k1_list_grid(cap);
+    ensure_partials(c, k1g);
+    launch_k1_list(c->d_cpts, cap, c->d_counts, c->d_partials, k1g, c->d_ticket, c->d_rec, s);
+    launch_map_rec(c->d_rec, c->d_cand, idx_bytes, base, s);
+    c->launches += 3;
+    check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
+    check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
+                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec)");
+    check_cuda(cudaStreamSynchronize(s), "kf + candidate extremes");
+  };
+  candidates(cap_c);
+  ++c->launches;  // kf_scan
+  tr.mark("kf+cand-k1");
+  f.sample_coverage = double(c->h_counts[2]) / double(sampled);
+  const std::uint64_t n_cand = c->h_counts[0];
+  f.candidates = n_cand;
+  if (c->h_counts[2] < gate_min) return false;  // KF did not run: low coverage
+  if (n_cand == 0 || c->h_counts[1] != 0) {
+    f.fuse_state = 5;  // a warp region overflowed: the two-pass path
+    return false;
+  }
+  if (n_cand > cap_c) {  // more candidates than the list buffers held
+    cap_c = n_cand;
+    candidates(cap_c);
+  }
+  check_cuda(cudaEventRecord(c->ev[3][1], s), "cudaEventRecord");
+  c->timed[3] = true;
+  *rec = *c->h_rec;
+  rec->n = n;
+  c->fz = {true, q, d_xy, n, base, n_cand};
+  return true;
+}
+
+// Fused pass, second half: with the (global) ExtremeSet and plan, the
+// points KF dropped have the reference label 0 iff Q lies inside the
+// octagon (exact error bounds) and holds none of the eight kept points;
+// then K2 runs over the candidates only, otherwise over all n points.
+void fused_finish(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+                  const ohx_extreme_set& ext, const ohx_filter_plan& plan,
+                  std::uint8_t* d_labels, std::uint64_t counts[4], FilterOut& f,
+                  cudaStream_t s) {
+  if (!c->fz.active || c->fz.d_xy != d_xy || c->fz.n != n || c->fz.base != base)
+    throw std::invalid_argument("filter_fused: no fused pass over these points in this context");
+  c->fz.active = false;
+  const KFRegion& q = c->fz.q;
+  bool ok = region_certified(plan, q) && fuse_mode() != 2;
+  f.fuse_state = 4;
+  for (int a = 0; a < 8 && ok; ++a) ok = !in_region_host(q, ext.x[a], ext.y[a]);
+  if (!ok) {  // not certified: the regular K2 pass over all points
+    filter(c, d_xy, n, base, plan, d_labels, counts, s);
+    return;
+  }
+  f.fuse_state = 1;
+  f.fused = true;
+  if (d_labels) check_cuda(cudaMemsetAsync(d_labels, 0, n, s), "cudaMemsetAsync(labels)");
+  filter_core(c, d_xy, n, base, plan, d_labels, counts, s, c->d_cand, c->fz.n_cand, c->d_cpts);
+}
+
+FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
+                             std::uint8_t* d_labels, cudaStream_t s) {
+  if (n == 0) throw std::invalid_argument("heaphull: empty point set");
+  FilterOut f{};
+  for (bool& t : c->timed) t = false;  // kernel_ms reports this pipeline's stages
+  Trace tr;
+  ohx_extremes_rec rec;
+  if (fused_begin(c, d_xy, n, 0, f, &rec, s, tr)) {
+    finish_extremes(c, d_xy, n, rec, f, s);
+    tr.mark("octagon+plan");
+    fused_finish(c, d_xy, n, 0, f.ext, f.plan, d_labels, f.counts, f, s);
+    tr.mark("k2");
+    return f;
+  }
+  // ---- two passes: K1, then K2
+  extremes(c, d_xy, n, 0, &rec, s);
+  finish_extremes(c, d_xy, n, rec, f, s);
+  filter(c, d_xy, n, 0, f.plan, d_labels, f.counts, s);
+  return f;
+}
+
+}  // namespace ohx

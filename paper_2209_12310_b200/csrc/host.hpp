@@ -1,0 +1,141 @@
+// host.hpp -- shared by the host-side translation units of the library
+// (context.cpp, plan.cpp, device.cpp, capi.cpp): the device context and its
+// workspaces, the plan geometry, and the fused pass's two halves.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "internal.hpp"
+#include "ohx.h"
+#include "pipeline.hpp"
+
+// ====================================================================== ctx
+struct ohx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  std::uint64_t launches = 0;
+
+  // K1 / K1b scratch
+  int partial_cap = 0;
+  ohx::K1Partial* d_partials = nullptr;
+  unsigned* d_ticket = nullptr;
+  ohx_extremes_rec* d_rec = nullptr;
+  ohx_corner_rec* d_crec = nullptr;
+  ohx_extremes_rec* h_rec = nullptr;  // pinned
+  ohx_corner_rec* h_crec = nullptr;   // pinned
+  unsigned long long* d_counts = nullptr;
+  unsigned long long* h_counts = nullptr;  // pinned
+
+  // K2 scratch and queues
+  std::uint64_t* d_status = nullptr;
+  std::uint64_t status_bytes = 0;
+  void* d_queues = nullptr;
+  std::uint64_t queue_bytes = 0;
+
+  // result of the last ohx_filter
+  const double* last_xy = nullptr;
+  std::uint64_t last_n = 0, last_base = 0, last_cap = 0;
+  int last_idx_bytes = 4;
+  std::uint64_t last_counts[4] = {0, 0, 0, 0};
+
+  // staging for host-API calls
+  double* d_pts = nullptr;
+  std::uint64_t pts_bytes = 0;
+  std::uint8_t* d_labels = nullptr;
+  std::uint64_t labels_bytes = 0;
+  double* d_gather = nullptr;
+  std::uint64_t gather_bytes = 0;
+
+  // fused single-pass mode: sample, candidate list, coverage counter
+  double* d_sample = nullptr;
+  std::uint64_t sample_bytes = 0;
+  void* d_cand = nullptr;
+  std::uint64_t cand_bytes = 0;
+  void* d_regions = nullptr;  // KF per-warp candidate regions
+  std::uint64_t regions_bytes = 0;
+  double* d_cpts = nullptr;  // gathered candidate coordinates
+  std::uint64_t cpts_bytes = 0;
+  void* d_hsort = nullptr;  // hull stage: device sweep sort work + sorted arcs
+  std::uint64_t hsort_bytes = 0;
+  void* h_sorted = nullptr;  // pinned: the sorted arcs on the host
+  std::uint64_t h_sorted_bytes = 0;
+  cudaEvent_t arc_ev[4] = {};  // their per-arc copies
+  unsigned long long* d_cnt = nullptr;
+  unsigned long long* h_cnt = nullptr;  // pinned
+
+  ohx_run_info last_run = {};
+
+  // the last fused pass (fused_begin) awaiting its fused_finish
+  struct {
+    bool active = false;
+    ohx::KFRegion q{};
+    const double* d_xy = nullptr;
+    std::uint64_t n = 0, base = 0, n_cand = 0;
+  } fz;
+
+  // pinned staging ring for host copies of pageable user buffers
+  static constexpr int kStageBufs = 4;
+  void* h_stage[kStageBufs] = {};
+  cudaEvent_t stage_ev[kStageBufs] = {};
+
+  // CUDA events bracketing the last launch of each stage: K1 (or KF), K1b,
+  // K2, and the fused path's candidate stage (compaction + candidate K1)
+  cudaEvent_t ev[4][2] = {};
+  bool timed[4] = {false, false, false, false};
+};
+
+namespace ohx {
+
+// OHX_TRACE=1: host wall time of each pipeline phase on stderr
+struct Trace {
+  bool on = [] {
+    const char* e = std::getenv("OHX_TRACE");
+    return e && *e && std::string(e) != "0";
+  }();
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ohx] %-14s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
+// ---- context workspaces (context.cpp)
+const char* last_error();  // this thread's last error message
+void dev_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what);
+void host_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what);
+cudaStream_t pick(ohx_ctx* c, void* s);
+void bind(ohx_ctx* c);
+void ensure_partials(ohx_ctx* c, int grid);
+std::uint64_t load_pts2_device(ohx_ctx* c, const std::string& path, double* d_xy,
+                               std::uint64_t cap, cudaStream_t s);
+
+// ---- plan geometry (plan.cpp)
+bool certify_corner(const ohx_extremes_rec& r, int k);
+void fit_box(const double* oct, int m, const double* ea, const double* ec, double box[4]);
+bool region_certified(const ohx_filter_plan& plan, const KFRegion& q);
+bool in_region_host(const KFRegion& q, double x, double y);
+std::vector<P2> clip_left(const std::vector<P2>& poly, P2 a, P2 b);
+bool fit_region(const std::vector<P2>& R, const double lim[8], KFRegion* q);
+
+// ---- the fused pass (device.cpp)
+bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+                 FilterOut& f, ohx_extremes_rec* rec, cudaStream_t s, Trace& tr);
+void fused_finish(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
+                  const ohx_extreme_set& ext, const ohx_filter_plan& plan,
+                  std::uint8_t* d_labels, std::uint64_t counts[4], FilterOut& f,
+                  cudaStream_t s);
+
+}  // namespace ohx
