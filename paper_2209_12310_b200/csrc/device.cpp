@@ -186,8 +186,9 @@ void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s) {
 }
 // Survivor counts from which the hull stage's sweep sort runs on the device
 constexpr std::uint64_t kDeviceSortMin = 1u << 17;
-PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s) {
-  // reference hull.cpp:164-183 on the device queues
+std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
+                               const HullSink& sink) {
+  // reference hull.cpp:164-183 on the device queues; the hull goes to sink
   const std::uint64_t total = f.counts[0] + f.counts[1] + f.counts[2] + f.counts[3];
   const P2 anchors[4] = {{f.ext.x[OHX_EAST], f.ext.y[OHX_EAST]},
                          {f.ext.x[OHX_NORTH], f.ext.y[OHX_NORTH]},
@@ -230,13 +231,18 @@ PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s) {
       off += len[q];
     }
     std::atomic<int> failed{cudaSuccess};  // set by the arc threads (no throwing there)
-    PVec cyc = hull_from_sorted_arcs(arcs, len, [&](int q) {
-      const cudaError_t e = cudaEventSynchronize(c->arc_ev[q]);
-      if (e != cudaSuccess) failed = e;
-    });
-    check_cuda(static_cast<cudaError_t>(failed.load()), "cudaEventSynchronize(sorted arc)");
+    const std::size_t h = hull_from_sorted_arcs(
+        arcs, len,
+        [&](int q) {
+          const cudaError_t e = cudaEventSynchronize(c->arc_ev[q]);
+          if (e != cudaSuccess) failed = e;
+        },
+        [&](std::size_t hh) {
+          check_cuda(static_cast<cudaError_t>(failed.load()), "cudaEventSynchronize(sorted arc)");
+          return sink(hh);
+        });
     tr.mark("hull D2H + host");
-    return cyc;
+    return h;
   }
   // one gather launch and one D2H of the survivors' coordinates, then the
   // host hull stage
@@ -248,7 +254,18 @@ PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s) {
     qp[k] = packed.data() + off;
     off += f.counts[k];
   }
-  return hull_from_queue_points(anchors, qp, f.counts);
+  const PVec cyc = hull_from_queue_points(anchors, qp, f.counts);
+  copy_points(sink(cyc.size()), cyc.data(), cyc.size());
+  return cyc.size();
+}
+
+PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s) {
+  PVec out;
+  device_queues_hull(c, f, s, [&](std::size_t h) {
+    out.resize(h);
+    return out.data();
+  });
+  return out;
 }
 void finish_extremes(ohx_ctx* c, const double* d_xy, std::uint64_t n,
                      const ohx_extremes_rec& rec, FilterOut& f, cudaStream_t s) {

@@ -31,6 +31,7 @@
 #include <cstring>
 #include <string>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <thread>
@@ -621,16 +622,78 @@ struct ArcChain {
 
 }  // namespace
 
-// The chains of the four arcs (already in sweep order), concatenated in arc
-// order, each without its last point (the next arc's entry): the cycle the
-// clean-up takes (reference hull.cpp:164-183).  Arcs of >= par_min points
-// run in parallel chunks (all arcs' chunks in one parallel loop); wait_arc(q)
-// is called before arc q is read.
-PVec chain_arcs(const P2* const arcs[4], const std::uint64_t len[4],
-                const std::function<void(int)>& wait_arc) {
+namespace {
+
+// A cycle held as pieces of other buffers (the arcs' chain stacks), read as
+// one virtual sequence.
+struct PieceCycle {
+  std::vector<const P2*> ptr;
+  std::vector<std::size_t> off{0};  // piece k = [off[k], off[k+1])
+  std::size_t n = 0;
+  void add(const P2* p, std::size_t len) {
+    if (!len) return;
+    ptr.push_back(p);
+    n += len;
+    off.push_back(n);
+  }
+  std::size_t piece_of(std::size_t i) const {
+    return static_cast<std::size_t>(std::upper_bound(off.begin(), off.end(), i) - off.begin()) - 1;
+  }
+  const P2& at(std::size_t i) const {
+    const std::size_t k = piece_of(i);
+    return ptr[k][i - off[k]];
+  }
+  // f(i, p) for i in [b, e), in order
+  template <class F>
+  void walk(std::size_t b, std::size_t e, F&& f) const {
+    if (b >= e) return;
+    std::size_t k = piece_of(b), j = b - off[k];
+    for (std::size_t i = b; i < e; ++i, ++j) {
+      while (j >= off[k + 1] - off[k]) {
+        ++k;
+        j = 0;
+      }
+      f(i, ptr[k][j]);
+    }
+  }
+  // dst[0, e - b) = sequence[b, e)
+  void copy_out(P2* dst, std::size_t b, std::size_t e) const {
+    const std::size_t k0 = b < e ? piece_of(b) : 0;
+    for (std::size_t k = k0; k + 1 < off.size() && off[k] < e; ++k) {
+      const std::size_t s0 = std::max(b, off[k]), s1 = std::min(e, off[k + 1]);
+      if (s0 < s1)
+        std::memcpy(static_cast<void*>(dst + (s0 - b)), ptr[k] + (s0 - off[k]), (s1 - s0) * sizeof(P2));
+    }
+  }
+  void copy_out_parallel(P2* dst, std::size_t b, std::size_t e) const {
+    const std::size_t len = e - b;
+    if (len < kParMin) {
+      copy_out(dst, b, e);
+      return;
+    }
+#pragma omp parallel
+    {
+      const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+      const std::size_t s0 = b + len * t / nt, s1 = b + len * (t + 1) / nt;
+      copy_out(dst + (s0 - b), s0, s1);
+    }
+  }
+};
+
+struct ChainedArcs {
+  ArcChain A[4];
+  PieceCycle cycle;  // every arc's chain minus its last entry, in arc order
+};
+
+// The chains of the four arcs (already in sweep order); arcs of >= par_min
+// points run in parallel chunks (all arcs' chunks in one parallel loop);
+// wait_arc(q) is called before arc q is read.
+std::unique_ptr<ChainedArcs> run_chains(const P2* const arcs[4], const std::uint64_t len[4],
+                                        const std::function<void(int)>& wait_arc) {
   const std::size_t par_min = chain_par_min();
   static const std::size_t chunks = std::max<std::size_t>(2, env_size("OHX_CHAIN_CHUNKS", 16));
-  ArcChain A[4];
+  auto R = std::make_unique<ChainedArcs>();
+  ArcChain* A = R->A;
   struct Task {
     int q;
     std::size_t j;
@@ -650,35 +713,90 @@ PVec chain_arcs(const P2* const arcs[4], const std::uint64_t len[4],
     return A[x.q].runs[x.j].e - A[x.q].runs[x.j].b > A[y.q].runs[y.j].e - A[y.q].runs[y.j].b;
   });
   const std::uint64_t total = len[0] + len[1] + len[2] + len[3];
+  const double t0 = now_ms();
 #pragma omp parallel for schedule(dynamic, 1) if (total >= (1u << 12))
   for (std::int64_t i = 0; i < static_cast<std::int64_t>(tasks.size()); ++i) {
     if (wait_arc) wait_arc(tasks[i].q);
     A[tasks[i].q].local_run(tasks[i].j);
   }
+  const double t1 = now_ms();
 #pragma omp parallel for schedule(dynamic, 1) if (total >= (1u << 12))
   for (int q = 0; q < 4; ++q)
     if (A[q].n) A[q].resolve();
-  // assembly: every arc's slices, minus its last entry, straight into the cycle
-  struct Piece {
-    const P2* src;
-    std::size_t len, dst;
-  };
-  std::vector<Piece> pieces;
-  std::size_t h = 0;
   for (int q = 0; q < 4; ++q) {
     if (A[q].gsize == 0) continue;
-    std::size_t keep = A[q].gsize - 1;
+    std::size_t keep = A[q].gsize - 1;  // the arc's last point is the next arc's entry
     for (const auto& sl : A[q].G) {
       const std::size_t l = std::min(keep, sl.to - sl.from);
-      if (l) pieces.push_back({sl.base + sl.from, l, h});
-      h += l;
+      R->cycle.add(sl.base + sl.from, l);
       keep -= l;
     }
   }
-  PVec cycle(h);
-#pragma omp parallel for schedule(dynamic, 1) if (h >= kParMin)
-  for (std::int64_t i = 0; i < static_cast<std::int64_t>(pieces.size()); ++i)
-    copy_points(cycle.data() + pieces[i].dst, pieces[i].src, pieces[i].len);
+  if (trace_on())
+    std::fprintf(stderr, "[ohx]   chains: local runs %.3f ms, resolve %.3f ms (%zu tasks)\n",
+                 t1 - t0, now_ms() - t1, tasks.size());
+  return R;
+}
+
+// One parallel pass over a piece cycle: duplicates?  all collinear with
+// (c0, c1)?  any non-strict turn?  the start vertex.
+struct PieceScan {
+  bool dups = false, flat = true, bad = false;
+  std::size_t best = 0;
+};
+
+PieceScan scan_pieces(const PieceCycle& c) {
+  PieceScan r;
+  const std::size_t m = c.n;
+  const P2 c0 = c.at(0), c1 = c.at(1);
+  const int T = m >= kParMin ? omp_get_max_threads() : 1;
+  std::vector<std::size_t> pb(T, m);
+  std::vector<unsigned char> dups(T, 0), flat(T, 1), bad(T, 0);
+#pragma omp parallel num_threads(T)
+  {
+    const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+    const std::size_t b = m * t / nt, e = m * (t + 1) / nt;
+    if (b < e) {
+      bool du = false, fl = true, ba = false;
+      std::size_t bi = b;
+      P2 bp = c.at(b);
+      P2 prev = c.at(b == 0 ? m - 1 : b - 1), cur = bp;
+      // cur = element i; the walk delivers i + 1 as `nx`
+      auto step = [&](std::size_t i, const P2& nx) {
+        if (i > 0) du = du || same(prev, cur);
+        if (i >= 2) fl = fl && orient(c0, c1, cur) == 0;
+        ba = ba || orient(prev, cur, nx) <= 0;
+        if (i > b && starts_before(cur, bp)) {
+          bi = i;
+          bp = cur;
+        }
+        prev = cur;
+        cur = nx;
+      };
+      c.walk(b + 1, e, [&](std::size_t i, const P2& nx) { step(i - 1, nx); });
+      step(e - 1, c.at(e == m ? 0 : e));
+      dups[t] = du;
+      flat[t] = fl;
+      bad[t] = ba;
+      pb[t] = bi;
+    }
+  }
+  for (int t = 0; t < T; ++t) {
+    r.dups = r.dups || dups[t];
+    r.flat = r.flat && flat[t];
+    r.bad = r.bad || bad[t];
+    if (pb[t] < m && (t == 0 || starts_before(c.at(pb[t]), c.at(r.best)))) r.best = pb[t];
+  }
+  return r;
+}
+
+}  // namespace
+
+PVec chain_arcs(const P2* const arcs[4], const std::uint64_t len[4],
+                const std::function<void(int)>& wait_arc) {
+  auto R = run_chains(arcs, len, wait_arc);
+  PVec cycle(R->cycle.n);
+  R->cycle.copy_out_parallel(cycle.data(), 0, R->cycle.n);
   return cycle;
 }
 
@@ -780,17 +898,50 @@ PVec finalize_cycle(PVec cycle) {
   return d;
 }
 
-PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
-                           const std::function<void(int)>& wait_arc) {
+std::size_t hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
+                                  const std::function<void(int)>& wait_arc, const HullSink& sink) {
   const std::uint64_t total = len[0] + len[1] + len[2] + len[3];
   const double t0 = now_ms();
-  PVec cycle = chain_arcs(arcs, len, wait_arc);
+  auto R = run_chains(arcs, len, wait_arc);
+  const PieceCycle& pc = R->cycle;
   const double t1 = now_ms();
-  PVec out = finalize_cycle(std::move(cycle));
+  std::size_t h = 0;
+  // fast path: no duplicates, no non-strict turn, not flat (the clean-up
+  // keeps every vertex): the hull is the cycle rotated to its start
+  // vertex, copied once, straight from the chain stacks to the output
+  bool done = false;
+  if (pc.n > 2 && !same(pc.at(0), pc.at(pc.n - 1))) {
+    const PieceScan sc = scan_pieces(pc);
+    if (!sc.dups && !sc.flat && !sc.bad) {
+      h = pc.n;
+      P2* out = sink(h);
+      pc.copy_out_parallel(out, sc.best, pc.n);
+      pc.copy_out_parallel(out + (pc.n - sc.best), 0, sc.best);
+      done = true;
+    }
+  }
+  if (!done) {  // the general clean-up on a contiguous copy
+    PVec cycle(pc.n);
+    pc.copy_out_parallel(cycle.data(), 0, pc.n);
+    PVec d = finalize_cycle(std::move(cycle));
+    h = d.size();
+    copy_points(sink(h), d.data(), h);
+  }
   if (trace_on())
     std::fprintf(stderr,
-                 "[ohx] hull chains (sorted arcs, %llu pts) %.3f ms, finalize %zu vertices %.3f ms\n",
-                 static_cast<unsigned long long>(total), t1 - t0, out.size(), now_ms() - t1);
+                 "[ohx] hull chains (sorted arcs, %llu pts) %.3f ms, clean-up + output %zu vertices %.3f ms%s\n",
+                 static_cast<unsigned long long>(total), t1 - t0, h, now_ms() - t1,
+                 done ? " (fast path)" : "");
+  return h;
+}
+
+PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
+                           const std::function<void(int)>& wait_arc) {
+  PVec out;
+  hull_from_sorted_arcs(arcs, len, wait_arc, [&](std::size_t h) {
+    out.resize(h);
+    return out.data();
+  });
   return out;
 }
 

@@ -66,10 +66,11 @@ ExtremeSet from_set(const ohx_extreme_set& s) {
 // hull.cpp:164-183): survivor coordinates are gathered on the device in
 // queue (= index) order and copied back, then chained on the host.
 HullPolygon hull_from_device(Device& d, const ohx::FilterOut& f) {
-  const ohx::PVec cyc = ohx::device_queues_hull(d.c, f, d.s);
   HullPolygon h;
-  h.vertices.resize(cyc.size());
-  ohx::copy_points(reinterpret_cast<ohx::P2*>(h.vertices.data()), cyc.data(), cyc.size());
+  ohx::device_queues_hull(d.c, f, d.s, [&](std::size_t n) {
+    h.vertices.resize(n);
+    return reinterpret_cast<ohx::P2*>(h.vertices.data());
+  });
   return h;
 }
 

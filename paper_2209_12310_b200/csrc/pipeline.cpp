@@ -34,6 +34,16 @@ void copy_hull(const std::vector<octohull::Point2D>& v, double* out, std::uint64
                    v.size());
 }
 
+// the caller's hull buffer as the hull stage's sink (capacity checked, the
+// size reported either way)
+ohx::HullSink hull_sink(double* h_hull, std::uint64_t cap, std::uint64_t* h) {
+  return [=](std::size_t hh) {
+    *h = hh;
+    if (hh > cap) throw std::invalid_argument("hull output capacity too small");
+    return reinterpret_cast<ohx::P2*>(h_hull);
+  };
+}
+
 }  // namespace
 
 using ohx::guard;
@@ -54,10 +64,7 @@ int ohx_heaphull(const double* h_xy, uint64_t n, double* h_hull, uint64_t cap, u
     const double* d_xy = ohx::stage_points(ctx, h_xy, n, s);
     const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
     const auto t1 = Clock::now();
-    const ohx::PVec cyc = ohx::device_queues_hull(ctx, f, s);
-    *h = cyc.size();
-    if (cyc.size() > cap) throw std::invalid_argument("hull output capacity too small");
-    ohx::copy_points(reinterpret_cast<ohx::P2*>(h_hull), cyc.data(), cyc.size());
+    ohx::device_queues_hull(ctx, f, s, hull_sink(h_hull, cap, h));
     if (timings) {
       timings[0] = ms(t0, t1);
       timings[1] = ms(t1, Clock::now());
@@ -77,10 +84,7 @@ int ohx_heaphull_device(ohx_ctx* ctx, const double* d_xy, uint64_t n, double* h_
     const auto t0 = Clock::now();
     const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
     const auto t1 = Clock::now();
-    const ohx::PVec cyc = ohx::device_queues_hull(ctx, f, s);
-    *h = cyc.size();
-    if (cyc.size() > cap) throw std::invalid_argument("hull output capacity too small");
-    ohx::copy_points(reinterpret_cast<ohx::P2*>(h_hull), cyc.data(), cyc.size());
+    ohx::device_queues_hull(ctx, f, s, hull_sink(h_hull, cap, h));
     const auto t2 = Clock::now();
     if (timings) {
       timings[0] = ms(t0, t1);
@@ -106,10 +110,7 @@ int ohx_heaphull_pts2(const char* path, double* h_hull, uint64_t cap, uint64_t* 
     const auto tl = Clock::now();
     const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
     const auto t1 = Clock::now();
-    const ohx::PVec cyc = ohx::device_queues_hull(ctx, f, s);
-    *h = cyc.size();
-    if (cyc.size() > cap) throw std::invalid_argument("hull output capacity too small");
-    ohx::copy_points(reinterpret_cast<ohx::P2*>(h_hull), cyc.data(), cyc.size());
+    ohx::device_queues_hull(ctx, f, s, hull_sink(h_hull, cap, h));
     if (timings) {
       timings[0] = ms(tl, t1);
       timings[1] = ms(t1, Clock::now());

@@ -67,6 +67,9 @@ void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s);
 // host hull stage on the queues of the last filter (survivors gathered and
 // copied back in one launch)
 PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s);
+// ... written to sink(h) instead (the caller's buffer); returns h
+std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
+                               const HullSink& sink);
 
 // K1 -> certificate -> (K1b) -> octagon -> plan -> K2 on one device
 FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
