@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=float, default=1e8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dists", action="store_true",
+                    help="skip the per-distribution lines (square / circle 1e8)")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the full-size parity gate against the reference library")
     return ap.parse_args()
@@ -381,6 +383,42 @@ def run_b200_arm(a):
                "sample": f"{a.dist} n={ns} seed={a.seed}, reference heaphull_run x2 "
                          f"(ReduceEngine chunk 32, {r['cores']} workers), mean {t:.3f} s"}
 
+    # ---------------- the other distributions (rank 0, N = 1): BASELINE
+    # configs[1] (uniform square 1e8, pure streaming) and configs[3]
+    # (circumference 1e8, nothing filtered: compaction- and hull-bound),
+    # device-resident, 5 timed steps each
+    dists = None
+    if rank == 0 and world == 1 and not a.no_dists:
+        dists = []
+        for dname, dn in (("square", 100_000_000), ("circle", 100_000_000)):
+            hbuf = torch.empty((dn, 2), dtype=torch.float64, pin_memory=True)
+            P.check(P.lib.ohx_generate(P.DISTS[dname], dn, a.seed, 0.0,
+                                       hbuf.numpy().ctypes.data_as(P._dp), 0))
+            dd = hbuf.to(dev)
+            del hbuf
+            for _ in range(2):
+                ctx.heaphull_device(dd, dn)
+            torch.cuda.synchronize()
+            start.record()
+            kms = []
+            for _ in range(5):
+                ctx.heaphull_device(dd, dn)
+                kms.append(ctx.kernel_ms())
+            stop.record()
+            torch.cuda.synchronize()
+            dms = start.elapsed_time(stop) / 5
+            info = ctx.last_run()
+            k_ms = statistics.mean(k["k1"] for k in kms)
+            k_bytes = 16 * dn + (4 * info["candidates"] if info["fused"] else 0)
+            dists.append({"dist": dname, "points": dn, "value": dn / (dms * 1e-3) / 1e9,
+                          "unit": UNIT, "ms_per_step": dms, "fused": info["fused"],
+                          "survivors": sum(info["counts"]),
+                          "streaming_kernel": "kf_filter" if info["fused"] else "k1_extremes",
+                          "streaming_gbs": k_bytes / (k_ms * 1e-3) / 1e9,
+                          "streaming_frac": k_bytes / (k_ms * 1e-3) / 1e9 / peak})
+            del dd
+            torch.cuda.empty_cache()
+
     # ---------------- full-size parity gate (rank 0, N = 1): the reference
     # library's own heaphull_run / find_extremes on these very points
     parity = None
@@ -423,7 +461,8 @@ def run_b200_arm(a):
                        "l2": "inputs 16 GB/GPU >> 126 MB L2 (no flush needed)",
                        "survivors": stats["counts"], "corner_certificate": "pass" if not
                        stats["uncertified"] else f"fallback mask {stats['uncertified']}"},
-            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity, "clocks": clk,
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
+            "distributions": dists, "clocks": clk,
             "clocks_e2e": clocks_e2e_summary, "gpu_launches": launches,
             "setup_s": setup_s,
         }
