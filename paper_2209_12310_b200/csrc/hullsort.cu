@@ -7,7 +7,10 @@
 // (circle 1e8: 4 x 25M points, ~0.85 s each on 16 host cores), so the arcs
 // are built and sorted here and come back to the host already in sweep
 // order; the chain and the cycle clean-up stay on the host (their
-// decisions are the reference's sequential predicate sequence).
+// decisions are the reference's predicate sequence).  The sort runs on the
+// 64-bit primary key (half the radix passes of the full 128-bit key); runs
+// of equal primary key are then ordered by the secondary key (repair_ties),
+// and arcs with runs longer than 64 fall back to the 128-bit sort.
 //
 // Keys: each coordinate maps to an order-preserving u64 (negative values
 // bit-complemented, others with the sign bit set); a descending component
@@ -63,6 +66,7 @@ __global__ void build_arc_keys(const double2* __restrict__ packed, ulonglong4 qo
     else if (k == a1 - 1) p = anchors[(q + 1) & 3];
     else p = packed[p0 + (k - a0 - 1)];
     arcs[k] = p;
+    if (keys == nullptr) continue;  // the fast path computes its own keys
     const std::uint64_t ax = asc_key(p.x), ay = asc_key(p.y);
     SweepKey key;
     switch (q) {
@@ -73,6 +77,71 @@ __global__ void build_arc_keys(const double2* __restrict__ packed, ulonglong4 qo
     }
     keys[k] = key;
     vals[k] = static_cast<std::uint32_t>(k - a0);
+  }
+}
+
+// Primary sweep key only (u64), for the fast sort: arc q ascending by
+//   q1 ~x, q2 ~y, q3 x, q4 y; ties are repaired afterwards by the secondary
+// key (repair_ties).
+__device__ __forceinline__ std::uint64_t primary_key(int q, double2 p) {
+  switch (q) {
+    case 0: return ~asc_key(p.x);
+    case 1: return ~asc_key(p.y);
+    case 2: return asc_key(p.x);
+    default: return asc_key(p.y);
+  }
+}
+__device__ __forceinline__ std::uint64_t secondary_key(int q, double2 p) {
+  switch (q) {
+    case 0: return asc_key(p.y);
+    case 1: return ~asc_key(p.x);
+    case 2: return ~asc_key(p.y);
+    default: return asc_key(p.x);
+  }
+}
+
+__global__ void primary_keys(const double2* __restrict__ arcs, ulonglong4 aoff, std::uint64_t total,
+                             std::uint64_t* __restrict__ keys, std::uint32_t* __restrict__ vals) {
+  for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += std::uint64_t(gridDim.x) * blockDim.x) {
+    const int q = (k >= aoff.y) + (k >= aoff.z) + (k >= aoff.w);
+    const std::uint64_t a0 = q == 0 ? aoff.x : (q == 1 ? aoff.y : (q == 2 ? aoff.z : aoff.w));
+    keys[k] = primary_key(q, arcs[k]);
+    vals[k] = static_cast<std::uint32_t>(k - a0);
+  }
+}
+
+// Runs of equal primary key (equal coordinate) ordered by the secondary
+// key: one thread per run, insertion sort; runs longer than 64 (degenerate
+// inputs: many equal coordinates) raise *long_run and the arcs are sorted
+// again by the full 128-bit key.
+constexpr int kMaxRun = 64;
+__global__ void repair_ties(const std::uint64_t* __restrict__ keys, std::uint32_t* vals,
+                            const double2* __restrict__ arcs, ulonglong4 aoff, std::uint64_t total,
+                            int* long_run) {
+  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += std::uint64_t(gridDim.x) * blockDim.x) {
+    const int q = (i >= aoff.y) + (i >= aoff.z) + (i >= aoff.w);
+    const std::uint64_t a0 = q == 0 ? aoff.x : (q == 1 ? aoff.y : (q == 2 ? aoff.z : aoff.w));
+    const std::uint64_t a1 = q == 0 ? aoff.y : (q == 1 ? aoff.z : (q == 2 ? aoff.w : total));
+    const std::uint64_t key = keys[i];
+    if (i + 1 >= a1 || keys[i + 1] != key || (i > a0 && keys[i - 1] == key)) continue;
+    std::uint64_t j = i + 1;
+    while (j < a1 && keys[j] == key && j - i <= kMaxRun) ++j;
+    if (j - i > kMaxRun) {
+      atomicExch(long_run, 1);
+      continue;
+    }
+    for (std::uint64_t k = i + 1; k < j; ++k) {  // insertion sort by the secondary key
+      const std::uint32_t v = vals[k];
+      const std::uint64_t sk = secondary_key(q, arcs[a0 + v]);
+      std::uint64_t m = k;
+      while (m > i && secondary_key(q, arcs[a0 + vals[m - 1]]) > sk) {
+        vals[m] = vals[m - 1];
+        --m;
+      }
+      vals[m] = v;
+    }
   }
 }
 
@@ -109,15 +178,19 @@ ArcLayout arc_layout(const std::uint64_t counts[4]) {
   return L;
 }
 
-std::size_t cub_tmp_bytes(std::uint64_t max_len) {
-  std::size_t bytes = 0;
+std::size_t cub_tmp_bytes(std::uint64_t max_len) {  // for either sort
+  std::size_t b128 = 0, b64 = 0;
   cub::DoubleBuffer<SweepKey> kb(nullptr, nullptr);
+  cub::DoubleBuffer<std::uint64_t> kb64(nullptr, nullptr);
   cub::DoubleBuffer<std::uint32_t> vb(nullptr, nullptr);
-  check_cuda(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb,
+  check_cuda(cub::DeviceRadixSort::SortPairs(nullptr, b128, kb, vb,
                                              static_cast<std::int64_t>(max_len),
                                              SweepDecomposer{}),
              "cub temp size");
-  return bytes;
+  check_cuda(cub::DeviceRadixSort::SortPairs(nullptr, b64, kb64, vb,
+                                             static_cast<std::int64_t>(max_len)),
+             "cub temp size");
+  return b128 > b64 ? b128 : b64;
 }
 
 std::size_t align256(std::size_t b) { return (b + 255) & ~std::size_t(255); }
@@ -157,28 +230,63 @@ void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const doub
              "cudaMemcpyAsync(anchors)");
   const unsigned grid = static_cast<unsigned>(L.total < 148ull * 2048 ? (L.total + 255) / 256 : 148 * 8);
   build_arc_keys<<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(d_packed), L.qoff, L.aoff,
-                                      L.total, d_anchors, arcs, k0, v0);
+                                      L.total, d_anchors, arcs, nullptr, nullptr);
   check_cuda(cudaGetLastError(), "build_arc_keys launch");
   const std::uint64_t ao[4] = {L.aoff.x, L.aoff.y, L.aoff.z, L.aoff.w};
+  // fast path: 64-bit primary keys (half the radix passes), ties repaired
+  auto* p0 = reinterpret_cast<std::uint64_t*>(k1);  // k1 is free until the fallback
+  auto* p1 = p0 + L.total;
+  primary_keys<<<grid, 256, 0, s>>>(arcs, L.aoff, L.total, p0, v1);
+  check_cuda(cudaGetLastError(), "primary_keys launch");
   int sel[4];
   for (int q = 0; q < 4; ++q) {
-    cub::DoubleBuffer<SweepKey> kb(k0 + ao[q], k1 + ao[q]);
-    cub::DoubleBuffer<std::uint32_t> vb(v0 + ao[q], v1 + ao[q]);
+    cub::DoubleBuffer<std::uint64_t> kb(p0 + ao[q], p1 + ao[q]);
+    cub::DoubleBuffer<std::uint32_t> vb(v1 + ao[q], v0 + ao[q]);
     std::size_t tb = tmp_bytes;
-    check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb,
-                                               static_cast<std::int64_t>(L.len[q]),
-                                               SweepDecomposer{}, 0, 128, s),
-               "cub::DeviceRadixSort::SortPairs");
-    sel[q] = vb.selector;
+    check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, static_cast<std::int64_t>(L.len[q]),
+                                               0, 64, s),
+               "cub::DeviceRadixSort::SortPairs(u64)");
+    sel[q] = kb.selector;
   }
-  // each arc's sorted positions end in the buffer its sort selected: bring
-  // them all into arc 0's
-  std::uint32_t* vals = sel[0] ? v1 : v0;
+  // bring every arc's sorted keys / positions into the same pair of buffers
+  std::uint64_t* keys = sel[0] ? p1 : p0;
+  std::uint32_t* vals = sel[0] ? v0 : v1;
   for (int q = 1; q < 4; ++q)
-    if (sel[q] != sel[0])
-      check_cuda(cudaMemcpyAsync(vals + ao[q], (sel[q] ? v1 : v0) + ao[q], L.len[q] * 4,
-                                 cudaMemcpyDeviceToDevice, s),
-                 "cudaMemcpyAsync(sorted positions)");
+    if (sel[q] != sel[0]) {
+      check_cuda(cudaMemcpyAsync(keys + ao[q], (sel[q] ? p1 : p0) + ao[q], L.len[q] * 8,
+                                 cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync(sorted keys)");
+      check_cuda(cudaMemcpyAsync(vals + ao[q], (sel[q] ? v0 : v1) + ao[q], L.len[q] * 4,
+                                 cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync(sorted positions)");
+    }
+  int* d_flag = reinterpret_cast<int*>(d_anchors + 8);  // 4 bytes after the 4 anchors
+  check_cuda(cudaMemsetAsync(d_flag, 0, sizeof(int), s), "cudaMemsetAsync(flag)");
+  repair_ties<<<grid, 256, 0, s>>>(keys, vals, arcs, L.aoff, L.total, d_flag);
+  check_cuda(cudaGetLastError(), "repair_ties launch");
+  int long_run = 0;
+  check_cuda(cudaMemcpyAsync(&long_run, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s),
+             "cudaMemcpyAsync(flag)");
+  check_cuda(cudaStreamSynchronize(s), "hull sort ties");
+  if (long_run) {  // degenerate arcs: the full 128-bit key sort
+    build_arc_keys<<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(d_packed), L.qoff,
+                                        L.aoff, L.total, d_anchors, arcs, k0, v0);
+    check_cuda(cudaGetLastError(), "build_arc_keys launch");
+    for (int q = 0; q < 4; ++q) {
+      cub::DoubleBuffer<SweepKey> kb(k0 + ao[q], k1 + ao[q]);
+      cub::DoubleBuffer<std::uint32_t> vb(v0 + ao[q], v1 + ao[q]);
+      std::size_t tb = tmp_bytes;
+      check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb,
+                                                 static_cast<std::int64_t>(L.len[q]),
+                                                 SweepDecomposer{}, 0, 128, s),
+                 "cub::DeviceRadixSort::SortPairs");
+      sel[q] = vb.selector;
+    }
+    vals = sel[0] ? v1 : v0;
+    for (int q = 1; q < 4; ++q)
+      if (sel[q] != sel[0])
+        check_cuda(cudaMemcpyAsync(vals + ao[q], (sel[q] ? v1 : v0) + ao[q], L.len[q] * 4,
+                                   cudaMemcpyDeviceToDevice, s),
+                   "cudaMemcpyAsync(sorted positions)");
+  }
   gather_sorted<<<grid, 256, 0, s>>>(arcs, vals, L.aoff, L.total,
                                      reinterpret_cast<double2*>(d_sorted));
   check_cuda(cudaGetLastError(), "gather_sorted launch");
