@@ -298,9 +298,9 @@ def test_fused_verification_failure_falls_back(tmp_path):
 
 
 @pytest.mark.parametrize("fuse", ["auto", "0"])
-def test_register_streaming_variant_matches_oracle(fuse):
-    # OHX_STREAM=reg selects the register-staged K1/KF streaming kernels
-    # instead of the TMA bulk-copy pipeline: same results, bit for bit
+def test_tma_streaming_variant_matches_oracle(fuse):
+    # OHX_STREAM=tma selects the TMA bulk-copy (cp.async.bulk + mbarrier)
+    # K1 instead of the register-staged default: same results, bit for bit
     import subprocess
     import sys
     code = (
@@ -316,11 +316,11 @@ def test_register_streaming_variant_matches_oracle(fuse):
         "    assert np.array_equal(hull, want_hull), dist\n"
         "    info = ctx.last_run()\n"
         "    assert info['counts'] == [int((want_labels == q).sum()) for q in (1, 2, 3, 4)]\n"
-        "print('reg ok')\n")
-    env = dict(os.environ, OHX_STREAM="reg", OHX_FUSE=fuse, PYTHONPATH=ROOT)
+        "print('tma ok')\n")
+    env = dict(os.environ, OHX_STREAM="tma", OHX_FUSE=fuse, PYTHONPATH=ROOT)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=600)
-    assert r.returncode == 0 and "reg ok" in r.stdout, r.stderr[-3000:]
+    assert r.returncode == 0 and "tma ok" in r.stdout, r.stderr[-3000:]
 
 
 def test_forced_fusion_heavy_candidates_match_oracle():
