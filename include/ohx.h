@@ -121,6 +121,10 @@ int ohx_device_count(int* n);
  * parallel.hpp:50-52); distinct contexts may run concurrently. */
 int ohx_ctx_create(int device, ohx_ctx** out);
 int ohx_ctx_destroy(ohx_ctx* ctx);
+/* Releases the context's grow-only device / pinned workspaces and the
+ * library's cache of large host blocks (the hull stage's); later calls
+ * regrow what they need.  Drops a pending ohx_fused_extremes. */
+int ohx_ctx_trim(ohx_ctx* ctx);
 /* Process-wide lazily created context for `device` (used by the C++ API). */
 int ohx_ctx_default(int device, ohx_ctx** out);
 int ohx_ctx_device(const ohx_ctx* ctx);

@@ -185,6 +185,11 @@ class Context:
         self.device = device
         self._owned = not default
 
+    def trim(self):
+        """Release this context's grow-only workspaces (and the host block
+        cache); later calls regrow them."""
+        check(lib.ohx_ctx_trim(self.h))
+
     def close(self):
         if self._owned and self.h:
             lib.ohx_ctx_destroy(self.h)

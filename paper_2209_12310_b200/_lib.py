@@ -67,6 +67,7 @@ PROTOTYPES = [
     ("ohx_device_count", C.c_int, [C.POINTER(C.c_int)]),
     ("ohx_ctx_create", C.c_int, [C.c_int, C.POINTER(_vp)]),
     ("ohx_ctx_destroy", C.c_int, [_vp]),
+    ("ohx_ctx_trim", C.c_int, [_vp]),
     ("ohx_ctx_default", C.c_int, [C.c_int, C.POINTER(_vp)]),
     ("ohx_ctx_device", C.c_int, [_vp]),
     ("ohx_ctx_launches", _u64, [_vp]),

@@ -48,6 +48,13 @@ int ohx_ctx_destroy(ohx_ctx* ctx) {
   return guard([&] { destroy_ctx(ctx); });
 }
 
+int ohx_ctx_trim(ohx_ctx* ctx) {
+  return guard([&] {
+    std::lock_guard<std::mutex> g(ctx->mu);
+    trim_ctx(ctx);
+  });
+}
+
 int ohx_ctx_default(int device, ohx_ctx** out) {
   return guard([&] { *out = default_ctx(device); });
 }

@@ -302,6 +302,41 @@ void destroy_ctx(ohx_ctx* c) {
   delete c;
 }
 
+// Frees the context's grow-only workspaces (device, pinned) and the host
+// block cache; the next call regrows what it needs.  Any pending fused pass
+// or filter result of the context is dropped.
+void trim_ctx(ohx_ctx* c) {
+  bind(c);
+  check_cuda(cudaStreamSynchronize(c->stream), "trim");
+  auto dfree = [](auto*& p, std::uint64_t* bytes) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    if (bytes) *bytes = 0;
+  };
+  dfree(c->d_status, &c->status_bytes);
+  dfree(c->d_queues, &c->queue_bytes);
+  dfree(c->d_pts, &c->pts_bytes);
+  dfree(c->d_labels, &c->labels_bytes);
+  dfree(c->d_gather, &c->gather_bytes);
+  dfree(c->d_sample, &c->sample_bytes);
+  dfree(c->d_cand, &c->cand_bytes);
+  dfree(c->d_regions, &c->regions_bytes);
+  dfree(c->d_cpts, &c->cpts_bytes);
+  dfree(c->d_hsort, &c->hsort_bytes);
+  if (c->h_sorted) cudaFreeHost(c->h_sorted);
+  c->h_sorted = nullptr;
+  c->h_sorted_bytes = 0;
+  for (int b = 0; b < ohx_ctx::kStageBufs; ++b) {
+    if (c->h_stage[b]) cudaFreeHost(c->h_stage[b]);
+    if (c->stage_ev[b]) cudaEventDestroy(c->stage_ev[b]);
+    c->h_stage[b] = nullptr;
+    c->stage_ev[b] = nullptr;
+  }
+  c->fz.active = false;
+  c->last_n = 0;
+  big_cache_trim();
+}
+
 ohx_ctx* default_ctx(int device) {
   static std::mutex mu;
   static std::vector<ohx_ctx*> ctxs;  // intentionally leaked at exit

@@ -52,7 +52,7 @@ struct BigCache {
   };
   std::vector<Block> blocks;  // freed blocks kept mapped (pages faulted)
   std::size_t held = 0;
-  static constexpr std::size_t kMaxHeld = std::size_t(16) << 30;
+  static constexpr std::size_t kMaxHeld = std::size_t(8) << 30;
   static constexpr std::size_t kMaxBlocks = 8;
 };
 BigCache& big_cache() {
@@ -83,6 +83,14 @@ void* big_alloc(std::size_t bytes) {
   if (posix_memalign(&p, std::size_t(2) << 20, bytes) != 0) throw std::bad_alloc();
   madvise(p, bytes, MADV_HUGEPAGE);
   return p;
+}
+
+void big_cache_trim() noexcept {
+  BigCache& c = big_cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  for (const auto& b : c.blocks) std::free(b.p);
+  c.blocks.clear();
+  c.held = 0;
 }
 
 void big_free(void* p, std::size_t bytes) noexcept {

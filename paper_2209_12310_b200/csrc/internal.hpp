@@ -191,6 +191,7 @@ struct P2 {
 constexpr std::size_t kBigBlock = std::size_t(64) << 20;
 void* big_alloc(std::size_t bytes);
 void big_free(void* p, std::size_t bytes) noexcept;
+void big_cache_trim() noexcept;  // frees the recycled blocks
 
 template <class T>
 struct DefaultInitAlloc : std::allocator<T> {

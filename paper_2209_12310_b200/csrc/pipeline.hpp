@@ -29,6 +29,7 @@ struct FilterOut {
 
 ohx_ctx* create_ctx(int device);
 void destroy_ctx(ohx_ctx* c);
+void trim_ctx(ohx_ctx* c);
 ohx_ctx* default_ctx(int device = -1);
 cudaStream_t ctx_stream(ohx_ctx* c);
 std::mutex& ctx_mutex(ohx_ctx* c);

@@ -479,3 +479,14 @@ def test_degenerate_large_inputs(ctx, oracle, shape):
     assert np.array_equal(hull, want_hull), shape
     info = ctx.last_run()
     assert info["counts"] == [int((want_labels == q).sum()) for q in (1, 2, 3, 4)], (shape, info)
+
+
+def test_trim_releases_and_regrows(oracle):
+    c = P.Context(0)
+    pts = P.generate("circle", 2_000_000, 5, 1.0)
+    d = dev(pts)
+    h1, _ = c.heaphull_device(d, len(pts))
+    c.trim()
+    h2, _ = c.heaphull_device(d, len(pts))
+    assert np.array_equal(h1, h2) and np.array_equal(h1, oracle.heaphull(pts))
+    c.close()
