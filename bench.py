@@ -27,10 +27,11 @@ per launch (16 B per point read; the fused KF pass also writes 4 B per
 candidate index) over its CUDA-event duration on the launching stream,
 against the measured HBM copy bandwidth in MEASURED_PEAKS.json.
 cpu_baseline: the reference library itself (oracle/_ref, compiled from the reference sources) timed on
-the host cores on a bounded 1e8-point sample.
+the host cores on the bench's own points (the full per-GPU workload).
 
 `--impl reference` times that reference CPU implementation on the same
-metric (rank 0 only), each step a bounded sample of the workload.
+metric (rank 0 only), each step one heaphull_run over the full per-GPU
+workload (--cpu-sample bounds it).
 """
 
 from __future__ import annotations
@@ -61,7 +62,8 @@ def parse():
     ap.add_argument("--dist", default="normal")
     ap.add_argument("--points", "--n", dest="n", type=float, default=1e9, help="points per GPU")
     ap.add_argument("--seed", type=int, default=7)
-    ap.add_argument("--cpu-sample", type=float, default=1e8)
+    ap.add_argument("--cpu-sample", type=float, default=0,
+                    help="points of the CPU reference's sample (0: the full per-GPU workload)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dists", action="store_true",
@@ -152,14 +154,17 @@ def ncu_traffic():
 
 
 # ------------------------------------------------------- CPU reference ----
-def cpu_reference(n_sample: int, reps: int, seed: int, dist: str):
-    """The reference heaphull_run (oracle/_ref) on all host cores."""
+def cpu_reference(n_sample: int, reps: int, seed: int, dist: str, pts=None):
+    """The reference heaphull_run (oracle/_ref) on all host cores, on `pts`
+    (the bench's own points) or a generated sample of n_sample points."""
     import numpy as np
 
     import paper_2209_12310_b200 as P
     from oracle import Oracle, Reference
 
-    pts = P.generate(dist, n_sample, seed)
+    if pts is None:
+        pts = P.generate(dist, n_sample, seed)
+    n_sample = len(pts)
     cores = os.cpu_count() or 1
     if Reference.available():
         eng = Reference().engine(cores, 32)
@@ -186,12 +191,14 @@ def run_reference_arm(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n = int(a.cpu_sample)
+    n = int(a.cpu_sample) or int(a.n)
     r = cpu_reference(n, a.warmup + a.steps, a.seed, a.dist)
     timed = r["times"][a.warmup:]
     ms = 1e3 * sum(timed) / len(timed)
     value = n / (ms * 1e-3) / 1e9
-    sample = f"{a.dist} n={n} seed={a.seed} (bounded sample of the {WORKLOAD} workload), full heaphull_run"
+    sample = (f"{a.dist} n={n} seed={a.seed} ("
+              + ("the full per-GPU workload" if n == int(a.n) else f"bounded sample of the {WORKLOAD} workload")
+              + "), full heaphull_run")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
@@ -377,11 +384,14 @@ def run_b200_arm(a):
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         ns = int(a.cpu_sample)
-        r = cpu_reference(ns, 2, a.seed, a.dist)
+        r = cpu_reference(ns, 2, a.seed, a.dist, pts=None if ns else hp)
+        ns = r["n"]
         t = statistics.mean(r["times"])
         cpu = {"value": ns / t / 1e9, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
-               "sample": f"{a.dist} n={ns} seed={a.seed}, reference heaphull_run x2 "
-                         f"(ReduceEngine chunk 32, {r['cores']} workers), mean {t:.3f} s"}
+               "sample": f"{a.dist} n={ns} seed={a.seed}"
+                         f"{' (the bench workload itself)' if ns == n else ''}, reference "
+                         f"heaphull_run x2 (ReduceEngine chunk 32, {r['cores']} workers), "
+                         f"mean {t:.3f} s"}
 
     # ---------------- the other distributions (rank 0, N = 1): BASELINE
     # configs[1] (uniform square 1e8, pure streaming) and configs[3]
