@@ -279,6 +279,12 @@ int ohx_generate(int dist, uint64_t n, uint64_t seed, double distort_pct,
  * run in parallel chunks with the reference loop's exact decisions. */
 int ohx_chain(const double* h_xy, uint64_t n, double* h_out, uint64_t* m);
 
+/* The hull stage on the four arcs [anchor q, queue q, anchor q+1] already
+ * in their quadrant's sweep order (what the device sort hands the host:
+ * hull.cpp:133-150 without the sort, then 94-120); h_hull capacity cap. */
+int ohx_hull_from_sorted_arcs(const double* const arcs_xy[4], const uint64_t len[4],
+                              double* h_hull, uint64_t cap, uint64_t* h);
+
 /* Host hull stage of heaphull_run (hull.cpp:164-183) on given queues:
  * pts = all points (host), queues as global indices. */
 int ohx_hull_from_queues(const double* h_xy, const uint64_t ext_axis[4],

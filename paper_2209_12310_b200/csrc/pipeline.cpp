@@ -157,6 +157,15 @@ int ohx_find_extremes(const double* h_xy, uint64_t n, uint64_t ext[8]) {
   });
 }
 
+int ohx_hull_from_sorted_arcs(const double* const arcs_xy[4], const uint64_t len[4],
+                              double* h_hull, uint64_t cap, uint64_t* h) {
+  return guard([&] {
+    const ohx::P2* arcs[4];
+    for (int q = 0; q < 4; ++q) arcs[q] = reinterpret_cast<const ohx::P2*>(arcs_xy[q]);
+    ohx::hull_from_sorted_arcs(arcs, len, {}, hull_sink(h_hull, cap, h));
+  });
+}
+
 int ohx_chain(const double* h_xy, uint64_t n, double* h_out, uint64_t* m) {
   return guard([&] {
     const ohx::PVec c = ohx::chain_sorted(reinterpret_cast<const ohx::P2*>(h_xy), n);

@@ -347,3 +347,56 @@ def test_parallel_chain_equals_the_reference_loop_directly(chunks):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=900)
     assert r.returncode == 0 and "chains ok" in r.stdout, r.stdout + r.stderr[-3000:]
+
+
+SORTED_ARCS_SCRIPT = r"""
+import sys, numpy as np, ctypes as C
+sys.path.insert(0, ROOT_DIR)
+sys.path.insert(0, ROOT_DIR + "/tests")
+import paper_2209_12310_b200 as P
+from oracle import Oracle
+dp = C.POINTER(C.c_double)
+o = Oracle()
+
+def sweep_sorted(a, q):  # the reference comparator's order (hull.cpp:18-30)
+    x, y = a[:, 0], a[:, 1]
+    keys = {1: (y, -x), 2: (-x, -y), 3: (-y, x), 4: (x, y)}[q]
+    return np.ascontiguousarray(a[np.lexsort(keys)])
+
+def lib_hull(pts):
+    ext = o.find_extremes(pts)
+    lab = o.classify(pts)
+    anchors = pts[ext[:4].astype(np.int64)]
+    arcs = []
+    for q in range(4):
+        arc = np.concatenate([anchors[q:q + 1], pts[lab == q + 1], anchors[(q + 1) % 4:(q + 1) % 4 + 1]])
+        arcs.append(sweep_sorted(arc, q + 1))
+    ptrs = (dp * 4)(*[a.ctypes.data_as(dp) for a in arcs])
+    lens = (C.c_uint64 * 4)(*[len(a) for a in arcs])
+    out = np.empty((sum(len(a) for a in arcs) + 8, 2)); h = C.c_uint64()
+    P.check(P.lib.ohx_hull_from_sorted_arcs(ptrs, lens, out.ctypes.data_as(dp), len(out), C.byref(h)))
+    return out[: h.value]
+
+rng = np.random.default_rng(9)
+cases = [o.generate("circle", 200_000, 3, 0.0), o.generate("circle", 150_000, 4, 1.0),
+         o.generate("disk", 200_000, 5, 0.0), o.generate("normal", 100_000, 6, 0.0)]
+t = rng.uniform(0, 2 * np.pi, 120_000)
+cases.append(np.round(np.stack([np.cos(t), np.sin(t)], 1) * 300.0))      # duplicates, ties
+cases.append(rng.integers(-9, 10, size=(50_000, 2)).astype(float))       # degenerate grid
+bad = sum(not np.array_equal(lib_hull(np.ascontiguousarray(a)), o.heaphull(np.ascontiguousarray(a)))
+          for a in cases)
+print("arcs ok" if bad == 0 else f"{bad} mismatches")
+"""
+
+
+@pytest.mark.parametrize("par_min,chunks", [("1000000000", "16"), ("64", "3"), ("64", "16")])
+def test_hull_from_sorted_arcs_matches_oracle(par_min, chunks):
+    # the device-sort path's host half (chains, piece-cycle clean-up and the
+    # single rotated copy) on arcs sorted here, sequential and chunked chains
+    import subprocess
+    import sys
+    env = dict(os.environ, OHX_CHAIN_PAR_MIN=par_min, OHX_CHAIN_CHUNKS=chunks)
+    code = SORTED_ARCS_SCRIPT.replace("ROOT_DIR", repr(ROOT))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=900)
+    assert r.returncode == 0 and "arcs ok" in r.stdout, r.stdout + r.stderr[-3000:]
