@@ -380,8 +380,9 @@ def run_b200_arm(a):
                 "pipeline": "fused single pass (KF)" if fused else "two passes (K1, K2)",
                 "candidates": cand}
 
-    # ---------------- CPU baseline (rank 0, N = 1)
+    # ---------------- CPU baseline (rank 0, N = 1) + full-size parity check
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not a.no_cpu:
         ns = int(a.cpu_sample)
         r = cpu_reference(ns, 2, a.seed, a.dist, pts=None if ns else hp)
@@ -392,6 +393,35 @@ def run_b200_arm(a):
                          f"{' (the bench workload itself)' if ns == n else ''}, reference "
                          f"heaphull_run x2 (ReduceEngine chunk 32, {r['cores']} workers), "
                          f"mean {t:.3f} s"}
+        # the same leg checks the device results against the reference's
+        # own heaphull_run / find_extremes on these very points (outside
+        # every timed region; the reference is the checker here)
+        if not a.no_parity and r["kind"] == "reference" and ns == n:
+            from oracle import Reference
+            if Reference.available():
+                ref = Reference()
+                cores = os.cpu_count() or 1
+                t0 = time.perf_counter()
+                ref_hull, ref_labels, _ = ref.heaphull_run(hp, cores, 32)
+                ref_ext = ref.find_extremes(hp, cores, 32)
+                ref_s = time.perf_counter() - t0
+                hull_dev = step_device()
+                info = ctx.last_run()
+                queues_ok = True
+                for q in range(4):
+                    want = np.flatnonzero(ref_labels == q + 1)
+                    got = ctx.queue(q + 1, info["counts"][q])[0]
+                    queues_ok &= bool(np.array_equal(got, want))
+                parity = {"checked_against": f"reference heaphull_run + find_extremes (oracle/_ref, "
+                                             f"{cores} workers) on the same {n} points",
+                          "hull_equal": bool(np.array_equal(hull_dev, ref_hull)),
+                          "extremes_equal": stats["ext"] == [int(v) for v in ref_ext],
+                          "queues_equal": queues_ok,
+                          "survivors": int((ref_labels != 0).sum()), "h": int(len(ref_hull)),
+                          "reference_s": ref_s}
+                del ref_labels
+            else:
+                parity = {"checked_against": None, "why": "oracle/_ref not built"}
 
     # ---------------- the other distributions (rank 0, N = 1): BASELINE
     # configs[1] (uniform square 1e8, pure streaming) and configs[3]
@@ -428,36 +458,6 @@ def run_b200_arm(a):
                           "streaming_frac": k_bytes / (k_ms * 1e-3) / 1e9 / peak})
             del dd
             torch.cuda.empty_cache()
-
-    # ---------------- full-size parity gate (rank 0, N = 1): the reference
-    # library's own heaphull_run / find_extremes on these very points
-    parity = None
-    if rank == 0 and world == 1 and not a.no_parity:
-        from oracle import Reference
-        if Reference.available():
-            ref = Reference()
-            cores = os.cpu_count() or 1
-            t0 = time.perf_counter()
-            ref_hull, ref_labels, _ = ref.heaphull_run(hp, cores, 32)
-            ref_ext = ref.find_extremes(hp, cores, 32)
-            ref_s = time.perf_counter() - t0
-            hull_dev = step_device()
-            info = ctx.last_run()
-            queues_ok = True
-            for q in range(4):
-                want = np.flatnonzero(ref_labels == q + 1)
-                got = ctx.queue(q + 1, info["counts"][q])[0]
-                queues_ok &= bool(np.array_equal(got, want))
-            parity = {"checked_against": f"reference heaphull_run + find_extremes (oracle/_ref, "
-                                         f"{cores} workers) on the same {n} points",
-                      "hull_equal": bool(np.array_equal(hull_dev, ref_hull)),
-                      "extremes_equal": stats["ext"] == [int(v) for v in ref_ext],
-                      "queues_equal": queues_ok,
-                      "survivors": int((ref_labels != 0).sum()), "h": int(len(ref_hull)),
-                      "reference_s": ref_s}
-            del ref_labels
-        else:
-            parity = {"checked_against": None, "why": "oracle/_ref not built"}
 
     if rank == 0:
         clk = clocks.summary()

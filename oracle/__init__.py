@@ -1,8 +1,10 @@
 """ctypes front-end for the parity checkers (TEST INFRASTRUCTURE ONLY).
 
 Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
-``cpu_baseline`` leg and ``--impl reference`` arm) may import this package.
-The product path (``paper_2209_12310_b200``) never does.
+``cpu_baseline`` leg -- which also checks the device results against the
+reference on the same points, outside every timed region -- and its
+``--impl reference`` arm) may import this package.  The product path
+(``paper_2209_12310_b200``) never does.
 
 Two checkers live here:
 
