@@ -185,7 +185,14 @@ void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s) {
   check_cuda(cudaStreamSynchronize(s), "queues fetch");
 }
 // Survivor counts from which the hull stage's sweep sort runs on the device
-constexpr std::uint64_t kDeviceSortMin = 1u << 17;
+// (OHX_DEVICE_SORT_MIN overrides; a test and tuning hook)
+std::uint64_t device_sort_min() {
+  static const std::uint64_t v = [] {
+    const char* e = std::getenv("OHX_DEVICE_SORT_MIN");
+    return e && *e ? static_cast<std::uint64_t>(std::atoll(e)) : std::uint64_t(1) << 17;
+  }();
+  return v;
+}
 std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
                                const HullSink& sink) {
   // reference hull.cpp:164-183 on the device queues; the hull goes to sink
@@ -194,7 +201,7 @@ std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
                          {f.ext.x[OHX_NORTH], f.ext.y[OHX_NORTH]},
                          {f.ext.x[OHX_WEST], f.ext.y[OHX_WEST]},
                          {f.ext.x[OHX_SOUTH], f.ext.y[OHX_SOUTH]}};
-  if (total >= kDeviceSortMin) {
+  if (total >= device_sort_min()) {
     // large survivor sets: the arcs are built and sorted on the device and
     // come back in sweep order; the chains and the clean-up run on the host
     dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, total * 16, "gather");
@@ -308,7 +315,14 @@ int fuse_mode() {
 }
 constexpr int kSampleLen = 8192;     // points per sample run
 static_assert(kSampleLen % 2048 == 0, "k1_small reads sample runs 2048 points at a time");
-constexpr int kCoverageStep = 4;      // coverage counted on every 4th run
+constexpr int kCoverageRuns = 64;     // coverage counted on 64 evenly spaced runs
+int coverage_step(int segs) {  // OHX_COVERAGE_STEP overrides (tuning hook)
+  static const int v = [] {
+    const char* e = std::getenv("OHX_COVERAGE_STEP");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v >= 1 ? v : std::max(1, segs / kCoverageRuns);
+}
 constexpr int kSampleMaxSegs = 1024;  // runs (8M points, 128 MB) for n >= 2^27
 // OHX_SAMPLE_SEGS overrides the cap (experiment switch)
 int sample_max_segs() {
@@ -354,7 +368,9 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   tr.mark("sample k1");
   const int slot[8] = {OHX_EAST, OHX_NE, OHX_NORTH, OHX_NW,
                        OHX_WEST, OHX_SW, OHX_SOUTH, OHX_SE};
-  std::vector<P2> region;
+  std::vector<P2> region, clipped;
+  region.reserve(64);
+  clipped.reserve(64);
   for (int g = 0; g < kSubSamples; ++g) {
     ohx_extreme_set es;
     resolve_extremes(rs[g], &es);  // heuristic octagons: diagonal winners need no certificate
@@ -371,7 +387,8 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
     }
     for (int i = 0; i < m && region.size() >= 3; ++i) {
       const int j = i + 1 == m ? 0 : i + 1;
-      region = clip_left(region, {oct[2 * i], oct[2 * i + 1]}, {oct[2 * j], oct[2 * j + 1]});
+      clip_left(region, {oct[2 * i], oct[2 * i + 1]}, {oct[2 * j], oct[2 * j + 1]}, clipped);
+      region.swap(clipped);
     }
     if (region.size() < 3) return false;
   }
@@ -384,9 +401,10 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   tr.mark("region fit");
   // the coverage count stays on the device: KF reads it and runs only when
   // enough of the sample falls inside Q (no host round trip here)
-  launch_count_in_region(d_xy, n, segs, kSampleLen, kCoverageStep, *q, c->d_cnt, s);
+  const int step = coverage_step(segs);
+  launch_count_in_region(d_xy, n, segs, kSampleLen, step, *q, c->d_cnt, s);
   ++c->launches;
-  *sampled = std::uint64_t((segs + kCoverageStep - 1) / kCoverageStep) * kSampleLen;
+  *sampled = std::uint64_t((segs + step - 1) / step) * kSampleLen;
   f.fuse_state = 3;
   return true;
 }

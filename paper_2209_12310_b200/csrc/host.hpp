@@ -127,7 +127,7 @@ bool certify_corner(const ohx_extremes_rec& r, int k);
 void fit_box(const double* oct, int m, const double* ea, const double* ec, double box[4]);
 bool region_certified(const ohx_filter_plan& plan, const KFRegion& q);
 bool in_region_host(const KFRegion& q, double x, double y);
-std::vector<P2> clip_left(const std::vector<P2>& poly, P2 a, P2 b);
+void clip_left(const std::vector<P2>& poly, P2 a, P2 b, std::vector<P2>& out);
 bool fit_region(const std::vector<P2>& R, const double lim[8], KFRegion* q);
 
 // ---- the fused pass (device.cpp)

@@ -450,8 +450,8 @@ bool in_region_host(const KFRegion& q, double x, double y) {
 }
 // Part of the convex polygon `poly` on the left of a -> b (Sutherland-Hodgman
 // step; heuristic geometry, the box is certified exactly after the pass).
-std::vector<P2> clip_left(const std::vector<P2>& poly, P2 a, P2 b) {
-  std::vector<P2> out;
+void clip_left(const std::vector<P2>& poly, P2 a, P2 b, std::vector<P2>& out) {
+  out.clear();
   const std::size_t m = poly.size();
   auto side = [&](P2 p) { return (b.x - a.x) * (p.y - a.y) - (b.y - a.y) * (p.x - a.x); };
   for (std::size_t i = 0; i < m; ++i) {
@@ -463,7 +463,6 @@ std::vector<P2> clip_left(const std::vector<P2>& poly, P2 a, P2 b) {
       out.push_back({p.x + t * (q.x - p.x), p.y + t * (q.y - p.y)});
     }
   }
-  return out;
 }
 
 
@@ -484,7 +483,14 @@ double slot_key(int a, double x, double y) {
 // Is the region {key_a <= b[a]} inside the convex CCW polygon R?  (R is
 // convex, so the region's vertices decide.)  Heuristic geometry in double,
 // no allocation: it runs a few hundred times per fit.
-bool region_inside(const double b[8], const std::vector<P2>& R) {
+// a provisional region: at most 8 + 7 * 8 vertices (one octagon clipped by seven)
+constexpr std::size_t kMaxRegion = 64;
+
+struct REdge {
+  double ax, ay, ex, ey;  // edge start, edge vector
+};
+
+bool region_inside(const double b[8], const REdge* R, std::size_t r) {
   P2 poly[16], out[16];
   int m = 4;
   poly[0] = {-b[2], -b[3]};
@@ -508,21 +514,14 @@ bool region_inside(const double b[8], const std::vector<P2>& R) {
     for (int i = 0; i < m; ++i) poly[i] = out[i];
   }
   if (m < 3) return false;
-  const std::size_t r = R.size();
-  for (int v = 0; v < m; ++v)
-    for (std::size_t i = 0; i < r; ++i) {
-      const P2 a = R[i], c = R[i + 1 == r ? 0 : i + 1];
-      if ((c.x - a.x) * (poly[v].y - a.y) - (c.y - a.y) * (poly[v].x - a.x) < 0) return false;
-    }
+  for (int v = 0; v < m; ++v) {
+    const P2 p = poly[v];
+    for (std::size_t i = 0; i < r; ++i)
+      if (R[i].ex * (p.y - R[i].ay) - R[i].ey * (p.x - R[i].ax) < 0) return false;
+  }
   return true;
 }
 
-// The fused pass's region Q: an octagon with the slot directions as edge
-// normals, fitted inside the convex polygon R.  Start from R's own slot
-// support values scaled towards R's centroid until the octagon fits, then
-// push each bound out on its own (a few rounds), then pull everything 0.2 %
-// back towards the centre.  Finally every bound is clamped strictly below
-// lim[a] (the sample's best / second key of the slot).
 bool fit_region(const std::vector<P2>& R, const double lim[8], KFRegion* q) {
   if (R.size() < 3) return false;
   double cx = 0, cy = 0;
@@ -532,6 +531,14 @@ bool fit_region(const std::vector<P2>& R, const double lim[8], KFRegion* q) {
   }
   cx /= double(R.size());
   cy /= double(R.size());
+  const std::size_t nr = R.size();
+  REdge E[kMaxRegion];
+  if (nr > kMaxRegion) return false;
+  for (std::size_t i = 0; i < nr; ++i) {
+    const P2 a = R[i], c = R[i + 1 == nr ? 0 : i + 1];
+    E[i] = {a.x, a.y, c.x - a.x, c.y - a.y};
+  }
+  auto inside = [&](const double* bb) { return region_inside(bb, E, nr); };
   double h[8], c0[8], b[8];
   for (int a = 0; a < 8; ++a) {
     h[a] = -INFINITY;
@@ -544,27 +551,28 @@ bool fit_region(const std::vector<P2>& R, const double lim[8], KFRegion* q) {
   };
   double lo = 0, hi = 1;
   at(1e-6, b);
-  if (!region_inside(b, R)) return false;
-  // bisections to ~1e-4 of the span: Q is pulled 0.2 % inwards afterwards
-  for (int it = 0; it < 14; ++it) {
+  if (!inside(b)) return false;
+  // bisections to ~1e-3 of the span (Q is pulled 0.2 % inwards afterwards),
+  // then one round of per-slot bisections: more rounds or steps add host
+  // time on the pass's critical path but no measurable coverage
+  for (int it = 0; it < 10; ++it) {
     const double mid = (lo + hi) / 2;
     at(mid, b);
-    if (region_inside(b, R)) lo = mid;
+    if (inside(b)) lo = mid;
     else hi = mid;
   }
   at(lo, b);
-  for (int round = 0; round < 2; ++round)
-    for (int a = 0; a < 8; ++a) {
-      double good = b[a], bad = h[a];
-      for (int it = 0; it < 10; ++it) {
-        double t[8];
-        std::memcpy(t, b, sizeof(t));
-        t[a] = (good + bad) / 2;
-        if (region_inside(t, R)) good = t[a];
-        else bad = t[a];
-      }
-      b[a] = good;
+  for (int a = 0; a < 8; ++a) {
+    double good = b[a], bad = h[a];
+    for (int it = 0; it < 6; ++it) {
+      double t[8];
+      std::memcpy(t, b, sizeof(t));
+      t[a] = (good + bad) / 2;
+      if (inside(t)) good = t[a];
+      else bad = t[a];
     }
+    b[a] = good;
+  }
   double r[8];
   for (int a = 0; a < 8; ++a) {
     r[a] = c0[a] + 0.998 * (b[a] - c0[a]);
