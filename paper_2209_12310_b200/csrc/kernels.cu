@@ -492,7 +492,8 @@ struct SampleMap {
   }
 };
 
-__device__ __forceinline__ void k1_visit(ArgState<8, 4>& st, double2 p, std::uint64_t j) {
+template <typename LI>
+__device__ __forceinline__ void k1_visit(ArgState<8, 4, LI>& st, double2 p, LI j) {
   const double t = __dadd_rn(p.x, p.y);
   const double d = __dsub_rn(p.x, p.y);
   upd(st.k[0], st.i[0], p.x, j);
@@ -505,7 +506,10 @@ __device__ __forceinline__ void k1_visit(ArgState<8, 4>& st, double2 p, std::uin
   upd2(st.k[7], st.i[7], st.s[3], d, j);
 }
 
-template <bool kSampled>
+// List mode: threads track 32-bit indices whenever the list fits (one
+// select per slot update instead of two), widened before the block / grid
+// reduction.
+template <bool kSampled, typename LI>
 __global__ void __launch_bounds__(256)
     k1_small(const double2* __restrict__ pts, std::uint64_t n, const unsigned long long* d_n,
              const SampleMap sm, K1Partial* partials, unsigned* ticket, ohx_extremes_rec* out) {
@@ -514,11 +518,13 @@ __global__ void __launch_bounds__(256)
   partials += std::uint64_t(g) * gridDim.x;
   ticket += g;
   out += g;
-  ArgState<8, 4> st;
-  st.init();
+  ArgState<8, 4, LI> lst;
+  lst.init();
   if constexpr (kSampled) {
-    // global indices only grow along a thread's runs (run b increases with
-    // s); 8 loads in flight per thread (runs are multiples of 2048 points)
+    // global indices (LI = u64: a 32-bit run-local index measured slower
+    // here) only grow along a thread's runs (run b increases with r); 8
+    // loads in flight per thread (runs are multiples of 2048 points)
+    static_assert(!kSampled || sizeof(LI) == 8, "sampled indices are global");
     const int nrun = sm.segs / sm.subs;
     for (int r = blockIdx.x; r < nrun; r += gridDim.x) {
       const std::uint64_t start = sm.run_start(std::uint64_t(r) * sm.subs + g);
@@ -527,7 +533,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int u = 0; u < 8; ++u) v[u] = ld_stream(pts + start + k0 + u * 256);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) k1_visit(st, v[u], start + k0 + u * 256);
+        for (int u = 0; u < 8; ++u) k1_visit(lst, v[u], LI(start + k0 + u * 256));
       }
     }
   } else {
@@ -538,10 +544,20 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int u = 0; u < 4; ++u) v[u] = ld_stream(pts + j + u * stride);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) k1_visit(st, v[u], j + u * stride);
+      for (int u = 0; u < 4; ++u) k1_visit(lst, v[u], LI(j + u * stride));
     }
-    for (; j < n; j += stride) k1_visit(st, ld_stream(pts + j), j);
+    for (; j < n; j += stride) k1_visit(lst, ld_stream(pts + j), LI(j));
   }
+  ArgState<8, 4> st;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    st.k[a] = lst.k[a];
+    std::uint64_t i = ~std::uint64_t(0);  // untouched slot
+    if (lst.i[a] != ~LI(0)) i = lst.i[a];
+    st.i[a] = i;
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) st.s[a] = lst.s[a];
   block_reduce<8, 4, 256>(st);
   if (!grid_combine<8, 4, 256>(st, partials, ticket)) return;
   if (threadIdx.x < 8) {
@@ -1538,22 +1554,33 @@ void launch_k1_sample(const double* d_xy, std::uint64_t n, int segs, int len, in
                       K1Partial* partials, unsigned* ticket, ohx_extremes_rec* d_recs,
                       cudaStream_t stream) {
   const SampleMap sm{n, segs, len, subs};
-  k1_small<true><<<dim3(segs / subs, subs), 256, 0, stream>>>(
+  k1_small<true, std::uint64_t><<<dim3(segs / subs, subs), 256, 0, stream>>>(
       reinterpret_cast<const double2*>(d_xy), 0, nullptr, sm, partials, ticket, d_recs);
   check_cuda(cudaGetLastError(), "k1_small<sample> launch");
 }
 
 int k1_list_grid(std::uint64_t n) {
+  // at most one wave (the reduction's cost grows with the grid); the list
+  // length is often counted on the device, n is then its capacity
+  static const int wave = [] {
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    return occupancy_grid(dev, k1_small<false, std::uint32_t>, 256, ~0ull);
+  }();
   const std::uint64_t b = (n + 256 * 16 - 1) / (256 * 16);
-  return static_cast<int>(b < 1 ? 1 : (b > 148 * 4 ? 148 * 4 : b));
+  return static_cast<int>(b < 1 ? 1 : (b > std::uint64_t(wave) ? wave : b));
 }
 
 void launch_k1_list(const double* d_xy, std::uint64_t n, const unsigned long long* d_n,
                     K1Partial* partials, int grid, unsigned* ticket, ohx_extremes_rec* d_rec,
                     cudaStream_t stream) {
-  k1_small<false><<<dim3(grid, 1), 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n,
-                                                    d_n, SampleMap{0, 1, 1, 1}, partials, ticket,
-                                                    d_rec);
+  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  if (n < 0xffffffffull)
+    k1_small<false, std::uint32_t><<<dim3(grid, 1), 256, 0, stream>>>(
+        pts, n, d_n, SampleMap{0, 1, 1, 1}, partials, ticket, d_rec);
+  else
+    k1_small<false, std::uint64_t><<<dim3(grid, 1), 256, 0, stream>>>(
+        pts, n, d_n, SampleMap{0, 1, 1, 1}, partials, ticket, d_rec);
   check_cuda(cudaGetLastError(), "k1_small<list> launch");
 }
 

@@ -367,6 +367,37 @@ def test_sorted_input_overflows_warp_regions_and_stays_exact(ctx, oracle):
     assert info["counts"] == [int((want_labels == q).sum()) for q in (1, 2, 3, 4)]
 
 
+def test_device_sweep_sort_forced_on_small_survivor_sets():
+    # OHX_DEVICE_SORT_MIN=0 sends every survivor set -- empty queues, single
+    # points, lattices full of duplicates and collinear runs -- through the
+    # device sweep sort (default: 2^17 survivors and up); hulls must match
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, paper_2209_12310_b200 as P\n"
+        "from oracle import Oracle\n"
+        "o = Oracle()\n"
+        "ctx = P.Context(0)\n"
+        "cases = [P.generate('normal', 1_000_000, 7), P.generate('square', 70_001, 3),\n"
+        "         P.generate('circle', 5_000, 2), P.generate('disk', 3, 1),\n"
+        "         np.array([[0.0, 0.0], [1.0, 0.0], [2.0, 0.0]]),\n"
+        "         np.array([[1.0, 1.0]] * 5), np.array([[0.0, -0.0], [-0.0, 0.0], [1.0, 1.0]])]\n"
+        "g = np.stack(np.meshgrid(np.arange(-40, 41.0), np.arange(-40, 41.0)), -1).reshape(-1, 2)\n"
+        "cases.append(np.ascontiguousarray(np.concatenate([g, g[::7]])))\n"
+        "rng = np.random.default_rng(3)\n"
+        "cases.append(np.ascontiguousarray(np.round(rng.normal(size=(20_000, 2)) * 3)))\n"
+        "for pts in cases:\n"
+        "    pts = np.ascontiguousarray(pts, dtype=np.float64)\n"
+        "    hull, _ = ctx.heaphull_device(torch.from_numpy(pts).cuda(), len(pts))\n"
+        "    assert np.array_equal(hull, o.heaphull(pts)), len(pts)\n"
+        "    assert np.array_equal(P.heaphull(pts), hull)\n"
+        "print('dsort ok')\n")
+    env = dict(os.environ, OHX_DEVICE_SORT_MIN="0", PYTHONPATH=ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=600)
+    assert r.returncode == 0 and "dsort ok" in r.stdout, r.stderr[-3000:]
+
+
 @pytest.mark.parametrize("scale", [50.0, 3000.0, 1e6])
 def test_device_sorted_hull_on_degenerate_survivors(oracle, scale):
     # survivor sets past the device sweep-sort threshold, full of duplicates,
