@@ -449,9 +449,8 @@ bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
   const std::uint64_t cap_w = std::min<std::uint64_t>(
       per, 256 + static_cast<std::uint64_t>(1.5 * (1.0 - min_cov) * double(per)));
   dev_grow(&c->d_regions, &c->regions_bytes, nw * cap_w * idx_bytes, "kf regions");
-  dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes, nw * 12 + 16, "kf counts");
+  dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes, nw * 4 + 16, "kf counts");
   auto* d_wcounts = reinterpret_cast<std::uint32_t*>(c->d_status);
-  auto* d_offsets = c->d_status + (nw + 1) / 2;  // 8-byte aligned after the u32 counts
   check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
   launch_kf(d_xy, n, q, grid, c->d_regions, idx_bytes, cap_w, d_wcounts, c->d_cnt, gate_min, s);
   check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
@@ -460,19 +459,18 @@ bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
   // candidate list + coordinates and K1 over them, sized on the device: the
   // list buffers hold cap_c candidates (more: regrown and redone below)
   check_cuda(cudaEventRecord(c->ev[3][0], s), "cudaEventRecord");
-  launch_kf_scan(d_wcounts, nw, cap_w, d_offsets, c->d_cnt, c->d_counts, s);
   std::uint64_t cap_c = std::max<std::uint64_t>(c->cpts_bytes / 16,
                                                 std::max<std::uint64_t>(1u << 20, n / 32));
   auto candidates = [&](std::uint64_t cap) {
     dev_grow(&c->d_cand, &c->cand_bytes, cap * idx_bytes, "candidates");
     dev_grow(reinterpret_cast<void**>(&c->d_cpts), &c->cpts_bytes, cap * 16, "candidate points");
-    launch_kf_gather(d_xy, c->d_regions, idx_bytes, cap_w, d_wcounts, d_offsets, nw, c->d_cand,
-                     c->d_cpts, cap, s);
+    launch_kf_gather(d_xy, c->d_regions, idx_bytes, cap_w, d_wcounts, nw, c->d_cnt, c->d_counts,
+                     c->d_cand, c->d_cpts, cap, s);
     const int k1g = k1_list_grid(cap);
     ensure_partials(c, k1g);
-    launch_k1_list(c->d_cpts, cap, c->d_counts, c->d_partials, k1g, c->d_ticket, c->d_rec, s);
-    launch_map_rec(c->d_rec, c->d_cand, idx_bytes, base, s);
-    c->launches += 3;
+    launch_k1_list(c->d_cpts, cap, c->d_counts, c->d_cand, idx_bytes, base, c->d_partials, k1g,
+                   c->d_ticket, c->d_rec, s);
+    c->launches += 2;
     check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
     check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
@@ -480,7 +478,6 @@ bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
     check_cuda(cudaStreamSynchronize(s), "kf + candidate extremes");
   };
   candidates(cap_c);
-  ++c->launches;  // kf_scan
   tr.mark("kf+cand-k1");
   f.sample_coverage = double(c->h_counts[2]) / double(sampled);
   const std::uint64_t n_cand = c->h_counts[0];

@@ -106,18 +106,12 @@ constexpr int kKFWarpsPerBlock = 8;
 void launch_kf(const double* d_xy, std::uint64_t n, const KFRegion& q, int grid, void* d_regions,
                int idx_bytes, std::uint64_t cap_w, std::uint32_t* d_warp_counts,
                const unsigned long long* d_gate, std::uint64_t gate_min, cudaStream_t stream);
-// d_counts[0] = candidates, [1] = 1 if some warp region overflowed, [2] = *d_gate
-void launch_kf_scan(const std::uint32_t* d_warp_counts, std::uint64_t nw, std::uint64_t cap_w,
-                    std::uint64_t* d_offsets, const unsigned long long* d_gate,
-                    unsigned long long* d_counts, cudaStream_t stream);
-// the first cap_c candidates (ordered) and their coordinates
+// the first cap_c candidates (ordered) and their coordinates; d_counts[0] =
+// candidates, [1] = 1 if some warp region overflowed, [2] = *d_gate
 void launch_kf_gather(const double* d_xy, const void* d_regions, int idx_bytes,
-                      std::uint64_t cap_w, const std::uint32_t* d_warp_counts,
-                      const std::uint64_t* d_offsets, std::uint64_t nw, void* d_cand,
-                      double* d_cpts, std::uint64_t cap_c, cudaStream_t stream);
-// K1 record indices of a gathered candidate buffer -> candidate indices + base
-void launch_map_rec(ohx_extremes_rec* d_rec, const void* d_cand, int idx_bytes,
-                    std::uint64_t base, cudaStream_t stream);
+                      std::uint64_t cap_w, const std::uint32_t* d_warp_counts, std::uint64_t nw,
+                      const unsigned long long* d_gate, unsigned long long* d_counts,
+                      void* d_cand, double* d_cpts, std::uint64_t cap_c, cudaStream_t stream);
 // K1 over the provisional region's sample, read in place: `segs` runs of
 // `len` points at evenly spaced offsets, run b belonging to sub-sample
 // b % subs; one record per sub-sample (global indices).  Partials: subs x
@@ -127,8 +121,11 @@ void launch_k1_sample(const double* d_xy, std::uint64_t n, int segs, int len, in
                       cudaStream_t stream);
 // K1 over a short contiguous list (the fused pass's candidates)
 int k1_list_grid(std::uint64_t n);
-// (n capped by *d_n when d_n is set: a length counted on the device)
+// (n capped by *d_n when d_n is set: a length counted on the device; the
+// record's indices are d_map[i] + map_base when d_map is set -- map_bytes 4
+// or 8 -- else positions in the list)
 void launch_k1_list(const double* d_xy, std::uint64_t n, const unsigned long long* d_n,
+                    const void* d_map, int map_bytes, std::uint64_t map_base,
                     K1Partial* partials, int grid, unsigned* ticket, ohx_extremes_rec* d_rec,
                     cudaStream_t stream);
 // points of the sample runs 0, step, 2 step, ... inside Q

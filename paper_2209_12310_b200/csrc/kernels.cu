@@ -484,6 +484,13 @@ __global__ void __launch_bounds__(kK1Block, kK1MinBlocks)
 //            of `len` consecutive points starting at (n - len) * b /
 //            (segs - 1); reported indices are global.
 //   list:    input 0 is pts[0, n).
+// list mode: the published indices are map[i] + base (the fused pass's
+// candidate list maps gathered positions back to point indices)
+struct ListMap {
+  const void* idx;
+  int bytes;  // 4 or 8
+  std::uint64_t base;
+};
 struct SampleMap {
   std::uint64_t n;
   int segs, len, subs;
@@ -512,7 +519,8 @@ __device__ __forceinline__ void k1_visit(ArgState<8, 4, LI>& st, double2 p, LI j
 template <bool kSampled, typename LI>
 __global__ void __launch_bounds__(256)
     k1_small(const double2* __restrict__ pts, std::uint64_t n, const unsigned long long* d_n,
-             const SampleMap sm, K1Partial* partials, unsigned* ticket, ohx_extremes_rec* out) {
+             const SampleMap sm, const ListMap lm, K1Partial* partials, unsigned* ticket,
+             ohx_extremes_rec* out) {
   if (d_n != nullptr && *d_n < n) n = *d_n;  // list length counted on the device
   const int g = blockIdx.y;
   partials += std::uint64_t(g) * gridDim.x;
@@ -573,6 +581,9 @@ __global__ void __launch_bounds__(256)
       }
     const std::uint64_t cnt = kSampled ? std::uint64_t(sm.segs / sm.subs) * sm.len : n;
     const double2 p = cnt ? pts[i] : make_double2(0.0, 0.0);  // an empty list has no winner
+    if (cnt && lm.idx)
+      i = lm.base + (lm.bytes == 4 ? std::uint64_t(static_cast<const std::uint32_t*>(lm.idx)[i])
+                                   : static_cast<const std::uint64_t*>(lm.idx)[i]);
     out->key[a] = k;
     out->idx[a] = i;
     out->x[a] = p.x;
@@ -1025,10 +1036,10 @@ __global__ void __launch_bounds__(kK2cBlock)
 // the eight extremes and the second-best keys are exactly those of the
 // points OUTSIDE Q (the candidates).  KF therefore only streams the points
 // once, tests Q (2 DADD + 8 DSETP per point, the same rounded keys as K1)
-// and appends the candidates' indices to per-warp regions; kf_scan +
-// kf_gather turn those into one ordered candidate list with the candidates'
-// coordinates gathered next to it, K1 runs on the gathered candidates, and after the octagon is known the host checks that Q lies
-// inside it (exact error bounds) and holds no kept point; then every
+// and appends the candidates' indices to per-warp regions; kf_gather turns
+// those into one ordered candidate list with the candidates' coordinates
+// gathered next to it, K1 runs on the gathered candidates, and after the
+// octagon is known the host checks that Q lies inside it (exact error bounds) and holds no kept point; then every
 // dropped point has the reference label 0 and only the candidates need K2
 // (gather mode).  Otherwise the regular K2 pass runs over all points.
 constexpr int kKFBlock = 256;
@@ -1133,88 +1144,70 @@ __global__ void __launch_bounds__(kKFBlock, kKFMinBlocks)
   if ((threadIdx.x & 31) == 0) warp_counts[gw] = c;
 }
 
-// Exclusive scan of the per-warp counts (one block): offsets, the total and
-// whether any region overflowed -> counts[0] = total, counts[1] = overflow,
-// counts[2] = the coverage count KF was gated on.
-constexpr int kScanBlock = 1024;
-__global__ void __launch_bounds__(kScanBlock)
-    kf_scan(const std::uint32_t* __restrict__ warp_counts, std::uint64_t nw, std::uint64_t cap_w,
-            std::uint64_t* __restrict__ offsets, const unsigned long long* gate,
-            unsigned long long* counts) {
-  __shared__ std::uint64_t s_warp[kScanBlock / 32];
-  __shared__ std::uint64_t s_carry;
-  __shared__ int s_over;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    s_carry = 0;
-    s_over = 0;
-  }
-  __syncthreads();
-  for (std::uint64_t base = 0; base < nw; base += kScanBlock) {
-    const std::uint64_t i = base + threadIdx.x;
-    const std::uint64_t v = i < nw ? warp_counts[i] : 0;
-    if (v > cap_w) s_over = 1;
-    std::uint64_t incl = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const std::uint64_t o = __shfl_up_sync(kFull, incl, off);
-      if (lane >= off) incl += o;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      const std::uint64_t w = s_warp[lane];
-      std::uint64_t wi = w;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const std::uint64_t o = __shfl_up_sync(kFull, wi, off);
-        if (lane >= off) wi += o;
-      }
-      s_warp[lane] = wi - w;
-    }
-    __syncthreads();
-    const std::uint64_t carry = s_carry;
-    if (i < nw) offsets[i] = carry + s_warp[warp] + incl - v;
-    __syncthreads();
-    if (threadIdx.x == kScanBlock - 1) s_carry = carry + s_warp[warp] + incl;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    counts[0] = s_carry;
-    counts[1] = s_over;
-    counts[2] = *gate;
-  }
-}
-
 // One warp per KF warp region: copies its candidates to the ordered list
 // and gathers their coordinates (cpts[k] = pts[cand[k]]) for the candidate
-// K1 and the gather-mode K2.
+// K1 and the gather-mode K2.  The list offsets need no scan launch: block b
+// sums the counts of warps [0, 8b) itself (<= 19 KB of L2 reads), and the
+// last block publishes counts[0] = total, counts[1] = whether a region
+// overflowed, counts[2] = the coverage count KF was gated on.
 template <typename IdxT>
 __global__ void __launch_bounds__(256)
     kf_gather(const double2* __restrict__ pts, const IdxT* __restrict__ regions,
               std::uint64_t cap_w, std::uint64_t nw, const std::uint32_t* __restrict__ warp_counts,
-              const std::uint64_t* __restrict__ offsets, IdxT* __restrict__ cand,
-              double2* __restrict__ cpts, std::uint64_t cap_c) {
-  const std::uint64_t w = std::uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  if (w >= nw) return;
-  const std::uint64_t o = offsets[w];
-  if (o >= cap_c) return;
-  const std::uint64_t cnt = min(std::uint64_t(warp_counts[w]), cap_c - o);
+              const unsigned long long* __restrict__ gate, unsigned long long* __restrict__ counts,
+              IdxT* __restrict__ cand, double2* __restrict__ cpts, std::uint64_t cap_c) {
+  __shared__ std::uint64_t s_sum[8];
+  __shared__ std::uint32_t s_max[8], s_own[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const std::uint64_t w0 = std::uint64_t(blockIdx.x) * 8;  // a multiple of 4: uint4 reads
+  std::uint64_t acc = 0;
+  std::uint32_t mx = 0;
+  const auto* c4 = reinterpret_cast<const uint4*>(warp_counts);
+  const std::uint64_t n4 = w0 / 4;
+  for (std::uint64_t i = threadIdx.x; i < n4; i += 256 * 4) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = i + u * 256 < n4 ? c4[i + u * 256] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc += std::uint64_t(v[u].x) + v[u].y + v[u].z + v[u].w;
+      mx = max(mx, max(max(v[u].x, v[u].y), max(v[u].z, v[u].w)));
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    acc += __shfl_xor_sync(kFull, acc, off);
+    mx = max(mx, __shfl_xor_sync(kFull, mx, off));
+  }
+  if (lane == 0) {
+    s_sum[warp] = acc;
+    s_max[warp] = mx;
+    s_own[warp] = w0 + warp < nw ? warp_counts[w0 + warp] : 0;
+  }
+  __syncthreads();
+  std::uint64_t o = 0, total = 0;
+  std::uint32_t over = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    o += s_sum[k] + (k < warp ? s_own[k] : 0);
+    total += s_sum[k] + s_own[k];
+    over = max(over, max(s_max[k], s_own[k]));
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    counts[0] = total;
+    counts[1] = over > cap_w;
+    counts[2] = *gate;
+  }
+  const std::uint64_t w = w0 + warp;
+  if (w >= nw || o >= cap_c) return;
+  const std::uint64_t cnt = min(std::uint64_t(s_own[warp]), cap_c - o);
   const IdxT* r = regions + w * cap_w;
-  for (std::uint64_t k = threadIdx.x & 31; k < cnt; k += 32) {
+  for (std::uint64_t k = lane; k < cnt; k += 32) {
     const IdxT j = r[k];
     cand[o + k] = j;
     cpts[o + k] = ld_stream(pts + j);
   }
-}
-
-// K1's record indices refer to the gathered candidate buffer: map them back
-// to the candidates' (shard-local) indices, + base.
-template <typename IdxT>
-__global__ void map_rec_idx(ohx_extremes_rec* rec, const IdxT* __restrict__ cand,
-                            std::uint64_t base) {
-  const int a = threadIdx.x;
-  if (a < 8 && rec->n > 0) rec->idx[a] = base + static_cast<std::uint64_t>(cand[rec->idx[a]]);
 }
 
 // ====================================================== K1 (TMA variant) ==
@@ -1516,46 +1509,39 @@ void launch_kf(const double* d_xy, std::uint64_t n, const KFRegion& q, int grid,
   check_cuda(cudaGetLastError(), "kf_filter launch");
 }
 
-void launch_kf_scan(const std::uint32_t* d_warp_counts, std::uint64_t nw, std::uint64_t cap_w,
-                    std::uint64_t* d_offsets, const unsigned long long* d_gate,
-                    unsigned long long* d_counts, cudaStream_t stream) {
-  kf_scan<<<1, kScanBlock, 0, stream>>>(d_warp_counts, nw, cap_w, d_offsets, d_gate, d_counts);
-  check_cuda(cudaGetLastError(), "kf_scan launch");
-}
-
 void launch_kf_gather(const double* d_xy, const void* d_regions, int idx_bytes,
-                      std::uint64_t cap_w, const std::uint32_t* d_warp_counts,
-                      const std::uint64_t* d_offsets, std::uint64_t nw, void* d_cand,
-                      double* d_cpts, std::uint64_t cap_c, cudaStream_t stream) {
+                      std::uint64_t cap_w, const std::uint32_t* d_warp_counts, std::uint64_t nw,
+                      const unsigned long long* d_gate, unsigned long long* d_counts,
+                      void* d_cand, double* d_cpts, std::uint64_t cap_c, cudaStream_t stream) {
   const auto* pts = reinterpret_cast<const double2*>(d_xy);
   auto* cp = reinterpret_cast<double2*>(d_cpts);
   const unsigned grid = static_cast<unsigned>((nw + 7) / 8);
   if (idx_bytes == 4)
-    kf_gather<<<grid, 256, 0, stream>>>(
-        pts, static_cast<const std::uint32_t*>(d_regions), cap_w, nw, d_warp_counts, d_offsets,
-        static_cast<std::uint32_t*>(d_cand), cp, cap_c);
+    kf_gather<<<grid, 256, 0, stream>>>(pts, static_cast<const std::uint32_t*>(d_regions), cap_w,
+                                        nw, d_warp_counts, d_gate, d_counts,
+                                        static_cast<std::uint32_t*>(d_cand), cp, cap_c);
   else
-    kf_gather<<<grid, 256, 0, stream>>>(
-        pts, static_cast<const std::uint64_t*>(d_regions), cap_w, nw, d_warp_counts, d_offsets,
-        static_cast<std::uint64_t*>(d_cand), cp, cap_c);
+    kf_gather<<<grid, 256, 0, stream>>>(pts, static_cast<const std::uint64_t*>(d_regions), cap_w,
+                                        nw, d_warp_counts, d_gate, d_counts,
+                                        static_cast<std::uint64_t*>(d_cand), cp, cap_c);
   check_cuda(cudaGetLastError(), "kf_gather launch");
-}
-
-void launch_map_rec(ohx_extremes_rec* d_rec, const void* d_cand, int idx_bytes,
-                    std::uint64_t base, cudaStream_t stream) {
-  if (idx_bytes == 4)
-    map_rec_idx<<<1, 32, 0, stream>>>(d_rec, static_cast<const std::uint32_t*>(d_cand), base);
-  else
-    map_rec_idx<<<1, 32, 0, stream>>>(d_rec, static_cast<const std::uint64_t*>(d_cand), base);
-  check_cuda(cudaGetLastError(), "map_rec_idx launch");
 }
 
 void launch_k1_sample(const double* d_xy, std::uint64_t n, int segs, int len, int subs,
                       K1Partial* partials, unsigned* ticket, ohx_extremes_rec* d_recs,
                       cudaStream_t stream) {
   const SampleMap sm{n, segs, len, subs};
-  k1_small<true, std::uint64_t><<<dim3(segs / subs, subs), 256, 0, stream>>>(
-      reinterpret_cast<const double2*>(d_xy), 0, nullptr, sm, partials, ticket, d_recs);
+  // 4 runs per block (58 -> 52 us at 1e9: fewer partials to combine);
+  // OHX_SAMPLE_RPB overrides (tuning hook)
+  static const int runs_per_block = [] {
+    const char* e = std::getenv("OHX_SAMPLE_RPB");
+    const int k = e ? std::atoi(e) : 0;
+    return k >= 1 ? k : 4;
+  }();
+  const int bx = std::max(1, segs / subs / runs_per_block);
+  k1_small<true, std::uint64_t><<<dim3(bx, subs), 256, 0, stream>>>(
+      reinterpret_cast<const double2*>(d_xy), 0, nullptr, sm, ListMap{nullptr, 0, 0}, partials,
+      ticket, d_recs);
   check_cuda(cudaGetLastError(), "k1_small<sample> launch");
 }
 
@@ -1572,15 +1558,17 @@ int k1_list_grid(std::uint64_t n) {
 }
 
 void launch_k1_list(const double* d_xy, std::uint64_t n, const unsigned long long* d_n,
+                    const void* d_map, int map_bytes, std::uint64_t map_base,
                     K1Partial* partials, int grid, unsigned* ticket, ohx_extremes_rec* d_rec,
                     cudaStream_t stream) {
   const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  const ListMap lm{d_map, map_bytes, map_base};
   if (n < 0xffffffffull)
     k1_small<false, std::uint32_t><<<dim3(grid, 1), 256, 0, stream>>>(
-        pts, n, d_n, SampleMap{0, 1, 1, 1}, partials, ticket, d_rec);
+        pts, n, d_n, SampleMap{0, 1, 1, 1}, lm, partials, ticket, d_rec);
   else
     k1_small<false, std::uint64_t><<<dim3(grid, 1), 256, 0, stream>>>(
-        pts, n, d_n, SampleMap{0, 1, 1, 1}, partials, ticket, d_rec);
+        pts, n, d_n, SampleMap{0, 1, 1, 1}, lm, partials, ticket, d_rec);
   check_cuda(cudaGetLastError(), "k1_small<list> launch");
 }
 
