@@ -753,7 +753,9 @@ struct PieceScan {
   std::size_t best = 0;
 };
 
-PieceScan scan_pieces(const PieceCycle& c) {
+// (dst set: element i is also copied to dst[i] -- the unrotated cycle -- in
+// the same pass)
+PieceScan scan_pieces(const PieceCycle& c, P2* dst = nullptr) {
   PieceScan r;
   const std::size_t m = c.n;
   const P2 c0 = c.at(0), c1 = c.at(1);
@@ -771,6 +773,7 @@ PieceScan scan_pieces(const PieceCycle& c) {
       P2 prev = c.at(b == 0 ? m - 1 : b - 1), cur = bp;
       // cur = element i; the walk delivers i + 1 as `nx`
       auto step = [&](std::size_t i, const P2& nx) {
+        if (dst) dst[i] = cur;
         if (i > 0) du = du || same(prev, cur);
         if (i >= 2) fl = fl && orient(c0, c1, cur) == 0;
         ba = ba || orient(prev, cur, nx) <= 0;
@@ -915,16 +918,27 @@ std::size_t hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t l
   const double t1 = now_ms();
   std::size_t h = 0;
   // fast path: no duplicates, no non-strict turn, not flat (the clean-up
-  // keeps every vertex): the hull is the cycle rotated to its start
-  // vertex, copied once, straight from the chain stacks to the output
+  // keeps every vertex): the hull is the cycle rotated to its start vertex.
+  // The checking scan also copies the cycle to the output (one pass over
+  // the chain stacks instead of two); the start is nearly always the first
+  // vertex (the east anchor), else the rotated copy is redone.
   bool done = false;
   if (pc.n > 2 && !same(pc.at(0), pc.at(pc.n - 1))) {
-    const PieceScan sc = scan_pieces(pc);
+    P2* out = nullptr;
+    try {
+      out = sink(pc.n);
+    } catch (...) {  // no room for the whole cycle: check first, the hull may be smaller
+      out = nullptr;
+    }
+    const PieceScan sc = scan_pieces(pc, out);
+    if (trace_on()) std::fprintf(stderr, "[ohx]   piece scan + copy %.3f ms\n", now_ms() - t1);
     if (!sc.dups && !sc.flat && !sc.bad) {
       h = pc.n;
-      P2* out = sink(h);
-      pc.copy_out_parallel(out, sc.best, pc.n);
-      pc.copy_out_parallel(out + (pc.n - sc.best), 0, sc.best);
+      if (!out || sc.best != 0) {
+        if (!out) out = sink(h);
+        pc.copy_out_parallel(out, sc.best, pc.n);
+        pc.copy_out_parallel(out + (pc.n - sc.best), 0, sc.best);
+      }
       done = true;
     }
   }

@@ -239,8 +239,9 @@ void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const doub
 // arc: the arcs may still be arriving from the device)
 PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
                            const std::function<void(int)>& wait_arc = {});
-// Same, the hull written to sink(h) (called once with the hull size; it
-// returns where the h vertices go and may throw); returns h.
+// Same, the hull written to sink(h) (it returns where h vertices go and may
+// throw; it may first be called with a larger size -- the chained cycle
+// before its clean-up -- the last call's size is the hull's); returns h.
 using HullSink = std::function<P2*(std::size_t)>;
 std::size_t hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
                                   const std::function<void(int)>& wait_arc, const HullSink& sink);

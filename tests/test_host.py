@@ -363,7 +363,7 @@ def sweep_sorted(a, q):  # the reference comparator's order (hull.cpp:18-30)
     keys = {1: (y, -x), 2: (-x, -y), 3: (-y, x), 4: (x, y)}[q]
     return np.ascontiguousarray(a[np.lexsort(keys)])
 
-def lib_hull(pts):
+def lib_hull(pts, cap=None, rc_want=0):
     ext = o.find_extremes(pts)
     lab = o.classify(pts)
     anchors = pts[ext[:4].astype(np.int64)]
@@ -374,7 +374,12 @@ def lib_hull(pts):
     ptrs = (dp * 4)(*[a.ctypes.data_as(dp) for a in arcs])
     lens = (C.c_uint64 * 4)(*[len(a) for a in arcs])
     out = np.empty((sum(len(a) for a in arcs) + 8, 2)); h = C.c_uint64()
-    P.check(P.lib.ohx_hull_from_sorted_arcs(ptrs, lens, out.ctypes.data_as(dp), len(out), C.byref(h)))
+    rc = P.lib.ohx_hull_from_sorted_arcs(ptrs, lens, out.ctypes.data_as(dp),
+                                         len(out) if cap is None else cap, C.byref(h))
+    if rc_want:
+        assert rc == rc_want, rc
+        return h.value
+    P.check(rc)
     return out[: h.value]
 
 rng = np.random.default_rng(9)
@@ -383,8 +388,18 @@ cases = [o.generate("circle", 200_000, 3, 0.0), o.generate("circle", 150_000, 4,
 t = rng.uniform(0, 2 * np.pi, 120_000)
 cases.append(np.round(np.stack([np.cos(t), np.sin(t)], 1) * 300.0))      # duplicates, ties
 cases.append(rng.integers(-9, 10, size=(50_000, 2)).astype(float))       # degenerate grid
+d = o.generate("disk", 50_000, 8, 0.0) * 900.0   # two east-most points: the start vertex is
+d[0], d[5] = (1e3, 1.0), (1e3, -1.0)              # not the east anchor (smallest index)
+cases.append(d)
 bad = sum(not np.array_equal(lib_hull(np.ascontiguousarray(a)), o.heaphull(np.ascontiguousarray(a)))
           for a in cases)
+# the output buffer sized to the hull exactly (smaller than the chained
+# cycle when the clean-up drops vertices), and one vertex short
+for a in cases:
+    a = np.ascontiguousarray(a)
+    want = o.heaphull(a)
+    bad += not np.array_equal(lib_hull(a, cap=len(want)), want)
+    bad += lib_hull(a, cap=len(want) - 1, rc_want=P.OHX_E_INVALID) != len(want)
 print("arcs ok" if bad == 0 else f"{bad} mismatches")
 """
 
