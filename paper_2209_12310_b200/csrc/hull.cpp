@@ -166,11 +166,11 @@ inline std::uint64_t asc_key(double v) {
 }
 
 // Sweep sort of a mid-sized arc: LSD radix sort (11-bit digits, digits all
-// keys share skipped) on the primary key, then runs of equal primary key
-// sorted by the comparator (rare: equal coordinates).  Linear passes
-// instead of ~n log n mispredicted comparisons (~50 ns per point on the
-// box's host for random arcs).  Equal points may come out in any order, as
-// with std::sort.
+// keys share skipped) on the top 33 bits of the primary key, then runs of
+// equal top bits sorted by the comparator (rare for arcs of < 2^17 points:
+// equal or nearly equal coordinates).  Three linear passes instead of ~n
+// log n mispredicted comparisons (~50 ns per point on the box's host for
+// random arcs).  Equal points may come out in any order, as with std::sort.
 template <int Q>
 void radix_sweep_sort(std::vector<P2>& pts) {
   struct E {
@@ -187,7 +187,8 @@ void radix_sweep_sort(std::vector<P2>& pts) {
   }
   constexpr int kBits = 11, kBuckets = 1 << kBits;
   std::vector<std::uint32_t> cnt(kBuckets + 1);
-  for (int shift = 0; shift < 64; shift += kBits) {
+  constexpr int kLow = 64 - 3 * kBits;  // bits below are left to the fix-up
+  for (int shift = kLow; shift < 64; shift += kBits) {
     auto digit = [&](const E& e) { return static_cast<std::uint32_t>((e.k >> shift) & (kBuckets - 1)); };
     std::fill(cnt.begin(), cnt.end(), 0u);
     for (const E& e : a) ++cnt[digit(e) + 1];
@@ -198,9 +199,9 @@ void radix_sweep_sort(std::vector<P2>& pts) {
   }
   std::vector<P2> out(n);
   for (std::size_t i = 0; i < n; ++i) out[i] = pts[a[i].i];
-  for (std::size_t r = 0; r < n;) {  // equal primary keys: secondary order
+  for (std::size_t r = 0; r < n;) {  // equal top bits: the comparator's order
     std::size_t e = r + 1;
-    while (e < n && a[e].k == a[r].k) ++e;
+    while (e < n && (a[e].k >> kLow) == (a[r].k >> kLow)) ++e;
     if (e - r > 1) std::sort(out.begin() + r, out.begin() + e, SweepLess<Q>{});
     r = e;
   }

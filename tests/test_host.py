@@ -111,6 +111,10 @@ def test_host_hull_large_degenerate_sets(oracle):
         cases.append(rng.integers(-g, g + 1, size=(20_000, 2)).astype(float) * 0.5)
     t2 = rng.uniform(0, 2 * np.pi, 30_000)
     cases.append(np.round(np.stack([np.cos(t2), np.sin(t2)], 1) * 400.0))
+    # coordinates that differ only below the radix passes' top 33 key bits
+    # (the comparator orders those runs)
+    cases.append(1.0 + rng.integers(0, 3000, size=(20_000, 2)) * 2.0 ** -40)
+    cases.append(-1.0 - rng.uniform(0, 2.0 ** -25, size=(20_000, 2)))
     for a in cases:
         a = np.ascontiguousarray(a)
         assert np.array_equal(hull_via_library(oracle, a), oracle.heaphull(a))
