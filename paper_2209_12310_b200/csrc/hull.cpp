@@ -32,6 +32,7 @@
 #include <string>
 #include <functional>
 #include <memory>
+#include <condition_variable>
 #include <mutex>
 #include <new>
 #include <thread>
@@ -968,6 +969,68 @@ PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
   return out;
 }
 
+// Three persistent workers for the arcs 1..3 of hull_from_queue_points
+// (the caller runs arc 0): starting threads per call cost more than the
+// sorts of a few thousand points, and the workers keep warm heaps.  One
+// job at a time (calls from several host threads queue on the mutex).
+class ArcWorkers {
+ public:
+  static ArcWorkers& get() {
+    static ArcWorkers w;
+    return w;
+  }
+  void run4(const std::function<void(int)>& f) {
+    std::lock_guard<std::mutex> call(call_);
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      job_ = &f;
+      left_ = 3;
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [&] { return left_ == 0; });
+    job_ = nullptr;
+  }
+  ~ArcWorkers() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+
+ private:
+  ArcWorkers() {
+    for (int k = 1; k <= 3; ++k) th_.emplace_back([this, k] { loop(k); });
+  }
+  void loop(int k) {
+    std::uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        f = job_;
+      }
+      (*f)(k);
+      std::lock_guard<std::mutex> lk(m_);
+      if (--left_ == 0) done_.notify_one();
+    }
+  }
+  std::mutex call_, m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int left_ = 0;
+  std::uint64_t gen_ = 0;
+  bool stop_ = false;
+  std::vector<std::thread> th_;
+};
+
 PVec hull_from_queue_points(const P2 anchors[4], const P2* const q_pts[4],
                             const std::uint64_t q_len[4]) {
   // reference hull.cpp:164-183: arc q runs from anchor q-1 (entry) to
@@ -983,9 +1046,8 @@ PVec hull_from_queue_points(const P2 anchors[4], const P2* const q_pts[4],
   };
   const std::uint64_t total = q_len[0] + q_len[1] + q_len[2] + q_len[3];
   if (total >= (1u << 12)) {  // one thread per arc
-    std::vector<std::thread> th;
-    for (int q = 0; q < 4; ++q) th.emplace_back(arc, q);
-    for (auto& t : th) t.join();
+    const std::function<void(int)> job = arc;
+    ArcWorkers::get().run4(job);
   } else {
     for (int q = 0; q < 4; ++q) arc(q);
   }
