@@ -20,6 +20,7 @@
 //    test cannot change (see peel).
 #include <omp.h>
 #include <sys/mman.h>
+#include <unistd.h>
 
 #include <parallel/algorithm>
 
@@ -30,6 +31,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <exception>
 #include <functional>
 #include <memory>
 #include <condition_variable>
@@ -976,10 +978,16 @@ PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
 class ArcWorkers {
  public:
   static ArcWorkers& get() {
-    static ArcWorkers w;
-    return w;
+    // never destroyed: the workers wait until process exit ends them (no
+    // join at exit; a forked child's copy holds threads it does not have)
+    static ArcWorkers* w = new ArcWorkers;
+    return *w;
   }
   void run4(const std::function<void(int)>& f) {
+    if (getpid() != pid_) {  // a forked child: the workers did not survive the fork
+      for (int q = 0; q < 4; ++q) f(q);
+      return;
+    }
     std::lock_guard<std::mutex> call(call_);
     {
       std::lock_guard<std::mutex> lk(m_);
@@ -988,22 +996,22 @@ class ArcWorkers {
       ++gen_;
     }
     cv_.notify_all();
-    f(0);
-    std::unique_lock<std::mutex> lk(m_);
-    done_.wait(lk, [&] { return left_ == 0; });
-    job_ = nullptr;
-  }
-  ~ArcWorkers() {
-    {
-      std::lock_guard<std::mutex> lk(m_);
-      stop_ = true;
+    std::exception_ptr mine;
+    try {
+      f(0);
+    } catch (...) {
+      mine = std::current_exception();
     }
-    cv_.notify_all();
-    for (auto& t : th_) t.join();
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [&] { return left_ == 0; });  // the workers hold f: always wait
+    job_ = nullptr;
+    std::exception_ptr e = mine ? mine : err_;
+    err_ = nullptr;
+    if (e) std::rethrow_exception(e);
   }
 
  private:
-  ArcWorkers() {
+  ArcWorkers() : pid_(getpid()) {
     for (int k = 1; k <= 3; ++k) th_.emplace_back([this, k] { loop(k); });
   }
   void loop(int k) {
@@ -1012,22 +1020,28 @@ class ArcWorkers {
       const std::function<void(int)>* f;
       {
         std::unique_lock<std::mutex> lk(m_);
-        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
-        if (stop_) return;
+        cv_.wait(lk, [&] { return gen_ != seen; });
         seen = gen_;
         f = job_;
       }
-      (*f)(k);
+      std::exception_ptr e;
+      try {
+        (*f)(k);
+      } catch (...) {
+        e = std::current_exception();
+      }
       std::lock_guard<std::mutex> lk(m_);
+      if (e && !err_) err_ = e;
       if (--left_ == 0) done_.notify_one();
     }
   }
+  const pid_t pid_;
   std::mutex call_, m_;
   std::condition_variable cv_, done_;
   const std::function<void(int)>* job_ = nullptr;
+  std::exception_ptr err_;
   int left_ = 0;
   std::uint64_t gen_ = 0;
-  bool stop_ = false;
   std::vector<std::thread> th_;
 };
 

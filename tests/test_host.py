@@ -419,3 +419,32 @@ def test_hull_from_sorted_arcs_matches_oracle(par_min, chunks):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=900)
     assert r.returncode == 0 and "arcs ok" in r.stdout, r.stdout + r.stderr[-3000:]
+
+
+def test_host_hull_workers_survive_fork(oracle):
+    # the arc workers are process-local: a forked child runs the arcs itself
+    # (no hang waiting for threads it does not have), with the same result
+    import subprocess
+    import sys
+    code = (
+        "import os, sys, numpy as np\n"
+        f"sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {ROOT!r} + '/tests')\n"
+        "import paper_2209_12310_b200 as P\n"
+        "from oracle import Oracle\n"
+        "o = Oracle()\n"
+        "pts = o.generate('disk', 400_000, 5, 0.0)\n"
+        "ext = o.find_extremes(pts); lab = o.classify(pts)\n"
+        "anchors = pts[ext[:4].astype(np.int64)]\n"
+        "queues = [pts[np.flatnonzero(lab == q)] for q in (1, 2, 3, 4)]\n"
+        "assert sum(len(q) for q in queues) >= 4096\n"
+        "want = P.hull_from_queue_points(anchors, queues)\n"
+        "pid = os.fork()\n"
+        "if pid == 0:\n"
+        "    got = P.hull_from_queue_points(anchors, queues)\n"
+        "    os._exit(0 if np.array_equal(got, want) else 3)\n"
+        "_, st = os.waitpid(pid, 0)\n"
+        "assert os.WEXITSTATUS(st) == 0, st\n"
+        "assert np.array_equal(P.hull_from_queue_points(anchors, queues), want)\n"
+        "print('fork ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "fork ok" in r.stdout, r.stdout + r.stderr[-3000:]
