@@ -182,7 +182,7 @@ std::uint64_t load_pts2_device(ohx_ctx* c, const std::string& path, double* d_xy
     if (k >= ohx_ctx::kStageBufs)
       check_cuda(cudaEventSynchronize(c->stage_ev[b]), "cudaEventSynchronize(staging)");
     char* dst = static_cast<char*>(c->h_stage[b]);
-#pragma omp parallel num_threads(len >= (16u << 20) ? 8 : 1) reduction(&& : ok)
+#pragma omp parallel num_threads(team(len >= (16u << 20) ? 8 : 1)) reduction(&& : ok)
     {
       const int t = omp_get_thread_num(), nt = omp_get_num_threads();
       std::uint64_t p = len * t / nt, e = len * (t + 1) / nt;

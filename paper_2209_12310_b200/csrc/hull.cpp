@@ -19,6 +19,7 @@
 //    reference's LIFO worklist exactly while skipping the vertices whose
 //    test cannot change (see peel).
 #include <omp.h>
+#include <pthread.h>
 #include <sys/mman.h>
 #include <unistd.h>
 
@@ -109,6 +110,17 @@ void big_free(void* p, std::size_t bytes) noexcept {
   }
   std::free(p);
 }
+
+namespace {
+bool g_forked = false;
+void on_fork_child() {
+  g_forked = true;
+  omp_set_num_threads(1);
+}
+[[maybe_unused]] const int g_atfork = pthread_atfork(nullptr, nullptr, on_fork_child);
+}  // namespace
+
+int team(int want) { return g_forked || want < 1 ? 1 : want; }
 
 int orient(const P2& a, const P2& b, const P2& c) {
   // reference geometry.hpp:27-32

@@ -18,6 +18,11 @@
 
 namespace ohx {
 
+// Host worker teams for OpenMP regions: `want` threads, 1 in a forked child
+// (the parent's OpenMP pool does not survive a fork; a child that used it
+// would hang).  A fork handler also sets the child's default team to 1.
+int team(int want);
+
 // ---- kernel-side plan (K2): the C-ABI plan with shard-local kept indices
 struct KPlan {
   double ax[8], ay[8], ea[8], ec[8];

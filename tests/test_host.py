@@ -422,8 +422,9 @@ def test_hull_from_sorted_arcs_matches_oracle(par_min, chunks):
 
 
 def test_host_hull_workers_survive_fork(oracle):
-    # the arc workers are process-local: a forked child runs the arcs itself
-    # (no hang waiting for threads it does not have), with the same result
+    # the arc workers and the OpenMP pool are process-local: a forked child
+    # runs single-threaded (no hang waiting for threads it does not have),
+    # with the same results
     import subprocess
     import sys
     code = (
@@ -438,10 +439,14 @@ def test_host_hull_workers_survive_fork(oracle):
         "queues = [pts[np.flatnonzero(lab == q)] for q in (1, 2, 3, 4)]\n"
         "assert sum(len(q) for q in queues) >= 4096\n"
         "want = P.hull_from_queue_points(anchors, queues)\n"
+        "t = np.random.default_rng(1).uniform(0, 2 * np.pi, 600_000)\n"
+        "circ = np.ascontiguousarray(np.stack([np.cos(t), np.sin(t)], 1))\n"
+        "mc = P.monotone_chain(circ)  # parallel sort + OpenMP clean-up in the parent\n"
         "pid = os.fork()\n"
         "if pid == 0:\n"
         "    got = P.hull_from_queue_points(anchors, queues)\n"
-        "    os._exit(0 if np.array_equal(got, want) else 3)\n"
+        "    ok = np.array_equal(got, want) and np.array_equal(P.monotone_chain(circ), mc)\n"
+        "    os._exit(0 if ok else 3)\n"
         "_, st = os.waitpid(pid, 0)\n"
         "assert os.WEXITSTATUS(st) == 0, st\n"
         "assert np.array_equal(P.hull_from_queue_points(anchors, queues), want)\n"
