@@ -287,7 +287,8 @@ void destroy_ctx(ohx_ctx* c) {
                   c->d_regions, static_cast<void*>(c->d_cpts), c->d_hsort})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_crec),
-                  static_cast<void*>(c->h_counts), static_cast<void*>(c->h_cnt), c->h_sorted})
+                  static_cast<void*>(c->h_counts), static_cast<void*>(c->h_cnt), c->h_sorted,
+                  static_cast<void*>(c->h_spec)})
     if (p) cudaFreeHost(p);
   for (int b = 0; b < ohx_ctx::kStageBufs; ++b) {
     if (c->h_stage[b]) cudaFreeHost(c->h_stage[b]);
@@ -334,6 +335,7 @@ void trim_ctx(ohx_ctx* c) {
   }
   c->fz.active = false;
   c->last_n = 0;
+  c->spec_n = ~0ull;
   big_cache_trim();
 }
 

@@ -88,6 +88,7 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
   const KPlan kp = make_kplan(plan, base, n);
   const std::uint64_t items = d_cand ? n_cand : n;
   const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
+  c->spec_n = ~0ull;
   if (items == 0) {  // no candidates at all
     for (int q = 0; q < 4; ++q) counts[q] = 0;
   } else {
@@ -109,15 +110,29 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
       check_cuda(cudaEventRecord(c->ev[2][1], s), "cudaEventRecord");
       c->timed[2] = true;
       c->launches += 2;
+      // the first survivors' coordinates ride along with the counts: a
+      // small survivor set needs no second round trip (queues_fetch_xy)
+      constexpr std::uint64_t kSpec = ohx_ctx::kSpecSurvivors;
+      dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, kSpec * 16, "gather");
+      host_grow(reinterpret_cast<void**>(&c->h_spec), &c->spec_bytes, kSpec * 16,
+                "cudaMallocHost(survivors)");
+      launch_gather4_dev(d_xy, c->d_queues, idx_bytes, cap, c->d_counts, kSpec, c->d_gather, s);
+      ++c->launches;
       check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
+      check_cuda(cudaMemcpyAsync(c->h_spec, c->d_gather, kSpec * 16, cudaMemcpyDeviceToHost, s),
+                 "cudaMemcpyAsync(survivors)");
       check_cuda(cudaStreamSynchronize(s), "k2_filter");
-      std::uint64_t mx = 0;
+      std::uint64_t mx = 0, total = 0;
       for (int q = 0; q < 4; ++q) {
         counts[q] = c->h_counts[q];
         mx = std::max<std::uint64_t>(mx, counts[q]);
+        total += counts[q];
       }
-      if (mx <= cap) break;
+      if (mx <= cap) {
+        if (total <= kSpec) c->spec_n = total;
+        break;
+      }
       if (attempt == 1) throw Error(OHX_E_INTERNAL, "k2_filter: queue overflow after regrow");
       cap = std::min<std::uint64_t>(items, mx + mx / 8 + 1024);
     }
@@ -176,6 +191,10 @@ void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s) {
   const std::uint64_t total =
       c->last_counts[0] + c->last_counts[1] + c->last_counts[2] + c->last_counts[3];
   if (total == 0) return;
+  if (c->spec_n == total) {  // already fetched with the counts
+    std::memcpy(h_xy, c->h_spec, total * 16);
+    return;
+  }
   dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, total * 16, "gather");
   launch_gather4(c->last_xy, c->d_queues, c->last_idx_bytes, c->last_cap, c->last_counts,
                  c->d_gather, s);

@@ -55,6 +55,12 @@ struct ohx_ctx {
   std::uint64_t labels_bytes = 0;
   double* d_gather = nullptr;
   std::uint64_t gather_bytes = 0;
+  // the first survivors' coordinates, fetched with the K2 counts (pinned):
+  // valid for the last filter when spec_n != ~0 (how many are there)
+  static constexpr std::uint64_t kSpecSurvivors = 4096;
+  double* h_spec = nullptr;
+  std::uint64_t spec_bytes = 0;
+  std::uint64_t spec_n = ~0ull;
 
   // fused single-pass mode: sample, candidate list, coverage counter
   double* d_sample = nullptr;

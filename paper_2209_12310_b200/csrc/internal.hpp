@@ -144,6 +144,10 @@ void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
                     cudaStream_t stream);
 void launch_gather(const double* d_xy, const void* d_idx, int idx_bytes,
                    std::uint64_t count, double* d_out, cudaStream_t stream);
+// the first `limit` survivors' coordinates with the counts read on the device
+void launch_gather4_dev(const double* d_xy, const void* d_queues, int idx_bytes,
+                        std::uint64_t cap, const unsigned long long* d_counts,
+                        std::uint64_t limit, double* d_out, cudaStream_t stream);
 
 // ---- host helpers (capi.cpp)
 struct Error : std::runtime_error {

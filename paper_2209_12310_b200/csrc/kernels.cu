@@ -1356,6 +1356,26 @@ __global__ void gather_xy4(const double2* __restrict__ pts, const IdxT* __restri
   }
 }
 
+// The same with the counts read on the device, for the first `limit`
+// survivors: launched right behind K2 so that a small survivor set comes
+// back with the counts, in the same round trip.  Nothing is written when a
+// queue overflowed its capacity (the host re-runs K2 then).
+template <typename IdxT>
+__global__ void gather_xy4_dev(const double2* __restrict__ pts, const IdxT* __restrict__ queues,
+                               std::uint64_t cap, const unsigned long long* __restrict__ counts,
+                               std::uint64_t limit, double2* __restrict__ out) {
+  const std::uint64_t c0 = counts[0], c1 = counts[1], c2 = counts[2], c3 = counts[3];
+  if (c0 > cap || c1 > cap || c2 > cap || c3 > cap) return;
+  const ulonglong4 ends = make_ulonglong4(c0, c0 + c1, c0 + c1 + c2, c0 + c1 + c2 + c3);
+  const std::uint64_t total = ends.w < limit ? ends.w : limit;
+  for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += std::uint64_t(gridDim.x) * blockDim.x) {
+    const int q = (k >= ends.x) + (k >= ends.y) + (k >= ends.z);
+    const std::uint64_t start = q == 0 ? 0 : (q == 1 ? ends.x : (q == 2 ? ends.y : ends.z));
+    out[k] = pts[queues[std::uint64_t(q) * cap + (k - start)]];
+  }
+}
+
 }  // namespace
 
 // ============================================================ launchers ==
@@ -1604,6 +1624,22 @@ void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
     gather_xy4<<<grid, 256, 0, stream>>>(pts, static_cast<const std::uint64_t*>(d_queues), cap,
                                          ends, reinterpret_cast<double2*>(d_out));
   check_cuda(cudaGetLastError(), "gather_xy4 launch");
+}
+
+void launch_gather4_dev(const double* d_xy, const void* d_queues, int idx_bytes,
+                        std::uint64_t cap, const unsigned long long* d_counts,
+                        std::uint64_t limit, double* d_out, cudaStream_t stream) {
+  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  const unsigned grid = static_cast<unsigned>((limit + 255) / 256);
+  if (idx_bytes == 4)
+    gather_xy4_dev<<<grid, 256, 0, stream>>>(pts, static_cast<const std::uint32_t*>(d_queues),
+                                             cap, d_counts, limit,
+                                             reinterpret_cast<double2*>(d_out));
+  else
+    gather_xy4_dev<<<grid, 256, 0, stream>>>(pts, static_cast<const std::uint64_t*>(d_queues),
+                                             cap, d_counts, limit,
+                                             reinterpret_cast<double2*>(d_out));
+  check_cuda(cudaGetLastError(), "gather_xy4_dev launch");
 }
 
 void launch_gather(const double* d_xy, const void* d_idx, int idx_bytes,
