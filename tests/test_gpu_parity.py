@@ -521,3 +521,23 @@ def test_trim_releases_and_regrows(oracle):
     h2, _ = c.heaphull_device(d, len(pts))
     assert np.array_equal(h1, h2) and np.array_equal(h1, oracle.heaphull(pts))
     c.close()
+
+
+@pytest.mark.parametrize("scale,offset", [(1e300, 0.0), (1e-300, 0.0), (1e-310, 0.0),
+                                          (1.0, 1e15), (3e-9, -7.0)])
+@pytest.mark.parametrize("n", [1_000_003, 9_000_000])
+def test_extreme_magnitudes_match_oracle(ctx, oracle, scale, offset, n):
+    # x + y overflowing to +-inf (1e300), subnormal coordinates (1e-300,
+    # 1e-310), and points whose spread is a few ulps of their offset (ties
+    # galore): the fused pass's region, its certification and the two-pass
+    # path must still give the reference's results bit for bit
+    pts = np.ascontiguousarray(P.generate("normal", n, 11) * scale + offset)
+    assert np.isfinite(pts).all()
+    hull, _ = ctx.heaphull_device(dev(pts), n)
+    info = ctx.last_run()
+    want_hull, want_labels = oracle.heaphull(pts, with_labels=True)
+    assert np.array_equal(hull, want_hull), info
+    assert info["counts"] == [int((want_labels == q).sum()) for q in (1, 2, 3, 4)], info
+    for q in range(4):
+        idx, _ = ctx.queue(q + 1, info["counts"][q])
+        assert np.array_equal(idx, np.flatnonzero(want_labels == q + 1)), q
