@@ -342,7 +342,7 @@ int coverage_step(int segs) {  // OHX_COVERAGE_STEP overrides (tuning hook)
   }();
   return v >= 1 ? v : std::max(1, segs / kCoverageRuns);
 }
-constexpr int kSampleMaxSegs = 1024;  // runs (8M points, 128 MB) for n >= 2^27
+constexpr int kSampleMaxSegs = 512;  // runs (4M points, 64 MB) for n >= 2^26
 // OHX_SAMPLE_SEGS overrides the cap (experiment switch)
 int sample_max_segs() {
   static const int v = [] {
@@ -352,10 +352,23 @@ int sample_max_segs() {
   }();
   return v;
 }
-constexpr int kSubSamples = 8;  // disjoint sub-samples of kSampleSegs / 8 runs each
+// Four disjoint sub-samples (tools/sample_config_sweep.py, normal 1e9 over
+// seeds: 8 x 128 runs -> 1.19M candidates, 2.570 ms; 4 x 128 -> 0.68M,
+// 2.521 ms; 3 -> 0.61M, 2.510 ms; 2 sub-samples left a 30M-point region
+// uncertified once -- fewer octagons to intersect, a larger but riskier Q).
+constexpr int kMaxSubSamples = 8;
+constexpr int kSubSamples = 4;
+int sub_samples() {  // OHX_SUBSAMPLES overrides (2..8; tuning hook)
+  static const int v = [] {
+    const char* e = std::getenv("OHX_SUBSAMPLES");
+    const int k = e ? std::atoi(e) : 0;
+    return k >= 2 && k <= kMaxSubSamples ? k : kSubSamples;
+  }();
+  return v;
+}
 constexpr double kFuseMinCoverage = 0.8;
 // The provisional region of the fused pass.  A sample of about n/16 points
-// (up to 8M: runs of kSampleLen consecutive points at evenly spaced offsets,
+// (up to 4M: runs of kSampleLen consecutive points at evenly spaced offsets,
 // read in place) is split into kSubSamples disjoint sub-samples (run b goes
 // to sub-sample b % kSubSamples, so each spans the whole index range); each
 // one's eight extremes (one batched launch) give an octagon, and Q is fitted
@@ -371,16 +384,17 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
                         std::uint64_t* sampled, cudaStream_t s, FilterOut& f, Trace& tr) {
   if (n < kFuseMinPoints || fuse_mode() == 0) return false;
   f.fuse_state = 2;
-  // about n/16 sampled points, 64..1024 runs, a multiple of kSubSamples
+  // about n/16 sampled points, 64..1024 runs, a multiple of the sub-samples
+  const int subs = sub_samples();
   const int segs = static_cast<int>(std::clamp<std::uint64_t>(
-                       n / (16ull * kSampleLen), 64, sample_max_segs())) / kSubSamples * kSubSamples;
+                       n / (16ull * kSampleLen), 64, sample_max_segs())) / subs * subs;
   dev_grow(reinterpret_cast<void**>(&c->d_sample), &c->sample_bytes,
-           kSubSamples * sizeof(ohx_extremes_rec), "sample records");
+           kMaxSubSamples * sizeof(ohx_extremes_rec), "sample records");
   auto* d_recs = reinterpret_cast<ohx_extremes_rec*>(c->d_sample);
   ensure_partials(c, segs);
-  launch_k1_sample(d_xy, n, segs, kSampleLen, kSubSamples, c->d_partials, c->d_ticket, d_recs, s);
+  launch_k1_sample(d_xy, n, segs, kSampleLen, subs, c->d_partials, c->d_ticket, d_recs, s);
   ++c->launches;
-  ohx_extremes_rec rs[kSubSamples];
+  ohx_extremes_rec rs[kMaxSubSamples];
   check_cuda(cudaMemcpyAsync(rs, d_recs, sizeof(rs), cudaMemcpyDeviceToHost, s),
              "cudaMemcpyAsync(sample recs)");
   check_cuda(cudaStreamSynchronize(s), "sample extremes");
@@ -390,7 +404,7 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   std::vector<P2> region, clipped;
   region.reserve(64);
   clipped.reserve(64);
-  for (int g = 0; g < kSubSamples; ++g) {
+  for (int g = 0; g < subs; ++g) {
     ohx_extreme_set es;
     resolve_extremes(rs[g], &es);  // heuristic octagons: diagonal winners need no certificate
     double cand[16], oct[16];
@@ -413,7 +427,7 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   }
   // the whole sample's best (axis) / second (diagonal) keys
   ohx_extremes_rec all;
-  combine_extremes(rs, kSubSamples, &all);
+  combine_extremes(rs, subs, &all);
   double lim[8];
   for (int a = 0; a < 8; ++a) lim[a] = a < 4 ? all.key[a] : all.second[a - 4];
   if (!fit_region(region, lim, q)) return false;
