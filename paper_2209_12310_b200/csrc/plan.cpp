@@ -573,9 +573,15 @@ bool fit_region(const std::vector<P2>& R, const double lim[8], KFRegion* q) {
     }
     b[a] = good;
   }
+  // pulled 0.2 % towards the centre (OHX_REGION_PULL overrides; tuning hook)
+  static const double keep = [] {
+    const char* e = std::getenv("OHX_REGION_PULL");
+    const double p = e ? std::atof(e) : -1.0;
+    return p >= 0.0 && p < 0.5 ? 1.0 - p : 0.998;
+  }();
   double r[8];
   for (int a = 0; a < 8; ++a) {
-    r[a] = c0[a] + 0.998 * (b[a] - c0[a]);
+    r[a] = c0[a] + keep * (b[a] - c0[a]);
     const double below = std::nextafter(lim[a], -INFINITY);
     if (r[a] > below) r[a] = below;
   }

@@ -14,7 +14,8 @@ import torch  # noqa: E402
 import paper_2209_12310_b200 as P  # noqa: E402
 
 ctx = P.Context(0)
-tag = f"subs={os.environ.get('OHX_SUBSAMPLES', '8')} segs={os.environ.get('OHX_SAMPLE_SEGS', '1024')}"
+tag = (f"subs={os.environ.get('OHX_SUBSAMPLES', 'default')} "
+       f"segs={os.environ.get('OHX_SAMPLE_SEGS', 'default')} pull={os.environ.get('OHX_REGION_PULL', 'default')}")
 for dist, n, seeds in [("normal", 30_000_000, range(6)), ("normal", 100_000_000, range(6)),
                        ("square", 100_000_000, range(3)), ("normal", 1_000_000_000, range(3))]:
     d = torch.empty((n, 2), dtype=torch.float64, device="cuda")
