@@ -53,6 +53,13 @@ UNIT = "Gpoints/s"
 WORKLOAD = "normal-distribution 2D points, 1e9 per GPU (BASELINE configs[2]; C5 shape at N>1)"
 
 
+def workload(dist: str, n: int) -> str:
+    """The workload name: BASELINE configs[2] at its defaults, else what ran."""
+    if dist == "normal" and n == 1_000_000_000:
+        return WORKLOAD
+    return f"{dist}-distribution 2D points, {n:.3g} per GPU (BASELINE configs[2] shape)"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -197,14 +204,15 @@ def run_reference_arm(a):
     ms = 1e3 * sum(timed) / len(timed)
     value = n / (ms * 1e-3) / 1e9
     sample = (f"{a.dist} n={n} seed={a.seed} ("
-              + ("the full per-GPU workload" if n == int(a.n) else f"bounded sample of the {WORKLOAD} workload")
+              + ("the full per-GPU workload" if n == int(a.n)
+                 else f"bounded sample of the {workload(a.dist, int(a.n))} workload")
               + "), full heaphull_run")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator, seed 7)",
-        "config": {"workload": WORKLOAD, "dist": a.dist, "sample_points": n,
+        "config": {"workload": workload(a.dist, int(a.n)), "dist": a.dist, "sample_points": n,
                    "parallelism": f"ReduceEngine({{32, {r['cores']}}}) host lanes"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
                          "sample": sample},
@@ -466,9 +474,10 @@ def run_b200_arm(a):
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic: reference generator ({a.dist}, seed {a.seed}+rank), bit-identical",
-            "config": {"workload": WORKLOAD, "dist": a.dist, "points_per_gpu": n,
+            "config": {"workload": workload(a.dist, n), "dist": a.dist, "points_per_gpu": n,
                        "points_total": world * n, "parallelism": f"index-range shards x{world}",
-                       "l2": "inputs 16 GB/GPU >> 126 MB L2 (no flush needed)",
+                       "l2": f"inputs {n * 16 / 1e9:.3g} GB/GPU vs 126 MB L2"
+                             + (" (no flush needed)" if n * 16 > 4 * 126e6 else " (L2-resident: not a roofline point)"),
                        "survivors": stats["counts"], "corner_certificate": "pass" if not
                        stats["uncertified"] else f"fallback mask {stats['uncertified']}"},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
