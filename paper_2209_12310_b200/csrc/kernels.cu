@@ -1551,12 +1551,13 @@ void launch_k1_sample(const double* d_xy, std::uint64_t n, int segs, int len, in
                       K1Partial* partials, unsigned* ticket, ohx_extremes_rec* d_recs,
                       cudaStream_t stream) {
   const SampleMap sm{n, segs, len, subs};
-  // 4 runs per block (58 -> 52 us at 1e9: fewer partials to combine);
+  // 2 runs per block (4 sub-samples x 128 runs at 1e9: 256 blocks; 1 run:
+  // 36 us, 2: 33 us, 4: 37 us -- fewer partials vs. fewer blocks in flight);
   // OHX_SAMPLE_RPB overrides (tuning hook)
   static const int runs_per_block = [] {
     const char* e = std::getenv("OHX_SAMPLE_RPB");
     const int k = e ? std::atoi(e) : 0;
-    return k >= 1 ? k : 4;
+    return k >= 1 ? k : 2;
   }();
   const int bx = std::max(1, segs / subs / runs_per_block);
   k1_small<true, std::uint64_t><<<dim3(bx, subs), 256, 0, stream>>>(
