@@ -227,6 +227,15 @@ int ohx_queue_fetch(ohx_ctx* ctx, int q, uint64_t* h_idx, double* h_xy,
 int ohx_queue_device(ohx_ctx* ctx, int q, const void** d_idx,
                      int* idx_bytes, uint64_t* count);
 
+/* Hull vertex indices (the north star's parity output; the reference itself
+ * emits coordinates only, hull.cpp:196-203): for each of the h vertices of
+ * a hull computed by the last pipeline / filter call on ctx (NULL: the
+ * default context, i.e. after ohx_heaphull), the smallest input index with
+ * equal coordinates (-0.0 == +0.0), in the hull's order.  OHX_E_INVALID if
+ * a vertex is not among that call's survivors. */
+int ohx_hull_indices(ohx_ctx* ctx, const double* h_hull, uint64_t h,
+                     uint64_t* h_idx, void* stream);
+
 /* ---- pipeline-level (host buffers; the reference's bound entry points) --- */
 
 /* heaphull (hull.cpp:196-203; python/module.cpp:62-75): host points in,

@@ -24,7 +24,7 @@ import numpy as np
 from ._lib import (DISTS, OHX_E_INVALID, SLOTS, CornerRec, ExtremeSet, ExtremesRec, FilterPlan,
                    OhxError, RunInfo, check, lib)
 
-__all__ = ["classify", "filter_rate", "generate", "heaphull", "heaphull_file", "write_pts2",
+__all__ = ["classify", "filter_rate", "generate", "heaphull", "heaphull_file", "hull_indices", "write_pts2",
            "monotone_chain",
            "heaphull_run", "find_extremes", "Context", "OhxError", "device_count"]
 
@@ -74,6 +74,17 @@ def heaphull(points, threads: int = 1, chunk: int = 32) -> np.ndarray:
                            len(hull), C.byref(h), None))
     # small hulls are copied out of the (virtual, n-sized) buffer
     return hull[: h.value].copy() if h.value < (1 << 20) else hull[: h.value]
+
+
+def hull_indices(hull) -> np.ndarray:
+    """Vertex indices of the hull the last heaphull call returned (default
+    context): for each vertex, the smallest input index with those
+    coordinates, in the hull's order."""
+    hv = np.ascontiguousarray(hull, dtype=np.float64).reshape(-1, 2)
+    idx = np.empty(len(hv), dtype=np.uint64)
+    check(lib.ohx_hull_indices(None, hv.ctypes.data_as(_dp), len(hv), idx.ctypes.data_as(_u64p),
+                               None))
+    return idx.astype(np.int64)
 
 
 def heaphull_run(points):
@@ -273,6 +284,15 @@ class Context:
                                   None if xy is None else xy.ctypes.data_as(_dp), count,
                                   _stream(stream)))
         return idx, xy
+
+    def hull_indices(self, hull, stream=None) -> np.ndarray:
+        """Vertex indices of a hull from this context's last pipeline call:
+        the smallest input index with each vertex's coordinates."""
+        hv = np.ascontiguousarray(hull, dtype=np.float64).reshape(-1, 2)
+        idx = np.empty(len(hv), dtype=np.uint64)
+        check(lib.ohx_hull_indices(self.h, hv.ctypes.data_as(_dp), len(hv),
+                                   idx.ctypes.data_as(_u64p), _stream(stream)))
+        return idx.astype(np.int64)
 
     def load_pts2(self, path, d_xy=None, stream=None):
         """A PTS2 file into device memory -> (n, tensor or the given buffer)."""

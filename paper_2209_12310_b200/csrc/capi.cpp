@@ -190,6 +190,41 @@ int ohx_queue_fetch(ohx_ctx* ctx, int q, uint64_t* h_idx, double* h_xy, uint64_t
   });
 }
 
+int ohx_hull_indices(ohx_ctx* ctx, const double* h_hull, uint64_t h, uint64_t* h_idx,
+                     void* stream) {
+  return guard([&] {
+    if (!ctx) ctx = default_ctx(-1);
+    std::lock_guard<std::mutex> g(ctx->mu);
+    bind(ctx);
+    if (ctx->last_n == 0) throw std::invalid_argument("hull_indices: no filter result in this context");
+    if (h == 0) return;
+    if (h >= 0xffffffffull) throw std::invalid_argument("hull_indices: hull too large");
+    cudaStream_t s = pick(ctx, stream);
+    std::uint64_t nslots = 1;
+    while (nslots < 2 * h) nslots <<= 1;
+    // one stream-ordered scratch block: hull copy, result, table
+    const std::uint64_t bytes = h * 16 + h * 8 + nslots * 4;
+    void* scratch = nullptr;
+    check_cuda(cudaMallocAsync(&scratch, bytes, s), "cudaMallocAsync(hull indices)");
+    auto* d_hull = static_cast<double*>(scratch);
+    auto* d_res = reinterpret_cast<unsigned long long*>(d_hull + 2 * h);
+    auto* d_slots = reinterpret_cast<std::uint32_t*>(d_res + h);
+    cudaError_t err = cudaMemcpyAsync(d_hull, h_hull, h * 16, cudaMemcpyHostToDevice, s);
+    if (err == cudaSuccess) {
+      launch_hull_indices(ctx->last_xy, ctx->d_queues, ctx->last_idx_bytes, ctx->last_cap,
+                          ctx->last_counts, ctx->last_base, d_hull, h, d_slots, nslots, d_res, s);
+      ctx->launches += 2;
+      err = cudaMemcpyAsync(h_idx, d_res, h * 8, cudaMemcpyDeviceToHost, s);
+    }
+    cudaFreeAsync(scratch, s);
+    check_cuda(err, "hull indices");
+    check_cuda(cudaStreamSynchronize(s), "hull indices");
+    for (std::uint64_t i = 0; i < h; ++i)
+      if (h_idx[i] == ~0ull)
+        throw std::invalid_argument("hull_indices: a vertex is not among the last call's survivors");
+  });
+}
+
 int ohx_queue_device(ohx_ctx* ctx, int q, const void** d_idx, int* idx_bytes,
                      uint64_t* count) {
   return guard([&] {

@@ -144,6 +144,12 @@ void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
                     cudaStream_t stream);
 void launch_gather(const double* d_xy, const void* d_idx, int idx_bytes,
                    std::uint64_t count, double* d_out, cudaStream_t stream);
+// hull vertices -> smallest survivor index (+ base) with equal coordinates
+// (d_res, ~0 where none; nslots a power of two >= 2h)
+void launch_hull_indices(const double* d_xy, const void* d_queues, int idx_bytes,
+                         std::uint64_t cap, const std::uint64_t counts[4], std::uint64_t base,
+                         const double* d_hull, std::uint64_t h, std::uint32_t* d_slots,
+                         std::uint64_t nslots, unsigned long long* d_res, cudaStream_t stream);
 // the first `limit` survivors' coordinates with the counts read on the device
 void launch_gather4_dev(const double* d_xy, const void* d_queues, int idx_bytes,
                         std::uint64_t cap, const unsigned long long* d_counts,

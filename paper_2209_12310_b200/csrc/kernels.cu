@@ -1376,6 +1376,56 @@ __global__ void gather_xy4_dev(const double2* __restrict__ pts, const IdxT* __re
   }
 }
 
+// ------------------------------------------------- hull vertex indices ----
+// Each hull vertex -> the smallest input index with equal coordinates.
+// Every hull vertex is a survivor (the extremes carry their queue label),
+// and duplicates of a vertex share its label except duplicates of a kept
+// extreme -- whose index is already the smallest with that key -- so the
+// survivors are the only points to probe: the vertices go into an
+// open-addressing table (distinct coordinates: the clean-up leaves strict
+// turns), the survivors probe it and atomicMin their index.  -0.0 and
+// +0.0 are the same coordinate (the reference's == comparisons).
+__device__ __forceinline__ std::uint64_t coord_bits(double v) {
+  return static_cast<std::uint64_t>(__double_as_longlong(v == 0.0 ? 0.0 : v));
+}
+__device__ __forceinline__ std::uint64_t coord_hash(double2 p) {
+  std::uint64_t z = coord_bits(p.x) * 0x9E3779B97F4A7C15ull ^ coord_bits(p.y);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void hidx_insert(const double2* __restrict__ hull, std::uint64_t h,
+                            std::uint32_t* __restrict__ slots, std::uint64_t mask) {
+  const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= h) return;
+  for (std::uint64_t s = coord_hash(hull[i]) & mask;; s = (s + 1) & mask)
+    if (atomicCAS(slots + s, 0xffffffffu, static_cast<std::uint32_t>(i)) == 0xffffffffu) return;
+}
+
+template <typename IdxT>
+__global__ void hidx_probe(const double2* __restrict__ pts, const IdxT* __restrict__ queues,
+                           std::uint64_t cap, ulonglong4 ends, std::uint64_t base,
+                           const double2* __restrict__ hull, const std::uint32_t* __restrict__ slots,
+                           std::uint64_t mask, unsigned long long* __restrict__ res) {
+  for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < ends.w;
+       k += std::uint64_t(gridDim.x) * blockDim.x) {
+    const int q = (k >= ends.x) + (k >= ends.y) + (k >= ends.z);
+    const std::uint64_t start = q == 0 ? 0 : (q == 1 ? ends.x : (q == 2 ? ends.y : ends.z));
+    const std::uint64_t j = queues[std::uint64_t(q) * cap + (k - start)];
+    const double2 p = pts[j];
+    for (std::uint64_t s = coord_hash(p) & mask;; s = (s + 1) & mask) {
+      const std::uint32_t v = slots[s];
+      if (v == 0xffffffffu) break;  // not a hull vertex
+      const double2 c = hull[v];
+      if (c.x == p.x && c.y == p.y) {
+        atomicMin(res + v, static_cast<unsigned long long>(base + j));
+        break;
+      }
+    }
+  }
+}
+
 }  // namespace
 
 // ============================================================ launchers ==
@@ -1641,6 +1691,31 @@ void launch_gather4_dev(const double* d_xy, const void* d_queues, int idx_bytes,
                                              cap, d_counts, limit,
                                              reinterpret_cast<double2*>(d_out));
   check_cuda(cudaGetLastError(), "gather_xy4_dev launch");
+}
+
+void launch_hull_indices(const double* d_xy, const void* d_queues, int idx_bytes,
+                         std::uint64_t cap, const std::uint64_t counts[4], std::uint64_t base,
+                         const double* d_hull, std::uint64_t h, std::uint32_t* d_slots,
+                         std::uint64_t nslots, unsigned long long* d_res, cudaStream_t stream) {
+  const auto* hull = reinterpret_cast<const double2*>(d_hull);
+  check_cuda(cudaMemsetAsync(d_slots, 0xff, nslots * 4, stream), "cudaMemsetAsync(slots)");
+  check_cuda(cudaMemsetAsync(d_res, 0xff, h * 8, stream), "cudaMemsetAsync(hull indices)");
+  hidx_insert<<<static_cast<unsigned>((h + 255) / 256), 256, 0, stream>>>(hull, h, d_slots,
+                                                                         nslots - 1);
+  check_cuda(cudaGetLastError(), "hidx_insert launch");
+  const ulonglong4 ends = make_ulonglong4(counts[0], counts[0] + counts[1],
+                                          counts[0] + counts[1] + counts[2],
+                                          counts[0] + counts[1] + counts[2] + counts[3]);
+  if (ends.w == 0) return;
+  const unsigned grid = static_cast<unsigned>(ends.w < 148ull * 2048 ? (ends.w + 255) / 256 : 148 * 8);
+  const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  if (idx_bytes == 4)
+    hidx_probe<<<grid, 256, 0, stream>>>(pts, static_cast<const std::uint32_t*>(d_queues), cap,
+                                         ends, base, hull, d_slots, nslots - 1, d_res);
+  else
+    hidx_probe<<<grid, 256, 0, stream>>>(pts, static_cast<const std::uint64_t*>(d_queues), cap,
+                                         ends, base, hull, d_slots, nslots - 1, d_res);
+  check_cuda(cudaGetLastError(), "hidx_probe launch");
 }
 
 void launch_gather(const double* d_xy, const void* d_idx, int idx_bytes,

@@ -541,3 +541,47 @@ def test_extreme_magnitudes_match_oracle(ctx, oracle, scale, offset, n):
     for q in range(4):
         idx, _ = ctx.queue(q + 1, info["counts"][q])
         assert np.array_equal(idx, np.flatnonzero(want_labels == q + 1)), q
+
+
+def _min_index_of(pts, hull):
+    """For each hull vertex, the smallest index j with pts[j] == vertex."""
+    z = pts + 0.0  # -0.0 -> +0.0: the reference compares with ==
+    order = np.lexsort((np.arange(len(z)), z[:, 1], z[:, 0]))
+    zs = z[order]
+    first = np.ones(len(zs), dtype=bool)
+    first[1:] = (zs[1:] != zs[:-1]).any(axis=1)
+    keys = {(a, b): int(j) for (a, b), j in zip(map(tuple, zs[first]), order[first])}
+    return np.array([keys[(a + 0.0, b + 0.0)] for a, b in hull], dtype=np.int64)
+
+
+@pytest.mark.parametrize("case", ["normal_1e6", "normal_9e6", "lattice_dups", "circle",
+                                  "signed_zeros", "collinear"])
+def test_hull_vertex_indices(ctx, oracle, case):
+    # the north star's parity output "hull vertex indices": the smallest
+    # input index with each vertex's coordinates, in the hull's order
+    rng = np.random.default_rng(3)
+    if case == "normal_1e6":
+        pts = P.generate("normal", 1_000_000, 7)
+    elif case == "normal_9e6":
+        pts = P.generate("normal", 9_000_000, 7)
+    elif case == "lattice_dups":  # every vertex repeated, later copies first in the array
+        g = rng.integers(-30, 31, size=(2_000_000, 2)).astype(float)
+        pts = np.concatenate([g[::-1], g])
+    elif case == "circle":
+        pts = P.generate("circle", 300_000, 5)
+    elif case == "signed_zeros":
+        g = rng.integers(-2, 3, size=(200_000, 2)).astype(float)
+        g[rng.random(len(g)) < 0.5] *= -1.0  # -0.0 copies of the zero coordinates
+        pts = g
+    else:
+        t = rng.integers(0, 1000, 100_000).astype(float)
+        pts = np.stack([t, 2 * t], 1)
+    pts = np.ascontiguousarray(pts, dtype=np.float64)
+    hull, _ = ctx.heaphull_device(dev(pts), len(pts))
+    assert np.array_equal(hull, oracle.heaphull(pts))
+    idx = ctx.hull_indices(hull)
+    assert np.array_equal(idx, _min_index_of(pts, hull)), case
+    assert np.array_equal(pts[idx] + 0.0, hull + 0.0)
+    # the host API and the default context
+    assert np.array_equal(P.heaphull(pts), hull)
+    assert np.array_equal(P.hull_indices(hull), idx)
