@@ -235,6 +235,12 @@ int ohx_queue_device(ohx_ctx* ctx, int q, const void** d_idx,
  * a vertex is not among that call's survivors. */
 int ohx_hull_indices(ohx_ctx* ctx, const double* h_hull, uint64_t h,
                      uint64_t* h_idx, void* stream);
+/* Same over one shard's survivors (global indices: index_base of the
+ * shard's filter call added); UINT64_MAX where the shard holds no point with
+ * a vertex's coordinates, no error.  The job's answer is the minimum over
+ * the shards (sharded.py: an all-reduce MIN). */
+int ohx_hull_indices_partial(ohx_ctx* ctx, const double* h_hull, uint64_t h,
+                             uint64_t* h_idx, void* stream);
 
 /* ---- pipeline-level (host buffers; the reference's bound entry points) --- */
 

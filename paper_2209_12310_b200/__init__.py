@@ -285,14 +285,16 @@ class Context:
                                   _stream(stream)))
         return idx, xy
 
-    def hull_indices(self, hull, stream=None) -> np.ndarray:
+    def hull_indices(self, hull, partial: bool = False, stream=None) -> np.ndarray:
         """Vertex indices of a hull from this context's last pipeline call:
-        the smallest input index with each vertex's coordinates."""
+        the smallest input index with each vertex's coordinates.  partial:
+        over this shard's survivors only, -1 where it has none."""
         hv = np.ascontiguousarray(hull, dtype=np.float64).reshape(-1, 2)
         idx = np.empty(len(hv), dtype=np.uint64)
-        check(lib.ohx_hull_indices(self.h, hv.ctypes.data_as(_dp), len(hv),
-                                   idx.ctypes.data_as(_u64p), _stream(stream)))
-        return idx.astype(np.int64)
+        fn = lib.ohx_hull_indices_partial if partial else lib.ohx_hull_indices
+        check(fn(self.h, hv.ctypes.data_as(_dp), len(hv), idx.ctypes.data_as(_u64p),
+                 _stream(stream)))
+        return idx.astype(np.int64)  # UINT64_MAX -> -1
 
     def load_pts2(self, path, d_xy=None, stream=None):
         """A PTS2 file into device memory -> (n, tensor or the given buffer)."""

@@ -190,9 +190,10 @@ int ohx_queue_fetch(ohx_ctx* ctx, int q, uint64_t* h_idx, double* h_xy, uint64_t
   });
 }
 
-int ohx_hull_indices(ohx_ctx* ctx, const double* h_hull, uint64_t h, uint64_t* h_idx,
-                     void* stream) {
-  return guard([&] {
+namespace {
+void hull_indices_impl(ohx_ctx* ctx, const double* h_hull, uint64_t h, uint64_t* h_idx,
+                       void* stream, bool partial) {
+  {
     if (!ctx) ctx = default_ctx(-1);
     std::lock_guard<std::mutex> g(ctx->mu);
     bind(ctx);
@@ -219,10 +220,21 @@ int ohx_hull_indices(ohx_ctx* ctx, const double* h_hull, uint64_t h, uint64_t* h
     cudaFreeAsync(scratch, s);
     check_cuda(err, "hull indices");
     check_cuda(cudaStreamSynchronize(s), "hull indices");
-    for (std::uint64_t i = 0; i < h; ++i)
+    for (std::uint64_t i = 0; i < h && !partial; ++i)
       if (h_idx[i] == ~0ull)
         throw std::invalid_argument("hull_indices: a vertex is not among the last call's survivors");
-  });
+  }
+}
+}  // namespace
+
+int ohx_hull_indices(ohx_ctx* ctx, const double* h_hull, uint64_t h, uint64_t* h_idx,
+                     void* stream) {
+  return guard([&] { hull_indices_impl(ctx, h_hull, h, h_idx, stream, false); });
+}
+
+int ohx_hull_indices_partial(ohx_ctx* ctx, const double* h_hull, uint64_t h, uint64_t* h_idx,
+                             void* stream) {
+  return guard([&] { hull_indices_impl(ctx, h_hull, h, h_idx, stream, true); });
 }
 
 int ohx_queue_device(ohx_ctx* ctx, int q, const void** d_idx, int* idx_bytes,

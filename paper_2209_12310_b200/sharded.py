@@ -61,6 +61,10 @@ class CudaShard:
         self.counts = self.ctx.filter(self.d_xy, self.n, plan, self.base)
         return self.counts
 
+    def hull_indices(self, hull) -> np.ndarray:
+        """This shard's part of the hull vertex indices (-1: none here)."""
+        return self.ctx.hull_indices(hull, partial=True)
+
     def queue_xy(self, q: int, count: int) -> np.ndarray:
         if count == 0:
             return np.zeros((0, 2), dtype=np.float64)
@@ -147,6 +151,37 @@ def sharded_heaphull(shard, device=None, root: int = 0, stats: dict | None = Non
     return hull_from_queue_points(anchors, gathered)
 
 
+def sharded_hull_indices(shard, hull, device=None, root: int = 0):
+    """Hull vertex indices of the last sharded_heaphull (the hull given on
+    `root`): the smallest global input index with each vertex's
+    coordinates -- every shard maps the vertices over its own survivors,
+    then a MIN all-reduce.  Returns the (h,) int64 array on `root`."""
+    dist = _dist()
+    if dist is None or dist.get_world_size() == 1:
+        idx = shard.hull_indices(hull)
+        if (idx < 0).any():
+            raise ValueError("hull_indices: a vertex is not among the survivors")
+        return idx
+    import torch
+    rank = dist.get_rank()
+    h = torch.tensor([len(hull) if rank == root else 0], dtype=torch.int64, device=device)
+    dist.broadcast(h, root)
+    hv = torch.zeros((int(h.item()), 2), dtype=torch.float64, device=device)
+    if rank == root:
+        hv.copy_(torch.from_numpy(np.ascontiguousarray(hull, dtype=np.float64)))
+    dist.broadcast(hv, root)
+    part = shard.hull_indices(hv.cpu().numpy())
+    big = np.iinfo(np.int64).max
+    t = torch.from_numpy(np.where(part < 0, big, part)).to(device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    if rank != root:
+        return None
+    idx = t.cpu().numpy()
+    if (idx == big).any():
+        raise ValueError("hull_indices: a vertex is not among the survivors")
+    return idx
+
+
 def shard_range(n_total: int, world: int, rank: int):
     """Contiguous index range of `rank`: [floor(r n / G), floor((r+1) n / G))."""
     b0 = (n_total * rank) // world
@@ -154,4 +189,4 @@ def shard_range(n_total: int, world: int, rank: int):
     return b0, b1 - b0
 
 
-__all__ = ["CudaShard", "sharded_heaphull", "shard_range"]
+__all__ = ["CudaShard", "sharded_heaphull", "sharded_hull_indices", "shard_range"]

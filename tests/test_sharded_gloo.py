@@ -82,7 +82,8 @@ def _gpu_worker(rank, world, port, q):
 
     import paper_2209_12310_b200 as P
     from oracle import Oracle
-    from paper_2209_12310_b200.sharded import CudaShard, shard_range, sharded_heaphull
+    from paper_2209_12310_b200.sharded import (CudaShard, shard_range, sharded_heaphull,
+                                               sharded_hull_indices)
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -95,10 +96,18 @@ def _gpu_worker(rank, world, port, q):
             b0, cnt = shard_range(n, world, rank)
             d = torch.from_numpy(pts[b0:b0 + cnt]).cuda()
             stats = {}
-            hull = sharded_heaphull(CudaShard(ctx, d, cnt, b0), device="cpu", stats=stats)
+            shard = CudaShard(ctx, d, cnt, b0)
+            hull = sharded_heaphull(shard, device="cpu", stats=stats)
+            idx = sharded_hull_indices(shard, hull, device="cpu")
             if rank == 0:
                 want = o.heaphull(pts)
-                out.append((dist_name, hull.tolist() == want.tolist(), stats["fused"]))
+                ok = hull.tolist() == want.tolist()
+                # vertex indices: the smallest global index with the vertex's
+                # coordinates (brute force over the whole input)
+                for v, j in zip(hull, idx):
+                    ok = ok and int(j) == int(np.flatnonzero((pts[:, 0] == v[0]) &
+                                                             (pts[:, 1] == v[1]))[0])
+                out.append((dist_name, ok, stats["fused"]))
         if rank == 0:
             q.put(out)
         ctx.close()
