@@ -363,7 +363,7 @@ def run_b200_arm(a):
                           "note": "fused pass: region test + candidate append"},
             "candidate_stage": {"ms": statistics.mean(kc),
                                 "bytes": cand * (idx_b * 2 + 16 * 2 + 16),
-                                "note": "scan + gather + K1 over candidates (+ host sync)"},
+                                "note": "ordered gather + K1 over the candidates (+ host sync)"},
             "k2_gather": {"ms": k2_ms, "bytes": cand * (idx_b + 16) + idx_b * s_local,
                           "note": "K2 on the candidates only"},
         }
