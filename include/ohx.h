@@ -150,6 +150,11 @@ int ohx_ctx_last_run(const ohx_ctx* ctx, ohx_run_info* info);
  * compaction + K1 over the candidates); -1 for a stage that did not run
  * (a pipeline call resets all four). */
 int ohx_ctx_kernel_ms(ohx_ctx* ctx, double ms[4]);
+/* Running sums of those stage times over the calls since the last reset
+ * (each call's stages counted once, when they have completed; count[k] =
+ * calls that ran stage k): a timing loop reads them once at its end
+ * instead of querying events between calls.  reset != 0 zeroes them. */
+int ohx_ctx_kernel_ms_sum(ohx_ctx* ctx, double sum[4], uint64_t count[4], int reset);
 
 /* ---- kernel-level (one shard, device-resident points) ------------------ */
 

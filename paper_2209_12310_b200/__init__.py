@@ -223,6 +223,14 @@ class Context:
         check(lib.ohx_ctx_kernel_ms(self.h, out))
         return {"k1": out[0], "k1b": out[1], "k2": out[2], "kc": out[3]}
 
+    def kernel_ms_sum(self, reset: bool = False) -> dict:
+        """Running sums of the stage durations over the calls since the last
+        reset: {stage: (total_ms, calls)} (read once after a timing loop)."""
+        tot = (C.c_double * 4)()
+        cnt = (C.c_uint64 * 4)()
+        check(lib.ohx_ctx_kernel_ms_sum(self.h, tot, cnt, 1 if reset else 0))
+        return {k: (tot[i], int(cnt[i])) for i, k in enumerate(("k1", "k1b", "k2", "kc"))}
+
     def last_run(self) -> dict:
         """How the last pipeline call on this context ran (fused single pass
         or two passes, corner fallback, candidates, queue lengths)."""

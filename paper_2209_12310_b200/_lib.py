@@ -72,6 +72,7 @@ PROTOTYPES = [
     ("ohx_ctx_device", C.c_int, [_vp]),
     ("ohx_ctx_launches", _u64, [_vp]),
     ("ohx_ctx_kernel_ms", C.c_int, [_vp, _dp]),
+    ("ohx_ctx_kernel_ms_sum", C.c_int, [_vp, _dp, _u64p, C.c_int]),
     ("ohx_ctx_last_run", C.c_int, [_vp, C.POINTER(RunInfo)]),
     ("ohx_extremes", C.c_int, [_vp, _vp, _u64, _u64, C.POINTER(ExtremesRec), _vp]),
     ("ohx_fused_extremes", C.c_int, [_vp, _vp, _u64, _u64, C.POINTER(ExtremesRec),

@@ -82,6 +82,22 @@ int ohx_ctx_kernel_ms(ohx_ctx* ctx, double ms[4]) {
   });
 }
 
+int ohx_ctx_kernel_ms_sum(ohx_ctx* ctx, double sum[4], uint64_t count[4], int reset) {
+  return guard([&] {
+    std::lock_guard<std::mutex> g(ctx->mu);
+    bind(ctx);
+    fold_stage_times(ctx, true);
+    for (int k = 0; k < 4; ++k) {
+      sum[k] = ctx->ksum[k];
+      count[k] = ctx->kcnt[k];
+      if (reset) {
+        ctx->ksum[k] = 0;
+        ctx->kcnt[k] = 0;
+      }
+    }
+  });
+}
+
 int ohx_extremes(ohx_ctx* ctx, const double* d_xy, uint64_t n, uint64_t index_base,
                  ohx_extremes_rec* h_rec, void* stream) {
   return guard([&] {

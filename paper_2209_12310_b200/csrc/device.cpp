@@ -27,6 +27,29 @@
 
 namespace ohx {
 
+// stage k's events bracket a launch of this call
+void mark_timed(ohx_ctx* c, int k) {
+  c->timed[k] = true;
+  c->folded[k] = false;
+}
+// add this call's completed stage times to the context's running sums
+// (wait: block until the events complete, else leave unfinished ones)
+void fold_stage_times(ohx_ctx* c, bool wait) {
+  for (int k = 0; k < 4; ++k) {
+    if (!c->timed[k] || c->folded[k]) continue;
+    if (wait) check_cuda(cudaEventSynchronize(c->ev[k][1]), "cudaEventSynchronize");
+    else if (cudaEventQuery(c->ev[k][1]) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    float v = 0.f;
+    check_cuda(cudaEventElapsedTime(&v, c->ev[k][0], c->ev[k][1]), "cudaEventElapsedTime");
+    c->ksum[k] += v;
+    ++c->kcnt[k];
+    c->folded[k] = true;
+  }
+}
+
 void extremes(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
               ohx_extremes_rec* out, cudaStream_t s) {
   if (n == 0) throw std::invalid_argument("find_axis_extremes: empty point set");
@@ -35,7 +58,7 @@ void extremes(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t bas
   check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
   launch_k1(d_xy, n, base, c->d_partials, grid, c->d_ticket, c->d_rec, s);
   check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
-  c->timed[0] = true;
+  mark_timed(c, 0);
   ++c->launches;
   check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
                              cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec)");
@@ -52,7 +75,7 @@ void corners_exact(ohx_ctx* c, const double* d_xy, std::uint64_t n,
   check_cuda(cudaEventRecord(c->ev[1][0], s), "cudaEventRecord");
   launch_k1b(d_xy, n, base, bbox, c->d_partials, grid, c->d_ticket, c->d_crec, s);
   check_cuda(cudaEventRecord(c->ev[1][1], s), "cudaEventRecord");
-  c->timed[1] = true;
+  mark_timed(c, 1);
   ++c->launches;
   check_cuda(cudaMemcpyAsync(c->h_crec, c->d_crec, sizeof(ohx_corner_rec),
                              cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(crec)");
@@ -108,7 +131,7 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
       launch_k2(d_xy, items, kp, c->d_status, ntiles, c->d_queues, idx_bytes, cap, d_labels,
                 c->d_counts, s, d_cand, d_cpts);  // k2_filter + k2_compact
       check_cuda(cudaEventRecord(c->ev[2][1], s), "cudaEventRecord");
-      c->timed[2] = true;
+      mark_timed(c, 2);
       c->launches += 2;
       // the first survivors' coordinates ride along with the counts: a
       // small survivor set needs no second round trip (queues_fetch_xy)
@@ -138,6 +161,7 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
     }
     c->last_cap = cap;
   }
+  fold_stage_times(c, false);  // every stage of this call has completed (K2 synced)
   c->last_xy = d_xy;
   c->last_n = n;
   c->last_base = base;
@@ -487,7 +511,7 @@ bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
   check_cuda(cudaEventRecord(c->ev[0][0], s), "cudaEventRecord");
   launch_kf(d_xy, n, q, grid, c->d_regions, idx_bytes, cap_w, d_wcounts, c->d_cnt, gate_min, s);
   check_cuda(cudaEventRecord(c->ev[0][1], s), "cudaEventRecord");
-  c->timed[0] = true;
+  mark_timed(c, 0);
   ++c->launches;
   // candidate list + coordinates and K1 over them, sized on the device: the
   // list buffers hold cap_c candidates (more: regrown and redone below)
@@ -525,7 +549,7 @@ bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
     candidates(cap_c);
   }
   check_cuda(cudaEventRecord(c->ev[3][1], s), "cudaEventRecord");
-  c->timed[3] = true;
+  mark_timed(c, 3);
   *rec = *c->h_rec;
   rec->n = n;
   c->fz = {true, q, d_xy, n, base, n_cand};

@@ -98,6 +98,11 @@ struct ohx_ctx {
   // K2, and the fused path's candidate stage (compaction + candidate K1)
   cudaEvent_t ev[4][2] = {};
   bool timed[4] = {false, false, false, false};
+  // running sums of those stage times over calls (folded once per call when
+  // its events have completed; read and reset by ohx_ctx_kernel_ms_sum)
+  bool folded[4] = {true, true, true, true};
+  double ksum[4] = {0, 0, 0, 0};
+  std::uint64_t kcnt[4] = {0, 0, 0, 0};
 };
 
 namespace ohx {
@@ -117,6 +122,10 @@ struct Trace {
     t = now;
   }
 };
+
+// ---- stage timing (device.cpp)
+void mark_timed(ohx_ctx* c, int k);
+void fold_stage_times(ohx_ctx* c, bool wait);
 
 // ---- context workspaces (context.cpp)
 const char* last_error();  // this thread's last error message
