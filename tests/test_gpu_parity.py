@@ -585,3 +585,21 @@ def test_hull_vertex_indices(ctx, oracle, case):
     # the host API and the default context
     assert np.array_equal(P.heaphull(pts), hull)
     assert np.array_equal(P.hull_indices(hull), idx)
+
+
+def test_stage_time_sums_count_each_call_once(ctx):
+    # ohx_ctx_kernel_ms_sum: per-stage CUDA-event sums over the calls since
+    # the reset, each call's stages counted once (the bench reads them once
+    # after its timed loop instead of querying events between steps)
+    pts = P.generate("normal", 9_000_000, 7)
+    d = dev(pts)
+    ctx.heaphull_device(d, len(pts))
+    ctx.kernel_ms_sum(reset=True)
+    for _ in range(3):
+        ctx.heaphull_device(d, len(pts))
+    s = ctx.kernel_ms_sum()
+    assert ctx.last_run()["fused"]
+    assert s["k1"][1] == 3 and s["kc"][1] == 3 and s["k2"][1] == 3 and s["k1b"][1] == 0, s
+    assert all(s[k][0] > 0 for k in ("k1", "kc", "k2")), s
+    assert ctx.kernel_ms_sum() == s  # reading does not count again
+    assert ctx.kernel_ms_sum(reset=True) == s and ctx.kernel_ms_sum()["k1"] == (0.0, 0)
