@@ -4,12 +4,15 @@
     python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
     (N > 1: launched by torch.distributed.run, one rank per GPU, NCCL)
 
-Workload: BASELINE.json configs[2] -- normal-distribution 2D points,
-N = 1e9 per GPU (16 GB of AoS binary64 points, larger than the 126 MB L2,
-so no flush is needed), seed 7 + rank.  Weak scaling: every rank owns a
-1e9-point shard of the global index range; the shards are filtered
-independently and only the ~300 B extremes records and the survivors
-cross GPUs (sharded.py).
+Workload (the job's corpus is always ONE reference corpus,
+generate({dist, points_total, seed}), so every number is checkable against
+the reference on the same bytes):
+  N = 1  BASELINE.json configs[2]: normal, 1e9 points, seed 7 (16 GB of AoS
+         binary64 points, larger than the 126 MB L2: no flush needed).
+  N > 1  BASELINE.json configs[4]: normal, 4e9 points in total, seed 7,
+         strong scaling; rank r holds the contiguous slice
+         [r*4e9/N, (r+1)*4e9/N) of that corpus, generated in place
+         (ohx_generate_range).  --weak: 1e9 points per GPU instead.
 
 A step is one full hull of the whole job's points:
   value  -- inputs resident in HBM: the fused single pass (sample ->
@@ -19,19 +22,25 @@ A step is one full hull of the whole job's points:
             host hull, Gpoints/s over all ranks,
   e2e    -- the same through the reference-facing API with host buffers:
             N = 1 the C ABI call ohx_heaphull (octohull::heaphull) on
-            pinned host points, N > 1 the sharded API with each rank's
-            pinned shard uploaded inside the step.
+            pinned host points, N > 1 each rank's pinned slice uploaded
+            inside the step; e2e.roofline is the PCIe bound (the measured
+            raw pinned H2D bandwidth of the same buffer).
 Steps are timed with CUDA events after a barrier + synchronize on both
 sides, max over ranks.  roofline: the dominant kernel's algorithmic bytes
 per launch (16 B per point read; the fused KF pass also writes 4 B per
 candidate index) over its CUDA-event duration on the launching stream,
 against the measured HBM copy bandwidth in MEASURED_PEAKS.json.
-cpu_baseline: the reference library itself (oracle/_ref, compiled from the reference sources) timed on
-the host cores on the bench's own points (the full per-GPU workload).
+cpu_baseline: the reference library itself (oracle/_ref, compiled from the
+reference sources) timed on the host cores on the bench's own points (the
+full per-GPU workload); the same leg checks the device results against it
+(parity).  distributions: BASELINE configs[1] and configs[3] (square and
+circle 1e8), timed device-resident and checked against the reference.
 
 `--impl reference` times that reference CPU implementation on the same
-metric (rank 0 only), each step one heaphull_run over the full per-GPU
-workload (--cpu-sample bounds it).
+metric and config (rank 0 only; the points come from the reference's own
+generator, nothing of this repository's library is loaded), each step one
+heaphull_run over the first --cpu-sample points of the job's corpus
+(default: the whole corpus up to 1e9 points).
 """
 
 from __future__ import annotations
@@ -50,14 +59,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Gpoints/s end-to-end hull and filter HBM GB/s vs peak at 1/2/4/8 B200"
 UNIT = "Gpoints/s"
-WORKLOAD = "normal-distribution 2D points, 1e9 per GPU (BASELINE configs[2]; C5 shape at N>1)"
-
-
-def workload(dist: str, n: int) -> str:
-    """The workload name: BASELINE configs[2] at its defaults, else what ran."""
-    if dist == "normal" and n == 1_000_000_000:
-        return WORKLOAD
-    return f"{dist}-distribution 2D points, {n:.3g} per GPU (BASELINE configs[2] shape)"
+STRONG_TOTAL = 4_000_000_000  # BASELINE configs[4]
 
 
 def parse():
@@ -67,17 +69,59 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--dist", default="normal")
-    ap.add_argument("--points", "--n", dest="n", type=float, default=1e9, help="points per GPU")
+    ap.add_argument("--points", "--n", dest="n", type=float, default=1e9,
+                    help="points per GPU at N = 1 (and with --weak)")
+    ap.add_argument("--points-total", type=float, default=0,
+                    help="points of the whole job at N > 1 (default 4e9: BASELINE configs[4])")
+    ap.add_argument("--weak", action="store_true", help="N > 1: --points per GPU")
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--cpu-sample", type=float, default=0,
-                    help="points of the CPU reference's sample (0: the full per-GPU workload)")
+                    help="points of the CPU reference's sample (0: the corpus, up to 1e9)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dists", action="store_true",
                     help="skip the per-distribution lines (square / circle 1e8)")
     ap.add_argument("--no-parity", action="store_true",
-                    help="skip the full-size parity gate against the reference library")
+                    help="skip the full-size parity checks against the reference library")
     return ap.parse_args()
+
+
+def job(a, world: int) -> dict:
+    """The job's corpus and how it is split over the ranks."""
+    if world == 1:
+        total, scaling = int(a.n), "weak"
+    elif a.weak:
+        total, scaling = world * int(a.n), "weak"
+    else:
+        total, scaling = int(a.points_total) or STRONG_TOTAL, "strong"
+    return {"total": total, "scaling": scaling, "dist": a.dist, "seed": a.seed}
+
+
+def shard_of(total: int, world: int, rank: int):
+    """Rank r's contiguous slice [floor(r T / N), floor((r+1) T / N))."""
+    b0 = total * rank // world
+    return b0, total * (rank + 1) // world - b0
+
+
+def config(a, world: int) -> dict:
+    """The line's `config` -- identical for both arms."""
+    j = job(a, world)
+    per = j["total"] // world
+    if world == 1 and j["dist"] == "normal" and j["total"] == 1_000_000_000 and j["seed"] == 7:
+        name = "BASELINE configs[2]: normal-distribution 2D points N=1e9 on 1 B200"
+    elif world > 1 and j["dist"] == "normal" and j["total"] == STRONG_TOTAL and j["seed"] == 7:
+        name = f"BASELINE configs[4]: normal-distribution 4e9 points sharded across {world} B200"
+    else:
+        name = (f"{j['dist']}-distribution 2D points, {j['total']:.3g} in total on {world} B200"
+                f" ({j['scaling']} scaling)")
+    return {"workload": name, "dist": j["dist"], "seed": j["seed"], "points_total": j["total"],
+            "points_per_gpu": per, "scaling": j["scaling"],
+            "corpus": f"generate({{{j['dist']}, {j['total']}, {j['seed']}}}), rank r holds "
+                      f"index range [r*T/N, (r+1)*T/N)",
+            "parallelism": f"index-range shards x{world}",
+            "l2": f"inputs {per * 16 / 1e9:.3g} GB/GPU vs 126 MB L2"
+                  + (" (larger: no flush needed)" if per * 16 > 4 * 126e6
+                     else " (L2-resident: not a roofline point)")}
 
 
 # ---------------------------------------------------------------- clocks --
@@ -161,67 +205,164 @@ def ncu_traffic():
 
 
 # ------------------------------------------------------- CPU reference ----
-def cpu_reference(n_sample: int, reps: int, seed: int, dist: str, pts=None):
-    """The reference heaphull_run (oracle/_ref) on all host cores, on `pts`
-    (the bench's own points) or a generated sample of n_sample points."""
-    import numpy as np
-
-    import paper_2209_12310_b200 as P
+def cpu_reference(pts, reps: int):
+    """The reference heaphull_run (oracle/_ref) on all host cores over `pts`
+    (the C restatement, single-threaded, where the reference was never
+    built); -> {kind, cores, times}."""
     from oracle import Oracle, Reference
 
-    if pts is None:
-        pts = P.generate(dist, n_sample, seed)
-    n_sample = len(pts)
     cores = os.cpu_count() or 1
     if Reference.available():
         eng = Reference().engine(cores, 32)
-        kind = "reference"
-        run = eng.heaphull
-    else:  # the C restatement, single-threaded
+        kind, run = "reference", eng.heaphull
+    else:
         o = Oracle()
         kind, cores = "port", 1
-
-        def run(a):
-            t0 = time.perf_counter()
-            h = o.heaphull(a)
-            return len(h), {"total_ms": (time.perf_counter() - t0) * 1e3}
+        run = o.heaphull
     times = []
     for _ in range(reps):
         t0 = time.perf_counter()
         run(pts)
         times.append(time.perf_counter() - t0)
-    del np
-    return {"kind": kind, "cores": cores, "times": times, "n": n_sample}
+    return {"kind": kind, "cores": cores, "times": times}
+
+
+def reference_parity(ref, pts, ctx, hull_dev, ext_dev) -> dict:
+    """The device results of the last call on ctx (hull, extremes, queues)
+    against the reference's own heaphull_run / find_extremes on the same
+    points (outside every timed region; the reference is the checker)."""
+    import numpy as np
+
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    ref_hull, ref_labels, _ = ref.heaphull_run(pts, cores, 32)
+    ref_ext = ref.find_extremes(pts, cores, 32)
+    ref_s = time.perf_counter() - t0
+    info = ctx.last_run()
+    queues_ok = True
+    for q in range(4):
+        want = np.flatnonzero(ref_labels == q + 1)
+        got = ctx.queue(q + 1, info["counts"][q])[0]
+        queues_ok &= bool(np.array_equal(got, want))
+    out = {"checked_against": f"reference heaphull_run + find_extremes (oracle/_ref, {cores} "
+                              f"workers) on the same {len(pts)} points",
+           "hull_equal": bool(np.array_equal(hull_dev, ref_hull)),
+           "extremes_equal": [int(v) for v in ext_dev] == [int(v) for v in ref_ext],
+           "queues_equal": queues_ok,
+           "survivors": int((ref_labels != 0).sum()), "h": int(len(ref_hull)),
+           "reference_s": ref_s}
+    del ref_labels
+    return out
 
 
 def run_reference_arm(a):
+    """Rank 0 only: the reference's heaphull_run on the first `sample`
+    points of the job's corpus, from the reference's own generator (the
+    first k points of generate({dist, T, seed}) are generate({dist, k,
+    seed})).  Nothing of this repository's library is loaded here."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    n = int(a.cpu_sample) or int(a.n)
-    r = cpu_reference(n, a.warmup + a.steps, a.seed, a.dist)
+    from oracle import Oracle, Reference
+
+    j = job(a, world)
+    n = min(j["total"], int(a.cpu_sample) or 1_000_000_000)
+    t0 = time.perf_counter()
+    gen = Reference() if Reference.available() else Oracle()
+    pts = gen.generate(j["dist"], n, j["seed"])
+    gen_s = time.perf_counter() - t0
+    r = cpu_reference(pts, a.warmup + a.steps)
     timed = r["times"][a.warmup:]
     ms = 1e3 * sum(timed) / len(timed)
     value = n / (ms * 1e-3) / 1e9
-    sample = (f"{a.dist} n={n} seed={a.seed} ("
-              + ("the full per-GPU workload" if n == int(a.n)
-                 else f"bounded sample of the {workload(a.dist, int(a.n))} workload")
-              + "), full heaphull_run")
+    sample = (f"{j['dist']} n={n} seed={j['seed']} ("
+              + ("the whole corpus" if n == j["total"]
+                 else f"the first {n} points of the {j['total']}-point corpus")
+              + f"), full heaphull_run, ReduceEngine({{32, {r['cores']}}})")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
-        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generator, seed 7)",
-        "config": {"workload": workload(a.dist, int(a.n)), "dist": a.dist, "sample_points": n,
-                   "parallelism": f"ReduceEngine({{32, {r['cores']}}}) host lanes"},
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": j["scaling"], "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: the reference's own generator ({j['dist']}, seed {j['seed']})",
+        "config": config(a, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "generate_s": gen_s,
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------- B200 arm --
+def h2d_bandwidth(host, dev) -> float:
+    """Raw pinned H2D GB/s of host -> dev (the e2e step's PCIe bound),
+    best of 3 copies timed with CUDA events."""
+    import torch
+
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dev.copy_(host, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, host.numel() * host.element_size() / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    return best
+
+
+def distributions_leg(a, P, ctx, dev, start, stop, peak, check_parity):
+    """BASELINE configs[1] (uniform square 1e8, pure streaming) and
+    configs[3] (circumference 1e8, nothing filtered: compaction- and
+    hull-bound), device-resident, 5 timed steps each, then checked against
+    the reference's heaphull_run on the same points."""
+    import numpy as np
+    import torch
+
+    out = []
+    for dname, dn in (("square", 100_000_000), ("circle", 100_000_000)):
+        hbuf = torch.empty((dn, 2), dtype=torch.float64, pin_memory=True)
+        hp = hbuf.numpy()
+        P.check(P.lib.ohx_generate(P.DISTS[dname], dn, a.seed, 0.0, hp.ctypes.data_as(P._dp), 0))
+        dd = hbuf.to(dev)
+        for _ in range(2):
+            ctx.heaphull_device(dd, dn)
+        torch.cuda.synchronize()
+        ctx.kernel_ms_sum(reset=True)
+        start.record()
+        for _ in range(5):
+            hull, _ = ctx.heaphull_device(dd, dn)
+        stop.record()
+        torch.cuda.synchronize()
+        dms = start.elapsed_time(stop) / 5
+        ksum = ctx.kernel_ms_sum()
+        info = ctx.last_run()
+        stream_ms = ksum["k1"][0] / max(1, ksum["k1"][1])
+        k_bytes = 16 * dn + (4 * info["candidates"] if info["fused"] else 0)
+        row = {"dist": dname, "points": dn, "seed": a.seed, "value": dn / (dms * 1e-3) / 1e9,
+               "unit": UNIT, "ms_per_step": dms, "fused": info["fused"],
+               "survivors": sum(info["counts"]), "h": int(len(hull)),
+               "streaming_kernel": "kf_filter" if info["fused"] else "k1_extremes",
+               "streaming_ms": stream_ms,
+               "streaming_gbs": k_bytes / (stream_ms * 1e-3) / 1e9,
+               "streaming_frac": k_bytes / (stream_ms * 1e-3) / 1e9 / peak,
+               "k2_ms": ksum["k2"][0] / max(1, ksum["k2"][1])}
+        if check_parity:
+            from oracle import Reference
+            if Reference.available():
+                rec = ctx.extremes(dd, dn)  # the library's find_extremes on the device points
+                e, mask = P.resolve_extremes(rec)
+                if mask:
+                    e = P.apply_corners(e, ctx.corners_exact(dd, dn, (rec.x[0], rec.y[1],
+                                                                      rec.x[2], rec.y[3])))
+                hull, _ = ctx.heaphull_device(dd, dn)  # the queues of this very call are checked
+                row["parity"] = reference_parity(Reference(), hp, ctx, hull, list(e.ext))
+        out.append(row)
+        del dd, hbuf, hp
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_b200_arm(a):
     import numpy as np
     import torch
@@ -261,16 +402,23 @@ def run_b200_arm(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    n = int(a.n)
-    base = rank * n
+    def sum_over_ranks(v: int) -> int:
+        if world == 1:
+            return int(v)
+        t = torch.tensor([int(v)], dtype=torch.int64, device=xdev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return int(t.item())
+
+    j = job(a, world)
+    total = j["total"]
+    base, n = shard_of(total, world, rank)
     t0 = time.perf_counter()
     try:  # pinned: the e2e step's H2D runs at PCIe speed
         host = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
     except RuntimeError:  # e.g. 8 ranks x 16 GB beyond the host's pinnable memory
         host = torch.empty((n, 2), dtype=torch.float64)
     hp = host.numpy()
-    P.check(P.lib.ohx_generate(P.DISTS[a.dist], n, a.seed + rank, 0.0,
-                               hp.ctypes.data_as(P._dp), 0))
+    P.generate_range(a.dist, total, base, n, a.seed, out=hp)
     d = host.to(dev)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
@@ -290,6 +438,7 @@ def run_b200_arm(a):
     if rank == 0 and world == 1:
         hull1 = step_device()
         assert np.array_equal(hull0, hull1), "pipeline disagreement"
+    survivors_job = sum_over_ranks(sum(stats["counts"]))
 
     # ---------------- device-resident timed region
     for _ in range(a.warmup):
@@ -310,13 +459,14 @@ def run_b200_arm(a):
     last = ctx.last_run()
     runs = [dict(last, fused=last["fused"] and ksum["kc"][1] == a.steps)]
     ms = max_over_ranks(start.elapsed_time(stop) / a.steps)
-    value = world * n / (ms * 1e-3) / 1e9
+    value = total / (ms * 1e-3) / 1e9
 
     # ---------------- e2e through the host-buffer API
     e2e = None
+    clocks_e2e_summary = None
     if not a.no_e2e:
-        s_local = sum(stats["counts"])
         if world == 1:
+            s_local = sum(stats["counts"])
             out = np.empty((n + 8, 2), dtype=np.float64) if n < 10_000_000 else np.empty((s_local + 8 + 64, 2))
             h = P.C.c_uint64(0)
 
@@ -340,15 +490,23 @@ def run_b200_arm(a):
             stop.record()
             barrier()
         ms_e2e = max_over_ranks(start.elapsed_time(stop) / a.steps)
-        e2e = {"value": world * n / (ms_e2e * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_e2e,
-               "h2d_bytes_per_step": world * n * 16,
-               "d2h_bytes_per_step": sum(stats["counts"]) * 16 * world + 2 * 320,
+        # the bound of this step: the raw pinned H2D of the same buffer
+        h2d = h2d_bandwidth(host, d if world == 1 else d2) if host.is_pinned() else None
+        h2d = max_over_ranks(h2d or 0.0) if world > 1 else h2d
+        e2e_gbs = total * 16 / (ms_e2e * 1e-3) / 1e9
+        e2e = {"value": total / (ms_e2e * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": total * 16,
+               # survivors' coordinates (16 B each) + the two small records
+               "d2h_bytes_per_step": survivors_job * 16 + world * 2 * 320,
                "api": ("ohx_heaphull (C ABI) on {} host points" if world == 1
                        else "sharded_heaphull with per-rank {} shard H2D").format(
-                           "pinned" if host.is_pinned() else "pageable")}
+                           "pinned" if host.is_pinned() else "pageable"),
+               "roofline": {"bound": "pcie", "achieved": e2e_gbs, "unit": "GB/s",
+                            "peak": h2d, "frac": e2e_gbs / h2d if h2d else None,
+                            "peak_source": "raw pinned H2D of the same buffer, measured in this "
+                                           "run (best of 3, CUDA events)"
+                                           + (", max over ranks" if world > 1 else "")}}
         clocks_e2e_summary = clocks_e2e.summary()
-    else:
-        clocks_e2e_summary = None
 
     # ---------------- roofline of the dominant kernel
     # algorithmic bytes per launch: every point read once by the
@@ -379,13 +537,16 @@ def run_b200_arm(a):
         v["gbs"] = v["bytes"] / (v["ms"] * 1e-3) / 1e9
         v["frac"] = v["gbs"] / peak
     dom = max(kern, key=lambda k: kern[k]["ms"])
-    traffic = None
+    traffic, traffic_src = None, None
     tr = ncu_traffic()
     if tr and dom in tr:
         traffic = tr[dom]["dram_bytes_per_point"] * n
+        traffic_src = (f"not measured in this run: dram__bytes_read.sum + dram__bytes_write.sum "
+                       f"per point from the committed ncu --set full capture "
+                       f"({tr.get('source', 'profiles/ncu_traffic.json')}) x {n} points")
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak,
                 "unit": "GB/s", "frac": kern[dom]["gbs"] / peak, "traffic": traffic,
-                "peak_source": peak_src,
+                "traffic_source": traffic_src, "peak_source": peak_src,
                 "algorithmic_bytes": kern[dom]["bytes"],
                 "kernels": kern,
                 "pipeline": "fused single pass (KF)" if fused else "two passes (K1, K2)",
@@ -395,94 +556,39 @@ def run_b200_arm(a):
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        ns = int(a.cpu_sample)
-        r = cpu_reference(ns, 2, a.seed, a.dist, pts=None if ns else hp)
-        ns = r["n"]
+        ns = min(n, int(a.cpu_sample) or n)
+        pts = hp[:ns]
+        r = cpu_reference(pts, 2)
         t = statistics.mean(r["times"])
         cpu = {"value": ns / t / 1e9, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
                "sample": f"{a.dist} n={ns} seed={a.seed}"
-                         f"{' (the bench workload itself)' if ns == n else ''}, reference "
-                         f"heaphull_run x2 (ReduceEngine chunk 32, {r['cores']} workers), "
+                         f"{' (the bench workload itself)' if ns == n else ' (the first points of the workload)'}"
+                         f", reference heaphull_run x2 (ReduceEngine chunk 32, {r['cores']} workers), "
                          f"mean {t:.3f} s"}
-        # the same leg checks the device results against the reference's
-        # own heaphull_run / find_extremes on these very points (outside
-        # every timed region; the reference is the checker here)
         if not a.no_parity and r["kind"] == "reference" and ns == n:
             from oracle import Reference
-            if Reference.available():
-                ref = Reference()
-                cores = os.cpu_count() or 1
-                t0 = time.perf_counter()
-                ref_hull, ref_labels, _ = ref.heaphull_run(hp, cores, 32)
-                ref_ext = ref.find_extremes(hp, cores, 32)
-                ref_s = time.perf_counter() - t0
-                hull_dev = step_device()
-                info = ctx.last_run()
-                queues_ok = True
-                for q in range(4):
-                    want = np.flatnonzero(ref_labels == q + 1)
-                    got = ctx.queue(q + 1, info["counts"][q])[0]
-                    queues_ok &= bool(np.array_equal(got, want))
-                parity = {"checked_against": f"reference heaphull_run + find_extremes (oracle/_ref, "
-                                             f"{cores} workers) on the same {n} points",
-                          "hull_equal": bool(np.array_equal(hull_dev, ref_hull)),
-                          "extremes_equal": stats["ext"] == [int(v) for v in ref_ext],
-                          "queues_equal": queues_ok,
-                          "survivors": int((ref_labels != 0).sum()), "h": int(len(ref_hull)),
-                          "reference_s": ref_s}
-                del ref_labels
-            else:
-                parity = {"checked_against": None, "why": "oracle/_ref not built"}
+            hull_dev = step_device()
+            parity = reference_parity(Reference(), hp, ctx, hull_dev, stats["ext"])
 
-    # ---------------- the other distributions (rank 0, N = 1): BASELINE
-    # configs[1] (uniform square 1e8, pure streaming) and configs[3]
-    # (circumference 1e8, nothing filtered: compaction- and hull-bound),
-    # device-resident, 5 timed steps each
+    # ---------------- the other distributions (rank 0, N = 1)
     dists = None
     if rank == 0 and world == 1 and not a.no_dists:
-        dists = []
-        for dname, dn in (("square", 100_000_000), ("circle", 100_000_000)):
-            hbuf = torch.empty((dn, 2), dtype=torch.float64, pin_memory=True)
-            P.check(P.lib.ohx_generate(P.DISTS[dname], dn, a.seed, 0.0,
-                                       hbuf.numpy().ctypes.data_as(P._dp), 0))
-            dd = hbuf.to(dev)
-            del hbuf
-            for _ in range(2):
-                ctx.heaphull_device(dd, dn)
-            torch.cuda.synchronize()
-            start.record()
-            kms = []
-            for _ in range(5):
-                ctx.heaphull_device(dd, dn)
-                kms.append(ctx.kernel_ms())
-            stop.record()
-            torch.cuda.synchronize()
-            dms = start.elapsed_time(stop) / 5
-            info = ctx.last_run()
-            k_ms = statistics.mean(k["k1"] for k in kms)
-            k_bytes = 16 * dn + (4 * info["candidates"] if info["fused"] else 0)
-            dists.append({"dist": dname, "points": dn, "value": dn / (dms * 1e-3) / 1e9,
-                          "unit": UNIT, "ms_per_step": dms, "fused": info["fused"],
-                          "survivors": sum(info["counts"]),
-                          "streaming_kernel": "kf_filter" if info["fused"] else "k1_extremes",
-                          "streaming_gbs": k_bytes / (k_ms * 1e-3) / 1e9,
-                          "streaming_frac": k_bytes / (k_ms * 1e-3) / 1e9 / peak})
-            del dd
-            torch.cuda.empty_cache()
+        del d
+        torch.cuda.empty_cache()
+        dists = distributions_leg(a, P, ctx, dev, start, stop, peak, not a.no_parity)
 
     if rank == 0:
         clk = clocks.summary()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64",
-            "data": f"synthetic: reference generator ({a.dist}, seed {a.seed}+rank), bit-identical",
-            "config": {"workload": workload(a.dist, n), "dist": a.dist, "points_per_gpu": n,
-                       "points_total": world * n, "parallelism": f"index-range shards x{world}",
-                       "l2": f"inputs {n * 16 / 1e9:.3g} GB/GPU vs 126 MB L2"
-                             + (" (no flush needed)" if n * 16 > 4 * 126e6 else " (L2-resident: not a roofline point)"),
-                       "survivors": stats["counts"], "corner_certificate": "pass" if not
-                       stats["uncertified"] else f"fallback mask {stats['uncertified']}"},
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": j["scaling"], "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic: generate({a.dist}, {total}, seed {a.seed}) -- bit-identical to "
+                    f"the reference generator, each rank generating its own slice",
+            "config": config(a, world),
+            "run": {"survivors": survivors_job, "survivors_rank0": stats["counts"],
+                    "corner_certificate": "pass" if not stats["uncertified"]
+                    else f"fallback mask {stats['uncertified']}", "fused": stats.get("fused")},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
             "distributions": dists, "clocks": clk,
             "clocks_e2e": clocks_e2e_summary, "gpu_launches": launches,

@@ -292,6 +292,11 @@ int ohx_monotone_chain(const double* h_xy, uint64_t n, double* h_hull,
  * reference's single-threaded stream; threads = 0 -> all cores. */
 int ohx_generate(int dist, uint64_t n, uint64_t seed, double distort_pct,
                  double* h_xy, int threads);
+/* Points [lo, lo + count) of the same n-point corpus: a shard's slice of
+ * generate({dist, n, seed, distort}) without generating the rest (normal:
+ * the rejection attempts before lo are counted, not emitted). */
+int ohx_generate_range(int dist, uint64_t n, uint64_t seed, double distort_pct,
+                       uint64_t lo, uint64_t count, double* h_xy, int threads);
 
 /* The strict-left-turn chain of an arc already in sweep order (the loop of
  * quadrant_hull, hull.cpp:140-149, without its sort): h_out receives the

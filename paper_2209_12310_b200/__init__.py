@@ -24,7 +24,7 @@ import numpy as np
 from ._lib import (DISTS, OHX_E_INVALID, SLOTS, CornerRec, ExtremeSet, ExtremesRec, FilterPlan,
                    OhxError, RunInfo, check, lib)
 
-__all__ = ["classify", "filter_rate", "generate", "heaphull", "heaphull_file", "hull_indices", "write_pts2",
+__all__ = ["classify", "filter_rate", "generate", "generate_range", "heaphull", "heaphull_file", "hull_indices", "write_pts2",
            "monotone_chain",
            "heaphull_run", "find_extremes", "Context", "OhxError", "device_count"]
 
@@ -61,6 +61,22 @@ def generate(dist: str, n: int, seed: int = 0, distort: float = 0.0, threads: in
     out = np.empty((max(int(n), 0), 2), dtype=np.float64)
     check(lib.ohx_generate(DISTS[dist], int(n), int(seed), float(distort),
                            out.ctypes.data_as(_dp), int(threads)))
+    return out
+
+
+def generate_range(dist: str, n: int, lo: int, count: int, seed: int = 0, distort: float = 0.0,
+                   threads: int = 0, out=None) -> np.ndarray:
+    """Points [lo, lo + count) of generate(dist, n, seed, distort) -- a
+    shard's slice of the corpus, without generating the rest.  `out`
+    (optional) is a C-contiguous (count, 2) float64 buffer to fill."""
+    if dist not in DISTS:
+        raise ValueError(f"unknown distribution '{dist}' (expected normal|square|disk|circle)")
+    if out is None:
+        out = np.empty((max(int(count), 0), 2), dtype=np.float64)
+    if out.shape != (int(count), 2) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous (count, 2) float64 array")
+    check(lib.ohx_generate_range(DISTS[dist], int(n), int(seed), float(distort), int(lo),
+                                 int(count), out.ctypes.data_as(_dp), int(threads)))
     return out
 
 

@@ -105,6 +105,7 @@ PROTOTYPES = [
     ("ohx_chain", C.c_int, [_dp, _u64, _dp, _u64p]),
     ("ohx_hull_from_sorted_arcs", C.c_int, [C.POINTER(_dp), _u64p, _dp, _u64, _u64p]),
     ("ohx_generate", C.c_int, [C.c_int, _u64, _u64, C.c_double, _dp, C.c_int]),
+    ("ohx_generate_range", C.c_int, [C.c_int, _u64, _u64, C.c_double, _u64, _u64, _dp, C.c_int]),
     ("ohx_hull_from_queues", C.c_int, [_dp, _u64p, C.POINTER(_u64p), _u64p, _dp, _u64, _u64p]),
     ("ohx_hull_from_queue_points", C.c_int, [_dp, C.POINTER(_dp), _u64p, _dp, _u64, _u64p]),
 ]

@@ -61,10 +61,18 @@ int ohx_ctx_default(int device, ohx_ctx** out) {
 
 int ohx_ctx_device(const ohx_ctx* ctx) { return ctx ? ctx->device : -1; }
 
-uint64_t ohx_ctx_launches(const ohx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+// both read state that pipeline calls write under the context's lock
+uint64_t ohx_ctx_launches(const ohx_ctx* ctx) {
+  if (!ctx) return 0;
+  std::lock_guard<std::mutex> g(const_cast<ohx_ctx*>(ctx)->mu);
+  return ctx->launches;
+}
 
 int ohx_ctx_last_run(const ohx_ctx* ctx, ohx_run_info* info) {
-  return guard([&] { *info = ctx->last_run; });
+  return guard([&] {
+    std::lock_guard<std::mutex> g(const_cast<ohx_ctx*>(ctx)->mu);
+    *info = ctx->last_run;
+  });
 }
 
 int ohx_ctx_kernel_ms(ohx_ctx* ctx, double ms[4]) {

@@ -281,16 +281,20 @@ std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
       off += len[q];
     }
     std::atomic<int> failed{cudaSuccess};  // set by the arc threads (no throwing there)
-    const std::size_t h = hull_from_sorted_arcs(
-        arcs, len,
-        [&](int q) {
-          const cudaError_t e = cudaEventSynchronize(c->arc_ev[q]);
-          if (e != cudaSuccess) failed = e;
-        },
-        [&](std::size_t hh) {
-          check_cuda(static_cast<cudaError_t>(failed.load()), "cudaEventSynchronize(sorted arc)");
-          return sink(hh);
-        });
+    std::size_t h = 0;
+    try {
+      h = hull_from_sorted_arcs(
+          arcs, len,
+          [&](int q) {
+            const cudaError_t e = cudaEventSynchronize(c->arc_ev[q]);
+            if (e != cudaSuccess) failed = e;
+            return e == cudaSuccess;
+          },
+          sink);
+    } catch (...) {  // a lost arc: report the CUDA error behind it
+      check_cuda(static_cast<cudaError_t>(failed.load()), "cudaEventSynchronize(sorted arc)");
+      throw;
+    }
     tr.mark("hull D2H + host");
     return h;
   }

@@ -26,6 +26,7 @@
 #include <parallel/algorithm>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -713,7 +714,7 @@ struct ChainedArcs {
 // points run in parallel chunks (all arcs' chunks in one parallel loop);
 // wait_arc(q) is called before arc q is read.
 std::unique_ptr<ChainedArcs> run_chains(const P2* const arcs[4], const std::uint64_t len[4],
-                                        const std::function<void(int)>& wait_arc) {
+                                        const ArcWait& wait_arc) {
   const std::size_t par_min = chain_par_min();
   static const std::size_t chunks = std::max<std::size_t>(2, env_size("OHX_CHAIN_CHUNKS", 16));
   auto R = std::make_unique<ChainedArcs>();
@@ -738,11 +739,21 @@ std::unique_ptr<ChainedArcs> run_chains(const P2* const arcs[4], const std::uint
   });
   const std::uint64_t total = len[0] + len[1] + len[2] + len[3];
   const double t0 = now_ms();
+  // an arc whose input never arrived (wait_arc false) is not chained: the
+  // caller learns of the failure at once instead of after chaining garbage
+  std::atomic<bool> lost[4] = {false, false, false, false};
 #pragma omp parallel for schedule(dynamic, 1) if (total >= (1u << 12))
   for (std::int64_t i = 0; i < static_cast<std::int64_t>(tasks.size()); ++i) {
-    if (wait_arc) wait_arc(tasks[i].q);
-    A[tasks[i].q].local_run(tasks[i].j);
+    const int q = tasks[i].q;
+    if (lost[q] || (wait_arc && !wait_arc(q))) {
+      lost[q] = true;
+      continue;
+    }
+    A[q].local_run(tasks[i].j);
   }
+  for (int q = 0; q < 4; ++q)
+    if (lost[q]) throw std::runtime_error("hull stage: the input of arc " + std::to_string(q + 1) +
+                                          " did not arrive");
   const double t1 = now_ms();
 #pragma omp parallel for schedule(dynamic, 1) if (total >= (1u << 12))
   for (int q = 0; q < 4; ++q)
@@ -820,7 +831,7 @@ PieceScan scan_pieces(const PieceCycle& c, P2* dst = nullptr) {
 }  // namespace
 
 PVec chain_arcs(const P2* const arcs[4], const std::uint64_t len[4],
-                const std::function<void(int)>& wait_arc) {
+                const ArcWait& wait_arc) {
   auto R = run_chains(arcs, len, wait_arc);
   PVec cycle(R->cycle.n);
   R->cycle.copy_out_parallel(cycle.data(), 0, R->cycle.n);
@@ -926,7 +937,7 @@ PVec finalize_cycle(PVec cycle) {
 }
 
 std::size_t hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
-                                  const std::function<void(int)>& wait_arc, const HullSink& sink) {
+                                  const ArcWait& wait_arc, const HullSink& sink) {
   const std::uint64_t total = len[0] + len[1] + len[2] + len[3];
   const double t0 = now_ms();
   auto R = run_chains(arcs, len, wait_arc);
@@ -974,7 +985,7 @@ std::size_t hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t l
 }
 
 PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
-                           const std::function<void(int)>& wait_arc) {
+                           const ArcWait& wait_arc) {
   PVec out;
   hull_from_sorted_arcs(arcs, len, wait_arc, [&](std::size_t h) {
     out.resize(h);

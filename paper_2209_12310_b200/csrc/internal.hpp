@@ -236,11 +236,14 @@ using PVec = std::vector<P2, DefaultInitAlloc<P2>>;
 void copy_points(P2* dst, const P2* src, std::size_t n);
 
 PVec quadrant_chain(std::vector<P2> pts, int quadrant);
+// wait_arc(q): called before arc q is read (the arcs may still be arriving
+// from the device); false = its input will never arrive (the stage throws)
+using ArcWait = std::function<bool(int)>;
 // chain of an arc already in sweep order (the arc's last point dropped)
 PVec chain_sorted(const P2* pts, std::size_t n);
 // the four arcs' chains concatenated (the cycle of hull.cpp:164-183)
 PVec chain_arcs(const P2* const arcs[4], const std::uint64_t len[4],
-                const std::function<void(int)>& wait_arc);
+                const ArcWait& wait_arc);
 // The hull stage's sweep sort on the device (hullsort.cu): the four arcs
 // [anchor q, queue q (packed [q1|q2|q3|q4] coordinates), anchor q+1], each
 // sorted in its quadrant's sweep order, written back to back to d_sorted
@@ -253,13 +256,13 @@ void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const doub
 // (wait_arc(q), when set, is called by arc q's thread before it reads the
 // arc: the arcs may still be arriving from the device)
 PVec hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
-                           const std::function<void(int)>& wait_arc = {});
+                           const ArcWait& wait_arc = {});
 // Same, the hull written to sink(h) (it returns where h vertices go and may
 // throw; it may first be called with a larger size -- the chained cycle
 // before its clean-up -- the last call's size is the hull's); returns h.
 using HullSink = std::function<P2*(std::size_t)>;
 std::size_t hull_from_sorted_arcs(const P2* const arcs[4], const std::uint64_t len[4],
-                                  const std::function<void(int)>& wait_arc, const HullSink& sink);
+                                  const ArcWait& wait_arc, const HullSink& sink);
 PVec finalize_cycle(PVec cycle);
 PVec hull_from_queue_points(const P2 anchors[4], const P2* const q_pts[4],
                             const std::uint64_t q_len[4]);
@@ -275,5 +278,8 @@ std::string nonfinite_message(std::uint64_t i);
 // ---- host generator (pointgen.cpp)
 void generate_points(int dist, std::uint64_t n, std::uint64_t seed,
                      double distort_pct, double* xy, int threads);
+// points [lo, lo + cnt) of the same n-point corpus (a shard's slice)
+void generate_points_range(int dist, std::uint64_t n, std::uint64_t seed, double distort_pct,
+                           std::uint64_t lo, std::uint64_t cnt, double* xy, int threads);
 
 }  // namespace ohx

@@ -187,6 +187,13 @@ int ohx_generate(int dist, uint64_t n, uint64_t seed, double distort_pct, double
   return guard([&] { ohx::generate_points(dist, n, seed, distort_pct, h_xy, threads); });
 }
 
+int ohx_generate_range(int dist, uint64_t n, uint64_t seed, double distort_pct, uint64_t lo,
+                       uint64_t count, double* h_xy, int threads) {
+  return guard([&] {
+    ohx::generate_points_range(dist, n, seed, distort_pct, lo, count, h_xy, threads);
+  });
+}
+
 int ohx_hull_from_queues(const double* h_xy, const uint64_t ext_axis[4],
                          const uint64_t* const q_idx[4], const uint64_t q_len[4],
                          double* h_hull, uint64_t cap, uint64_t* h) {

@@ -72,12 +72,17 @@ inline bool normal_accepts(std::uint64_t seed, std::uint64_t a) {
   return !(s >= 1.0 || s == 0.0);
 }
 
-void gen_normal(std::uint64_t n, std::uint64_t seed, double* xy, int threads) {
+// outputs [lo, lo + cnt) of the normal stream: attempts are counted block
+// by block until lo + cnt points are accepted; only the blocks whose
+// outputs meet the range are emitted
+void gen_normal(std::uint64_t lo, std::uint64_t cnt, std::uint64_t seed, double* xy,
+                int threads) {
+  const std::uint64_t end = lo + cnt;
   std::vector<std::uint64_t> accepted;  // per attempt block
   std::uint64_t have = 0;
-  while (have < n) {
+  while (have < end) {
     // acceptance is pi/4; overshoot slightly, then extend if still short
-    const std::uint64_t want = n - have;
+    const std::uint64_t want = end - have;
     const std::uint64_t more =
         std::max<std::uint64_t>(1, (want * 1.28 + 4096) / kAttemptBlock + 1);
     const std::uint64_t first = accepted.size();
@@ -98,13 +103,15 @@ void gen_normal(std::uint64_t n, std::uint64_t seed, double* xy, int threads) {
   }
   parallel_for(accepted.size(), threads, [&](std::uint64_t b) {
     std::uint64_t out = start[b];
-    if (out >= n) return;
+    if (out >= end || out + accepted[b] <= lo) return;
     const std::uint64_t a0 = b * kAttemptBlock;
-    for (std::uint64_t a = a0; a < a0 + kAttemptBlock && out < n; ++a) {
+    for (std::uint64_t a = a0; a < a0 + kAttemptBlock && out < end; ++a) {
       double x, y;
       if (normal_attempt(seed, a, x, y)) {
-        xy[2 * out] = x;
-        xy[2 * out + 1] = y;
+        if (out >= lo) {
+          xy[2 * (out - lo)] = x;
+          xy[2 * (out - lo) + 1] = y;
+        }
         ++out;
       }
     }
@@ -115,6 +122,11 @@ void gen_normal(std::uint64_t n, std::uint64_t seed, double* xy, int threads) {
 
 void generate_points(int dist, std::uint64_t n, std::uint64_t seed,
                      double distort_pct, double* xy, int threads) {
+  generate_points_range(dist, n, seed, distort_pct, 0, n, xy, threads);
+}
+
+void generate_points_range(int dist, std::uint64_t n, std::uint64_t seed, double distort_pct,
+                           std::uint64_t lo, std::uint64_t cnt, double* xy, int threads) {
   // validation and messages of reference pointgen.cpp:45-55
   if (n < 1) throw std::invalid_argument("generate: n must be >= 1");
   if (distort_pct < 0.0) throw std::invalid_argument("generate: distort_pct must be >= 0");
@@ -122,19 +134,21 @@ void generate_points(int dist, std::uint64_t n, std::uint64_t seed,
     throw std::invalid_argument("generate: distortion applies to the circle distribution only");
   if (dist < OHX_NORMAL || dist > OHX_CIRCLE)
     throw std::invalid_argument("unknown distribution value");
+  if (lo > n || cnt > n - lo) throw std::invalid_argument("generate: range outside [0, n)");
+  if (cnt == 0) return;
   if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-  if (n < 4 * kPointBlock) threads = 1;
+  if (lo + cnt < 4 * kPointBlock) threads = 1;
 
   if (dist == OHX_NORMAL) {
-    gen_normal(n, seed, xy, threads);
+    gen_normal(lo, cnt, seed, xy, threads);
     return;
   }
   constexpr double two_pi = 2.0 * std::numbers::pi;
   const double scale = distort_pct / 100.0;
-  const std::uint64_t blocks = (n + kPointBlock - 1) / kPointBlock;
+  const std::uint64_t blocks = (cnt + kPointBlock - 1) / kPointBlock;
   parallel_for(blocks, threads, [&](std::uint64_t b) {
-    const std::uint64_t i1 = std::min(n, (b + 1) * kPointBlock);
-    for (std::uint64_t i = b * kPointBlock; i < i1; ++i) {
+    const std::uint64_t i1 = lo + std::min(cnt, (b + 1) * kPointBlock);
+    for (std::uint64_t i = lo + b * kPointBlock; i < i1; ++i) {
       const double u1 = unit_at(seed, 2 * i + 1);
       const double u2 = unit_at(seed, 2 * i + 2);
       double x, y;
@@ -153,8 +167,8 @@ void generate_points(int dist, std::uint64_t n, std::uint64_t seed,
         x = r * std::cos(th);
         y = r * std::sin(th);
       }
-      xy[2 * i] = x;
-      xy[2 * i + 1] = y;
+      xy[2 * (i - lo)] = x;
+      xy[2 * (i - lo) + 1] = y;
     }
   });
 }

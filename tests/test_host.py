@@ -53,6 +53,20 @@ def test_generator_bit_exact(oracle, dist, n, seed, d):
     assert np.array_equal(a, P.generate(dist, n, seed, d, threads=3))
 
 
+@pytest.mark.parametrize("dist,d", [("normal", 0.0), ("square", 0.0), ("disk", 0.0),
+                                    ("circle", 2.0)])
+def test_generator_range_is_a_slice_of_the_corpus(oracle, dist, d):
+    # a shard's slice (bench.py at N > 1: rank r generates only its range
+    # of generate({dist, n_total, seed}))
+    n = 1_000_003
+    whole = oracle.generate(dist, n, 11, d)
+    for lo, cnt in [(0, 1), (0, n), (1, 262144), (333_333, 333_334), (n - 5, 5), (n, 0)]:
+        got = P.generate_range(dist, n, lo, cnt, 11, d, threads=4)
+        assert np.array_equal(got, whole[lo: lo + cnt]), (lo, cnt)
+    with pytest.raises(ValueError):
+        P.generate_range(dist, n, n - 1, 2, 11, d)
+
+
 def test_generator_errors():
     with pytest.raises(ValueError):
         P.generate("triangle", 10)

@@ -150,10 +150,11 @@ def test_bench_multi_rank_path_on_one_gpu(tmp_path):
     env = dict(os.environ, OHX_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(root, "bench.py"), "--gpus", "2", "--points", "1.2e7", "--steps", "3",
+           os.path.join(root, "bench.py"), "--gpus", "2", "--points-total", "2.4e7", "--steps", "3",
            "--warmup", "3"]
     r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900, cwd=root)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["points_total"] == 24_000_000
+    assert line["scaling"] == "strong" and line["config"]["points_per_gpu"] == 12_000_000
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0

@@ -78,9 +78,24 @@ for name, dist, n, seed, distort in CONFIGS:
         ts = []
         for r in range(2):
             t0 = time.perf_counter()
-            hh, _ = eng.heaphull(hp)
+            eng.heaphull(hp)
             ts.append((time.perf_counter() - t0) * 1e3)
         line["ref_ms"] = min(ts)
         line["ref_cores"] = os.cpu_count()
         line["speedup_host_api_vs_ref"] = line["ref_ms"] / line["host_api_ms"]
+        # parity on the same bytes: the reference's hull, labels and
+        # extremes against the device pipeline's hull, queues and extremes
+        ref_hull, ref_labels, _ = ref.heaphull_run(hp, os.cpu_count() or 1, 32)
+        d = host.cuda()
+        hull_dev, _ = ctx.heaphull_device(d, n)
+        info = ctx.last_run()
+        q_ok = all(np.array_equal(ctx.queue(q + 1, info["counts"][q])[0],
+                                  np.flatnonzero(ref_labels == q + 1)) for q in range(4))
+        line["parity"] = {"hull_equal": bool(np.array_equal(hull_dev, ref_hull)),
+                          "queues_equal": bool(q_ok),
+                          "extremes_equal": [int(v) for v in ref.find_extremes(hp, os.cpu_count() or 1)]
+                          == [int(v) for v in P.find_extremes(hp)],
+                          "h_ref": int(len(ref_hull))}
+        del d, ref_labels
+        torch.cuda.empty_cache()
     print(json.dumps(line), flush=True)
