@@ -261,6 +261,11 @@ int ohx_heaphull_device(ohx_ctx* ctx, const double* d_xy, uint64_t n,
 /* classify (python/module.cpp:91-108): find_extremes + build_octagon +
  * classify_points, labels to the host. */
 int ohx_classify(const double* h_xy, uint64_t n, uint8_t* h_labels);
+/* classify_points (filter.cpp:104-131) with the caller's polygon (m
+ * vertices, any m -- build_octagon makes <= 8, callers may pass more) and
+ * ExtremeSet ext[8] in slot order; labels to the host. */
+int ohx_classify_points(const double* h_xy, uint64_t n, const double* poly_xy, uint64_t m,
+                        const uint64_t ext[8], uint8_t* h_labels);
 /* heaphull_run (hull.cpp:152-194): hull + labels + timings. */
 int ohx_heaphull_run(const double* h_xy, uint64_t n, double* h_hull,
                      uint64_t cap, uint64_t* h, uint8_t* h_labels,

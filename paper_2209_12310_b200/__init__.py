@@ -24,7 +24,7 @@ import numpy as np
 from ._lib import (DISTS, OHX_E_INVALID, SLOTS, CornerRec, ExtremeSet, ExtremesRec, FilterPlan,
                    OhxError, RunInfo, check, lib)
 
-__all__ = ["classify", "filter_rate", "generate", "generate_range", "heaphull", "heaphull_file", "hull_indices", "write_pts2",
+__all__ = ["classify", "classify_points", "filter_rate", "generate", "generate_range", "heaphull", "heaphull_file", "hull_indices", "write_pts2",
            "monotone_chain",
            "heaphull_run", "find_extremes", "Context", "OhxError", "device_count"]
 
@@ -155,6 +155,21 @@ def classify(points, threads: int = 1, chunk: int = 32) -> np.ndarray:
     if len(a) == 0:
         raise ValueError("find_axis_extremes: empty point set")
     check(lib.ohx_classify(a.ctypes.data_as(_dp), len(a), labels.ctypes.data_as(_u8p)))
+    return labels
+
+
+def classify_points(points, polygon, ext) -> np.ndarray:
+    """classify_points with a given polygon (any vertex count) and
+    ExtremeSet (8 indices {east, north, west, south, ne, nw, sw, se})."""
+    a = _points(points)
+    poly = np.ascontiguousarray(polygon, dtype=np.float64).reshape(-1, 2)
+    e = np.ascontiguousarray(ext, dtype=np.uint64)
+    if e.shape != (8,):
+        raise ValueError("ext must hold 8 indices")
+    labels = np.empty(len(a), dtype=np.uint8)
+    check(lib.ohx_classify_points(a.ctypes.data_as(_dp), len(a), poly.ctypes.data_as(_dp),
+                                  len(poly), e.ctypes.data_as(_u64p),
+                                  labels.ctypes.data_as(_u8p)))
     return labels
 
 

@@ -96,6 +96,7 @@ PROTOTYPES = [
     ("ohx_hull_indices", C.c_int, [_vp, _dp, _u64, _u64p, _vp]),
     ("ohx_hull_indices_partial", C.c_int, [_vp, _dp, _u64, _u64p, _vp]),
     ("ohx_classify", C.c_int, [_dp, _u64, _u8p]),
+    ("ohx_classify_points", C.c_int, [_dp, _u64, _dp, _u64, _u64p, _u8p]),
     ("ohx_heaphull_run", C.c_int, [_dp, _u64, _dp, _u64, _u64p, _u8p, _dp]),
     ("ohx_pts2_count", C.c_int, [C.c_char_p, _u64p]),
     ("ohx_pts2_load_device", C.c_int, [_vp, C.c_char_p, _vp, _u64, _u64p, _vp]),

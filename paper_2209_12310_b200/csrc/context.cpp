@@ -26,8 +26,8 @@
 
 namespace ohx {
 
-void dev_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what) {
-  if (*have >= need && *p) return;
+bool dev_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what) {
+  if (*have >= need && *p) return false;
   if (*p) check_cuda(cudaFree(*p), "cudaFree");
   *p = nullptr;
   *have = 0;
@@ -39,6 +39,7 @@ void dev_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* wha
                                  cudaGetErrorString(e));
   }
   *have = need;
+  return true;
 }
 
 cudaStream_t pick(ohx_ctx* c, void* s) {
@@ -73,6 +74,7 @@ void check_cuda(cudaError_t e, const char* what) {
 cudaStream_t ctx_stream(ohx_ctx* c) { return c->stream; }
 std::mutex& ctx_mutex(ohx_ctx* c) { return c->mu; }
 void ctx_bind(ohx_ctx* c) { bind(c); }
+void ctx_set_host_lanes(ohx_ctx* c, int lanes) { c->host_lanes = lanes; }
 
 // ---- host <-> device copies of user buffers.  Page-locked memory is
 // copied directly; pageable memory (std::vector, numpy: what the reference's
@@ -101,12 +103,12 @@ void ensure_stage(ohx_ctx* c) {
   }
 }
 
-void host_memcpy(void* dst, const void* src, std::uint64_t bytes) {
-  if (bytes < (8ull << 20)) {
+void host_memcpy(void* dst, const void* src, std::uint64_t bytes, int lanes) {
+  if (bytes < (8ull << 20) || lanes == 1) {
     std::memcpy(dst, src, bytes);
     return;
   }
-#pragma omp parallel
+#pragma omp parallel num_threads(team(lanes > 0 ? lanes : omp_get_max_threads()))
   {
     const int t = omp_get_thread_num(), nt = omp_get_num_threads();
     const std::uint64_t b = bytes * t / nt, e = bytes * (t + 1) / nt;
@@ -126,7 +128,7 @@ void copy_h2d(ohx_ctx* c, void* d, const void* h, std::uint64_t bytes, cudaStrea
     const std::uint64_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
     if (k >= ohx_ctx::kStageBufs)
       check_cuda(cudaEventSynchronize(c->stage_ev[b]), "cudaEventSynchronize(staging)");
-    host_memcpy(c->h_stage[b], static_cast<const char*>(h) + off, len);
+    host_memcpy(c->h_stage[b], static_cast<const char*>(h) + off, len, c->host_lanes);
     check_cuda(cudaMemcpyAsync(static_cast<char*>(d) + off, c->h_stage[b], len,
                                cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(H2D chunk)");
     check_cuda(cudaEventRecord(c->stage_ev[b], s), "cudaEventRecord(staging)");
@@ -145,7 +147,7 @@ void copy_d2h(ohx_ctx* c, void* h, const void* d, std::uint64_t bytes, cudaStrea
     const int b = static_cast<int>(k % ohx_ctx::kStageBufs);
     const std::uint64_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
     check_cuda(cudaEventSynchronize(c->stage_ev[b]), "cudaEventSynchronize(staging)");
-    host_memcpy(static_cast<char*>(h) + off, c->h_stage[b], len);
+    host_memcpy(static_cast<char*>(h) + off, c->h_stage[b], len, c->host_lanes);
   };
   for (std::uint64_t k = 0; k < chunks; ++k) {
     const int b = static_cast<int>(k % ohx_ctx::kStageBufs);
@@ -284,7 +286,7 @@ void destroy_ctx(ohx_ctx* c) {
                   c->d_queues, static_cast<void*>(c->d_pts),
                   static_cast<void*>(c->d_labels), static_cast<void*>(c->d_gather),
                   static_cast<void*>(c->d_sample), c->d_cand, static_cast<void*>(c->d_cnt),
-                  c->d_regions, static_cast<void*>(c->d_cpts), c->d_hsort})
+                  c->d_regions, static_cast<void*>(c->d_cpts), c->d_hsort, c->d_poly})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_crec),
                   static_cast<void*>(c->h_counts), static_cast<void*>(c->h_cnt), c->h_sorted,
@@ -319,11 +321,13 @@ void trim_ctx(ohx_ctx* c) {
   dfree(c->d_pts, &c->pts_bytes);
   dfree(c->d_labels, &c->labels_bytes);
   dfree(c->d_gather, &c->gather_bytes);
+  c->spec_zeroed = false;
   dfree(c->d_sample, &c->sample_bytes);
   dfree(c->d_cand, &c->cand_bytes);
   dfree(c->d_regions, &c->regions_bytes);
   dfree(c->d_cpts, &c->cpts_bytes);
   dfree(c->d_hsort, &c->hsort_bytes);
+  dfree(c->d_poly, &c->poly_bytes);
   if (c->h_sorted) cudaFreeHost(c->h_sorted);
   c->h_sorted = nullptr;
   c->h_sorted_bytes = 0;

@@ -136,7 +136,12 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
       // the first survivors' coordinates ride along with the counts: a
       // small survivor set needs no second round trip (queues_fetch_xy)
       constexpr std::uint64_t kSpec = ohx_ctx::kSpecSurvivors;
-      dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, kSpec * 16, "gather");
+      grow_gather(c, kSpec * 16);
+      if (!c->spec_zeroed) {  // the fixed-size copy below reads past the survivors
+        // actually gathered: make those bytes defined (compute-sanitizer initcheck)
+        check_cuda(cudaMemsetAsync(c->d_gather, 0, kSpec * 16, s), "cudaMemsetAsync(gather)");
+        c->spec_zeroed = true;
+      }
       host_grow(reinterpret_cast<void**>(&c->h_spec), &c->spec_bytes, kSpec * 16,
                 "cudaMallocHost(survivors)");
       launch_gather4_dev(d_xy, c->d_queues, idx_bytes, cap, c->d_counts, kSpec, c->d_gather, s);
@@ -176,6 +181,29 @@ void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
   if (n == 0) throw std::invalid_argument("classify_points: empty point set");
   filter_core(c, d_xy, n, base, plan, d_labels, counts, s, nullptr, 0, nullptr);
 }
+void polygon_labels(ohx_ctx* c, const double* d_xy, std::uint64_t n, const double* poly, int m,
+                    const ohx_extreme_set& ext, std::uint8_t* d_labels, cudaStream_t s) {
+  // kept overrides and find_queue edges from an ordinary plan; the
+  // polygon's own edges (reference orientation constants) go separately
+  ohx_filter_plan plan;
+  make_plan(ext, nullptr, 0, &plan);
+  const KPlan kp = make_kplan(plan, 0, n);
+  std::vector<double> e(4 * static_cast<std::size_t>(m));
+  for (int i = 0; i < m; ++i) {
+    const int j = i + 1 == m ? 0 : i + 1;
+    e[4 * i] = poly[2 * i];
+    e[4 * i + 1] = poly[2 * i + 1];
+    e[4 * i + 2] = poly[2 * j] - poly[2 * i];          // (b.x - a.x)
+    e[4 * i + 3] = poly[2 * j + 1] - poly[2 * i + 1];  // (b.y - a.y)
+  }
+  dev_grow(&c->d_poly, &c->poly_bytes, e.size() * 8, "polygon edges");
+  check_cuda(cudaMemcpyAsync(c->d_poly, e.data(), e.size() * 8, cudaMemcpyHostToDevice, s),
+             "cudaMemcpyAsync(polygon)");
+  launch_polygon_labels(d_xy, n, static_cast<const double*>(c->d_poly), m, kp, d_labels, s);
+  ++c->launches;
+  check_cuda(cudaStreamSynchronize(s), "k3_polygon_labels");  // e is freed on return
+}
+
 void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
                  std::uint64_t cap, cudaStream_t s) {
   if (q < 1 || q > 4) throw std::invalid_argument("queue must be 1..4");
@@ -186,7 +214,7 @@ void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
   const auto* qbase = static_cast<const char*>(c->d_queues) +
                       std::uint64_t(q - 1) * c->last_cap * c->last_idx_bytes;
   if (h_xy) {
-    dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, cnt * 16, "gather");
+    grow_gather(c, cnt * 16);
     launch_gather(c->last_xy, qbase, c->last_idx_bytes, cnt, c->d_gather, s);
     ++c->launches;
     check_cuda(cudaMemcpyAsync(h_xy, c->d_gather, cnt * 16, cudaMemcpyDeviceToHost, s),
@@ -219,7 +247,7 @@ void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s) {
     std::memcpy(h_xy, c->h_spec, total * 16);
     return;
   }
-  dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, total * 16, "gather");
+  grow_gather(c, total * 16);
   launch_gather4(c->last_xy, c->d_queues, c->last_idx_bytes, c->last_cap, c->last_counts,
                  c->d_gather, s);
   ++c->launches;
@@ -247,7 +275,7 @@ std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
   if (total >= device_sort_min()) {
     // large survivor sets: the arcs are built and sorted on the device and
     // come back in sweep order; the chains and the clean-up run on the host
-    dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, total * 16, "gather");
+    grow_gather(c, total * 16);
     launch_gather4(c->last_xy, c->d_queues, c->last_idx_bytes, c->last_cap, c->last_counts,
                    c->d_gather, s);
     ++c->launches;

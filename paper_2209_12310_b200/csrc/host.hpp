@@ -48,6 +48,13 @@ struct ohx_ctx {
   int last_idx_bytes = 4;
   std::uint64_t last_counts[4] = {0, 0, 0, 0};
 
+  // host threads the current call may use for staging copies (0 = all):
+  // the C++ API sets it to the caller's ReduceEngine workers -- the host
+  // lanes the reference grants a call (parallel.hpp:18-21)
+  int host_lanes = 0;
+  bool spec_zeroed = false;
+  void* d_poly = nullptr;  // classify_points' edges of a polygon with > 8 vertices
+  std::uint64_t poly_bytes = 0;  // d_gather's speculative survivor slots are cleared
   // staging for host-API calls
   double* d_pts = nullptr;
   std::uint64_t pts_bytes = 0;
@@ -129,7 +136,14 @@ void fold_stage_times(ohx_ctx* c, bool wait);
 
 // ---- context workspaces (context.cpp)
 const char* last_error();  // this thread's last error message
-void dev_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what);
+// grow-only device buffer; true when (re)allocated
+bool dev_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what);
+// the survivor gather buffer (ohx_ctx::d_gather); a new allocation is not
+// yet cleared for the fixed-size speculative survivor copy
+inline void grow_gather(ohx_ctx* c, std::uint64_t bytes) {
+  if (dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, bytes, "gather"))
+    c->spec_zeroed = false;
+}
 void host_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what);
 cudaStream_t pick(ohx_ctx* c, void* s);
 void bind(ohx_ctx* c);

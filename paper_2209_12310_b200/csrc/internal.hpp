@@ -136,6 +136,11 @@ void launch_k1_list(const double* d_xy, std::uint64_t n, const unsigned long lon
 // points of the sample runs 0, step, 2 step, ... inside Q
 void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int len, int step,
                             const KFRegion& q, unsigned long long* d_count, cudaStream_t stream);
+// labels of classify_points against a polygon of m > 8 vertices: d_edges =
+// m x {a.x, a.y, fl(b.x-a.x), fl(b.y-a.y)}; kept overrides and find_queue
+// edges from plan (its own octagon part unused)
+void launch_polygon_labels(const double* d_xy, std::uint64_t n, const double* d_edges, int m,
+                           const KPlan& plan, std::uint8_t* d_labels, cudaStream_t stream);
 // *d_first = the smallest index with a non-finite coordinate, else ~0
 void launch_first_nonfinite(const double* d_xy, std::uint64_t n, unsigned long long* d_first,
                             cudaStream_t stream);

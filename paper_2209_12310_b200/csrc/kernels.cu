@@ -1334,6 +1334,43 @@ __global__ void first_nonfinite(const double2* __restrict__ pts, std::uint64_t n
   if ((threadIdx.x & 31) == 0 && mine != ~0ull) atomicMin(first, mine);
 }
 
+// classify_points with a caller's polygon of more than 8 vertices
+// (filter.cpp:104-131 accepts any vertex list; build_octagon never makes
+// one): kept overrides first, then "some edge has orientation < 0" over all
+// m edges (geometry.cpp:16-22, edges read through the read-only cache: every
+// thread of a warp reads the same edge), then find_queue.  Labels only --
+// the queues of a heaphull always come from K2 on a <= 8-vertex octagon.
+__global__ void __launch_bounds__(256)
+    k3_polygon_labels(const double2* __restrict__ pts, std::uint64_t n,
+                      const double4* __restrict__ edges, int m, const KPlan plan,
+                      std::uint8_t* __restrict__ labels) {
+  for (std::uint64_t j = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += std::uint64_t(gridDim.x) * blockDim.x) {
+    std::uint32_t lab = 0xff;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (lab == 0xff && j == plan.kept[k]) lab = plan.kept_label[k];
+    if (lab == 0xff) {
+      const double2 p = ld_stream(pts + j);
+      bool out = false;
+      for (int e = 0; e < m && !out; ++e) {
+        const double2 lo = __ldg(reinterpret_cast<const double2*>(edges + e));
+        const double2 hi = __ldg(reinterpret_cast<const double2*>(edges + e) + 1);
+        out = right_of(p.x, p.y, make_double4(lo.x, lo.y, hi.x, hi.y));
+      }
+      lab = 0;
+      if (out) {
+        lab = 1;
+#pragma unroll
+        for (int k = 3; k >= 0; --k)
+          if (right_of(p.x, p.y, make_double4(plan.qax[k], plan.qay[k], plan.qa[k], plan.qc[k])))
+            lab = k + 1;
+      }
+    }
+    labels[j] = static_cast<std::uint8_t>(lab);
+  }
+}
+
 template <typename IdxT>
 __global__ void gather_xy(const double2* __restrict__ pts,
                           const IdxT* __restrict__ idx, std::uint64_t count,
@@ -1649,6 +1686,16 @@ void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int l
   count_in_region<<<(segs + step - 1) / step, 256, 0, stream>>>(
       reinterpret_cast<const double2*>(d_xy), SampleMap{n, segs, len, 1}, step, q, d_count);
   check_cuda(cudaGetLastError(), "count_in_region launch");
+}
+
+void launch_polygon_labels(const double* d_xy, std::uint64_t n, const double* d_edges, int m,
+                           const KPlan& plan, std::uint8_t* d_labels, cudaStream_t stream) {
+  const std::uint64_t blocks = (n + 255) / 256;
+  const unsigned grid = static_cast<unsigned>(blocks < 148ull * 16 ? blocks : 148ull * 16);
+  k3_polygon_labels<<<grid, 256, 0, stream>>>(reinterpret_cast<const double2*>(d_xy), n,
+                                              reinterpret_cast<const double4*>(d_edges), m, plan,
+                                              d_labels);
+  check_cuda(cudaGetLastError(), "k3_polygon_labels launch");
 }
 
 void launch_first_nonfinite(const double* d_xy, std::uint64_t n, unsigned long long* d_first,

@@ -32,14 +32,25 @@ const double* raw(std::span<const Point2D> pts) {
   return reinterpret_cast<const double*>(pts.data());
 }
 
-// Exclusive use of the default device context for one API call.
+// Exclusive use of the default device context for one API call; the
+// caller's engine grants the call its host lanes (staging copies of
+// pageable input and labels run on that many threads).
 struct Device {
   ohx_ctx* c;
   std::unique_lock<std::mutex> lock;
   cudaStream_t s;
-  Device() : c(ohx::default_ctx()), lock(ohx::ctx_mutex(c)), s(ohx::ctx_stream(c)) {
+  explicit Device(const ReduceEngine* e = nullptr)
+      : c(ohx::default_ctx()), lock(ohx::ctx_mutex(c)), s(ohx::ctx_stream(c)) {
     ohx::ctx_bind(c);
+    const int own = ohx::api_lanes_override();
+    ohx::ctx_set_host_lanes(
+        c, own >= 0 ? own
+           : e  ? static_cast<int>(std::min<std::size_t>(e->config().workers, 1024))
+                : 0);
   }
+  ~Device() { ohx::ctx_set_host_lanes(c, 0); }
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
 };
 
 ohx_extreme_set to_set(const ExtremeSet& e, std::span<const Point2D> pts) {
@@ -201,10 +212,10 @@ PointSet generate(const GenSpec& spec) {
 }
 
 // ================================================================== filter
-AxisExtremes find_axis_extremes(std::span<const Point2D> pts, ReduceEngine&) {
+AxisExtremes find_axis_extremes(std::span<const Point2D> pts, ReduceEngine& engine) {
   // reference filter.cpp:8-23 -> K1
   if (pts.empty()) throw std::invalid_argument("find_axis_extremes: empty point set");
-  Device d;
+  Device d(&engine);
   const double* dx = ohx::stage_points(d.c, raw(pts), pts.size(), d.s);
   ohx_extremes_rec rec;
   ohx::extremes(d.c, dx, pts.size(), 0, &rec, d.s);
@@ -212,22 +223,22 @@ AxisExtremes find_axis_extremes(std::span<const Point2D> pts, ReduceEngine&) {
 }
 
 CornerExtremes find_corner_extremes(std::span<const Point2D> pts, const AxisExtremes& axis,
-                                    ReduceEngine&) {
+                                    ReduceEngine& engine) {
   // reference filter.cpp:25-45 -> K1b against the caller's axis extremes
   if (pts.empty()) throw std::invalid_argument("find_corner_extremes: empty point set");
   const double bbox[4] = {pts[axis.east].x, pts[axis.north].y, pts[axis.west].x,
                           pts[axis.south].y};
-  Device d;
+  Device d(&engine);
   const double* dx = ohx::stage_points(d.c, raw(pts), pts.size(), d.s);
   ohx_corner_rec rec;
   ohx::corners_exact(d.c, dx, pts.size(), 0, bbox, &rec, d.s);
   return {rec.idx[0], rec.idx[1], rec.idx[2], rec.idx[3]};
 }
 
-ExtremeSet find_extremes(std::span<const Point2D> pts, ReduceEngine&) {
+ExtremeSet find_extremes(std::span<const Point2D> pts, ReduceEngine& engine) {
   // reference filter.cpp:47-52 -> K1 + corner certificate (+ K1b)
   if (pts.empty()) throw std::invalid_argument("find_axis_extremes: empty point set");
-  Device d;
+  Device d(&engine);
   const double* dx = ohx::stage_points(d.c, raw(pts), pts.size(), d.s);
   ohx_extremes_rec rec;
   ohx::extremes(d.c, dx, pts.size(), 0, &rec, d.s);
@@ -271,15 +282,25 @@ int find_queue(const Point2D& p, const ExtremeSet& ext, std::span<const Point2D>
 }
 
 LabelArray classify_points(std::span<const Point2D> pts, const Octagon& oct,
-                           const ExtremeSet& ext, ReduceEngine&) {
+                           const ExtremeSet& ext, ReduceEngine& engine) {
   // reference filter.cpp:104-131 -> K2 with the caller's octagon/extremes
   if (pts.empty()) return {};
-  if (oct.vertices.size() > 8) throw std::invalid_argument("octagon has more than 8 vertices");
   const ohx_extreme_set set = to_set(ext, pts);
+  if (oct.vertices.size() > 8) {  // any vertex list is accepted (filter.cpp:118-128)
+    Device d(&engine);
+    const double* dx = ohx::stage_points(d.c, raw(pts), pts.size(), d.s);
+    std::uint8_t* dl = ohx::stage_labels(d.c, pts.size());
+    ohx::polygon_labels(d.c, dx, pts.size(), reinterpret_cast<const double*>(oct.vertices.data()),
+                        static_cast<int>(oct.vertices.size()), set, dl, d.s);
+    LabelArray labels(pts.size());
+    ohx::fetch_labels(d.c, labels.data(), dl, pts.size(), d.s);
+    ohx::check_cuda(cudaStreamSynchronize(d.s), "classify_points");
+    return labels;
+  }
   ohx_filter_plan plan;
   ohx::make_plan(set, reinterpret_cast<const double*>(oct.vertices.data()),
                  static_cast<int>(oct.vertices.size()), &plan);
-  Device d;
+  Device d(&engine);
   const double* dx = ohx::stage_points(d.c, raw(pts), pts.size(), d.s);
   std::uint8_t* dl = ohx::stage_labels(d.c, pts.size());
   std::uint64_t counts[4];
@@ -308,11 +329,11 @@ std::vector<Point2D> quadrant_hull(std::vector<Point2D> pts, int quadrant) {
   return out;
 }
 
-HeaphullRun heaphull_run(std::span<const Point2D> pts, ReduceEngine&) {
+HeaphullRun heaphull_run(std::span<const Point2D> pts, ReduceEngine& engine) {
   // reference hull.cpp:152-194: same stages and timer boundaries
   if (pts.empty()) throw std::invalid_argument("heaphull: empty point set");
   const auto t0 = Clock::now();
-  Device d;
+  Device d(&engine);
   const double* dx = ohx::stage_points(d.c, raw(pts), pts.size(), d.s);
   std::uint8_t* dl = ohx::stage_labels(d.c, pts.size());
   const ohx::FilterOut f = ohx::device_filter(d.c, dx, pts.size(), dl, d.s);
@@ -329,10 +350,10 @@ HeaphullRun heaphull_run(std::span<const Point2D> pts, ReduceEngine&) {
   return run;
 }
 
-HullPolygon heaphull(std::span<const Point2D> pts, ReduceEngine&) {
+HullPolygon heaphull(std::span<const Point2D> pts, ReduceEngine& engine) {
   // reference hull.cpp:196-198; labels are not materialised on this path
   if (pts.empty()) throw std::invalid_argument("heaphull: empty point set");
-  Device d;
+  Device d(&engine);
   const double* dx = ohx::stage_points(d.c, raw(pts), pts.size(), d.s);
   const ohx::FilterOut f = ohx::device_filter(d.c, dx, pts.size(), nullptr, d.s);
   return hull_from_device(d, f);

@@ -46,6 +46,15 @@ ohx::HullSink hull_sink(double* h_hull, std::uint64_t cap, std::uint64_t* h) {
 
 }  // namespace
 
+namespace ohx {
+namespace {
+thread_local int tl_api_lanes = -1;
+}
+int api_lanes_override() { return tl_api_lanes; }
+ApiLanes::ApiLanes(int lanes) : saved(tl_api_lanes) { tl_api_lanes = lanes; }
+ApiLanes::~ApiLanes() { tl_api_lanes = saved; }
+}  // namespace ohx
+
 using ohx::guard;
 
 extern "C" {
@@ -123,6 +132,7 @@ int ohx_heaphull_pts2(const char* path, double* h_hull, uint64_t cap, uint64_t* 
 int ohx_classify(const double* h_xy, uint64_t n, uint8_t* h_labels) {
   return guard([&] {
     octohull::ReduceEngine engine;
+    const ohx::ApiLanes all_cores(0);
     const auto pts = pts_of(h_xy, n);
     const octohull::ExtremeSet ext = octohull::find_extremes(pts, engine);
     const octohull::Octagon oct = octohull::build_octagon(pts, ext);
@@ -131,10 +141,30 @@ int ohx_classify(const double* h_xy, uint64_t n, uint8_t* h_labels) {
   });
 }
 
+int ohx_classify_points(const double* h_xy, uint64_t n, const double* poly_xy, uint64_t m,
+                        const uint64_t ext[8], uint8_t* h_labels) {
+  // octohull::classify_points (filter.cpp:104-131; python/module.cpp binds
+  // it) with the caller's polygon and extremes
+  return guard([&] {
+    octohull::ReduceEngine engine;
+    const ohx::ApiLanes all_cores(0);
+    const auto pts = pts_of(h_xy, n);
+    octohull::Octagon oct;
+    oct.vertices.assign(reinterpret_cast<const octohull::Point2D*>(poly_xy),
+                        reinterpret_cast<const octohull::Point2D*>(poly_xy) + m);
+    octohull::ExtremeSet e;
+    e.axis = {ext[0], ext[1], ext[2], ext[3]};
+    e.corner = {ext[4], ext[5], ext[6], ext[7]};
+    const octohull::LabelArray l = octohull::classify_points(pts, oct, e, engine);
+    std::memcpy(h_labels, l.data(), l.size());
+  });
+}
+
 int ohx_heaphull_run(const double* h_xy, uint64_t n, double* h_hull, uint64_t cap,
                      uint64_t* h, uint8_t* h_labels, double* timings) {
   return guard([&] {
     octohull::ReduceEngine engine;
+    const ohx::ApiLanes all_cores(0);
     const octohull::HeaphullRun run = octohull::heaphull_run(pts_of(h_xy, n), engine);
     copy_hull(run.hull.vertices, h_hull, cap, h);
     if (h_labels) std::memcpy(h_labels, run.labels.data(), run.labels.size());
@@ -150,6 +180,7 @@ int ohx_heaphull_run(const double* h_xy, uint64_t n, double* h_hull, uint64_t ca
 int ohx_find_extremes(const double* h_xy, uint64_t n, uint64_t ext[8]) {
   return guard([&] {
     octohull::ReduceEngine engine;
+    const ohx::ApiLanes all_cores(0);
     const octohull::ExtremeSet e = octohull::find_extremes(pts_of(h_xy, n), engine);
     const uint64_t v[8] = {e.axis.east, e.axis.north, e.axis.west, e.axis.south,
                            e.corner.ne, e.corner.nw,  e.corner.sw, e.corner.se};

@@ -27,6 +27,16 @@ struct FilterOut {
   double sample_coverage;
 };
 
+// Host lanes of C++ API calls made on this thread (-1: the caller's
+// ReduceEngine workers decide).  The C ABI's pipeline wrappers, which
+// construct a one-worker engine only to call the C++ API, grant all cores.
+int api_lanes_override();
+struct ApiLanes {
+  explicit ApiLanes(int lanes);
+  ~ApiLanes();
+  int saved;
+};
+
 ohx_ctx* create_ctx(int device);
 void destroy_ctx(ohx_ctx* c);
 void trim_ctx(ohx_ctx* c);
@@ -34,6 +44,8 @@ ohx_ctx* default_ctx(int device = -1);
 cudaStream_t ctx_stream(ohx_ctx* c);
 std::mutex& ctx_mutex(ohx_ctx* c);
 void ctx_bind(ohx_ctx* c);
+// host threads of the staging copies for the calls that follow (0: all)
+void ctx_set_host_lanes(ohx_ctx* c, int lanes);
 
 const double* stage_points(ohx_ctx* c, const double* h_xy, std::uint64_t n,
                            cudaStream_t s);
@@ -59,6 +71,9 @@ void make_plan(const ohx_extreme_set& e, const double* oct, int m,
 void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
             const ohx_filter_plan& plan, std::uint8_t* d_labels,
             std::uint64_t counts[4], cudaStream_t s);
+// classify_points' labels against a caller's polygon of m > 8 vertices
+void polygon_labels(ohx_ctx* c, const double* d_xy, std::uint64_t n, const double* poly, int m,
+                    const ohx_extreme_set& ext, std::uint8_t* d_labels, cudaStream_t s);
 void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
                  std::uint64_t cap, cudaStream_t s);
 

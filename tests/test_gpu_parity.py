@@ -149,6 +149,21 @@ def test_degenerate_octagon_filters_nothing(ctx, oracle):
     assert (labels != 0).all()
 
 
+@pytest.mark.parametrize("m", [3, 8, 9, 37, 1000])
+def test_classify_points_any_polygon(oracle, m):
+    # classify_points takes the caller's polygon (filter.cpp:104-131 accepts
+    # any vertex list): regular m-gons inside a disk, ties on the boundary,
+    # plus a reversed (clockwise) one; kept overrides from find_extremes
+    pts = P.generate("disk", 300_001, 5)
+    ext = oracle.find_extremes(pts)
+    th = np.linspace(0, 2 * np.pi, m, endpoint=False)
+    poly = np.stack([0.9 * np.cos(th), 0.9 * np.sin(th)], axis=1)
+    pts[:m] = poly  # points exactly on the vertices
+    for pg in (poly, poly[::-1].copy()):
+        got = P.classify_points(pts, pg, ext)
+        assert np.array_equal(got, oracle.classify(pts, ext, pg)), m
+
+
 # ------------------------------------------------------------ sharding ----
 @pytest.mark.parametrize("shards", [2, 3, 7])
 def test_shard_records_combine_to_whole(ctx, oracle, shards):
