@@ -155,10 +155,10 @@ def test_classify_points_any_polygon(oracle, m):
     # any vertex list): regular m-gons inside a disk, ties on the boundary,
     # plus a reversed (clockwise) one; kept overrides from find_extremes
     pts = P.generate("disk", 300_001, 5)
-    ext = oracle.find_extremes(pts)
     th = np.linspace(0, 2 * np.pi, m, endpoint=False)
     poly = np.stack([0.9 * np.cos(th), 0.9 * np.sin(th)], axis=1)
     pts[:m] = poly  # points exactly on the vertices
+    ext = oracle.find_extremes(pts)
     for pg in (poly, poly[::-1].copy()):
         got = P.classify_points(pts, pg, ext)
         assert np.array_equal(got, oracle.classify(pts, ext, pg)), m
