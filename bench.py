@@ -77,6 +77,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--cpu-sample", type=float, default=0,
                     help="points of the CPU reference's sample (0: the corpus, up to 1e9)")
+    ap.add_argument("--mg-vshards", type=int, default=1,
+                    help="shards per rank through the native multi-GPU layer (N = 1: > 1 "
+                         "routes the step through ohx_mg with that many shards on one GPU)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dists", action="store_true",
@@ -227,10 +230,12 @@ def cpu_reference(pts, reps: int):
     return {"kind": kind, "cores": cores, "times": times}
 
 
-def reference_parity(ref, pts, ctx, hull_dev, ext_dev) -> dict:
+def reference_parity(ref, pts, ctx, hull_dev, ext_dev, counts=None) -> dict:
     """The device results of the last call on ctx (hull, extremes, queues)
     against the reference's own heaphull_run / find_extremes on the same
-    points (outside every timed region; the reference is the checker)."""
+    points (outside every timed region; the reference is the checker).
+    ctx None (a multi-shard call): the queue lengths `counts` are compared
+    instead of the queues themselves."""
     import numpy as np
 
     cores = os.cpu_count() or 1
@@ -238,12 +243,15 @@ def reference_parity(ref, pts, ctx, hull_dev, ext_dev) -> dict:
     ref_hull, ref_labels, _ = ref.heaphull_run(pts, cores, 32)
     ref_ext = ref.find_extremes(pts, cores, 32)
     ref_s = time.perf_counter() - t0
-    info = ctx.last_run()
     queues_ok = True
-    for q in range(4):
-        want = np.flatnonzero(ref_labels == q + 1)
-        got = ctx.queue(q + 1, info["counts"][q])[0]
-        queues_ok &= bool(np.array_equal(got, want))
+    if ctx is not None:
+        info = ctx.last_run()
+        for q in range(4):
+            want = np.flatnonzero(ref_labels == q + 1)
+            got = ctx.queue(q + 1, info["counts"][q])[0]
+            queues_ok &= bool(np.array_equal(got, want))
+    else:
+        queues_ok = [int((ref_labels == q + 1).sum()) for q in range(4)] == list(counts)
     out = {"checked_against": f"reference heaphull_run + find_extremes (oracle/_ref, {cores} "
                               f"workers) on the same {len(pts)} points",
            "hull_equal": bool(np.array_equal(hull_dev, ref_hull)),
@@ -363,13 +371,77 @@ def distributions_leg(a, P, ctx, dev, start, stop, peak, check_parity):
     return out
 
 
+class Runner:
+    """One step of the job on this rank, in one of three shapes:
+      single  -- N = 1: ctx.heaphull_device (the device pipeline)
+      mg      -- the native multi-GPU layer (ohx_mg_*, NCCL): N > 1 over
+                 NCCL, or N = 1 with --mg-vshards k (k shards on one GPU)
+      sharded -- N > 1 with OHX_BENCH_BACKEND=gloo: sharded.py over gloo
+                 (ranks sharing a GPU; a test mode of the multi-rank code)
+    first() -> (hull, stats) with stats: counts (this rank), job_counts,
+    uncertified, ext, fused; step() -> hull (rank 0) or None."""
+
+    def __init__(self, mode, P, ctx, d, n, base, world, rank, local_dev, xdev, vshards):
+        self.mode, self.P, self.d, self.n, self.base = mode, P, d, n, base
+        self.world, self.rank, self.xdev, self.vshards = world, rank, xdev, vshards
+        self.ctx = ctx
+        if mode == "mg":
+            import torch
+            import torch.distributed as dist
+            from paper_2209_12310_b200.mg import MultiGPU, unique_id
+            uid = torch.zeros(128, dtype=torch.uint8, device=xdev)
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(unique_id()), dtype=torch.uint8))
+            if world > 1:
+                dist.broadcast(uid, 0)
+            self.mg = MultiGPU.init_rank(bytes(uid.cpu().numpy()), world, rank, local_dev)
+            self.ctx = self.mg.shard_context(0, 0)  # stage times / launches of shard 0
+            self.ctxs = [self.mg.shard_context(0, v) for v in range(vshards)]
+        elif mode == "sharded":
+            from paper_2209_12310_b200.sharded import CudaShard
+            self.shard = CudaShard(ctx, d, n, base)
+
+    def launches(self) -> int:
+        cs = self.ctxs if self.mode == "mg" else [self.ctx]
+        return sum(c.launches for c in cs)
+
+    def step(self, d=None):
+        d = self.d if d is None else d
+        if self.mode == "single":
+            return self.ctx.heaphull_device(d, self.n)[0]
+        if self.mode == "mg":
+            return self.mg.heaphull_shard(d, self.n, self.base, self.vshards)[0]
+        from paper_2209_12310_b200.sharded import CudaShard, sharded_heaphull
+        sh = self.shard if d is self.d else CudaShard(self.ctx, d, self.n, self.base)
+        return sharded_heaphull(sh, device=self.xdev)
+
+    def first(self):
+        import numpy as np
+        if self.mode == "mg":
+            hull, info = self.mg.heaphull_shard(self.d, self.n, self.base, self.vshards)
+            mine = [sum(c.last_run()["counts"][q] for c in self.ctxs) for q in range(4)]
+            return hull, {"counts": mine, "job_counts": info["counts"],
+                          "uncertified": int(info["corner_pass"]), "ext": info["ext"],
+                          "fused": info["fused_shards"] == info["shards"], "mg": info}
+        from paper_2209_12310_b200.sharded import sharded_heaphull
+        stats = {}
+        shard = self.shard if self.mode == "sharded" else \
+            __import__("paper_2209_12310_b200.sharded", fromlist=["CudaShard"]).CudaShard(
+                self.ctx, self.d, self.n, self.base)
+        hull = sharded_heaphull(shard, device=self.xdev, stats=stats)
+        stats["job_counts"] = None
+        if self.mode == "single":
+            assert np.array_equal(hull, self.step()), "pipeline disagreement"
+            stats["job_counts"] = stats["counts"]
+        return hull, stats
+
+
 def run_b200_arm(a):
-    import numpy as np
+    import numpy as np  # noqa: F811
     import torch
     import torch.distributed as dist
 
     import paper_2209_12310_b200 as P
-    from paper_2209_12310_b200.sharded import CudaShard, sharded_heaphull
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -389,6 +461,8 @@ def run_b200_arm(a):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
+    mode = ("mg" if backend == "nccl" and (world > 1 or a.mg_vshards > 1)
+            else "sharded" if world > 1 else "single")
 
     def barrier():
         if world > 1:
@@ -422,28 +496,23 @@ def run_b200_arm(a):
     d = host.to(dev)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
-    ctx = P.Context(local_dev)
-    shard = CudaShard(ctx, d, n, base)
+    ctx0 = P.Context(local_dev)
+    run = Runner(mode, P, ctx0, d, n, base, world, rank, local_dev, xdev, max(1, a.mg_vshards))
+    ctx = run.ctx  # the (first) shard's context: stage times, last run
 
-    def step_device(stats=None):
-        if world == 1:
-            hull, _ = ctx.heaphull_device(d, n)
-            return hull
-        return sharded_heaphull(shard, device=xdev, stats=stats)
+    def step_device():
+        return run.step()
 
-    # correctness gate on this very workload: the sharded / single pipeline
-    # must equal the kernel-level path (and K1/K2 are oracle-checked in tests)
-    stats = {}
-    hull0 = sharded_heaphull(shard, device=xdev, stats=stats)
-    if rank == 0 and world == 1:
-        hull1 = step_device()
-        assert np.array_equal(hull0, hull1), "pipeline disagreement"
-    survivors_job = sum_over_ranks(sum(stats["counts"]))
+    # correctness gate on this very workload (single: the pipeline equals the
+    # kernel-level path; K1/K2 are oracle-checked in tests) + the run's stats
+    hull0, stats = run.first()
+    survivors_job = (sum(stats["job_counts"]) if stats["job_counts"] is not None
+                     else sum_over_ranks(sum(stats["counts"])))
 
     # ---------------- device-resident timed region
     for _ in range(a.warmup):
         step_device()
-    launches0 = ctx.launches
+    launches0 = run.launches()
     ctx.kernel_ms_sum(reset=True)  # per-stage CUDA-event sums, read once after the loop
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_dev) as clocks:
@@ -453,7 +522,7 @@ def run_b200_arm(a):
             step_device()
         stop.record()
         barrier()
-    launches = ctx.launches - launches0
+    launches = run.launches() - launches0
     ksum = ctx.kernel_ms_sum()
     k1, k2, kc = ([ksum[k][0] / ksum[k][1]] if ksum[k][1] else [-1.0] for k in ("k1", "k2", "kc"))
     last = ctx.last_run()
@@ -465,7 +534,7 @@ def run_b200_arm(a):
     e2e = None
     clocks_e2e_summary = None
     if not a.no_e2e:
-        if world == 1:
+        if mode == "single":
             s_local = sum(stats["counts"])
             out = np.empty((n + 8, 2), dtype=np.float64) if n < 10_000_000 else np.empty((s_local + 8 + 64, 2))
             h = P.C.c_uint64(0)
@@ -473,13 +542,16 @@ def run_b200_arm(a):
             def step_e2e():
                 P.check(P.lib.ohx_heaphull(hp.ctypes.data_as(P._dp), n, out.ctypes.data_as(P._dp),
                                            len(out), P.C.byref(h), None))
+            api = "ohx_heaphull (C ABI) on {} host points"
         else:
             d2 = torch.empty_like(d)
 
             def step_e2e():
                 d2.copy_(host, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
-                sharded_heaphull(CudaShard(ctx, d2, n, base), device=xdev)
+                run.step(d2)
+            api = ("ohx_mg_heaphull_shard (C ABI, NCCL) after each rank's H2D of its {} slice"
+                   if mode == "mg" else "sharded_heaphull (gloo) after each rank's H2D of its {} slice")
         for _ in range(a.warmup):
             step_e2e()
         with ClockSampler(local_dev) as clocks_e2e:
@@ -491,21 +563,20 @@ def run_b200_arm(a):
             barrier()
         ms_e2e = max_over_ranks(start.elapsed_time(stop) / a.steps)
         # the bound of this step: the raw pinned H2D of the same buffer
-        h2d = h2d_bandwidth(host, d if world == 1 else d2) if host.is_pinned() else None
+        h2d = h2d_bandwidth(host, d if mode == "single" else d2) if host.is_pinned() else None
         h2d = max_over_ranks(h2d or 0.0) if world > 1 else h2d
         e2e_gbs = total * 16 / (ms_e2e * 1e-3) / 1e9
         e2e = {"value": total / (ms_e2e * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": total * 16,
-               # survivors' coordinates (16 B each) + the two small records
+               # survivors' coordinates (16 B each) + the small records
                "d2h_bytes_per_step": survivors_job * 16 + world * 2 * 320,
-               "api": ("ohx_heaphull (C ABI) on {} host points" if world == 1
-                       else "sharded_heaphull with per-rank {} shard H2D").format(
-                           "pinned" if host.is_pinned() else "pageable"),
+               "api": api.format("pinned" if host.is_pinned() else "pageable"),
                "roofline": {"bound": "pcie", "achieved": e2e_gbs, "unit": "GB/s",
-                            "peak": h2d, "frac": e2e_gbs / h2d if h2d else None,
+                            "peak": h2d * world if (h2d and world > 1) else h2d,
+                            "frac": e2e_gbs / (h2d * world) if h2d else None,
                             "peak_source": "raw pinned H2D of the same buffer, measured in this "
                                            "run (best of 3, CUDA events)"
-                                           + (", max over ranks" if world > 1 else "")}}
+                                           + (" x ranks (one PCIe link each)" if world > 1 else "")}}
         clocks_e2e_summary = clocks_e2e.summary()
 
     # ---------------- roofline of the dominant kernel
@@ -568,14 +639,15 @@ def run_b200_arm(a):
         if not a.no_parity and r["kind"] == "reference" and ns == n:
             from oracle import Reference
             hull_dev = step_device()
-            parity = reference_parity(Reference(), hp, ctx, hull_dev, stats["ext"])
+            parity = reference_parity(Reference(), hp, ctx if mode == "single" else None,
+                                      hull_dev, stats["ext"], stats["job_counts"])
 
     # ---------------- the other distributions (rank 0, N = 1)
     dists = None
     if rank == 0 and world == 1 and not a.no_dists:
         del d
         torch.cuda.empty_cache()
-        dists = distributions_leg(a, P, ctx, dev, start, stop, peak, not a.no_parity)
+        dists = distributions_leg(a, P, ctx0, dev, start, stop, peak, not a.no_parity)
 
     if rank == 0:
         clk = clocks.summary()
@@ -588,7 +660,11 @@ def run_b200_arm(a):
             "config": config(a, world),
             "run": {"survivors": survivors_job, "survivors_rank0": stats["counts"],
                     "corner_certificate": "pass" if not stats["uncertified"]
-                    else f"fallback mask {stats['uncertified']}", "fused": stats.get("fused")},
+                    else f"fallback mask {stats['uncertified']}", "fused": stats.get("fused"),
+                    "path": {"single": "ohx_heaphull_device (one device pipeline)",
+                             "mg": f"ohx_mg_heaphull_shard (NCCL, {world} rank(s), "
+                                   f"{max(1, a.mg_vshards)} shard(s) per rank)",
+                             "sharded": "sharded.py over gloo (test mode)"}[mode]},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
             "distributions": dists, "clocks": clk,
             "clocks_e2e": clocks_e2e_summary, "gpu_launches": launches,

@@ -327,6 +327,65 @@ int ohx_hull_from_queue_points(const double anchors_xy[8],
                                const uint64_t q_len[4], double* h_hull,
                                uint64_t cap, uint64_t* h);
 
+/* ---- multi-GPU (the reference's ReduceConfig.workers,
+ * parallel.hpp:18-21, mapped to devices) ---------------------------------
+ * One NCCL rank per GPU.  The job's points are contiguous index-range
+ * shards; each rank filters its own (fused pass or K1, then K2), the
+ * 296-byte extremes records and the queue lengths are exchanged with
+ * ncclAllGather (the same exact combine on every rank), and the survivors'
+ * coordinates go to rank 0 only (one ncclSend/ncclRecv per queue and rank,
+ * straight into place), which runs the hull stage.  Results equal the
+ * single-device pipeline's bit for bit.  A rank may hold several virtual
+ * shards (vshards): the same exchange with several shards per device.
+ * NCCL is loaded at run time (libnccl.so.2); without it these calls fail
+ * with OHX_E_NODEVICE.  A call that fails mid-exchange aborts the
+ * communicator: destroy and recreate the handle. */
+typedef struct ohx_mg ohx_mg;
+typedef struct {
+  uint64_t ext[8];       /* the job's ExtremeSet, slot order (global indices) */
+  uint64_t counts[4];    /* the job's queue lengths */
+  uint64_t n_total;      /* points in the job */
+  uint32_t corner_pass;  /* the corner certificate failed: K1b ran on every shard */
+  uint32_t fused_shards; /* shards whose K2 ran on their fused-pass candidates only */
+  uint32_t shards;       /* shards in the job */
+  uint32_t pad;
+  double ms[4];          /* this rank's host wall time: extremes + exchange,
+                            K2, survivor gather, hull stage (root) */
+} ohx_mg_info;
+/* ncclGetUniqueId, for the process of rank 0 to hand to the others. */
+int ohx_mg_unique_id(uint8_t id[128]);
+/* One process per GPU: this process is `rank` of `world`, on `device`
+ * (ncclCommInitRank; collective over the world). */
+int ohx_mg_init_rank(const uint8_t id[128], int world, int rank, int device, ohx_mg** out);
+/* One process driving `ndev` GPUs, one thread per device in every call
+ * (ncclCommInitAll); devices NULL = 0..ndev-1. */
+int ohx_mg_init_all(int ndev, const int* devices, ohx_mg** out);
+int ohx_mg_destroy(ohx_mg* mg);
+int ohx_mg_world(const ohx_mg* mg, int* world, int* local_ranks);
+int ohx_mg_nccl_version(int* version);
+/* The context of shard `shard` of local rank `local_rank` (created if need
+ * be; owned by the handle): its launch counter, stage times and last run
+ * describe that shard's part of the last call. */
+int ohx_mg_ctx(ohx_mg* mg, int local_rank, int shard, ohx_ctx** ctx);
+/* Collective (ohx_mg_init_rank handles): this rank's device-resident shard
+ * [index_base, index_base + n) of the job, split into vshards virtual
+ * shards; every rank calls it with its own range, ranks in index order.
+ * Rank 0 receives the hull (h_hull capacity cap, *h); elsewhere *h = 0.
+ * h_labels (nullable): this shard's n labels. */
+int ohx_mg_heaphull_shard(ohx_mg* mg, const double* d_xy, uint64_t n, uint64_t index_base,
+                          int vshards, uint8_t* h_labels, double* h_hull, uint64_t cap,
+                          uint64_t* h, ohx_mg_info* info);
+/* Single process (ohx_mg_init_all): nshards device-resident shards, in
+ * index order, nshards / ndev consecutive ones on each device. */
+int ohx_mg_heaphull_device(ohx_mg* mg, int nshards, const double* const* d_xy, const uint64_t* n,
+                           uint8_t* h_labels, double* h_hull, uint64_t cap, uint64_t* h,
+                           ohx_mg_info* info);
+/* Single process: host points split evenly over the devices (vshards
+ * each), every device staging its own slice (heaphull / heaphull_run of
+ * the C++ API with ReduceConfig.workers > 1 on a multi-GPU box). */
+int ohx_mg_heaphull(ohx_mg* mg, const double* h_xy, uint64_t n, int vshards, uint8_t* h_labels,
+                    double* h_hull, uint64_t cap, uint64_t* h, ohx_mg_info* info);
+
 #ifdef __cplusplus
 }
 #endif

@@ -427,3 +427,6 @@ def hull_from_queue_points(anchors, queues) -> np.ndarray:
     check(lib.ohx_hull_from_queue_points(a.ctypes.data_as(_dp), ptrs, lens,
                                          out.ctypes.data_as(_dp), total, C.byref(h)))
     return out[: h.value].copy()
+
+
+from .mg import MultiGPU, mg_heaphull_device  # noqa: E402  (multi-GPU, NCCL)

@@ -60,6 +60,12 @@ class FilterPlan(C.Structure):
                 ("kept_label", C.c_uint8 * 8), ("m", C.c_int32), ("pad", C.c_int32)]
 
 
+class MgInfo(C.Structure):
+    _fields_ = [("ext", _u64 * 8), ("counts", _u64 * 4), ("n_total", _u64),
+                ("corner_pass", C.c_uint32), ("fused_shards", C.c_uint32),
+                ("shards", C.c_uint32), ("pad", C.c_uint32), ("ms", C.c_double * 4)]
+
+
 # (name, restype, argtypes) of every entry point declared in include/ohx.h
 PROTOTYPES = [
     ("ohx_abi_version", C.c_int, []),
@@ -109,6 +115,20 @@ PROTOTYPES = [
     ("ohx_generate_range", C.c_int, [C.c_int, _u64, _u64, C.c_double, _u64, _u64, _dp, C.c_int]),
     ("ohx_hull_from_queues", C.c_int, [_dp, _u64p, C.POINTER(_u64p), _u64p, _dp, _u64, _u64p]),
     ("ohx_hull_from_queue_points", C.c_int, [_dp, C.POINTER(_dp), _u64p, _dp, _u64, _u64p]),
+    ("ohx_mg_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
+    ("ohx_mg_init_rank", C.c_int, [C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(_vp)]),
+    ("ohx_mg_init_all", C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(_vp)]),
+    ("ohx_mg_destroy", C.c_int, [_vp]),
+    ("ohx_mg_world", C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("ohx_mg_nccl_version", C.c_int, [C.POINTER(C.c_int)]),
+    ("ohx_mg_ctx", C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),
+    ("ohx_mg_heaphull_shard", C.c_int, [_vp, _vp, _u64, _u64, C.c_int, _u8p, _dp, _u64, _u64p,
+                                        C.POINTER(MgInfo)]),
+    ("ohx_mg_heaphull_device", C.c_int, [_vp, C.c_int, C.POINTER(_vp), _u64p, _u8p, _dp, _u64,
+                                         _u64p, C.POINTER(MgInfo)]),
+    ("ohx_mg_heaphull", C.c_int, [_vp, _dp, _u64, C.c_int, _u8p, _dp, _u64, _u64p,
+                                  C.POINTER(MgInfo)]),
 ]
 
 

@@ -264,70 +264,95 @@ std::uint64_t device_sort_min() {
   }();
   return v;
 }
+// The hull stage (reference hull.cpp:164-183) on survivors' coordinates
+// already packed on the device as [q1|q2|q3|q4] in index order; the hull
+// goes to sink.  Large sets: the arcs are built and sorted on the device
+// and come back in sweep order, the chains and the clean-up run on the
+// host; small sets: one D2H, then the host hull stage.
+std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint64_t counts[4],
+                             const P2 anchors[4], cudaStream_t s, const HullSink& sink) {
+  const std::uint64_t total = counts[0] + counts[1] + counts[2] + counts[3];
+  if (total < device_sort_min()) {
+    std::vector<P2> packed(total);
+    if (total) {
+      check_cuda(cudaMemcpyAsync(packed.data(), d_packed, total * 16, cudaMemcpyDeviceToHost, s),
+                 "cudaMemcpyAsync(survivors)");
+      check_cuda(cudaStreamSynchronize(s), "survivors D2H");
+    }
+    const P2* qp[4];
+    std::uint64_t off = 0;
+    for (int k = 0; k < 4; ++k) {
+      qp[k] = packed.data() + off;
+      off += counts[k];
+    }
+    const PVec cyc = hull_from_queue_points(anchors, qp, counts);
+    copy_points(sink(cyc.size()), cyc.data(), cyc.size());
+    return cyc.size();
+  }
+  const std::uint64_t arcs_n = total + 8;
+  dev_grow(&c->d_hsort, &c->hsort_bytes, sort_arcs_work_bytes(counts) + arcs_n * 16,
+           "hull sort work");
+  auto* d_sorted = reinterpret_cast<double*>(static_cast<unsigned char*>(c->d_hsort) +
+                                             sort_arcs_work_bytes(counts));
+  Trace tr;
+  sort_arcs(d_packed, counts, reinterpret_cast<const double*>(anchors), c->d_hsort, d_sorted, s);
+  c->launches += 2 + 4 * 4;  // build/gather + four radix sorts
+  if (tr.on) {
+    check_cuda(cudaStreamSynchronize(s), "hull sort");
+    tr.mark("hull dev sort");
+  }
+  host_grow(&c->h_sorted, &c->h_sorted_bytes, arcs_n * 16, "cudaMallocHost(sorted arcs)");
+  // one copy per arc: arc q's chain starts as soon as its copy lands
+  if (!c->arc_ev[0])
+    for (auto& e : c->arc_ev)
+      check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate(arc)");
+  const P2* arcs[4];
+  std::uint64_t len[4], off = 0;
+  for (int q = 0; q < 4; ++q) {
+    arcs[q] = static_cast<const P2*>(c->h_sorted) + off;
+    len[q] = counts[q] + 2;
+    check_cuda(cudaMemcpyAsync(static_cast<P2*>(c->h_sorted) + off,
+                               reinterpret_cast<const P2*>(d_sorted) + off, len[q] * 16,
+                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(sorted arc)");
+    check_cuda(cudaEventRecord(c->arc_ev[q], s), "cudaEventRecord(arc)");
+    off += len[q];
+  }
+  std::atomic<int> failed{cudaSuccess};  // set by the arc threads (no throwing there)
+  std::size_t h = 0;
+  try {
+    h = hull_from_sorted_arcs(
+        arcs, len,
+        [&](int q) {
+          const cudaError_t e = cudaEventSynchronize(c->arc_ev[q]);
+          if (e != cudaSuccess) failed = e;
+          return e == cudaSuccess;
+        },
+        sink);
+  } catch (...) {  // a lost arc: report the CUDA error behind it
+    check_cuda(static_cast<cudaError_t>(failed.load()), "cudaEventSynchronize(sorted arc)");
+    throw;
+  }
+  tr.mark("hull D2H + host");
+  return h;
+}
+
 std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
                                const HullSink& sink) {
-  // reference hull.cpp:164-183 on the device queues; the hull goes to sink
+  // reference hull.cpp:164-183 on the device queues of the last filter
   const std::uint64_t total = f.counts[0] + f.counts[1] + f.counts[2] + f.counts[3];
   const P2 anchors[4] = {{f.ext.x[OHX_EAST], f.ext.y[OHX_EAST]},
                          {f.ext.x[OHX_NORTH], f.ext.y[OHX_NORTH]},
                          {f.ext.x[OHX_WEST], f.ext.y[OHX_WEST]},
                          {f.ext.x[OHX_SOUTH], f.ext.y[OHX_SOUTH]}};
   if (total >= device_sort_min()) {
-    // large survivor sets: the arcs are built and sorted on the device and
-    // come back in sweep order; the chains and the clean-up run on the host
     grow_gather(c, total * 16);
     launch_gather4(c->last_xy, c->d_queues, c->last_idx_bytes, c->last_cap, c->last_counts,
                    c->d_gather, s);
     ++c->launches;
-    const std::uint64_t arcs_n = total + 8;
-    dev_grow(&c->d_hsort, &c->hsort_bytes, sort_arcs_work_bytes(f.counts) + arcs_n * 16,
-             "hull sort work");
-    auto* d_sorted = reinterpret_cast<double*>(static_cast<unsigned char*>(c->d_hsort) +
-                                               sort_arcs_work_bytes(f.counts));
-    Trace tr;
-    sort_arcs(c->d_gather, f.counts, reinterpret_cast<const double*>(anchors), c->d_hsort,
-              d_sorted, s);
-    c->launches += 2 + 4 * 4;  // build/gather + four radix sorts
-    if (tr.on) {
-      check_cuda(cudaStreamSynchronize(s), "hull sort");
-      tr.mark("hull dev sort");
-    }
-    host_grow(&c->h_sorted, &c->h_sorted_bytes, arcs_n * 16, "cudaMallocHost(sorted arcs)");
-    // one copy per arc: arc q's chain starts as soon as its copy lands
-    if (!c->arc_ev[0])
-      for (auto& e : c->arc_ev)
-        check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate(arc)");
-    const P2* arcs[4];
-    std::uint64_t len[4], off = 0;
-    for (int q = 0; q < 4; ++q) {
-      arcs[q] = static_cast<const P2*>(c->h_sorted) + off;
-      len[q] = f.counts[q] + 2;
-      check_cuda(cudaMemcpyAsync(static_cast<P2*>(c->h_sorted) + off,
-                                 reinterpret_cast<const P2*>(d_sorted) + off, len[q] * 16,
-                                 cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(sorted arc)");
-      check_cuda(cudaEventRecord(c->arc_ev[q], s), "cudaEventRecord(arc)");
-      off += len[q];
-    }
-    std::atomic<int> failed{cudaSuccess};  // set by the arc threads (no throwing there)
-    std::size_t h = 0;
-    try {
-      h = hull_from_sorted_arcs(
-          arcs, len,
-          [&](int q) {
-            const cudaError_t e = cudaEventSynchronize(c->arc_ev[q]);
-            if (e != cudaSuccess) failed = e;
-            return e == cudaSuccess;
-          },
-          sink);
-    } catch (...) {  // a lost arc: report the CUDA error behind it
-      check_cuda(static_cast<cudaError_t>(failed.load()), "cudaEventSynchronize(sorted arc)");
-      throw;
-    }
-    tr.mark("hull D2H + host");
-    return h;
+    return hull_from_packed(c, c->d_gather, f.counts, anchors, s, sink);
   }
-  // one gather launch and one D2H of the survivors' coordinates, then the
-  // host hull stage
+  // small sets: the survivors' coordinates (usually already fetched with
+  // the K2 counts), then the host hull stage
   std::vector<P2> packed(total);
   queues_fetch_xy(c, reinterpret_cast<double*>(packed.data()), s);
   const P2* qp[4];

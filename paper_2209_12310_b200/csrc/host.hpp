@@ -52,9 +52,9 @@ struct ohx_ctx {
   // the C++ API sets it to the caller's ReduceEngine workers -- the host
   // lanes the reference grants a call (parallel.hpp:18-21)
   int host_lanes = 0;
-  bool spec_zeroed = false;
-  void* d_poly = nullptr;  // classify_points' edges of a polygon with > 8 vertices
-  std::uint64_t poly_bytes = 0;  // d_gather's speculative survivor slots are cleared
+  bool spec_zeroed = false;  // d_gather's speculative survivor slots are cleared
+  void* d_poly = nullptr;    // classify_points' edges of a polygon with > 8 vertices
+  std::uint64_t poly_bytes = 0;
   // staging for host-API calls
   double* d_pts = nullptr;
   std::uint64_t pts_bytes = 0;

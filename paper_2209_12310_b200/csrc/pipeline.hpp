@@ -80,6 +80,9 @@ void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
 // survivor coordinates of all four queues, packed [q1|q2|q3|q4], one launch
 void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s);
 
+// hull stage on survivor coordinates packed on the device [q1|q2|q3|q4]
+std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint64_t counts[4],
+                             const P2 anchors[4], cudaStream_t s, const HullSink& sink);
 // host hull stage on the queues of the last filter (survivors gathered and
 // copied back in one launch)
 PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s);
@@ -90,5 +93,13 @@ std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
 // K1 -> certificate -> (K1b) -> octagon -> plan -> K2 on one device
 FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
                         std::uint8_t* d_labels, cudaStream_t s);
+
+// ---- multi-GPU (mg.cpp)
+// process-wide single-process communicator over devices 0..ndev-1
+ohx_mg* mg_default(int ndev);
+// host points over the handle's devices (vshards shards each), labels
+// (nullable) for every point; the hull to sink
+std::size_t mg_heaphull_host(ohx_mg* M, const double* h_xy, std::uint64_t n, int vshards,
+                             std::uint8_t* h_labels, const HullSink& sink, ohx_mg_info* info);
 
 }  // namespace ohx

@@ -17,12 +17,16 @@ of the reference (parallel.hpp:34-43) holds across shards.
   5. K2 on every shard -> four index-ordered queues per shard (fused: on the
      shard's candidates only, once its region is certified inside the
      global octagon)
-  6. survivor coordinates gathered to the root in rank order (= global
+  6. survivor coordinates sent to the root only, in rank order (= global
      index order, so the concatenation equals build_queues of the whole)
   7. the root runs the host hull stage (reference semantics) on them.
 
-The only exchanges are those small collectives: the data path itself is
-never communicated.  The per-shard compute sits behind a tiny interface
+The only exchanges are those small collectives and the survivors' trip to
+the root: the data path itself is never communicated.  This is the
+torch.distributed rendering of the protocol (gloo in the CPU tests, ranks
+sharing one GPU); the production multi-GPU path is the native NCCL layer
+behind the C ABI (csrc/mg.cpp, ohx_mg_*), which runs the same steps with
+the survivors moving device to device.  The per-shard compute sits behind a tiny interface
 (`extremes`, `corners_exact`, `filter`, `queue_xy`) implemented here by
 `CudaShard` over the C ABI; the CPU tests plug in an emulated shard to
 exercise the orchestration with world_size 2 over gloo.
@@ -89,8 +93,10 @@ def _allgather_structs(obj, cls, device):
 
 
 def _gather_queues(queues, device, root):
-    """Survivor coordinates of the 4 queues from every rank to `root`,
-    concatenated per quadrant in rank order."""
+    """Survivor coordinates of the 4 queues from every rank to `root` only
+    (exact-size point-to-point sends after an all-gather of the 4 queue
+    lengths), concatenated per quadrant in rank order.  Returns the 4
+    arrays on `root`, None elsewhere."""
     dist = _dist()
     if dist is None or dist.get_world_size() == 1:
         return queues
@@ -100,24 +106,30 @@ def _gather_queues(queues, device, root):
     all_counts = [torch.empty_like(counts) for _ in range(world)]
     dist.all_gather(all_counts, counts)
     all_counts = [c.cpu().numpy() for c in all_counts]
-    width = int(max(c.sum() for c in all_counts))
-    flat = np.zeros((max(width, 1), 2), dtype=np.float64)
-    mine = np.concatenate(queues) if sum(len(q) for q in queues) else np.zeros((0, 2))
-    flat[: len(mine)] = mine
-    t = torch.from_numpy(flat).to(device)
-    bufs = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(bufs, t)
     if rank != root:
+        mine = np.concatenate(queues) if sum(len(q) for q in queues) else np.zeros((0, 2))
+        if len(mine):
+            dist.send(torch.from_numpy(np.ascontiguousarray(mine)).to(device), dst=root)
         return None
-    per_q = [[] for _ in range(4)]
+    per_rank = []
     for r in range(world):
-        a = bufs[r].cpu().numpy()
-        off = 0
-        for q in range(4):
-            k = int(all_counts[r][q])
-            per_q[q].append(a[off: off + k])
-            off += k
-    return [np.concatenate(p) if p else np.zeros((0, 2)) for p in per_q]
+        k = int(all_counts[r].sum())
+        if r == root:
+            per_rank.append(np.concatenate(queues) if k else np.zeros((0, 2)))
+        elif k:
+            buf = torch.empty((k, 2), dtype=torch.float64, device=device)
+            dist.recv(buf, src=r)
+            per_rank.append(buf.cpu().numpy())
+        else:
+            per_rank.append(np.zeros((0, 2)))
+    out = []
+    for q in range(4):
+        parts = []
+        for r in range(world):
+            off = int(all_counts[r][:q].sum())
+            parts.append(per_rank[r][off: off + int(all_counts[r][q])])
+        out.append(np.concatenate(parts))
+    return out
 
 
 def sharded_heaphull(shard, device=None, root: int = 0, stats: dict | None = None):
