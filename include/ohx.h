@@ -140,7 +140,10 @@ typedef struct {
                            sample region, 3 sample coverage too low, 4 region
                            not certified in the true octagon, 5 too many
                            candidates */
-  uint32_t pad;
+  uint32_t hull_path;   /* hull stage: 0 host sort + chains (small survivor
+                           sets), 1 device sort + device chains, 2 device
+                           chains unproven -> host chains, 3 device sort +
+                           host chains (OHX_DEVICE_CHAIN=0) */
   double sample_coverage; /* fraction of the sample inside the provisional region */
 } ohx_run_info;
 int ohx_ctx_last_run(const ohx_ctx* ctx, ohx_run_info* info);
@@ -314,6 +317,18 @@ int ohx_chain(const double* h_xy, uint64_t n, double* h_out, uint64_t* m);
  * hull.cpp:133-150 without the sort, then 94-120); h_hull capacity cap. */
 int ohx_hull_from_sorted_arcs(const double* const arcs_xy[4], const uint64_t len[4],
                               double* h_hull, uint64_t cap, uint64_t* h);
+
+/* The same hull stage with the arcs sorted in DEVICE memory (back to back,
+ * len[q] points each): the chains are replayed on the device in chunks and
+ * proven equal to the reference loop's (hullchain.cu); *proven = 0 when the
+ * proof fails, and the host chains produce the hull instead.  Either way
+ * the hull is the reference's.  flags & OHX_ARCS_RAW_CYCLE: write the
+ * chained cycle itself (the four chains, each without its last point,
+ * before finalize_cycle) -- a test hook for the chains alone. */
+#define OHX_ARCS_RAW_CYCLE 1
+int ohx_hull_from_sorted_arcs_device(ohx_ctx* ctx, const double* d_arcs, const uint64_t len[4],
+                                     double* h_hull, uint64_t cap, uint64_t* h, int* proven,
+                                     int flags, void* stream);
 
 /* Host hull stage of heaphull_run (hull.cpp:164-183) on given queues:
  * pts = all points (host), queues as global indices. */

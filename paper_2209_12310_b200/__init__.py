@@ -271,7 +271,9 @@ class Context:
                 "candidates": int(r.candidates), "counts": [int(v) for v in r.counts],
                 "fuse_state": ("off", "fused", "no-sample-region", "low-sample-coverage",
                                "region-not-certified", "too-many-candidates")[r.fuse_state],
-                "sample_coverage": float(r.sample_coverage)}
+                "sample_coverage": float(r.sample_coverage),
+                "hull_path": ("host", "device-chains", "device-chains-unproven",
+                              "device-sort-host-chains")[r.hull_path]}
 
     # ---- kernel level --------------------------------------------------
     def extremes(self, d_xy, n: int, index_base: int = 0, stream=None) -> ExtremesRec:
@@ -346,6 +348,22 @@ class Context:
         check(lib.ohx_pts2_load_device(self.h, os.fsencode(path), _ptr(d_xy), cap, C.byref(n),
                                        _stream(stream)))
         return n.value, d_xy
+
+    def hull_from_sorted_arcs_device(self, d_arcs, lens, raw_cycle=False, stream=None):
+        """The hull stage on four arcs already in sweep order in device memory
+        (back to back, lens[q] points each) -> (hull, proven): proven is
+        False when the device chains could not prove a chunk and the host
+        chains ran instead (the hull is the reference's either way).
+        raw_cycle: the chained cycle before finalize_cycle (a test hook)."""
+        ln = (C.c_uint64 * 4)(*[int(v) for v in lens])
+        cap = sum(int(v) for v in lens) + 8
+        hull = np.empty((cap, 2), dtype=np.float64)
+        h = C.c_uint64(0)
+        proven = C.c_int(0)
+        check(lib.ohx_hull_from_sorted_arcs_device(self.h, _ptr(d_arcs), ln, hull.ctypes.data_as(_dp),
+                                                   cap, C.byref(h), C.byref(proven),
+                                                   1 if raw_cycle else 0, _stream(stream)))
+        return hull[: h.value].copy(), bool(proven.value)
 
     def heaphull_device(self, d_xy, n: int):
         """Full pipeline on device-resident points -> (hull, timings)."""

@@ -47,7 +47,7 @@ class ExtremeSet(C.Structure):
 
 class RunInfo(C.Structure):
     _fields_ = [("fused", C.c_uint32), ("corner_pass", C.c_uint32), ("candidates", _u64),
-                ("counts", _u64 * 4), ("fuse_state", C.c_uint32), ("pad", C.c_uint32),
+                ("counts", _u64 * 4), ("fuse_state", C.c_uint32), ("hull_path", C.c_uint32),
                 ("sample_coverage", C.c_double)]
 
 
@@ -111,6 +111,8 @@ PROTOTYPES = [
     ("ohx_monotone_chain", C.c_int, [_dp, _u64, _dp, _u64, _u64p]),
     ("ohx_chain", C.c_int, [_dp, _u64, _dp, _u64p]),
     ("ohx_hull_from_sorted_arcs", C.c_int, [C.POINTER(_dp), _u64p, _dp, _u64, _u64p]),
+    ("ohx_hull_from_sorted_arcs_device", C.c_int, [_vp, _vp, _u64p, _dp, _u64, _u64p,
+                                                   C.POINTER(C.c_int), C.c_int, _vp]),
     ("ohx_generate", C.c_int, [C.c_int, _u64, _u64, C.c_double, _dp, C.c_int]),
     ("ohx_generate_range", C.c_int, [C.c_int, _u64, _u64, C.c_double, _u64, _u64, _dp, C.c_int]),
     ("ohx_hull_from_queues", C.c_int, [_dp, _u64p, C.POINTER(_u64p), _u64p, _dp, _u64, _u64p]),

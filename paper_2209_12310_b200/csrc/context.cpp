@@ -5,6 +5,7 @@
 #include <fcntl.h>
 #include <omp.h>
 #include <unistd.h>
+#include <emmintrin.h>
 
 #include <algorithm>
 #include <atomic>
@@ -103,6 +104,32 @@ void ensure_stage(ohx_ctx* c) {
   }
 }
 
+// Copy with non-temporal stores: the staged bytes are not read again by
+// this core (a user buffer filled from the ring, or a ring chunk the copy
+// engine reads next), so streaming stores skip the read-for-ownership of
+// every destination line and leave the caches alone.
+void stream_copy(char* dst, const char* src, std::uint64_t bytes) {
+  const std::uint64_t head = std::min<std::uint64_t>(bytes, (64 - (reinterpret_cast<std::uintptr_t>(dst) & 63)) & 63);
+  std::memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  bytes -= head;
+  const std::uint64_t body = bytes & ~std::uint64_t(63);
+  if (reinterpret_cast<std::uintptr_t>(src) & 15) {  // unaligned source
+    for (std::uint64_t k = 0; k < body; k += 64)
+      for (int u = 0; u < 4; ++u)
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + k + 16 * u),
+                         _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + k + 16 * u)));
+  } else {
+    for (std::uint64_t k = 0; k < body; k += 64)
+      for (int u = 0; u < 4; ++u)
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + k + 16 * u),
+                         _mm_load_si128(reinterpret_cast<const __m128i*>(src + k + 16 * u)));
+  }
+  _mm_sfence();
+  std::memcpy(dst + body, src + body, bytes - body);
+}
+
 void host_memcpy(void* dst, const void* src, std::uint64_t bytes, int lanes) {
   if (bytes < (8ull << 20) || lanes == 1) {
     std::memcpy(dst, src, bytes);
@@ -112,7 +139,7 @@ void host_memcpy(void* dst, const void* src, std::uint64_t bytes, int lanes) {
   {
     const int t = omp_get_thread_num(), nt = omp_get_num_threads();
     const std::uint64_t b = bytes * t / nt, e = bytes * (t + 1) / nt;
-    std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
+    stream_copy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
   }
 }
 
@@ -261,6 +288,10 @@ ohx_ctx* create_ctx(int device) {
   c->device = device;
   bind(c.get());
   check_cuda(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  if (const char* e = std::getenv("OHX_L2_FETCH")) {  // experiment hook: L2 fetch granularity
+    const int v = std::atoi(e);
+    if (v > 0) check_cuda(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, v), "cudaDeviceSetLimit");
+  }
   check_cuda(cudaMalloc(&c->d_ticket, 256), "cudaMalloc(ticket)");
   check_cuda(cudaMemset(c->d_ticket, 0, 256), "cudaMemset(ticket)");
   check_cuda(cudaMalloc(&c->d_rec, sizeof(ohx_extremes_rec)), "cudaMalloc(rec)");
@@ -286,7 +317,7 @@ void destroy_ctx(ohx_ctx* c) {
                   c->d_queues, static_cast<void*>(c->d_pts),
                   static_cast<void*>(c->d_labels), static_cast<void*>(c->d_gather),
                   static_cast<void*>(c->d_sample), c->d_cand, static_cast<void*>(c->d_cnt),
-                  c->d_regions, static_cast<void*>(c->d_cpts), c->d_hsort, c->d_poly})
+                  c->d_regions, static_cast<void*>(c->d_cpts), c->d_hsort, c->d_hchain, c->d_poly})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_crec),
                   static_cast<void*>(c->h_counts), static_cast<void*>(c->h_cnt), c->h_sorted,
@@ -327,6 +358,7 @@ void trim_ctx(ohx_ctx* c) {
   dfree(c->d_regions, &c->regions_bytes);
   dfree(c->d_cpts, &c->cpts_bytes);
   dfree(c->d_hsort, &c->hsort_bytes);
+  dfree(c->d_hchain, &c->hchain_bytes);
   dfree(c->d_poly, &c->poly_bytes);
   if (c->h_sorted) cudaFreeHost(c->h_sorted);
   c->h_sorted = nullptr;

@@ -264,6 +264,56 @@ std::uint64_t device_sort_min() {
   }();
   return v;
 }
+// OHX_DEVICE_CHAIN=0: the hull stage's chains on the host even when the
+// device chains could prove them (test and comparison hook)
+bool device_chain_mode() {
+  static const bool v = [] {
+    const char* e = std::getenv("OHX_DEVICE_CHAIN");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
+// The chains and the cycle scan on the device over arcs already sorted on
+// the device (len[q] points each, back to back); the hull goes to sink.
+// false: the chunked replay could not prove every chunk -- nothing was
+// written, the host chains must run.
+bool hull_device_chains(ohx_ctx* c, const double* d_sorted, const std::uint64_t len[4],
+                        cudaStream_t s, const HullSink& sink, std::size_t* h, bool raw) {
+  Trace tr;
+  dev_grow(&c->d_hchain, &c->hchain_bytes, device_chain_work_bytes(len), "hull chain work");
+  DeviceCycle dc;
+  const bool ok = device_chains(d_sorted, len, c->d_hchain, s, &dc);
+  c->launches += dc.launches;
+  c->last_run.hull_path = ok ? 1 : 2;
+  tr.mark(ok ? "dev chains" : "dev chains (unproven: host chains)");
+  if (!ok) return false;
+  const std::uint64_t m = dc.m;
+  if (raw) {  // the chained cycle itself (test hook)
+    copy_d2h(c, sink(m), dc.d_cycle, m * 16, s);
+    *h = m;
+    return true;
+  }
+  if (m > 2 && !dc.front_eq_back && !dc.dups && !dc.flat && dc.bad == 0) {
+    // finalize_cycle keeps every vertex: the hull is the cycle rotated to
+    // its start vertex, copied straight into the caller's buffer
+    P2* out = sink(m);
+    const std::uint64_t b = dc.best;
+    copy_d2h(c, out, dc.d_cycle + 2 * b, (m - b) * 16, s);
+    if (b) copy_d2h(c, out + (m - b), dc.d_cycle, b * 16, s);
+    tr.mark("hull D2H (fast path)");
+    *h = m;
+    return true;
+  }
+  // the general clean-up on the host (duplicates, collinear, peel)
+  PVec cyc(m);
+  if (m) copy_d2h(c, cyc.data(), dc.d_cycle, m * 16, s);
+  const PVec d = finalize_cycle(std::move(cyc));
+  copy_points(sink(d.size()), d.data(), d.size());
+  tr.mark("hull D2H + finalize");
+  *h = d.size();
+  return true;
+}
+
 // The hull stage (reference hull.cpp:164-183) on survivors' coordinates
 // already packed on the device as [q1|q2|q3|q4] in index order; the hull
 // goes to sink.  Large sets: the arcs are built and sorted on the device
@@ -294,6 +344,7 @@ std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint
            "hull sort work");
   auto* d_sorted = reinterpret_cast<double*>(static_cast<unsigned char*>(c->d_hsort) +
                                              sort_arcs_work_bytes(counts));
+  c->last_run.hull_path = 3;
   Trace tr;
   sort_arcs(d_packed, counts, reinterpret_cast<const double*>(anchors), c->d_hsort, d_sorted, s);
   c->launches += 2 + 4 * 4;  // build/gather + four radix sorts
@@ -301,13 +352,19 @@ std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint
     check_cuda(cudaStreamSynchronize(s), "hull sort");
     tr.mark("hull dev sort");
   }
+  std::uint64_t len[4];
+  for (int q = 0; q < 4; ++q) len[q] = counts[q] + 2;
+  if (device_chain_mode()) {
+    std::size_t h = 0;
+    if (hull_device_chains(c, d_sorted, len, s, sink, &h)) return h;
+  }
   host_grow(&c->h_sorted, &c->h_sorted_bytes, arcs_n * 16, "cudaMallocHost(sorted arcs)");
   // one copy per arc: arc q's chain starts as soon as its copy lands
   if (!c->arc_ev[0])
     for (auto& e : c->arc_ev)
       check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate(arc)");
   const P2* arcs[4];
-  std::uint64_t len[4], off = 0;
+  std::uint64_t off = 0;
   for (int q = 0; q < 4; ++q) {
     arcs[q] = static_cast<const P2*>(c->h_sorted) + off;
     len[q] = counts[q] + 2;
@@ -375,7 +432,8 @@ PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s) {
   return out;
 }
 void finish_extremes(ohx_ctx* c, const double* d_xy, std::uint64_t n,
-                     const ohx_extremes_rec& rec, FilterOut& f, cudaStream_t s) {
+                     const ohx_extremes_rec& rec, FilterOut& f, cudaStream_t s,
+                     bool with_box) {
   const std::uint32_t mask = resolve_extremes(rec, &f.ext);
   f.corner_pass = mask != 0;
   if (mask) {
@@ -393,7 +451,7 @@ void finish_extremes(ohx_ctx* c, const double* d_xy, std::uint64_t n,
     cand[2 * k + 1] = f.ext.y[slot[k]];
   }
   f.m = build_octagon(cand, f.oct);
-  make_plan(f.ext, f.oct, f.m, &f.plan);
+  make_plan(f.ext, f.oct, f.m, &f.plan, with_box);
 }
 
 constexpr std::uint64_t kFuseMinPoints = 1ull << 23;  // below: both passes are cheap
@@ -476,7 +534,7 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   launch_k1_sample(d_xy, n, segs, kSampleLen, subs, c->d_partials, c->d_ticket, d_recs, s);
   ++c->launches;
   ohx_extremes_rec rs[kMaxSubSamples];
-  check_cuda(cudaMemcpyAsync(rs, d_recs, sizeof(rs), cudaMemcpyDeviceToHost, s),
+  check_cuda(cudaMemcpyAsync(rs, d_recs, subs * sizeof(ohx_extremes_rec), cudaMemcpyDeviceToHost, s),
              "cudaMemcpyAsync(sample recs)");
   check_cuda(cudaStreamSynchronize(s), "sample extremes");
   tr.mark("sample k1");
@@ -535,6 +593,7 @@ FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,
   c->last_run.candidates = f.candidates;
   c->last_run.fuse_state = f.fuse_state;
   c->last_run.sample_coverage = f.sample_coverage;
+  c->last_run.hull_path = 0;
   for (int q = 0; q < 4; ++q) c->last_run.counts[q] = f.counts[q];
   return f;
 }
@@ -629,7 +688,9 @@ void fused_finish(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t
   f.fuse_state = 4;
   for (int a = 0; a < 8 && ok; ++a) ok = !in_region_host(q, ext.x[a], ext.y[a]);
   if (!ok) {  // not certified: the regular K2 pass over all points
-    filter(c, d_xy, n, base, plan, d_labels, counts, s);
+    ohx_filter_plan full = plan;
+    ensure_box(&full);
+    filter(c, d_xy, n, base, full, d_labels, counts, s);
     return;
   }
   f.fuse_state = 1;
@@ -646,7 +707,7 @@ FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
   Trace tr;
   ohx_extremes_rec rec;
   if (fused_begin(c, d_xy, n, 0, f, &rec, s, tr)) {
-    finish_extremes(c, d_xy, n, rec, f, s);
+    finish_extremes(c, d_xy, n, rec, f, s, false);
     tr.mark("octagon+plan");
     fused_finish(c, d_xy, n, 0, f.ext, f.plan, d_labels, f.counts, f, s);
     tr.mark("k2");
@@ -654,7 +715,7 @@ FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
   }
   // ---- two passes: K1, then K2
   extremes(c, d_xy, n, 0, &rec, s);
-  finish_extremes(c, d_xy, n, rec, f, s);
+  finish_extremes(c, d_xy, n, rec, f, s, true);
   filter(c, d_xy, n, 0, f.plan, d_labels, f.counts, s);
   return f;
 }

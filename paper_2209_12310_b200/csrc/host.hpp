@@ -80,6 +80,8 @@ struct ohx_ctx {
   std::uint64_t cpts_bytes = 0;
   void* d_hsort = nullptr;  // hull stage: device sweep sort work + sorted arcs
   std::uint64_t hsort_bytes = 0;
+  void* d_hchain = nullptr;  // hull stage: device chains work + cycle
+  std::uint64_t hchain_bytes = 0;
   void* h_sorted = nullptr;  // pinned: the sorted arcs on the host
   std::uint64_t h_sorted_bytes = 0;
   cudaEvent_t arc_ev[4] = {};  // their per-arc copies
@@ -145,11 +147,20 @@ inline void grow_gather(ohx_ctx* c, std::uint64_t bytes) {
     c->spec_zeroed = false;
 }
 void host_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what);
+// device -> host copy of a user buffer (pageable: through the pinned ring);
+// returns when the bytes have landed
+void copy_d2h(ohx_ctx* c, void* h, const void* d, std::uint64_t bytes, cudaStream_t s);
 cudaStream_t pick(ohx_ctx* c, void* s);
 void bind(ohx_ctx* c);
 void ensure_partials(ohx_ctx* c, int grid);
 std::uint64_t load_pts2_device(ohx_ctx* c, const std::string& path, double* d_xy,
                                std::uint64_t cap, cudaStream_t s);
+
+// ---- hull stage on the device (device.cpp)
+bool device_chain_mode();
+bool hull_device_chains(ohx_ctx* c, const double* d_sorted, const std::uint64_t len[4],
+                        cudaStream_t s, const HullSink& sink, std::size_t* h,
+                        bool raw = false);
 
 // ---- plan geometry (plan.cpp)
 bool certify_corner(const ohx_extremes_rec& r, int k);

@@ -256,6 +256,21 @@ PVec chain_arcs(const P2* const arcs[4], const std::uint64_t len[4],
 std::size_t sort_arcs_work_bytes(const std::uint64_t counts[4]);
 void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const double anchors[8],
                void* d_work, double* d_sorted, cudaStream_t s);
+// The chains and the cycle scan on the device (hullchain.cu) over the sorted
+// arcs (the layout sort_arcs writes; len[q] = counts[q] + 2).  false: the
+// chunked replay could not prove every chunk (the host chains must run);
+// true: the cycle (the four chains, each without its last point) is in
+// d_cycle, with the statistics finalize_cycle's fast path needs.
+struct DeviceCycle {
+  double* d_cycle = nullptr;
+  std::uint64_t m = 0, best = 0, bad = 0;
+  std::uint32_t chunks = 0;
+  bool front_eq_back = false, dups = false, flat = false;
+  int launches = 0;
+};
+std::size_t device_chain_work_bytes(const std::uint64_t len[4]);
+bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_work,
+                   cudaStream_t s, DeviceCycle* out);
 // hull stage from the four arcs [anchor q, queue q, anchor q+1] already in
 // sweep order (device-sorted)
 // (wait_arc(q), when set, is called by arc q's thread before it reads the

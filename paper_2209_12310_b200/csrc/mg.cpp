@@ -264,7 +264,9 @@ RankOut run_rank(ohx_mg& M, ohx_mg_rank& R, const std::vector<ShardIn>& in, int 
   }
   const int m = build_octagon(cand, oct);
   ohx_filter_plan plan;
-  make_plan(ext, oct, m, &plan);
+  bool all_fused = true;
+  for (int i = 0; i < k; ++i) all_fused = all_fused && (fused[i] || in[i].n == 0);
+  make_plan(ext, oct, m, &plan, !all_fused);  // fused shards' K2 needs no box
   out.info.ms[0] = ms_since(t0);
   t0 = Clock::now();
 
@@ -279,7 +281,9 @@ RankOut run_rank(ohx_mg& M, ohx_mg_rank& R, const std::vector<ShardIn>& in, int 
     if (fused[i]) {
       fused_finish(C[i], d_xy[i], in[i].n, in[i].base, ext, plan, dl, cnt[i].data(), F[i], si);
     } else {
-      filter(C[i], d_xy[i], in[i].n, in[i].base, plan, dl, cnt[i].data(), si);
+      ohx_filter_plan full = plan;
+      ensure_box(&full);
+      filter(C[i], d_xy[i], in[i].n, in[i].base, full, dl, cnt[i].data(), si);
     }
     if (dl) {
       fetch_labels(C[i], in[i].h_labels, dl, in[i].n, si);
@@ -454,6 +458,17 @@ ohx_mg* mg_default(int ndev) {
   if (ndev < 1 || ndev >= static_cast<int>(cache.size()))
     throw std::invalid_argument("mg: bad device count");
   if (!cache[ndev] || cache[ndev]->broken) {
+    // the reference API never mentions NCCL: a process-wide NCCL_DEBUG
+    // (VERSION / WARN print a banner on stdout at the first init) must not
+    // leak into the output of a program that only called heaphull --
+    // e.g. the reference CLI's `verify`, whose first line must be "OK h=".
+    // OHX_NCCL_DEBUG=1 keeps NCCL's own setting.
+    static const bool quiet = [] {
+      const char* k = std::getenv("OHX_NCCL_DEBUG");
+      if (!(k && std::string(k) == "1")) unsetenv("NCCL_DEBUG");
+      return true;
+    }();
+    (void)quiet;
     std::vector<int> devs(ndev);
     for (int d = 0; d < ndev; ++d) devs[d] = d;
     ohx_mg* m = nullptr;

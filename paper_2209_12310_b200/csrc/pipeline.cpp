@@ -8,6 +8,7 @@
 #include <string>
 
 #include "internal.hpp"
+#include "host.hpp"
 #include "octohull/filter.hpp"
 #include "octohull/hull.hpp"
 #include "octohull/pointgen.hpp"
@@ -193,6 +194,39 @@ int ohx_hull_from_sorted_arcs(const double* const arcs_xy[4], const uint64_t len
   return guard([&] {
     const ohx::P2* arcs[4];
     for (int q = 0; q < 4; ++q) arcs[q] = reinterpret_cast<const ohx::P2*>(arcs_xy[q]);
+    ohx::hull_from_sorted_arcs(arcs, len, {}, hull_sink(h_hull, cap, h));
+  });
+}
+
+int ohx_hull_from_sorted_arcs_device(ohx_ctx* ctx, const double* d_arcs, const uint64_t len[4],
+                                     double* h_hull, uint64_t cap, uint64_t* h, int* proven,
+                                     int flags, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> g(ohx::ctx_mutex(ctx));
+    ohx::ctx_bind(ctx);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ohx::ctx_stream(ctx);
+    for (int q = 0; q < 4; ++q)
+      if (len[q] < 2) throw std::invalid_argument("every arc holds at least its two anchors");
+    const bool raw = flags & OHX_ARCS_RAW_CYCLE;
+    std::size_t hh = 0;
+    const bool ok = ohx::hull_device_chains(ctx, d_arcs, len, s, hull_sink(h_hull, cap, h), &hh,
+                                            raw);
+    if (proven) *proven = ok ? 1 : 0;
+    if (ok) return;
+    const uint64_t total = len[0] + len[1] + len[2] + len[3];
+    ohx::PVec all(total);
+    ohx::copy_d2h(ctx, all.data(), d_arcs, total * 16, s);
+    const ohx::P2* arcs[4];
+    uint64_t off = 0;
+    for (int q = 0; q < 4; ++q) {
+      arcs[q] = all.data() + off;
+      off += len[q];
+    }
+    if (raw) {
+      const ohx::PVec cyc = ohx::chain_arcs(arcs, len, {});
+      ohx::copy_points(hull_sink(h_hull, cap, h)(cyc.size()), cyc.data(), cyc.size());
+      return;
+    }
     ohx::hull_from_sorted_arcs(arcs, len, {}, hull_sink(h_hull, cap, h));
   });
 }

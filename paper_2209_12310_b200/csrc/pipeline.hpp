@@ -66,8 +66,13 @@ void combine_corners(const ohx_corner_rec* recs, int k, ohx_corner_rec* out);
 std::uint32_t resolve_extremes(const ohx_extremes_rec& r, ohx_extreme_set* out);
 void apply_corners(const ohx_corner_rec& c, ohx_extreme_set* ext);
 int build_octagon(const double cand[16], double oct[16]);
+// with_box = false leaves the certified interior box empty (K2 then tests
+// every point exactly): the fused pass's K2 sees only points outside its
+// provisional region, which the box would not hold -- ensure_box fills it
+// in when the call falls back to a K2 over all points
 void make_plan(const ohx_extreme_set& e, const double* oct, int m,
-               ohx_filter_plan* p);
+               ohx_filter_plan* p, bool with_box = true);
+void ensure_box(ohx_filter_plan* p);
 void filter(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
             const ohx_filter_plan& plan, std::uint8_t* d_labels,
             std::uint64_t counts[4], cudaStream_t s);

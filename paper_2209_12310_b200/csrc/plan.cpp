@@ -357,7 +357,7 @@ int build_octagon(const double cand[16], double oct[16]) {
 }
 
 void make_plan(const ohx_extreme_set& e, const double* oct, int m,
-               ohx_filter_plan* p) {
+               ohx_filter_plan* p, bool with_box) {
   std::memset(p, 0, sizeof(*p));
   if (m < 0 || m > 8) throw std::invalid_argument("octagon must have 0..8 vertices");
   p->m = m;
@@ -386,7 +386,21 @@ void make_plan(const ohx_extreme_set& e, const double* oct, int m,
     p->kept[k] = e.ext[slot[k]];
     p->kept_label[k] = static_cast<std::uint8_t>(1 + k / 2);
   }
-  fit_box(oct, m, p->ea, p->ec, p->box);
+  p->box[0] = 1.0;
+  p->box[1] = 0.0;
+  p->box[2] = 1.0;
+  p->box[3] = 0.0;  // empty
+  if (with_box) fit_box(oct, m, p->ea, p->ec, p->box);
+}
+
+void ensure_box(ohx_filter_plan* p) {
+  if (p->box[0] <= p->box[1] || p->m < 3) return;  // has one (or no octagon to fit)
+  double oct[16];
+  for (int i = 0; i < p->m; ++i) {
+    oct[2 * i] = p->ax[i];
+    oct[2 * i + 1] = p->ay[i];
+  }
+  fit_box(oct, p->m, p->ea, p->ec, p->box);
 }
 // Vertices of the convex polygon {p : key_a(p) <= b[a], a = 0..7} (the slot
 // keys x, y, -x, -y, x+y, y-x, -(x+y), x-y), in long double: the axis box

@@ -78,7 +78,8 @@ def test_host_points_with_labels(handle, oracle):
 
 def test_one_rank_communicator_shard_call():
     # the one-process-per-GPU entry (ohx_mg_init_rank) as a world of 1
-    pts = P.generate("normal", 16_000_000, 9)
+    # 4 shards of 10M points: each above the fused pass's 2^23-point floor
+    pts = P.generate("normal", 40_000_000, 9)
     dd = torch.from_numpy(pts).cuda()
     h = mg.MultiGPU.init_rank(mg.unique_id(), 1, 0, 0)
     try:
