@@ -261,6 +261,13 @@ int ohx_heaphull(const double* h_xy, uint64_t n, double* h_hull, uint64_t cap,
 int ohx_heaphull_device(ohx_ctx* ctx, const double* d_xy, uint64_t n,
                         double* h_hull, uint64_t cap, uint64_t* h,
                         double* timings);
+/* The same with the hull left in DEVICE memory (d_hull, capacity cap
+ * points, on ctx's device): for a consumer on the GPU, the hull stage skips
+ * the PCIe copy of the hull (96.8M vertices = 1.55 GB for points on a
+ * circle).  Small survivor sets still chain on the host; their hull is
+ * copied up. */
+int ohx_heaphull_device_out(ohx_ctx* ctx, const double* d_xy, uint64_t n, double* d_hull,
+                            uint64_t cap, uint64_t* h, double* timings);
 /* classify (python/module.cpp:91-108): find_extremes + build_octagon +
  * classify_points, labels to the host. */
 int ohx_classify(const double* h_xy, uint64_t n, uint8_t* h_labels);

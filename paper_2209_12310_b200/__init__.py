@@ -365,8 +365,26 @@ class Context:
                                                    1 if raw_cycle else 0, _stream(stream)))
         return hull[: h.value].copy(), bool(proven.value)
 
-    def heaphull_device(self, d_xy, n: int):
-        """Full pipeline on device-resident points -> (hull, timings)."""
+    def heaphull_device(self, d_xy, n: int, out: str = "host"):
+        """Full pipeline on device-resident points -> (hull, timings).
+        out="device": the hull stays in device memory (a torch tensor on this
+        context's device) -- ohx_heaphull_device_out."""
+        if out == "device":
+            import torch
+            cap = n + 8 if n <= (1 << 26) else 1 << 24
+            while True:
+                hull = torch.empty((cap, 2), dtype=torch.float64, device=f"cuda:{self.device}")
+                h = C.c_uint64(0)
+                t = np.zeros(4, dtype=np.float64)
+                rc = lib.ohx_heaphull_device_out(self.h, _ptr(d_xy), n, _ptr(hull), cap,
+                                                 C.byref(h), t.ctypes.data_as(_dp))
+                if rc == OHX_E_INVALID and h.value > cap:
+                    cap = h.value
+                    continue
+                check(rc)
+                return hull[: h.value], dict(filter_ms=t[0], hull_ms=t[1], total_ms=t[2])
+        if out != "host":
+            raise ValueError("out must be 'host' or 'device'")
         # the output buffer is virtual until written: full size up to 2^28
         # points, else start at 2^24 and grow if the hull outgrows it
         cap = n + 8 if n <= (1 << 28) else 1 << 24

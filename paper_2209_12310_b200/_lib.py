@@ -99,6 +99,7 @@ PROTOTYPES = [
                                    C.POINTER(_u64)]),
     ("ohx_heaphull", C.c_int, [_dp, _u64, _dp, _u64, _u64p, _dp]),
     ("ohx_heaphull_device", C.c_int, [_vp, _vp, _u64, _dp, _u64, _u64p, _dp]),
+    ("ohx_heaphull_device_out", C.c_int, [_vp, _vp, _u64, _vp, _u64, _u64p, _dp]),
     ("ohx_hull_indices", C.c_int, [_vp, _dp, _u64, _u64p, _vp]),
     ("ohx_hull_indices_partial", C.c_int, [_vp, _dp, _u64, _u64p, _vp]),
     ("ohx_classify", C.c_int, [_dp, _u64, _u8p]),

@@ -288,10 +288,6 @@ ohx_ctx* create_ctx(int device) {
   c->device = device;
   bind(c.get());
   check_cuda(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
-  if (const char* e = std::getenv("OHX_L2_FETCH")) {  // experiment hook: L2 fetch granularity
-    const int v = std::atoi(e);
-    if (v > 0) check_cuda(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, v), "cudaDeviceSetLimit");
-  }
   check_cuda(cudaMalloc(&c->d_ticket, 256), "cudaMalloc(ticket)");
   check_cuda(cudaMemset(c->d_ticket, 0, 256), "cudaMemset(ticket)");
   check_cuda(cudaMalloc(&c->d_rec, sizeof(ohx_extremes_rec)), "cudaMalloc(rec)");

@@ -273,12 +273,37 @@ bool device_chain_mode() {
   }();
   return v;
 }
+// A host-computed hull into the sink (a device sink: one H2D copy).
+std::size_t emit_host_hull(const PVec& cyc, const HullSink& sink, bool dev, cudaStream_t s) {
+  P2* out = sink(cyc.size());
+  if (!dev) {
+    copy_points(out, cyc.data(), cyc.size());
+  } else if (!cyc.empty()) {
+    check_cuda(cudaMemcpyAsync(out, cyc.data(), cyc.size() * 16, cudaMemcpyHostToDevice, s),
+               "cudaMemcpyAsync(hull H2D)");
+    check_cuda(cudaStreamSynchronize(s), "hull H2D");
+  }
+  return cyc.size();
+}
+// bytes of device memory into the sink (host: the staging path; device: D2D)
+void emit_device_bytes(ohx_ctx* c, P2* out, const double* d_src, std::uint64_t bytes, bool dev,
+                       cudaStream_t s) {
+  if (!bytes) return;
+  if (!dev) {
+    copy_d2h(c, out, d_src, bytes, s);
+    return;
+  }
+  check_cuda(cudaMemcpyAsync(out, d_src, bytes, cudaMemcpyDeviceToDevice, s),
+             "cudaMemcpyAsync(hull D2D)");
+}
+
 // The chains and the cycle scan on the device over arcs already sorted on
 // the device (len[q] points each, back to back); the hull goes to sink.
 // false: the chunked replay could not prove every chunk -- nothing was
 // written, the host chains must run.
 bool hull_device_chains(ohx_ctx* c, const double* d_sorted, const std::uint64_t len[4],
-                        cudaStream_t s, const HullSink& sink, std::size_t* h, bool raw) {
+                        cudaStream_t s, const HullSink& sink, std::size_t* h, bool raw,
+                        bool dev) {
   Trace tr;
   dev_grow(&c->d_hchain, &c->hchain_bytes, device_chain_work_bytes(len), "hull chain work");
   DeviceCycle dc;
@@ -289,7 +314,8 @@ bool hull_device_chains(ohx_ctx* c, const double* d_sorted, const std::uint64_t 
   if (!ok) return false;
   const std::uint64_t m = dc.m;
   if (raw) {  // the chained cycle itself (test hook)
-    copy_d2h(c, sink(m), dc.d_cycle, m * 16, s);
+    emit_device_bytes(c, sink(m), dc.d_cycle, m * 16, dev, s);
+    if (dev) check_cuda(cudaStreamSynchronize(s), "hull D2D");
     *h = m;
     return true;
   }
@@ -298,9 +324,10 @@ bool hull_device_chains(ohx_ctx* c, const double* d_sorted, const std::uint64_t 
     // its start vertex, copied straight into the caller's buffer
     P2* out = sink(m);
     const std::uint64_t b = dc.best;
-    copy_d2h(c, out, dc.d_cycle + 2 * b, (m - b) * 16, s);
-    if (b) copy_d2h(c, out + (m - b), dc.d_cycle, b * 16, s);
-    tr.mark("hull D2H (fast path)");
+    emit_device_bytes(c, out, dc.d_cycle + 2 * b, (m - b) * 16, dev, s);
+    emit_device_bytes(c, out + (m - b), dc.d_cycle, b * 16, dev, s);
+    if (dev) check_cuda(cudaStreamSynchronize(s), "hull D2D");
+    tr.mark(dev ? "hull D2D (fast path)" : "hull D2H (fast path)");
     *h = m;
     return true;
   }
@@ -308,7 +335,7 @@ bool hull_device_chains(ohx_ctx* c, const double* d_sorted, const std::uint64_t 
   PVec cyc(m);
   if (m) copy_d2h(c, cyc.data(), dc.d_cycle, m * 16, s);
   const PVec d = finalize_cycle(std::move(cyc));
-  copy_points(sink(d.size()), d.data(), d.size());
+  emit_host_hull(d, sink, dev, s);
   tr.mark("hull D2H + finalize");
   *h = d.size();
   return true;
@@ -320,7 +347,8 @@ bool hull_device_chains(ohx_ctx* c, const double* d_sorted, const std::uint64_t 
 // and come back in sweep order, the chains and the clean-up run on the
 // host; small sets: one D2H, then the host hull stage.
 std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint64_t counts[4],
-                             const P2 anchors[4], cudaStream_t s, const HullSink& sink) {
+                             const P2 anchors[4], cudaStream_t s, const HullSink& sink,
+                             bool dev) {
   const std::uint64_t total = counts[0] + counts[1] + counts[2] + counts[3];
   if (total < device_sort_min()) {
     std::vector<P2> packed(total);
@@ -335,9 +363,7 @@ std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint
       qp[k] = packed.data() + off;
       off += counts[k];
     }
-    const PVec cyc = hull_from_queue_points(anchors, qp, counts);
-    copy_points(sink(cyc.size()), cyc.data(), cyc.size());
-    return cyc.size();
+    return emit_host_hull(hull_from_queue_points(anchors, qp, counts), sink, dev, s);
   }
   const std::uint64_t arcs_n = total + 8;
   dev_grow(&c->d_hsort, &c->hsort_bytes, sort_arcs_work_bytes(counts) + arcs_n * 16,
@@ -356,7 +382,7 @@ std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint
   for (int q = 0; q < 4; ++q) len[q] = counts[q] + 2;
   if (device_chain_mode()) {
     std::size_t h = 0;
-    if (hull_device_chains(c, d_sorted, len, s, sink, &h)) return h;
+    if (hull_device_chains(c, d_sorted, len, s, sink, &h, false, dev)) return h;
   }
   host_grow(&c->h_sorted, &c->h_sorted_bytes, arcs_n * 16, "cudaMallocHost(sorted arcs)");
   // one copy per arc: arc q's chain starts as soon as its copy lands
@@ -376,6 +402,11 @@ std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint
   }
   std::atomic<int> failed{cudaSuccess};  // set by the arc threads (no throwing there)
   std::size_t h = 0;
+  PVec host_out;  // a device sink: the host result, copied up once
+  const HullSink host_sink = [&](std::size_t hh) {
+    host_out.resize(hh);
+    return host_out.data();
+  };
   try {
     h = hull_from_sorted_arcs(
         arcs, len,
@@ -384,17 +415,18 @@ std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint
           if (e != cudaSuccess) failed = e;
           return e == cudaSuccess;
         },
-        sink);
+        dev ? host_sink : sink);
   } catch (...) {  // a lost arc: report the CUDA error behind it
     check_cuda(static_cast<cudaError_t>(failed.load()), "cudaEventSynchronize(sorted arc)");
     throw;
   }
+  if (dev) emit_host_hull(host_out, sink, true, s);
   tr.mark("hull D2H + host");
   return h;
 }
 
 std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
-                               const HullSink& sink) {
+                               const HullSink& sink, bool dev) {
   // reference hull.cpp:164-183 on the device queues of the last filter
   const std::uint64_t total = f.counts[0] + f.counts[1] + f.counts[2] + f.counts[3];
   const P2 anchors[4] = {{f.ext.x[OHX_EAST], f.ext.y[OHX_EAST]},
@@ -406,7 +438,7 @@ std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
     launch_gather4(c->last_xy, c->d_queues, c->last_idx_bytes, c->last_cap, c->last_counts,
                    c->d_gather, s);
     ++c->launches;
-    return hull_from_packed(c, c->d_gather, f.counts, anchors, s, sink);
+    return hull_from_packed(c, c->d_gather, f.counts, anchors, s, sink, dev);
   }
   // small sets: the survivors' coordinates (usually already fetched with
   // the K2 counts), then the host hull stage
@@ -418,9 +450,7 @@ std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
     qp[k] = packed.data() + off;
     off += f.counts[k];
   }
-  const PVec cyc = hull_from_queue_points(anchors, qp, f.counts);
-  copy_points(sink(cyc.size()), cyc.data(), cyc.size());
-  return cyc.size();
+  return emit_host_hull(hull_from_queue_points(anchors, qp, f.counts), sink, dev, s);
 }
 
 PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s) {
@@ -699,6 +729,16 @@ void fused_finish(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t
   filter_core(c, d_xy, n, base, plan, d_labels, counts, s, c->d_cand, c->fz.n_cand, c->d_cpts);
 }
 
+// OHX_FUSED_BOX=1: fit the certified interior box in the fused path too
+// (A/B hook: K2 there sees only candidates, outside the provisional region)
+bool fused_box() {
+  static const bool v = [] {
+    const char* e = std::getenv("OHX_FUSED_BOX");
+    return e && std::string(e) == "1";
+  }();
+  return v;
+}
+
 FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
                              std::uint8_t* d_labels, cudaStream_t s) {
   if (n == 0) throw std::invalid_argument("heaphull: empty point set");
@@ -707,7 +747,7 @@ FilterOut device_filter_impl(ohx_ctx* c, const double* d_xy, std::uint64_t n,
   Trace tr;
   ohx_extremes_rec rec;
   if (fused_begin(c, d_xy, n, 0, f, &rec, s, tr)) {
-    finish_extremes(c, d_xy, n, rec, f, s, false);
+    finish_extremes(c, d_xy, n, rec, f, s, fused_box());
     tr.mark("octagon+plan");
     fused_finish(c, d_xy, n, 0, f.ext, f.plan, d_labels, f.counts, f, s);
     tr.mark("k2");

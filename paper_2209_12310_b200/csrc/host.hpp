@@ -160,7 +160,7 @@ std::uint64_t load_pts2_device(ohx_ctx* c, const std::string& path, double* d_xy
 bool device_chain_mode();
 bool hull_device_chains(ohx_ctx* c, const double* d_sorted, const std::uint64_t len[4],
                         cudaStream_t s, const HullSink& sink, std::size_t* h,
-                        bool raw = false);
+                        bool raw = false, bool dev = false);
 
 // ---- plan geometry (plan.cpp)
 bool certify_corner(const ohx_extremes_rec& r, int k);

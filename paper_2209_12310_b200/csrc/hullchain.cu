@@ -47,8 +47,8 @@
 #include <cstdint>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
-#include <cub/iterator/counting_input_iterator.cuh>
-#include <cub/iterator/transform_input_iterator.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "internal.hpp"
 
@@ -315,8 +315,8 @@ std::size_t scan_tmp_bytes(std::uint32_t chunks) {
 
 std::size_t stat_tmp_bytes(std::uint64_t m) {
   std::size_t b = 0;
-  cub::CountingInputIterator<std::uint64_t> it(0);
-  cub::TransformInputIterator<CycStat, StatOf, cub::CountingInputIterator<std::uint64_t>> tin(
+  thrust::counting_iterator<std::uint64_t> it(0);
+  thrust::transform_iterator<StatOf, thrust::counting_iterator<std::uint64_t>, CycStat> tin(
       it, StatOf{nullptr, 1});
   check_cuda(cub::DeviceReduce::Reduce(nullptr, b, tin, static_cast<CycStat*>(nullptr),
                                        static_cast<std::int64_t>(m), StatCombine{}, CycStat{}),
@@ -425,8 +425,8 @@ bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_w
   out->m = m;
   out->chunks = G;
   if (m == 0) return true;
-  cub::CountingInputIterator<std::uint64_t> it(0);
-  cub::TransformInputIterator<CycStat, StatOf, cub::CountingInputIterator<std::uint64_t>> tin(
+  thrust::counting_iterator<std::uint64_t> it(0);
+  thrust::transform_iterator<StatOf, thrust::counting_iterator<std::uint64_t>, CycStat> tin(
       it, StatOf{cycle, m});
   CycStat init{};
   init.bx = -INFINITY;

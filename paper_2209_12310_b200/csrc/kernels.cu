@@ -668,7 +668,7 @@ constexpr std::uint64_t kFlagP = 2ull << 62;  // inclusive prefix published
 constexpr std::uint64_t kValMask = (1ull << 62) - 1;
 constexpr int kK2Warps = kK2Block / 32;
 constexpr int kK2Seg = kK2Items * kK2Warps;  // (item, warp) segments of a tile
-constexpr int kK2Stage = 128;  // staged hard points per warp (half its items)
+constexpr int kK2Stage = 256;  // staged hard points per warp (all its items)
 
 // orientation(a, b, p) < 0 with the edge constants A = fl(b.x-a.x),
 // C = fl(b.y-a.y): det = fl(fl(A*fl(p.y-a.y)) - fl(C*fl(p.x-a.x))) is
@@ -701,21 +701,6 @@ __device__ __forceinline__ double4 edge_at(const double4* e) {
   return r;
 }
 
-// Full classification of a point outside the certified box: the octagon test
-// (filter.cpp:125-128, geometry.cpp:16-22; "some edge < 0" in any order, so
-// all edges are evaluated branch-free) and then find_queue in its fixed
-// first-match order (filter.cpp:94-101).
-__device__ __forceinline__ std::uint32_t classify_hard(const double4* E, int m, double2 p) {
-  bool out = m < 3;  // degenerate octagon filters nothing (filter.cpp:125)
-#pragma unroll
-  for (int e = 0; e < 8; ++e) out |= right_of(p.x, p.y, edge_at(E + e));
-  if (!out) return 0;
-  std::uint32_t q = 1;  // default queue (filter.cpp:101)
-#pragma unroll
-  for (int k = 3; k >= 0; --k)  // the lowest matching edge wins
-    if (right_of(p.x, p.y, edge_at(E + 8 + k))) q = k + 1;
-  return q;
-}
 
 // One warp walks back over predecessor status words of one quadrant and
 // returns the exclusive prefix (decoupled look-back).
@@ -794,33 +779,60 @@ __device__ __forceinline__ std::uint32_t k2_label_tile(const KPlan& plan, const 
     }
     hard |= std::uint32_t(h) << it;
   }
-  // 2) the warp's hard points are packed into shared memory, four items at
-  //    a time, and classified 32 at a time: a few out-of-box lanes do not
-  //    make every item of the warp pay for the full test, and the full test
-  //    is instantiated once (a rolled loop) instead of per item
+  // 2) the warp's hard points are packed into shared memory and classified
+  //    there: a few out-of-box lanes do not make every item of the warp pay
+  //    for the full test, and each lane tests up to four staged points per
+  //    read of an edge's constants (warp-uniform shared loads: with one
+  //    point per read they were the shared-memory pipe's whole budget on
+  //    inputs where every point is hard -- ncu, circle 1e8: L1/shared 93 %
+  //    busy, FP64 pipe 40 %)
   if (__any_sync(kFull, hard != 0)) {
+    std::uint32_t H = 0;
 #pragma unroll
-    for (int half = 0; half < kK2Items / 4; ++half) {
-      std::uint32_t H = 0;
+    for (int it = 0; it < kK2Items; ++it) {
+      const unsigned hb = __ballot_sync(kFull, hard >> it & 1u);
+      if (hard >> it & 1u) S.stage[warp][H + __popc(hb & lt)] = v[it];
+      H += __popc(hb);
+    }
+    __syncwarp();
+    // (gather mode holds more live state: two points per read there)
+    constexpr int U = std::is_void_v<GIdx> ? 4 : 2;
+    for (std::uint32_t s0 = lane; s0 < H; s0 += U * 32) {
+      double2 p[U];
 #pragma unroll
-      for (int it = 4 * half; it < 4 * half + 4; ++it) {
-        const unsigned hb = __ballot_sync(kFull, hard >> it & 1u);
-        if (hard >> it & 1u) S.stage[warp][H + __popc(hb & lt)] = v[it];
-        H += __popc(hb);
+      for (int u = 0; u < U; ++u)
+        p[u] = s0 + 32 * u < H ? S.stage[warp][s0 + 32 * u] : make_double2(0.0, 0.0);
+      bool out[U];
+      std::uint32_t q[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        out[u] = plan.m < 3;  // degenerate octagon filters nothing (filter.cpp:125)
+        q[u] = 1;             // default queue (filter.cpp:101)
       }
-      if (H == 0) continue;
-      __syncwarp();
-      for (std::uint32_t slot = lane; slot < H; slot += 32)
-        S.lab[warp][slot] = static_cast<std::uint8_t>(classify_hard(S.edge, plan.m, S.stage[warp][slot]));
-      __syncwarp();
-      H = 0;
 #pragma unroll
-      for (int it = 4 * half; it < 4 * half + 4; ++it) {
-        const unsigned hb = __ballot_sync(kFull, hard >> it & 1u);
-        if (hard >> it & 1u) labs |= std::uint32_t(S.lab[warp][H + __popc(hb & lt)]) << (4 * it);
-        H += __popc(hb);
+      for (int e = 0; e < 8; ++e) {  // "some edge < 0", in any order
+        const double4 E = edge_at(S.edge + e);
+#pragma unroll
+        for (int u = 0; u < U; ++u) out[u] |= right_of(p[u].x, p[u].y, E);
       }
-      __syncwarp();  // the next half reuses the stage
+#pragma unroll
+      for (int k = 3; k >= 0; --k) {  // find_queue: the lowest matching edge wins
+        const double4 E = edge_at(S.edge + 8 + k);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (right_of(p[u].x, p[u].y, E)) q[u] = k + 1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (s0 + 32 * u < H) S.lab[warp][s0 + 32 * u] = static_cast<std::uint8_t>(out[u] ? q[u] : 0);
+    }
+    __syncwarp();
+    H = 0;
+#pragma unroll
+    for (int it = 0; it < kK2Items; ++it) {
+      const unsigned hb = __ballot_sync(kFull, hard >> it & 1u);
+      if (hard >> it & 1u) labs |= std::uint32_t(S.lab[warp][H + __popc(hb & lt)]) << (4 * it);
+      H += __popc(hb);
     }
   }
   return labs;
@@ -951,6 +963,7 @@ __global__ void __launch_bounds__(kK2cBlock)
   __shared__ std::uint32_t s_tot[4];
   __shared__ std::uint32_t s_pre[4][G];  // group-level exclusive prefix per tile
   __shared__ std::uint16_t s_src[4][G];  // quadrant offset inside each tile slice
+  __shared__ std::uint16_t s_cnt[4][G];  // survivors of each quadrant in each tile
   __shared__ std::uint32_t s_w0[4];      // warp 0's totals
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const std::uint64_t ngroups = (ntiles + G - 1) / G;
@@ -966,6 +979,8 @@ __global__ void __launch_bounds__(kK2cBlock)
     s_src[1][threadIdx.x] = static_cast<std::uint16_t>(c[0]);
     s_src[2][threadIdx.x] = static_cast<std::uint16_t>(c[0] + c[1]);
     s_src[3][threadIdx.x] = static_cast<std::uint16_t>(c[0] + c[1] + c[2]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s_cnt[q][threadIdx.x] = static_cast<std::uint16_t>(c[q]);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       std::uint32_t incl = c[q];
@@ -1001,26 +1016,32 @@ __global__ void __launch_bounds__(kK2cBlock)
     }
   }
   __syncthreads();
-  // flattened copy: survivor k of quadrant q in this group lives in the tile
-  // found by binary search over the prefix, so all loads are independent
+  // copy: one warp per (quadrant, tile) run -- a run is contiguous in the
+  // tile's scratch slice and in the queue, so loads and stores coalesce;
+  // four independent loads in flight per lane (survivor-heavy inputs: with
+  // a per-survivor binary search over the group prefix this kernel was
+  // latency-bound, 0.39 ms for the circle's 1e8 survivors)
+  constexpr int kWarps = kK2cBlock / 32;
 #pragma unroll 1
-  for (int q = 0; q < 4; ++q) {
-    const std::uint32_t total = s_tot[q];
-    IdxT* out = queues + std::uint64_t(q) * cap + s_excl[q];
-    const std::uint64_t room = cap > s_excl[q] ? cap - s_excl[q] : 0;
-    for (std::uint32_t k = threadIdx.x; k < total; k += kK2cBlock) {
-      int lo = 0, hi = G - 1;  // the last tile whose prefix is <= k
+  for (int r = warp; r < 4 * G; r += kWarps) {
+    const int q = r / G, ti = r % G;
+    const std::uint32_t cnt = s_cnt[q][ti];
+    if (cnt == 0) continue;
+    const std::uint64_t t = g * G + ti;
+    const std::uint64_t dst = s_excl[q] + s_pre[q][ti];
+    IdxT* out = queues + std::uint64_t(q) * cap;
+    const std::uint16_t* src = scratch + t * kK2Tile + s_src[q][ti];
+    for (std::uint32_t e0 = lane; e0 < cnt; e0 += 4 * 32) {
+      std::uint16_t v[4];
 #pragma unroll
-      for (int step = 0; step < 6; ++step) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_pre[q][mid] <= k) lo = mid;
-        else hi = mid - 1;
-      }
-      const std::uint64_t t = g * G + lo;
-      const std::uint32_t e = k - s_pre[q][lo];
-      if (k < room) {
-        const std::uint64_t item = t * kK2Tile + scratch[t * kK2Tile + s_src[q][lo] + e];
-        out[k] = kGather ? gidx[item] : static_cast<IdxT>(item);
+      for (int u = 0; u < 4; ++u) v[u] = e0 + 32 * u < cnt ? src[e0 + 32 * u] : std::uint16_t(0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const std::uint32_t e = e0 + 32 * u;
+        if (e < cnt && dst + e < cap) {
+          const std::uint64_t item = t * kK2Tile + v[u];
+          out[dst + e] = kGather ? gidx[item] : static_cast<IdxT>(item);
+        }
       }
     }
   }

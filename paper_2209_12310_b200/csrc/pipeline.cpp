@@ -105,6 +105,27 @@ int ohx_heaphull_device(ohx_ctx* ctx, const double* d_xy, uint64_t n, double* h_
   });
 }
 
+int ohx_heaphull_device_out(ohx_ctx* ctx, const double* d_xy, uint64_t n, double* d_hull,
+                            uint64_t cap, uint64_t* h, double* timings) {
+  return guard([&] {
+    if (n == 0) throw std::invalid_argument("heaphull: empty point set");
+    std::lock_guard<std::mutex> g(ohx::ctx_mutex(ctx));
+    ohx::ctx_bind(ctx);
+    cudaStream_t s = ohx::ctx_stream(ctx);
+    const auto t0 = Clock::now();
+    const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
+    const auto t1 = Clock::now();
+    ohx::device_queues_hull(ctx, f, s, hull_sink(d_hull, cap, h), true);
+    const auto t2 = Clock::now();
+    if (timings) {
+      timings[0] = ms(t0, t1);
+      timings[1] = ms(t1, t2);
+      timings[2] = ms(t0, t2);
+      timings[3] = 0.0;
+    }
+  });
+}
+
 int ohx_heaphull_pts2(const char* path, double* h_hull, uint64_t cap, uint64_t* h,
                       double* timings) {
   // the reference CLI's read_points(Binary) + heaphull (tools/octohull_main

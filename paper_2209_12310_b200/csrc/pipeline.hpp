@@ -86,14 +86,16 @@ void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
 void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s);
 
 // hull stage on survivor coordinates packed on the device [q1|q2|q3|q4]
+// (dev: sink hands out DEVICE memory -- the hull stays on the device)
 std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint64_t counts[4],
-                             const P2 anchors[4], cudaStream_t s, const HullSink& sink);
+                             const P2 anchors[4], cudaStream_t s, const HullSink& sink,
+                             bool dev = false);
 // host hull stage on the queues of the last filter (survivors gathered and
 // copied back in one launch)
 PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s);
 // ... written to sink(h) instead (the caller's buffer); returns h
 std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
-                               const HullSink& sink);
+                               const HullSink& sink, bool dev = false);
 
 // K1 -> certificate -> (K1b) -> octagon -> plan -> K2 on one device
 FilterOut device_filter(ohx_ctx* c, const double* d_xy, std::uint64_t n,

@@ -180,12 +180,15 @@ from oracle import Oracle
 o = Oracle(); ctx = P.Context(0)
 for dist, n, seed, d, want_path in [("circle", 1_000_000, 3, 0.0, "device-chains"),
                                     ("circle", 1_000_000, 5, 2.0, None),
-                                    ("disk", 2_000_000, 7, 0.0, None)]:
+                                    ("disk", 2_000_000, 7, 0.0, None),
+                                    ("normal", 300_000, 2, 0.0, "host")]:
     pts = P.generate(dist, n, seed, d)
     dx = torch.from_numpy(pts).cuda()
     hull, _ = ctx.heaphull_device(dx, n)
     info = ctx.last_run()
     assert np.array_equal(hull, o.heaphull(pts)), (dist, n, info)
+    dh, _ = ctx.heaphull_device(dx, n, out="device")  # the hull left on the device
+    assert dh.is_cuda and np.array_equal(dh.cpu().numpy(), hull), (dist, n)
     assert want_path is None or info["hull_path"] == want_path, info
     print(dist, n, info["hull_path"], len(hull))
 print("pipeline ok")

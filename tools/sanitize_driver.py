@@ -50,7 +50,10 @@ for k, (dist, n, seed, dd) in enumerate(cases):
     info = ctx.last_run()
     idx = ctx.hull_indices(hull)
     assert (idx >= 0).all()
-    print(f"case {k} {dist} {n}: pipeline ok, fused {info['fused']}, h {len(hull)}", flush=True)
+    dh, _ = ctx.heaphull_device(d, n, out="device")  # the hull left on the device
+    assert np.array_equal(dh.cpu().numpy(), hull), (dist, n)
+    print(f"case {k} {dist} {n}: pipeline ok, fused {info['fused']}, hull path "
+          f"{info['hull_path']}, h {len(hull)}", flush=True)
 if not which or "pts2" in which:
     pts = P.generate("square", 100_000, 1)
     pts[77_777, 1] = np.inf
