@@ -355,6 +355,22 @@ def distributions_leg(a, P, ctx, dev, start, stop, peak, check_parity):
                "streaming_gbs": k_bytes / (stream_ms * 1e-3) / 1e9,
                "streaming_frac": k_bytes / (stream_ms * 1e-3) / 1e9 / peak,
                "k2_ms": ksum["k2"][0] / max(1, ksum["k2"][1])}
+        # the same pipeline with the hull left in device memory
+        # (ohx_heaphull_device_out): no PCIe copy of a 96.8M-vertex hull
+        dbuf = torch.empty((dn + 8, 2), dtype=torch.float64, device=dev)  # reused output
+        dh, _ = ctx.heaphull_device(dd, dn, out=dbuf)
+        torch.cuda.synchronize()
+        start.record()
+        for _ in range(5):
+            dh, _ = ctx.heaphull_device(dd, dn, out=dbuf)
+        stop.record()
+        torch.cuda.synchronize()
+        dms_dev = start.elapsed_time(stop) / 5
+        row["hull_on_device"] = {"value": dn / (dms_dev * 1e-3) / 1e9, "unit": UNIT,
+                                 "ms_per_step": dms_dev, "api": "ohx_heaphull_device_out",
+                                 "hull_path": ctx.last_run()["hull_path"],
+                                 "hull_equal": bool(np.array_equal(dh.cpu().numpy(), hull))}
+        del dh, dbuf
         if check_parity:
             from oracle import Reference
             if Reference.available():
@@ -430,6 +446,12 @@ class Runner:
                 self.ctx, self.d, self.n, self.base)
         hull = sharded_heaphull(shard, device=self.xdev, stats=stats)
         stats["job_counts"] = None
+        if self.mode == "sharded":  # the job's queue lengths: a sum over ranks
+            import torch
+            import torch.distributed as dist
+            t = torch.tensor(stats["counts"], dtype=torch.int64, device=self.xdev)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            stats["job_counts"] = [int(v) for v in t.tolist()]
         if self.mode == "single":
             assert np.array_equal(hull, self.step()), "pipeline disagreement"
             stats["job_counts"] = stats["counts"]
@@ -641,6 +663,28 @@ def run_b200_arm(a):
             hull_dev = step_device()
             parity = reference_parity(Reference(), hp, ctx if mode == "single" else None,
                                       hull_dev, stats["ext"], stats["job_counts"])
+    if world > 1 and not a.no_parity:
+        # N > 1: the job's hull, extremes and queue lengths (one multi-GPU
+        # step, collective) against the reference on the WHOLE corpus, which
+        # rank 0 regenerates on its host cores (configs[4]: 4e9 points,
+        # 64 GB, about a minute); the other ranks wait at the barrier
+        hull_dev = step_device()
+        if rank == 0:
+            need = 16 * total * 2.2  # the points + the reference's labels and copies
+            have = os.sysconf("SC_PHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+            from oracle import Reference
+            if not Reference.available():
+                parity = {"skipped": "reference library not built (oracle/_ref)"}
+            elif need > have * 0.6:
+                parity = {"skipped": f"host RAM {have / 2**30:.0f} GiB < the corpus + checker "
+                                     f"({need / 2**30:.0f} GiB at 60 %)"}
+            else:
+                full = P.generate(a.dist, total, a.seed)
+                parity = reference_parity(Reference(), full, None, hull_dev, stats["ext"],
+                                          stats["job_counts"])
+                parity["corpus"] = f"generate({{{a.dist}, {total}, {a.seed}}}) on rank 0"
+                del full
+        barrier()
 
     # ---------------- the other distributions (rank 0, N = 1)
     dists = None

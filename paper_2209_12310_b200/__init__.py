@@ -365,10 +365,18 @@ class Context:
                                                    1 if raw_cycle else 0, _stream(stream)))
         return hull[: h.value].copy(), bool(proven.value)
 
-    def heaphull_device(self, d_xy, n: int, out: str = "host"):
+    def heaphull_device(self, d_xy, n: int, out="host"):
         """Full pipeline on device-resident points -> (hull, timings).
         out="device": the hull stays in device memory (a torch tensor on this
-        context's device) -- ohx_heaphull_device_out."""
+        context's device) -- ohx_heaphull_device_out; out=<(cap, 2) float64
+        CUDA tensor>: written there (a reused buffer), a view returned."""
+        if not isinstance(out, str):  # a caller's device buffer
+            cap = out.numel() // 2
+            h = C.c_uint64(0)
+            t = np.zeros(4, dtype=np.float64)
+            check(lib.ohx_heaphull_device_out(self.h, _ptr(d_xy), n, _ptr(out), cap, C.byref(h),
+                                              t.ctypes.data_as(_dp)))
+            return out.view(-1, 2)[: h.value], dict(filter_ms=t[0], hull_ms=t[1], total_ms=t[2])
         if out == "device":
             import torch
             cap = n + 8 if n <= (1 << 26) else 1 << 24

@@ -116,6 +116,43 @@ def test_device_chains_equal_the_reference_loop(ctx, name):
         assert proven, name  # these decompose: the device path must carry them
 
 
+def fuzz_arc(rng, kind, n):
+    """One sweep-ordered arc of quadrant 1 (x descending), of a given texture."""
+    if kind == "noisy_circle":  # rounding-level to visible noise
+        t = np.sort(rng.uniform(0, np.pi / 2, n))
+        r = 1 + rng.normal(0, 10.0 ** rng.uniform(-16, -6), (n, 1))
+        a = np.stack([np.cos(t), np.sin(t)], 1) * r
+    elif kind == "grid":  # duplicates, collinear runs
+        a = rng.integers(0, int(rng.integers(3, 60)), size=(n, 2)).astype(float)
+    elif kind == "walk":
+        a = np.cumsum(rng.normal(0, 1, (n, 2)), 0)
+    elif kind == "crescent":  # a disk's survivor arc: thin band, many pops
+        t = rng.uniform(0, np.pi / 2, n)
+        r = 1 - rng.uniform(0, 0.02, (n, 1)) ** 2
+        a = np.stack([np.cos(t), np.sin(t)], 1) * r
+    else:  # "mixed": convex runs broken by outliers
+        t = np.sort(rng.uniform(0, np.pi / 2, n))
+        a = np.stack([np.cos(t), np.sin(t)], 1)
+        k = rng.integers(0, n, size=max(1, n // 500))
+        a[k] *= rng.uniform(0.5, 1.5, (len(k), 1))
+    a = a[np.lexsort((a[:, 1], -a[:, 0]))]  # the sweep order (hull.cpp:18-22)
+    return np.ascontiguousarray(a)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_device_chains_fuzz(ctx, seed):
+    # whatever the texture, the device path either proves its chunks and
+    # returns the reference loop's chains, or hands over to the host chains
+    rng = np.random.default_rng(1000 + seed)
+    kinds = ["noisy_circle", "grid", "walk", "crescent", "mixed"]
+    arcs = [fuzz_arc(rng, kinds[(seed + q) % len(kinds)], int(rng.integers(2, 9000)))
+            for q in range(4)]
+    cyc, proven = device_run(ctx, arcs, raw=True)
+    assert np.array_equal(cyc, np.concatenate([seq_chain(x) for x in arcs])), proven
+    hull, _ = device_run(ctx, arcs, raw=False)
+    assert np.array_equal(hull, host_hull(arcs))
+
+
 @pytest.mark.parametrize("n", [2, 3, 1023, 1024, 2047, 2048, 2049, 5000, 70001])
 def test_device_chains_chunk_boundaries(ctx, n):
     rng = np.random.default_rng(n)

@@ -158,3 +158,5 @@ def test_bench_multi_rank_path_on_one_gpu(tmp_path):
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["points_total"] == 24_000_000
     assert line["scaling"] == "strong" and line["config"]["points_per_gpu"] == 12_000_000
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    par = line["parity"]  # the 2-rank job against the reference on the whole corpus
+    assert par["hull_equal"] and par["extremes_equal"] and par["queues_equal"], par

@@ -18,9 +18,10 @@ FP64 = {"DADD", "DMUL", "DFMA", "DSETP", "DMNMX"}
 def short(name):
     for w in WANT:
         if w in name:
-            m = re.search(r"I([jmv])E", name)
-            return w + ("<u32>" if m and m.group(1) == "j" else "<u64>" if m and m.group(1) == "m"
-                        else "")
+            dem = subprocess.run(["c++filt", name], capture_output=True, text=True).stdout.strip()
+            m = re.search(w + r"(<[^(]*>)?", dem)
+            t = (m.group(1) or "") if m else ""
+            return w + t.replace("unsigned int", "u32").replace("unsigned long", "u64")
     return None
 
 
@@ -40,14 +41,14 @@ def main():
             s = short(name)
             if s is None:
                 continue
-            ops = collections.Counter(re.findall(r"/\*[0-9a-f]{4}\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]+)", block))
+            ops = collections.Counter(re.findall(r"/\*[0-9a-f]{4,6}\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]+)", block))
             base = collections.Counter()
             for op, c in ops.items():
                 base[op.split(".")[0]] += c
             loads = {op: c for op, c in ops.items() if op.startswith("LDG")}
             fp64 = {op: base[op] for op in sorted(FP64) if base[op]}
             r = regs.get(name, ("?", "?", "?"))
-            out.append(f"{s:22s} {sum(ops.values()):6d} instr  regs {r[0]}  stack {r[1]}  smem {r[2]}\n"
+            out.append(f"{s:34s} {sum(ops.values()):6d} instr  regs {r[0]}  stack {r[1]}  smem {r[2]}\n"
                        f"    FP64 {fp64}\n    loads {loads}\n"
                        f"    top {base.most_common(8)}")
     print("SASS summary (cuobjdump -sass, sm_100a; static instruction counts)\n")
