@@ -294,6 +294,7 @@ ohx_ctx* create_ctx(int device) {
   check_cuda(cudaMalloc(&c->d_crec, sizeof(ohx_corner_rec)), "cudaMalloc(crec)");
   check_cuda(cudaMalloc(&c->d_counts, 64), "cudaMalloc(counts)");
   check_cuda(cudaMallocHost(&c->h_rec, sizeof(ohx_extremes_rec)), "cudaMallocHost");
+  check_cuda(cudaMallocHost(&c->h_srec, 8 * sizeof(ohx_extremes_rec)), "cudaMallocHost");
   check_cuda(cudaMallocHost(&c->h_crec, sizeof(ohx_corner_rec)), "cudaMallocHost");
   check_cuda(cudaMallocHost(&c->h_counts, 64), "cudaMallocHost");
   check_cuda(cudaMalloc(&c->d_cnt, 64), "cudaMalloc(cnt)");
@@ -315,7 +316,8 @@ void destroy_ctx(ohx_ctx* c) {
                   static_cast<void*>(c->d_sample), c->d_cand, static_cast<void*>(c->d_cnt),
                   c->d_regions, static_cast<void*>(c->d_cpts), c->d_hsort, c->d_hchain, c->d_poly})
     if (p) cudaFree(p);
-  for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_crec),
+  for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_srec),
+                  static_cast<void*>(c->h_crec),
                   static_cast<void*>(c->h_counts), static_cast<void*>(c->h_cnt), c->h_sorted,
                   static_cast<void*>(c->h_spec)})
     if (p) cudaFreeHost(p);
@@ -349,6 +351,7 @@ void trim_ctx(ohx_ctx* c) {
   dfree(c->d_labels, &c->labels_bytes);
   dfree(c->d_gather, &c->gather_bytes);
   c->spec_zeroed = false;
+  c->spec_zero_cap = 0;
   dfree(c->d_sample, &c->sample_bytes);
   dfree(c->d_cand, &c->cand_bytes);
   dfree(c->d_regions, &c->regions_bytes);

@@ -102,6 +102,17 @@ KPlan make_kplan(const ohx_filter_plan& plan, std::uint64_t base, std::uint64_t 
   return kp;
 }
 
+// OHX_K2_ONEPASS=0: K2 over a candidate list as k2_filter + k2_compact +
+// the survivors' coordinate gather (A/B hook), default: one launch writing
+// queues and coordinates
+bool k2_one_pass_mode() {
+  static const bool v = [] {
+    const char* e = std::getenv("OHX_K2_ONEPASS");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
+
 // K2 over the n points of a shard, or (d_cand != null) over the n_cand
 // candidates listed there (shard-local indices, same width as the queues).
 void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t base,
@@ -116,8 +127,12 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
     for (int q = 0; q < 4; ++q) counts[q] = 0;
   } else {
     const std::uint64_t ntiles = (items + kK2Tile - 1) / kK2Tile;
+    // candidate lists: one K2 launch that also writes the survivors'
+    // coordinates; all points: k2_filter + k2_compact + a coordinate gather
+    const bool one_pass = d_cand != nullptr && d_cpts != nullptr &&
+                          ntiles <= kK2OnePassMaxTiles && k2_one_pass_mode();
     dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes,
-             k2_work_bytes(ntiles), "k2 work area");
+             k2_work_bytes(ntiles, one_pass), "k2 work area");
     // queue capacity: 1/16 of the items (at least 1M); grown to the exact
     // counts and re-run on overflow (counts are exact even when stores are
     // dropped)
@@ -125,31 +140,45 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
         std::min<std::uint64_t>(items, std::max<std::uint64_t>(1u << 20, items / 16));
     if (c->queue_bytes / (4ull * idx_bytes) > cap)
       cap = std::min<std::uint64_t>(items, c->queue_bytes / (4ull * idx_bytes));
+    constexpr std::uint64_t kSpec = ohx_ctx::kSpecSurvivors;
+    host_grow(reinterpret_cast<void**>(&c->h_spec), &c->spec_bytes, kSpec * 16,
+              "cudaMallocHost(survivors)");
     for (int attempt = 0; attempt < 2; ++attempt) {
       dev_grow(&c->d_queues, &c->queue_bytes, 4ull * idx_bytes * cap, "queues");
-      check_cuda(cudaEventRecord(c->ev[2][0], s), "cudaEventRecord");
-      launch_k2(d_xy, items, kp, c->d_status, ntiles, c->d_queues, idx_bytes, cap, d_labels,
-                c->d_counts, s, d_cand, d_cpts);  // k2_filter + k2_compact
-      check_cuda(cudaEventRecord(c->ev[2][1], s), "cudaEventRecord");
-      mark_timed(c, 2);
-      c->launches += 2;
       // the first survivors' coordinates ride along with the counts: a
       // small survivor set needs no second round trip (queues_fetch_xy)
-      constexpr std::uint64_t kSpec = ohx_ctx::kSpecSurvivors;
-      grow_gather(c, kSpec * 16);
-      if (!c->spec_zeroed) {  // the fixed-size copy below reads past the survivors
-        // actually gathered: make those bytes defined (compute-sanitizer initcheck)
+      // one pass: the first `per_q` of each quadrant's coordinates (one 2D
+      // copy), else the first kSpec packed [q1|q2|q3|q4] by gather_xy4_dev
+      const std::uint64_t per_q = std::min<std::uint64_t>(kSpec / 4, cap);
+      grow_gather(c, one_pass ? 4 * cap * 16 : kSpec * 16);
+      // the fixed-size copies below read past the survivors actually
+      // written: make those bytes defined once (compute-sanitizer initcheck)
+      if (!one_pass && !c->spec_zeroed) {
         check_cuda(cudaMemsetAsync(c->d_gather, 0, kSpec * 16, s), "cudaMemsetAsync(gather)");
         c->spec_zeroed = true;
       }
-      host_grow(reinterpret_cast<void**>(&c->h_spec), &c->spec_bytes, kSpec * 16,
-                "cudaMallocHost(survivors)");
-      launch_gather4_dev(d_xy, c->d_queues, idx_bytes, cap, c->d_counts, kSpec, c->d_gather, s);
-      ++c->launches;
+      if (one_pass && c->spec_zero_cap != cap) {
+        check_cuda(cudaMemset2DAsync(c->d_gather, cap * 16, 0, per_q * 16, 4, s),
+                   "cudaMemset2DAsync(gather)");
+        c->spec_zero_cap = cap;
+      }
+      check_cuda(cudaEventRecord(c->ev[2][0], s), "cudaEventRecord");
+      launch_k2(d_xy, items, kp, c->d_status, ntiles, c->d_queues, idx_bytes, cap, d_labels,
+                c->d_counts, s, d_cand, d_cpts, one_pass ? c->d_gather : nullptr);
+      check_cuda(cudaEventRecord(c->ev[2][1], s), "cudaEventRecord");
+      mark_timed(c, 2);
       check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
-      check_cuda(cudaMemcpyAsync(c->h_spec, c->d_gather, kSpec * 16, cudaMemcpyDeviceToHost, s),
-                 "cudaMemcpyAsync(survivors)");
+      if (one_pass) {
+        ++c->launches;
+        check_cuda(cudaMemcpy2DAsync(c->h_spec, per_q * 16, c->d_gather, cap * 16, per_q * 16, 4,
+                                     cudaMemcpyDeviceToHost, s), "cudaMemcpy2DAsync(survivors)");
+      } else {  // k2_filter + k2_compact, then the survivors' coordinates
+        c->launches += 3;
+        launch_gather4_dev(d_xy, c->d_queues, idx_bytes, cap, c->d_counts, kSpec, c->d_gather, s);
+        check_cuda(cudaMemcpyAsync(c->h_spec, c->d_gather, kSpec * 16, cudaMemcpyDeviceToHost, s),
+                   "cudaMemcpyAsync(survivors)");
+      }
       check_cuda(cudaStreamSynchronize(s), "k2_filter");
       std::uint64_t mx = 0, total = 0;
       for (int q = 0; q < 4; ++q) {
@@ -158,7 +187,16 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
         total += counts[q];
       }
       if (mx <= cap) {
-        if (total <= kSpec) c->spec_n = total;
+        if (!one_pass) {
+          if (total <= kSpec) c->spec_n = total;
+        } else if (mx <= per_q) {  // every quadrant's survivors came back: pack them
+          std::uint64_t off = 0;
+          for (int q = 0; q < 4; ++q) {
+            std::memmove(c->h_spec + 2 * off, c->h_spec + 2 * q * per_q, counts[q] * 16);
+            off += counts[q];
+          }
+          c->spec_n = total;
+        }
         break;
       }
       if (attempt == 1) throw Error(OHX_E_INTERNAL, "k2_filter: queue overflow after regrow");
@@ -531,7 +569,7 @@ int sub_samples() {  // OHX_SUBSAMPLES overrides (2..8; tuning hook)
   static const int v = [] {
     const char* e = std::getenv("OHX_SUBSAMPLES");
     const int k = e ? std::atoi(e) : 0;
-    return k >= 2 && k <= kMaxSubSamples ? k : kSubSamples;
+    return k >= 1 && k <= kMaxSubSamples ? k : kSubSamples;
   }();
   return v;
 }
@@ -563,9 +601,10 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
   ensure_partials(c, segs);
   launch_k1_sample(d_xy, n, segs, kSampleLen, subs, c->d_partials, c->d_ticket, d_recs, s);
   ++c->launches;
-  ohx_extremes_rec rs[kMaxSubSamples];
-  check_cuda(cudaMemcpyAsync(rs, d_recs, subs * sizeof(ohx_extremes_rec), cudaMemcpyDeviceToHost, s),
-             "cudaMemcpyAsync(sample recs)");
+  static_assert(kMaxSubSamples <= 8, "h_srec holds 8 records");
+  const ohx_extremes_rec* rs = c->h_srec;  // pinned: a direct DMA, no staging copy
+  check_cuda(cudaMemcpyAsync(c->h_srec, d_recs, subs * sizeof(ohx_extremes_rec),
+                             cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(sample recs)");
   check_cuda(cudaStreamSynchronize(s), "sample extremes");
   tr.mark("sample k1");
   const int slot[8] = {OHX_EAST, OHX_NE, OHX_NORTH, OHX_NW,

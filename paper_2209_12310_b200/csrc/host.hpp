@@ -32,6 +32,7 @@ struct ohx_ctx {
   ohx_extremes_rec* d_rec = nullptr;
   ohx_corner_rec* d_crec = nullptr;
   ohx_extremes_rec* h_rec = nullptr;  // pinned
+  ohx_extremes_rec* h_srec = nullptr;  // pinned: the fused pass's sub-sample records
   ohx_corner_rec* h_crec = nullptr;   // pinned
   unsigned long long* d_counts = nullptr;
   unsigned long long* h_counts = nullptr;  // pinned
@@ -53,6 +54,7 @@ struct ohx_ctx {
   // lanes the reference grants a call (parallel.hpp:18-21)
   int host_lanes = 0;
   bool spec_zeroed = false;  // d_gather's speculative survivor slots are cleared
+  std::uint64_t spec_zero_cap = 0;  // ... those of the one-pass K2 for this queue capacity
   void* d_poly = nullptr;    // classify_points' edges of a polygon with > 8 vertices
   std::uint64_t poly_bytes = 0;
   // staging for host-API calls
@@ -143,8 +145,10 @@ bool dev_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* wha
 // the survivor gather buffer (ohx_ctx::d_gather); a new allocation is not
 // yet cleared for the fixed-size speculative survivor copy
 inline void grow_gather(ohx_ctx* c, std::uint64_t bytes) {
-  if (dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, bytes, "gather"))
+  if (dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, bytes, "gather")) {
     c->spec_zeroed = false;
+    c->spec_zero_cap = 0;
+  }
 }
 void host_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what);
 // device -> host copy of a user buffer (pageable: through the pinned ring);

@@ -181,47 +181,55 @@ inline std::uint64_t asc_key(double v) {
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
-// Sweep sort of a mid-sized arc: LSD radix sort (11-bit digits, digits all
-// keys share skipped) on the top 33 bits of the primary key, then runs of
-// equal top bits sorted by the comparator (rare for arcs of < 2^17 points:
-// equal or nearly equal coordinates).  Three linear passes instead of ~n
-// log n mispredicted comparisons (~50 ns per point on the box's host for
-// random arcs).  Equal points may come out in any order, as with std::sort.
+// Sweep sort of a mid-sized arc: LSD radix sort (8-bit digits, one
+// histogram pass for all four, digits all keys share skipped) on the top
+// 32 bits of the primary key, then runs of equal top bits sorted by the
+// comparator (rare for arcs of < 2^17 points: equal or nearly equal
+// coordinates).  A few linear passes over per-thread scratch instead of
+// ~n log n mispredicted comparisons (~50 ns per point on the box's host for
+// random arcs; 11-bit digits with per-call vectors: ~25 ns per point at a
+// few thousand points, the histograms' fixed cost).  Equal points may come
+// out in any order, as with std::sort.
 template <int Q>
 void radix_sweep_sort(std::vector<P2>& pts) {
   struct E {
-    std::uint64_t k;
-    std::uint32_t i;
+    std::uint32_t k, i;
   };
   const std::size_t n = pts.size();
-  std::vector<E> a(n), b(n);
+  thread_local std::vector<E> a, b;
+  thread_local std::vector<P2> out;
+  if (a.size() < n) {
+    a.resize(n);
+    b.resize(n);
+    out.resize(n);
+  }
+  constexpr int kDigits = 4;
+  std::uint32_t cnt[kDigits][257] = {};
   for (std::size_t i = 0; i < n; ++i) {
     const P2& p = pts[i];
-    const std::uint64_t k = Q == 1 ? ~asc_key(p.x) : Q == 2 ? ~asc_key(p.y)
-                          : Q == 3 ? asc_key(p.x) : asc_key(p.y);
+    const std::uint64_t k64 = Q == 1 ? ~asc_key(p.x) : Q == 2 ? ~asc_key(p.y)
+                            : Q == 3 ? asc_key(p.x) : asc_key(p.y);
+    const auto k = static_cast<std::uint32_t>(k64 >> 32);
     a[i] = {k, static_cast<std::uint32_t>(i)};
+    for (int d = 0; d < kDigits; ++d) ++cnt[d][((k >> (8 * d)) & 255u) + 1];
   }
-  constexpr int kBits = 11, kBuckets = 1 << kBits;
-  std::vector<std::uint32_t> cnt(kBuckets + 1);
-  constexpr int kLow = 64 - 3 * kBits;  // bits below are left to the fix-up
-  for (int shift = kLow; shift < 64; shift += kBits) {
-    auto digit = [&](const E& e) { return static_cast<std::uint32_t>((e.k >> shift) & (kBuckets - 1)); };
-    std::fill(cnt.begin(), cnt.end(), 0u);
-    for (const E& e : a) ++cnt[digit(e) + 1];
-    if (cnt[digit(a[0]) + 1] == n) continue;  // every key has this digit
-    for (int d = 0; d < kBuckets; ++d) cnt[d + 1] += cnt[d];
-    for (const E& e : a) b[cnt[digit(e)]++] = e;
-    a.swap(b);
+  E* src = a.data();
+  E* dst = b.data();
+  for (int d = 0; d < kDigits; ++d) {
+    std::uint32_t* c = cnt[d];
+    if (c[((src[0].k >> (8 * d)) & 255u) + 1] == n) continue;  // every key has this digit
+    for (int v = 0; v < 256; ++v) c[v + 1] += c[v];
+    for (std::size_t i = 0; i < n; ++i) dst[c[(src[i].k >> (8 * d)) & 255u]++] = src[i];
+    std::swap(src, dst);
   }
-  std::vector<P2> out(n);
-  for (std::size_t i = 0; i < n; ++i) out[i] = pts[a[i].i];
+  for (std::size_t i = 0; i < n; ++i) out[i] = pts[src[i].i];
   for (std::size_t r = 0; r < n;) {  // equal top bits: the comparator's order
     std::size_t e = r + 1;
-    while (e < n && (a[e].k >> kLow) == (a[r].k >> kLow)) ++e;
+    while (e < n && src[e].k == src[r].k) ++e;
     if (e - r > 1) std::sort(out.begin() + r, out.begin() + e, SweepLess<Q>{});
     r = e;
   }
-  pts.swap(out);
+  std::copy(out.begin(), out.begin() + n, pts.begin());
 }
 
 template <int Q>

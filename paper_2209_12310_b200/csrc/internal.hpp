@@ -56,6 +56,8 @@ void launch_k1b(const double* d_xy, std::uint64_t n, std::uint64_t base,
 // K2 work area: [2 counters | k2_compact look-back words (4 per group of 64
 // tiles) | per-tile queue counts (4 x u32 per tile) | survivor scratch
 // (one 16-bit slot per point)].  Only the first part is cleared per launch.
+// One-pass mode (gather mode): [2 counters | 4 count words per tile], all
+// cleared per launch.
 constexpr std::uint64_t kK2GroupTiles = 64;
 struct K2Work {
   unsigned* tile_counter;
@@ -66,17 +68,21 @@ struct K2Work {
   std::uint64_t clear_bytes;
   std::uint64_t total_bytes;
 };
-inline K2Work k2_work_layout(void* base, std::uint64_t ntiles) {
+inline K2Work k2_work_layout(void* base, std::uint64_t ntiles, bool one_pass = false) {
   const std::uint64_t ngroups = (ntiles + kK2GroupTiles - 1) / kK2GroupTiles;
   auto* b = static_cast<unsigned char*>(base);
-  K2Work w;
+  K2Work w{};
   std::uint64_t off = 0;
   w.tile_counter = reinterpret_cast<unsigned*>(b + off);
   w.group_counter = reinterpret_cast<unsigned*>(b + off + 4);
   off += 256;
   w.status = reinterpret_cast<std::uint64_t*>(b + off);
-  off += 4 * ngroups * 8;
+  off += 4 * (one_pass ? ntiles : ngroups) * 8;
   w.clear_bytes = off;
+  if (one_pass) {
+    w.total_bytes = off;
+    return w;
+  }
   off = (off + 255) & ~std::uint64_t(255);
   w.tile_counts = reinterpret_cast<std::uint32_t*>(b + off);
   off += 4 * ntiles * 4;
@@ -86,17 +92,23 @@ inline K2Work k2_work_layout(void* base, std::uint64_t ntiles) {
   w.total_bytes = off;
   return w;
 }
-inline std::uint64_t k2_work_bytes(std::uint64_t ntiles) {
-  return k2_work_layout(nullptr, ntiles).total_bytes;
+inline std::uint64_t k2_work_bytes(std::uint64_t ntiles, bool one_pass = false) {
+  return k2_work_layout(nullptr, ntiles, one_pass).total_bytes;
 }
 // K2 (k2_filter + k2_compact; re-arms its work area first).  d_queues holds
 // 4 queues of `cap` shard-local indices of idx_bytes each.
 // d_gather (nullable): gather mode over a candidate list of n shard-local
 // indices (same width as the queues); labels are then scattered.
+// d_qxy (gather mode with d_gather_xy, at most kK2OnePassMaxTiles tiles):
+// one launch, and the survivors' coordinates too, d_qxy[q * cap + i] for
+// queue entry i of quadrant q (work area: k2_work_bytes(ntiles, true));
+// null: k2_filter + k2_compact.
+constexpr std::uint64_t kK2OnePassMaxTiles = 2048;
 void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_work,
                std::uint64_t ntiles, void* d_queues, int idx_bytes, std::uint64_t cap,
                std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream,
-               const void* d_gather = nullptr, const double* d_gather_xy = nullptr);
+               const void* d_gather = nullptr, const double* d_gather_xy = nullptr,
+               double* d_qxy = nullptr);
 // The fused pass's provisional region Q (heuristic; certified inside the
 // true octagon after the pass): x0 <= x <= x1, y0 <= y <= y1,
 // t0 <= fl(x+y) <= t1, d0 <= fl(x-y) <= d1.

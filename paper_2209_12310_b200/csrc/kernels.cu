@@ -838,13 +838,85 @@ __device__ __forceinline__ std::uint32_t k2_label_tile(const KPlan& plan, const 
   return labs;
 }
 
+// One-pass mode (gather mode over a candidate list of at most
+// kK2OnePassMaxTiles tiles): each tile publishes its four quadrant counts
+// and sums the counts of ALL the tiles before it (one load per lane per 32
+// tiles, in parallel: a chained look-back advances one L2 round trip per
+// 32 tiles, and with every tile resident at once that chain was the
+// kernel's critical path); then it writes its survivors' indices and
+// coordinates straight into the four queues -- no scratch slice, no
+// k2_compact, no separate coordinate gather.  Tile ids are taken in launch
+// order, so the tiles before a tile are resident or done.
+struct K2OnePass {
+  std::uint64_t* status;  // 4 x ntiles count words (kFlagA | count)
+  void* queues;           // 4 queues of cap entries (the list's index type)
+  double2* qxy;           // 4 x cap survivor coordinates, same positions
+  std::uint64_t cap;
+  unsigned long long* counts;
+};
+
+// One-pass tail (see K2OnePass): the tile's quadrant totals are in
+// S.qbase, the per-(item, warp) exclusive offsets in S.off.
 template <typename GIdx>
+__device__ __forceinline__ void k2_one_pass_tail(const GIdx* __restrict__ gidx,
+                                                 const double2* __restrict__ cpts,
+                                                 std::uint64_t t0, std::uint64_t tile,
+                                                 std::uint64_t ntiles, std::uint32_t labs,
+                                                 K2Shared& S, const K2OnePass& op) {
+  constexpr int W = kK2Warps;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  __shared__ std::uint64_t s_excl[4];
+  if (warp < 4) {
+    const int q = warp;
+    const std::uint64_t agg = S.qbase[q];
+    std::uint64_t* st = op.status + std::uint64_t(q) * ntiles;
+    if (lane == 0) st_relaxed(st + tile, kFlagA | agg);
+    std::uint64_t excl = 0;
+    for (std::uint64_t k = lane; k < tile; k += 32) {
+      std::uint64_t w;
+      do {
+        w = ld_relaxed(st + k);
+      } while ((w >> 62) == 0);
+      excl += w & kValMask;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) excl += __shfl_xor_sync(kFull, excl, off);
+    if (lane == 0) {
+      s_excl[q] = excl;
+      if (tile == ntiles - 1) op.counts[q] = excl + agg;
+    }
+  }
+  __syncthreads();
+  GIdx* queues = static_cast<GIdx*>(op.queues);
+#define LAB(it) ((labs >> (4 * (it))) & 0xFu)
+#pragma unroll
+  for (int it = 0; it < kK2Items; ++it) {
+    const std::uint32_t q = LAB(it) - 1u;
+    const unsigned live = __ballot_sync(kFull, LAB(it) != 0);
+    if (!live) continue;
+    const unsigned b0 = __ballot_sync(kFull, q & 1u);
+    const unsigned b1 = __ballot_sync(kFull, q & 2u);
+    if (LAB(it) == 0) continue;
+    const unsigned mine = live & ((q & 1u) ? b0 : ~b0) & ((q & 2u) ? b1 : ~b1);
+    const std::uint64_t pos = s_excl[q] + S.off[q][it * W + warp] + __popc(mine & lt);
+    if (pos < op.cap) {
+      const std::uint64_t k = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
+      queues[q * op.cap + pos] = gidx[k];
+      op.qxy[q * op.cap + pos] = cpts[k];
+    }
+  }
+#undef LAB
+}
+
+template <typename GIdx, bool kOnePass = false>
 __global__ void __launch_bounds__(kK2Block, 4)
     k2_filter(const double2* __restrict__ pts, const GIdx* __restrict__ gidx,
               const double2* __restrict__ cpts, std::uint64_t n,
               const __grid_constant__ KPlan plan, unsigned* tile_counter,
               std::uint32_t* tile_counts, std::uint64_t ntiles,
-              std::uint16_t* scratch, std::uint8_t* labels) {
+              std::uint16_t* scratch, std::uint8_t* labels, const K2OnePass op) {
+  static_assert(!kOnePass || !std::is_void_v<GIdx>, "one-pass mode is gather mode");
   constexpr int W = kK2Warps;
   extern __shared__ __align__(16) unsigned char k2_smem[];
   K2Shared& S = *reinterpret_cast<K2Shared*>(k2_smem);
@@ -879,7 +951,7 @@ __global__ void __launch_bounds__(kK2Block, 4)
       if (j < n) labels[item_index(gidx, j)] = static_cast<std::uint8_t>(LAB(it));
     }
   }
-  if (!__syncthreads_or(labs != 0)) {
+  if (!__syncthreads_or(labs != 0) && !kOnePass) {
     if (threadIdx.x < 4) tile_counts[threadIdx.x * ntiles + tile] = 0;
     return;
   }
@@ -922,11 +994,15 @@ __global__ void __launch_bounds__(kK2Block, 4)
       run += c[r];
     }
     if (lane == 31) {
-      tile_counts[warp * ntiles + tile] = incl;
+      if (!kOnePass) tile_counts[warp * ntiles + tile] = incl;
       S.qbase[warp] = incl;  // the quadrant total, turned into a base below
     }
   }
   __syncthreads();
+  if constexpr (kOnePass) {
+    k2_one_pass_tail<GIdx>(gidx, cpts, t0, tile, ntiles, labs, S, op);
+    return;
+  }
   const std::uint32_t tot0 = S.qbase[0], tot1 = S.qbase[1], tot2 = S.qbase[2];
   const std::uint32_t tot01 = tot0 + tot1, tot012 = tot01 + tot2;
   std::uint16_t* slice = scratch + t0;
@@ -1318,21 +1394,33 @@ __global__ void __launch_bounds__(kSBlock, 2)
 }
 
 // Number of the sample's points inside the region Q (sample coverage
-// estimate): block b counts run b * step.
+// estimate): runs 0, step, 2 step, ... of the sample, each split over
+// kCountSplit blocks (1024 points per block, 4 loads in flight per thread:
+// one block per run left most SMs idle, 9 us for 8 MB).
+constexpr int kCountSplit = 8;
 __global__ void __launch_bounds__(256)
     count_in_region(const double2* __restrict__ pts, const SampleMap sm, int step,
                     const KFRegion q, unsigned long long* count) {
-  const std::uint64_t start = sm.run_start(std::uint64_t(blockIdx.x) * step);
+  __shared__ unsigned s_c[8];
+  const int part = blockIdx.x % kCountSplit;
+  const std::uint64_t start = sm.run_start(std::uint64_t(blockIdx.x / kCountSplit) * step);
+  const int span = sm.len / kCountSplit;  // a multiple of 1024
   unsigned c = 0;
-  for (int k0 = threadIdx.x; k0 < sm.len; k0 += 256 * 8) {
-    double2 v[8];
+  for (int k0 = part * span + threadIdx.x; k0 < (part + 1) * span; k0 += 256 * 4) {
+    double2 v[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = ld_stream(pts + start + k0 + u * 256);
+    for (int u = 0; u < 4; ++u) v[u] = ld_stream(pts + start + k0 + u * 256);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) c += in_region(q, v[u]);
+    for (int u = 0; u < 4; ++u) c += in_region(q, v[u]);
   }
   c = __reduce_add_sync(kFull, c);
-  if ((threadIdx.x & 31) == 0) atomicAdd(count, static_cast<unsigned long long>(c));
+  if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < 8; ++w) t += s_c[w];
+    atomicAdd(count, static_cast<unsigned long long>(t));
+  }
 }
 
 // The smallest index of a point with a non-finite coordinate (the PTS2
@@ -1566,21 +1654,22 @@ void launch_k1b(const double* d_xy, std::uint64_t n, std::uint64_t base,
   check_cuda(cudaGetLastError(), "k1b_corners launch");
 }
 
-template <typename GIdx>
+template <typename GIdx, bool kOnePass = false>
 static void k2_filter_launch(const double2* pts, const GIdx* gidx, const double2* cpts,
                              std::uint64_t n,
                              const KPlan& plan, const K2Work& w, std::uint64_t ntiles,
-                             std::uint8_t* d_labels, cudaStream_t stream) {
+                             std::uint8_t* d_labels, cudaStream_t stream,
+                             const K2OnePass& op = K2OnePass{}) {
   constexpr int smem = sizeof(K2Shared);
   static bool configured = false;  // opt in to > 48 KB dynamic smem once per instantiation
   if (!configured) {
-    check_cuda(cudaFuncSetAttribute(k2_filter<GIdx>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    smem),
+    check_cuda(cudaFuncSetAttribute(k2_filter<GIdx, kOnePass>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "cudaFuncSetAttribute");
     configured = true;
   }
-  k2_filter<GIdx><<<static_cast<unsigned>(ntiles), kK2Block, smem, stream>>>(
-      pts, gidx, cpts, n, plan, w.tile_counter, w.tile_counts, ntiles, w.scratch, d_labels);
+  k2_filter<GIdx, kOnePass><<<static_cast<unsigned>(ntiles), kK2Block, smem, stream>>>(
+      pts, gidx, cpts, n, plan, w.tile_counter, w.tile_counts, ntiles, w.scratch, d_labels, op);
   check_cuda(cudaGetLastError(), "k2_filter launch");
 }
 
@@ -1594,30 +1683,42 @@ static void k2_compact_launch(const K2Work& w, std::uint64_t ntiles, IdxT* queue
   check_cuda(cudaGetLastError(), "k2_compact launch");
 }
 
+template <typename IdxT>
+static void k2_launch(const double2* pts, std::uint64_t n, const KPlan& plan, void* d_work,
+                      std::uint64_t ntiles, IdxT* q, std::uint64_t cap, std::uint8_t* d_labels,
+                      unsigned long long* d_counts, cudaStream_t stream, const IdxT* g,
+                      const double2* cp, double2* qxy) {
+  const bool one_pass = qxy != nullptr;
+  if (one_pass && (g == nullptr || cp == nullptr || ntiles > kK2OnePassMaxTiles))
+    throw Error(OHX_E_INTERNAL, "k2 one-pass mode: a candidate list of <= kK2OnePassMaxTiles tiles");
+  const K2Work w = k2_work_layout(d_work, ntiles, one_pass);
+  // re-arm the work counters and the look-back words
+  check_cuda(cudaMemsetAsync(d_work, 0, w.clear_bytes, stream), "cudaMemsetAsync(k2 work)");
+  if (one_pass) {
+    const K2OnePass op{w.status, q, qxy, cap, d_counts};
+    k2_filter_launch<IdxT, true>(pts, g, cp, n, plan, w, ntiles, d_labels, stream, op);
+  } else if (g) {
+    k2_filter_launch(pts, g, cp, n, plan, w, ntiles, d_labels, stream);
+    k2_compact_launch<IdxT, true>(w, ntiles, q, cap, d_counts, g, stream);
+  } else {
+    k2_filter_launch<void>(pts, nullptr, nullptr, n, plan, w, ntiles, d_labels, stream);
+    k2_compact_launch<IdxT, false>(w, ntiles, q, cap, d_counts, nullptr, stream);
+  }
+}
+
 void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_work,
                std::uint64_t ntiles, void* d_queues, int idx_bytes, std::uint64_t cap,
                std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream,
-               const void* d_gather, const double* d_gather_xy) {
-  const K2Work w = k2_work_layout(d_work, ntiles);
-  const auto* cp = reinterpret_cast<const double2*>(d_gather_xy);
-  // re-arm the two work counters and the look-back words of k2_compact
-  check_cuda(cudaMemsetAsync(d_work, 0, w.clear_bytes, stream), "cudaMemsetAsync(k2 work)");
+               const void* d_gather, const double* d_gather_xy, double* d_qxy) {
   const auto* pts = reinterpret_cast<const double2*>(d_xy);
-  if (idx_bytes == 4) {
-    const auto* g = static_cast<const std::uint32_t*>(d_gather);
-    if (g) k2_filter_launch(pts, g, cp, n, plan, w, ntiles, d_labels, stream);
-    else k2_filter_launch<void>(pts, nullptr, nullptr, n, plan, w, ntiles, d_labels, stream);
-    auto* q = static_cast<std::uint32_t*>(d_queues);
-    if (g) k2_compact_launch<std::uint32_t, true>(w, ntiles, q, cap, d_counts, g, stream);
-    else k2_compact_launch<std::uint32_t, false>(w, ntiles, q, cap, d_counts, nullptr, stream);
-  } else {
-    const auto* g = static_cast<const std::uint64_t*>(d_gather);
-    if (g) k2_filter_launch(pts, g, cp, n, plan, w, ntiles, d_labels, stream);
-    else k2_filter_launch<void>(pts, nullptr, nullptr, n, plan, w, ntiles, d_labels, stream);
-    auto* q = static_cast<std::uint64_t*>(d_queues);
-    if (g) k2_compact_launch<std::uint64_t, true>(w, ntiles, q, cap, d_counts, g, stream);
-    else k2_compact_launch<std::uint64_t, false>(w, ntiles, q, cap, d_counts, nullptr, stream);
-  }
+  const auto* cp = reinterpret_cast<const double2*>(d_gather_xy);
+  auto* qxy = reinterpret_cast<double2*>(d_qxy);
+  if (idx_bytes == 4)
+    k2_launch(pts, n, plan, d_work, ntiles, static_cast<std::uint32_t*>(d_queues), cap, d_labels,
+              d_counts, stream, static_cast<const std::uint32_t*>(d_gather), cp, qxy);
+  else
+    k2_launch(pts, n, plan, d_work, ntiles, static_cast<std::uint64_t*>(d_queues), cap, d_labels,
+              d_counts, stream, static_cast<const std::uint64_t*>(d_gather), cp, qxy);
 }
 
 int kf_grid(int device) {
@@ -1704,7 +1805,8 @@ void launch_k1_list(const double* d_xy, std::uint64_t n, const unsigned long lon
 void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int len, int step,
                             const KFRegion& q, unsigned long long* d_count, cudaStream_t stream) {
   check_cuda(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), stream), "cudaMemsetAsync");
-  count_in_region<<<(segs + step - 1) / step, 256, 0, stream>>>(
+  if (len % (kCountSplit * 1024) != 0) throw Error(OHX_E_INTERNAL, "count_in_region: run length");
+  count_in_region<<<(segs + step - 1) / step * kCountSplit, 256, 0, stream>>>(
       reinterpret_cast<const double2*>(d_xy), SampleMap{n, segs, len, 1}, step, q, d_count);
   check_cuda(cudaGetLastError(), "count_in_region launch");
 }

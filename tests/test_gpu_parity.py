@@ -338,10 +338,13 @@ def test_tma_streaming_variant_matches_oracle(fuse):
     assert r.returncode == 0 and "tma ok" in r.stdout, r.stderr[-3000:]
 
 
-def test_forced_fusion_heavy_candidates_match_oracle():
+@pytest.mark.parametrize("one_pass", ["1", "0"])
+def test_forced_fusion_heavy_candidates_match_oracle(one_pass):
     # OHX_FUSE=force fuses even when the provisional region covers the data
     # poorly (disk: ~25 % candidates, most warp tiles spill past their
-    # 15-offset slot); the result must still be exact
+    # 15-offset slot); the result must still be exact -- with K2 over the
+    # candidates in one launch (look-back in k2_filter) and as k2_filter +
+    # k2_compact (OHX_K2_ONEPASS=0)
     import subprocess
     import sys
     code = (
@@ -361,7 +364,7 @@ def test_forced_fusion_heavy_candidates_match_oracle():
         "        idx, _ = ctx.queue(q + 1, info['counts'][q])\n"
         "        assert np.array_equal(idx, np.flatnonzero(want_labels == q + 1)), (dist, q)\n"
         "print('force ok')\n")
-    env = dict(os.environ, OHX_FUSE="force", PYTHONPATH=ROOT)
+    env = dict(os.environ, OHX_FUSE="force", OHX_K2_ONEPASS=one_pass, PYTHONPATH=ROOT)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=600)
     assert r.returncode == 0 and "force ok" in r.stdout, r.stderr[-3000:]
