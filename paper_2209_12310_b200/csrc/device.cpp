@@ -123,6 +123,7 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
   const std::uint64_t items = d_cand ? n_cand : n;
   const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
   c->spec_n = ~0ull;
+  c->qxy_valid = false;
   if (items == 0) {  // no candidates at all
     for (int q = 0; q < 4; ++q) counts[q] = 0;
   } else {
@@ -203,6 +204,7 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
       cap = std::min<std::uint64_t>(items, mx + mx / 8 + 1024);
     }
     c->last_cap = cap;
+    c->qxy_valid = one_pass;
   }
   fold_stage_times(c, false);  // every stage of this call has completed (K2 synced)
   c->last_xy = d_xy;
@@ -251,8 +253,12 @@ void queue_fetch(ohx_ctx* c, int q, std::uint64_t* h_idx, double* h_xy,
   if (cnt == 0) return;
   const auto* qbase = static_cast<const char*>(c->d_queues) +
                       std::uint64_t(q - 1) * c->last_cap * c->last_idx_bytes;
-  if (h_xy) {
+  if (h_xy && c->qxy_valid) {  // the one-pass K2 wrote them already
+    check_cuda(cudaMemcpyAsync(h_xy, c->d_gather + 2 * std::uint64_t(q - 1) * c->last_cap,
+                               cnt * 16, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(queue xy)");
+  } else if (h_xy) {
     grow_gather(c, cnt * 16);
+    c->qxy_valid = false;
     launch_gather(c->last_xy, qbase, c->last_idx_bytes, cnt, c->d_gather, s);
     ++c->launches;
     check_cuda(cudaMemcpyAsync(h_xy, c->d_gather, cnt * 16, cudaMemcpyDeviceToHost, s),
@@ -283,6 +289,18 @@ void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s) {
   if (total == 0) return;
   if (c->spec_n == total) {  // already fetched with the counts
     std::memcpy(h_xy, c->h_spec, total * 16);
+    return;
+  }
+  if (c->qxy_valid) {  // the one-pass K2 wrote them per quadrant: plain copies
+    std::uint64_t off = 0;
+    for (int q = 0; q < 4; ++q) {
+      if (c->last_counts[q])
+        check_cuda(cudaMemcpyAsync(h_xy + 2 * off, c->d_gather + 2 * std::uint64_t(q) * c->last_cap,
+                                   c->last_counts[q] * 16, cudaMemcpyDeviceToHost, s),
+                   "cudaMemcpyAsync(queues xy)");
+      off += c->last_counts[q];
+    }
+    check_cuda(cudaStreamSynchronize(s), "queues fetch");
     return;
   }
   grow_gather(c, total * 16);
@@ -473,6 +491,7 @@ std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
                          {f.ext.x[OHX_SOUTH], f.ext.y[OHX_SOUTH]}};
   if (total >= device_sort_min()) {
     grow_gather(c, total * 16);
+    c->qxy_valid = false;
     launch_gather4(c->last_xy, c->d_queues, c->last_idx_bytes, c->last_cap, c->last_counts,
                    c->d_gather, s);
     ++c->launches;
@@ -565,7 +584,7 @@ int sample_max_segs() {
 // uncertified once -- fewer octagons to intersect, a larger but riskier Q).
 constexpr int kMaxSubSamples = 8;
 constexpr int kSubSamples = 4;
-int sub_samples() {  // OHX_SUBSAMPLES overrides (2..8; tuning hook)
+int sub_samples() {  // OHX_SUBSAMPLES overrides (1..8; tuning hook)
   static const int v = [] {
     const char* e = std::getenv("OHX_SUBSAMPLES");
     const int k = e ? std::atoi(e) : 0;
@@ -708,7 +727,9 @@ bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
     dev_grow(reinterpret_cast<void**>(&c->d_cpts), &c->cpts_bytes, cap * 16, "candidate points");
     launch_kf_gather(d_xy, c->d_regions, idx_bytes, cap_w, d_wcounts, nw, c->d_cnt, c->d_counts,
                      c->d_cand, c->d_cpts, cap, s);
-    const int k1g = k1_list_grid(cap);
+    // grid sized for ~16 candidates per thread from the last call's count
+    // (a hint only: the kernel covers the device-side count whatever the grid)
+    const int k1g = k1_list_grid(c->cand_hint ? std::min<std::uint64_t>(cap, 2 * c->cand_hint) : cap);
     ensure_partials(c, k1g);
     launch_k1_list(c->d_cpts, cap, c->d_counts, c->d_cand, idx_bytes, base, c->d_partials, k1g,
                    c->d_ticket, c->d_rec, s);
@@ -738,6 +759,7 @@ bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
   *rec = *c->h_rec;
   rec->n = n;
   c->fz = {true, q, d_xy, n, base, n_cand};
+  c->cand_hint = n_cand;
   return true;
 }
 

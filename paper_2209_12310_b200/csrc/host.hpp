@@ -55,6 +55,9 @@ struct ohx_ctx {
   int host_lanes = 0;
   bool spec_zeroed = false;  // d_gather's speculative survivor slots are cleared
   std::uint64_t spec_zero_cap = 0;  // ... those of the one-pass K2 for this queue capacity
+  // d_gather holds the last filter's survivor coordinates per quadrant
+  // (one-pass K2: entry i of quadrant q at q * last_cap + i)
+  bool qxy_valid = false;
   void* d_poly = nullptr;    // classify_points' edges of a polygon with > 8 vertices
   std::uint64_t poly_bytes = 0;
   // staging for host-API calls
@@ -99,6 +102,7 @@ struct ohx_ctx {
     const double* d_xy = nullptr;
     std::uint64_t n = 0, base = 0, n_cand = 0;
   } fz;
+  std::uint64_t cand_hint = 0;  // candidates of the last fused pass (sizes the next K1 grid)
 
   // pinned staging ring for host copies of pageable user buffers
   static constexpr int kStageBufs = 4;
@@ -148,6 +152,7 @@ inline void grow_gather(ohx_ctx* c, std::uint64_t bytes) {
   if (dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, bytes, "gather")) {
     c->spec_zeroed = false;
     c->spec_zero_cap = 0;
+    c->qxy_valid = false;
   }
 }
 void host_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what);

@@ -1,0 +1,12 @@
+# bucket sweep sort for the hull stage: circle 1e8 stage split (bucket vs
+# radix), launch list, and the hull GPU tests
+set -x
+O=gpurun_out/r02t
+mkdir -p $O
+for v in bucket radix; do
+OHX_HULL_SORT=$v OHX_TRACE=1 timeout 600 python tools/hull_output_probe.py --dist circle --n 1e8 --reps 2 > $O/probe_circle_$v.log 2>&1
+done
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv --log-file $O/launches_circle.csv python tools/kernel_driver.py --dist circle --n 1e8 --reps 1 --pipeline > $O/ncu_circle.log 2>&1
+python tools/launch_summary.py $O/launches_circle.csv > $O/launches_circle.txt 2>&1
+timeout 1800 python -m pytest tests/test_gpu_hullchain.py -q -x > $O/pytest.log 2>&1
+echo "pytest rc=$?" >> $O/pytest.log
