@@ -226,11 +226,13 @@ class Context:
         self.h = h
         self.device = device
         self._owned = not default
+        self._hbuf = None  # heaphull_device's host output scratch (small hulls are copied out)
 
     def trim(self):
         """Release this context's grow-only workspaces (and the host block
         cache); later calls regrow them."""
         check(lib.ohx_ctx_trim(self.h))
+        self._hbuf = None
 
     def close(self):
         if self._owned and self.h:
@@ -369,7 +371,20 @@ class Context:
         """Full pipeline on device-resident points -> (hull, timings).
         out="device": the hull stays in device memory (a torch tensor on this
         context's device) -- ohx_heaphull_device_out; out=<(cap, 2) float64
-        CUDA tensor>: written there (a reused buffer), a view returned."""
+        CUDA tensor>: written there (a reused buffer), a view returned;
+        out=<(cap, 2) float64 C-contiguous host array or CPU tensor>: the
+        hull copied there (a reused -- e.g. pinned -- host buffer: pinned
+        memory takes one direct DMA), a view returned."""
+        if isinstance(out, np.ndarray) or (not isinstance(out, str) and not out.is_cuda):
+            host = out if isinstance(out, np.ndarray) else out.numpy()
+            if host.dtype != np.float64 or not host.flags.c_contiguous or host.size % 2:
+                raise ValueError("out: a C-contiguous float64 (cap, 2) host buffer")
+            h = C.c_uint64(0)
+            t = np.zeros(4, dtype=np.float64)
+            check(lib.ohx_heaphull_device(self.h, _ptr(d_xy), n, host.ctypes.data_as(_dp),
+                                          host.size // 2, C.byref(h), t.ctypes.data_as(_dp)))
+            return host.reshape(-1, 2)[: h.value], dict(filter_ms=t[0], hull_ms=t[1],
+                                                       total_ms=t[2])
         if not isinstance(out, str):  # a caller's device buffer
             cap = out.numel() // 2
             h = C.c_uint64(0)
@@ -394,19 +409,28 @@ class Context:
         if out != "host":
             raise ValueError("out must be 'host' or 'device'")
         # the output buffer is virtual until written: full size up to 2^28
-        # points, else start at 2^24 and grow if the hull outgrows it
+        # points, else start at 2^24 and grow if the hull outgrows it.  It is
+        # kept for the next call while hulls come back as copies (< 2^20
+        # vertices); a larger hull is returned in it (the buffer goes with it)
         cap = n + 8 if n <= (1 << 28) else 1 << 24
         while True:
-            hull = np.empty((cap, 2), dtype=np.float64)
+            hull = self._hbuf if self._hbuf is not None and len(self._hbuf) >= cap else None
+            if hull is None:
+                hull = np.empty((cap, 2), dtype=np.float64)
+            self._hbuf = None
             h = C.c_uint64(0)
             t = np.zeros(4, dtype=np.float64)
             rc = lib.ohx_heaphull_device(self.h, _ptr(d_xy), n, hull.ctypes.data_as(_dp),
                                          len(hull), C.byref(h), t.ctypes.data_as(_dp))
-            if rc == OHX_E_INVALID and h.value > cap:  # the hull outgrew the buffer
+            if rc == OHX_E_INVALID and h.value > len(hull):  # the hull outgrew the buffer
                 cap = h.value
                 continue
             check(rc)
-            out = hull[: h.value].copy() if h.value < (1 << 20) else hull[: h.value]
+            if h.value < (1 << 20):
+                self._hbuf = hull
+                out = hull[: h.value].copy()
+            else:
+                out = hull[: h.value]
             return out, dict(filter_ms=t[0], hull_ms=t[1], total_ms=t[2])
 
 

@@ -290,13 +290,16 @@ ohx_ctx* create_ctx(int device) {
   check_cuda(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
   check_cuda(cudaMalloc(&c->d_ticket, 256), "cudaMalloc(ticket)");
   check_cuda(cudaMemset(c->d_ticket, 0, 256), "cudaMemset(ticket)");
-  check_cuda(cudaMalloc(&c->d_rec, sizeof(ohx_extremes_rec)), "cudaMalloc(rec)");
+  // the extremes record and the four counts side by side (one copy brings
+  // both back after the fused pass's candidate stage)
+  check_cuda(cudaMalloc(&c->d_rec, kRecBlock), "cudaMalloc(rec)");
+  check_cuda(cudaMemset(c->d_rec, 0, kRecBlock), "cudaMemset(rec)");  // the gap is copied too
   check_cuda(cudaMalloc(&c->d_crec, sizeof(ohx_corner_rec)), "cudaMalloc(crec)");
-  check_cuda(cudaMalloc(&c->d_counts, 64), "cudaMalloc(counts)");
-  check_cuda(cudaMallocHost(&c->h_rec, sizeof(ohx_extremes_rec)), "cudaMallocHost");
+  c->d_counts = rec_counts(c->d_rec);
+  check_cuda(cudaMallocHost(&c->h_rec, kRecBlock), "cudaMallocHost");
   check_cuda(cudaMallocHost(&c->h_srec, 8 * sizeof(ohx_extremes_rec)), "cudaMallocHost");
   check_cuda(cudaMallocHost(&c->h_crec, sizeof(ohx_corner_rec)), "cudaMallocHost");
-  check_cuda(cudaMallocHost(&c->h_counts, 64), "cudaMallocHost");
+  c->h_counts = rec_counts(c->h_rec);
   check_cuda(cudaMalloc(&c->d_cnt, 64), "cudaMalloc(cnt)");
   check_cuda(cudaMallocHost(&c->h_cnt, 64), "cudaMallocHost");
   for (auto& pair : c->ev)
@@ -310,15 +313,16 @@ void destroy_ctx(ohx_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (void* p : {static_cast<void*>(c->d_partials), static_cast<void*>(c->d_ticket),
                   static_cast<void*>(c->d_rec), static_cast<void*>(c->d_crec),
-                  static_cast<void*>(c->d_counts), static_cast<void*>(c->d_status),
+                  static_cast<void*>(c->d_status),
                   c->d_queues, static_cast<void*>(c->d_pts),
                   static_cast<void*>(c->d_labels), static_cast<void*>(c->d_gather),
                   static_cast<void*>(c->d_sample), c->d_cand, static_cast<void*>(c->d_cnt),
-                  c->d_regions, static_cast<void*>(c->d_cpts), c->d_hsort, c->d_hchain, c->d_poly})
+                  c->d_regions, static_cast<void*>(c->d_cpts), c->d_hsort, c->d_hchain, c->d_poly,
+                  c->d_k2op, static_cast<void*>(c->d_spec)})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_srec),
                   static_cast<void*>(c->h_crec),
-                  static_cast<void*>(c->h_counts), static_cast<void*>(c->h_cnt), c->h_sorted,
+                  static_cast<void*>(c->h_cnt), c->h_sorted,
                   static_cast<void*>(c->h_spec)})
     if (p) cudaFreeHost(p);
   for (int b = 0; b < ohx_ctx::kStageBufs; ++b) {
@@ -350,8 +354,10 @@ void trim_ctx(ohx_ctx* c) {
   dfree(c->d_pts, &c->pts_bytes);
   dfree(c->d_labels, &c->labels_bytes);
   dfree(c->d_gather, &c->gather_bytes);
+  dfree(c->d_k2op, &c->k2op_bytes);
+  dfree(c->d_spec, &c->dspec_bytes);
   c->spec_zeroed = false;
-  c->spec_zero_cap = 0;
+  c->qxy_valid = false;
   dfree(c->d_sample, &c->sample_bytes);
   dfree(c->d_cand, &c->cand_bytes);
   dfree(c->d_regions, &c->regions_bytes);

@@ -132,8 +132,9 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
     // coordinates; all points: k2_filter + k2_compact + a coordinate gather
     const bool one_pass = d_cand != nullptr && d_cpts != nullptr &&
                           ntiles <= kK2OnePassMaxTiles && k2_one_pass_mode();
-    dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes,
-             k2_work_bytes(ntiles, one_pass), "k2 work area");
+    if (!one_pass)
+      dev_grow(reinterpret_cast<void**>(&c->d_status), &c->status_bytes, k2_work_bytes(ntiles),
+               "k2 work area");
     // queue capacity: 1/16 of the items (at least 1M); grown to the exact
     // counts and re-run on overflow (counts are exact even when stores are
     // dropped)
@@ -142,58 +143,65 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
     if (c->queue_bytes / (4ull * idx_bytes) > cap)
       cap = std::min<std::uint64_t>(items, c->queue_bytes / (4ull * idx_bytes));
     constexpr std::uint64_t kSpec = ohx_ctx::kSpecSurvivors;
-    host_grow(reinterpret_cast<void**>(&c->h_spec), &c->spec_bytes, kSpec * 16,
-              "cudaMallocHost(survivors)");
+    constexpr std::uint32_t kSpecQ = kSpec / 4;
+    host_grow(reinterpret_cast<void**>(&c->h_spec), &c->spec_bytes,
+              k2_one_pass_spec_bytes(kSpecQ), "cudaMallocHost(survivors)");
+    if (one_pass) {
+      // work words: zeroed once here, then left zeroed by the kernel;
+      // the returned block: defined once (its copy reads unused slots)
+      if (dev_grow(&c->d_k2op, &c->k2op_bytes, k2_one_pass_work_bytes(), "k2 one-pass work"))
+        check_cuda(cudaMemsetAsync(c->d_k2op, 0, c->k2op_bytes, s), "cudaMemsetAsync(k2 work)");
+      if (dev_grow(reinterpret_cast<void**>(&c->d_spec), &c->dspec_bytes,
+                   k2_one_pass_spec_bytes(kSpecQ), "k2 survivor block"))
+        check_cuda(cudaMemsetAsync(c->d_spec, 0, c->dspec_bytes, s), "cudaMemsetAsync(spec)");
+    }
     for (int attempt = 0; attempt < 2; ++attempt) {
       dev_grow(&c->d_queues, &c->queue_bytes, 4ull * idx_bytes * cap, "queues");
       // the first survivors' coordinates ride along with the counts: a
       // small survivor set needs no second round trip (queues_fetch_xy)
-      // one pass: the first `per_q` of each quadrant's coordinates (one 2D
-      // copy), else the first kSpec packed [q1|q2|q3|q4] by gather_xy4_dev
-      const std::uint64_t per_q = std::min<std::uint64_t>(kSpec / 4, cap);
+      // one pass: the first spec_q of each quadrant + the counts in one
+      // copy; else the first kSpec packed [q1|q2|q3|q4] by gather_xy4_dev
+      const auto spec_q = static_cast<std::uint32_t>(std::min<std::uint64_t>(kSpecQ, cap));
       grow_gather(c, one_pass ? 4 * cap * 16 : kSpec * 16);
-      // the fixed-size copies below read past the survivors actually
-      // written: make those bytes defined once (compute-sanitizer initcheck)
-      if (!one_pass && !c->spec_zeroed) {
+      if (!one_pass && !c->spec_zeroed) {  // the fixed-size copy below reads past the
+        // survivors actually gathered: make those bytes defined (initcheck)
         check_cuda(cudaMemsetAsync(c->d_gather, 0, kSpec * 16, s), "cudaMemsetAsync(gather)");
         c->spec_zeroed = true;
       }
-      if (one_pass && c->spec_zero_cap != cap) {
-        check_cuda(cudaMemset2DAsync(c->d_gather, cap * 16, 0, per_q * 16, 4, s),
-                   "cudaMemset2DAsync(gather)");
-        c->spec_zero_cap = cap;
-      }
       check_cuda(cudaEventRecord(c->ev[2][0], s), "cudaEventRecord");
+      const K2OnePassBufs ob{c->d_k2op, c->d_gather, c->d_spec, spec_q};
       launch_k2(d_xy, items, kp, c->d_status, ntiles, c->d_queues, idx_bytes, cap, d_labels,
-                c->d_counts, s, d_cand, d_cpts, one_pass ? c->d_gather : nullptr);
+                c->d_counts, s, d_cand, d_cpts, one_pass ? &ob : nullptr);
       check_cuda(cudaEventRecord(c->ev[2][1], s), "cudaEventRecord");
       mark_timed(c, 2);
-      check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
+      const unsigned long long* hc = c->h_counts;
       if (one_pass) {
         ++c->launches;
-        check_cuda(cudaMemcpy2DAsync(c->h_spec, per_q * 16, c->d_gather, cap * 16, per_q * 16, 4,
-                                     cudaMemcpyDeviceToHost, s), "cudaMemcpy2DAsync(survivors)");
+        check_cuda(cudaMemcpyAsync(c->h_spec, c->d_spec, k2_one_pass_spec_bytes(spec_q),
+                                   cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(survivors)");
+        hc = reinterpret_cast<const unsigned long long*>(c->h_spec + 8ull * spec_q);
       } else {  // k2_filter + k2_compact, then the survivors' coordinates
         c->launches += 3;
         launch_gather4_dev(d_xy, c->d_queues, idx_bytes, cap, c->d_counts, kSpec, c->d_gather, s);
+        check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
         check_cuda(cudaMemcpyAsync(c->h_spec, c->d_gather, kSpec * 16, cudaMemcpyDeviceToHost, s),
                    "cudaMemcpyAsync(survivors)");
       }
       check_cuda(cudaStreamSynchronize(s), "k2_filter");
       std::uint64_t mx = 0, total = 0;
       for (int q = 0; q < 4; ++q) {
-        counts[q] = c->h_counts[q];
+        counts[q] = hc[q];
         mx = std::max<std::uint64_t>(mx, counts[q]);
         total += counts[q];
       }
       if (mx <= cap) {
         if (!one_pass) {
           if (total <= kSpec) c->spec_n = total;
-        } else if (mx <= per_q) {  // every quadrant's survivors came back: pack them
+        } else if (mx <= spec_q) {  // every quadrant's survivors came back: pack them
           std::uint64_t off = 0;
           for (int q = 0; q < 4; ++q) {
-            std::memmove(c->h_spec + 2 * off, c->h_spec + 2 * q * per_q, counts[q] * 16);
+            std::memmove(c->h_spec + 2 * off, c->h_spec + 2 * q * spec_q, counts[q] * 16);
             off += counts[q];
           }
           c->spec_n = total;
@@ -734,10 +742,9 @@ bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
     launch_k1_list(c->d_cpts, cap, c->d_counts, c->d_cand, idx_bytes, base, c->d_partials, k1g,
                    c->d_ticket, c->d_rec, s);
     c->launches += 2;
-    check_cuda(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(counts)");
-    check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(ohx_extremes_rec),
-                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec)");
+    // the record and the counts after it: one copy
+    check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, kRecCountsOff + 4 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec + counts)");
     check_cuda(cudaStreamSynchronize(s), "kf + candidate extremes");
   };
   candidates(cap_c);

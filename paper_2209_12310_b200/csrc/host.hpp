@@ -19,6 +19,13 @@
 #include "pipeline.hpp"
 
 // ====================================================================== ctx
+// d_rec / h_rec blocks: the extremes record, then 8 count words
+constexpr std::size_t kRecCountsOff = (sizeof(ohx_extremes_rec) + 63) / 64 * 64;
+constexpr std::size_t kRecBlock = kRecCountsOff + 64;
+inline unsigned long long* rec_counts(ohx_extremes_rec* r) {
+  return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(r) + kRecCountsOff);
+}
+
 struct ohx_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -34,8 +41,8 @@ struct ohx_ctx {
   ohx_extremes_rec* h_rec = nullptr;  // pinned
   ohx_extremes_rec* h_srec = nullptr;  // pinned: the fused pass's sub-sample records
   ohx_corner_rec* h_crec = nullptr;   // pinned
-  unsigned long long* d_counts = nullptr;
-  unsigned long long* h_counts = nullptr;  // pinned
+  unsigned long long* d_counts = nullptr;  // 8 words right after d_rec (kRecBlock)
+  unsigned long long* h_counts = nullptr;  // pinned, right after h_rec
 
   // K2 scratch and queues
   std::uint64_t* d_status = nullptr;
@@ -54,10 +61,15 @@ struct ohx_ctx {
   // lanes the reference grants a call (parallel.hpp:18-21)
   int host_lanes = 0;
   bool spec_zeroed = false;  // d_gather's speculative survivor slots are cleared
-  std::uint64_t spec_zero_cap = 0;  // ... those of the one-pass K2 for this queue capacity
   // d_gather holds the last filter's survivor coordinates per quadrant
   // (one-pass K2: entry i of quadrant q at q * last_cap + i)
   bool qxy_valid = false;
+  // one-pass K2: its self-clearing work words and the small block it
+  // returns (the first survivors' coordinates + the counts)
+  void* d_k2op = nullptr;
+  std::uint64_t k2op_bytes = 0;
+  double* d_spec = nullptr;
+  std::uint64_t dspec_bytes = 0;
   void* d_poly = nullptr;    // classify_points' edges of a polygon with > 8 vertices
   std::uint64_t poly_bytes = 0;
   // staging for host-API calls
@@ -151,8 +163,7 @@ bool dev_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* wha
 inline void grow_gather(ohx_ctx* c, std::uint64_t bytes) {
   if (dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, bytes, "gather")) {
     c->spec_zeroed = false;
-    c->spec_zero_cap = 0;
-    c->qxy_valid = false;
+      c->qxy_valid = false;
   }
 }
 void host_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what);

@@ -56,8 +56,6 @@ void launch_k1b(const double* d_xy, std::uint64_t n, std::uint64_t base,
 // K2 work area: [2 counters | k2_compact look-back words (4 per group of 64
 // tiles) | per-tile queue counts (4 x u32 per tile) | survivor scratch
 // (one 16-bit slot per point)].  Only the first part is cleared per launch.
-// One-pass mode (gather mode): [2 counters | 4 count words per tile], all
-// cleared per launch.
 constexpr std::uint64_t kK2GroupTiles = 64;
 struct K2Work {
   unsigned* tile_counter;
@@ -68,7 +66,7 @@ struct K2Work {
   std::uint64_t clear_bytes;
   std::uint64_t total_bytes;
 };
-inline K2Work k2_work_layout(void* base, std::uint64_t ntiles, bool one_pass = false) {
+inline K2Work k2_work_layout(void* base, std::uint64_t ntiles) {
   const std::uint64_t ngroups = (ntiles + kK2GroupTiles - 1) / kK2GroupTiles;
   auto* b = static_cast<unsigned char*>(base);
   K2Work w{};
@@ -77,12 +75,8 @@ inline K2Work k2_work_layout(void* base, std::uint64_t ntiles, bool one_pass = f
   w.group_counter = reinterpret_cast<unsigned*>(b + off + 4);
   off += 256;
   w.status = reinterpret_cast<std::uint64_t*>(b + off);
-  off += 4 * (one_pass ? ntiles : ngroups) * 8;
+  off += 4 * ngroups * 8;
   w.clear_bytes = off;
-  if (one_pass) {
-    w.total_bytes = off;
-    return w;
-  }
   off = (off + 255) & ~std::uint64_t(255);
   w.tile_counts = reinterpret_cast<std::uint32_t*>(b + off);
   off += 4 * ntiles * 4;
@@ -92,23 +86,34 @@ inline K2Work k2_work_layout(void* base, std::uint64_t ntiles, bool one_pass = f
   w.total_bytes = off;
   return w;
 }
-inline std::uint64_t k2_work_bytes(std::uint64_t ntiles, bool one_pass = false) {
-  return k2_work_layout(nullptr, ntiles, one_pass).total_bytes;
+inline std::uint64_t k2_work_bytes(std::uint64_t ntiles) {
+  return k2_work_layout(nullptr, ntiles).total_bytes;
 }
 // K2 (k2_filter + k2_compact; re-arms its work area first).  d_queues holds
 // 4 queues of `cap` shard-local indices of idx_bytes each.
 // d_gather (nullable): gather mode over a candidate list of n shard-local
 // indices (same width as the queues); labels are then scattered.
-// d_qxy (gather mode with d_gather_xy, at most kK2OnePassMaxTiles tiles):
-// one launch, and the survivors' coordinates too, d_qxy[q * cap + i] for
-// queue entry i of quadrant q (work area: k2_work_bytes(ntiles, true));
-// null: k2_filter + k2_compact.
+// op (gather mode with d_gather_xy, at most kK2OnePassMaxTiles tiles): one
+// launch that writes the queues, the survivors' coordinates (qxy[q * cap +
+// i] for queue entry i of quadrant q) and, for the first spec_q of each
+// quadrant, spec[q * spec_q + i], then the four counts after them
+// (k2_one_pass_spec_bytes); d_counts is not written.  op->work
+// (k2_one_pass_work_bytes) must be zero the first time -- the kernel leaves
+// it zeroed.  Null: k2_filter + k2_compact.
 constexpr std::uint64_t kK2OnePassMaxTiles = 2048;
+struct K2OnePassBufs {
+  void* work;
+  double* qxy;
+  double* spec;
+  std::uint32_t spec_q;
+};
+inline std::uint64_t k2_one_pass_work_bytes() { return 256 + 4 * kK2OnePassMaxTiles * 8; }
+inline std::uint64_t k2_one_pass_spec_bytes(std::uint32_t spec_q) { return 4ull * spec_q * 16 + 64; }
 void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_work,
                std::uint64_t ntiles, void* d_queues, int idx_bytes, std::uint64_t cap,
                std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream,
                const void* d_gather = nullptr, const double* d_gather_xy = nullptr,
-               double* d_qxy = nullptr);
+               const K2OnePassBufs* op = nullptr);
 // The fused pass's provisional region Q (heuristic; certified inside the
 // true octagon after the pass): x0 <= x <= x1, y0 <= y <= y1,
 // t0 <= fl(x+y) <= t1, d0 <= fl(x-y) <= d1.

@@ -847,13 +847,23 @@ __device__ __forceinline__ std::uint32_t k2_label_tile(const KPlan& plan, const 
 // coordinates straight into the four queues -- no scratch slice, no
 // k2_compact, no separate coordinate gather.  Tile ids are taken in launch
 // order, so the tiles before a tile are resident or done.
+// The work words are left zeroed by the kernel itself (the last tile to
+// finish clears them and re-arms the counters): no memset per launch.
+// The first spec_q survivors of each quadrant also go to `spec` ([q][spec_q]
+// coordinates, then the four counts): one small copy brings the host both.
 struct K2OnePass {
   std::uint64_t* status;  // 4 x ntiles count words (kFlagA | count)
+  unsigned* tile_counter;
+  unsigned* done;         // finished tiles
   void* queues;           // 4 queues of cap entries (the list's index type)
   double2* qxy;           // 4 x cap survivor coordinates, same positions
   std::uint64_t cap;
-  unsigned long long* counts;
+  double2* spec;          // 4 x spec_q coordinates + 4 counts (u64)
+  std::uint32_t spec_q;
 };
+__host__ __device__ inline unsigned long long* k2_spec_counts(double2* spec, std::uint32_t spec_q) {
+  return reinterpret_cast<unsigned long long*>(spec + 4ull * spec_q);
+}
 
 // One-pass tail (see K2OnePass): the tile's quadrant totals are in
 // S.qbase, the per-(item, warp) exclusive offsets in S.off.
@@ -884,7 +894,7 @@ __device__ __forceinline__ void k2_one_pass_tail(const GIdx* __restrict__ gidx,
     for (int off = 16; off > 0; off >>= 1) excl += __shfl_xor_sync(kFull, excl, off);
     if (lane == 0) {
       s_excl[q] = excl;
-      if (tile == ntiles - 1) op.counts[q] = excl + agg;
+      if (tile == ntiles - 1) k2_spec_counts(op.spec, op.spec_q)[q] = excl + agg;
     }
   }
   __syncthreads();
@@ -902,11 +912,27 @@ __device__ __forceinline__ void k2_one_pass_tail(const GIdx* __restrict__ gidx,
     const std::uint64_t pos = s_excl[q] + S.off[q][it * W + warp] + __popc(mine & lt);
     if (pos < op.cap) {
       const std::uint64_t k = t0 + std::uint64_t(it) * kK2Block + threadIdx.x;
+      const double2 p = cpts[k];
       queues[q * op.cap + pos] = gidx[k];
-      op.qxy[q * op.cap + pos] = cpts[k];
+      op.qxy[q * op.cap + pos] = p;
+      if (pos < op.spec_q) op.spec[q * op.spec_q + pos] = p;
     }
   }
 #undef LAB
+  // the last tile to finish leaves the work words zeroed for the next launch
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(op.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  for (std::uint64_t i = threadIdx.x; i < 4 * ntiles; i += kK2Block) op.status[i] = 0;
+  if (threadIdx.x == 0) {
+    *op.tile_counter = 0;
+    *op.done = 0;
+  }
 }
 
 template <typename GIdx, bool kOnePass = false>
@@ -1687,17 +1713,26 @@ template <typename IdxT>
 static void k2_launch(const double2* pts, std::uint64_t n, const KPlan& plan, void* d_work,
                       std::uint64_t ntiles, IdxT* q, std::uint64_t cap, std::uint8_t* d_labels,
                       unsigned long long* d_counts, cudaStream_t stream, const IdxT* g,
-                      const double2* cp, double2* qxy) {
-  const bool one_pass = qxy != nullptr;
-  if (one_pass && (g == nullptr || cp == nullptr || ntiles > kK2OnePassMaxTiles))
-    throw Error(OHX_E_INTERNAL, "k2 one-pass mode: a candidate list of <= kK2OnePassMaxTiles tiles");
-  const K2Work w = k2_work_layout(d_work, ntiles, one_pass);
+                      const double2* cp, const K2OnePassBufs* op_bufs) {
+  if (op_bufs) {
+    if (g == nullptr || cp == nullptr || ntiles > kK2OnePassMaxTiles)
+      throw Error(OHX_E_INTERNAL, "k2 one-pass mode: a candidate list of <= kK2OnePassMaxTiles tiles");
+    // the work area [tile counter | done | 4 x ntiles words] is zero on entry
+    // (cleared once when allocated, then by the kernel's last tile)
+    auto* w = static_cast<unsigned char*>(op_bufs->work);
+    K2Work kw{};
+    kw.tile_counter = reinterpret_cast<unsigned*>(w);
+    const K2OnePass op{reinterpret_cast<std::uint64_t*>(w + 256), reinterpret_cast<unsigned*>(w),
+                       reinterpret_cast<unsigned*>(w + 4), q,
+                       reinterpret_cast<double2*>(op_bufs->qxy), cap,
+                       reinterpret_cast<double2*>(op_bufs->spec), op_bufs->spec_q};
+    k2_filter_launch<IdxT, true>(pts, g, cp, n, plan, kw, ntiles, d_labels, stream, op);
+    return;
+  }
+  const K2Work w = k2_work_layout(d_work, ntiles);
   // re-arm the work counters and the look-back words
   check_cuda(cudaMemsetAsync(d_work, 0, w.clear_bytes, stream), "cudaMemsetAsync(k2 work)");
-  if (one_pass) {
-    const K2OnePass op{w.status, q, qxy, cap, d_counts};
-    k2_filter_launch<IdxT, true>(pts, g, cp, n, plan, w, ntiles, d_labels, stream, op);
-  } else if (g) {
+  if (g) {
     k2_filter_launch(pts, g, cp, n, plan, w, ntiles, d_labels, stream);
     k2_compact_launch<IdxT, true>(w, ntiles, q, cap, d_counts, g, stream);
   } else {
@@ -1709,16 +1744,15 @@ static void k2_launch(const double2* pts, std::uint64_t n, const KPlan& plan, vo
 void launch_k2(const double* d_xy, std::uint64_t n, const KPlan& plan, void* d_work,
                std::uint64_t ntiles, void* d_queues, int idx_bytes, std::uint64_t cap,
                std::uint8_t* d_labels, unsigned long long* d_counts, cudaStream_t stream,
-               const void* d_gather, const double* d_gather_xy, double* d_qxy) {
+               const void* d_gather, const double* d_gather_xy, const K2OnePassBufs* op) {
   const auto* pts = reinterpret_cast<const double2*>(d_xy);
   const auto* cp = reinterpret_cast<const double2*>(d_gather_xy);
-  auto* qxy = reinterpret_cast<double2*>(d_qxy);
   if (idx_bytes == 4)
     k2_launch(pts, n, plan, d_work, ntiles, static_cast<std::uint32_t*>(d_queues), cap, d_labels,
-              d_counts, stream, static_cast<const std::uint32_t*>(d_gather), cp, qxy);
+              d_counts, stream, static_cast<const std::uint32_t*>(d_gather), cp, op);
   else
     k2_launch(pts, n, plan, d_work, ntiles, static_cast<std::uint64_t*>(d_queues), cap, d_labels,
-              d_counts, stream, static_cast<const std::uint64_t*>(d_gather), cp, qxy);
+              d_counts, stream, static_cast<const std::uint64_t*>(d_gather), cp, op);
 }
 
 int kf_grid(int device) {
