@@ -38,12 +38,13 @@ void fold_stage_times(ohx_ctx* c, bool wait) {
   for (int k = 0; k < 4; ++k) {
     if (!c->timed[k] || c->folded[k]) continue;
     if (wait) check_cuda(cudaEventSynchronize(c->ev[k][1]), "cudaEventSynchronize");
-    else if (cudaEventQuery(c->ev[k][1]) != cudaSuccess) {
+    float v = 0.f;
+    const cudaError_t e = cudaEventElapsedTime(&v, c->ev[k][0], c->ev[k][1]);
+    if (e == cudaErrorNotReady) {  // (not waiting: left for a later fold)
       cudaGetLastError();
       continue;
     }
-    float v = 0.f;
-    check_cuda(cudaEventElapsedTime(&v, c->ev[k][0], c->ev[k][1]), "cudaEventElapsedTime");
+    check_cuda(e, "cudaEventElapsedTime");
     c->ksum[k] += v;
     ++c->kcnt[k];
     c->folded[k] = true;
@@ -119,6 +120,7 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
                  const ohx_filter_plan& plan, std::uint8_t* d_labels, std::uint64_t counts[4],
                  cudaStream_t s, const void* d_cand, std::uint64_t n_cand,
                  const double* d_cpts) {
+  Trace tr;
   const KPlan kp = make_kplan(plan, base, n);
   const std::uint64_t items = d_cand ? n_cand : n;
   const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
@@ -168,6 +170,7 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
         check_cuda(cudaMemsetAsync(c->d_gather, 0, kSpec * 16, s), "cudaMemsetAsync(gather)");
         c->spec_zeroed = true;
       }
+      tr.fine("  k2 prep");
       check_cuda(cudaEventRecord(c->ev[2][0], s), "cudaEventRecord");
       const K2OnePassBufs ob{c->d_k2op, c->d_gather, c->d_spec, spec_q};
       launch_k2(d_xy, items, kp, c->d_status, ntiles, c->d_queues, idx_bytes, cap, d_labels,
@@ -188,7 +191,9 @@ void filter_core(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
         check_cuda(cudaMemcpyAsync(c->h_spec, c->d_gather, kSpec * 16, cudaMemcpyDeviceToHost, s),
                    "cudaMemcpyAsync(survivors)");
       }
+      tr.fine("  k2 issued");
       check_cuda(cudaStreamSynchronize(s), "k2_filter");
+      tr.fine("  k2 synced");
       std::uint64_t mx = 0, total = 0;
       for (int q = 0; q < 4; ++q) {
         counts[q] = hc[q];
@@ -626,8 +631,9 @@ bool provisional_region(ohx_ctx* c, const double* d_xy, std::uint64_t n, KFRegio
            kMaxSubSamples * sizeof(ohx_extremes_rec), "sample records");
   auto* d_recs = reinterpret_cast<ohx_extremes_rec*>(c->d_sample);
   ensure_partials(c, segs);
-  launch_k1_sample(d_xy, n, segs, kSampleLen, subs, c->d_partials, c->d_ticket, d_recs, s);
+  launch_k1_sample(d_xy, n, segs, kSampleLen, subs, c->d_partials, c->d_ticket, d_recs, c->d_cnt, s);
   ++c->launches;
+  tr.fine("  sample issued");
   static_assert(kMaxSubSamples <= 8, "h_srec holds 8 records");
   const ohx_extremes_rec* rs = c->h_srec;  // pinned: a direct DMA, no staging copy
   check_cuda(cudaMemcpyAsync(c->h_srec, d_recs, subs * sizeof(ohx_extremes_rec),
@@ -705,6 +711,7 @@ bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
   c->fz.active = false;
   KFRegion q;
   std::uint64_t sampled = 0;
+  tr.fine("  enter");
   if (!provisional_region(c, d_xy, n, &q, &sampled, s, f, tr)) return false;
   const int idx_bytes = n <= 0xffffffffull ? 4 : 8;
   const int grid = kf_grid(c->device);
@@ -745,8 +752,10 @@ bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
     // the record and the counts after it: one copy
     check_cuda(cudaMemcpyAsync(c->h_rec, c->d_rec, kRecCountsOff + 4 * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(rec + counts)");
+    tr.fine("  cand issued");
     check_cuda(cudaStreamSynchronize(s), "kf + candidate extremes");
   };
+  tr.fine("  kf issued");
   candidates(cap_c);
   tr.mark("kf+cand-k1");
   f.sample_coverage = double(c->h_counts[2]) / double(sampled);
@@ -793,6 +802,7 @@ void fused_finish(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t
   }
   f.fuse_state = 1;
   f.fused = true;
+  Trace().fine("  certified");
   if (d_labels) check_cuda(cudaMemsetAsync(d_labels, 0, n, s), "cudaMemsetAsync(labels)");
   filter_core(c, d_xy, n, base, plan, d_labels, counts, s, c->d_cand, c->fz.n_cand, c->d_cpts);
 }

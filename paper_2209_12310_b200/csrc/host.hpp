@@ -135,18 +135,34 @@ struct ohx_ctx {
 namespace ohx {
 
 // OHX_TRACE=1: host wall time of each pipeline phase on stderr
-struct Trace {
-  bool on = [] {
+// OHX_TRACE=1: stage marks on stderr; OHX_TRACE=2: sub-stage marks too
+inline int trace_level() {
+  static const int v = [] {
     const char* e = std::getenv("OHX_TRACE");
-    return e && *e && std::string(e) != "0";
+    return e && *e ? std::atoi(e) : 0;
   }();
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  return v;
+}
+struct Trace {
+  bool on = trace_level() >= 1;
+  void fine(const char* what) {
+    if (trace_level() >= 2) mark(what);
+  }
+  // one timeline per thread: a mark measures from the previous mark of any
+  // Trace (OHX_TRACE=2), or of this one (OHX_TRACE=1)
+  static std::chrono::steady_clock::time_point& last() {
+    thread_local std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    return t;
+  }
+  std::chrono::steady_clock::time_point t =
+      trace_level() >= 2 ? last() : std::chrono::steady_clock::now();
   void mark(const char* what) {
     if (!on) return;
     const auto now = std::chrono::steady_clock::now();
+    const auto from = trace_level() >= 2 ? last() : t;
     std::fprintf(stderr, "[ohx] %-14s %8.3f ms\n", what,
-                 std::chrono::duration<double, std::milli>(now - t).count());
-    t = now;
+                 std::chrono::duration<double, std::milli>(now - from).count());
+    t = last() = std::chrono::steady_clock::now();  // the print itself not counted
   }
 };
 

@@ -182,13 +182,13 @@ inline std::uint64_t asc_key(double v) {
 }
 
 // Sweep sort of a mid-sized arc: LSD radix sort (8-bit digits, one
-// histogram pass for all four, digits all keys share skipped) on the top
-// 32 bits of the primary key, then runs of equal top bits sorted by the
-// comparator (rare for arcs of < 2^17 points: equal or nearly equal
-// coordinates).  A few linear passes over per-thread scratch instead of
-// ~n log n mispredicted comparisons (~50 ns per point on the box's host for
-// random arcs; 11-bit digits with per-call vectors: ~25 ns per point at a
-// few thousand points, the histograms' fixed cost).  Equal points may come
+// histogram pass for all four, digits all keys share skipped) of a 32-bit
+// key -- the primary key relative to the arc's smallest, shifted so that
+// the arc's key range fills 32 bits (survivors cluster: a fixed top-32-bit
+// slice of the key left long runs of equal keys) -- then runs of equal
+// 32-bit keys sorted by the comparator (rare).  A few linear passes over
+// per-thread scratch instead of ~n log n mispredicted comparisons (~50 ns
+// per point on the box's host for random arcs).  Equal points may come
 // out in any order, as with std::sort.
 template <int Q>
 void radix_sweep_sort(std::vector<P2>& pts) {
@@ -197,19 +197,29 @@ void radix_sweep_sort(std::vector<P2>& pts) {
   };
   const std::size_t n = pts.size();
   thread_local std::vector<E> a, b;
+  thread_local std::vector<std::uint64_t> k64;
   thread_local std::vector<P2> out;
   if (a.size() < n) {
     a.resize(n);
     b.resize(n);
+    k64.resize(n);
     out.resize(n);
   }
+  std::uint64_t lo = ~0ull, hi = 0;
+  for (std::size_t i = 0; i < n; ++i) {
+    const P2& p = pts[i];
+    const std::uint64_t k = Q == 1 ? ~asc_key(p.x) : Q == 2 ? ~asc_key(p.y)
+                          : Q == 3 ? asc_key(p.x) : asc_key(p.y);
+    k64[i] = k;
+    lo = std::min(lo, k);
+    hi = std::max(hi, k);
+  }
+  const std::uint64_t span = hi - lo;
+  const int shift = span >> 32 ? 64 - __builtin_clzll(span) - 32 : 0;
   constexpr int kDigits = 4;
   std::uint32_t cnt[kDigits][257] = {};
   for (std::size_t i = 0; i < n; ++i) {
-    const P2& p = pts[i];
-    const std::uint64_t k64 = Q == 1 ? ~asc_key(p.x) : Q == 2 ? ~asc_key(p.y)
-                            : Q == 3 ? asc_key(p.x) : asc_key(p.y);
-    const auto k = static_cast<std::uint32_t>(k64 >> 32);
+    const auto k = static_cast<std::uint32_t>((k64[i] - lo) >> shift);
     a[i] = {k, static_cast<std::uint32_t>(i)};
     for (int d = 0; d < kDigits; ++d) ++cnt[d][((k >> (8 * d)) & 255u) + 1];
   }
@@ -223,7 +233,7 @@ void radix_sweep_sort(std::vector<P2>& pts) {
     std::swap(src, dst);
   }
   for (std::size_t i = 0; i < n; ++i) out[i] = pts[src[i].i];
-  for (std::size_t r = 0; r < n;) {  // equal top bits: the comparator's order
+  for (std::size_t r = 0; r < n;) {  // equal 32-bit keys: the comparator's order
     std::size_t e = r + 1;
     while (e < n && src[e].k == src[r].k) ++e;
     if (e - r > 1) std::sort(out.begin() + r, out.begin() + e, SweepLess<Q>{});

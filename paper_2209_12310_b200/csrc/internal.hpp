@@ -138,9 +138,10 @@ void launch_kf_gather(const double* d_xy, const void* d_regions, int idx_bytes,
 // `len` points at evenly spaced offsets, run b belonging to sub-sample
 // b % subs; one record per sub-sample (global indices).  Partials: subs x
 // (segs / subs) entries, tickets: subs.
+// *d_count (the coverage counter of launch_count_in_region) is zeroed.
 void launch_k1_sample(const double* d_xy, std::uint64_t n, int segs, int len, int subs,
                       K1Partial* partials, unsigned* ticket, ohx_extremes_rec* d_recs,
-                      cudaStream_t stream);
+                      unsigned long long* d_count, cudaStream_t stream);
 // K1 over a short contiguous list (the fused pass's candidates)
 int k1_list_grid(std::uint64_t n);
 // (n capped by *d_n when d_n is set: a length counted on the device; the
@@ -150,7 +151,8 @@ void launch_k1_list(const double* d_xy, std::uint64_t n, const unsigned long lon
                     const void* d_map, int map_bytes, std::uint64_t map_base,
                     K1Partial* partials, int grid, unsigned* ticket, ohx_extremes_rec* d_rec,
                     cudaStream_t stream);
-// points of the sample runs 0, step, 2 step, ... inside Q
+// points of the sample runs 0, step, 2 step, ... inside Q, added to
+// *d_count (zeroed by launch_k1_sample)
 void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int len, int step,
                             const KFRegion& q, unsigned long long* d_count, cudaStream_t stream);
 // labels of classify_points against a polygon of m > 8 vertices: d_edges =

@@ -520,7 +520,9 @@ template <bool kSampled, typename LI>
 __global__ void __launch_bounds__(256)
     k1_small(const double2* __restrict__ pts, std::uint64_t n, const unsigned long long* d_n,
              const SampleMap sm, const ListMap lm, K1Partial* partials, unsigned* ticket,
-             ohx_extremes_rec* out) {
+             ohx_extremes_rec* out, unsigned long long* zero = nullptr) {
+  // (sample mode: zero the coverage counter count_in_region adds to next)
+  if (zero != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *zero = 0;
   if (d_n != nullptr && *d_n < n) n = *d_n;  // list length counted on the device
   const int g = blockIdx.y;
   partials += std::uint64_t(g) * gridDim.x;
@@ -1792,7 +1794,7 @@ void launch_kf_gather(const double* d_xy, const void* d_regions, int idx_bytes,
 
 void launch_k1_sample(const double* d_xy, std::uint64_t n, int segs, int len, int subs,
                       K1Partial* partials, unsigned* ticket, ohx_extremes_rec* d_recs,
-                      cudaStream_t stream) {
+                      unsigned long long* d_count, cudaStream_t stream) {
   const SampleMap sm{n, segs, len, subs};
   // 2 runs per block (4 sub-samples x 128 runs at 1e9: 256 blocks; 1 run:
   // 36 us, 2: 33 us, 4: 37 us -- fewer partials vs. fewer blocks in flight);
@@ -1805,7 +1807,7 @@ void launch_k1_sample(const double* d_xy, std::uint64_t n, int segs, int len, in
   const int bx = std::max(1, segs / subs / runs_per_block);
   k1_small<true, std::uint64_t><<<dim3(bx, subs), 256, 0, stream>>>(
       reinterpret_cast<const double2*>(d_xy), 0, nullptr, sm, ListMap{nullptr, 0, 0}, partials,
-      ticket, d_recs);
+      ticket, d_recs, d_count);
   check_cuda(cudaGetLastError(), "k1_small<sample> launch");
 }
 
@@ -1838,7 +1840,7 @@ void launch_k1_list(const double* d_xy, std::uint64_t n, const unsigned long lon
 
 void launch_count_in_region(const double* d_xy, std::uint64_t n, int segs, int len, int step,
                             const KFRegion& q, unsigned long long* d_count, cudaStream_t stream) {
-  check_cuda(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), stream), "cudaMemsetAsync");
+  // (*d_count was zeroed by the sample kernel, earlier on this stream)
   if (len % (kCountSplit * 1024) != 0) throw Error(OHX_E_INTERNAL, "count_in_region: run length");
   count_in_region<<<(segs + step - 1) / step * kCountSplit, 256, 0, stream>>>(
       reinterpret_cast<const double2*>(d_xy), SampleMap{n, segs, len, 1}, step, q, d_count);
