@@ -744,7 +744,7 @@ bool fused_begin(ohx_ctx* c, const double* d_xy, std::uint64_t n, std::uint64_t 
                      c->d_cand, c->d_cpts, cap, s);
     // grid sized for ~16 candidates per thread from the last call's count
     // (a hint only: the kernel covers the device-side count whatever the grid)
-    const int k1g = k1_list_grid(c->cand_hint ? std::min<std::uint64_t>(cap, 2 * c->cand_hint) : cap);
+    const int k1g = k1_list_grid(c->cand_hint ? std::min<std::uint64_t>(cap, c->cand_hint) : cap);
     ensure_partials(c, k1g);
     launch_k1_list(c->d_cpts, cap, c->d_counts, c->d_cand, idx_bytes, base, c->d_partials, k1g,
                    c->d_ticket, c->d_rec, s);

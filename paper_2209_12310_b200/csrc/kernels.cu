@@ -1819,7 +1819,13 @@ int k1_list_grid(std::uint64_t n) {
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     return occupancy_grid(dev, k1_small<false, std::uint32_t>, 256, ~0ull);
   }();
-  const std::uint64_t b = (n + 256 * 16 - 1) / (256 * 16);
+  // points per thread aimed at (OHX_K1LIST_PER overrides; tuning hook)
+  static const std::uint64_t per = [] {
+    const char* e = std::getenv("OHX_K1LIST_PER");
+    const int k = e ? std::atoi(e) : 0;
+    return static_cast<std::uint64_t>(k >= 1 ? k : 16);
+  }();
+  const std::uint64_t b = (n + 256 * per - 1) / (256 * per);
   return static_cast<int>(b < 1 ? 1 : (b > std::uint64_t(wave) ? wave : b));
 }
 
