@@ -322,7 +322,7 @@ void destroy_ctx(ohx_ctx* c) {
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_srec),
                   static_cast<void*>(c->h_crec),
-                  static_cast<void*>(c->h_cnt), c->h_sorted,
+                  static_cast<void*>(c->h_cnt), c->h_sorted, c->h_packed,
                   static_cast<void*>(c->h_spec)})
     if (p) cudaFreeHost(p);
   for (int b = 0; b < ohx_ctx::kStageBufs; ++b) {
@@ -368,6 +368,9 @@ void trim_ctx(ohx_ctx* c) {
   if (c->h_sorted) cudaFreeHost(c->h_sorted);
   c->h_sorted = nullptr;
   c->h_sorted_bytes = 0;
+  if (c->h_packed) cudaFreeHost(c->h_packed);
+  c->h_packed = nullptr;
+  c->h_packed_bytes = 0;
   for (int b = 0; b < ohx_ctx::kStageBufs; ++b) {
     if (c->h_stage[b]) cudaFreeHost(c->h_stage[b]);
     if (c->stage_ev[b]) cudaEventDestroy(c->stage_ev[b]);

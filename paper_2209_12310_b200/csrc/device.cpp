@@ -420,16 +420,18 @@ std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint
                              bool dev) {
   const std::uint64_t total = counts[0] + counts[1] + counts[2] + counts[3];
   if (total < device_sort_min()) {
-    std::vector<P2> packed(total);
+    host_grow(&c->h_packed, &c->h_packed_bytes, std::max<std::uint64_t>(16, total * 16),
+              "cudaMallocHost(survivors)");
+    const auto* packed = static_cast<const P2*>(c->h_packed);
     if (total) {
-      check_cuda(cudaMemcpyAsync(packed.data(), d_packed, total * 16, cudaMemcpyDeviceToHost, s),
+      check_cuda(cudaMemcpyAsync(c->h_packed, d_packed, total * 16, cudaMemcpyDeviceToHost, s),
                  "cudaMemcpyAsync(survivors)");
       check_cuda(cudaStreamSynchronize(s), "survivors D2H");
     }
     const P2* qp[4];
     std::uint64_t off = 0;
     for (int k = 0; k < 4; ++k) {
-      qp[k] = packed.data() + off;
+      qp[k] = packed + off;
       off += counts[k];
     }
     return emit_host_hull(hull_from_queue_points(anchors, qp, counts), sink, dev, s);
@@ -511,13 +513,20 @@ std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
     return hull_from_packed(c, c->d_gather, f.counts, anchors, s, sink, dev);
   }
   // small sets: the survivors' coordinates (usually already fetched with
-  // the K2 counts), then the host hull stage
-  std::vector<P2> packed(total);
-  queues_fetch_xy(c, reinterpret_cast<double*>(packed.data()), s);
+  // the K2 counts; else copied into a pinned buffer -- pageable copies
+  // went through the driver's staging, ~0.1 ms for the square's 16K), then
+  // the host hull stage reads them in place
+  const P2* packed = reinterpret_cast<const P2*>(c->h_spec);
+  if (c->spec_n != total) {
+    host_grow(&c->h_packed, &c->h_packed_bytes, std::max<std::uint64_t>(16, total * 16),
+              "cudaMallocHost(survivors)");
+    queues_fetch_xy(c, static_cast<double*>(c->h_packed), s);
+    packed = static_cast<const P2*>(c->h_packed);
+  }
   const P2* qp[4];
   std::uint64_t off = 0;
   for (int k = 0; k < 4; ++k) {
-    qp[k] = packed.data() + off;
+    qp[k] = packed + off;
     off += f.counts[k];
   }
   return emit_host_hull(hull_from_queue_points(anchors, qp, f.counts), sink, dev, s);

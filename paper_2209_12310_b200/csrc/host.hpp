@@ -101,6 +101,8 @@ struct ohx_ctx {
   std::uint64_t hchain_bytes = 0;
   void* h_sorted = nullptr;  // pinned: the sorted arcs on the host
   std::uint64_t h_sorted_bytes = 0;
+  void* h_packed = nullptr;  // pinned: a small survivor set's coordinates for the host hull
+  std::uint64_t h_packed_bytes = 0;
   cudaEvent_t arc_ev[4] = {};  // their per-arc copies
   unsigned long long* d_cnt = nullptr;
   unsigned long long* h_cnt = nullptr;  // pinned
