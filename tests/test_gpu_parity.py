@@ -343,8 +343,9 @@ def test_forced_fusion_heavy_candidates_match_oracle(one_pass):
     # OHX_FUSE=force fuses even when the provisional region covers the data
     # poorly (disk: ~25 % candidates, most warp tiles spill past their
     # 15-offset slot); the result must still be exact -- with K2 over the
-    # candidates in one launch (look-back in k2_filter) and as k2_filter +
-    # k2_compact (OHX_K2_ONEPASS=0)
+    # candidates in one launch (up to 2048 tiles; a 20M-point disk's 5M
+    # candidates take the two kernels) and as k2_filter + k2_compact
+    # (OHX_K2_ONEPASS=0)
     import subprocess
     import sys
     code = (
@@ -352,7 +353,9 @@ def test_forced_fusion_heavy_candidates_match_oracle(one_pass):
         "from oracle import Oracle\n"
         "o = Oracle()\n"
         "ctx = P.Context(0)\n"
-        "for dist, n, seed in [('disk', 9_000_000, 5), ('square', 8_500_003, 2), ('normal', 8_388_700, 9)]:\n"
+        "cases = [('disk', 9_000_000, 5), ('square', 8_500_003, 2), ('normal', 8_388_700, 9)]\n"
+        "if one_pass: cases.append(('disk', 20_000_000, 6))  # > 2048 candidate tiles: two kernels\n"
+        "for dist, n, seed in cases:\n"
         "    pts = P.generate(dist, n, seed)\n"
         "    hull, _ = ctx.heaphull_device(torch.from_numpy(pts).cuda(), n)\n"
         "    info = ctx.last_run()\n"
@@ -363,7 +366,7 @@ def test_forced_fusion_heavy_candidates_match_oracle(one_pass):
         "    for q in range(4):\n"
         "        idx, _ = ctx.queue(q + 1, info['counts'][q])\n"
         "        assert np.array_equal(idx, np.flatnonzero(want_labels == q + 1)), (dist, q)\n"
-        "print('force ok')\n")
+        "print('force ok')\n").replace("one_pass", repr(one_pass == "1"))
     env = dict(os.environ, OHX_FUSE="force", OHX_K2_ONEPASS=one_pass, PYTHONPATH=ROOT)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=600)
