@@ -24,8 +24,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cub/block/block_merge_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda/std/tuple>
+#include <cstdlib>
+#include <string>
 
 #include "internal.hpp"
 
@@ -155,6 +158,200 @@ __global__ void gather_sorted(const double2* __restrict__ arcs, const std::uint3
   }
 }
 
+// ---- first tier: 32-bit keys linear in the primary coordinate ----------
+// The primary coordinate mapped onto 32 bits over the input's bounding box
+// (the anchors: east / west / north / south extremes), t =
+// sqrt(fl(fl(X - x) / fl(X - W))) * 2^32 truncated: every step is monotone
+// (IEEE rounding is), so the key never decreases along the sweep order and
+// ties in it only group points; 4 radix passes over (u32, u32) pairs
+// instead of 8 over (u64, u32).  Runs of equal keys (equal or nearly equal
+// primary coordinates -- a few hundred points where an arc's coordinate is
+// stationary, e.g. a circle's tangent points) are then put in the full
+// sweep order: up to 32 points by one thread, up to kRunMax by one block
+// (cub::BlockMergeSort over the comparator); a longer run sends the call to
+// the 64-bit tier below.  This tier reads the arcs' points where they are
+// (the packed survivors + the anchors): no materialised copy of the arcs.
+constexpr std::uint32_t kRunSmall = 32;
+constexpr int kRunThreads = 256, kRunItems = 8;
+constexpr std::uint32_t kRunMax = kRunThreads * kRunItems;  // 2048
+constexpr std::uint32_t kRunCap = 8192;  // large runs handled per call
+
+// the four arcs [anchor q, packed[qoff[q] ...], anchor q+1] at aoff[q]
+struct ArcSrc {
+  const double2* packed;
+  const double2* anchors;
+  ulonglong4 qoff, aoff;
+  std::uint64_t total;
+  __device__ __forceinline__ int arc_of(std::uint64_t k) const {
+    return (k >= aoff.y) + (k >= aoff.z) + (k >= aoff.w);
+  }
+  __device__ __forceinline__ std::uint64_t begin(int q) const {
+    return q == 0 ? aoff.x : (q == 1 ? aoff.y : (q == 2 ? aoff.z : aoff.w));
+  }
+  __device__ __forceinline__ std::uint64_t end(int q) const {
+    return q == 0 ? aoff.y : (q == 1 ? aoff.z : (q == 2 ? aoff.w : total));
+  }
+  // point j of arc q
+  __device__ __forceinline__ double2 point(int q, std::uint64_t j) const {
+    const std::uint64_t p0 = q == 0 ? qoff.x : (q == 1 ? qoff.y : (q == 2 ? qoff.z : qoff.w));
+    if (j == 0) return anchors[q];
+    if (j == end(q) - begin(q) - 1) return anchors[(q + 1) & 3];
+    return packed[p0 + j - 1];
+  }
+};
+
+__global__ void linear_keys(const ArcSrc A, std::uint32_t* __restrict__ keys,
+                            std::uint32_t* __restrict__ vals) {
+  const double xE = A.anchors[0].x, yN = A.anchors[1].y, xW = A.anchors[2].x, yS = A.anchors[3].y;
+  const double sx = __dsub_rn(xE, xW), sy = __dsub_rn(yN, yS);
+  for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < A.total;
+       k += std::uint64_t(gridDim.x) * blockDim.x) {
+    const int q = A.arc_of(k);
+    const std::uint64_t j = k - A.begin(q);
+    const double2 p = A.point(q, j);
+    double t;
+    switch (q) {
+      case 0: t = __ddiv_rn(__dsub_rn(xE, p.x), sx); break;  // x descending
+      case 1: t = __ddiv_rn(__dsub_rn(yN, p.y), sy); break;  // y descending
+      case 2: t = __ddiv_rn(__dsub_rn(p.x, xW), sx); break;  // x ascending
+      default: t = __ddiv_rn(__dsub_rn(p.y, yS), sy); break;  // y ascending
+    }
+    // sqrt: the arc's anchor end is where survivors crowd (an arc leaves
+    // its anchor tangent to the anchor's axis: on a circle x = cos(theta),
+    // so sqrt(1 - x) is linear in the angle there); correctly rounded,
+    // hence monotone like the steps before it
+    t = __dmul_rn(__dsqrt_rn(t), 4294967296.0);
+    keys[k] = t >= 4294967295.0 ? 0xffffffffu : (t > 0.0 ? static_cast<std::uint32_t>(t) : 0u);
+    vals[k] = static_cast<std::uint32_t>(j);
+  }
+}
+
+__device__ __forceinline__ bool sweep_less(int q, double2 a, double2 b) {  // hull.cpp:18-30
+  switch (q) {
+    case 0: return a.x != b.x ? a.x > b.x : a.y < b.y;
+    case 1: return a.y != b.y ? a.y > b.y : a.x > b.x;
+    case 2: return a.x != b.x ? a.x < b.x : a.y > b.y;
+    default: return a.y != b.y ? a.y < b.y : a.x < b.x;
+  }
+}
+struct SweepLessOp {
+  int q;
+  __device__ __forceinline__ bool operator()(const double2& a, const double2& b) const {
+    return sweep_less(q, a, b);
+  }
+};
+
+// Runs of equal keys, fixed on the gathered points (contiguous, in key
+// order): short ones sorted here by the comparator, the others listed for
+// sort_runs; flag = a run past kRunMax points or more than kRunCap runs.
+// Warp-cooperative scan: lane l looks at key w0 + l (coalesced) and its
+// neighbours by shuffle; only run starts do any work.
+__device__ __forceinline__ void fix_run_at(const std::uint32_t* __restrict__ keys, double2* out,
+                                           const ArcSrc& A, std::uint64_t i, std::uint32_t key,
+                                           std::uint32_t prev, std::uint32_t next, uint2* runs,
+                                           unsigned* nruns, int* flag) {
+  const int q = A.arc_of(i);
+  const std::uint64_t a0 = A.begin(q), a1 = A.end(q);
+  if (i + 1 >= a1 || next != key || (i > a0 && prev == key)) return;  // not a run start
+  std::uint64_t j = i + 2;
+  while (j < a1 && keys[j] == key && j - i <= kRunMax) ++j;
+  const std::uint64_t len = j - i;
+  if (len > kRunMax) {
+    atomicExch(flag, 1);
+    return;
+  }
+  if (len > kRunSmall) {
+    const unsigned r = atomicAdd(nruns, 1u);
+    if (r < kRunCap) runs[r] = make_uint2(static_cast<unsigned>(i), static_cast<unsigned>(len));
+    else atomicExch(flag, 1);
+    return;
+  }
+  for (std::uint64_t k = i + 1; k < j; ++k) {  // insertion sort by the comparator
+    const double2 pv = out[k];
+    std::uint64_t m = k;
+    while (m > i && sweep_less(q, pv, out[m - 1])) {
+      out[m] = out[m - 1];
+      --m;
+    }
+    out[m] = pv;
+  }
+}
+
+// Warp-cooperative scan: lane l reads keys w0 + 4l .. w0 + 4l + 3 (one
+// 16-byte load; keys 16-byte aligned), the neighbours across lanes by
+// shuffle; only run starts do any work.
+__global__ void fix_runs(const std::uint32_t* __restrict__ keys, double2* out, const ArcSrc A,
+                         uint2* runs, unsigned* nruns, int* flag) {
+  const int lane = threadIdx.x & 31;
+  const std::uint64_t nwarps = std::uint64_t(gridDim.x) * (blockDim.x / 32);
+  const std::uint64_t n = A.total;
+  for (std::uint64_t w0 = (std::uint64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 128;
+       w0 < n; w0 += nwarps * 128) {
+    const std::uint64_t i0 = w0 + 4 * lane;
+    std::uint32_t k[4];
+    if (i0 + 3 < n) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(keys + i0));
+      k[0] = v.x;
+      k[1] = v.y;
+      k[2] = v.z;
+      k[3] = v.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) k[e] = i0 + e < n ? keys[i0 + e] : 0u;
+    }
+    std::uint32_t prev = __shfl_up_sync(0xffffffffu, k[3], 1);
+    std::uint32_t next = __shfl_down_sync(0xffffffffu, k[0], 1);
+    if (lane == 0 && i0 > 0 && i0 < n) prev = keys[i0 - 1];
+    if (lane == 31 && i0 + 4 < n) next = keys[i0 + 4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const std::uint64_t i = i0 + e;
+      if (i >= n) break;
+      fix_run_at(keys, out, A, i, k[e], e == 0 ? prev : k[e - 1], e == 3 ? next : k[e + 1], runs,
+                 nruns, flag);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRunThreads)
+    sort_runs(const uint2* __restrict__ runs, const unsigned* __restrict__ nruns, double2* out,
+              const ArcSrc A) {
+  using Sort = cub::BlockMergeSort<double2, kRunThreads, kRunItems>;
+  __shared__ typename Sort::TempStorage tmp;
+  if (blockIdx.x >= min(*nruns, kRunCap)) return;
+  const uint2 run = runs[blockIdx.x];
+  const std::uint64_t i = run.x;
+  const int n = static_cast<int>(run.y);
+  const int q = A.arc_of(i);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  double2 pad;  // after every finite point in this quadrant's order
+  switch (q) {
+    case 0: pad = make_double2(-inf, inf); break;
+    case 1: pad = make_double2(-inf, -inf); break;
+    case 2: pad = make_double2(inf, -inf); break;
+    default: pad = make_double2(inf, inf); break;
+  }
+  double2 key[kRunItems];
+#pragma unroll
+  for (int u = 0; u < kRunItems; ++u) {
+    const int t = threadIdx.x * kRunItems + u;
+    key[u] = t < n ? out[i + t] : pad;
+  }
+  Sort(tmp).Sort(key, SweepLessOp{q}, n, pad);
+#pragma unroll
+  for (int u = 0; u < kRunItems; ++u) {
+    const int t = threadIdx.x * kRunItems + u;
+    if (t < n) out[i + t] = key[u];
+  }
+}
+
+__global__ void gather_arcs(const ArcSrc A, const std::uint32_t* __restrict__ vals,
+                            double2* __restrict__ out) {
+  for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < A.total;
+       k += std::uint64_t(gridDim.x) * blockDim.x)
+    out[k] = A.point(A.arc_of(k), vals[k]);
+}
+
 struct ArcLayout {
   std::uint64_t total;
   ulonglong4 qoff, aoff;
@@ -195,6 +392,15 @@ std::size_t cub_tmp_bytes(std::uint64_t max_len) {  // for either sort
 
 std::size_t align256(std::size_t b) { return (b + 255) & ~std::size_t(255); }
 
+// OHX_HULL_SORT=u64: skip the 32-bit linear-key tier (A/B and test hook)
+bool linear_tier() {
+  static const bool v = [] {
+    const char* e = std::getenv("OHX_HULL_SORT");
+    return !(e && std::string(e) == "u64");
+  }();
+  return v;
+}
+
 }  // namespace
 
 std::size_t sort_arcs_work_bytes(const std::uint64_t counts[4]) {
@@ -229,11 +435,56 @@ void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const doub
   check_cuda(cudaMemcpyAsync(d_anchors, anchors, 64, cudaMemcpyHostToDevice, s),
              "cudaMemcpyAsync(anchors)");
   const unsigned grid = static_cast<unsigned>(L.total < 148ull * 2048 ? (L.total + 255) / 256 : 148 * 8);
+  const std::uint64_t ao[4] = {L.aoff.x, L.aoff.y, L.aoff.z, L.aoff.w};
+  int* d_flag = reinterpret_cast<int*>(d_anchors + 8);  // 4 bytes after the 4 anchors
+  // first tier: 32-bit linear keys (needs a bounding box of positive extent)
+  if (linear_tier() && anchors[0] > anchors[4] && anchors[3] > anchors[7]) {
+    auto* q0 = reinterpret_cast<std::uint32_t*>(k1);
+    auto* q1 = q0 + (L.total + 3) / 4 * 4;  // 16-byte aligned (fix_runs' vector loads)
+    auto* runs = reinterpret_cast<uint2*>(k0);
+    auto* nruns = reinterpret_cast<unsigned*>(d_flag + 1);
+    const ArcSrc A{reinterpret_cast<const double2*>(d_packed), d_anchors, L.qoff, L.aoff, L.total};
+    linear_keys<<<grid, 256, 0, s>>>(A, q0, v1);
+    check_cuda(cudaGetLastError(), "linear_keys launch");
+    int lsel[4];
+    for (int q = 0; q < 4; ++q) {
+      cub::DoubleBuffer<std::uint32_t> kb(q0 + ao[q], q1 + ao[q]);
+      cub::DoubleBuffer<std::uint32_t> vb(v1 + ao[q], v0 + ao[q]);
+      std::size_t tb = tmp_bytes;
+      check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb,
+                                                 static_cast<std::int64_t>(L.len[q]), 0, 32, s),
+                 "cub::DeviceRadixSort::SortPairs(u32)");
+      lsel[q] = kb.selector;
+    }
+    std::uint32_t* lkeys = lsel[0] ? q1 : q0;
+    std::uint32_t* lvals = lsel[0] ? v0 : v1;
+    for (int q = 1; q < 4; ++q)
+      if (lsel[q] != lsel[0]) {
+        check_cuda(cudaMemcpyAsync(lkeys + ao[q], (lsel[q] ? q1 : q0) + ao[q], L.len[q] * 4,
+                                   cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync(sorted keys)");
+        check_cuda(cudaMemcpyAsync(lvals + ao[q], (lsel[q] ? v0 : v1) + ao[q], L.len[q] * 4,
+                                   cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync(sorted positions)");
+      }
+    // the points in key order, then the runs of equal keys in full order
+    auto* out = reinterpret_cast<double2*>(d_sorted);
+    gather_arcs<<<grid, 256, 0, s>>>(A, lvals, out);
+    check_cuda(cudaGetLastError(), "gather_arcs launch");
+    check_cuda(cudaMemsetAsync(d_flag, 0, 2 * sizeof(int), s), "cudaMemsetAsync(flag)");
+    fix_runs<<<grid, 256, 0, s>>>(lkeys, out, A, runs, nruns, d_flag);
+    check_cuda(cudaGetLastError(), "fix_runs launch");
+    sort_runs<<<kRunCap, kRunThreads, 0, s>>>(runs, nruns, out, A);
+    check_cuda(cudaGetLastError(), "sort_runs launch");
+    int too_long = 0;
+    check_cuda(cudaMemcpyAsync(&too_long, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s),
+               "cudaMemcpyAsync(flag)");
+    check_cuda(cudaStreamSynchronize(s), "hull sort runs");
+    if (!too_long) return;
+  }
+  // the arcs materialised for the tiers below
   build_arc_keys<<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(d_packed), L.qoff, L.aoff,
                                       L.total, d_anchors, arcs, nullptr, nullptr);
   check_cuda(cudaGetLastError(), "build_arc_keys launch");
-  const std::uint64_t ao[4] = {L.aoff.x, L.aoff.y, L.aoff.z, L.aoff.w};
-  // fast path: 64-bit primary keys (half the radix passes), ties repaired
+  // second tier: 64-bit primary keys (half the passes of the full key), ties repaired
   auto* p0 = reinterpret_cast<std::uint64_t*>(k1);  // k1 is free until the fallback
   auto* p1 = p0 + L.total;
   primary_keys<<<grid, 256, 0, s>>>(arcs, L.aoff, L.total, p0, v1);
@@ -258,7 +509,6 @@ void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const doub
       check_cuda(cudaMemcpyAsync(vals + ao[q], (sel[q] ? v0 : v1) + ao[q], L.len[q] * 4,
                                  cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync(sorted positions)");
     }
-  int* d_flag = reinterpret_cast<int*>(d_anchors + 8);  // 4 bytes after the 4 anchors
   check_cuda(cudaMemsetAsync(d_flag, 0, sizeof(int), s), "cudaMemsetAsync(flag)");
   repair_ties<<<grid, 256, 0, s>>>(keys, vals, arcs, L.aoff, L.total, d_flag);
   check_cuda(cudaGetLastError(), "repair_ties launch");

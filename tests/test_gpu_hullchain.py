@@ -238,3 +238,13 @@ def test_pipeline_device_chains_match_oracle():
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=900)
     assert r.returncode == 0 and "pipeline ok" in r.stdout, r.stdout + r.stderr[-3000:]
+
+
+def test_pipeline_device_chains_64bit_sort_tier():
+    # OHX_HULL_SORT=u64 skips the sweep sort's 32-bit linear-key tier: the
+    # 64-bit primary-key tier (and its 128-bit fallback) against the oracle
+    env = dict(os.environ, OHX_DEVICE_SORT_MIN="100000", OHX_HULL_SORT="u64")
+    code = PIPE_SCRIPT.replace("ROOT_DIR", repr(ROOT))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=900)
+    assert r.returncode == 0 and "pipeline ok" in r.stdout, r.stdout + r.stderr[-3000:]
