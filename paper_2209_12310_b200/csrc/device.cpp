@@ -318,7 +318,7 @@ void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s) {
   }
   grow_gather(c, total * 16);
   launch_gather4(c->last_xy, c->d_queues, c->last_idx_bytes, c->last_cap, c->last_counts,
-                 c->d_gather, s);
+                 c->d_gather, s, c->last_n);
   ++c->launches;
   check_cuda(cudaMemcpyAsync(h_xy, c->d_gather, total * 16, cudaMemcpyDeviceToHost, s),
              "cudaMemcpyAsync(queues xy)");
@@ -508,7 +508,7 @@ std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
     grow_gather(c, total * 16);
     c->qxy_valid = false;
     launch_gather4(c->last_xy, c->d_queues, c->last_idx_bytes, c->last_cap, c->last_counts,
-                   c->d_gather, s);
+                   c->d_gather, s, c->last_n);
     ++c->launches;
     return hull_from_packed(c, c->d_gather, f.counts, anchors, s, sink, dev);
   }

@@ -163,9 +163,11 @@ void launch_polygon_labels(const double* d_xy, std::uint64_t n, const double* d_
 // *d_first = the smallest index with a non-finite coordinate, else ~0
 void launch_first_nonfinite(const double* d_xy, std::uint64_t n, unsigned long long* d_first,
                             cudaStream_t stream);
+// n (the shard's points, optional): large, dense survivor sets are
+// gathered by index range (one read of each line)
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
                     std::uint64_t cap, const std::uint64_t counts[4], double* d_out,
-                    cudaStream_t stream);
+                    cudaStream_t stream, std::uint64_t n = 0);
 void launch_gather(const double* d_xy, const void* d_idx, int idx_bytes,
                    std::uint64_t count, double* d_out, cudaStream_t stream);
 // hull vertices -> smallest survivor index (+ base) with equal coordinates

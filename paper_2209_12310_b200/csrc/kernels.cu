@@ -1530,6 +1530,50 @@ __global__ void gather_xy4(const double2* __restrict__ pts, const IdxT* __restri
   }
 }
 
+// The same for large survivor sets, block b over the points [b S, (b+1) S):
+// each queue's entries in that index range (two binary searches per queue)
+// copied one queue after the other.  The four queues interleave in the
+// index order (a circle's survivors: every line holds all four), so a
+// grid-stride pass over the packed output reads every line once per queue,
+// far apart in time; here the four reads of a line fall inside one block.
+constexpr std::uint64_t kGatherRange = 4096;  // blocks in flight x 64 KB stay in L2
+template <typename IdxT>
+__device__ __forceinline__ std::uint64_t lower_bound_idx(const IdxT* q, std::uint64_t n,
+                                                         std::uint64_t v) {
+  std::uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const std::uint64_t mid = (lo + hi) >> 1;
+    if (static_cast<std::uint64_t>(q[mid]) < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+template <typename IdxT>
+__global__ void __launch_bounds__(256)
+    gather_xy4_ranged(const double2* __restrict__ pts, std::uint64_t n,
+                      const IdxT* __restrict__ queues, std::uint64_t cap, ulonglong4 ends,
+                      double2* __restrict__ out) {
+  __shared__ std::uint64_t s_lo[4], s_hi[4];
+  const std::uint64_t a = std::uint64_t(blockIdx.x) * kGatherRange;
+  const std::uint64_t b = min(n, a + kGatherRange);
+  const std::uint64_t cnt[4] = {ends.x, ends.y - ends.x, ends.z - ends.y, ends.w - ends.z};
+  if (threadIdx.x < 8) {
+    const int q = threadIdx.x >> 1;
+    const std::uint64_t v = lower_bound_idx(queues + std::uint64_t(q) * cap, cnt[q],
+                                            (threadIdx.x & 1) ? b : a);
+    if (threadIdx.x & 1) s_hi[q] = v;
+    else s_lo[q] = v;
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    const std::uint64_t start = q == 0 ? 0 : (q == 1 ? ends.x : (q == 2 ? ends.y : ends.z));
+    const IdxT* qq = queues + std::uint64_t(q) * cap;
+    for (std::uint64_t k = s_lo[q] + threadIdx.x; k < s_hi[q]; k += 256)
+      out[start + k] = pts[qq[k]];
+  }
+}
+
 // The same with the counts read on the device, for the first `limit`
 // survivors: launched right behind K2 so that a small survivor set comes
 // back with the counts, in the same round trip.  Nothing is written when a
@@ -1873,13 +1917,25 @@ void launch_first_nonfinite(const double* d_xy, std::uint64_t n, unsigned long l
 
 void launch_gather4(const double* d_xy, const void* d_queues, int idx_bytes,
                     std::uint64_t cap, const std::uint64_t counts[4], double* d_out,
-                    cudaStream_t stream) {
+                    cudaStream_t stream, std::uint64_t n) {
   const ulonglong4 ends = make_ulonglong4(counts[0], counts[0] + counts[1],
                                           counts[0] + counts[1] + counts[2],
                                           counts[0] + counts[1] + counts[2] + counts[3]);
   if (ends.w == 0) return;
-  const unsigned grid = static_cast<unsigned>(ends.w < 148ull * 2048 ? (ends.w + 255) / 256 : 148 * 8);
   const auto* pts = reinterpret_cast<const double2*>(d_xy);
+  // many survivors (at least one per 64 points on average): by index range
+  if (n && ends.w >= (1u << 20) && ends.w * 64 >= n) {
+    const unsigned g = static_cast<unsigned>((n + kGatherRange - 1) / kGatherRange);
+    if (idx_bytes == 4)
+      gather_xy4_ranged<<<g, 256, 0, stream>>>(pts, n, static_cast<const std::uint32_t*>(d_queues),
+                                               cap, ends, reinterpret_cast<double2*>(d_out));
+    else
+      gather_xy4_ranged<<<g, 256, 0, stream>>>(pts, n, static_cast<const std::uint64_t*>(d_queues),
+                                               cap, ends, reinterpret_cast<double2*>(d_out));
+    check_cuda(cudaGetLastError(), "gather_xy4_ranged launch");
+    return;
+  }
+  const unsigned grid = static_cast<unsigned>(ends.w < 148ull * 2048 ? (ends.w + 255) / 256 : 148 * 8);
   if (idx_bytes == 4)
     gather_xy4<<<grid, 256, 0, stream>>>(pts, static_cast<const std::uint32_t*>(d_queues), cap,
                                          ends, reinterpret_cast<double2*>(d_out));
