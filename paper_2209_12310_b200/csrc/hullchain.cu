@@ -233,7 +233,17 @@ __global__ void __launch_bounds__(128) chain_copy(const double2* __restrict__ lo
   const double2* s = loc + p.b + st.base[c];
   double2* d = cycle + st.offs[c];
   const std::uint64_t L = st.slice[c];
-  for (std::uint64_t i = threadIdx.x; i < L; i += blockDim.x) d[i] = s[i];
+  // four independent loads in flight per thread (one at a time left the
+  // copy latency-bound: 0.65 -> 0.55 ms for the circle's 1.55 GB)
+  std::uint64_t i = threadIdx.x;
+  for (; i + 3 * blockDim.x < L; i += 4 * blockDim.x) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = s[i + u * blockDim.x];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) d[i + u * blockDim.x] = v[u];
+  }
+  for (; i < L; i += blockDim.x) d[i] = s[i];
 }
 
 // ---- cycle statistics (finalize_cycle's fast-path test)
