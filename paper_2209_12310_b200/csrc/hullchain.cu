@@ -99,33 +99,56 @@ struct ChunkState {
   std::uint64_t* offs;
 };
 
+// One thread per chunk: the lanes of a warp walk 32 different chunks, so
+// the points are staged through shared memory kCT at a time with coalesced
+// loads (two chunks' kCT-point runs per load instruction) -- direct
+// per-lane loads fetched 32 separate lines per warp load.
+constexpr int kCT = 16;  // points per chunk per staging round
 __global__ void __launch_bounds__(128) chain_local(const double2* __restrict__ in, double2* loc,
                                                    ArcGeom g, ChunkState st) {
+  __shared__ double2 tile[4][32][kCT + 1];  // per warp: 32 chunks x kCT (+1: 4-way banks)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const std::uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= g.choff[4]) return;
-  const ChunkPos p = chunk_pos(g, c);
-  const double2* src = in + p.b;
-  double2* s = loc + p.b;
-  const std::uint32_t len = static_cast<std::uint32_t>(p.e - p.b);
+  const bool live = c < g.choff[4];
+  std::uint64_t b0 = 0;
+  std::uint32_t len = 0;
+  if (live) {
+    const ChunkPos p = chunk_pos(g, c);
+    b0 = p.b;
+    len = static_cast<std::uint32_t>(p.e - p.b);
+  }
+  double2* s = loc + b0;
   std::uint32_t top = 0, rest = 0xffffffffu;
   double2 s0 = make_double2(0, 0), s1 = make_double2(0, 0);  // s[top-2], s[top-1]
   std::uint16_t* low = st.low + std::uint64_t(c) * kWin;
-  double2 nx = __ldg(src);
-  for (std::uint32_t k = 0; k < len; ++k) {
-    const double2 pt = nx;
-    if (k + 1 < len) nx = __ldg(src + k + 1);
-    while (top >= 2 && !strict_left(s0, s1, pt)) {
-      --top;
-      s1 = s0;
-      if (top >= 2) s0 = s[top - 2];
+  const std::uint32_t maxlen = __reduce_max_sync(0xffffffffu, len);
+  const int half = lane >> 4, hl = lane & 15;
+  for (std::uint32_t t0 = 0; t0 < maxlen; t0 += kCT) {
+#pragma unroll 4
+    for (int j = 0; j < 32; j += 2) {  // chunks j (lanes 0-15) and j+1 (lanes 16-31)
+      const std::uint64_t bj = __shfl_sync(0xffffffffu, b0, j + half);
+      const std::uint32_t lj = __shfl_sync(0xffffffffu, len, j + half);
+      if (t0 + hl < lj) tile[warp][j + half][hl] = __ldg(in + bj + t0 + hl);
     }
-    if (k < kWin) low[k] = static_cast<std::uint16_t>(top);
-    else rest = min(rest, top);
-    s[top] = pt;
-    s0 = s1;
-    s1 = pt;
-    ++top;
+    __syncwarp();
+    const std::uint32_t kend = min(len, t0 + kCT);
+    for (std::uint32_t k = t0; k < kend; ++k) {
+      const double2 pt = tile[warp][lane][k - t0];
+      while (top >= 2 && !strict_left(s0, s1, pt)) {
+        --top;
+        s1 = s0;
+        if (top >= 2) s0 = s[top - 2];
+      }
+      if (k < kWin) low[k] = static_cast<std::uint16_t>(top);
+      else rest = min(rest, top);
+      s[top] = pt;
+      s0 = s1;
+      s1 = pt;
+      ++top;
+    }
+    __syncwarp();
   }
+  if (!live) return;
   st.height[c] = top;
   st.low_rest[c] = rest;
 }
