@@ -376,14 +376,18 @@ bool hull_device_chains(ohx_ctx* c, const double* d_sorted, const std::uint64_t 
   Trace tr;
   dev_grow(&c->d_hchain, &c->hchain_bytes, device_chain_work_bytes(len), "hull chain work");
   DeviceCycle dc;
-  const bool ok = device_chains(d_sorted, len, c->d_hchain, s, &dc);
+  const bool ok = device_chains(d_sorted, len, c->d_hchain, s, &dc, dev ? c->dev_out : nullptr,
+                                dev ? c->dev_out_cap : 0);
   c->launches += dc.launches;
   c->last_run.hull_path = ok ? 1 : 2;
   tr.mark(ok ? "dev chains" : "dev chains (unproven: host chains)");
   if (!ok) return false;
   const std::uint64_t m = dc.m;
+  const bool direct = dev && dc.d_cycle == c->dev_out;  // the cycle is in the caller's buffer
   if (raw) {  // the chained cycle itself (test hook)
-    emit_device_bytes(c, sink(m), dc.d_cycle, m * 16, dev, s);
+    P2* out = sink(m);
+    if (!(direct && reinterpret_cast<double*>(out) == dc.d_cycle))
+      emit_device_bytes(c, out, dc.d_cycle, m * 16, dev, s);
     if (dev) check_cuda(cudaStreamSynchronize(s), "hull D2D");
     *h = m;
     return true;
@@ -393,8 +397,19 @@ bool hull_device_chains(ohx_ctx* c, const double* d_sorted, const std::uint64_t 
     // its start vertex, copied straight into the caller's buffer
     P2* out = sink(m);
     const std::uint64_t b = dc.best;
-    emit_device_bytes(c, out, dc.d_cycle + 2 * b, (m - b) * 16, dev, s);
-    emit_device_bytes(c, out + (m - b), dc.d_cycle, b * 16, dev, s);
+    const double* cyc = dc.d_cycle;
+    if (direct && reinterpret_cast<double*>(out) == dc.d_cycle) {
+      if (b == 0) {  // already the hull, in place
+        tr.mark("hull in place (fast path)");
+        *h = m;
+        return true;
+      }
+      check_cuda(cudaMemcpyAsync(dc.d_scratch, dc.d_cycle, m * 16, cudaMemcpyDeviceToDevice, s),
+                 "cudaMemcpyAsync(cycle)");
+      cyc = dc.d_scratch;
+    }
+    emit_device_bytes(c, out, cyc + 2 * b, (m - b) * 16, dev, s);
+    emit_device_bytes(c, out + (m - b), cyc, b * 16, dev, s);
     if (dev) check_cuda(cudaStreamSynchronize(s), "hull D2D");
     tr.mark(dev ? "hull D2D (fast path)" : "hull D2H (fast path)");
     *h = m;

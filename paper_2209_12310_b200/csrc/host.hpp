@@ -64,6 +64,10 @@ struct ohx_ctx {
   // d_gather holds the last filter's survivor coordinates per quadrant
   // (one-pass K2: entry i of quadrant q at q * last_cap + i)
   bool qxy_valid = false;
+  // ohx_heaphull_device_out's buffer, for the duration of that call: the
+  // device hull stage writes its cycle there directly
+  double* dev_out = nullptr;
+  std::uint64_t dev_out_cap = 0;
   // one-pass K2: its self-clearing work words and the small block it
   // returns (the first survivors' coordinates + the counts)
   void* d_k2op = nullptr;

@@ -402,11 +402,14 @@ ChainLayout chain_layout(const std::uint64_t len[4]) {
 std::size_t device_chain_work_bytes(const std::uint64_t len[4]) { return chain_layout(len).bytes; }
 
 bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_work,
-                   cudaStream_t s, DeviceCycle* out) {
+                   cudaStream_t s, DeviceCycle* out, double* direct, std::uint64_t direct_cap) {
   const ChainLayout L = chain_layout(len);
   auto* w = static_cast<unsigned char*>(d_work);
   auto* loc = reinterpret_cast<double2*>(w + L.o_loc);
-  auto* cycle = reinterpret_cast<double2*>(w + L.o_cycle);
+  // the cycle straight into the caller's device buffer when it can hold
+  // every arc point (the hull is usually the cycle as is)
+  auto* cycle = direct != nullptr && direct_cap >= L.total ? reinterpret_cast<double2*>(direct)
+                                                           : reinterpret_cast<double2*>(w + L.o_cycle);
   ChunkState st;
   st.height = reinterpret_cast<std::uint32_t*>(w + L.o_h);
   st.low_rest = reinterpret_cast<std::uint32_t*>(w + L.o_lr);
@@ -455,6 +458,7 @@ bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_w
   if (hd.fail) return false;
   const std::uint64_t m = hd.last_off + hd.last_len;
   out->d_cycle = reinterpret_cast<double*>(cycle);
+  out->d_scratch = reinterpret_cast<double*>(w + L.o_cycle);
   out->m = m;
   out->chunks = G;
   if (m == 0) return true;

@@ -284,14 +284,18 @@ void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const doub
 // d_cycle, with the statistics finalize_cycle's fast path needs.
 struct DeviceCycle {
   double* d_cycle = nullptr;
+  double* d_scratch = nullptr;  // room for a copy of the cycle (when d_cycle is the caller's)
   std::uint64_t m = 0, best = 0, bad = 0;
   std::uint32_t chunks = 0;
   bool front_eq_back = false, dups = false, flat = false;
   int launches = 0;
 };
 std::size_t device_chain_work_bytes(const std::uint64_t len[4]);
+// direct (nullable): the caller's device output; the cycle is written there
+// when direct_cap covers every arc point.
 bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_work,
-                   cudaStream_t s, DeviceCycle* out);
+                   cudaStream_t s, DeviceCycle* out, double* direct = nullptr,
+                   std::uint64_t direct_cap = 0);
 // hull stage from the four arcs [anchor q, queue q, anchor q+1] already in
 // sweep order (device-sorted)
 // (wait_arc(q), when set, is called by arc q's thread before it reads the

@@ -115,6 +115,17 @@ int ohx_heaphull_device_out(ohx_ctx* ctx, const double* d_xy, uint64_t n, double
     const auto t0 = Clock::now();
     const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
     const auto t1 = Clock::now();
+    struct DevOut {  // the caller's buffer, visible to the hull stage for this call only
+      ohx_ctx* c;
+      DevOut(ohx_ctx* c_, double* p, std::uint64_t k) : c(c_) {
+        c->dev_out = p;
+        c->dev_out_cap = k;
+      }
+      ~DevOut() {
+        c->dev_out = nullptr;
+        c->dev_out_cap = 0;
+      }
+    } dev_out(ctx, d_hull, cap);
     ohx::device_queues_hull(ctx, f, s, hull_sink(d_hull, cap, h), true);
     const auto t2 = Clock::now();
     if (timings) {

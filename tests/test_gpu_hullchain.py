@@ -248,3 +248,43 @@ def test_pipeline_device_chains_64bit_sort_tier():
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=900)
     assert r.returncode == 0 and "pipeline ok" in r.stdout, r.stdout + r.stderr[-3000:]
+
+
+ROTATED_SCRIPT = r"""
+import sys
+sys.path.insert(0, ROOT_DIR)
+import numpy as np, torch, paper_2209_12310_b200 as P
+from oracle import Oracle
+o = Oracle()
+ctx = P.Context(0)
+pts = P.generate("circle", 1_200_000, 8)
+e = int(np.argmax(pts[:, 0]))
+# a second point at the largest x, below the east extreme and with a larger
+# index: it joins the S -> E arc and is the hull's first vertex (max x, then
+# min y), so the chained cycle must be rotated
+extra = np.array([[pts[e, 0], pts[e, 1] - 1e-7]])
+pts = np.ascontiguousarray(np.concatenate([pts, extra]))
+n = len(pts)
+dx = torch.from_numpy(pts).cuda()
+want = o.heaphull(pts)
+assert want[0, 0] == pts[e, 0] and want[0, 1] == extra[0, 1], want[:2]
+hull, _ = ctx.heaphull_device(dx, n)
+assert np.array_equal(hull, want)
+buf = torch.empty((n + 8, 2), dtype=torch.float64, device="cuda")
+dh, _ = ctx.heaphull_device(dx, n, out=buf)  # the cycle written into buf, then rotated
+info = ctx.last_run()
+assert info["hull_path"] == "device-chains", info
+assert np.array_equal(dh.cpu().numpy(), want)
+print("rotated ok")
+"""
+
+
+def test_device_hull_rotated_into_caller_buffer():
+    # the device hull stage writes its cycle straight into the caller's
+    # device buffer; when the hull's first vertex is not the cycle's first
+    # point the cycle is copied aside and rotated back into it
+    env = dict(os.environ, OHX_DEVICE_SORT_MIN="100000")
+    code = ROTATED_SCRIPT.replace("ROOT_DIR", repr(ROOT))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=600)
+    assert r.returncode == 0 and "rotated ok" in r.stdout, r.stdout + r.stderr[-3000:]
