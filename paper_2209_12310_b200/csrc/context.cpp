@@ -318,6 +318,7 @@ void destroy_ctx(ohx_ctx* c) {
                   static_cast<void*>(c->d_labels), static_cast<void*>(c->d_gather),
                   static_cast<void*>(c->d_sample), c->d_cand, static_cast<void*>(c->d_cnt),
                   c->d_regions, static_cast<void*>(c->d_cpts), c->d_hsort, c->d_hchain, c->d_poly,
+                  static_cast<void*>(c->d_cycfull),
                   c->d_k2op, static_cast<void*>(c->d_spec)})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(c->h_rec), static_cast<void*>(c->h_srec),
@@ -331,6 +332,9 @@ void destroy_ctx(ohx_ctx* c) {
   }
   for (auto& e : c->arc_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->pipe_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (auto& pair : c->ev)
     for (auto& e : pair)
       if (e) cudaEventDestroy(e);
@@ -365,6 +369,7 @@ void trim_ctx(ohx_ctx* c) {
   dfree(c->d_hsort, &c->hsort_bytes);
   dfree(c->d_hchain, &c->hchain_bytes);
   dfree(c->d_poly, &c->poly_bytes);
+  dfree(c->d_cycfull, &c->cycfull_bytes);
   if (c->h_sorted) cudaFreeHost(c->h_sorted);
   c->h_sorted = nullptr;
   c->h_sorted_bytes = 0;

@@ -425,6 +425,100 @@ bool hull_device_chains(ohx_ctx* c, const double* d_sorted, const std::uint64_t 
   return true;
 }
 
+// OHX_HULL_PIPE=0: the hull stage of a large survivor set never pipelined
+// with its own transfer (A/B and test hook)
+bool hull_pipe_mode() {
+  static const bool v = [] {
+    const char* e = std::getenv("OHX_HULL_PIPE");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
+constexpr std::uint64_t kPipeMin = 1u << 22;  // survivors from which pipelining pays
+
+// The hull stage of a large survivor set whose hull goes to PINNED host
+// memory, arc by arc: each arc is sorted and chained on the device and its
+// chain copied to the host on a second stream while the next arc is
+// sorted and chained -- the hull's own transfer (1.55 GB for the circle's
+// 96.8M vertices, 28 ms over PCIe) then hides most of the device work.
+// The statistics over the whole cycle decide at the end: the cycle is the
+// hull as is (the usual case), a rotation of it, or the host clean-up runs
+// from the copy already in the caller's buffer.  false: not taken (the
+// caller runs the regular stage; nothing was returned).
+bool hull_pipelined(ohx_ctx* c, const double* d_packed, const std::uint64_t counts[4],
+                    const P2 anchors[4], cudaStream_t s, const HullSink& sink, std::size_t* h) {
+  const std::uint64_t total = counts[0] + counts[1] + counts[2] + counts[3];
+  if (total < kPipeMin || !hull_pipe_mode() || !device_chain_mode()) return false;
+  const std::uint64_t arcs_n = total + 8;
+  P2* out = nullptr;
+  try {
+    out = sink(arcs_n);  // room for every arc point (the regular path otherwise)
+  } catch (const std::exception&) {
+    return false;
+  }
+  if (!is_pinned(out)) return false;
+  Trace tr;
+  dev_grow(&c->d_hsort, &c->hsort_bytes, sort_arcs_work_bytes(counts) + arcs_n * 16,
+           "hull sort work");
+  auto* d_sorted = reinterpret_cast<double*>(static_cast<unsigned char*>(c->d_hsort) +
+                                             sort_arcs_work_bytes(counts));
+  std::uint64_t len[4];
+  for (int q = 0; q < 4; ++q) len[q] = counts[q] + 2;
+  dev_grow(&c->d_hchain, &c->hchain_bytes, device_chain_work_bytes(len), "hull chain work");
+  dev_grow(reinterpret_cast<void**>(&c->d_cycfull), &c->cycfull_bytes, arcs_n * 16, "hull cycle");
+  if (!c->copy_stream)
+    check_cuda(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking),
+               "cudaStreamCreate(copy)");
+  if (!c->pipe_ev[0])
+    for (auto& e : c->pipe_ev)
+      check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate(pipe)");
+  std::uint64_t off = 0;
+  for (int q = 0; q < 4; ++q) {
+    sort_arcs(d_packed, counts, reinterpret_cast<const double*>(anchors), c->d_hsort, d_sorted, s,
+              q);
+    DeviceCycle dc;  // arc q's chain written straight after the arcs before it
+    const bool ok = device_chains(d_sorted, len, c->d_hchain, s, &dc, c->d_cycfull + 2 * off,
+                                  arcs_n - off, q);
+    c->launches += 4 + dc.launches;
+    if (!ok) {  // an arc the chunked chains cannot prove: the regular stage
+      check_cuda(cudaStreamSynchronize(c->copy_stream), "hull copy");
+      return false;
+    }
+    if (dc.m) {  // (a chain not written in place: copied there -- not expected)
+      if (dc.d_cycle != c->d_cycfull + 2 * off)
+        check_cuda(cudaMemcpyAsync(c->d_cycfull + 2 * off, dc.d_cycle, dc.m * 16,
+                                   cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync(arc chain)");
+      check_cuda(cudaEventRecord(c->pipe_ev[q], s), "cudaEventRecord(pipe)");
+      check_cuda(cudaStreamWaitEvent(c->copy_stream, c->pipe_ev[q], 0), "cudaStreamWaitEvent");
+      check_cuda(cudaMemcpyAsync(out + off, c->d_cycfull + 2 * off, dc.m * 16,
+                                 cudaMemcpyDeviceToHost, c->copy_stream), "cudaMemcpyAsync(arc D2H)");
+    }
+    off += dc.m;
+  }
+  tr.mark("arcs sorted + chained");
+  const std::uint64_t m = off;
+  DeviceCycle st;
+  device_cycle_stats(c->d_cycfull, m, len, c->d_hchain, s, &st);
+  c->launches += st.launches;
+  check_cuda(cudaStreamSynchronize(c->copy_stream), "hull copy");
+  tr.mark("hull D2H (pipelined)");
+  c->last_run.hull_path = 1;
+  if (m > 2 && !st.front_eq_back && !st.dups && !st.flat && st.bad == 0) {
+    const std::uint64_t b = st.best;
+    if (b != 0) {  // the hull starts elsewhere in the cycle: rotated from the device copy
+      copy_d2h(c, out, c->d_cycfull + 2 * b, (m - b) * 16, s);
+      copy_d2h(c, out + (m - b), c->d_cycfull, b * 16, s);
+    }
+    sink(m);
+    *h = m;
+    return true;
+  }
+  // the general clean-up on the host, from the copy already there
+  const PVec d = finalize_cycle(PVec(out, out + m));
+  *h = emit_host_hull(d, sink, false, s);
+  return true;
+}
+
 // The hull stage (reference hull.cpp:164-183) on survivors' coordinates
 // already packed on the device as [q1|q2|q3|q4] in index order; the hull
 // goes to sink.  Large sets: the arcs are built and sorted on the device
@@ -450,6 +544,10 @@ std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint
       off += counts[k];
     }
     return emit_host_hull(hull_from_queue_points(anchors, qp, counts), sink, dev, s);
+  }
+  if (!dev) {
+    std::size_t h = 0;
+    if (hull_pipelined(c, d_packed, counts, anchors, s, sink, &h)) return h;
   }
   const std::uint64_t arcs_n = total + 8;
   dev_grow(&c->d_hsort, &c->hsort_bytes, sort_arcs_work_bytes(counts) + arcs_n * 16,

@@ -108,6 +108,12 @@ struct ohx_ctx {
   void* h_packed = nullptr;  // pinned: a small survivor set's coordinates for the host hull
   std::uint64_t h_packed_bytes = 0;
   cudaEvent_t arc_ev[4] = {};  // their per-arc copies
+  // the pipelined hull stage: the whole cycle on the device, a copy stream
+  // and one event per arc
+  double* d_cycfull = nullptr;
+  std::uint64_t cycfull_bytes = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t pipe_ev[4] = {};
   unsigned long long* d_cnt = nullptr;
   unsigned long long* h_cnt = nullptr;  // pinned
 
@@ -189,6 +195,8 @@ inline void grow_gather(ohx_ctx* c, std::uint64_t bytes) {
   }
 }
 void host_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what);
+// page-locked (or registered) host memory: copies to / from it are direct DMA
+bool is_pinned(const void* h);
 // device -> host copy of a user buffer (pageable: through the pinned ring);
 // returns when the bytes have landed
 void copy_d2h(ohx_ctx* c, void* h, const void* d, std::uint64_t bytes, cudaStream_t s);

@@ -45,6 +45,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstring>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -68,6 +69,7 @@ __device__ __forceinline__ bool strict_left(double2 a, double2 b, double2 p) {
 struct ArcGeom {
   std::uint64_t aoff[4], len[4];
   std::uint32_t nch[4], choff[5];  // chunks per arc, first chunk of each arc
+  std::uint32_t c_lo, c_hi;        // the chunks a launch works on (all, or one arc's)
 };
 
 struct ChunkPos {
@@ -108,8 +110,8 @@ __global__ void __launch_bounds__(128) chain_local(const double2* __restrict__ i
                                                    ArcGeom g, ChunkState st) {
   __shared__ double2 tile[4][32][kCT + 1];  // per warp: 32 chunks x kCT (+1: 4-way banks)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const std::uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = c < g.choff[4];
+  const std::uint32_t c = g.c_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = c < g.c_hi;
   std::uint64_t b0 = 0;
   std::uint32_t len = 0;
   if (live) {
@@ -156,8 +158,8 @@ __global__ void __launch_bounds__(128) chain_local(const double2* __restrict__ i
 __global__ void __launch_bounds__(128) chain_replay(const double2* __restrict__ in,
                                                     const double2* __restrict__ loc, ArcGeom g,
                                                     ChunkState st) {
-  const std::uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= g.choff[4]) return;
+  const std::uint32_t c = g.c_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.c_hi) return;
   const ChunkPos p = chunk_pos(g, c);
   if (p.j == 0) {  // the arc's first chunk: its local run is the true run
     st.base[c] = 0;
@@ -228,8 +230,8 @@ __global__ void __launch_bounds__(128) chain_replay(const double2* __restrict__ 
 
 // slice lengths; *fail set when the chunk decomposition does not hold
 __global__ void chain_check(ArcGeom g, ChunkState st, int* fail) {
-  const std::uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= g.choff[4]) return;
+  const std::uint32_t c = g.c_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.c_hi) return;
   const ChunkPos p = chunk_pos(g, c);
   const bool last = p.j + 1 == g.nch[p.q];
   bool ok = st.synced[c] != 0;
@@ -251,7 +253,7 @@ __global__ void chain_check(ArcGeom g, ChunkState st, int* fail) {
 
 __global__ void __launch_bounds__(128) chain_copy(const double2* __restrict__ loc, ArcGeom g,
                                                   ChunkState st, double2* __restrict__ cycle) {
-  const std::uint32_t c = blockIdx.x;
+  const std::uint32_t c = g.c_lo + blockIdx.x;
   const ChunkPos p = chunk_pos(g, c);
   const double2* s = loc + p.b + st.base[c];
   double2* d = cycle + st.offs[c];
@@ -334,6 +336,8 @@ ArcGeom arc_geom(const std::uint64_t len[4]) {
     ch += g.nch[q];
   }
   g.choff[4] = ch;
+  g.c_lo = 0;
+  g.c_hi = ch;
   return g;
 }
 
@@ -399,17 +403,26 @@ ChainLayout chain_layout(const std::uint64_t len[4]) {
 
 }  // namespace
 
+static void cycle_stats_into(const double2* cycle, std::uint64_t m, CycStat* stat, void* tmp,
+                             std::size_t tmp_bytes, cudaStream_t s, DeviceCycle* out);
+
 std::size_t device_chain_work_bytes(const std::uint64_t len[4]) { return chain_layout(len).bytes; }
 
 bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_work,
-                   cudaStream_t s, DeviceCycle* out, double* direct, std::uint64_t direct_cap) {
-  const ChainLayout L = chain_layout(len);
+                   cudaStream_t s, DeviceCycle* out, double* direct, std::uint64_t direct_cap,
+                   int only_q) {
+  ChainLayout L = chain_layout(len);
+  if (only_q >= 0) {  // one arc's chain, alone, at the start of the cycle buffer
+    L.g.c_lo = L.g.choff[only_q];
+    L.g.c_hi = L.g.choff[only_q + 1];
+  }
+  const std::uint64_t need = only_q >= 0 ? len[only_q] : L.total;
   auto* w = static_cast<unsigned char*>(d_work);
   auto* loc = reinterpret_cast<double2*>(w + L.o_loc);
   // the cycle straight into the caller's device buffer when it can hold
   // every arc point (the hull is usually the cycle as is)
-  auto* cycle = direct != nullptr && direct_cap >= L.total ? reinterpret_cast<double2*>(direct)
-                                                           : reinterpret_cast<double2*>(w + L.o_cycle);
+  auto* cycle = direct != nullptr && direct_cap >= need ? reinterpret_cast<double2*>(direct)
+                                                        : reinterpret_cast<double2*>(w + L.o_cycle);
   ChunkState st;
   st.height = reinterpret_cast<std::uint32_t*>(w + L.o_h);
   st.low_rest = reinterpret_cast<std::uint32_t*>(w + L.o_lr);
@@ -424,7 +437,7 @@ bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_w
   int* flag = reinterpret_cast<int*>(w + L.o_flag);
   void* tmp = w + L.o_tmp;
   const auto* in = reinterpret_cast<const double2*>(d_sorted);
-  const std::uint32_t G = L.g.choff[4];
+  const std::uint32_t G = L.g.c_hi - L.g.c_lo;
   const unsigned blocks = (G + 127) / 128;
 
   check_cuda(cudaMemsetAsync(flag, 0, sizeof(int), s), "cudaMemsetAsync(chain flag)");
@@ -435,7 +448,8 @@ bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_w
   chain_check<<<blocks, 128, 0, s>>>(L.g, st, flag);
   check_cuda(cudaGetLastError(), "chain_check launch");
   std::size_t tb = L.tmp_bytes;
-  check_cuda(cub::DeviceScan::ExclusiveSum(tmp, tb, st.slice, st.offs, static_cast<int>(G), s),
+  check_cuda(cub::DeviceScan::ExclusiveSum(tmp, tb, st.slice + L.g.c_lo, st.offs + L.g.c_lo,
+                                           static_cast<int>(G), s),
              "cub::DeviceScan::ExclusiveSum(slices)");
   struct Head {
     int fail;
@@ -443,17 +457,18 @@ bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_w
     std::uint64_t last_off, last_len;
   };
   Head hd{};
-  check_cuda(cudaMemcpyAsync(&hd.fail, flag, sizeof(int), cudaMemcpyDeviceToHost, s),
-             "cudaMemcpyAsync(chain flag)");
-  check_cuda(cudaMemcpyAsync(&hd.last_off, st.offs + (G - 1), 8, cudaMemcpyDeviceToHost, s),
-             "cudaMemcpyAsync(cycle size)");
-  check_cuda(cudaMemcpyAsync(&hd.last_len, st.slice + (G - 1), 8, cudaMemcpyDeviceToHost, s),
-             "cudaMemcpyAsync(cycle size)");
+  const SmallRead rd[3] = {{flag, sizeof(int)},
+                           {st.offs + (L.g.c_hi - 1), 8},
+                           {st.slice + (L.g.c_hi - 1), 8}};
+  const unsigned char* hv = small_reads(rd, 3, s);
   // the copy runs regardless (harmless on failure: every slice length is
   // then whatever chain_check wrote, bounded by the chunk)
   chain_copy<<<G, 128, 0, s>>>(loc, L.g, st, cycle);
   check_cuda(cudaGetLastError(), "chain_copy launch");
   check_cuda(cudaStreamSynchronize(s), "device chains");
+  std::memcpy(&hd.fail, hv, sizeof(int));
+  std::memcpy(&hd.last_off, hv + 8, 8);
+  std::memcpy(&hd.last_len, hv + 16, 8);
   out->launches = 5;
   if (hd.fail) return false;
   const std::uint64_t m = hd.last_off + hd.last_len;
@@ -461,7 +476,15 @@ bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_w
   out->d_scratch = reinterpret_cast<double*>(w + L.o_cycle);
   out->m = m;
   out->chunks = G;
-  if (m == 0) return true;
+  if (m == 0 || only_q >= 0) return true;  // (one arc: no cycle statistics)
+  cycle_stats_into(cycle, m, stat, tmp, L.tmp_bytes, s, out);
+  return true;
+}
+
+// finalize_cycle's fast-path statistics of a cycle of m points (m >= 1)
+static void cycle_stats_into(const double2* cycle, std::uint64_t m, CycStat* stat, void* tmp,
+                             std::size_t tmp_bytes, cudaStream_t s, DeviceCycle* out) {
+  std::size_t tb;
   thrust::counting_iterator<std::uint64_t> it(0);
   thrust::transform_iterator<StatOf, thrust::counting_iterator<std::uint64_t>, CycStat> tin(
       it, StatOf{cycle, m});
@@ -469,26 +492,36 @@ bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_w
   init.bx = -INFINITY;
   init.by = INFINITY;
   init.bi = ~0ull;
-  tb = L.tmp_bytes;
+  tb = tmp_bytes;
   check_cuda(cub::DeviceReduce::Reduce(tmp, tb, tin, stat, static_cast<std::int64_t>(m),
                                        StatCombine{}, init, s),
              "cub::DeviceReduce::Reduce(cycle stats)");
   CycStat hs;
-  check_cuda(cudaMemcpyAsync(&hs, stat, sizeof(hs), cudaMemcpyDeviceToHost, s),
-             "cudaMemcpyAsync(cycle stats)");
   double2 ends[2];
-  check_cuda(cudaMemcpyAsync(&ends[0], cycle, 16, cudaMemcpyDeviceToHost, s),
-             "cudaMemcpyAsync(cycle front)");
-  check_cuda(cudaMemcpyAsync(&ends[1], cycle + (m - 1), 16, cudaMemcpyDeviceToHost, s),
-             "cudaMemcpyAsync(cycle back)");
+  static_assert(sizeof(CycStat) <= 64 && sizeof(CycStat) % 8 == 0, "small_reads slots");
+  const SmallRead rd[3] = {{stat, sizeof(CycStat)}, {cycle, 16}, {cycle + (m - 1), 16}};
+  const unsigned char* hv = small_reads(rd, 3, s);
   check_cuda(cudaStreamSynchronize(s), "cycle stats");
+  std::memcpy(&hs, hv, sizeof(hs));
+  std::memcpy(&ends[0], hv + sizeof(CycStat), 16);
+  std::memcpy(&ends[1], hv + sizeof(CycStat) + 16, 16);
   out->launches += 2;
   out->front_eq_back = ends[0].x == ends[1].x && ends[0].y == ends[1].y;
   out->dups = hs.dups != 0;
   out->flat = hs.notflat == 0;
   out->bad = hs.bad;
   out->best = hs.bi;
-  return true;
+}
+
+void device_cycle_stats(const double* d_cycle, std::uint64_t m, const std::uint64_t len[4],
+                        void* d_work, cudaStream_t s, DeviceCycle* out) {
+  const ChainLayout L = chain_layout(len);
+  auto* w = static_cast<unsigned char*>(d_work);
+  out->d_cycle = const_cast<double*>(d_cycle);
+  out->m = m;
+  if (m == 0) return;
+  cycle_stats_into(reinterpret_cast<const double2*>(d_cycle), m,
+                   reinterpret_cast<CycStat*>(w + L.o_stat), w + L.o_tmp, L.tmp_bytes, s, out);
 }
 
 }  // namespace ohx

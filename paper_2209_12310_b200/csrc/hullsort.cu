@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 #include <cub/block/block_merge_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda/std/tuple>
@@ -200,11 +201,12 @@ struct ArcSrc {
   }
 };
 
+// (kernels of this tier work on the elements [lo, hi): all four arcs, or one)
 __global__ void linear_keys(const ArcSrc A, std::uint32_t* __restrict__ keys,
-                            std::uint32_t* __restrict__ vals) {
+                            std::uint32_t* __restrict__ vals, std::uint64_t lo, std::uint64_t hi) {
   const double xE = A.anchors[0].x, yN = A.anchors[1].y, xW = A.anchors[2].x, yS = A.anchors[3].y;
   const double sx = __dsub_rn(xE, xW), sy = __dsub_rn(yN, yS);
-  for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < A.total;
+  for (std::uint64_t k = lo + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < hi;
        k += std::uint64_t(gridDim.x) * blockDim.x) {
     const int q = A.arc_of(k);
     const std::uint64_t j = k - A.begin(q);
@@ -281,12 +283,14 @@ __device__ __forceinline__ void fix_run_at(const std::uint32_t* __restrict__ key
 // 16-byte load; keys 16-byte aligned), the neighbours across lanes by
 // shuffle; only run starts do any work.
 __global__ void fix_runs(const std::uint32_t* __restrict__ keys, double2* out, const ArcSrc A,
-                         uint2* runs, unsigned* nruns, int* flag) {
+                         uint2* runs, unsigned* nruns, int* flag, std::uint64_t lo,
+                         std::uint64_t hi) {
   const int lane = threadIdx.x & 31;
   const std::uint64_t nwarps = std::uint64_t(gridDim.x) * (blockDim.x / 32);
   const std::uint64_t n = A.total;
-  for (std::uint64_t w0 = (std::uint64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 128;
-       w0 < n; w0 += nwarps * 128) {
+  for (std::uint64_t w0 = lo / 128 * 128 +
+                          (std::uint64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 128;
+       w0 < hi; w0 += nwarps * 128) {
     const std::uint64_t i0 = w0 + 4 * lane;
     std::uint32_t k[4];
     if (i0 + 3 < n) {
@@ -306,7 +310,8 @@ __global__ void fix_runs(const std::uint32_t* __restrict__ keys, double2* out, c
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const std::uint64_t i = i0 + e;
-      if (i >= n) break;
+      if (i >= hi) break;
+      if (i < lo) continue;
       fix_run_at(keys, out, A, i, k[e], e == 0 ? prev : k[e - 1], e == 3 ? next : k[e + 1], runs,
                  nruns, flag);
     }
@@ -346,8 +351,8 @@ __global__ void __launch_bounds__(kRunThreads)
 }
 
 __global__ void gather_arcs(const ArcSrc A, const std::uint32_t* __restrict__ vals,
-                            double2* __restrict__ out) {
-  for (std::uint64_t k = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < A.total;
+                            double2* __restrict__ out, std::uint64_t lo, std::uint64_t hi) {
+  for (std::uint64_t k = lo + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < hi;
        k += std::uint64_t(gridDim.x) * blockDim.x)
     out[k] = A.point(A.arc_of(k), vals[k]);
 }
@@ -413,7 +418,7 @@ std::size_t sort_arcs_work_bytes(const std::uint64_t counts[4]) {
 }
 
 void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const double anchors[8],
-               void* d_work, double* d_sorted, cudaStream_t s) {
+               void* d_work, double* d_sorted, cudaStream_t s, int only_q) {
   const ArcLayout L = arc_layout(counts);
   if (L.total >= (1ull << 32)) throw Error(OHX_E_INVALID, "sort_arcs: > 2^32 survivors");
   std::uint64_t mx = 0;
@@ -444,10 +449,16 @@ void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const doub
     auto* runs = reinterpret_cast<uint2*>(k0);
     auto* nruns = reinterpret_cast<unsigned*>(d_flag + 1);
     const ArcSrc A{reinterpret_cast<const double2*>(d_packed), d_anchors, L.qoff, L.aoff, L.total};
-    linear_keys<<<grid, 256, 0, s>>>(A, q0, v1);
+    // one arc (only_q) or all four
+    const std::uint64_t lo = only_q >= 0 ? ao[only_q] : 0;
+    const std::uint64_t hi = only_q >= 0 ? lo + L.len[only_q] : L.total;
+    const unsigned g1 = static_cast<unsigned>(
+        hi - lo < 148ull * 2048 ? (hi - lo + 255) / 256 : 148 * 8);
+    linear_keys<<<g1, 256, 0, s>>>(A, q0, v1, lo, hi);
     check_cuda(cudaGetLastError(), "linear_keys launch");
-    int lsel[4];
+    int lsel[4] = {0, 0, 0, 0};
     for (int q = 0; q < 4; ++q) {
+      if (only_q >= 0 && q != only_q) continue;
       cub::DoubleBuffer<std::uint32_t> kb(q0 + ao[q], q1 + ao[q]);
       cub::DoubleBuffer<std::uint32_t> vb(v1 + ao[q], v0 + ao[q]);
       std::size_t tb = tmp_bytes;
@@ -456,9 +467,10 @@ void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const doub
                  "cub::DeviceRadixSort::SortPairs(u32)");
       lsel[q] = kb.selector;
     }
-    std::uint32_t* lkeys = lsel[0] ? q1 : q0;
-    std::uint32_t* lvals = lsel[0] ? v0 : v1;
-    for (int q = 1; q < 4; ++q)
+    const int q_ref = only_q >= 0 ? only_q : 0;
+    std::uint32_t* lkeys = lsel[q_ref] ? q1 : q0;
+    std::uint32_t* lvals = lsel[q_ref] ? v0 : v1;
+    for (int q = 1; q < 4 && only_q < 0; ++q)
       if (lsel[q] != lsel[0]) {
         check_cuda(cudaMemcpyAsync(lkeys + ao[q], (lsel[q] ? q1 : q0) + ao[q], L.len[q] * 4,
                                    cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync(sorted keys)");
@@ -467,17 +479,18 @@ void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const doub
       }
     // the points in key order, then the runs of equal keys in full order
     auto* out = reinterpret_cast<double2*>(d_sorted);
-    gather_arcs<<<grid, 256, 0, s>>>(A, lvals, out);
+    gather_arcs<<<g1, 256, 0, s>>>(A, lvals, out, lo, hi);
     check_cuda(cudaGetLastError(), "gather_arcs launch");
     check_cuda(cudaMemsetAsync(d_flag, 0, 2 * sizeof(int), s), "cudaMemsetAsync(flag)");
-    fix_runs<<<grid, 256, 0, s>>>(lkeys, out, A, runs, nruns, d_flag);
+    fix_runs<<<g1, 256, 0, s>>>(lkeys, out, A, runs, nruns, d_flag, lo, hi);
     check_cuda(cudaGetLastError(), "fix_runs launch");
     sort_runs<<<kRunCap, kRunThreads, 0, s>>>(runs, nruns, out, A);
     check_cuda(cudaGetLastError(), "sort_runs launch");
     int too_long = 0;
-    check_cuda(cudaMemcpyAsync(&too_long, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s),
-               "cudaMemcpyAsync(flag)");
+    const SmallRead rd{d_flag, sizeof(int)};
+    const unsigned char* hv = small_reads(&rd, 1, s);
     check_cuda(cudaStreamSynchronize(s), "hull sort runs");
+    std::memcpy(&too_long, hv, sizeof(int));
     if (!too_long) return;
   }
   // the arcs materialised for the tiers below
@@ -513,9 +526,10 @@ void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const doub
   repair_ties<<<grid, 256, 0, s>>>(keys, vals, arcs, L.aoff, L.total, d_flag);
   check_cuda(cudaGetLastError(), "repair_ties launch");
   int long_run = 0;
-  check_cuda(cudaMemcpyAsync(&long_run, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s),
-             "cudaMemcpyAsync(flag)");
+  const SmallRead rd{d_flag, sizeof(int)};
+  const unsigned char* hv = small_reads(&rd, 1, s);
   check_cuda(cudaStreamSynchronize(s), "hull sort ties");
+  std::memcpy(&long_run, hv, sizeof(int));
   if (long_run) {  // degenerate arcs: the full 128-bit key sort
     build_arc_keys<<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(d_packed), L.qoff,
                                         L.aoff, L.total, d_anchors, arcs, k0, v0);

@@ -275,8 +275,10 @@ PVec chain_arcs(const P2* const arcs[4], const std::uint64_t len[4],
 // sorted in its quadrant's sweep order, written back to back to d_sorted
 // (sum(counts) + 8 points).
 std::size_t sort_arcs_work_bytes(const std::uint64_t counts[4]);
+// only_q >= 0: arc only_q is the one that must come out sorted (the others
+// may or may not be; the layout is the same).
 void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const double anchors[8],
-               void* d_work, double* d_sorted, cudaStream_t s);
+               void* d_work, double* d_sorted, cudaStream_t s, int only_q = -1);
 // The chains and the cycle scan on the device (hullchain.cu) over the sorted
 // arcs (the layout sort_arcs writes; len[q] = counts[q] + 2).  false: the
 // chunked replay could not prove every chunk (the host chains must run);
@@ -293,9 +295,25 @@ struct DeviceCycle {
 std::size_t device_chain_work_bytes(const std::uint64_t len[4]);
 // direct (nullable): the caller's device output; the cycle is written there
 // when direct_cap covers every arc point.
+// Small device -> host reads that must not queue behind a bulk copy on the
+// copy engine (the pipelined hull stage streams the hull to the host while
+// the next arc is sorted and chained): one kernel stores up to 8 values
+// (<= 64 bytes each) into mapped pinned memory; the returned host view, the
+// values at 8-byte aligned offsets in order, is valid once s is
+// synchronised (until the calling thread's next small_reads).
+struct SmallRead {
+  const void* src;
+  std::uint32_t bytes;
+};
+const unsigned char* small_reads(const SmallRead* r, int k, cudaStream_t s);
+// The cycle statistics alone, for a cycle of m points assembled elsewhere
+// (d_work: a device_chain_work_bytes(len) area; out->d_cycle / m set too).
+void device_cycle_stats(const double* d_cycle, std::uint64_t m, const std::uint64_t len[4],
+                        void* d_work, cudaStream_t s, DeviceCycle* out);
+// only_q >= 0: arc only_q's chain alone (its chunks only; no statistics).
 bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_work,
                    cudaStream_t s, DeviceCycle* out, double* direct = nullptr,
-                   std::uint64_t direct_cap = 0);
+                   std::uint64_t direct_cap = 0, int only_q = -1);
 // hull stage from the four arcs [anchor q, queue q, anchor q+1] already in
 // sweep order (device-sorted)
 // (wait_arc(q), when set, is called by arc q's thread before it reads the

@@ -2000,4 +2000,53 @@ void launch_gather(const double* d_xy, const void* d_idx, int idx_bytes,
   check_cuda(cudaGetLastError(), "gather_xy launch");
 }
 
+// ---- small reads through mapped memory (see internal.hpp)
+namespace {
+struct SmallReadArgs {
+  const unsigned char* src[8];
+  std::uint32_t bytes[8], off[8];
+  int k;
+};
+__global__ void small_reads_k(SmallReadArgs a, unsigned char* dst) {
+  const int i = threadIdx.x;
+  if (i >= a.k) return;
+  for (std::uint32_t b = 0; b < a.bytes[i]; ++b) dst[a.off[i] + b] = a.src[i][b];
+}
+}  // namespace
+
+const unsigned char* small_reads(const SmallRead* r, int k, cudaStream_t s) {
+  if (k < 1 || k > 8) throw Error(OHX_E_INTERNAL, "small_reads: 1..8 values");
+  struct Buf {
+    unsigned char* h = nullptr;
+    unsigned char* d = nullptr;
+    ~Buf() {
+      if (h) cudaFreeHost(h);
+    }
+  };
+  thread_local Buf buf;
+  if (!buf.h) {
+    void* p = nullptr;
+    check_cuda(cudaHostAlloc(&p, 1024, cudaHostAllocMapped | cudaHostAllocPortable),
+               "cudaHostAlloc(small reads)");
+    buf.h = static_cast<unsigned char*>(p);
+    void* d = nullptr;
+    check_cuda(cudaHostGetDevicePointer(&d, p, 0), "cudaHostGetDevicePointer");
+    buf.d = static_cast<unsigned char*>(d);
+  }
+  SmallReadArgs a{};
+  std::uint32_t off = 0;
+  for (int i = 0; i < k; ++i) {
+    if (r[i].bytes > 64) throw Error(OHX_E_INTERNAL, "small_reads: a value over 64 bytes");
+    a.src[i] = static_cast<const unsigned char*>(r[i].src);
+    a.bytes[i] = r[i].bytes;
+    a.off[i] = off;
+    off += (r[i].bytes + 7) / 8 * 8;
+  }
+  a.k = k;
+  small_reads_k<<<1, 32, 0, s>>>(a, buf.d);
+  check_cuda(cudaGetLastError(), "small_reads launch");
+  return buf.h;
+}
+
 }  // namespace ohx
+

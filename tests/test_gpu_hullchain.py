@@ -288,3 +288,43 @@ def test_device_hull_rotated_into_caller_buffer():
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=600)
     assert r.returncode == 0 and "rotated ok" in r.stdout, r.stdout + r.stderr[-3000:]
+
+
+PIPE_OUT_SCRIPT = r"""
+import sys
+sys.path.insert(0, ROOT_DIR)
+import numpy as np, torch, paper_2209_12310_b200 as P
+from oracle import Oracle
+o = Oracle()
+ctx = P.Context(0)
+cases = []
+pts = P.generate("circle", 5_000_000, 9)
+cases.append(("circle", pts, "device-chains"))
+e = int(np.argmax(pts[:, 0]))
+extra = np.array([[pts[e, 0], pts[e, 1] - 1e-7]])  # the hull starts mid-cycle: a rotation
+cases.append(("circle, rotated", np.ascontiguousarray(np.concatenate([pts, extra])), "device-chains"))
+cases.append(("disk", P.generate("disk", 40_000_000, 3), None))  # chains unproven: regular stage
+for name, pts, want_path in cases:
+    n = len(pts)
+    dx = torch.from_numpy(pts).cuda()
+    out = torch.empty((n + 8, 2), dtype=torch.float64, pin_memory=True)
+    hull, _ = ctx.heaphull_device(dx, n, out=out)
+    info = ctx.last_run()
+    want = o.heaphull(pts)
+    assert np.array_equal(hull, want), (name, info)
+    assert want_path is None or info["hull_path"] == want_path, (name, info)
+    print(name, n, info["hull_path"], len(hull))
+print("pipe ok")
+"""
+
+
+@pytest.mark.parametrize("pipe", ["1", "0"])
+def test_pipelined_hull_stage_to_pinned_host_memory(pipe):
+    # a large survivor set with the hull going to pinned host memory: arcs
+    # sorted and chained one at a time, each arc's chain copied to the host
+    # behind the next arc's work (OHX_HULL_PIPE=0: the regular stage)
+    env = dict(os.environ, OHX_HULL_PIPE=pipe)
+    code = PIPE_OUT_SCRIPT.replace("ROOT_DIR", repr(ROOT))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=900)
+    assert r.returncode == 0 and "pipe ok" in r.stdout, r.stdout + r.stderr[-3000:]
