@@ -434,7 +434,14 @@ bool hull_pipe_mode() {
   }();
   return v;
 }
-constexpr std::uint64_t kPipeMin = 1u << 22;  // survivors from which pipelining pays
+// survivors from which pipelining pays (OHX_HULL_PIPE_MIN overrides; test hook)
+std::uint64_t pipe_min() {
+  static const std::uint64_t v = [] {
+    const char* e = std::getenv("OHX_HULL_PIPE_MIN");
+    return e && *e ? static_cast<std::uint64_t>(std::atoll(e)) : std::uint64_t(1) << 22;
+  }();
+  return v;
+}
 
 // The hull stage of a large survivor set whose hull goes to PINNED host
 // memory, arc by arc: each arc is sorted and chained on the device and its
@@ -448,7 +455,7 @@ constexpr std::uint64_t kPipeMin = 1u << 22;  // survivors from which pipelining
 bool hull_pipelined(ohx_ctx* c, const double* d_packed, const std::uint64_t counts[4],
                     const P2 anchors[4], cudaStream_t s, const HullSink& sink, std::size_t* h) {
   const std::uint64_t total = counts[0] + counts[1] + counts[2] + counts[3];
-  if (total < kPipeMin || !hull_pipe_mode() || !device_chain_mode()) return false;
+  if (total < pipe_min() || !hull_pipe_mode() || !device_chain_mode()) return false;
   const std::uint64_t arcs_n = total + 8;
   P2* out = nullptr;
   try {

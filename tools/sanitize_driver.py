@@ -7,7 +7,9 @@ two-pass K1 + K2 (+ labels) on normal 200k, K1b on a circle (the corner
 certificate fails there), the fused pass (sample K1, count, KF, kf_gather,
 candidate K1, K2 gather mode) on normal 9M, the device sweep sort + hull
 indices on a 300k circle, the K2 look-back across many tile groups
-(normal 3M two-pass with labels), the PTS2 loader's non-finite scan.
+(normal 3M two-pass with labels), the PTS2 loader's non-finite scan; the
+hull into a device buffer (in place) and into pinned host memory (the
+pipelined stage: OHX_HULL_PIPE_MIN lowered for the 300k circle).
 Every result is checked against the oracle, so a sanitizer run is also a
 parity run."""
 import os
@@ -16,6 +18,7 @@ import tempfile
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("OHX_DEVICE_SORT_MIN", "100000")
+os.environ.setdefault("OHX_HULL_PIPE_MIN", "100000")  # the pipelined stage on the 300k circle
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
@@ -52,6 +55,9 @@ for k, (dist, n, seed, dd) in enumerate(cases):
     assert (idx >= 0).all()
     dh, _ = ctx.heaphull_device(d, n, out="device")  # the hull left on the device
     assert np.array_equal(dh.cpu().numpy(), hull), (dist, n)
+    pin = torch.empty((n + 8, 2), dtype=torch.float64, pin_memory=True)
+    ph, _ = ctx.heaphull_device(d, n, out=pin)  # pinned host output (pipelined when large)
+    assert np.array_equal(ph, hull), (dist, n)
     print(f"case {k} {dist} {n}: pipeline ok, fused {info['fused']}, hull path "
           f"{info['hull_path']}, h {len(hull)}", flush=True)
 if not which or "pts2" in which:
