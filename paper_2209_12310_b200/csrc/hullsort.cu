@@ -5,22 +5,27 @@
 // [anchor q, queue q..., anchor q+1] by its CCW sweep order, then runs the
 // strict-left-turn chain.  For large survivor sets the sort dominates
 // (circle 1e8: 4 x 25M points, ~0.85 s each on 16 host cores), so the arcs
-// are built and sorted here and come back to the host already in sweep
-// order; the chain and the cycle clean-up stay on the host (their
-// decisions are the reference's predicate sequence).  The sort runs on the
-// 64-bit primary key (half the radix passes of the full 128-bit key); runs
-// of equal primary key are then ordered by the secondary key (repair_ties),
-// and arcs with runs longer than 64 fall back to the 128-bit sort.
+// are sorted here, in three tiers (the first that holds):
+//   1. a 32-bit key monotone in the primary coordinate (its position in the
+//      input's bounding box, square-rooted; see linear_keys), 4 radix
+//      passes, the points gathered in key order straight from the packed
+//      survivors, runs of equal keys put in the full comparator order;
+//   2. the 64-bit primary key (half the radix passes of the full 128-bit
+//      key), runs of equal primary key ordered by the secondary key
+//      (repair_ties, runs up to 64);
+//   3. the full 128-bit (primary, secondary) key.
+// One arc can be sorted alone (the pipelined hull stage).  The chains and
+// the cycle statistics follow in hullchain.cu.
 //
-// Keys: each coordinate maps to an order-preserving u64 (negative values
-// bit-complemented, others with the sign bit set); a descending component
-// is complemented once more.  -0.0 is folded onto +0.0 first, because the
-// reference's comparator treats them as equal (a.x != b.x is false).  The
-// sort is an LSD radix sort over the 128-bit (primary, secondary) key with a
-// u32 payload (the element's position), then the points are gathered.
-// Points equal under the comparator may come out in any order -- the
-// reference's std::sort is not stable either, and such points only differ
-// in the sign of a zero coordinate.
+// Keys of tiers 2-3: each coordinate maps to an order-preserving u64
+// (negative values bit-complemented, others with the sign bit set); a
+// descending component is complemented once more.  -0.0 is folded onto
+// +0.0 first, because the reference's comparator treats them as equal
+// (a.x != b.x is false).  LSD radix sorts with a u32 payload (the element's
+// position), then the points are gathered.  Points equal under the
+// comparator may come out in any order -- the reference's std::sort is not
+// stable either, and such points only differ in the sign of a zero
+// coordinate.
 #include <cuda_runtime.h>
 
 #include <cstdint>
