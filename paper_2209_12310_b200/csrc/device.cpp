@@ -457,13 +457,9 @@ bool hull_pipelined(ohx_ctx* c, const double* d_packed, const std::uint64_t coun
   const std::uint64_t total = counts[0] + counts[1] + counts[2] + counts[3];
   if (total < pipe_min() || !hull_pipe_mode() || !device_chain_mode()) return false;
   const std::uint64_t arcs_n = total + 8;
-  P2* out = nullptr;
-  try {
-    out = sink(arcs_n);  // room for every arc point (the regular path otherwise)
-  } catch (const std::exception&) {
-    return false;
-  }
-  if (!is_pinned(out)) return false;
+  // a C-ABI call's page-locked output with room for every arc point
+  if (c->host_out == nullptr || c->host_out_cap < arcs_n || !is_pinned(c->host_out)) return false;
+  auto* out = reinterpret_cast<P2*>(c->host_out);
   Trace tr;
   dev_grow(&c->d_hsort, &c->hsort_bytes, sort_arcs_work_bytes(counts) + arcs_n * 16,
            "hull sort work");

@@ -68,6 +68,10 @@ struct ohx_ctx {
   // device hull stage writes its cycle there directly
   double* dev_out = nullptr;
   std::uint64_t dev_out_cap = 0;
+  // ... and a C-ABI call's host output buffer: the pipelined hull stage
+  // streams the hull into it when it is page-locked
+  double* host_out = nullptr;
+  std::uint64_t host_out_cap = 0;
   // one-pass K2: its self-clearing work words and the small block it
   // returns (the first survivors' coordinates + the counts)
   void* d_k2op = nullptr;

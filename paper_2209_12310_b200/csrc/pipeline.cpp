@@ -35,6 +35,26 @@ void copy_hull(const std::vector<octohull::Point2D>& v, double* out, std::uint64
                    v.size());
 }
 
+// The caller's output buffer, visible to the hull stage for one call: a
+// device buffer (the cycle is chained straight into it) or a host buffer
+// (page-locked: the pipelined stage streams the hull into it).
+struct OutScope {
+  ohx_ctx* c;
+  OutScope(ohx_ctx* c_, double* p, std::uint64_t cap, bool device) : c(c_) {
+    if (device) {
+      c->dev_out = p;
+      c->dev_out_cap = cap;
+    } else {  // (whether it is page-locked is asked only when it matters)
+      c->host_out = p;
+      c->host_out_cap = cap;
+    }
+  }
+  ~OutScope() {
+    c->dev_out = c->host_out = nullptr;
+    c->dev_out_cap = c->host_out_cap = 0;
+  }
+};
+
 // the caller's hull buffer as the hull stage's sink (capacity checked, the
 // size reported either way)
 ohx::HullSink hull_sink(double* h_hull, std::uint64_t cap, std::uint64_t* h) {
@@ -74,6 +94,7 @@ int ohx_heaphull(const double* h_xy, uint64_t n, double* h_hull, uint64_t cap, u
     const double* d_xy = ohx::stage_points(ctx, h_xy, n, s);
     const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
     const auto t1 = Clock::now();
+    const OutScope os(ctx, h_hull, cap, false);
     ohx::device_queues_hull(ctx, f, s, hull_sink(h_hull, cap, h));
     if (timings) {
       timings[0] = ms(t0, t1);
@@ -94,6 +115,7 @@ int ohx_heaphull_device(ohx_ctx* ctx, const double* d_xy, uint64_t n, double* h_
     const auto t0 = Clock::now();
     const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
     const auto t1 = Clock::now();
+    const OutScope os(ctx, h_hull, cap, false);
     ohx::device_queues_hull(ctx, f, s, hull_sink(h_hull, cap, h));
     const auto t2 = Clock::now();
     if (timings) {
@@ -115,17 +137,7 @@ int ohx_heaphull_device_out(ohx_ctx* ctx, const double* d_xy, uint64_t n, double
     const auto t0 = Clock::now();
     const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
     const auto t1 = Clock::now();
-    struct DevOut {  // the caller's buffer, visible to the hull stage for this call only
-      ohx_ctx* c;
-      DevOut(ohx_ctx* c_, double* p, std::uint64_t k) : c(c_) {
-        c->dev_out = p;
-        c->dev_out_cap = k;
-      }
-      ~DevOut() {
-        c->dev_out = nullptr;
-        c->dev_out_cap = 0;
-      }
-    } dev_out(ctx, d_hull, cap);
+    const OutScope os(ctx, d_hull, cap, true);
     ohx::device_queues_hull(ctx, f, s, hull_sink(d_hull, cap, h), true);
     const auto t2 = Clock::now();
     if (timings) {
@@ -152,6 +164,7 @@ int ohx_heaphull_pts2(const char* path, double* h_hull, uint64_t cap, uint64_t* 
     const auto tl = Clock::now();
     const ohx::FilterOut f = ohx::device_filter(ctx, d_xy, n, nullptr, s);
     const auto t1 = Clock::now();
+    const OutScope os(ctx, h_hull, cap, false);
     ohx::device_queues_hull(ctx, f, s, hull_sink(h_hull, cap, h));
     if (timings) {
       timings[0] = ms(tl, t1);
