@@ -257,9 +257,10 @@ __device__ __forceinline__ void fix_run_at(const std::uint32_t* __restrict__ key
                                            const ArcSrc& A, std::uint64_t i, std::uint32_t key,
                                            std::uint32_t prev, std::uint32_t next, uint2* runs,
                                            unsigned* nruns, int* flag) {
+  if (next != key) return;  // (nearly every element: no arc arithmetic)
   const int q = A.arc_of(i);
   const std::uint64_t a0 = A.begin(q), a1 = A.end(q);
-  if (i + 1 >= a1 || next != key || (i > a0 && prev == key)) return;  // not a run start
+  if (i + 1 >= a1 || (i > a0 && prev == key)) return;  // not a run start
   std::uint64_t j = i + 2;
   while (j < a1 && keys[j] == key && j - i <= kRunMax) ++j;
   const std::uint64_t len = j - i;
