@@ -328,3 +328,34 @@ def test_pipelined_hull_stage_to_pinned_host_memory(pipe):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=900)
     assert r.returncode == 0 and "pipe ok" in r.stdout, r.stdout + r.stderr[-3000:]
+
+
+PIPE_DEGEN_SCRIPT = r"""
+import sys
+sys.path.insert(0, ROOT_DIR)
+import numpy as np, torch, paper_2209_12310_b200 as P
+from oracle import Oracle
+o = Oracle()
+ctx = P.Context(0)
+rng = np.random.default_rng(5)
+for scale in (1000.0, 3e4, 1e7):
+    t = rng.uniform(0, 2 * np.pi, 1_300_000)
+    pts = np.ascontiguousarray(np.round(np.stack([np.cos(t), np.sin(t)], 1) * scale))
+    n = len(pts)
+    out = torch.empty((n + 8, 2), dtype=torch.float64, pin_memory=True)
+    hull, _ = ctx.heaphull_device(torch.from_numpy(pts).cuda(), n, out=out)
+    assert np.array_equal(hull, o.heaphull(pts)), (scale, ctx.last_run())
+    print(scale, ctx.last_run()["hull_path"], len(hull))
+print("degenerate pipe ok")
+"""
+
+
+def test_pipelined_hull_stage_on_degenerate_survivors():
+    # duplicates, collinear runs and -0.0 through the pipelined stage (its
+    # threshold lowered): the cycle statistics send these to the host
+    # clean-up, from the copy already in the caller's buffer
+    env = dict(os.environ, OHX_DEVICE_SORT_MIN="100000", OHX_HULL_PIPE_MIN="100000")
+    code = PIPE_DEGEN_SCRIPT.replace("ROOT_DIR", repr(ROOT))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=900)
+    assert r.returncode == 0 and "degenerate pipe ok" in r.stdout, r.stdout + r.stderr[-3000:]
