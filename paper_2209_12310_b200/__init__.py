@@ -380,17 +380,17 @@ class Context:
             if host.dtype != np.float64 or not host.flags.c_contiguous or host.size % 2:
                 raise ValueError("out: a C-contiguous float64 (cap, 2) host buffer")
             h = C.c_uint64(0)
-            t = np.zeros(4, dtype=np.float64)
+            t = (C.c_double * 4)()
             check(lib.ohx_heaphull_device(self.h, _ptr(d_xy), n, host.ctypes.data_as(_dp),
-                                          host.size // 2, C.byref(h), t.ctypes.data_as(_dp)))
+                                          host.size // 2, C.byref(h), t))
             return host.reshape(-1, 2)[: h.value], dict(filter_ms=t[0], hull_ms=t[1],
                                                        total_ms=t[2])
         if not isinstance(out, str):  # a caller's device buffer
             cap = out.numel() // 2
             h = C.c_uint64(0)
-            t = np.zeros(4, dtype=np.float64)
+            t = (C.c_double * 4)()
             check(lib.ohx_heaphull_device_out(self.h, _ptr(d_xy), n, _ptr(out), cap, C.byref(h),
-                                              t.ctypes.data_as(_dp)))
+                                              t))
             return out.view(-1, 2)[: h.value], dict(filter_ms=t[0], hull_ms=t[1], total_ms=t[2])
         if out == "device":
             import torch
@@ -398,9 +398,9 @@ class Context:
             while True:
                 hull = torch.empty((cap, 2), dtype=torch.float64, device=f"cuda:{self.device}")
                 h = C.c_uint64(0)
-                t = np.zeros(4, dtype=np.float64)
+                t = (C.c_double * 4)()
                 rc = lib.ohx_heaphull_device_out(self.h, _ptr(d_xy), n, _ptr(hull), cap,
-                                                 C.byref(h), t.ctypes.data_as(_dp))
+                                                 C.byref(h), t)
                 if rc == OHX_E_INVALID and h.value > cap:
                     cap = h.value
                     continue
@@ -414,20 +414,24 @@ class Context:
         # vertices); a larger hull is returned in it (the buffer goes with it)
         cap = n + 8 if n <= (1 << 28) else 1 << 24
         while True:
-            hull = self._hbuf if self._hbuf is not None and len(self._hbuf) >= cap else None
-            if hull is None:
+            # the scratch is kept with its ctypes pointer (numpy's .ctypes
+            # costs microseconds per call on a 2.5 ms step)
+            hb = self._hbuf
+            if hb is not None and len(hb[0]) >= cap:
+                hull, hptr = hb
+            else:
                 hull = np.empty((cap, 2), dtype=np.float64)
+                hptr = hull.ctypes.data_as(_dp)
             self._hbuf = None
             h = C.c_uint64(0)
-            t = np.zeros(4, dtype=np.float64)
-            rc = lib.ohx_heaphull_device(self.h, _ptr(d_xy), n, hull.ctypes.data_as(_dp),
-                                         len(hull), C.byref(h), t.ctypes.data_as(_dp))
+            t = (C.c_double * 4)()
+            rc = lib.ohx_heaphull_device(self.h, _ptr(d_xy), n, hptr, len(hull), C.byref(h), t)
             if rc == OHX_E_INVALID and h.value > len(hull):  # the hull outgrew the buffer
                 cap = h.value
                 continue
             check(rc)
             if h.value < (1 << 20):
-                self._hbuf = hull
+                self._hbuf = (hull, hptr)
                 out = hull[: h.value].copy()
             else:
                 out = hull[: h.value]

@@ -195,7 +195,7 @@ bool dev_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* wha
 inline void grow_gather(ohx_ctx* c, std::uint64_t bytes) {
   if (dev_grow(reinterpret_cast<void**>(&c->d_gather), &c->gather_bytes, bytes, "gather")) {
     c->spec_zeroed = false;
-      c->qxy_valid = false;
+    c->qxy_valid = false;
   }
 }
 void host_grow(void** p, std::uint64_t* have, std::uint64_t need, const char* what);
