@@ -612,6 +612,25 @@ std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint
   return h;
 }
 
+std::size_t hull_from_host_packed(ohx_ctx* c, const P2* h_packed, const std::uint64_t counts[4],
+                                  const P2 anchors[4], cudaStream_t s, const HullSink& sink) {
+  const std::uint64_t total = counts[0] + counts[1] + counts[2] + counts[3];
+  if (total >= device_sort_min()) {  // (the same stage as the device-resident survivors)
+    grow_gather(c, total * 16);
+    c->qxy_valid = false;
+    check_cuda(cudaMemcpyAsync(c->d_gather, h_packed, total * 16, cudaMemcpyHostToDevice, s),
+               "cudaMemcpyAsync(survivors H2D)");
+    return hull_from_packed(c, c->d_gather, counts, anchors, s, sink);
+  }
+  const P2* qp[4];
+  std::uint64_t off = 0;
+  for (int k = 0; k < 4; ++k) {
+    qp[k] = h_packed + off;
+    off += counts[k];
+  }
+  return emit_host_hull(hull_from_queue_points(anchors, qp, counts), sink, false, s);
+}
+
 std::size_t device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s,
                                const HullSink& sink, bool dev) {
   // reference hull.cpp:164-183 on the device queues of the last filter

@@ -15,8 +15,11 @@
 //   4. build_octagon + plan on the host (identical on every rank)
 //   5. K2 per shard (candidates only when the shard's fused region is
 //      certified against the global octagon)
-//   6. the shard's survivors' coordinates packed on its device, [q1..q4]
-//   7. ncclAllGather of the per-rank queue lengths
+//   6. ncclAllGather of one fixed-size block per rank: its queue lengths
+//      and, when they fit (up to kMgBlock, already on the host with the K2
+//      counts), its survivors' coordinates [q1..q4]; if every rank's fit,
+//      the root runs the host hull stage on them and the call ends here
+//   7. else: the shard's survivors' coordinates packed on its device
 //   8. survivors to the root only: each queue of each rank is one
 //      ncclSend / ncclRecv straight into its place in the root's
 //      [Q1|Q2|Q3|Q4] buffer (rank order = global index order, so the
@@ -109,6 +112,10 @@ struct Nccl {
   }
 };
 
+// survivors per rank that travel inside the fixed-size exchange block
+// (step 6): 16 KB per rank, the whole survivor set of a normal corpus
+constexpr std::uint64_t kMgBlock = 1024;
+
 void check_nccl(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return;
   throw Error(OHX_E_CUDA, std::string(what) + ": " + Nccl::get().GetErrorString(r));
@@ -137,6 +144,10 @@ struct ohx_mg_rank {
   std::uint64_t pack_bytes = 0;
   void* d_recv = nullptr;        // root: the job's survivors, [Q1|Q2|Q3|Q4]
   std::uint64_t recv_bytes = 0;
+  void* h_blk = nullptr;         // pinned: this rank's block, then every rank's
+  std::uint64_t hblk_bytes = 0;
+  void* h_job = nullptr;         // pinned, root: small job survivors [Q1|Q2|Q3|Q4]
+  std::uint64_t hjob_bytes = 0;
 };
 
 struct ohx_mg {
@@ -304,31 +315,45 @@ RankOut run_rank(ohx_mg& M, ohx_mg_rank& R, const std::vector<ShardIn>& in, int 
   out.info.ms[1] = ms_since(t0);
   t0 = Clock::now();
 
-  // 6. this rank's survivors packed [q1|q2|q3|q4] (shards in index order)
+  // 6. small survivor sets (the common case) travel in ONE fixed-size
+  //    all-gather with the queue lengths: every shard's survivors came back
+  //    to the host with its K2 counts (ctx->h_spec, packed [q1..q4]), so
+  //    the rank's block is [counts, fused, shards, points, flag | up to
+  //    kMgBlock survivors, q1..q4 with the shards in index order]; the root
+  //    then runs the host hull on them -- no device pack, no second
+  //    exchange, no send / recv, no survivor D2H.  Any rank over the block
+  //    (or a shard whose survivors stayed on the device) sends every rank
+  //    down steps 7-9 below with the lengths already known.
   const std::uint64_t my_total = mine[0] + mine[1] + mine[2] + mine[3];
-  dev_grow(&R.d_pack, &R.pack_bytes, std::max<std::uint64_t>(16, my_total * 16), "mg survivors");
-  auto* pack = static_cast<double*>(R.d_pack);
-  {
-    std::uint64_t off = 0;
-    for (int q = 0; q < 4; ++q) {
-      for (int i = 0; i < k; ++i) {
-        const std::uint64_t c = cnt[i][q];
-        if (!c) continue;
-        const auto* qbase = static_cast<const char*>(C[i]->d_queues) +
-                            std::uint64_t(q) * C[i]->last_cap * C[i]->last_idx_bytes;
-        launch_gather(C[i]->last_xy, qbase, C[i]->last_idx_bytes, c, pack + 2 * off,
-                      ctx_stream(C[i]));
-        ++C[i]->launches;
-        off += c;
-      }
-    }
-    for (int i = 0; i < k; ++i)
-      check_cuda(cudaStreamSynchronize(ctx_stream(C[i])), "mg survivor pack");
+  bool small = my_total <= kMgBlock;
+  for (int i = 0; i < k && small; ++i) {
+    const std::uint64_t t = cnt[i][0] + cnt[i][1] + cnt[i][2] + cnt[i][3];
+    small = !in[i].n || t == 0 || C[i]->spec_n == t;
   }
-
-  // 7. per-rank queue lengths (+ fused / shard / point counts)
+  mine[7] = small ? 1 : 0;
+  constexpr std::uint64_t kBlockBytes = 64 + kMgBlock * 16;
+  host_grow(&R.h_blk, &R.hblk_bytes, kBlockBytes * (M.world + 1), "cudaMallocHost(mg block)");
+  auto* blk = static_cast<unsigned char*>(R.h_blk);  // [mine | all ranks' blocks]
+  std::memcpy(blk, mine, 64);
+  if (small) {
+    auto* dst = reinterpret_cast<P2*>(blk + 64);
+    std::uint64_t off = 0;
+    for (int q = 0; q < 4; ++q)
+      for (int i = 0; i < k; ++i) {
+        if (!cnt[i][q]) continue;
+        std::uint64_t qo = 0;  // q's start in shard i's packed survivors
+        for (int u = 0; u < q; ++u) qo += cnt[i][u];
+        std::memcpy(dst + off, reinterpret_cast<const P2*>(C[i]->h_spec) + qo, cnt[i][q] * 16);
+        off += cnt[i][q];
+      }
+  }
+  allgather_host(N, R, M.world, blk, blk + kBlockBytes, kBlockBytes, s);
   std::vector<std::uint64_t> allc(8 * M.world);
-  allgather_host(N, R, M.world, mine, allc.data(), sizeof(mine), s);
+  bool all_small = true;
+  for (int r = 0; r < M.world; ++r) {
+    std::memcpy(&allc[8 * r], blk + kBlockBytes * (r + 1), 64);
+    all_small = all_small && allc[8 * r + 7] == 1;
+  }
   std::uint64_t tq[4] = {0, 0, 0, 0};
   for (int r = 0; r < M.world; ++r) {
     for (int q = 0; q < 4; ++q) tq[q] += allc[8 * r + q];
@@ -336,53 +361,95 @@ RankOut run_rank(ohx_mg& M, ohx_mg_rank& R, const std::vector<ShardIn>& in, int 
     out.info.shards += static_cast<std::uint32_t>(allc[8 * r + 5]);
   }
   const std::uint64_t total = tq[0] + tq[1] + tq[2] + tq[3];
-
-  // 8. survivors to the root, each queue slice straight into its place
-  if (R.rank == root) {
-    dev_grow(&R.d_recv, &R.recv_bytes, std::max<std::uint64_t>(16, total * 16), "mg job survivors");
-  }
-  auto* recv = static_cast<double*>(R.d_recv);
-  check_nccl(N.GroupStart(), "ncclGroupStart");
-  {
-    std::uint64_t qoff = 0;  // start of Q_q in the job buffer
-    std::uint64_t my_off = 0;  // start of q in this rank's pack
-    for (int q = 0; q < 4; ++q) {
-      std::uint64_t pos = qoff;
-      for (int r = 0; r < M.world; ++r) {
-        const std::uint64_t c = allc[8 * r + q];
-        if (c) {
-          if (R.rank == root && r == root) {
-            check_cuda(cudaMemcpyAsync(recv + 2 * pos, pack + 2 * my_off, c * 16,
-                                       cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync(mg own)");
-          } else if (R.rank == root) {
-            check_nccl(N.Recv(recv + 2 * pos, 2 * c, ncclFloat64, r, R.comm, s), "ncclRecv");
-          } else if (r == R.rank) {
-            check_nccl(N.Send(pack + 2 * my_off, 2 * c, ncclFloat64, root, R.comm, s), "ncclSend");
-          }
+  const P2 anchors[4] = {{ext.x[OHX_EAST], ext.y[OHX_EAST]},
+                         {ext.x[OHX_NORTH], ext.y[OHX_NORTH]},
+                         {ext.x[OHX_WEST], ext.y[OHX_WEST]},
+                         {ext.x[OHX_SOUTH], ext.y[OHX_SOUTH]}};
+  if (all_small) {
+    out.info.ms[2] = ms_since(t0);
+    t0 = Clock::now();
+    if (R.rank == root) {  // the job's [Q1|Q2|Q3|Q4]: queue q of rank 0, 1, ...
+      host_grow(&R.h_job, &R.hjob_bytes, std::max<std::uint64_t>(16, total * 16),
+                "cudaMallocHost(mg job survivors)");
+      auto* job = static_cast<P2*>(R.h_job);
+      std::uint64_t off = 0;
+      for (int q = 0; q < 4; ++q)
+        for (int r = 0; r < M.world; ++r) {
+          const std::uint64_t c = allc[8 * r + q];
+          if (!c) continue;
+          std::uint64_t qo = 0;
+          for (int u = 0; u < q; ++u) qo += allc[8 * r + u];
+          std::memcpy(job + off, reinterpret_cast<const P2*>(blk + kBlockBytes * (r + 1) + 64) + qo,
+                      c * 16);
+          off += c;
         }
-        pos += c;
-      }
-      my_off += allc[8 * R.rank + q];
-      qoff += tq[q];
+      out.h = hull_from_host_packed(C[0], job, tq, anchors, s, sink);
     }
-  }
-  check_nccl(N.GroupEnd(), "ncclGroupEnd");
-  check_cuda(cudaStreamSynchronize(s), "mg survivor gather");
-  out.info.ms[2] = ms_since(t0);
-  t0 = Clock::now();
+  } else {
+    // 7. this rank's survivors packed on its device [q1|q2|q3|q4]
+    dev_grow(&R.d_pack, &R.pack_bytes, std::max<std::uint64_t>(16, my_total * 16),
+             "mg survivors");
+    auto* pack = static_cast<double*>(R.d_pack);
+    {
+      std::uint64_t off = 0;
+      for (int q = 0; q < 4; ++q) {
+        for (int i = 0; i < k; ++i) {
+          const std::uint64_t c = cnt[i][q];
+          if (!c) continue;
+          const auto* qbase = static_cast<const char*>(C[i]->d_queues) +
+                              std::uint64_t(q) * C[i]->last_cap * C[i]->last_idx_bytes;
+          launch_gather(C[i]->last_xy, qbase, C[i]->last_idx_bytes, c, pack + 2 * off,
+                        ctx_stream(C[i]));
+          ++C[i]->launches;
+          off += c;
+        }
+      }
+      for (int i = 0; i < k; ++i)
+        check_cuda(cudaStreamSynchronize(ctx_stream(C[i])), "mg survivor pack");
+    }
 
+    // 8. survivors to the root only, each queue slice straight into its place
+    if (R.rank == root) {
+      dev_grow(&R.d_recv, &R.recv_bytes, std::max<std::uint64_t>(16, total * 16),
+               "mg job survivors");
+    }
+    auto* recv = static_cast<double*>(R.d_recv);
+    check_nccl(N.GroupStart(), "ncclGroupStart");
+    {
+      std::uint64_t qoff = 0;  // start of Q_q in the job buffer
+      std::uint64_t my_off = 0;  // start of q in this rank's pack
+      for (int q = 0; q < 4; ++q) {
+        std::uint64_t pos = qoff;
+        for (int r = 0; r < M.world; ++r) {
+          const std::uint64_t c = allc[8 * r + q];
+          if (c) {
+            if (R.rank == root && r == root) {
+              check_cuda(cudaMemcpyAsync(recv + 2 * pos, pack + 2 * my_off, c * 16,
+                                         cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync(mg own)");
+            } else if (R.rank == root) {
+              check_nccl(N.Recv(recv + 2 * pos, 2 * c, ncclFloat64, r, R.comm, s), "ncclRecv");
+            } else if (r == R.rank) {
+              check_nccl(N.Send(pack + 2 * my_off, 2 * c, ncclFloat64, root, R.comm, s),
+                         "ncclSend");
+            }
+          }
+          pos += c;
+        }
+        my_off += allc[8 * R.rank + q];
+        qoff += tq[q];
+      }
+    }
+    check_nccl(N.GroupEnd(), "ncclGroupEnd");
+    check_cuda(cudaStreamSynchronize(s), "mg survivor gather");
+    out.info.ms[2] = ms_since(t0);
+    t0 = Clock::now();
+    // 9. the hull stage on the root, on the device-resident survivors
+    if (R.rank == root) out.h = hull_from_packed(C[0], recv, tq, anchors, s, sink);
+  }
   for (int a = 0; a < 8; ++a) out.info.ext[a] = ext.ext[a];
   for (int q = 0; q < 4; ++q) out.info.counts[q] = tq[q];
   out.info.n_total = g.n;
   out.info.corner_pass = mask != 0;
-  // 9. the hull stage on the root
-  if (R.rank == root) {
-    const P2 anchors[4] = {{ext.x[OHX_EAST], ext.y[OHX_EAST]},
-                           {ext.x[OHX_NORTH], ext.y[OHX_NORTH]},
-                           {ext.x[OHX_WEST], ext.y[OHX_WEST]},
-                           {ext.x[OHX_SOUTH], ext.y[OHX_SOUTH]}};
-    out.h = hull_from_packed(C[0], recv, tq, anchors, s, sink);
-  }
   out.info.ms[3] = ms_since(t0);
   return out;
 }
@@ -574,7 +641,8 @@ int ohx_mg_destroy(ohx_mg* mg) {
         for (ohx_ctx* c : R.shards) ohx::destroy_ctx(c);
         for (void* p : {R.d_x, R.d_pack, R.d_recv})
           if (p) cudaFree(p);
-        if (R.h_x) cudaFreeHost(R.h_x);
+        for (void* p : {R.h_x, R.h_blk, R.h_job})
+          if (p) cudaFreeHost(p);
       }
     }
     delete mg;

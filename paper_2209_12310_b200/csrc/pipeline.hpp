@@ -90,6 +90,11 @@ void queues_fetch_xy(ohx_ctx* c, double* h_xy, cudaStream_t s);
 std::size_t hull_from_packed(ohx_ctx* c, const double* d_packed, const std::uint64_t counts[4],
                              const P2 anchors[4], cudaStream_t s, const HullSink& sink,
                              bool dev = false);
+// hull stage on survivor coordinates already in host memory, packed
+// [q1|q2|q3|q4]: the host hull stage below device_sort_min() survivors,
+// else one H2D through the context's gather buffer and hull_from_packed
+std::size_t hull_from_host_packed(ohx_ctx* c, const P2* h_packed, const std::uint64_t counts[4],
+                                  const P2 anchors[4], cudaStream_t s, const HullSink& sink);
 // host hull stage on the queues of the last filter (survivors gathered and
 // copied back in one launch)
 PVec device_queues_hull(ohx_ctx* c, const FilterOut& f, cudaStream_t s);
