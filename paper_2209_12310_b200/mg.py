@@ -96,18 +96,29 @@ class MultiGPU:
         except Exception:
             pass
 
-    @staticmethod
-    def _call(fn, cap):
-        """fn(hull buffer, cap, &h) -> (hull, h); regrows when the hull outgrew cap."""
+    def _call(self, fn, cap):
+        """fn(hull buffer, cap, &h) -> (hull, h); regrows when the hull outgrew cap.
+        The output buffer (and its ctypes pointer) is kept for the next call
+        while hulls come back as copies (< 2^20 vertices), as Context does:
+        a fresh 256 MB buffer per call costs an mmap / munmap pair."""
         while True:
-            hull = np.empty((max(cap, 1), 2), dtype=np.float64)
+            hb = getattr(self, "_hbuf", None)
+            if hb is not None and len(hb[0]) >= cap:
+                hull, hptr = hb
+            else:
+                hull = np.empty((max(cap, 1), 2), dtype=np.float64)
+                hptr = hull.ctypes.data_as(_dp)
+            self._hbuf = None
             h = C.c_uint64(0)
             info = MgInfo()
-            rc = fn(hull.ctypes.data_as(_dp), cap, C.byref(h), C.byref(info))
-            if rc == -1 and h.value > cap:
+            rc = fn(hptr, len(hull), C.byref(h), C.byref(info))
+            if rc == -1 and h.value > len(hull):
                 cap = h.value
                 continue
             check(rc)
+            if h.value < (1 << 20):
+                self._hbuf = (hull, hptr)
+                return hull[: h.value].copy(), info
             return hull[: h.value], info
 
     def heaphull_shard(self, d_xy, n: int, base: int, vshards: int = 1, labels=None,
