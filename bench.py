@@ -540,7 +540,12 @@ def run_b200_arm(a):
     for _ in range(a.warmup):
         step_device()
     launches0 = run.launches()
-    ctx.kernel_ms_sum(reset=True)  # per-stage CUDA-event sums, read once after the loop
+    # per-stage CUDA-event sums, read once after the loop; with several
+    # (virtual) shards per rank their stages run one after another on this
+    # GPU, so a step's stage time is the sum over the shards' contexts
+    kctxs = run.ctxs if mode == "mg" else [ctx]
+    for c in kctxs:
+        c.kernel_ms_sum(reset=True)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_dev) as clocks:
         barrier()
@@ -550,7 +555,8 @@ def run_b200_arm(a):
         stop.record()
         barrier()
     launches = run.launches() - launches0
-    ksum = ctx.kernel_ms_sum()
+    ksums = [c.kernel_ms_sum() for c in kctxs]
+    ksum = {k: (sum(ks[k][0] for ks in ksums), ksums[0][k][1]) for k in ksums[0]}
     k1, k2, kc = ([ksum[k][0] / ksum[k][1]] if ksum[k][1] else [-1.0] for k in ("k1", "k2", "kc"))
     last = ctx.last_run()
     runs = [dict(last, fused=last["fused"] and ksum["kc"][1] == a.steps)]
