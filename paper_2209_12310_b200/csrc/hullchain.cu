@@ -43,9 +43,12 @@
 // intrinsics (no contraction; the TU is also built with -fmad=false).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
+#include <string>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -321,6 +324,139 @@ struct StatCombine {
   }
 };
 
+__device__ __forceinline__ CycStat stat_identity() {
+  CycStat s;
+  s.bx = -INFINITY;
+  s.by = INFINITY;
+  s.bi = ~0ull;
+  s.dups = 0;
+  s.notflat = 0;
+  s.bad = 0;
+  return s;
+}
+
+// one CycStat per 128-thread block (thread 0 holds it)
+__device__ __forceinline__ CycStat block_stat(CycStat v) {
+  __shared__ CycStat part[4];
+  const StatCombine comb;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    CycStat o;
+    o.bx = __shfl_down_sync(0xffffffffu, v.bx, off);
+    o.by = __shfl_down_sync(0xffffffffu, v.by, off);
+    o.bi = __shfl_down_sync(0xffffffffu, v.bi, off);
+    o.dups = __shfl_down_sync(0xffffffffu, v.dups, off);
+    o.notflat = 0;
+    o.bad = __shfl_down_sync(0xffffffffu, v.bad, off);
+    v = comb(v, o);
+  }
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int w = 1; w < 4; ++w) v = comb(v, part[w]);
+  return v;
+}
+
+// chain_copy + the cycle statistics of the slice's own positions (all four
+// arcs): every position's best-start candidacy, the duplicate test of every
+// pair inside the slice and the turn test of every position with both
+// neighbours inside it; the slice ends' tests need the neighbouring slices
+// and are done by chain_stat_ends once the cycle is written.  Saves the
+// reduction's second read of the whole cycle (1.55 GB on the circle).
+__global__ void __launch_bounds__(128) chain_copy_stats(const double2* __restrict__ loc,
+                                                        ArcGeom g, ChunkState st,
+                                                        double2* __restrict__ cycle,
+                                                        CycStat* __restrict__ part) {
+  const std::uint32_t c = g.c_lo + blockIdx.x;
+  const ChunkPos p = chunk_pos(g, c);
+  const double2* s = loc + p.b + st.base[c];
+  const std::uint64_t o = st.offs[c];
+  double2* d = cycle + o;
+  const std::uint64_t L = st.slice[c];
+  CycStat acc = stat_identity();
+  auto visit = [&](std::uint64_t i, double2 b) {
+    bool take;  // starts_before (hull.cpp:35-38), ties to the smaller index
+    if (b.x != acc.bx) take = b.x > acc.bx;
+    else if (b.y != acc.by) take = b.y < acc.by;
+    else take = o + i < acc.bi;
+    if (take) {
+      acc.bx = b.x;
+      acc.by = b.y;
+      acc.bi = o + i;
+    }
+    if (i >= 1) {
+      const double2 a = __ldg(s + i - 1);
+      acc.dups |= a.x == b.x && a.y == b.y;
+      if (i + 1 < L) acc.bad += orient_sign(a, b, __ldg(s + i + 1)) <= 0 ? 1 : 0;
+    }
+  };
+  std::uint64_t i = threadIdx.x;
+  for (; i + 3 * blockDim.x < L; i += 4 * blockDim.x) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = s[i + u * blockDim.x];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) d[i + u * blockDim.x] = v[u];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) visit(i + u * blockDim.x, v[u]);
+  }
+  for (; i < L; i += blockDim.x) {
+    const double2 v = s[i];
+    d[i] = v;
+    visit(i, v);
+  }
+  acc = block_stat(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+struct CycMeta {
+  double2 tail;            // cycle[m - 1]
+  std::uint64_t m;
+  std::uint32_t notflat3;  // orientation(c[0], c[1], c[2]) != 0
+  std::uint32_t pad;
+};
+
+// the slice ends' statistics (first and last position of every non-empty
+// slice, with their neighbours in the written cycle) into part[G + k]; the
+// cycle length, its last point and the first three points' turn into meta
+__global__ void chain_stat_ends(ArcGeom g, ChunkState st, const double2* __restrict__ cycle,
+                                CycStat* __restrict__ part, CycMeta* meta) {
+  const std::uint32_t G = g.c_hi - g.c_lo;
+  const std::uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= G) return;
+  const std::uint32_t c = g.c_lo + k, last = g.c_hi - 1;
+  const std::uint64_t m = st.offs[last] + st.slice[last];
+  CycStat acc = stat_identity();
+  const std::uint64_t L = st.slice[c];
+  if (L && m) {
+    const std::uint64_t p0 = st.offs[c], p1 = p0 + L - 1;
+    const double2 a0 = cycle[p0 ? p0 - 1 : m - 1], b0 = cycle[p0],
+                  n0 = cycle[p0 + 1 == m ? 0 : p0 + 1];
+    acc.dups = p0 > 0 && a0.x == b0.x && a0.y == b0.y;
+    acc.bad = orient_sign(a0, b0, n0) <= 0 ? 1 : 0;
+    if (L >= 2)
+      acc.bad += orient_sign(cycle[p1 - 1], cycle[p1], cycle[p1 + 1 == m ? 0 : p1 + 1]) <= 0 ? 1 : 0;
+  }
+  part[G + k] = acc;
+  if (k == 0) {
+    CycMeta mt{};
+    mt.m = m;
+    if (m) mt.tail = cycle[m - 1];
+    mt.notflat3 = m >= 3 && orient_sign(cycle[0], cycle[1], cycle[2]) != 0;
+    *meta = mt;
+  }
+}
+
+// OHX_CYCLE_STATS=reduce: the statistics as a separate reduction over the
+// whole cycle (A/B and test hook)
+bool fused_cycle_stats() {
+  static const bool v = [] {
+    const char* e = std::getenv("OHX_CYCLE_STATS");
+    return !(e && std::string(e) == "reduce");
+  }();
+  return v;
+}
+
 std::size_t align256(std::size_t b) { return (b + 255) & ~std::size_t(255); }
 
 ArcGeom arc_geom(const std::uint64_t len[4]) {
@@ -361,12 +497,21 @@ std::size_t stat_tmp_bytes(std::uint64_t m) {
   return b;
 }
 
+std::size_t part_tmp_bytes(std::uint64_t k) {
+  std::size_t b = 0;
+  check_cuda(cub::DeviceReduce::Reduce(nullptr, b, static_cast<const CycStat*>(nullptr),
+                                       static_cast<CycStat*>(nullptr),
+                                       static_cast<std::int64_t>(k), StatCombine{}, CycStat{}),
+             "cub reduce temp size");
+  return b;
+}
+
 struct ChainLayout {
   ArcGeom g;
   std::uint64_t total;
   std::size_t bytes;
   std::size_t o_loc, o_cycle, o_h, o_lr, o_low, o_base, o_keep, o_deep, o_sync, o_slice, o_offs,
-      o_stat, o_flag, o_tmp;
+      o_stat, o_part, o_flag, o_tmp;
   std::size_t tmp_bytes;
 };
 
@@ -393,9 +538,11 @@ ChainLayout chain_layout(const std::uint64_t len[4]) {
   L.o_slice = take(G * 8ull);
   L.o_offs = take(G * 8ull);
   L.o_stat = take(sizeof(CycStat));
+  L.o_part = take(2ull * G * sizeof(CycStat) + sizeof(CycMeta));
   L.o_flag = take(16);
-  const std::size_t a = scan_tmp_bytes(G), b = stat_tmp_bytes(L.total);
-  L.tmp_bytes = a > b ? a : b;
+  const std::size_t a = scan_tmp_bytes(G), b = stat_tmp_bytes(L.total),
+                    c = part_tmp_bytes(2ull * G);
+  L.tmp_bytes = std::max(a, std::max(b, c));
   L.o_tmp = take(L.tmp_bytes);
   L.bytes = o;
   return L;
@@ -457,19 +604,44 @@ bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_w
     std::uint64_t last_off, last_len;
   };
   Head hd{};
-  const SmallRead rd[3] = {{flag, sizeof(int)},
-                           {st.offs + (L.g.c_hi - 1), 8},
-                           {st.slice + (L.g.c_hi - 1), 8}};
-  const unsigned char* hv = small_reads(rd, 3, s);
+  // all four arcs: the cycle statistics with the copy (chain_copy_stats +
+  // the slice ends + a reduction over 2 G partials), read with the head in
+  // the same sync; one arc (the pipelined stage) needs none
+  const bool fused = only_q < 0 && fused_cycle_stats();
+  auto* part = reinterpret_cast<CycStat*>(w + L.o_part);
+  auto* meta = reinterpret_cast<CycMeta*>(part + 2ull * G);
   // the copy runs regardless (harmless on failure: every slice length is
   // then whatever chain_check wrote, bounded by the chunk)
-  chain_copy<<<G, 128, 0, s>>>(loc, L.g, st, cycle);
-  check_cuda(cudaGetLastError(), "chain_copy launch");
+  if (fused) {
+    chain_copy_stats<<<G, 128, 0, s>>>(loc, L.g, st, cycle, part);
+    check_cuda(cudaGetLastError(), "chain_copy_stats launch");
+    chain_stat_ends<<<(G + 127) / 128, 128, 0, s>>>(L.g, st, cycle, part, meta);
+    check_cuda(cudaGetLastError(), "chain_stat_ends launch");
+    CycStat init{};
+    init.bx = -INFINITY;
+    init.by = INFINITY;
+    init.bi = ~0ull;
+    tb = L.tmp_bytes;
+    check_cuda(cub::DeviceReduce::Reduce(tmp, tb, part, stat, static_cast<std::int64_t>(2ull * G),
+                                         StatCombine{}, init, s),
+               "cub::DeviceReduce::Reduce(cycle stat partials)");
+  } else {
+    chain_copy<<<G, 128, 0, s>>>(loc, L.g, st, cycle);
+    check_cuda(cudaGetLastError(), "chain_copy launch");
+  }
+  static_assert(sizeof(CycStat) <= 64 && sizeof(CycMeta) <= 64, "small_reads slots");
+  const SmallRead rd[6] = {{flag, sizeof(int)},
+                           {st.offs + (L.g.c_hi - 1), 8},
+                           {st.slice + (L.g.c_hi - 1), 8},
+                           {stat, sizeof(CycStat)},
+                           {meta, sizeof(CycMeta)},
+                           {cycle, 16}};
+  const unsigned char* hv = small_reads(rd, fused ? 6 : 3, s);
   check_cuda(cudaStreamSynchronize(s), "device chains");
   std::memcpy(&hd.fail, hv, sizeof(int));
   std::memcpy(&hd.last_off, hv + 8, 8);
   std::memcpy(&hd.last_len, hv + 16, 8);
-  out->launches = 5;
+  out->launches = fused ? 8 : 5;
   if (hd.fail) return false;
   const std::uint64_t m = hd.last_off + hd.last_len;
   out->d_cycle = reinterpret_cast<double*>(cycle);
@@ -477,6 +649,25 @@ bool device_chains(const double* d_sorted, const std::uint64_t len[4], void* d_w
   out->m = m;
   out->chunks = G;
   if (m == 0 || only_q >= 0) return true;  // (one arc: no cycle statistics)
+  if (fused) {
+    CycStat hs;
+    CycMeta mt;
+    double2 c0;
+    std::memcpy(&hs, hv + 24, sizeof(hs));
+    std::memcpy(&mt, hv + 24 + sizeof(CycStat), sizeof(mt));
+    std::memcpy(&c0, hv + 24 + sizeof(CycStat) + sizeof(CycMeta), 16);
+    // notflat is decided by the first three points when they turn (every
+    // non-degenerate cycle); a cycle starting with three collinear points
+    // takes the full reduction below
+    if (mt.m == m && mt.notflat3) {
+      out->front_eq_back = c0.x == mt.tail.x && c0.y == mt.tail.y;
+      out->dups = hs.dups != 0;
+      out->flat = false;
+      out->bad = hs.bad;
+      out->best = hs.bi;
+      return true;
+    }
+  }
   cycle_stats_into(cycle, m, stat, tmp, L.tmp_bytes, s, out);
   return true;
 }
