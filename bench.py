@@ -599,10 +599,19 @@ def run_b200_arm(a):
         h2d = h2d_bandwidth(host, d if mode == "single" else d2) if host.is_pinned() else None
         h2d = max_over_ranks(h2d or 0.0) if world > 1 else h2d
         e2e_gbs = total * 16 / (ms_e2e * 1e-3) / 1e9
+        if mode == "mg":
+            # the layer's read-backs on every rank: the record all-gather
+            # (296 B per rank) and the exchange block (16448 B per rank:
+            # queue lengths + up to 1024 survivors); survivors over the
+            # block go to the root's device and come back once
+            per_rank = max_over_ranks(float(sum(stats["counts"])))
+            d2h = world * world * (296 + 16448) + (0 if per_rank <= 1024 else survivors_job * 16)
+        else:
+            # survivors' coordinates (16 B each) + the small records
+            d2h = survivors_job * 16 + world * 2 * 320
         e2e = {"value": total / (ms_e2e * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": total * 16,
-               # survivors' coordinates (16 B each) + the small records
-               "d2h_bytes_per_step": survivors_job * 16 + world * 2 * 320,
+               "d2h_bytes_per_step": d2h,
                "api": api.format("pinned" if host.is_pinned() else "pageable"),
                "roofline": {"bound": "pcie", "achieved": e2e_gbs, "unit": "GB/s",
                             "peak": h2d * world if (h2d and world > 1) else h2d,
