@@ -356,11 +356,56 @@ __global__ void __launch_bounds__(kRunThreads)
   }
 }
 
+// The points in key order: random 16-byte reads.  Every read costs ~4 L2
+// sectors / ~116 B of DRAM whatever the path (ld default, .cg, .cs,
+// .nc.L1::no_allocate, cp.async .cg / .ca: ncu, circle 1e8, 11.6-12.9 GB
+// read for 1.6 GB of points); four reads in flight per thread through
+// cp.async.ca into the thread's shared-memory slots measured fastest
+// (2.37 vs 2.46 ms).  kAsync = false: one plain load at a time (A/B hook
+// OHX_GATHER_LD=0).
+template <bool kAsync>
 __global__ void gather_arcs(const ArcSrc A, const std::uint32_t* __restrict__ vals,
                             double2* __restrict__ out, std::uint64_t lo, std::uint64_t hi) {
-  for (std::uint64_t k = lo + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < hi;
-       k += std::uint64_t(gridDim.x) * blockDim.x)
-    out[k] = A.point(A.arc_of(k), vals[k]);
+  auto src_of = [&](std::uint64_t k) -> const double2* {
+    const int q = A.arc_of(k);
+    const std::uint64_t j = vals[k];
+    if (j == 0) return A.anchors + q;
+    if (j == A.end(q) - A.begin(q) - 1) return A.anchors + ((q + 1) & 3);
+    const std::uint64_t p0 =
+        q == 0 ? A.qoff.x : (q == 1 ? A.qoff.y : (q == 2 ? A.qoff.z : A.qoff.w));
+    return A.packed + p0 + j - 1;
+  };
+  const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
+  const std::uint64_t first = lo + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if constexpr (kAsync) {
+    __shared__ double2 slot[4][256];
+    for (std::uint64_t k0 = first; k0 < hi; k0 += 4 * stride) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const std::uint64_t k = k0 + u * stride;
+        if (k >= hi) break;
+        const unsigned dst =
+            static_cast<unsigned>(__cvta_generic_to_shared(&slot[u][threadIdx.x]));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src_of(k)));
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const std::uint64_t k = k0 + u * stride;
+        if (k < hi) out[k] = slot[u][threadIdx.x];
+      }
+    }
+  } else {
+    for (std::uint64_t k = first; k < hi; k += stride) out[k] = *src_of(k);
+  }
+}
+
+bool gather_async() {
+  static const bool v = [] {
+    const char* e = std::getenv("OHX_GATHER_LD");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
 }
 
 struct ArcLayout {
@@ -485,7 +530,8 @@ void sort_arcs(const double* d_packed, const std::uint64_t counts[4], const doub
       }
     // the points in key order, then the runs of equal keys in full order
     auto* out = reinterpret_cast<double2*>(d_sorted);
-    gather_arcs<<<g1, 256, 0, s>>>(A, lvals, out, lo, hi);
+    if (gather_async()) gather_arcs<true><<<g1, 256, 0, s>>>(A, lvals, out, lo, hi);
+    else gather_arcs<false><<<g1, 256, 0, s>>>(A, lvals, out, lo, hi);
     check_cuda(cudaGetLastError(), "gather_arcs launch");
     check_cuda(cudaMemsetAsync(d_flag, 0, 2 * sizeof(int), s), "cudaMemsetAsync(flag)");
     fix_runs<<<g1, 256, 0, s>>>(lkeys, out, A, runs, nruns, d_flag, lo, hi);
